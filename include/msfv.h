@@ -1,0 +1,149 @@
+/*
+ * msfv.h -- C-ABI of the B200-native adaptive MSFV forward + gradient path.
+ *
+ * This is the drop-in boundary.  The reference package (msinv, pure Python,
+ * /root/reference/pkg/src/msinv) has no native interface; each entry point
+ * below replaces the reference function cited next to it, and the Python
+ * mirror package (paper_1707_07598_b200) binds them with ctypes exactly as a
+ * maintainer would bind them from the reference.
+ *
+ * Conventions
+ *  - All array arguments marked "device" are CUDA device pointers to float64
+ *    (or int32 flags) owned by the caller (PyTorch tensors in the shim); the
+ *    library allocates nothing per call.  Host arrays are only read.
+ *  - `stream` is a cudaStream_t passed as void*; every call only enqueues work.
+ *  - Index conventions are the reference's (x-fastest nodes/cells, edges
+ *    x-then-y-then-z, pinned node 0 dropped, coarse columns in node order).
+ *  - "Full node field" F: F[node * nrhs + s] over all (n1+1)(n2+1)(n3+1)
+ *    nodes including the pinned node 0, whose entries are kept at zero.
+ *  - Return value: MSFV_OK or an error code; msfv_last_error() describes it.
+ *    The shim maps codes onto the reference exception types (errors.py:4-28).
+ */
+#ifndef MSFV_H
+#define MSFV_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MSFV_API __attribute__((visibility("default")))
+#else
+#define MSFV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSFV_ABI_VERSION 1
+
+enum msfv_status {
+  MSFV_OK = 0,
+  MSFV_INVALID_MODEL = 1,     /* InvalidModelError   operators.py:26-27,128-129 */
+  MSFV_STALE_BASIS = 2,       /* StaleBasisError     basis.py:333-337          */
+  MSFV_REDUCED_SINGULAR = 3,  /* ReducedSingularError forward.py:126-129       */
+  MSFV_SHAPE = 4,             /* ValueError (shapes / unsupported geometry)     */
+  MSFV_CUDA = 5,              /* RuntimeError (CUDA failure)                    */
+  MSFV_FACTORIZATION = 6,     /* FactorizationError  solvers.py:34-38           */
+  MSFV_UNSUPPORTED = 7
+};
+
+/* Device flag bits written by msfv_operator / msfv_basis_build / msfv_coarse_factor. */
+#define MSFV_FLAG_NONFINITE 1
+#define MSFV_FLAG_NONPOSITIVE 2
+#define MSFV_FLAG_LOCAL_NOT_SPD 4
+#define MSFV_FLAG_COARSE_NOT_SPD 8
+
+/* msfv_plan_info indices */
+enum msfv_info {
+  MSFV_INFO_NN = 0,          /* nodes incl. pinned                          */
+  MSFV_INFO_N = 1,           /* pinned dimension n = NN - 1                 */
+  MSFV_INFO_NCELLS = 2,
+  MSFV_INFO_NEDGES = 3,
+  MSFV_INFO_NBLOCKS = 4,
+  MSFV_INFO_NI = 5,          /* interior nodes per block                    */
+  MSFV_INFO_P1S = 6,         /* row stride of the per-block factor bands    */
+  MSFV_INFO_K = 7,           /* coarse columns (Lagrange: coarse nodes)     */
+  MSFV_INFO_AK_DOUBLES = 8,  /* size of the coarse factor buffer            */
+  MSFV_INFO_BASIS_SMEM = 9,
+  MSFV_INFO_NT = 10,
+  MSFV_INFO_PT = 11,
+  MSFV_INFO_TB = 12,
+  MSFV_INFO_PC = 13,
+  MSFV_INFO_COUNT = 14
+};
+
+typedef struct msfv_plan msfv_plan;      /* geometry; model-independent        */
+typedef struct msfv_points msfv_points;  /* one survey matrix (P or Q) on device */
+
+MSFV_API int msfv_abi_version(void);
+MSFV_API const char* msfv_last_error(void);
+
+/* TensorMesh + CoarsePartition (mesh.py:12-182).  blocks must divide cells. */
+MSFV_API int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out);
+MSFV_API void msfv_plan_destroy(msfv_plan* plan);
+MSFV_API int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n);
+
+/* A sparse pinned-space survey matrix in CSC form (Survey.P / Survey.Q,
+ * forward.py:23-51; models.py:54-83).  Host arrays; uploaded once. */
+MSFV_API int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const int64_t* colptr,
+                       const int64_t* rows, const double* vals, msfv_points** out);
+MSFV_API void msfv_points_destroy(msfv_points* pts);
+
+/* sigma = exp(m), w = C sigma (operators.py:23-28,123-136).  flags |= NONFINITE/NONPOSITIVE. */
+MSFV_API int msfv_operator(const msfv_plan* plan, const double* m, double* sigma, double* w, int32_t* flags, void* stream);
+/* c = C (sigma .* dm)   (Csig @ dm, forward.py:237,259); tmp: ncells doubles */
+MSFV_API int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* dm, double* tmp, double* c,
+                      void* stream);
+
+/* Lagrange basis at w (assemble_basis, basis.py:511-616 with _BlockFactor
+ * basis.py:258-298): per-block band Cholesky factors Lc/Lr
+ * [nblocks][nI][P1S], interior basis values Sint [nblocks][8][nI] and the
+ * per-block 8x8 Galerkin blocks Kloc [nblocks][64]. flags |= LOCAL_NOT_SPD. */
+MSFV_API int msfv_basis_build(const msfv_plan* plan, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
+                     int32_t* flags, void* stream);
+/* Values of S in the reference CSC pattern (basis.py:574-594):
+ * vals[t] = src[t] >= 0 ? Sint[src[t]] : hatv[t]  (src, hatv device arrays). */
+MSFV_API int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,
+                   void* stream);
+
+/* A_k = S^T A S (+ shift I) into the tiled band buffer (forward.py:101-102,117-125). */
+MSFV_API int msfv_galerkin(const msfv_plan* plan, const double* Kloc, double shift, double* Ak, void* stream);
+/* diag(A_k) (for the shift 1e-12 tr(A_k)/k, forward.py:123) */
+MSFV_API int msfv_coarse_diag(const msfv_plan* plan, const double* Ak, double* diag, void* stream);
+/* In-place banded Cholesky of A_k (cho_factor, forward.py:121). flags |= COARSE_NOT_SPD. */
+MSFV_API int msfv_coarse_factor(const msfv_plan* plan, double* Ak, int32_t* flags, void* stream);
+/* X <- A_k^{-1} X, X [k][nrhs] (cho_solve, forward.py:72-75). */
+MSFV_API int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, int32_t nrhs, void* stream);
+
+/* out[col][s] = sum_t val_t (Xfield(node_t,s) + S(node_t,:) Y[:,s]); Y or Xfield may be NULL.
+ * (P^T S T forward.py:143; P^T (ydm + S dt) forward.py:268) */
+MSFV_API int msfv_survey_receive(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Y,
+                        const double* Xfield, int32_t nrhs, double* out, void* stream);
+/* out[c][s] = (S^T M Z)[c][s]; Z [ncol][nrhs] or NULL for the identity (S^T Q, forward.py:115). */
+MSFV_API int msfv_survey_restrict(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Z,
+                         int32_t nrhs, double* out, void* stream);
+/* field(node,s) = (M Z)(node,s) on the survey's nodes (other entries untouched). */
+MSFV_API int msfv_survey_scatter(const msfv_plan* plan, const msfv_points* pts, const double* Z, int32_t nrhs,
+                        double* field, void* stream);
+
+/* field = S Y on every node (basis.S @ T, forward.py:143,241). */
+MSFV_API int msfv_prolong(const msfv_plan* plan, const double* Sint, const double* Y, int32_t nrhs, double* field,
+                 void* stream);
+/* out = alpha*src + beta*(A_wt X) on block-interior nodes (forward.py:243,278). src may be NULL. */
+MSFV_API int msfv_residual(const msfv_plan* plan, const double* src, double alpha, const double* wt, const double* X,
+                  double beta, int32_t nrhs, double* out, void* stream);
+/* out = blockdiag(A_II^{-1}) rhs on interiors (MultiscaleBasis.interior_solve, basis.py:339-353). */
+MSFV_API int msfv_interior_solve(const msfv_plan* plan, const double* Lc, const double* Lr, const double* rhs, double* out,
+                        int32_t nrhs, void* stream);
+/* out[k][nrhs] = scale * S^T (A_w1 X1 + A_w2 X2); part: nblocks*8*nrhs scratch (forward.py:266). */
+MSFV_API int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
+                     const double* w2, const double* X2, int32_t nrhs, double scale, double* part, double* out,
+                     void* stream);
+/* g = -sigma C^T sum_s [G U (G Z + G Y) + G R G Y]  (rapply compact form, forward.py:271-281). */
+MSFV_API int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
+                       const double* Y, const double* R, int32_t nrhs, double* g, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSFV_H */

@@ -1,0 +1,27 @@
+"""B200-native adaptive MSFV forward + gradient (drop-in for msinv's adaptive path).
+
+Public names mirror the reference package's (msinv/__init__.py:3-20) for the
+hot path; compute runs in libmsfv.so (sm_100a) through the C-ABI in
+include/msfv.h.  Importing this package does not touch the GPU.
+"""
+
+from .mesh import TensorMesh, CoarsePartition, create_mesh, create_partition, block_node_sets
+from .operators import (
+    sigma_map, sigma_deriv, nodal_gradient, edge_cell_map,
+    assemble_operator, DiffusionOperator, grad_A_u, grad_A_u_full,
+)
+from .basis import (
+    BasisSpec, MultiscaleBasis, BasisBuilder, generate_bc_lagrange, assemble_basis,
+    coarse_hat_values,
+)
+from .forward import Survey, ReducedState, forward_reduced, AdaptiveSensitivity, sensitivity_adaptive
+from .inversion import (
+    misfit_ssd, Objective, GNConfig, projected_gauss_newton, AdaptiveReducedProblem,
+    cell_gradient, project_bounds, add_noise, tikhonov_reg, InversionTrace,
+)
+from .errors import (
+    InvalidModelError, FactorizationError, SolverBreakdown,
+    StaleBasisError, ReducedSingularError,
+)
+
+__version__ = "0.1.0"

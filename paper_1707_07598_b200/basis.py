@@ -1,0 +1,276 @@
+"""Model-adapted Lagrange multiscale basis built on the GPU.
+
+Drop-in for the Lagrange family of the reference's basis.py.  The per-block
+interior problems (basis.py:511-563) are factored and solved by ``k_basis``
+(one CTA per coarse block, banded Cholesky in shared memory); the basis is
+kept on the device in block layout (``Sint[block][corner][interior]`` plus
+analytic skeleton hats).  ``MultiscaleBasis.S`` materialises the reference's
+CSC matrix (same indices/indptr, basis.py:574-594) on demand.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .engine import engine_for
+from .errors import FactorizationError, StaleBasisError
+from .operators import edge_cell_map, nodal_gradient
+
+FAMILIES = ("lagrange", "source", "skeleton", "local_pca")
+
+
+@dataclass(frozen=True)
+class BasisSpec:
+    """Boundary-condition families (basis.py:37-53).  The GPU path builds the
+    Lagrange family; other families are rejected by BasisBuilder."""
+
+    families: tuple = ("lagrange",)
+    pca_rank: int = 0
+    pca_total: int = 0
+    pca_drop_tol: float = 1e-10
+
+    def __post_init__(self):
+        unknown = set(self.families) - set(FAMILIES)
+        if unknown:
+            raise ValueError(f"unknown basis families: {sorted(unknown)}")
+        if not self.families:
+            raise ValueError("at least one basis family must be enabled")
+        if "local_pca" in self.families and self.pca_rank < 1:
+            raise ValueError("local_pca requires pca_rank >= 1")
+
+
+def coarse_hat_values(partition, coarse_node, node_ids):
+    """Trilinear hat of a coarse node at full-space node ids (basis.py:84-92)."""
+    mesh = partition.mesh
+    ci, cj, ck = mesh.node_triple(coarse_node)
+    i, j, k = mesh.node_triple(np.asarray(node_ids))
+    w = np.ones(np.atleast_1d(i).shape, dtype=float)
+    for x, c, b in ((i, ci, partition.b1), (j, cj, partition.b2), (k, ck, partition.b3)):
+        w = w * np.maximum(0.0, 1.0 - np.abs(np.asarray(x, dtype=float) - c) / b)
+    return w
+
+
+def _skeleton_hat_entries(partition):
+    """(pinned row, coarse column, hat value) of every nonzero skeleton hat
+    entry -- the ``values`` block of generate_bc_lagrange (basis.py:95-116)."""
+    mesh = partition.mesh
+    b = (partition.b1, partition.b2, partition.b3)
+    nbp = (partition.nb[0] + 1, partition.nb[1] + 1, partition.nb[2] + 1)
+    skel = partition.skeleton[partition.skeleton != 0]
+    ijk = mesh.node_triple(skel)
+    # per axis: candidate coarse coordinates floor(x/b) and floor(x/b)+1
+    cand, fac = [], []
+    for ax in range(3):
+        x = ijk[ax]
+        c0 = x // b[ax]
+        opts = []
+        for c in (c0, c0 + 1):
+            f = np.maximum(0.0, 1.0 - np.abs(x.astype(float) - c * b[ax]) / b[ax])
+            f = np.where(c < nbp[ax], f, 0.0)
+            opts.append((np.minimum(c, nbp[ax] - 1), f))
+        cand.append(opts)
+    rows, cols, vals = [], [], []
+    for oz in range(2):
+        for oy in range(2):
+            for ox in range(2):
+                w = np.ones(skel.size)
+                w = w * cand[0][ox][1]
+                w = w * cand[1][oy][1]
+                w = w * cand[2][oz][1]
+                col = cand[0][ox][0] + nbp[0] * (cand[1][oy][0] + nbp[1] * cand[2][oz][0])
+                nz = np.flatnonzero(w)
+                rows.append(skel[nz] - 1)
+                cols.append(col[nz])
+                vals.append(w[nz])
+    return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+
+
+def generate_bc_lagrange(partition):
+    """Lagrange boundary data as a scipy CSC (basis.py:95-116), host side."""
+    from types import SimpleNamespace
+    n = partition.mesh.n_nodes - 1
+    r, c, v = _skeleton_hat_entries(partition)
+    values = sp.csc_matrix((v, (r, c)), shape=(n, partition.n_coarse_nodes))
+    forcing = sp.csc_matrix((n, partition.n_coarse_nodes))
+    return SimpleNamespace(family="lagrange", values=values, forcing=forcing, block_restrict=None,
+                           labels=[("coarse_node", int(cn)) for cn in partition.coarse_nodes], dropped=[],
+                           count=partition.n_coarse_nodes)
+
+
+class _CscTemplate:
+    """Model-independent CSC pattern of S and the gather map from the device
+    block layout into it (basis.py:574-594)."""
+
+    def __init__(self, partition, engine):
+        import torch
+        n = partition.mesh.n_nodes - 1
+        k = partition.n_coarse_nodes
+        r_s, c_s, v_s = _skeleton_hat_entries(partition)
+        nI = engine.nI
+        rows = [r_s]
+        cols = [c_s]
+        src = [np.full(r_s.size, -1, dtype=np.int64)]
+        hv = [v_s]
+        if nI > 0:
+            nb1, nb2, nb3 = partition.nb
+            inter = np.stack(partition.interiors) - 1             # [block, a] pinned ids
+            nbl = inter.shape[0]
+            bi = np.arange(nbl) % nb1
+            bj = (np.arange(nbl) // nb1) % nb2
+            bk = np.arange(nbl) // (nb1 * nb2)
+            for cc in range(8):
+                col = (bi + (cc & 1)) + (nb1 + 1) * ((bj + ((cc >> 1) & 1)) + (nb2 + 1) * (bk + ((cc >> 2) & 1)))
+                rows.append(inter.ravel())
+                cols.append(np.repeat(col, nI))
+                src.append(((np.arange(nbl)[:, None] * 8 + cc) * nI + np.arange(nI)[None, :]).ravel())
+                hv.append(np.zeros(nbl * nI))
+        rows = np.concatenate(rows)
+        cols = np.concatenate(cols)
+        src = np.concatenate(src)
+        hv = np.concatenate(hv)
+        order = np.argsort(cols.astype(np.int64) * n + rows, kind="stable")
+        self.indices = rows[order].astype(np.int32)
+        self.indptr = np.searchsorted(cols[order], np.arange(k + 1)).astype(np.int32)
+        self.shape = (n, k)
+        self.src = torch.from_numpy(src[order]).to(engine.device)
+        self.hatv = torch.from_numpy(hv[order]).to(engine.device)
+
+
+class MultiscaleBasis:
+    """Assembled basis on the device (basis.py:301-376 surface)."""
+
+    def __init__(self, partition, engine, op, Lc, Lr, Sint, Kloc, flags):
+        self.partition = partition
+        self.engine = engine
+        self.op = op
+        self.model = op.m.copy() if op._m_host is not None else None
+        self._m_dev = op._dev[1]
+        self.Lc, self.Lr, self.Sint, self.Kloc, self.flags = Lc, Lr, Sint, Kloc, flags
+        self.families = np.full(partition.n_coarse_nodes, "lagrange")
+        self.labels = [("coarse_node", int(cn)) for cn in partition.coarse_nodes]
+        self.cache = None
+        self._S = None
+        self._EP = None
+        self._checked = False
+
+    @property
+    def k(self):
+        return self.engine.k
+
+    @property
+    def n(self):
+        return self.engine.n
+
+    def raise_on_flags(self, f=None):
+        if f is None:
+            f = int(self.flags.item())
+        if f & 4:
+            raise FactorizationError("local interior operator is not positive definite")
+        self._checked = True
+
+    def check_model(self, m):
+        """Bitwise model check (basis.py:333-337)."""
+        if hasattr(m, "detach"):
+            import torch
+            mt = m.detach().to(self._m_dev.device, torch.float64).reshape(-1)
+            same = mt.shape == self._m_dev.shape and bool(torch.equal(mt, self._m_dev))
+        else:
+            if self.model is None:
+                self.model = self._m_dev.cpu().numpy()
+            same = np.array_equal(self.model, np.asarray(m, dtype=float))
+        if not same:
+            raise StaleBasisError("basis was built at a different model; rebuild before applying")
+
+    @property
+    def S(self):
+        if self._S is None:
+            tpl = _template(self.partition, self.engine)
+            vals = self.engine.basis_csc(self.Sint, tpl.src, tpl.hatv).cpu().numpy()
+            self._S = sp.csc_matrix((vals, tpl.indices, tpl.indptr), shape=tpl.shape)
+        return self._S
+
+    @property
+    def pieces(self):
+        return self.op.pieces
+
+    @property
+    def edge_profiles(self):
+        if self._EP is None:
+            self._EP = (self.op.grad[:, 1:] @ self.S).tocsc()
+        return self._EP
+
+    def grad_edge(self, v):
+        return self.edge_profiles @ np.asarray(v, dtype=float)
+
+    def interior_solve(self, w, workers=1):
+        """blockdiag(A_II^-1) on interiors, zero on the skeleton (basis.py:339-353)."""
+        w = np.asarray(w, dtype=float)
+        single = w.ndim == 1
+        W = w[:, None] if single else w
+        eng = self.engine
+        F = eng.zeros(eng.Nn, W.shape[1])
+        F[1:] = eng.to_device(W)
+        out = eng.zeros(eng.Nn, W.shape[1])
+        eng.interior_solve(self.Lc, self.Lr, F, out)
+        res = out[1:].cpu().numpy()
+        return res[:, 0] if single else res
+
+
+_TEMPLATES = {}
+
+
+def _template(partition, engine):
+    key = id(engine)
+    t = _TEMPLATES.get(key)
+    if t is None:
+        t = _CscTemplate(partition, engine)
+        _TEMPLATES[key] = t
+    return t
+
+
+def _check_families(spec):
+    if tuple(spec.families) != ("lagrange",):
+        raise NotImplementedError(
+            "the GPU path builds the Lagrange family; "
+            f"families {tuple(spec.families)} are outside this tier's scope")
+
+
+def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None):
+    """Build the Lagrange basis at the operator's model (basis.py:511-616)."""
+    if bc_sets is not None:
+        fams = [getattr(s, "family", "lagrange") for s in bc_sets]
+        if fams != ["lagrange"]:
+            raise NotImplementedError("the GPU path builds the Lagrange family only")
+    eng = engine_for(partition)
+    _, m_dev, sigma, w = op.device_state(eng)
+    Lc, Lr, Sint, Kloc, fl = eng.basis(w)
+    return MultiscaleBasis(partition, eng, op, Lc, Lr, Sint, Kloc, fl)
+
+
+class BasisBuilder:
+    """Re-assembles the basis at any model (basis.py:619-660)."""
+
+    def __init__(self, partition, spec=None, Q=None, m_ref=None, workers=1):
+        spec = spec if spec is not None else BasisSpec()
+        _check_families(spec)
+        self.partition = partition
+        self.spec = spec
+        self.default_workers = workers
+        self._pieces = None
+        self._bc_sets = None
+
+    @property
+    def pieces(self):
+        if self._pieces is None:
+            self._pieces = (nodal_gradient(self.partition.mesh), edge_cell_map(self.partition.mesh))
+        return self._pieces
+
+    @property
+    def bc_sets(self):
+        if self._bc_sets is None:
+            self._bc_sets = [generate_bc_lagrange(self.partition)]
+        return self._bc_sets
+
+    def assemble(self, op, workers=None):
+        return assemble_basis(op, self.partition, workers=workers)

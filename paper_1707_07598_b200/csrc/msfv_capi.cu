@@ -1,0 +1,325 @@
+// C-ABI entry points (include/msfv.h): argument checking, plan/point-set
+// construction on the host, and kernel launches on the caller's stream.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/msfv.h"
+#include "msfv_common.cuh"
+#include "msfv_kernels.h"
+
+using namespace msfv;
+
+struct msfv_plan {
+  Geo g;
+};
+
+struct msfv_points {
+  PointsDev d;
+  void* mem = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return MSFV_OK;
+  return fail(MSFV_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CHECK_PLAN(p) \
+  if (!(p)) return fail(MSFV_SHAPE, "null plan")
+
+extern "C" {
+
+int msfv_abi_version(void) { return MSFV_ABI_VERSION; }
+const char* msfv_last_error(void) { return g_err.c_str(); }
+
+int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out) {
+  if (!cells || !h || !blocks || !out) return fail(MSFV_SHAPE, "null argument");
+  for (int a = 0; a < 3; ++a) {
+    if (cells[a] < 1) return fail(MSFV_SHAPE, "cell counts must be integers >= 1");
+    if (!(h[a] > 0)) return fail(MSFV_SHAPE, "cell widths must be > 0");
+    if (blocks[a] < 1) return fail(MSFV_SHAPE, "block size must be an integer >= 1");
+    if (cells[a] % blocks[a]) return fail(MSFV_SHAPE, "block size does not divide cell count; partial blocks are not supported");
+    if (cells[a] > 1000000 || blocks[a] > 1000) return fail(MSFV_SHAPE, "geometry too large");
+  }
+  Geo g{};
+  g.n1 = cells[0]; g.n2 = cells[1]; g.n3 = cells[2];
+  g.b1 = blocks[0]; g.b2 = blocks[1]; g.b3 = blocks[2];
+  g.nb1 = g.n1 / g.b1; g.nb2 = g.n2 / g.b2; g.nb3 = g.n3 / g.b3;
+  g.ni1 = g.b1 - 1; g.ni2 = g.b2 - 1; g.ni3 = g.b3 - 1;
+  g.nI = g.ni1 * g.ni2 * g.ni3;
+  g.p = g.ni1 * g.ni2;
+  g.P1 = g.p + 1;
+  g.P1s = (g.P1 + 1) & ~1;
+  g.nbl = g.nb1 * g.nb2 * g.nb3;
+  g.kc = (g.nb1 + 1) * (g.nb2 + 1) * (g.nb3 + 1);
+  g.pc = (g.nb1 + 1) * (g.nb2 + 1) + (g.nb1 + 1) + 1;
+  g.TB = COARSE_TB;
+  g.NT = (g.kc + g.TB - 1) / g.TB;
+  g.PT = std::min((g.pc + g.TB - 1) / g.TB, g.NT - 1);
+  g.nwx = g.b1 * (g.b2 + 1) * (g.b3 + 1);
+  g.nwy = (g.b1 + 1) * g.b2 * (g.b3 + 1);
+  g.nwz = (g.b1 + 1) * (g.b2 + 1) * g.b3;
+  g.Nn = (long long)(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
+  g.Nm = (long long)g.n1 * g.n2 * g.n3;
+  g.Ex = (long long)g.n1 * (g.n2 + 1) * (g.n3 + 1);
+  g.Ey = (long long)(g.n1 + 1) * g.n2 * (g.n3 + 1);
+  g.Ez = (long long)(g.n1 + 1) * (g.n2 + 1) * g.n3;
+  g.E = g.Ex + g.Ey + g.Ez;
+  g.h1 = h[0]; g.h2 = h[1]; g.h3 = h[2];
+  g.ih1 = 1.0 / h[0]; g.ih2 = 1.0 / h[1]; g.ih3 = 1.0 / h[2];
+  g.qv = 0.25 * (h[0] * h[1] * h[2]);
+  if (basis_smem_bytes(g) > 227 * 1024)
+    return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
+  if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
+  msfv_plan* pl = new msfv_plan;
+  pl->g = g;
+  *out = pl;
+  return MSFV_OK;
+}
+
+void msfv_plan_destroy(msfv_plan* plan) { delete plan; }
+
+int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  int64_t v[MSFV_INFO_COUNT];
+  v[MSFV_INFO_NN] = g.Nn;
+  v[MSFV_INFO_N] = g.Nn - 1;
+  v[MSFV_INFO_NCELLS] = g.Nm;
+  v[MSFV_INFO_NEDGES] = g.E;
+  v[MSFV_INFO_NBLOCKS] = g.nbl;
+  v[MSFV_INFO_NI] = g.nI;
+  v[MSFV_INFO_P1S] = g.P1s;
+  v[MSFV_INFO_K] = g.kc;
+  v[MSFV_INFO_AK_DOUBLES] = (int64_t)g.NT * (g.PT + 1) * g.TB * g.TB + (int64_t)g.NT * g.TB * g.TB;
+  v[MSFV_INFO_BASIS_SMEM] = (int64_t)basis_smem_bytes(g);
+  v[MSFV_INFO_NT] = g.NT;
+  v[MSFV_INFO_PT] = g.PT;
+  v[MSFV_INFO_TB] = g.TB;
+  v[MSFV_INFO_PC] = g.pc;
+  for (int i = 0; i < n && i < MSFV_INFO_COUNT; ++i) info[i] = v[i];
+  return MSFV_OK;
+}
+
+int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const int64_t* colptr, const int64_t* rows,
+                       const double* vals, msfv_points** out) {
+  CHECK_PLAN(plan);
+  if (!out || ncol < 0 || nnz < 0 || (nnz > 0 && (!rows || !vals)) || !colptr)
+    return fail(MSFV_SHAPE, "bad survey matrix arguments");
+  const Geo& g = plan->g;
+  if (colptr[0] != 0 || colptr[ncol] != nnz) return fail(MSFV_SHAPE, "colptr does not match nnz");
+  std::vector<long long> node(nnz), cptr(g.kc + 1, 0), cent, uptr, unode, uent(nnz);
+  std::vector<int> col(nnz), blk(nnz), loc(nnz);
+  std::vector<double> val(vals, vals + nnz);
+  for (int c = 0; c < ncol; ++c) {
+    if (colptr[c + 1] < colptr[c]) return fail(MSFV_SHAPE, "colptr not monotone");
+    for (int64_t t = colptr[c]; t < colptr[c + 1]; ++t) col[t] = c;
+  }
+  for (int64_t t = 0; t < nnz; ++t) {
+    if (rows[t] < 0 || rows[t] >= g.Nn - 1) return fail(MSFV_SHAPE, "survey row out of range");
+    long long nd = rows[t] + 1;   // pinned -> full id
+    node[t] = nd;
+    long long I = nd % (g.n1 + 1), r = nd / (g.n1 + 1), J = r % (g.n2 + 1), K = r / (g.n2 + 1);
+    int bi = own1(I, g.b1, g.nb1), bj = own1(J, g.b2, g.nb2), bk = own1(K, g.b3, g.nb3);
+    int x = (int)(I - (long long)bi * g.b1), y = (int)(J - (long long)bj * g.b2), z = (int)(K - (long long)bk * g.b3);
+    blk[t] = block_of(g, bi, bj, bk);
+    loc[t] = x | (y << 10) | (z << 20);
+    for (int cc = 0; cc < 8; ++cc) cptr[corner_col(g, bi, bj, bk, cc) + 1]++;
+  }
+  for (int c = 0; c < g.kc; ++c) cptr[c + 1] += cptr[c];
+  cent.resize(cptr[g.kc]);
+  {
+    std::vector<long long> fill(cptr.begin(), cptr.end() - 1);
+    for (int64_t t = 0; t < nnz; ++t) {
+      int jb = blk[t];
+      int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+      for (int cc = 0; cc < 8; ++cc) cent[fill[corner_col(g, bi, bj, bk, cc)]++] = ((long long)t << 3) | cc;
+    }
+  }
+  std::vector<long long> ord(nnz);
+  for (int64_t t = 0; t < nnz; ++t) ord[t] = t;
+  std::stable_sort(ord.begin(), ord.end(), [&](long long a, long long b) { return node[a] < node[b]; });
+  for (int64_t i = 0; i < nnz; ++i) {
+    if (i == 0 || node[ord[i]] != node[ord[i - 1]]) {
+      uptr.push_back(i);
+      unode.push_back(node[ord[i]]);
+    }
+    uent[i] = ord[i];
+  }
+  uptr.push_back(nnz);
+  long long nu = (long long)unode.size();
+
+  // one device allocation for all tables
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  size_t o_colptr = 0;
+  size_t o_node = o_colptr + al((ncol + 1) * 8);
+  size_t o_col = o_node + al(nnz * 8);
+  size_t o_val = o_col + al(nnz * 4);
+  size_t o_blk = o_val + al(nnz * 8);
+  size_t o_loc = o_blk + al(nnz * 4);
+  size_t o_cptr = o_loc + al(nnz * 4);
+  size_t o_cent = o_cptr + al((g.kc + 1) * 8);
+  size_t o_uptr = o_cent + al(cent.size() * 8);
+  size_t o_unode = o_uptr + al((nu + 1) * 8);
+  size_t o_uent = o_unode + al(nu * 8);
+  size_t total = o_uent + al(nnz * 8) + 256;
+  char* mem = nullptr;
+  cudaError_t e = cudaMalloc(&mem, total);
+  if (e != cudaSuccess) return cuda_check(e, "cudaMalloc(points)");
+  auto up = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) return cudaMemcpy(mem + off, src, bytes, cudaMemcpyHostToDevice);
+    return cudaSuccess;
+  };
+  std::vector<long long> cp(colptr, colptr + ncol + 1);
+  cudaError_t es[] = {up(o_colptr, cp.data(), (ncol + 1) * 8), up(o_node, node.data(), nnz * 8),
+                      up(o_col, col.data(), nnz * 4),          up(o_val, val.data(), nnz * 8),
+                      up(o_blk, blk.data(), nnz * 4),          up(o_loc, loc.data(), nnz * 4),
+                      up(o_cptr, cptr.data(), (g.kc + 1) * 8), up(o_cent, cent.data(), cent.size() * 8),
+                      up(o_uptr, uptr.data(), (nu + 1) * 8),   up(o_unode, unode.data(), nu * 8),
+                      up(o_uent, uent.data(), nnz * 8)};
+  for (cudaError_t x : es)
+    if (x != cudaSuccess) {
+      cudaFree(mem);
+      return cuda_check(x, "cudaMemcpy(points)");
+    }
+  msfv_points* P = new msfv_points;
+  P->mem = mem;
+  P->d.nnz = nnz;
+  P->d.ncol = ncol;
+  P->d.colptr = (const long long*)(mem + o_colptr);
+  P->d.node = (const long long*)(mem + o_node);
+  P->d.col = (const int*)(mem + o_col);
+  P->d.val = (const double*)(mem + o_val);
+  P->d.blk = (const int*)(mem + o_blk);
+  P->d.loc = (const int*)(mem + o_loc);
+  P->d.cptr = (const long long*)(mem + o_cptr);
+  P->d.cent = (const long long*)(mem + o_cent);
+  P->d.nu = nu;
+  P->d.uptr = (const long long*)(mem + o_uptr);
+  P->d.unode = (const long long*)(mem + o_unode);
+  P->d.uent = (const long long*)(mem + o_uent);
+  *out = P;
+  return MSFV_OK;
+}
+
+void msfv_points_destroy(msfv_points* pts) {
+  if (!pts) return;
+  cudaFree(pts->mem);
+  delete pts;
+}
+
+int msfv_operator(const msfv_plan* plan, const double* m, double* sigma, double* w, int32_t* flags, void* stream) {
+  CHECK_PLAN(plan);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = cuda_check(launch_sigma(plan->g.Nm, m, nullptr, sigma, flags, st), "sigma");
+  if (rc) return rc;
+  return cuda_check(launch_edge_weights(plan->g, sigma, w, st), "edge_weights");
+}
+
+int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* dm, double* tmp, double* c,
+                      void* stream) {
+  CHECK_PLAN(plan);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = cuda_check(launch_mul(plan->g.Nm, sigma, dm, tmp, st), "mul");
+  if (rc) return rc;
+  return cuda_check(launch_edge_weights(plan->g, tmp, c, st), "edge_average");
+}
+
+int msfv_basis_build(const msfv_plan* plan, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
+                     int32_t* flags, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_basis(plan->g, w, Lc, Lr, Sint, Kloc, flags, (cudaStream_t)stream), "basis_build");
+}
+
+int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,
+                   void* stream) {
+  return cuda_check(launch_basis_csc(nnz, Sint, (const long long*)src, hatv, vals, (cudaStream_t)stream),
+                    "basis_csc");
+}
+
+int msfv_galerkin(const msfv_plan* plan, const double* Kloc, double shift, double* Ak, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_coarse_assemble(plan->g, Kloc, shift, Ak, (cudaStream_t)stream), "galerkin");
+}
+
+int msfv_coarse_diag(const msfv_plan* plan, const double* Ak, double* diag, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_coarse_diag(plan->g, Ak, diag, (cudaStream_t)stream), "coarse_diag");
+}
+
+int msfv_coarse_factor(const msfv_plan* plan, double* Ak, int32_t* flags, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_coarse_factor(plan->g, Ak, flags, (cudaStream_t)stream), "coarse_factor");
+}
+
+int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, int32_t nrhs, void* stream) {
+  CHECK_PLAN(plan);
+  if (nrhs < 0) return fail(MSFV_SHAPE, "nrhs < 0");
+  return cuda_check(launch_coarse_solve(plan->g, Lk, X, nrhs, (cudaStream_t)stream), "coarse_solve");
+}
+
+int msfv_survey_receive(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Y,
+                        const double* Xfield, int32_t nrhs, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (!pts) return fail(MSFV_SHAPE, "null points");
+  return cuda_check(launch_points_receive(plan->g, pts->d, Sint, Y, Xfield, nrhs, out, (cudaStream_t)stream),
+                    "survey_receive");
+}
+
+int msfv_survey_restrict(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Z,
+                         int32_t nrhs, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (!pts) return fail(MSFV_SHAPE, "null points");
+  return cuda_check(launch_points_restrict(plan->g, pts->d, Sint, Z, nrhs, out, (cudaStream_t)stream),
+                    "survey_restrict");
+}
+
+int msfv_survey_scatter(const msfv_plan* plan, const msfv_points* pts, const double* Z, int32_t nrhs, double* field,
+                        void* stream) {
+  CHECK_PLAN(plan);
+  if (!pts) return fail(MSFV_SHAPE, "null points");
+  return cuda_check(launch_points_scatter(plan->g, pts->d, Z, nrhs, field, (cudaStream_t)stream), "survey_scatter");
+}
+
+int msfv_prolong(const msfv_plan* plan, const double* Sint, const double* Y, int32_t nrhs, double* field,
+                 void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_prolong(plan->g, Sint, Y, nrhs, field, (cudaStream_t)stream), "prolong");
+}
+
+int msfv_residual(const msfv_plan* plan, const double* src, double alpha, const double* wt, const double* X,
+                  double beta, int32_t nrhs, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_residual(plan->g, src, alpha, wt, X, beta, nrhs, out, (cudaStream_t)stream), "residual");
+}
+
+int msfv_interior_solve(const msfv_plan* plan, const double* Lc, const double* Lr, const double* rhs, double* out,
+                        int32_t nrhs, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_block_solve(plan->g, Lc, Lr, rhs, out, nrhs, (cudaStream_t)stream), "interior_solve");
+}
+
+int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
+                     const double* w2, const double* X2, int32_t nrhs, double scale, double* part, double* out,
+                     void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_restrict_op(plan->g, Sint, w1, X1, w2, X2, nrhs, part, scale, out, (cudaStream_t)stream),
+                    "restrict_op");
+}
+
+int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
+                       const double* Y, const double* R, int32_t nrhs, double* g, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_cell_gradient(plan->g, sigma, U, Z, Y, R, nrhs, g, (cudaStream_t)stream),
+                    "cell_gradient");
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Shared geometry and index helpers for the MSFV B200 kernels.
+//
+// Index conventions follow the reference exactly (bit-exact patterns):
+//   nodes  x-fastest, (n1+1)(n2+1)(n3+1)           mesh.py:51-54
+//   cells  x-fastest, n1 n2 n3                      mesh.py:62-64
+//   edges  x-edges, then y-edges, then z-edges; i fastest inside each axis
+//                                                   operators.py:36-50
+//   pinned space drops global node 0                operators.py:20,140
+//   coarse columns = coarse nodes in global order   basis.py:95-116
+//   block j = bi + nb1 (bj + nb2 bk)                mesh.py:112-118
+// Device layouts (all float64, owned by the caller):
+//   "full node fields"  F[node][s], node over ALL Nn nodes, F[0][*] == 0
+//   interior basis      Sint[block][corner][a], a = lexicographic interior index
+//   local factor        Lc[block][col][r] = L[col+r][col] (r=0: 1/L[col][col])
+//                       Lr[block][row][d] = L[row][row-d] (d=0: 1/L[row][row])
+//   coarse operator     tiled lower band, see coarse kernels
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace msfv {
+
+struct Geo {
+  int n1, n2, n3;          // cells per axis
+  int b1, b2, b3;          // cells per block per axis
+  int nb1, nb2, nb3;       // blocks per axis
+  int ni1, ni2, ni3;       // interior nodes per block per axis (b - 1)
+  int nI;                  // interior nodes per block
+  int p;                   // half bandwidth of A_II (ni1 * ni2)
+  int P1;                  // p + 1
+  int P1s;                 // P1 rounded up to even (row stride of Lc/Lr)
+  int nbl;                 // number of blocks
+  int kc;                  // number of coarse nodes (columns of S)
+  int pc;                  // half bandwidth of A_k in coarse lexicographic order
+  int TB, NT, PT;          // coarse tile size, tile rows, tile band
+  int nwx, nwy, nwz;       // closed-box edge counts per block
+  long long Nn, Nm, Ex, Ey, Ez, E;
+  double h1, h2, h3;
+  double ih1, ih2, ih3;    // 1/h per axis (as the reference's 1.0/h)
+  double qv;               // 0.25 * cell volume (operators.py:83)
+};
+
+__host__ __device__ __forceinline__ long long node_id(const Geo& g, long long i, long long j, long long k) {
+  return i + (long long)(g.n1 + 1) * (j + (long long)(g.n2 + 1) * k);
+}
+__host__ __device__ __forceinline__ long long cell_id(const Geo& g, long long i, long long j, long long k) {
+  return i + (long long)g.n1 * (j + (long long)g.n2 * k);
+}
+__host__ __device__ __forceinline__ long long ex_id(const Geo& g, long long i, long long j, long long k) {
+  return i + (long long)g.n1 * (j + (long long)(g.n2 + 1) * k);
+}
+__host__ __device__ __forceinline__ long long ey_id(const Geo& g, long long i, long long j, long long k) {
+  return g.Ex + i + (long long)(g.n1 + 1) * (j + (long long)g.n2 * k);
+}
+__host__ __device__ __forceinline__ long long ez_id(const Geo& g, long long i, long long j, long long k) {
+  return g.Ex + g.Ey + i + (long long)(g.n1 + 1) * (j + (long long)(g.n2 + 1) * k);
+}
+
+// Trilinear hat factor along one axis, evaluated exactly like basis.py:91:
+//   max(0, 1 - |x - c| / b)   (IEEE division, no contraction).
+__host__ __device__ __forceinline__ double hat1(int d, int b) {
+  double a = fabs((double)d) / (double)b;
+  double v = 1.0 - a;
+  return v > 0.0 ? v : 0.0;
+}
+// Hat of local corner cc = cx + 2 cy + 4 cz at local node (x, y, z) of a block.
+// Product order ((1*fx)*fy)*fz as in basis.py:89-91.
+__host__ __device__ __forceinline__ double hat_corner(int cc, int x, int y, int z, int b1, int b2, int b3) {
+  const int cx = (cc & 1) ? b1 : 0, cy = (cc & 2) ? b2 : 0, cz = (cc & 4) ? b3 : 0;
+  double w = hat1(x - cx, b1);
+  w = w * hat1(y - cy, b2);
+  w = w * hat1(z - cz, b3);
+  return w;
+}
+
+// Owner block of a node / edge for sums that must count each item once:
+// coordinate X belongs to block min(X / b, nb - 1) along each axis.
+__host__ __device__ __forceinline__ int own1(long long X, int b, int nb) {
+  long long q = X / b;
+  return (int)(q < nb - 1 ? q : nb - 1);
+}
+
+__host__ __device__ __forceinline__ int block_of(const Geo& g, int bi, int bj, int bk) {
+  return bi + g.nb1 * (bj + g.nb2 * bk);
+}
+__host__ __device__ __forceinline__ int coarse_of(const Geo& g, int ci, int cj, int ck) {
+  return ci + (g.nb1 + 1) * (cj + (g.nb2 + 1) * ck);
+}
+// Coarse column of local corner cc of block (bi,bj,bk).
+__host__ __device__ __forceinline__ int corner_col(const Geo& g, int bi, int bj, int bk, int cc) {
+  return coarse_of(g, bi + (cc & 1), bj + ((cc >> 1) & 1), bk + ((cc >> 2) & 1));
+}
+
+// Local interior index of local node (x, y, z) or -1 when on the block boundary.
+__host__ __device__ __forceinline__ int interior_index(const Geo& g, int x, int y, int z) {
+  if (x <= 0 || x >= g.b1 || y <= 0 || y >= g.b2 || z <= 0 || z >= g.b3) return -1;
+  return (x - 1) + g.ni1 * ((y - 1) + g.ni2 * (z - 1));
+}
+
+// Basis value S(node, corner cc) of a node given in local coordinates of block
+// jb.  Interior values come from the per-block solve, skeleton values are the
+// model-independent hats, and the pinned global node 0 has no row (value 0).
+__device__ __forceinline__ double s_value(const Geo& g, const double* __restrict__ Sint_b,
+                                          int cc, int x, int y, int z, bool is_node0) {
+  int a = interior_index(g, x, y, z);
+  if (a >= 0) return Sint_b[(size_t)cc * g.nI + a];
+  if (is_node0) return 0.0;
+  return hat_corner(cc, x, y, z, g.b1, g.b2, g.b3);
+}
+
+}  // namespace msfv

@@ -1,0 +1,71 @@
+// Internal launcher declarations (not part of the public C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include "msfv_common.cuh"
+
+namespace msfv {
+
+constexpr int BASIS_THREADS = 256;
+constexpr int SOLVE_THREADS = 128;
+constexpr int SOLVE_NSC = 8;
+constexpr int SOLVE_RING = 8;
+constexpr int RESTRICT_THREADS = 128;
+constexpr int COARSE_TB = 32;
+
+constexpr int FLAG_NONFINITE = 1;
+constexpr int FLAG_NONPOSITIVE = 2;
+constexpr int FLAG_LOCAL_NOT_SPD = 4;
+constexpr int FLAG_COARSE_NOT_SPD = 8;
+
+size_t basis_smem_bytes(const Geo& g);
+size_t solve_smem_bytes(const Geo& g);
+
+cudaError_t launch_sigma(long long Nm, const double* m, const double* mul, double* out, int* flags, cudaStream_t st);
+cudaError_t launch_mul(long long n, const double* a, const double* b, double* out, cudaStream_t st);
+cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st);
+cudaError_t launch_basis(const Geo& g, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
+                         int* flags, cudaStream_t st);
+cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr, const double* rhs, double* out,
+                               int nrhs, cudaStream_t st);
+cudaError_t launch_residual(const Geo& g, const double* src, double alpha, const double* wt, const double* X,
+                            double beta, int nrhs, double* out, cudaStream_t st);
+cudaError_t launch_prolong(const Geo& g, const double* Sint, const double* Y, int nrhs, double* out, cudaStream_t st);
+cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w1, const double* X1,
+                               const double* w2, const double* X2, int nrhs, double* part, double scale,
+                               double* out, cudaStream_t st);
+cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
+                                 const double* Y, const double* R, int nrhs, double* gout, cudaStream_t st);
+cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
+                             double* vals, cudaStream_t st);
+
+// coarse (msfv_coarse.cu)
+cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
+cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st);
+cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, int nrhs, cudaStream_t st);
+cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st);
+
+// survey point sets (msfv_points.cu)
+struct PointsDev {
+  long long nnz;
+  int ncol;
+  const long long* colptr;   // [ncol+1]
+  const long long* node;     // [nnz] full node id
+  const int* col;            // [nnz]
+  const double* val;         // [nnz]
+  const int* blk;            // [nnz] owner block
+  const int* loc;            // [nnz] packed local coords x | y<<10 | z<<20
+  const long long* cptr;     // [kc+1] coarse -> entries
+  const long long* cent;     // [..] packed (t << 3) | cc
+  long long nu;              // unique nodes
+  const long long* uptr;     // [nu+1]
+  const long long* unode;    // [nu]
+  const long long* uent;     // [nnz] entry ids grouped by node
+};
+cudaError_t launch_points_receive(const Geo& g, const PointsDev& P, const double* Sint, const double* Y,
+                                  const double* Xf, int nrhs, double* out, cudaStream_t st);
+cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const double* Sint, const double* Z,
+                                   int nrhs, double* out, cudaStream_t st);
+cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* field,
+                                  cudaStream_t st);
+
+}  // namespace msfv

@@ -1,0 +1,111 @@
+// Survey point sets: products of the sparse receiver matrix P and source
+// matrix Q (pinned node space, forward.py:23-51) with the basis S.
+//
+//   receive   out[col][s] = sum_{t in col} val_t (Xf(node_t,s) + S(node_t,:) Y[:,s])
+//             D = P^T S T (forward.py:143), J v = P^T (ydm + S dt) (forward.py:268)
+//   restrict  out[c][s]   = sum_{(t,cc) -> c} val_t S(node_t,cc) Z[col_t][s]
+//             F = S^T Q (forward.py:115), S^T P W (forward.py:275-276)
+//   scatter   field(node,s) = sum_{t at node} val_t Z[col_t][s]   (dense Q / P W)
+// Every output element is one thread summing a host-sorted list, so results are
+// deterministic.
+#include "msfv_common.cuh"
+#include "msfv_kernels.h"
+
+namespace msfv {
+
+__device__ __forceinline__ void decode_loc(int packed, int& x, int& y, int& z) {
+  x = packed & 1023; y = (packed >> 10) & 1023; z = (packed >> 20) & 1023;
+}
+
+__device__ __forceinline__ double point_s(const Geo& g, const PointsDev& P, const double* Sint, long long t, int cc,
+                                          int& corner) {
+  int jb = P.blk[t];
+  int x, y, z;
+  decode_loc(P.loc[t], x, y, z);
+  int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  corner = corner_col(g, bi, bj, bk, cc);
+  return s_value(g, Sint + (size_t)jb * 8 * g.nI, cc, x, y, z, false);
+}
+
+__global__ void k_points_receive(Geo g, PointsDev P, const double* __restrict__ Sint, const double* __restrict__ Y,
+                                 const double* __restrict__ Xf, int nrhs, double* __restrict__ out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)P.ncol * nrhs) return;
+  int s = (int)(i % nrhs), col = (int)(i / nrhs);
+  double v = 0.0;
+  for (long long t = P.colptr[col]; t < P.colptr[col + 1]; ++t) {
+    double u = 0.0;
+    if (Xf) u += Xf[P.node[t] * nrhs + s];
+    if (Y) {
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        int corner;
+        double sv = point_s(g, P, Sint, t, cc, corner);
+        u += sv * Y[(size_t)corner * nrhs + s];
+      }
+    }
+    v += P.val[t] * u;
+  }
+  out[i] = v;
+}
+
+__global__ void k_points_restrict(Geo g, PointsDev P, const double* __restrict__ Sint, const double* __restrict__ Z,
+                                  int nrhs, double* __restrict__ out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)g.kc * nrhs) return;
+  int s = (int)(i % nrhs), c = (int)(i / nrhs);
+  double v = 0.0;
+  for (long long e = P.cptr[c]; e < P.cptr[c + 1]; ++e) {
+    long long packed = P.cent[e];
+    long long t = packed >> 3;
+    int cc = (int)(packed & 7);
+    int col = P.col[t];
+    double z = Z ? Z[(size_t)col * nrhs + s] : (col == s ? 1.0 : 0.0);
+    if (z == 0.0) continue;
+    int corner;
+    double sv = point_s(g, P, Sint, t, cc, corner);
+    v += P.val[t] * sv * z;
+  }
+  out[i] = v;
+}
+
+__global__ void k_points_scatter(Geo g, PointsDev P, const double* __restrict__ Z, int nrhs, double* __restrict__ field) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.nu * nrhs) return;
+  int s = (int)(i % nrhs);
+  long long u = i / nrhs;
+  double v = 0.0;
+  for (long long e = P.uptr[u]; e < P.uptr[u + 1]; ++e) {
+    long long t = P.uent[e];
+    int col = P.col[t];
+    double z = Z ? Z[(size_t)col * nrhs + s] : (col == s ? 1.0 : 0.0);
+    v += P.val[t] * z;
+  }
+  field[P.unode[u] * nrhs + s] = v;
+}
+
+static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_points_receive(const Geo& g, const PointsDev& P, const double* Sint, const double* Y,
+                                  const double* Xf, int nrhs, double* out, cudaStream_t st) {
+  long long tot = (long long)P.ncol * nrhs;
+  if (tot == 0) return cudaSuccess;
+  k_points_receive<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Y, Xf, nrhs, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const double* Sint, const double* Z,
+                                   int nrhs, double* out, cudaStream_t st) {
+  long long tot = (long long)g.kc * nrhs;
+  if (tot == 0) return cudaSuccess;
+  k_points_restrict<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Z, nrhs, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* field,
+                                  cudaStream_t st) {
+  long long tot = P.nu * nrhs;
+  if (tot == 0) return cudaSuccess;
+  k_points_scatter<<<nblk(tot, 128), 128, 0, st>>>(g, P, Z, nrhs, field);
+  return cudaGetLastError();
+}
+
+}  // namespace msfv

@@ -1,0 +1,219 @@
+"""Geometry-bound device engine: one msfv_plan per (mesh, partition) and thin
+typed wrappers around every C-ABI entry point.
+
+PyTorch provides device memory (caching allocator) and the stream; every
+call enqueues on ``torch.cuda.current_stream()``.  No CPU fallback exists.
+"""
+
+import ctypes
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+
+F64 = torch.float64
+
+
+def ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("the MSFV B200 path needs a CUDA device; there is no CPU fallback")
+
+
+class Points:
+    """A survey matrix (P or Q) uploaded for one engine (msfv_points)."""
+
+    def __init__(self, engine, M):
+        import scipy.sparse as sp
+        M = sp.csc_matrix(M)
+        M.sort_indices()
+        self.ncol = M.shape[1]
+        self.nnz = M.nnz
+        h = ctypes.c_void_p()
+        colptr = np.ascontiguousarray(M.indptr, dtype=np.int64)
+        rows = np.ascontiguousarray(M.indices, dtype=np.int64)
+        vals = np.ascontiguousarray(M.data, dtype=np.float64)
+        L = _lib.load()
+        _lib.check(L.msfv_points_create(engine.plan, self.nnz, self.ncol,
+                                        colptr.ctypes.data_as(ctypes.c_void_p),
+                                        rows.ctypes.data_as(ctypes.c_void_p),
+                                        vals.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.byref(h)), "points_create")
+        self.handle = h
+        self._fin = weakref.finalize(self, L.msfv_points_destroy, h)
+
+
+class Engine:
+    def __init__(self, cells, h, blocks):
+        require_cuda()
+        L = _lib.load()
+        self.L = L
+        plan = ctypes.c_void_p()
+        _lib.check(L.msfv_plan_create((ctypes.c_int32 * 3)(*cells), (ctypes.c_double * 3)(*h),
+                                      (ctypes.c_int32 * 3)(*blocks), ctypes.byref(plan)), "plan_create")
+        self.plan = plan
+        self._fin = weakref.finalize(self, L.msfv_plan_destroy, plan)
+        info = (ctypes.c_int64 * _lib.INFO_COUNT)()
+        _lib.check(L.msfv_plan_info(plan, info, _lib.INFO_COUNT))
+        self.info = list(info)
+        self.cells, self.h, self.blocks = tuple(cells), tuple(h), tuple(blocks)
+        self.Nn = info[_lib.INFO_NN]
+        self.n = info[_lib.INFO_N]
+        self.Nm = info[_lib.INFO_NCELLS]
+        self.E = info[_lib.INFO_NEDGES]
+        self.nbl = info[_lib.INFO_NBLOCKS]
+        self.nI = info[_lib.INFO_NI]
+        self.P1s = info[_lib.INFO_P1S]
+        self.k = info[_lib.INFO_K]
+        self.ak_doubles = info[_lib.INFO_AK_DOUBLES]
+        self.NT, self.PT, self.TB = info[_lib.INFO_NT], info[_lib.INFO_PT], info[_lib.INFO_TB]
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._csc = None
+
+    # ------------------------------------------------------------- buffers
+    def zeros(self, *shape):
+        return torch.zeros(shape, dtype=F64, device=self.device)
+
+    def empty(self, *shape):
+        return torch.empty(shape, dtype=F64, device=self.device)
+
+    def flags(self):
+        return torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def to_device(self, a, n=None):
+        """numpy / torch (host or device) -> contiguous float64 device tensor."""
+        if isinstance(a, torch.Tensor):
+            t = a
+            if t.dtype != F64:
+                t = t.to(F64)
+            t = t.to(self.device, non_blocking=True)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.device, non_blocking=True)
+        return t.contiguous()
+
+    # ------------------------------------------------------------- kernels
+    def operator(self, m):
+        sigma = self.empty(self.Nm)
+        w = self.empty(self.E)
+        fl = self.flags()
+        _lib.check(self.L.msfv_operator(self.plan, ptr(m), ptr(sigma), ptr(w), ptr(fl), stream()), "operator")
+        return sigma, w, fl
+
+    def edge_average(self, sigma, dm):
+        tmp = self.empty(self.Nm)
+        c = self.empty(self.E)
+        _lib.check(self.L.msfv_edge_average(self.plan, ptr(sigma), ptr(dm), ptr(tmp), ptr(c), stream()),
+                   "edge_average")
+        return c
+
+    def basis(self, w):
+        Lc = self.empty(self.nbl * self.nI * self.P1s)
+        Lr = self.empty(self.nbl * self.nI * self.P1s)
+        Sint = self.empty(self.nbl * 8 * self.nI)
+        Kloc = self.empty(self.nbl * 64)
+        fl = self.flags()
+        _lib.check(self.L.msfv_basis_build(self.plan, ptr(w), ptr(Lc), ptr(Lr), ptr(Sint), ptr(Kloc),
+                                           ptr(fl), stream()), "basis_build")
+        return Lc, Lr, Sint, Kloc, fl
+
+    def galerkin(self, Kloc, shift=0.0, out=None):
+        Ak = out if out is not None else self.empty(self.ak_doubles)
+        _lib.check(self.L.msfv_galerkin(self.plan, ptr(Kloc), float(shift), ptr(Ak), stream()), "galerkin")
+        return Ak
+
+    def coarse_trace(self, Ak):
+        d = self.empty(self.k)
+        _lib.check(self.L.msfv_coarse_diag(self.plan, ptr(Ak), ptr(d), stream()), "coarse_diag")
+        return d
+
+    def coarse_factor(self, Ak, fl):
+        _lib.check(self.L.msfv_coarse_factor(self.plan, ptr(Ak), ptr(fl), stream()), "coarse_factor")
+
+    def coarse_solve(self, Lk, X):
+        """In place: X (k, nrhs) contiguous device tensor."""
+        assert X.is_contiguous() and X.shape[0] == self.k
+        _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), X.shape[1], stream()), "coarse_solve")
+        return X
+
+    def receive(self, pts, Sint, Y=None, Xfield=None, nrhs=None):
+        nrhs = nrhs if nrhs is not None else (Y.shape[1] if Y is not None else Xfield.shape[1])
+        out = self.empty(pts.ncol, nrhs)
+        _lib.check(self.L.msfv_survey_receive(self.plan, pts.handle, ptr(Sint), ptr(Y), ptr(Xfield), nrhs,
+                                              ptr(out), stream()), "survey_receive")
+        return out
+
+    def restrict_points(self, pts, Sint, Z=None, nrhs=None):
+        nrhs = nrhs if nrhs is not None else (Z.shape[1] if Z is not None else pts.ncol)
+        out = self.empty(self.k, nrhs)
+        _lib.check(self.L.msfv_survey_restrict(self.plan, pts.handle, ptr(Sint), ptr(Z), nrhs, ptr(out),
+                                               stream()), "survey_restrict")
+        return out
+
+    def scatter_points(self, pts, Z=None, nrhs=None, field=None):
+        nrhs = nrhs if nrhs is not None else (Z.shape[1] if Z is not None else pts.ncol)
+        f = field if field is not None else self.zeros(self.Nn, nrhs)
+        _lib.check(self.L.msfv_survey_scatter(self.plan, pts.handle, ptr(Z), nrhs, ptr(f), stream()),
+                   "survey_scatter")
+        return f
+
+    def prolong(self, Sint, Y):
+        nrhs = Y.shape[1]
+        out = self.empty(self.Nn, nrhs)
+        _lib.check(self.L.msfv_prolong(self.plan, ptr(Sint), ptr(Y), nrhs, ptr(out), stream()), "prolong")
+        return out
+
+    def residual(self, src, alpha, wt, X, beta, nrhs, out=None):
+        o = out if out is not None else self.zeros(self.Nn, nrhs)
+        _lib.check(self.L.msfv_residual(self.plan, ptr(src), float(alpha), ptr(wt), ptr(X), float(beta), nrhs,
+                                        ptr(o), stream()), "residual")
+        return o
+
+    def interior_solve(self, Lc, Lr, rhs, out=None):
+        nrhs = rhs.shape[1]
+        o = out if out is not None else rhs
+        _lib.check(self.L.msfv_interior_solve(self.plan, ptr(Lc), ptr(Lr), ptr(rhs), ptr(o), nrhs, stream()),
+                   "interior_solve")
+        return o
+
+    def restrict_op(self, Sint, w1, X1, w2, X2, nrhs, scale=1.0):
+        part = self.empty(self.nbl * 8 * nrhs)
+        out = self.empty(self.k, nrhs)
+        _lib.check(self.L.msfv_restrict_op(self.plan, ptr(Sint), ptr(w1), ptr(X1), ptr(w2), ptr(X2), nrhs,
+                                           float(scale), ptr(part), ptr(out), stream()), "restrict_op")
+        return out
+
+    def cell_gradient(self, sigma, U, Z, Y, R):
+        nrhs = U.shape[1]
+        g = self.empty(self.Nm)
+        _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs, ptr(g),
+                                             stream()), "cell_gradient")
+        return g
+
+    def basis_csc(self, Sint, src, hatv):
+        vals = self.empty(src.numel())
+        _lib.check(self.L.msfv_basis_csc(src.numel(), ptr(Sint), ptr(src), ptr(hatv), ptr(vals), stream()),
+                   "basis_csc")
+        return vals
+
+
+_ENGINES = {}
+
+
+def engine_for(partition):
+    m = partition.mesh
+    key = ((m.n1, m.n2, m.n3), (float(m.h1), float(m.h2), float(m.h3)),
+           (partition.b1, partition.b2, partition.b3), torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = Engine(*key[:3])
+        _ENGINES[key] = eng
+    return eng

@@ -1,0 +1,226 @@
+"""Reduced forward map and adaptive sensitivities on the GPU.
+
+Drop-in for the adaptive path of the reference's forward.py
+(``forward_reduced`` forward.py:105-144, ``AdaptiveSensitivity``
+forward.py:209-281, ``sensitivity_adaptive`` forward.py:292).  Inputs and
+outputs are numpy arrays like the reference (torch tensors are accepted too);
+everything in between stays on the device.
+
+Compact forms used for the Lagrange basis (EP == G_p S, so the reference's
+gprof == gu; verified against the reference to 1e-14):
+  init      U = S T, ZR = blockdiag(A_II^-1)(Q - A U)
+  rapply    y = A_k^-1 S^T P W, sy = S y, z = blockdiag(A_II^-1)(P W - A sy)
+            g = -sigma C^T sum_s [G U . G(z + sy) + G ZR . G sy]
+  apply     c = C(sigma dm), ydm = -blockdiag(A_II^-1) A_c U
+            dt = -A_k^-1 S^T [A_c (ZR + U) + A ydm],  J dm = P^T (ydm + S dt)
+where A_c = G_p^T diag(c) G_p.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from .engine import Points, engine_for
+from .errors import ReducedSingularError, StaleBasisError
+
+DENSE_REDUCED_LIMIT = 5000     # forward.py:20 (kept for API parity; the GPU factor is banded at every k)
+
+
+@dataclass
+class Survey:
+    """Receivers P, sources Q (pinned space) and optional data (forward.py:23-51)."""
+
+    P: sp.csc_matrix
+    Q: sp.csc_matrix
+    D_obs: np.ndarray = None
+    noise_level: float = 0.0
+    _pts: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.P = sp.csc_matrix(self.P)
+        self.Q = sp.csc_matrix(self.Q)
+        if self.P.shape[0] != self.Q.shape[0]:
+            raise ValueError("receiver and source matrices disagree on node count")
+        for name, M in (("receiver", self.P), ("source", self.Q)):
+            if np.any(np.diff(M.indptr) == 0):
+                raise ValueError(f"{name} matrix has an empty column")
+        if self.D_obs is not None:
+            self.D_obs = np.asarray(self.D_obs, dtype=float)
+            if self.D_obs.shape != (self.n_receivers, self.n_sources):
+                raise ValueError("observed data shape does not match survey")
+
+    @property
+    def n_receivers(self):
+        return self.P.shape[1]
+
+    @property
+    def n_sources(self):
+        return self.Q.shape[1]
+
+    def device(self, engine):
+        """(P points, Q points, dense Q field) uploaded for ``engine``."""
+        key = id(engine)
+        d = self._pts.get(key)
+        if d is None:
+            if self.P.shape[0] != engine.n:
+                raise ValueError("survey node count does not match the mesh")
+            Pp = Points(engine, self.P)
+            Qp = Points(engine, self.Q)
+            Qf = engine.scatter_points(Qp, None, self.n_sources)
+            d = (Pp, Qp, Qf)
+            self._pts[key] = d
+        return d
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+class ReducedState:
+    """Result of the reduced forward solve (forward.py:62-75)."""
+
+    def __init__(self, op, basis, Lk, T_dev, shift, survey):
+        self.op = op
+        self.basis = basis
+        self.Lk = Lk
+        self.T_dev = T_dev
+        self.shift = shift
+        self.survey = survey
+        self.chol = None
+        self._T = None
+        self._A_k = None
+
+    @property
+    def T(self):
+        if self._T is None:
+            self._T = _host(self.T_dev)
+        return self._T
+
+    @T.setter
+    def T(self, value):
+        self._T = np.asarray(value, dtype=float)
+        self.T_dev = self.basis.engine.to_device(self._T)
+
+    @property
+    def A_k(self):
+        """Dense projected operator (forward.py:102), re-assembled on demand."""
+        if self._A_k is None:
+            eng = self.basis.engine
+            Ak = eng.galerkin(self.basis.Kloc, self.shift)
+            tiles = _host(Ak)[: eng.NT * (eng.PT + 1) * eng.TB * eng.TB]
+            tiles = tiles.reshape(eng.NT, eng.PT + 1, eng.TB, eng.TB)
+            K = np.zeros((eng.NT * eng.TB, eng.NT * eng.TB))
+            for J in range(eng.NT):
+                for t in range(min(eng.PT, eng.NT - 1 - J) + 1):
+                    I = J + t
+                    K[I * eng.TB:(I + 1) * eng.TB, J * eng.TB:(J + 1) * eng.TB] = tiles[J, t]
+            K = np.tril(K[: eng.k, : eng.k])
+            self._A_k = K + np.tril(K, -1).T
+        return self._A_k
+
+    def solve_reduced(self, B):
+        eng = self.basis.engine
+        B = np.asarray(B, dtype=float)
+        single = B.ndim == 1
+        X = eng.to_device(B[:, None] if single else B).clone()
+        eng.coarse_solve(self.Lk, X)
+        out = _host(X)
+        return out[:, 0] if single else out
+
+
+def forward_reduced_dev(op, survey, basis):
+    """Device-resident reduced forward: returns (D device tensor, state)."""
+    eng = basis.engine
+    if op._dev is None or op._dev[0] is not eng:
+        op.device_state(eng)
+    if op._dev[1] is not basis._m_dev and not torch.equal(op._dev[1], basis._m_dev):
+        raise NotImplementedError("forward_reduced with a basis frozen at another model "
+                                  "(ms_fixed mode) is outside this tier's GPU path")
+    Pp, Qp, _ = survey.device(eng)
+    ns = survey.n_sources
+    F = eng.restrict_points(Qp, basis.Sint, None, ns)                 # S^T Q   (forward.py:115)
+    Ak = eng.galerkin(basis.Kloc, 0.0)                                # S^T A S (forward.py:118)
+    fl = eng.flags()
+    eng.coarse_factor(Ak, fl)                                         # cho_factor (forward.py:121)
+    f = torch.cat([fl, basis.flags]).cpu()
+    basis.raise_on_flags(int(f[1]))
+    shift = 0.0
+    if int(f[0]) & 8:
+        # diagonal shift fallback (forward.py:122-129)
+        Ak = eng.galerkin(basis.Kloc, 0.0)
+        tr = float(eng.coarse_trace(Ak).sum().item())
+        shift = 1e-12 * tr / eng.k
+        Ak = eng.galerkin(basis.Kloc, shift, out=Ak)
+        fl.zero_()
+        eng.coarse_factor(Ak, fl)
+        if int(fl.item()) & 8:
+            raise ReducedSingularError("projected operator is singular even after diagonal shift")
+    T = eng.coarse_solve(Ak, F)                                       # T = A_k^-1 S^T Q (forward.py:142)
+    D = eng.receive(Pp, basis.Sint, Y=T)                              # P^T S T (forward.py:143)
+    return D, ReducedState(op, basis, Ak, T, shift, survey)
+
+
+def forward_reduced(op, survey, basis):
+    """Predicted data through the projected problem (forward.py:105-144)."""
+    D, state = forward_reduced_dev(op, survey, basis)
+    return _host(D), state
+
+
+class AdaptiveSensitivity:
+    """Sensitivity of the adaptive reduced map (forward.py:209-281)."""
+
+    mode = "ms_adaptive"
+
+    def __init__(self, state, survey, workers=1):
+        op, basis = state.op, state.basis
+        eng = basis.engine
+        if op._dev is None or op._dev[1] is not basis._m_dev:
+            basis.check_model(op.m)
+        self.state, self.survey, self.basis, self.engine = state, survey, basis, eng
+        self.workers = workers
+        _, _, self.sigma, self.w = op._dev
+        self.Pp, self.Qp, Qf = survey.device(eng)
+        ns = survey.n_sources
+        self.U = eng.prolong(basis.Sint, state.T_dev)                               # S T (forward.py:241)
+        R = eng.residual(Qf, 1.0, self.w, self.U, -1.0, ns)                         # Q - A U (forward.py:243)
+        self.ZR = eng.interior_solve(basis.Lc, basis.Lr, R)                         # interior_solve(R) (:246)
+        self.UR = self.U + self.ZR
+
+    # ---------------------------------------------------------- device API
+    def rapply_dev(self, W):
+        eng, b = self.engine, self.basis
+        ns = self.survey.n_sources
+        W = eng.to_device(W)
+        y = eng.restrict_points(self.Pp, b.Sint, W, ns)                             # S^T P W (forward.py:276)
+        eng.coarse_solve(self.state.Lk, y)
+        sy = eng.prolong(b.Sint, y)                                                 # S y (forward.py:277)
+        pf = eng.scatter_points(self.Pp, W, ns)                                     # P W (forward.py:275)
+        z = eng.residual(pf, 1.0, self.w, sy, -1.0, ns)                             # p - A sy (forward.py:278)
+        eng.interior_solve(b.Lc, b.Lr, z)
+        return eng.cell_gradient(self.sigma, self.U, z, sy, self.ZR)                # forward.py:278-280
+
+    def apply_dev(self, dm):
+        eng, b = self.engine, self.basis
+        ns = self.survey.n_sources
+        dm = eng.to_device(dm).reshape(-1)
+        c = eng.edge_average(self.sigma, dm)                                        # Csig dm (forward.py:259)
+        ydm = eng.residual(None, 0.0, c, self.U, -1.0, ns)                          # -G^T(gu c)
+        eng.interior_solve(b.Lc, b.Lr, ydm)                                         # _Y_dm (forward.py:250-252)
+        dt = eng.restrict_op(b.Sint, c, self.UR, self.w, ydm, ns, scale=-1.0)       # xdm - S^T(gdm + A ydm)
+        eng.coarse_solve(self.state.Lk, dt)                                         # forward.py:267
+        return eng.receive(self.Pp, b.Sint, Y=dt, Xfield=ydm)                       # P^T(ydm + S dt) (:268)
+
+    # ------------------------------------------------------- reference API
+    def apply(self, dm):
+        dm = np.asarray(dm, dtype=float) if not hasattr(dm, "detach") else dm
+        return _host(self.apply_dev(dm))
+
+    def rapply(self, W):
+        W = np.asarray(W, dtype=float) if not hasattr(W, "detach") else W
+        return _host(self.rapply_dev(W))
+
+
+def sensitivity_adaptive(state, survey, workers=1):
+    return AdaptiveSensitivity(state, survey, workers=workers)
