@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: adaptive MSFV forward + gradient on BASELINE.json config 4.
+
+Contract (one JSON line from rank 0):
+  step   = one forward + misfit + gradient (J^T r) of the adaptive MSFV reduced
+           model: A(m), basis P(m) (all local block solves), Galerkin A_k,
+           coarse factor + solve, D = P^T S T, misfit, sensitivity init and
+           rapply.  Metric "MSFV forward+gradient s/iter" (lower is better).
+  value  = device-timed seconds per step (CUDA events, inputs resident in HBM)
+           divided by the number of replicas (whole-job aggregate).
+  e2e    = same step through the public drop-in API with host buffers
+           (pinned m in, D and g back to host), H2D/D2H inside the timed region.
+Workload: 128^3 cells, 8^3-cell blocks (4096 local solves), 16 dipoles,
+1024 receivers, m = 1.5 * smoothed GRF (sigma 6 cells), seed 0.  Every buffer
+of the step (factors ~1.1 GB) exceeds the 126 MB L2, so no flush is needed.
+
+--impl reference runs the CPU oracle port (oracle/, a numpy/scipy
+restatement of the reference msinv path) on a bounded z-slab sample of the
+same workload and scales it to the full config (see "sample").
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MSFV forward+gradient s/iter"
+UNIT = "s/iter"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(cfg_id):
+    from paper_1707_07598_b200.models import CONFIGS
+    c = CONFIGS[cfg_id]
+    n, b = c["n"], c["b"]
+    nb = n // b
+    return {
+        "workload": f"BASELINE config {cfg_id}: 3D {n}^3 cells, {b}^3-cell blocks "
+                    f"({nb ** 3} local block solves), {c['n_src'][0] * c['n_src'][1]} dipole sources, "
+                    f"{c['n_rec'][0] * c['n_rec'][1]} receivers, adaptive Lagrange MSFV forward+misfit+gradient",
+        "mesh": [n, n, n], "blocks": [b, b, b], "n_blocks": nb ** 3, "k_coarse": (nb + 1) ** 3,
+        "n_sources": c["n_src"][0] * c["n_src"][1], "n_receivers": c["n_rec"][0] * c["n_rec"][1],
+        "model": f"{c['field'][1]} * GRF(sigma={c['field'][0]} cells), seed 0",
+        "l2": "inputs larger than L2 (per-step factors/fields >> 126 MB); no flush",
+        "parallelism": "replicas",
+    }
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline
+
+def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None):
+    """Time the CPU oracle forward+gradient on a z-slab of the config (same
+    x/y extent, survey and per-block work; nz = 2 blocks) and return
+    (seconds per slab iteration, scale factor to the full config, description)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    from oracle import msfv_oracle as orc
+    from paper_1707_07598_b200.models import CONFIGS, gaussian_field
+    c = CONFIGS[cfg_id]
+    n, b = c["n"], c["b"]
+    nz = 2 * b
+    mesh = orc.Mesh(n, n, nz, 1.0 / n, 1.0 / n, 1.0 / n)
+    part = orc.make_partition(mesh, b, b, b)
+    srv = orc.top_survey(mesh, c["n_src"], c["n_rec"])
+    m = gaussian_field(mesh, c["field"][0], c["field"][1], seed)
+    prob = orc.AdaptiveProblem(part, srv)
+    d_obs = prob.simulate(m + 0.1)[0]
+    ts = []
+    for it in range(warm + reps):
+        t0 = time.perf_counter()
+        D, st = prob.simulate(m)
+        phi, r = orc.misfit(D, d_obs)
+        prob.jacobian(st).rapply(r)
+        dt = time.perf_counter() - t0
+        if it >= warm:
+            ts.append(dt)
+        if log:
+            log(f"oracle slab iteration {it}: {dt:.2f} s")
+    scale = n / nz
+    desc = (f"oracle port (numpy/scipy restatement of msinv, 1 thread, OPENBLAS_NUM_THREADS=1) forward+misfit+gradient "
+            f"on a {n}x{n}x{nz} z-slab ({part.n_blocks} of {(n // b) ** 3} blocks, same survey layout); "
+            f"seconds scaled x{scale:g} to the full config (coarse solve scaled linearly, which understates CPU cost)")
+    return float(np.median(ts)), scale, desc
+
+
+# --------------------------------------------------------------- GPU arm
+
+def fp64_peak():
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+            return json.loads(out.strip().splitlines()[-1])["fp64_fma_tflops"], "measured live (tools/fp64_peak FMA)"
+        except Exception:  # noqa: BLE001
+            pass
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return d["fp64_fma_tflops"], "profiles/fp64_peak.json (tools/fp64_peak on B200)"
+    except Exception:  # noqa: BLE001
+        return 34.2, "fallback: earlier tools/fp64_peak measurement"
+
+
+def basis_flops(nI, p, r=8, n_edges=0):
+    """Algorithmic FP64 flops of one block in k_basis (banded algorithm as executed)."""
+    f = 0
+    for j in range(nI):
+        rm = min(p, nI - 1 - j)
+        f += rm + rm * (rm + 1)            # column scale + rank-1 update (FMA = 2)
+    for i in range(nI):
+        f += 2 * 2 * min(p, nI - 1 - i) * r  # forward + backward substitution
+    f += n_edges * (r + 2 * 36 + 1)        # local Galerkin
+    return f
+
+
+def solve_flops(nI, p, nrhs):
+    f = 0
+    for i in range(nI):
+        f += 2 * 2 * min(p, nI - 1 - i) * nrhs
+    return f
+
+
+def run_gpu(args, rank, world, log):
+    import numpy as np
+    import torch
+    import paper_1707_07598_b200 as gp
+    from paper_1707_07598_b200 import _lib
+    from paper_1707_07598_b200.engine import PhaseTimer
+    from paper_1707_07598_b200.forward import forward_reduced_dev, sensitivity_adaptive
+    from paper_1707_07598_b200.models import config_problem
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    mesh, part, survey, m = config_problem(args.config, seed=args.seed)
+    m_obs = m + 0.25 * gp.models.gaussian_field(mesh, 6.0, 1.0, args.seed + 1)
+    builder = gp.BasisBuilder(part, gp.BasisSpec())
+    problem = gp.AdaptiveReducedProblem(builder, survey)
+    d_obs = problem.simulate(m_obs)[0]
+    dev = torch.device("cuda")
+    m_dev = torch.from_numpy(m).to(dev)
+    dobs_dev = torch.from_numpy(d_obs).to(dev)
+    L = _lib.load()
+
+    def step_dev():
+        op = gp.assemble_operator(mesh, m_dev)
+        basis = builder.assemble(op)
+        D, st = forward_reduced_dev(op, survey, basis)
+        resid = D - dobs_dev
+        phi = 0.5 * torch.sum(resid * resid)
+        g = sensitivity_adaptive(st, survey).rapply_dev(resid)
+        return phi, g
+
+    # correctness guard of the timed configuration: misfit and gradient finite
+    phi0, g0 = step_dev()
+    assert torch.isfinite(phi0).item() and torch.isfinite(g0).all().item()
+
+    for _ in range(args.warmup):
+        step_dev()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    clocks.start()
+    time.sleep(0.3)
+    n0 = L.msfv_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step_dev()
+    e1.record()
+    torch.cuda.synchronize()
+    launches = L.msfv_launch_count() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    log(f"device step {ms:.3f} ms")
+
+    # per-phase breakdown (one extra instrumented step)
+    PhaseTimer.start()
+    step_dev()
+    phases = PhaseTimer.stop()
+    log("phases (ms): " + json.dumps({k: round(v, 4) for k, v in phases.items()}))
+
+    # end to end through the public API: pinned host m in, D and g out
+    e2e = None
+    if not args.no_e2e:
+        m_pin = torch.from_numpy(m).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            D, st = problem.simulate(m_pin)
+            phi, resid = gp.misfit_ssd(D, d_obs)
+            problem.jacobian(st).rapply(resid)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            D, st = problem.simulate(m_pin)
+            phi, resid = gp.misfit_ssd(D, d_obs)
+            g_host = problem.jacobian(st).rapply(resid)
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = m.nbytes + resid.nbytes
+        d2h = D.nbytes + g_host.nbytes
+        e2e = {"value": e2e_ms / 1e3 / world, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 4),
+               "path": "AdaptiveReducedProblem.simulate -> misfit_ssd -> jacobian(state).rapply (numpy out)"}
+        log(f"e2e step {e2e_ms:.3f} ms")
+
+    eng = builder.assemble(gp.assemble_operator(mesh, m_dev)).engine
+    nI, p = eng.nI, eng.info[_lib.INFO_P1S] - 1
+    p = (part.b1 - 1) * (part.b2 - 1)
+    own_edges = 3 * part.b1 * part.b2 * part.b3
+    fl_block = basis_flops(nI, p, 8, own_edges)
+    t_basis = phases.get("basis", float("nan")) / 1e3
+    peak, peak_src = fp64_peak()
+    achieved = fl_block * eng.nbl / t_basis / 1e12
+    roof = {"kernel": "k_basis (per-block A_II band Cholesky + 8-RHS solve + local Galerkin)",
+            "bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "flops_per_block": fl_block, "blocks_per_launch": eng.nbl, "launch_ms": round(t_basis * 1e3, 4),
+            "peak_source": peak_src,
+            "note": "FP64 CUDA-core bound: tcgen05 has no f64 kind; DMMA measured at the same rate as FMA"}
+    return {
+        "ms": ms, "launches": launches, "clocks": clk, "phases": phases, "e2e": e2e, "roofline": roof,
+        "block_solves_per_s": eng.nbl / t_basis, "nbl": eng.nbl,
+        "interior_solve_ms": phases.get("interior_solve"),
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+
+    def log(msg):
+        if rank == 0:
+            print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+    cfg = workload_config(args.config)
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=args.steps, warm=args.warmup, log=log)
+        v = t * scale
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc,
+                                 "sample_seconds": t},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    if world > 1:
+        torch.distributed.init_process_group("nccl", init_method="env://")
+    res = run_gpu(args, rank, world, log)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=1, warm=1, log=log)
+        cpu = {"value": t * scale, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc, "sample_seconds": t}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["ms"] / 1e3 / world, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"], 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg, "roofline": res["roofline"], "cpu_baseline": cpu,
+            "e2e": res["e2e"], "gpu_launches": int(res["launches"]),
+            "gpu_launches_per_step": res["launches"] / args.steps, "clocks": res["clocks"],
+            "local_block_solves_per_s": round(res["block_solves_per_s"], 1),
+            "phases_ms": {k: round(v, 4) for k, v in res["phases"].items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

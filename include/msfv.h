@@ -77,6 +77,8 @@ typedef struct msfv_points msfv_points;  /* one survey matrix (P or Q) on device
 
 MSFV_API int msfv_abi_version(void);
 MSFV_API const char* msfv_last_error(void);
+/* Number of kernels this library has launched so far (process-wide counter). */
+MSFV_API int64_t msfv_launch_count(void);
 
 /* TensorMesh + CoarsePartition (mesh.py:12-182).  blocks must divide cells. */
 MSFV_API int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out);

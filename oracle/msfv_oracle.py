@@ -227,16 +227,29 @@ def hat(part, coarse_node, node_ids):
 
 
 def lagrange_values(part):
-    """Skeleton hat data, one column per coarse node (basis.py:95-116)."""
+    """Skeleton hat data, one column per coarse node (basis.py:95-116).
+
+    Same entries as the reference; the hat of each coarse node is evaluated
+    only on the skeleton nodes of its support box instead of the whole
+    skeleton (values outside the box are exactly zero there too)."""
     mesh = part.mesh
     n = mesh.n_nodes - 1
-    skel = part.skeleton[part.skeleton != 0]
+    is_skel = np.zeros(mesh.n_nodes, dtype=bool)
+    is_skel[part.skeleton] = True
+    is_skel[0] = False                                   # pinned node dropped (basis.py:100)
+    b1, b2, b3 = part.b
     rows, cols, vals = [], [], []
     for c, cn in enumerate(part.coarse_nodes):
-        # only skeleton nodes within one block of the coarse node can be nonzero
-        w = hat(part, cn, skel)
+        ci, cj, ck = mesh.node_ijk(cn)
+        ii = np.arange(max(ci - b1 + 1, 0), min(ci + b1 - 1, mesh.n1) + 1)
+        jj = np.arange(max(cj - b2 + 1, 0), min(cj + b2 - 1, mesh.n2) + 1)
+        kk = np.arange(max(ck - b3 + 1, 0), min(ck + b3 - 1, mesh.n3) + 1)
+        K, J, I = np.meshgrid(kk, jj, ii, indexing="ij")
+        ids = mesh.node(I.ravel(), J.ravel(), K.ravel())
+        ids = ids[is_skel[ids]]
+        w = hat(part, cn, ids)
         nz = np.flatnonzero(w)
-        rows.append(skel[nz] - 1)
+        rows.append(ids[nz] - 1)
         cols.append(np.full(nz.size, c))
         vals.append(w[nz])
     return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),

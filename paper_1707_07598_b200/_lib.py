@@ -40,6 +40,7 @@ _D = ctypes.c_double
 SIGNATURES = {
     "msfv_abi_version": (ctypes.c_int, []),
     "msfv_last_error": (ctypes.c_char_p, []),
+    "msfv_launch_count": (ctypes.c_int64, []),
     "msfv_plan_create": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_P)]),
     "msfv_plan_destroy": (None, [_P]),
     "msfv_plan_info": (ctypes.c_int, [_P, _P, _I32]),

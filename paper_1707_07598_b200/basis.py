@@ -144,7 +144,7 @@ class MultiscaleBasis:
         self.partition = partition
         self.engine = engine
         self.op = op
-        self.model = op.m.copy() if op._m_host is not None else None
+        self._model = None
         self._m_dev = op._dev[1]
         self.Lc, self.Lr, self.Sint, self.Kloc, self.flags = Lc, Lr, Sint, Kloc, flags
         self.families = np.full(partition.n_coarse_nodes, "lagrange")
@@ -153,6 +153,12 @@ class MultiscaleBasis:
         self._S = None
         self._EP = None
         self._checked = False
+
+    @property
+    def model(self):
+        if self._model is None:
+            self._model = self._m_dev.cpu().numpy()
+        return self._model
 
     @property
     def k(self):
@@ -176,8 +182,6 @@ class MultiscaleBasis:
             mt = m.detach().to(self._m_dev.device, torch.float64).reshape(-1)
             same = mt.shape == self._m_dev.shape and bool(torch.equal(mt, self._m_dev))
         else:
-            if self.model is None:
-                self.model = self._m_dev.cpu().numpy()
             same = np.array_equal(self.model, np.asarray(m, dtype=float))
         if not same:
             raise StaleBasisError("basis was built at a different model; rebuild before applying")

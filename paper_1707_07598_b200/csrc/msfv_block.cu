@@ -11,6 +11,8 @@
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
 
+#include <atomic>
+
 namespace msfv {
 
 // ----------------------------------------------------------------- operator
@@ -592,18 +594,25 @@ __global__ void k_basis_csc(long long nnz, const double* __restrict__ Sint, cons
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+static std::atomic<long long> g_launches{0};
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 cudaError_t launch_sigma(long long Nm, const double* m, const double* mul, double* out, int* flags, cudaStream_t st) {
   if (Nm == 0) return cudaSuccess;
   k_sigma<<<nblk(Nm, 256), 256, 0, st>>>(Nm, m, mul, out, flags);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_mul(long long n, const double* a, const double* b, double* out, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_mul<<<nblk(n, 256), 256, 0, st>>>(n, a, b, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st) {
   k_edge_weights<<<nblk(g.E, 256), 256, 0, st>>>(g, cv, w);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_basis(const Geo& g, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
@@ -612,6 +621,7 @@ cudaError_t launch_basis(const Geo& g, const double* w, double* Lc, double* Lr, 
   cudaError_t e = cudaFuncSetAttribute(k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_basis<<<g.nbl, BASIS_THREADS, smem, st>>>(g, w, Lc, Lr, Sint, Kloc, flags);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr, const double* rhs, double* out,
@@ -621,6 +631,7 @@ cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr,
   cudaError_t e = cudaFuncSetAttribute(k_block_solve<SOLVE_NSC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_block_solve<SOLVE_NSC><<<g.nbl, SOLVE_THREADS, smem, st>>>(g, Lc, Lr, rhs, out, nrhs);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_residual(const Geo& g, const double* src, double alpha, const double* wt, const double* X,
@@ -628,31 +639,37 @@ cudaError_t launch_residual(const Geo& g, const double* src, double alpha, const
   long long tot = (long long)g.nbl * g.nI * nrhs;
   if (tot == 0) return cudaSuccess;
   k_residual<<<nblk(tot, 256), 256, 0, st>>>(g, src, alpha, wt, X, beta, nrhs, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_prolong(const Geo& g, const double* Sint, const double* Y, int nrhs, double* out, cudaStream_t st) {
   long long tot = g.Nn * nrhs;
   k_prolong<<<nblk(tot, 256), 256, 0, st>>>(g, Sint, Y, nrhs, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w1, const double* X1,
                                const double* w2, const double* X2, int nrhs, double* part, double scale,
                                double* out, cudaStream_t st) {
   k_restrict_op<<<g.nbl, RESTRICT_THREADS, 0, st>>>(g, Sint, w1, X1, w2, X2, nrhs, part);
+  count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_gather_corners<<<nblk((long long)g.kc * nrhs, 256), 256, 0, st>>>(g, part, nrhs, scale, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
                                  const double* Y, const double* R, int nrhs, double* gout, cudaStream_t st) {
   k_cell_gradient<<<nblk(g.Nm, 128), 128, 0, st>>>(g, sigma, U, Z, Y, R, nrhs, gout);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
                              double* vals, cudaStream_t st) {
   if (nnz == 0) return cudaSuccess;
   k_basis_csc<<<nblk(nnz, 256), 256, 0, st>>>(nnz, Sint, src, hatv, vals);
+  count_launches(1);
   return cudaGetLastError();
 }
 

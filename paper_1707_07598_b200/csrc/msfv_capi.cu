@@ -39,6 +39,7 @@ extern "C" {
 
 int msfv_abi_version(void) { return MSFV_ABI_VERSION; }
 const char* msfv_last_error(void) { return g_err.c_str(); }
+int64_t msfv_launch_count(void) { return launch_count(); }
 
 int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out) {
   if (!cells || !h || !blocks || !out) return fail(MSFV_SHAPE, "null argument");

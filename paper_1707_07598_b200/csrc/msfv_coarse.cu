@@ -242,11 +242,13 @@ cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shif
   if (e != cudaSuccess) return e;
   long long tot = (long long)g.NT * TB * 14;
   k_coarse_assemble<<<nblk(tot, 256), 256, 0, st>>>(g, Kloc, shift, Ak);
+  count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st) {
   k_coarse_diag<<<nblk(g.kc, 256), 256, 0, st>>>(g, Ak, diag);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -255,9 +257,13 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   double* Dinv = Ak + (size_t)g.NT * (g.PT + 1) * TB * TB;
   for (int J = 0; J < g.NT; ++J) {
     k_coarse_panel<<<1, 256, 0, st>>>(g, J, Ak, Dinv, flags);
+    count_launches(1);
     int pt = g.PT < g.NT - 1 - J ? g.PT : g.NT - 1 - J;
     int npairs = pt * (pt + 1) / 2;
-    if (npairs > 0) k_coarse_update<<<npairs, 256, 0, st>>>(g, J, Ak);
+    if (npairs > 0) {
+      k_coarse_update<<<npairs, 256, 0, st>>>(g, J, Ak);
+      count_launches(1);
+    }
   }
   return cudaGetLastError();
 }
@@ -267,6 +273,7 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, int n
   const double* Dinv = Lk + (size_t)g.NT * (g.PT + 1) * TB * TB;
   constexpr int RC = 4;
   k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, 0, st>>>(g, Lk, Dinv, X, nrhs);
+  count_launches(1);
   return cudaGetLastError();
 }
 

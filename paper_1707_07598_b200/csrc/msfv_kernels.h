@@ -17,6 +17,9 @@ constexpr int FLAG_NONPOSITIVE = 2;
 constexpr int FLAG_LOCAL_NOT_SPD = 4;
 constexpr int FLAG_COARSE_NOT_SPD = 8;
 
+void count_launches(long long n);
+long long launch_count();
+
 size_t basis_smem_bytes(const Geo& g);
 size_t solve_smem_bytes(const Geo& g);
 

@@ -91,6 +91,7 @@ cudaError_t launch_points_receive(const Geo& g, const PointsDev& P, const double
   long long tot = (long long)P.ncol * nrhs;
   if (tot == 0) return cudaSuccess;
   k_points_receive<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Y, Xf, nrhs, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const double* Sint, const double* Z,
@@ -98,6 +99,7 @@ cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const doubl
   long long tot = (long long)g.kc * nrhs;
   if (tot == 0) return cudaSuccess;
   k_points_restrict<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Z, nrhs, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* field,
@@ -105,6 +107,7 @@ cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double
   long long tot = P.nu * nrhs;
   if (tot == 0) return cudaSuccess;
   k_points_scatter<<<nblk(tot, 128), 128, 0, st>>>(g, P, Z, nrhs, field);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,46 @@ def stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class PhaseTimer:
+    """Optional CUDA-event bracketing of named phases on the current stream
+    (used by bench.py for the per-kernel-class breakdown; off by default)."""
+
+    enabled = False
+    events = []
+
+    @classmethod
+    def start(cls):
+        cls.enabled = True
+        cls.events = []
+
+    @classmethod
+    def stop(cls):
+        """Synchronize and return {phase: total ms}."""
+        cls.enabled = False
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b in cls.events:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        cls.events = []
+        return out
+
+
+class phase:
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if PhaseTimer.enabled:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.a.record()
+
+    def __exit__(self, *exc):
+        if PhaseTimer.enabled:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            PhaseTimer.events.append((self.name, self.a, b))
+
+
 def require_cuda():
     if not torch.cuda.is_available():
         raise RuntimeError("the MSFV B200 path needs a CUDA device; there is no CPU fallback")
@@ -102,6 +142,10 @@ class Engine:
 
     # ------------------------------------------------------------- kernels
     def operator(self, m):
+        with phase("operator"):
+            return self._operator(m)
+
+    def _operator(self, m):
         sigma = self.empty(self.Nm)
         w = self.empty(self.E)
         fl = self.flags()
@@ -116,6 +160,10 @@ class Engine:
         return c
 
     def basis(self, w):
+        with phase("basis"):
+            return self._basis(w)
+
+    def _basis(self, w):
         Lc = self.empty(self.nbl * self.nI * self.P1s)
         Lr = self.empty(self.nbl * self.nI * self.P1s)
         Sint = self.empty(self.nbl * 8 * self.nI)
@@ -136,12 +184,14 @@ class Engine:
         return d
 
     def coarse_factor(self, Ak, fl):
-        _lib.check(self.L.msfv_coarse_factor(self.plan, ptr(Ak), ptr(fl), stream()), "coarse_factor")
+        with phase("coarse_factor"):
+            _lib.check(self.L.msfv_coarse_factor(self.plan, ptr(Ak), ptr(fl), stream()), "coarse_factor")
 
     def coarse_solve(self, Lk, X):
         """In place: X (k, nrhs) contiguous device tensor."""
         assert X.is_contiguous() and X.shape[0] == self.k
-        _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), X.shape[1], stream()), "coarse_solve")
+        with phase("coarse_solve"):
+            _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), X.shape[1], stream()), "coarse_solve")
         return X
 
     def receive(self, pts, Sint, Y=None, Xfield=None, nrhs=None):
@@ -180,7 +230,8 @@ class Engine:
     def interior_solve(self, Lc, Lr, rhs, out=None):
         nrhs = rhs.shape[1]
         o = out if out is not None else rhs
-        _lib.check(self.L.msfv_interior_solve(self.plan, ptr(Lc), ptr(Lr), ptr(rhs), ptr(o), nrhs, stream()),
+        with phase("interior_solve"):
+            _lib.check(self.L.msfv_interior_solve(self.plan, ptr(Lc), ptr(Lr), ptr(rhs), ptr(o), nrhs, stream()),
                    "interior_solve")
         return o
 
