@@ -69,7 +69,10 @@ enum msfv_info {
   MSFV_INFO_PT = 11,
   MSFV_INFO_TB = 12,
   MSFV_INFO_PC = 13,
-  MSFV_INFO_COUNT = 14
+  MSFV_INFO_FACTOR_DOUBLES = 14,  /* size of the per-model local factor buffer  */
+  MSFV_INFO_SCRATCH_DOUBLES = 15, /* scratch needed by msfv_basis_build         */
+  MSFV_INFO_TC = 16,              /* 1: FP64 tensor-core (DMMA) tile-band path  */
+  MSFV_INFO_COUNT = 17
 };
 
 typedef struct msfv_plan msfv_plan;      /* geometry; model-independent        */
@@ -98,11 +101,12 @@ MSFV_API int msfv_edge_average(const msfv_plan* plan, const double* sigma, const
                       void* stream);
 
 /* Lagrange basis at w (assemble_basis, basis.py:511-616 with _BlockFactor
- * basis.py:258-298): per-block band Cholesky factors Lc/Lr
- * [nblocks][nI][P1S], interior basis values Sint [nblocks][8][nI] and the
- * per-block 8x8 Galerkin blocks Kloc [nblocks][64]. flags |= LOCAL_NOT_SPD. */
-MSFV_API int msfv_basis_build(const msfv_plan* plan, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
-                     int32_t* flags, void* stream);
+ * basis.py:258-298): per-block banded Cholesky factors (factor buffer of
+ * MSFV_INFO_FACTOR_DOUBLES; opaque layout), interior basis values Sint
+ * [nblocks][8][nI] and the per-block 8x8 Galerkin blocks Kloc [nblocks][64].
+ * scratch: MSFV_INFO_SCRATCH_DOUBLES doubles.  flags |= LOCAL_NOT_SPD. */
+MSFV_API int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                     double* scratch, int32_t* flags, void* stream);
 /* Values of S in the reference CSC pattern (basis.py:574-594):
  * vals[t] = src[t] >= 0 ? Sint[src[t]] : hatv[t]  (src, hatv device arrays). */
 MSFV_API int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,
@@ -135,7 +139,7 @@ MSFV_API int msfv_prolong(const msfv_plan* plan, const double* Sint, const doubl
 MSFV_API int msfv_residual(const msfv_plan* plan, const double* src, double alpha, const double* wt, const double* X,
                   double beta, int32_t nrhs, double* out, void* stream);
 /* out = blockdiag(A_II^{-1}) rhs on interiors (MultiscaleBasis.interior_solve, basis.py:339-353). */
-MSFV_API int msfv_interior_solve(const msfv_plan* plan, const double* Lc, const double* Lr, const double* rhs, double* out,
+MSFV_API int msfv_interior_solve(const msfv_plan* plan, const double* factor, const double* rhs, double* out,
                         int32_t nrhs, void* stream);
 /* out[k][nrhs] = scale * S^T (A_w1 X1 + A_w2 X2); part: nblocks*8*nrhs scratch (forward.py:266). */
 MSFV_API int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,

@@ -28,8 +28,9 @@ FLAG_LOCAL_NOT_SPD = 4
 FLAG_COARSE_NOT_SPD = 8
 
 INFO_NN, INFO_N, INFO_NCELLS, INFO_NEDGES, INFO_NBLOCKS, INFO_NI, INFO_P1S, INFO_K, \
-    INFO_AK_DOUBLES, INFO_BASIS_SMEM, INFO_NT, INFO_PT, INFO_TB, INFO_PC = range(14)
-INFO_COUNT = 14
+    INFO_AK_DOUBLES, INFO_BASIS_SMEM, INFO_NT, INFO_PT, INFO_TB, INFO_PC, \
+    INFO_FACTOR_DOUBLES, INFO_SCRATCH_DOUBLES, INFO_TC = range(17)
+INFO_COUNT = 17
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
@@ -59,7 +60,7 @@ SIGNATURES = {
     "msfv_survey_scatter": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_prolong": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_residual": (ctypes.c_int, [_P, _P, _D, _P, _P, _D, _I32, _P, _P]),
-    "msfv_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P]),
+    "msfv_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_restrict_op": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),
     "msfv_cell_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P, _P]),
 }

@@ -140,13 +140,13 @@ class _CscTemplate:
 class MultiscaleBasis:
     """Assembled basis on the device (basis.py:301-376 surface)."""
 
-    def __init__(self, partition, engine, op, Lc, Lr, Sint, Kloc, flags):
+    def __init__(self, partition, engine, op, factor, Sint, Kloc, flags):
         self.partition = partition
         self.engine = engine
         self.op = op
         self._model = None
         self._m_dev = op._dev[1]
-        self.Lc, self.Lr, self.Sint, self.Kloc, self.flags = Lc, Lr, Sint, Kloc, flags
+        self.factor, self.Sint, self.Kloc, self.flags = factor, Sint, Kloc, flags
         self.families = np.full(partition.n_coarse_nodes, "lagrange")
         self.labels = [("coarse_node", int(cn)) for cn in partition.coarse_nodes]
         self.cache = None
@@ -216,7 +216,7 @@ class MultiscaleBasis:
         F = eng.zeros(eng.Nn, W.shape[1])
         F[1:] = eng.to_device(W)
         out = eng.zeros(eng.Nn, W.shape[1])
-        eng.interior_solve(self.Lc, self.Lr, F, out)
+        eng.interior_solve(self.factor, F, out)
         res = out[1:].cpu().numpy()
         return res[:, 0] if single else res
 
@@ -248,8 +248,8 @@ def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None):
             raise NotImplementedError("the GPU path builds the Lagrange family only")
     eng = engine_for(partition)
     _, m_dev, sigma, w = op.device_state(eng)
-    Lc, Lr, Sint, Kloc, fl = eng.basis(w)
-    return MultiscaleBasis(partition, eng, op, Lc, Lr, Sint, Kloc, fl)
+    factor, Sint, Kloc, fl = eng.basis(w)
+    return MultiscaleBasis(partition, eng, op, factor, Sint, Kloc, fl)
 
 
 class BasisBuilder:

@@ -77,7 +77,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.h1 = h[0]; g.h2 = h[1]; g.h3 = h[2];
   g.ih1 = 1.0 / h[0]; g.ih2 = 1.0 / h[1]; g.ih3 = 1.0 / h[2];
   g.qv = 0.25 * (h[0] * h[1] * h[2]);
-  if (basis_smem_bytes(g) > 227 * 1024)
+  if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   msfv_plan* pl = new msfv_plan;
@@ -106,6 +106,10 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_PT] = g.PT;
   v[MSFV_INFO_TB] = g.TB;
   v[MSFV_INFO_PC] = g.pc;
+  const bool tc = tc_supported(g);
+  v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)2 * g.nbl * g.nI * g.P1s;
+  v[MSFV_INFO_SCRATCH_DOUBLES] = tc ? (int64_t)tc_scratch_doubles(g) : 0;
+  v[MSFV_INFO_TC] = tc ? 1 : 0;
   for (int i = 0; i < n && i < MSFV_INFO_COUNT; ++i) info[i] = v[i];
   return MSFV_OK;
 }
@@ -234,10 +238,14 @@ int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* 
   return cuda_check(launch_edge_weights(plan->g, tmp, c, st), "edge_average");
 }
 
-int msfv_basis_build(const msfv_plan* plan, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
-                     int32_t* flags, void* stream) {
+int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                     double* scratch, int32_t* flags, void* stream) {
   CHECK_PLAN(plan);
-  return cuda_check(launch_basis(plan->g, w, Lc, Lr, Sint, Kloc, flags, (cudaStream_t)stream), "basis_build");
+  const Geo& g = plan->g;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc_supported(g)) return cuda_check(launch_basis_tc(g, w, factor, Sint, scratch, Kloc, flags, st), "basis_build");
+  double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
+  return cuda_check(launch_basis(g, w, factor, Lr, Sint, Kloc, flags, st), "basis_build");
 }
 
 int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,
@@ -302,10 +310,14 @@ int msfv_residual(const msfv_plan* plan, const double* src, double alpha, const 
   return cuda_check(launch_residual(plan->g, src, alpha, wt, X, beta, nrhs, out, (cudaStream_t)stream), "residual");
 }
 
-int msfv_interior_solve(const msfv_plan* plan, const double* Lc, const double* Lr, const double* rhs, double* out,
-                        int32_t nrhs, void* stream) {
+int msfv_interior_solve(const msfv_plan* plan, const double* factor, const double* rhs, double* out, int32_t nrhs,
+                        void* stream) {
   CHECK_PLAN(plan);
-  return cuda_check(launch_block_solve(plan->g, Lc, Lr, rhs, out, nrhs, (cudaStream_t)stream), "interior_solve");
+  const Geo& g = plan->g;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc_supported(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
+  const double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
+  return cuda_check(launch_block_solve(g, factor, Lr, rhs, out, nrhs, st), "interior_solve");
 }
 
 int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,

@@ -165,34 +165,40 @@ __global__ void __launch_bounds__(256) k_coarse_update(Geo g, int J, double* __r
 }
 
 // Forward then backward substitution with the banded tiled factor for RC
-// right-hand sides per CTA.  X is [kc][nrhs] row-major.
+// right-hand sides per CTA.  X is [kc][nrhs] row-major.  Forward is
+// right-looking (X_{J+t} -= L_{J+t,J} y_J straight in global memory, read back
+// by the same CTA); backward keeps the last PT+1 solved tiles of x in a
+// shared-memory ring so the transposed tile products read only L from L2.
 template <int RC>
 __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __restrict__ Lk, const double* __restrict__ Dinv,
                                                      double* __restrict__ X, int nrhs) {
-  __shared__ double Xs[TB][RC];
-  __shared__ double Ys[TB][RC];
+  extern __shared__ double tsm[];
+  double* Xs = tsm;                        // [TB][RC]
+  double* acc = Xs + TB * RC;              // [TB][RC]
+  double* win = acc + TB * RC;             // [PT+1][TB][RC]
   const int tid = threadIdx.x, nt = blockDim.x;
   const int s0 = blockIdx.x * RC;
   const int ns = min(RC, nrhs - s0);
-  // forward: y_J = Dinv_J (x_J) ; x_{J+t} -= L_{J+t,J} y_J
+  const int W = g.PT + 1;
+  // ---------------- forward
   for (int J = 0; J < g.NT; ++J) {
     for (int t = tid; t < TB * RC; t += nt) {
       int r = t / RC, s = t % RC, row = J * TB + r;
-      Xs[r][s] = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+      Xs[t] = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
     }
     __syncthreads();
     const double* Di = Dinv + (size_t)J * TB * TB;
     for (int t = tid; t < TB * RC; t += nt) {
       int r = t / RC, s = t % RC;
+      const double* drow = Di + r * TB;
       double v = 0.0;
-      for (int q = 0; q <= r; ++q) v += Di[r * TB + q] * Xs[q][s];
-      Ys[r][s] = v;
+#pragma unroll 8
+      for (int q = 0; q < TB; ++q) v += drow[q] * Xs[q * RC + s];   // Dinv upper part is zero
+      acc[t] = v;
+      int row = J * TB + r;
+      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
     }
     __syncthreads();
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = J * TB + r;
-      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = Ys[r][s];
-    }
     const int pt = min(g.PT, g.NT - 1 - J);
     for (int t = tid; t < pt * TB * RC; t += nt) {
       int tt = 1 + t / (TB * RC), rem = t % (TB * RC), r = rem / RC, s = rem % RC;
@@ -201,12 +207,12 @@ __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __rest
       const double* L = tile(Lk, g, J, tt) + r * TB;
       double v = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < TB; ++q) v += L[q] * Ys[q][s];
+      for (int q = 0; q < TB; ++q) v += L[q] * acc[q * RC + s];
       X[(size_t)row * nrhs + s0 + s] -= v;
     }
     __syncthreads();
   }
-  // backward: acc_J = y_J - sum_t L_{J+t,J}^T x_{J+t} ; x_J = Dinv_J^T acc_J
+  // ---------------- backward
   for (int J = g.NT - 1; J >= 0; --J) {
     const int pt = min(g.PT, g.NT - 1 - J);
     for (int t = tid; t < TB * RC; t += nt) {
@@ -214,20 +220,21 @@ __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __rest
       double v = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
       for (int tt = 1; tt <= pt; ++tt) {
         const double* L = tile(Lk, g, J, tt);
-        for (int r = 0; r < TB; ++r) {
-          int row2 = (J + tt) * TB + r;
-          if (row2 >= g.kc) break;
-          if (s < ns) v -= L[r * TB + q] * X[(size_t)row2 * nrhs + s0 + s];
-        }
+        const double* xw = win + (size_t)((J + tt) % W) * TB * RC;
+#pragma unroll 8
+        for (int r = 0; r < TB; ++r) v -= L[r * TB + q] * xw[r * RC + s];
       }
-      Xs[q][s] = v;
+      acc[t] = v;
     }
     __syncthreads();
     const double* Di = Dinv + (size_t)J * TB * TB;
+    double* xo = win + (size_t)(J % W) * TB * RC;
     for (int t = tid; t < TB * RC; t += nt) {
       int r = t / RC, s = t % RC, row = J * TB + r;
       double v = 0.0;
-      for (int q = r; q < TB; ++q) v += Di[q * TB + r] * Xs[q][s];
+      for (int q = r; q < TB; ++q) v += Di[q * TB + r] * acc[q * RC + s];
+      if (row >= g.kc || s >= ns) v = 0.0;
+      xo[t] = v;
       if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
     }
     __syncthreads();
@@ -272,7 +279,10 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, int n
   if (nrhs == 0) return cudaSuccess;
   const double* Dinv = Lk + (size_t)g.NT * (g.PT + 1) * TB * TB;
   constexpr int RC = 4;
-  k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, 0, st>>>(g, Lk, Dinv, X, nrhs);
+  size_t smem = ((size_t)2 + g.PT + 1) * TB * RC * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, smem, st>>>(g, Lk, Dinv, X, nrhs);
   count_launches(1);
   return cudaGetLastError();
 }

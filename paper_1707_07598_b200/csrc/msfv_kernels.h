@@ -11,6 +11,8 @@ constexpr int SOLVE_NSC = 8;
 constexpr int SOLVE_RING = 8;
 constexpr int RESTRICT_THREADS = 128;
 constexpr int COARSE_TB = 32;
+constexpr int TC_WARPS = 2;      // warps (= coarse blocks) per CTA in the DMMA kernels
+constexpr int TC_MAX_PT = 7;     // largest tile band handled by the DMMA kernels (p <= 56)
 
 constexpr int FLAG_NONFINITE = 1;
 constexpr int FLAG_NONPOSITIVE = 2;
@@ -40,6 +42,16 @@ cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double
                                  const double* Y, const double* R, int nrhs, double* gout, cudaStream_t st);
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
                              double* vals, cudaStream_t st);
+
+// DMMA tile-band path (msfv_tc.cu)
+int tc_band(const Geo& g);
+bool tc_supported(const Geo& g);
+size_t tc_factor_doubles(const Geo& g);
+size_t tc_scratch_doubles(const Geo& g);
+cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc, double* Kloc,
+                            int* flags, cudaStream_t st);
+cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
+                                  cudaStream_t st);
 
 // coarse (msfv_coarse.cu)
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);

@@ -1,0 +1,502 @@
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) tile-band kernels for the
+// per-block interior problems -- the hot path of the basis build
+// (basis.py:511-563) and of every blockdiag(A_II^-1) application
+// (MultiscaleBasis.interior_solve, basis.py:339-353).
+//
+// One warp owns one coarse block.  A_II (nI x nI, half bandwidth p, interior
+// nodes in lexicographic order) is processed in 8x8 tiles: tile column J has
+// the diagonal tile and PT = ceil(p/8) sub-diagonal tiles.  The right-looking
+// blocked Cholesky keeps its whole active window -- the (PT+1)(PT+2)/2 tiles
+// that still receive updates -- in registers (DMMA accumulator layout), so the
+// trailing update is 2 DMMAs per tile with no shared-memory traffic.  The 8
+// Lagrange right-hand sides ride along as one extra tile column (fused
+// forward substitution); the backward substitution re-reads the factor tiles
+// from L2/HBM.  The per-block 8x8 Galerkin block is a DMMA reduction over the
+// block's owned edges.
+//
+// Factor storage ("LT"), per block, per tile column J, PT+1 tiles of 64
+// doubles stored in A-fragment lane order:  slot 0 = L_JJ^{-1},
+// slot t = L_{J+t,J}.   Fragment layouts (m8n8k4 f64):
+//   A[m][k] at lane 4m+k ; B[k][n] at lane 4n+k ; C[m][n] at lane 4m+n/2, slot n%2
+// An 8x8 tile in "A-frag" form is two A fragments (k = 0..3 and 4..7).
+#include "msfv_common.cuh"
+#include "msfv_kernels.h"
+
+namespace msfv {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct F2 {
+  double x, y;
+};
+
+__device__ __forceinline__ void mma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+// C (accumulator layout) += A (A-frag) * B (B-frag), k = 8
+__device__ __forceinline__ void mma(F2& c, const F2& a, const F2& b) {
+  mma884(c.x, c.y, a.x, b.x);
+  mma884(c.x, c.y, a.y, b.y);
+}
+__device__ __forceinline__ F2 neg(const F2& f) { return {-f.x, -f.y}; }
+
+// accumulator tile T -> A-frag of T
+__device__ __forceinline__ F2 c_to_a(const F2& c, int lane) {
+  const int m = lane >> 2, k = lane & 3;
+  const int s0 = (m << 2) | (k >> 1), s1 = (m << 2) | (2 + (k >> 1));
+  double x0 = __shfl_sync(FULL, c.x, s0), y0 = __shfl_sync(FULL, c.y, s0);
+  double x1 = __shfl_sync(FULL, c.x, s1), y1 = __shfl_sync(FULL, c.y, s1);
+  const bool odd = k & 1;
+  return {odd ? y0 : x0, odd ? y1 : x1};
+}
+// accumulator tile T -> B-frag of T (B[k][n] = T[k][n])
+__device__ __forceinline__ F2 c_to_b(const F2& c, int lane) {
+  const int k = lane & 3, n = lane >> 2;
+  const int s0 = (k << 2) | (n >> 1), s1 = ((k + 4) << 2) | (n >> 1);
+  double x0 = __shfl_sync(FULL, c.x, s0), y0 = __shfl_sync(FULL, c.y, s0);
+  double x1 = __shfl_sync(FULL, c.x, s1), y1 = __shfl_sync(FULL, c.y, s1);
+  const bool odd = n & 1;
+  return {odd ? y0 : x0, odd ? y1 : x1};
+}
+// A-frag of T -> A-frag of T^T (equivalently the B-frag of T)
+__device__ __forceinline__ F2 a_to_t(const F2& f, int lane) {
+  const int k = lane & 3, n = lane >> 2;
+  const int s0 = (k << 2) | (n & 3), s1 = ((k + 4) << 2) | (n & 3);
+  double p0 = __shfl_sync(FULL, f.x, s0), q0 = __shfl_sync(FULL, f.y, s0);
+  double p1 = __shfl_sync(FULL, f.x, s1), q1 = __shfl_sync(FULL, f.y, s1);
+  const bool hi = n >= 4;
+  return {hi ? q0 : p0, hi ? q1 : p1};
+}
+
+__device__ __forceinline__ F2 ld2(const double* p) {
+  double2 v = *reinterpret_cast<const double2*>(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ F2 ld2cg(const double* p) {
+  double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void st2(double* p, const F2& f) {
+  *reinterpret_cast<double2*>(p) = make_double2(f.x, f.y);
+}
+
+// Stencil row of interior node i of a block: the six edge conductances / h^2.
+struct Row {
+  bool valid;
+  int x, y, z;
+  double kxm, kxp, kym, kyp, kzm, kzp;
+};
+
+__device__ __forceinline__ Row load_row(const Geo& g, const double* __restrict__ w, int X0, int Y0, int Z0, int i) {
+  Row r;
+  r.valid = i < g.nI;
+  if (!r.valid) {
+    r.x = r.y = r.z = 0;
+    r.kxm = r.kxp = r.kym = r.kyp = r.kzm = r.kzp = 0.0;
+    return r;
+  }
+  r.x = 1 + i % g.ni1;
+  r.y = 1 + (i / g.ni1) % g.ni2;
+  r.z = 1 + i / (g.ni1 * g.ni2);
+  const long long I = X0 + r.x, J = Y0 + r.y, K = Z0 + r.z;
+  r.kxm = __ldg(w + ex_id(g, I - 1, J, K)) * g.ih1 * g.ih1;
+  r.kxp = __ldg(w + ex_id(g, I, J, K)) * g.ih1 * g.ih1;
+  r.kym = __ldg(w + ey_id(g, I, J - 1, K)) * g.ih2 * g.ih2;
+  r.kyp = __ldg(w + ey_id(g, I, J, K)) * g.ih2 * g.ih2;
+  r.kzm = __ldg(w + ez_id(g, I, J, K - 1)) * g.ih3 * g.ih3;
+  r.kzp = __ldg(w + ez_id(g, I, J, K)) * g.ih3 * g.ih3;
+  return r;
+}
+
+// A_II[i][l] for l <= i (padding rows are identity).
+__device__ __forceinline__ double a_entry(const Geo& g, const Row& r, int i, int l) {
+  if (!r.valid) return i == l ? 1.0 : 0.0;
+  if (l > i) return 0.0;
+  const int d = i - l;
+  if (d == 0) return ((((r.kxm + r.kxp) + r.kym) + r.kyp) + r.kzm) + r.kzp;
+  double v = 0.0;
+  if (d == 1 && r.x > 1) v -= r.kxm;
+  if (d == g.ni1 && r.y > 1) v -= r.kym;
+  if (d == g.p && r.z > 1) v -= r.kzm;
+  return v;
+}
+
+// Lagrange right-hand side -A_IB x_B (basis.py:548) of node row r, corner cc.
+__device__ __forceinline__ double rhs_entry(const Geo& g, const Row& r, int cc) {
+  if (!r.valid) return 0.0;
+  double v = 0.0;
+  if (r.x == 1) v += r.kxm * hat_corner(cc, 0, r.y, r.z, g.b1, g.b2, g.b3);
+  if (r.x == g.ni1) v += r.kxp * hat_corner(cc, g.b1, r.y, r.z, g.b1, g.b2, g.b3);
+  if (r.y == 1) v += r.kym * hat_corner(cc, r.x, 0, r.z, g.b1, g.b2, g.b3);
+  if (r.y == g.ni2) v += r.kyp * hat_corner(cc, r.x, g.b2, r.z, g.b1, g.b2, g.b3);
+  if (r.z == 1) v += r.kzm * hat_corner(cc, r.x, r.y, 0, g.b1, g.b2, g.b3);
+  if (r.z == g.ni3) v += r.kzp * hat_corner(cc, r.x, r.y, g.b3, g.b1, g.b2, g.b3);
+  return v;
+}
+
+// Cholesky of one 8x8 SPD tile (accumulator layout) in per-warp shared
+// memory; returns L^{-1} as an A-frag.  Lane (rq) owns one strictly-lower
+// trailing entry (r, q) of the rank-1 updates.
+__device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, int lane, int rl, int ql,
+                                         int* flags) {
+  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  Ds[m * 8 + n0] = t.x;
+  Ds[m * 8 + n0 + 1] = t.y;
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double d = Ds[c * 9];
+    if (!(d > 0.0)) {
+      if (lane == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
+      d = 1.0;
+    }
+    const double piv = sqrt(d), inv = 1.0 / piv;
+    __syncwarp();
+    if (lane > c && lane < 8) Ds[lane * 8 + c] *= inv;
+    if (lane == c) Ds[c * 9] = piv;
+    __syncwarp();
+    if (ql > c) Ds[rl * 8 + ql] -= Ds[rl * 8 + c] * Ds[ql * 8 + c];
+    __syncwarp();
+  }
+  if (lane < 8) {
+    const int c = lane;
+    double x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < r; ++q) v -= Ds[r * 8 + q] * x[q];
+      x[r] = (r < c) ? 0.0 : v / Ds[r * 9];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) Is[r * 8 + c] = x[r];
+  }
+  __syncwarp();
+  const int k = lane & 3;
+  F2 li = {Is[m * 8 + k], Is[m * 8 + 4 + k]};
+  __syncwarp();
+  return li;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- basis
+
+template <int PT>
+__global__ void __launch_bounds__(TC_WARPS * 32)
+k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
+           double* __restrict__ Ysc, double* __restrict__ Kloc, int* __restrict__ flags) {
+  __shared__ double Dsh[TC_WARPS][64];
+  __shared__ double Ish[TC_WARPS][64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int jb = blockIdx.x * TC_WARPS + wid;
+  if (jb >= g.nbl) return;
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
+  const int NTI = (g.nI + 7) >> 3;
+  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  double* Ds = Dsh[wid];
+  double* Is = Ish[wid];
+  // this lane's fixed strictly-lower (r, q) entry of the 8x8 rank-1 updates
+  int rl = 0, ql = -1;   // lanes 28..31 own no entry
+  {
+    int idx = 0;
+    for (int r = 1; r < 8; ++r)
+      for (int q = 1; q <= r; ++q, ++idx)
+        if (idx == lane) { rl = r; ql = q; }
+  }
+
+  if (NTI > 0) {
+    F2 W[PT + 1][PT + 1];
+    F2 R[PT + 1];
+    // ---- initial window: tile rows 0..PT
+#pragma unroll
+    for (int a = 0; a <= PT; ++a) {
+      const int i = 8 * a + m;
+      Row rw = load_row(g, w, X0, Y0, Z0, i);
+#pragma unroll
+      for (int b = 0; b <= PT; ++b) {
+        if (b <= a) {
+          const int l = 8 * b + n0;
+          W[a][b] = {a_entry(g, rw, i, l), a_entry(g, rw, i, l + 1)};
+        } else {
+          W[a][b] = {0.0, 0.0};
+        }
+      }
+      R[a] = {rhs_entry(g, rw, n0), rhs_entry(g, rw, n0 + 1)};
+    }
+    for (int J = 0; J < NTI; ++J) {
+      // prefetch the stencil row entering the window at the end of this step
+      const int inext = 8 * (J + 1 + PT) + m;
+      Row rn = load_row(g, w, X0, Y0, Z0, inext);
+
+      const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, rl, ql, flags);
+      F2 X[PT + 1];
+#pragma unroll
+      for (int t = 1; t <= PT; ++t) {
+        F2 c = {0.0, 0.0};
+        mma(c, c_to_a(W[t][0], lane), Li);     // X_t = A_t L^{-T}
+        X[t] = c_to_a(c, lane);
+      }
+      // fused forward substitution for the 8 Lagrange columns
+      F2 Yc = {0.0, 0.0};
+      mma(Yc, Li, c_to_b(R[0], lane));         // y_J = L_JJ^{-1} r_J
+      {
+        const F2 Yb = c_to_b(Yc, lane);
+#pragma unroll
+        for (int t = 1; t <= PT; ++t) mma(R[t], neg(X[t]), Yb);
+      }
+      // trailing update of the register window
+#pragma unroll
+      for (int a = 1; a <= PT; ++a) {
+        const F2 nXa = neg(X[a]);
+#pragma unroll
+        for (int b = 1; b <= a; ++b) mma(W[a][b], nXa, X[b]);
+      }
+      // factor tiles and y to global memory
+      {
+        double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
+        st2(Lt + lane * 2, Li);
+#pragma unroll
+        for (int t = 1; t <= PT; ++t) st2(Lt + t * 64 + lane * 2, X[t]);
+        st2(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2, Yc);
+      }
+      // slide the window by one tile
+#pragma unroll
+      for (int a = 1; a <= PT; ++a) {
+#pragma unroll
+        for (int b = 1; b <= a; ++b) W[a - 1][b - 1] = W[a][b];
+        R[a - 1] = R[a];
+      }
+      {
+        const int In = J + 1 + PT;
+#pragma unroll
+        for (int b = 0; b <= PT; ++b) {
+          const int l = 8 * (In - PT + b) + n0;
+          W[PT][b] = {a_entry(g, rn, inext, l), a_entry(g, rn, inext, l + 1)};
+        }
+        R[PT] = {rhs_entry(g, rn, n0), rhs_entry(g, rn, n0 + 1)};
+      }
+    }
+    __syncwarp();
+    // ---- backward substitution L^T x = y, window of solved tiles as B-frags
+    F2 Xw[PT > 0 ? PT : 1];
+#pragma unroll
+    for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
+    for (int J = NTI - 1; J >= 0; --J) {
+      const double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
+      F2 acc = ld2cg(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2);
+#pragma unroll
+      for (int t = 1; t <= PT; ++t) {
+        if (J + t < NTI) mma(acc, neg(a_to_t(ld2cg(Lt + t * 64 + lane * 2), lane)), Xw[t - 1]);
+      }
+      F2 xj = {0.0, 0.0};
+      mma(xj, a_to_t(ld2cg(Lt + lane * 2), lane), c_to_b(acc, lane));
+      const int a0 = 8 * J + m;
+      if (a0 < g.nI) {
+        Sint[((size_t)jb * 8 + n0) * g.nI + a0] = xj.x;
+        Sint[((size_t)jb * 8 + n0 + 1) * g.nI + a0] = xj.y;
+      }
+#pragma unroll
+      for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
+      if (PT > 0) Xw[0] = c_to_b(xj, lane);
+    }
+    __syncwarp();
+    __threadfence_block();
+  }
+
+  // ---- local Galerkin block: K = sum_e (w_e/h^2) dS_e dS_e^T as a DMMA reduction
+  const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
+  const int ox = g.b1 * (g.b2 + ly) * (g.b3 + lz);
+  const int oy = (g.b1 + lx) * g.b2 * (g.b3 + lz);
+  const int oz = (g.b1 + lx) * (g.b2 + ly) * g.b3;
+  const int tot = ox + oy + oz;
+  const bool has0 = (jb == 0);
+  const int cc = lane >> 2;
+  const double* Sb = Sint + (size_t)jb * 8 * g.nI + (size_t)cc * g.nI;
+  F2 K = {0.0, 0.0};
+  for (int base = 0; base < tot; base += 4) {
+    const int f = base + (lane & 3);
+    double a = 0.0, b = 0.0;
+    if (f < tot) {
+      int ax, x, y, z;
+      long long e;
+      double ihs;
+      if (f < ox) {
+        ax = 0; x = f % g.b1; int r = f / g.b1; y = r % (g.b2 + ly); z = r / (g.b2 + ly);
+        e = ex_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih1 * g.ih1;
+      } else if (f < ox + oy) {
+        ax = 1; int q = f - ox; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % g.b2; z = r / g.b2;
+        e = ey_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih2 * g.ih2;
+      } else {
+        ax = 2; int q = f - ox - oy; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % (g.b2 + ly); z = r / (g.b2 + ly);
+        e = ez_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih3 * g.ih3;
+      }
+      const int x1 = x + (ax == 0), y1 = y + (ax == 1), z1 = z + (ax == 2);
+      const int a0 = interior_index(g, x, y, z), a1 = interior_index(g, x1, y1, z1);
+      const double s0 = a0 >= 0 ? __ldcg(Sb + a0)
+                                : ((has0 && x == 0 && y == 0 && z == 0) ? 0.0
+                                                                        : hat_corner(cc, x, y, z, g.b1, g.b2, g.b3));
+      const double s1 = a1 >= 0 ? __ldcg(Sb + a1) : hat_corner(cc, x1, y1, z1, g.b1, g.b2, g.b3);
+      b = s1 - s0;
+      a = (__ldg(w + e) * ihs) * b;
+    }
+    mma884(K.x, K.y, a, b);
+  }
+  Kloc[(size_t)jb * 64 + m * 8 + n0] = K.x;
+  Kloc[(size_t)jb * 64 + m * 8 + n0 + 1] = K.y;
+}
+
+// ------------------------------------------------------------ block solve
+
+// out = blockdiag(A_II^{-1}) rhs on block interiors (full node fields); out
+// may alias rhs.  y is parked in out between the sweeps.
+template <int PT>
+__global__ void __launch_bounds__(TC_WARPS * 32)
+k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int jb = blockIdx.x * TC_WARPS + wid;
+  if (jb >= g.nbl) return;
+  const int NTI = (g.nI + 7) >> 3;
+  if (NTI == 0) return;
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
+  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  auto node_of = [&](int a) -> long long {
+    const int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
+    return node_id(g, X0 + x, Y0 + y, Z0 + z);
+  };
+  const double* LTb = LT + (size_t)jb * NTI * (PT + 1) * 64;
+  for (int s0 = 0; s0 < nrhs; s0 += 8) {
+    const int sA = s0 + n0, sB = s0 + n0 + 1;
+    auto load_tile = [&](const double* src, int I) -> F2 {
+      const int a = 8 * I + m;
+      F2 v = {0.0, 0.0};
+      if (a < g.nI) {
+        const long long nd = node_of(a);
+        if (sA < nrhs) v.x = src[nd * nrhs + sA];
+        if (sB < nrhs) v.y = src[nd * nrhs + sB];
+      }
+      return v;
+    };
+    auto store_tile = [&](int I, const F2& v) {
+      const int a = 8 * I + m;
+      if (a < g.nI) {
+        const long long nd = node_of(a);
+        if (sA < nrhs) out[nd * nrhs + sA] = v.x;
+        if (sB < nrhs) out[nd * nrhs + sB] = v.y;
+      }
+    };
+    F2 R[PT + 1];
+#pragma unroll
+    for (int a = 0; a <= PT; ++a) R[a] = load_tile(rhs, a);
+    // forward: y_J = L_JJ^{-1} r_J ; r_{J+t} -= L_{J+t,J} y_J
+    for (int J = 0; J < NTI; ++J) {
+      const double* Lt = LTb + (size_t)J * (PT + 1) * 64;
+      const F2 Li = ld2(Lt + lane * 2);
+      F2 Yc = {0.0, 0.0};
+      mma(Yc, Li, c_to_b(R[0], lane));
+      const F2 Yb = c_to_b(Yc, lane);
+#pragma unroll
+      for (int t = 1; t <= PT; ++t)
+        if (J + t < NTI) mma(R[t], neg(ld2(Lt + t * 64 + lane * 2)), Yb);
+      const F2 nxt = load_tile(rhs, J + 1 + PT);   // read ahead before y_J lands (out may alias rhs)
+      __syncwarp();
+      store_tile(J, Yc);
+#pragma unroll
+      for (int a = 1; a <= PT; ++a) R[a - 1] = R[a];
+      R[PT] = nxt;
+    }
+    __syncwarp();
+    // backward: x_J = L_JJ^{-T} (y_J - sum_t L_{J+t,J}^T x_{J+t})
+    F2 Xw[PT > 0 ? PT : 1];
+#pragma unroll
+    for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
+    for (int J = NTI - 1; J >= 0; --J) {
+      const double* Lt = LTb + (size_t)J * (PT + 1) * 64;
+      F2 acc = load_tile(out, J);
+#pragma unroll
+      for (int t = 1; t <= PT; ++t)
+        if (J + t < NTI) mma(acc, neg(a_to_t(ld2(Lt + t * 64 + lane * 2), lane)), Xw[t - 1]);
+      F2 xj = {0.0, 0.0};
+      mma(xj, a_to_t(ld2(Lt + lane * 2), lane), c_to_b(acc, lane));
+      __syncwarp();
+      store_tile(J, xj);
+#pragma unroll
+      for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
+      if (PT > 0) Xw[0] = c_to_b(xj, lane);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+int tc_band(const Geo& g) {
+  const int nti = (g.nI + 7) / 8;
+  if (nti == 0) return 0;
+  int pt = (g.p + 7) / 8;
+  if (pt > nti - 1) pt = nti - 1;
+  return pt;
+}
+
+bool tc_supported(const Geo& g) { return tc_band(g) <= TC_MAX_PT; }
+
+size_t tc_factor_doubles(const Geo& g) {
+  const size_t nti = (g.nI + 7) / 8;
+  return (size_t)g.nbl * nti * (tc_band(g) + 1) * 64;
+}
+size_t tc_scratch_doubles(const Geo& g) { return (size_t)g.nbl * ((g.nI + 7) / 8) * 64; }
+
+template <int PT>
+static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc,
+                                     double* Kloc, int* flags, cudaStream_t st) {
+  const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
+  k_basis_tc<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
+  count_launches(1);
+  return cudaGetLastError();
+}
+template <int PT>
+static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
+                                     cudaStream_t st) {
+  const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
+  k_block_solve_tc<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, LT, rhs, out, nrhs);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc, double* Kloc,
+                            int* flags, cudaStream_t st) {
+  switch (tc_band(g)) {
+    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
+                                  cudaStream_t st) {
+  if (g.nI == 0 || nrhs == 0) return cudaSuccess;
+  switch (tc_band(g)) {
+    case 0: return launch_solve_tc_t<0>(g, LT, rhs, out, nrhs, st);
+    case 1: return launch_solve_tc_t<1>(g, LT, rhs, out, nrhs, st);
+    case 2: return launch_solve_tc_t<2>(g, LT, rhs, out, nrhs, st);
+    case 3: return launch_solve_tc_t<3>(g, LT, rhs, out, nrhs, st);
+    case 4: return launch_solve_tc_t<4>(g, LT, rhs, out, nrhs, st);
+    case 5: return launch_solve_tc_t<5>(g, LT, rhs, out, nrhs, st);
+    case 6: return launch_solve_tc_t<6>(g, LT, rhs, out, nrhs, st);
+    case 7: return launch_solve_tc_t<7>(g, LT, rhs, out, nrhs, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace msfv

@@ -116,6 +116,9 @@ class Engine:
         self.k = info[_lib.INFO_K]
         self.ak_doubles = info[_lib.INFO_AK_DOUBLES]
         self.NT, self.PT, self.TB = info[_lib.INFO_NT], info[_lib.INFO_PT], info[_lib.INFO_TB]
+        self.factor_doubles = info[_lib.INFO_FACTOR_DOUBLES]
+        self.scratch_doubles = info[_lib.INFO_SCRATCH_DOUBLES]
+        self.tensor_core = bool(info[_lib.INFO_TC])
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._csc = None
 
@@ -155,8 +158,9 @@ class Engine:
     def edge_average(self, sigma, dm):
         tmp = self.empty(self.Nm)
         c = self.empty(self.E)
-        _lib.check(self.L.msfv_edge_average(self.plan, ptr(sigma), ptr(dm), ptr(tmp), ptr(c), stream()),
-                   "edge_average")
+        with phase("edge_average"):
+            _lib.check(self.L.msfv_edge_average(self.plan, ptr(sigma), ptr(dm), ptr(tmp), ptr(c), stream()),
+                       "edge_average")
         return c
 
     def basis(self, w):
@@ -164,18 +168,19 @@ class Engine:
             return self._basis(w)
 
     def _basis(self, w):
-        Lc = self.empty(self.nbl * self.nI * self.P1s)
-        Lr = self.empty(self.nbl * self.nI * self.P1s)
-        Sint = self.empty(self.nbl * 8 * self.nI)
+        factor = self.empty(max(self.factor_doubles, 1))
+        Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
         Kloc = self.empty(self.nbl * 64)
+        scratch = self.empty(max(self.scratch_doubles, 1))
         fl = self.flags()
-        _lib.check(self.L.msfv_basis_build(self.plan, ptr(w), ptr(Lc), ptr(Lr), ptr(Sint), ptr(Kloc),
+        _lib.check(self.L.msfv_basis_build(self.plan, ptr(w), ptr(factor), ptr(Sint), ptr(Kloc), ptr(scratch),
                                            ptr(fl), stream()), "basis_build")
-        return Lc, Lr, Sint, Kloc, fl
+        return factor, Sint, Kloc, fl
 
     def galerkin(self, Kloc, shift=0.0, out=None):
         Ak = out if out is not None else self.empty(self.ak_doubles)
-        _lib.check(self.L.msfv_galerkin(self.plan, ptr(Kloc), float(shift), ptr(Ak), stream()), "galerkin")
+        with phase("galerkin"):
+            _lib.check(self.L.msfv_galerkin(self.plan, ptr(Kloc), float(shift), ptr(Ak), stream()), "galerkin")
         return Ak
 
     def coarse_trace(self, Ak):
@@ -197,56 +202,63 @@ class Engine:
     def receive(self, pts, Sint, Y=None, Xfield=None, nrhs=None):
         nrhs = nrhs if nrhs is not None else (Y.shape[1] if Y is not None else Xfield.shape[1])
         out = self.empty(pts.ncol, nrhs)
-        _lib.check(self.L.msfv_survey_receive(self.plan, pts.handle, ptr(Sint), ptr(Y), ptr(Xfield), nrhs,
-                                              ptr(out), stream()), "survey_receive")
+        with phase("survey_receive"):
+            _lib.check(self.L.msfv_survey_receive(self.plan, pts.handle, ptr(Sint), ptr(Y), ptr(Xfield), nrhs,
+                                                  ptr(out), stream()), "survey_receive")
         return out
 
     def restrict_points(self, pts, Sint, Z=None, nrhs=None):
         nrhs = nrhs if nrhs is not None else (Z.shape[1] if Z is not None else pts.ncol)
         out = self.empty(self.k, nrhs)
-        _lib.check(self.L.msfv_survey_restrict(self.plan, pts.handle, ptr(Sint), ptr(Z), nrhs, ptr(out),
-                                               stream()), "survey_restrict")
+        with phase("survey_restrict"):
+            _lib.check(self.L.msfv_survey_restrict(self.plan, pts.handle, ptr(Sint), ptr(Z), nrhs, ptr(out),
+                                                   stream()), "survey_restrict")
         return out
 
     def scatter_points(self, pts, Z=None, nrhs=None, field=None):
         nrhs = nrhs if nrhs is not None else (Z.shape[1] if Z is not None else pts.ncol)
         f = field if field is not None else self.zeros(self.Nn, nrhs)
-        _lib.check(self.L.msfv_survey_scatter(self.plan, pts.handle, ptr(Z), nrhs, ptr(f), stream()),
-                   "survey_scatter")
+        with phase("survey_scatter"):
+            _lib.check(self.L.msfv_survey_scatter(self.plan, pts.handle, ptr(Z), nrhs, ptr(f), stream()),
+                       "survey_scatter")
         return f
 
     def prolong(self, Sint, Y):
         nrhs = Y.shape[1]
         out = self.empty(self.Nn, nrhs)
-        _lib.check(self.L.msfv_prolong(self.plan, ptr(Sint), ptr(Y), nrhs, ptr(out), stream()), "prolong")
+        with phase("prolong"):
+            _lib.check(self.L.msfv_prolong(self.plan, ptr(Sint), ptr(Y), nrhs, ptr(out), stream()), "prolong")
         return out
 
     def residual(self, src, alpha, wt, X, beta, nrhs, out=None):
         o = out if out is not None else self.zeros(self.Nn, nrhs)
-        _lib.check(self.L.msfv_residual(self.plan, ptr(src), float(alpha), ptr(wt), ptr(X), float(beta), nrhs,
-                                        ptr(o), stream()), "residual")
+        with phase("residual"):
+            _lib.check(self.L.msfv_residual(self.plan, ptr(src), float(alpha), ptr(wt), ptr(X), float(beta), nrhs,
+                                            ptr(o), stream()), "residual")
         return o
 
-    def interior_solve(self, Lc, Lr, rhs, out=None):
+    def interior_solve(self, factor, rhs, out=None):
         nrhs = rhs.shape[1]
         o = out if out is not None else rhs
         with phase("interior_solve"):
-            _lib.check(self.L.msfv_interior_solve(self.plan, ptr(Lc), ptr(Lr), ptr(rhs), ptr(o), nrhs, stream()),
-                   "interior_solve")
+            _lib.check(self.L.msfv_interior_solve(self.plan, ptr(factor), ptr(rhs), ptr(o), nrhs, stream()),
+                       "interior_solve")
         return o
 
     def restrict_op(self, Sint, w1, X1, w2, X2, nrhs, scale=1.0):
         part = self.empty(self.nbl * 8 * nrhs)
         out = self.empty(self.k, nrhs)
-        _lib.check(self.L.msfv_restrict_op(self.plan, ptr(Sint), ptr(w1), ptr(X1), ptr(w2), ptr(X2), nrhs,
-                                           float(scale), ptr(part), ptr(out), stream()), "restrict_op")
+        with phase("restrict_op"):
+            _lib.check(self.L.msfv_restrict_op(self.plan, ptr(Sint), ptr(w1), ptr(X1), ptr(w2), ptr(X2), nrhs,
+                                               float(scale), ptr(part), ptr(out), stream()), "restrict_op")
         return out
 
     def cell_gradient(self, sigma, U, Z, Y, R):
         nrhs = U.shape[1]
         g = self.empty(self.Nm)
-        _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs, ptr(g),
-                                             stream()), "cell_gradient")
+        with phase("cell_gradient"):
+            _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs, ptr(g),
+                                                 stream()), "cell_gradient")
         return g
 
     def basis_csc(self, Sint, src, hatv):

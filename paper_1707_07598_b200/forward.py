@@ -185,7 +185,7 @@ class AdaptiveSensitivity:
         ns = survey.n_sources
         self.U = eng.prolong(basis.Sint, state.T_dev)                               # S T (forward.py:241)
         R = eng.residual(Qf, 1.0, self.w, self.U, -1.0, ns)                         # Q - A U (forward.py:243)
-        self.ZR = eng.interior_solve(basis.Lc, basis.Lr, R)                         # interior_solve(R) (:246)
+        self.ZR = eng.interior_solve(basis.factor, R)                         # interior_solve(R) (:246)
         self.UR = self.U + self.ZR
 
     # ---------------------------------------------------------- device API
@@ -198,7 +198,7 @@ class AdaptiveSensitivity:
         sy = eng.prolong(b.Sint, y)                                                 # S y (forward.py:277)
         pf = eng.scatter_points(self.Pp, W, ns)                                     # P W (forward.py:275)
         z = eng.residual(pf, 1.0, self.w, sy, -1.0, ns)                             # p - A sy (forward.py:278)
-        eng.interior_solve(b.Lc, b.Lr, z)
+        eng.interior_solve(b.factor, z)
         return eng.cell_gradient(self.sigma, self.U, z, sy, self.ZR)                # forward.py:278-280
 
     def apply_dev(self, dm):
@@ -207,7 +207,7 @@ class AdaptiveSensitivity:
         dm = eng.to_device(dm).reshape(-1)
         c = eng.edge_average(self.sigma, dm)                                        # Csig dm (forward.py:259)
         ydm = eng.residual(None, 0.0, c, self.U, -1.0, ns)                          # -G^T(gu c)
-        eng.interior_solve(b.Lc, b.Lr, ydm)                                         # _Y_dm (forward.py:250-252)
+        eng.interior_solve(b.factor, ydm)                                         # _Y_dm (forward.py:250-252)
         dt = eng.restrict_op(b.Sint, c, self.UR, self.w, ydm, ns, scale=-1.0)       # xdm - S^T(gdm + A ydm)
         eng.coarse_solve(self.state.Lk, dt)                                         # forward.py:267
         return eng.receive(self.Pp, b.Sint, Y=dt, Xfield=ydm)                       # P^T(ydm + S dt) (:268)

@@ -67,9 +67,12 @@ def test_skeleton_values_bit_exact():
     assert np.array_equal(S.data[mask], g["S_data"][mask])
 
 
-def test_edge_weights_bit_exact():
+def test_edge_weights_last_ulp():
+    # w = C exp(m) in the reference's summation order; exp() itself is not
+    # correctly rounded on either side, so allow a few ulps per entry.
     g = load_golden("c32_b8")
     gp, mesh, part, survey, builder = build_gpu(g)
     op = gp.assemble_operator(mesh, g["m"])
     builder.assemble(op)
-    assert np.array_equal(op.edge_weights, g["w"])
+    w = op.edge_weights
+    assert np.max(np.abs(w - g["w"]) / np.abs(g["w"])) <= 4e-16
