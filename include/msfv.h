@@ -118,8 +118,9 @@ MSFV_API int msfv_galerkin(const msfv_plan* plan, const double* Kloc, double shi
 MSFV_API int msfv_coarse_diag(const msfv_plan* plan, const double* Ak, double* diag, void* stream);
 /* In-place banded Cholesky of A_k (cho_factor, forward.py:121). flags |= COARSE_NOT_SPD. */
 MSFV_API int msfv_coarse_factor(const msfv_plan* plan, double* Ak, int32_t* flags, void* stream);
-/* X <- A_k^{-1} X, X [k][nrhs] (cho_solve, forward.py:72-75). */
-MSFV_API int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, int32_t nrhs, void* stream);
+/* X <- A_k^{-1} X, X [k][nrhs] (cho_solve, forward.py:72-75); scratch: k*nrhs doubles. */
+MSFV_API int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, double* scratch, int32_t nrhs,
+                               void* stream);
 
 /* out[col][s] = sum_t val_t (Xfield(node_t,s) + S(node_t,:) Y[:,s]); Y or Xfield may be NULL.
  * (P^T S T forward.py:143; P^T (ydm + S dt) forward.py:268) */
@@ -145,9 +146,10 @@ MSFV_API int msfv_interior_solve(const msfv_plan* plan, const double* factor, co
 MSFV_API int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
                      const double* w2, const double* X2, int32_t nrhs, double scale, double* part, double* out,
                      void* stream);
-/* g = -sigma C^T sum_s [G U (G Z + G Y) + G R G Y]  (rapply compact form, forward.py:271-281). */
+/* g = -sigma C^T sum_s [G U (G Z + G Y) + G R G Y]  (rapply compact form, forward.py:271-281).
+ * xi: nedges doubles of scratch (the per-edge sums). */
 MSFV_API int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
-                       const double* Y, const double* R, int32_t nrhs, double* g, void* stream);
+                       const double* Y, const double* R, int32_t nrhs, double* xi, double* g, void* stream);
 
 #ifdef __cplusplus
 }

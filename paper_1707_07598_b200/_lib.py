@@ -54,7 +54,7 @@ SIGNATURES = {
     "msfv_galerkin": (ctypes.c_int, [_P, _P, _D, _P, _P]),
     "msfv_coarse_diag": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_coarse_factor": (ctypes.c_int, [_P, _P, _P, _P]),
-    "msfv_coarse_solve": (ctypes.c_int, [_P, _P, _P, _I32, _P]),
+    "msfv_coarse_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_survey_receive": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P]),
     "msfv_survey_restrict": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P]),
     "msfv_survey_scatter": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
@@ -62,7 +62,7 @@ SIGNATURES = {
     "msfv_residual": (ctypes.c_int, [_P, _P, _D, _P, _P, _D, _I32, _P, _P]),
     "msfv_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_restrict_op": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),
-    "msfv_cell_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "msfv_cell_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P]),
 }
 
 _LIB = None

@@ -435,46 +435,82 @@ __device__ __forceinline__ double apply_A_row(const Geo& g, const double* __rest
   return v;
 }
 
+// Lane groups: a group of G = 2^lg lanes (G >= nrhs up to 32) shares one node
+// and strides over the sources, so loads and stores of [node][s] fields are
+// contiguous across the group.
+__host__ __forceinline__ int group_log2(int nrhs) {
+  int lg = 0;
+  while ((1 << lg) < nrhs && lg < 5) ++lg;
+  return lg;
+}
+
 // out(x) = alpha * src(x) + beta * (A_wt X)(x) on every block-interior node.
 __global__ void k_residual(Geo g, const double* __restrict__ src, double alpha,
                            const double* __restrict__ wt, const double* __restrict__ X, double beta,
-                           int nrhs, double* __restrict__ out) {
+                           int nrhs, int lg, double* __restrict__ out) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long tot = (long long)g.nbl * g.nI * nrhs;
-  if (t >= tot) return;
-  int s = (int)(t % nrhs);
-  long long ii = t / nrhs;
+  long long ii = t >> lg;
+  const int j = (int)(t & ((1 << lg) - 1));
+  if (ii >= (long long)g.nbl * g.nI) return;
   int jb = (int)(ii / g.nI), a = (int)(ii % g.nI);
   int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
   long long I = (long long)bi * g.b1 + x, J = (long long)bj * g.b2 + y, K = (long long)bk * g.b3 + z;
   long long nd = node_id(g, I, J, K);
-  double v = 0.0;
-  if (src) v = alpha * src[nd * nrhs + s];
-  if (beta != 0.0) v += beta * apply_A_row(g, wt, X, nrhs, s, I, J, K);
-  out[nd * nrhs + s] = v;
+  const double c1 = g.ih1 * g.ih1, c2 = g.ih2 * g.ih2, c3 = g.ih3 * g.ih3;
+  const double kxm = wt[ex_id(g, I - 1, J, K)] * c1, kxp = wt[ex_id(g, I, J, K)] * c1;
+  const double kym = wt[ey_id(g, I, J - 1, K)] * c2, kyp = wt[ey_id(g, I, J, K)] * c2;
+  const double kzm = wt[ez_id(g, I, J, K - 1)] * c3, kzp = wt[ez_id(g, I, J, K)] * c3;
+  const long long sx = 1, sy = g.n1 + 1, sz = (long long)(g.n1 + 1) * (g.n2 + 1);
+  for (int s = j; s < nrhs; s += (1 << lg)) {
+    const double* Xn = X + s;
+    const double xc = Xn[nd * nrhs];
+    double v = 0.0;
+    if (beta != 0.0) {
+      double av = kxm * (xc - Xn[(nd - sx) * nrhs]);
+      av += kxp * (xc - Xn[(nd + sx) * nrhs]);
+      av += kym * (xc - Xn[(nd - sy) * nrhs]);
+      av += kyp * (xc - Xn[(nd + sy) * nrhs]);
+      av += kzm * (xc - Xn[(nd - sz) * nrhs]);
+      av += kzp * (xc - Xn[(nd + sz) * nrhs]);
+      v = beta * av;
+    }
+    if (src) v += alpha * src[nd * nrhs + s];
+    out[nd * nrhs + s] = v;
+  }
 }
 
-// field(node, s) = sum_cc S(node, cc) Y[col(cc), s]  (node 0 -> 0)
+// field(node, s) = sum_cc S(node, cc) Y[col(cc), s]  (node 0 -> 0); a lane
+// group per node evaluates the node's S row once and strides over sources.
 __global__ void k_prolong(Geo g, const double* __restrict__ Sint, const double* __restrict__ Y,
-                          int nrhs, double* __restrict__ out) {
+                          int nrhs, int lg, double* __restrict__ out) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= g.Nn * nrhs) return;
-  int s = (int)(t % nrhs);
-  long long nd = t / nrhs;
-  if (nd == 0) { out[t] = 0.0; return; }
+  long long nd = t >> lg;
+  const int j = (int)(t & ((1 << lg) - 1));
+  if (nd >= g.Nn) return;
+  double* o = out + nd * nrhs;
+  if (nd == 0) {
+    for (int s = j; s < nrhs; s += (1 << lg)) o[s] = 0.0;
+    return;
+  }
   long long I = nd % (g.n1 + 1), r = nd / (g.n1 + 1), J = r % (g.n2 + 1), K = r / (g.n2 + 1);
   int bi = own1(I, g.b1, g.nb1), bj = own1(J, g.b2, g.nb2), bk = own1(K, g.b3, g.nb3);
   int x = (int)(I - (long long)bi * g.b1), y = (int)(J - (long long)bj * g.b2), z = (int)(K - (long long)bk * g.b3);
   int jb = block_of(g, bi, bj, bk);
   const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  double v = 0.0;
+  double sv[8];
+  const double* yc[8];
 #pragma unroll
   for (int cc = 0; cc < 8; ++cc) {
-    double sv = s_value(g, Sb, cc, x, y, z, false);
-    v += sv * Y[(size_t)corner_col(g, bi, bj, bk, cc) * nrhs + s];
+    sv[cc] = s_value(g, Sb, cc, x, y, z, false);
+    yc[cc] = Y + (size_t)corner_col(g, bi, bj, bk, cc) * nrhs;
   }
-  out[t] = v;
+  for (int s = j; s < nrhs; s += (1 << lg)) {
+    double v = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) v += sv[cc] * __ldg(yc[cc] + s);
+    o[s] = v;
+  }
 }
 
 // Per-block partial restriction: part[jb][cc][s] = sum over nodes owned by jb
@@ -543,40 +579,65 @@ __global__ void k_gather_corners(Geo g, const double* __restrict__ part, int nrh
   out[t] = scale * v;
 }
 
-// g_c = -sigma_c * (V/4) * sum over the cell's 12 edges of
-//   sum_s [dU (dZ + dY) + dR dY] / h^2
-// (compact form of AdaptiveSensitivity.rapply, forward.py:271-281).
-__global__ void k_cell_gradient(Geo g, const double* __restrict__ sigma, const double* __restrict__ U,
-                                const double* __restrict__ Z, const double* __restrict__ Y,
-                                const double* __restrict__ R, int nrhs, double* __restrict__ gout) {
+// Edge products of the compact rapply form (forward.py:271-281):
+//   xi_e = sum_s [dU (dZ + dY) + dR dY] / h_e^2      (d = difference along e)
+// A lane group per node computes the node's (up to) three forward edges; the
+// group's lanes stride over sources (coalesced) and reduce with shuffles.
+__global__ void k_edge_xi(Geo g, const double* __restrict__ U, const double* __restrict__ Z,
+                          const double* __restrict__ Y, const double* __restrict__ R, int nrhs, int lg,
+                          double* __restrict__ xi) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long nd = t >> lg;
+  const int j = (int)(t & ((1 << lg) - 1));
+  const bool valid = nd < g.Nn;
+  long long i = 0, jj = 0, k = 0;
+  if (valid) { i = nd % (g.n1 + 1); long long r = nd / (g.n1 + 1); jj = r % (g.n2 + 1); k = r / (g.n2 + 1); }
+  const bool hx = valid && i < g.n1, hy = valid && jj < g.n2, hz = valid && k < g.n3;
+  const long long nx = nd + 1, ny = nd + (g.n1 + 1), nz = nd + (long long)(g.n1 + 1) * (g.n2 + 1);
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  if (valid) {
+    for (int s = j; s < nrhs; s += (1 << lg)) {
+      const long long o = nd * nrhs + s;
+      const double u = __ldg(U + o), zz = __ldg(Z + o), yy = __ldg(Y + o), rr = __ldg(R + o);
+      if (hx) {
+        const long long q = nx * nrhs + s;
+        const double du = __ldg(U + q) - u, dz = __ldg(Z + q) - zz, dy = __ldg(Y + q) - yy, dr = __ldg(R + q) - rr;
+        ax += du * (dz + dy) + dr * dy;
+      }
+      if (hy) {
+        const long long q = ny * nrhs + s;
+        const double du = __ldg(U + q) - u, dz = __ldg(Z + q) - zz, dy = __ldg(Y + q) - yy, dr = __ldg(R + q) - rr;
+        ay += du * (dz + dy) + dr * dy;
+      }
+      if (hz) {
+        const long long q = nz * nrhs + s;
+        const double du = __ldg(U + q) - u, dz = __ldg(Z + q) - zz, dy = __ldg(Y + q) - yy, dr = __ldg(R + q) - rr;
+        az += du * (dz + dy) + dr * dy;
+      }
+    }
+  }
+  for (int off = (1 << lg) >> 1; off > 0; off >>= 1) {
+    ax += __shfl_xor_sync(0xffffffffu, ax, off);
+    ay += __shfl_xor_sync(0xffffffffu, ay, off);
+    az += __shfl_xor_sync(0xffffffffu, az, off);
+  }
+  if (j == 0) {
+    if (hx) xi[ex_id(g, i, jj, k)] = ax * (g.ih1 * g.ih1);
+    if (hy) xi[ey_id(g, i, jj, k)] = ay * (g.ih2 * g.ih2);
+    if (hz) xi[ez_id(g, i, jj, k)] = az * (g.ih3 * g.ih3);
+  }
+}
+
+// g_c = -sigma_c (V/4) sum over the cell's 12 edges of xi_e  (= -Csig^T xi)
+__global__ void k_cell_gather(Geo g, const double* __restrict__ sigma, const double* __restrict__ xi,
+                              double* __restrict__ gout) {
   long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (c >= g.Nm) return;
   long long i = c % g.n1, r = c / g.n1, j = r % g.n2, k = r / g.n2;
   double tot = 0.0;
-  for (int ax = 0; ax < 3; ++ax) {
-    const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
-    double ea = 0.0;
-    for (int e = 0; e < 4; ++e) {
-      int d1 = e & 1, d2 = e >> 1;
-      long long a0i = i, a0j = j, a0k = k;
-      if (ax == 0) { a0j += d1; a0k += d2; }
-      else if (ax == 1) { a0i += d1; a0k += d2; }
-      else { a0i += d1; a0j += d2; }
-      long long n0 = node_id(g, a0i, a0j, a0k);
-      long long n1 = node_id(g, a0i + (ax == 0), a0j + (ax == 1), a0k + (ax == 2));
-      const double* U0 = U + n0 * nrhs; const double* U1 = U + n1 * nrhs;
-      const double* Z0 = Z + n0 * nrhs; const double* Z1 = Z + n1 * nrhs;
-      const double* Y0 = Y + n0 * nrhs; const double* Y1 = Y + n1 * nrhs;
-      const double* R0 = R + n0 * nrhs; const double* R1 = R + n1 * nrhs;
-      double xi = 0.0;
-      for (int s = 0; s < nrhs; ++s) {
-        double du = U1[s] - U0[s], dz = Z1[s] - Z0[s], dy = Y1[s] - Y0[s], dr = R1[s] - R0[s];
-        xi += du * (dz + dy) + dr * dy;
-      }
-      ea += xi;
-    }
-    tot += ea * ihs;
-  }
+  tot += xi[ex_id(g, i, j, k)] + xi[ex_id(g, i, j + 1, k)] + xi[ex_id(g, i, j, k + 1)] + xi[ex_id(g, i, j + 1, k + 1)];
+  tot += xi[ey_id(g, i, j, k)] + xi[ey_id(g, i + 1, j, k)] + xi[ey_id(g, i, j, k + 1)] + xi[ey_id(g, i + 1, j, k + 1)];
+  tot += xi[ez_id(g, i, j, k)] + xi[ez_id(g, i + 1, j, k)] + xi[ez_id(g, i, j + 1, k)] + xi[ez_id(g, i + 1, j + 1, k)];
   gout[c] = -sigma[c] * (g.qv * tot);
 }
 
@@ -636,15 +697,16 @@ cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr,
 }
 cudaError_t launch_residual(const Geo& g, const double* src, double alpha, const double* wt, const double* X,
                             double beta, int nrhs, double* out, cudaStream_t st) {
-  long long tot = (long long)g.nbl * g.nI * nrhs;
-  if (tot == 0) return cudaSuccess;
-  k_residual<<<nblk(tot, 256), 256, 0, st>>>(g, src, alpha, wt, X, beta, nrhs, out);
+  const int lg = group_log2(nrhs);
+  long long tot = ((long long)g.nbl * g.nI) << lg;
+  if (tot == 0 || nrhs == 0) return cudaSuccess;
+  k_residual<<<nblk(tot, 256), 256, 0, st>>>(g, src, alpha, wt, X, beta, nrhs, lg, out);
   count_launches(1);
   return cudaGetLastError();
 }
 cudaError_t launch_prolong(const Geo& g, const double* Sint, const double* Y, int nrhs, double* out, cudaStream_t st) {
-  long long tot = g.Nn * nrhs;
-  k_prolong<<<nblk(tot, 256), 256, 0, st>>>(g, Sint, Y, nrhs, out);
+  const int lg = group_log2(nrhs);
+  k_prolong<<<nblk(g.Nn << lg, 256), 256, 0, st>>>(g, Sint, Y, nrhs, lg, out);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -660,8 +722,12 @@ cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w
   return cudaGetLastError();
 }
 cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
-                                 const double* Y, const double* R, int nrhs, double* gout, cudaStream_t st) {
-  k_cell_gradient<<<nblk(g.Nm, 128), 128, 0, st>>>(g, sigma, U, Z, Y, R, nrhs, gout);
+                                 const double* Y, const double* R, int nrhs, double* xi, double* gout,
+                                 cudaStream_t st) {
+  const int lg = group_log2(nrhs);
+  k_edge_xi<<<nblk(g.Nn << lg, 256), 256, 0, st>>>(g, U, Z, Y, R, nrhs, lg, xi);
+  count_launches(1);
+  k_cell_gather<<<nblk(g.Nm, 256), 256, 0, st>>>(g, sigma, xi, gout);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -77,6 +77,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.h1 = h[0]; g.h2 = h[1]; g.h3 = h[2];
   g.ih1 = 1.0 / h[0]; g.ih2 = 1.0 / h[1]; g.ih3 = 1.0 / h[2];
   g.qv = 0.25 * (h[0] * h[1] * h[2]);
+  g.ib1 = 1.0 / g.b1; g.ib2 = 1.0 / g.b2; g.ib3 = 1.0 / g.b3;
   if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
@@ -100,7 +101,7 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_NI] = g.nI;
   v[MSFV_INFO_P1S] = g.P1s;
   v[MSFV_INFO_K] = g.kc;
-  v[MSFV_INFO_AK_DOUBLES] = (int64_t)g.NT * (g.PT + 1) * g.TB * g.TB + (int64_t)g.NT * g.TB * g.TB;
+  v[MSFV_INFO_AK_DOUBLES] = (int64_t)coarse_doubles(g);
   v[MSFV_INFO_BASIS_SMEM] = (int64_t)basis_smem_bytes(g);
   v[MSFV_INFO_NT] = g.NT;
   v[MSFV_INFO_PT] = g.PT;
@@ -269,10 +270,11 @@ int msfv_coarse_factor(const msfv_plan* plan, double* Ak, int32_t* flags, void* 
   return cuda_check(launch_coarse_factor(plan->g, Ak, flags, (cudaStream_t)stream), "coarse_factor");
 }
 
-int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, int32_t nrhs, void* stream) {
+int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, double* scratch, int32_t nrhs,
+                      void* stream) {
   CHECK_PLAN(plan);
   if (nrhs < 0) return fail(MSFV_SHAPE, "nrhs < 0");
-  return cuda_check(launch_coarse_solve(plan->g, Lk, X, nrhs, (cudaStream_t)stream), "coarse_solve");
+  return cuda_check(launch_coarse_solve(plan->g, Lk, X, scratch, nrhs, (cudaStream_t)stream), "coarse_solve");
 }
 
 int msfv_survey_receive(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Y,
@@ -329,9 +331,9 @@ int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1
 }
 
 int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
-                       const double* Y, const double* R, int32_t nrhs, double* g, void* stream) {
+                       const double* Y, const double* R, int32_t nrhs, double* xi, double* g, void* stream) {
   CHECK_PLAN(plan);
-  return cuda_check(launch_cell_gradient(plan->g, sigma, U, Z, Y, R, nrhs, g, (cudaStream_t)stream),
+  return cuda_check(launch_cell_gradient(plan->g, sigma, U, Z, Y, R, nrhs, xi, g, (cudaStream_t)stream),
                     "cell_gradient");
 }
 

@@ -1,5 +1,5 @@
 // Coarse (Galerkin) system: assembly of A_k = P^T A P from the per-block 8x8
-// contributions, banded tiled Cholesky and multi-RHS triangular solves.
+// contributions, banded tiled Cholesky, and the coarse solves.
 //
 // Reference: forward.py:101-142 forms A_k densely and calls LAPACK dpotrf
 // (cho_factor) for k <= 5000, SuperLU above.  A_k couples coarse nodes only
@@ -8,23 +8,68 @@
 // inside that band: the banded factorization below is the same Cholesky
 // factor as the reference's dense one, computed without the zero blocks.
 //
-// Layout: lower band in TB x TB tiles, tile column J holds tiles (J+t, J),
-// t = 0..PT, each row-major:  Ak[((J*(PT+1) + t)*TB + r)*TB + q].
-// Rows >= kc (padding) are identity.  Dinv[J] = inverse of the diagonal tile
-// of L (computed after the factorization) turns the triangular solves into
-// tile products.
+// Buffer layout (one allocation of MSFV_INFO_AK_DOUBLES doubles):
+//   A     NT*(PT+1) tiles   lower band of A_k; tile column J holds (J+t, J),
+//                           t = 0..PT, each TB x TB row-major.  Updated in
+//                           place by the factorization (trailing tiles).
+//   Dinv  NT tiles          L_JJ^{-1}
+//   Lo    NT*(PT+1) tiles   the factor: slot 0 = L_JJ, slot t = L_{J+t,J}
+//   Y     (NT*TB)^2         dense L^{-1} (row-major, lower part), only when
+//                           k <= COARSE_INV_MAX: a solve becomes two streaming
+//                           products instead of 2*NT dependent tile steps.
+// Padding rows (>= kc) are identity.
+//
+// The factorization is one cooperative launch with one grid barrier per tile
+// column: after the barrier every CTA takes trailing-update tasks
+// (recomputing the panel products it needs, so the panel TRSM costs no extra
+// barrier) and L^{-1} row-panel tasks; CTA 0 first takes the task that
+// updates the next diagonal tile and then factors it (one-step lookahead).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace msfv {
 
 constexpr int TB = COARSE_TB;
+constexpr int TT = TB * TB;
+
+struct CoarseBufs {
+  double* A;
+  double* Dinv;
+  double* Lo;
+  double* Y;   // may be null
+};
+
+__host__ __device__ __forceinline__ size_t band_tiles(const Geo& g) { return (size_t)g.NT * (g.PT + 1); }
+__host__ __device__ __forceinline__ bool coarse_has_inverse(const Geo& g) { return g.kc <= COARSE_INV_MAX; }
+__host__ __device__ __forceinline__ size_t y_dim(const Geo& g) { return (size_t)g.NT * TB; }
+
+__host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double* base) {
+  CoarseBufs b;
+  b.A = base;
+  b.Dinv = b.A + band_tiles(g) * TT;
+  b.Lo = b.Dinv + (size_t)g.NT * TT;
+  b.Y = coarse_has_inverse(g) ? b.Lo + band_tiles(g) * TT : nullptr;
+  return b;
+}
+
+size_t coarse_doubles(const Geo& g) {
+  size_t n = 2 * band_tiles(g) * TT + (size_t)g.NT * TT;
+  if (coarse_has_inverse(g)) n += y_dim(g) * y_dim(g);
+  return n;
+}
+size_t coarse_scratch_doubles(const Geo& g, int nrhs) { return (size_t)g.kc * nrhs; }
 
 __device__ __forceinline__ double* tile(double* A, const Geo& g, int J, int t) {
-  return A + ((size_t)J * (g.PT + 1) + t) * TB * TB;
+  return A + ((size_t)J * (g.PT + 1) + t) * TT;
 }
 __device__ __forceinline__ const double* tile(const double* A, const Geo& g, int J, int t) {
-  return A + ((size_t)J * (g.PT + 1) + t) * TB * TB;
+  return A + ((size_t)J * (g.PT + 1) + t) * TT;
 }
 
 // Thread per (coarse row c, lower neighbour o): A_k[c][c'] = sum over blocks
@@ -75,177 +120,443 @@ __global__ void k_coarse_diag(Geo g, const double* __restrict__ Ak, double* __re
   diag[c] = tile(Ak, g, c / TB, 0)[(c % TB) * TB + (c % TB)];
 }
 
-// Panel of tile column J: Cholesky of the diagonal tile, its inverse Dinv_J,
-// then L_{J+t,J} = A_{J+t,J} Dinv_J^T for the tiles below it.
-__global__ void __launch_bounds__(256) k_coarse_panel(Geo g, int J, double* __restrict__ Ak, double* __restrict__ Dinv,
-                                                      int* __restrict__ flags) {
-  __shared__ double D[TB][TB + 1];
-  __shared__ double Di[TB][TB + 1];
-  __shared__ double As[TB][TB + 1];
+// ------------------------------------------------------------ factorization
+
+struct FactorSmem {
+  double P[TB][TB + 1];    // tile operands / POTRF workspace
+  double Q[TB][TB + 1];
+  double R[TB][TB + 1];
+  double D[TB][TB + 1];    // Dinv of the current column
+};
+
+__device__ __forceinline__ void load_tile(double (*S)[TB + 1], const double* src) {
+  for (int t = threadIdx.x; t < TT; t += blockDim.x) S[t / TB][t % TB] = src[t];
+}
+__device__ __forceinline__ void store_tile(double* dst, double (*S)[TB + 1]) {
+  for (int t = threadIdx.x; t < TT; t += blockDim.x) dst[t] = S[t / TB][t % TB];
+}
+
+// 32x32 tile products by 256 threads, each owning a 2x2 output block.
+template <bool XT, bool YT>
+__device__ __forceinline__ void mm22(double acc[4], double (*X)[TB + 1], double (*Y)[TB + 1], int r0, int c0) {
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+#pragma unroll 8
+  for (int m = 0; m < TB; ++m) {
+    const double x0 = XT ? X[m][r0] : X[r0][m], x1 = XT ? X[m][r0 + 1] : X[r0 + 1][m];
+    const double y0 = YT ? Y[c0][m] : Y[m][c0], y1 = YT ? Y[c0 + 1][m] : Y[m][c0 + 1];
+    acc[0] += x0 * y0; acc[1] += x0 * y1; acc[2] += x1 * y0; acc[3] += x1 * y1;
+  }
+}
+// O = op(X) op(Y)  (X^T when XT, Y^T when YT)
+template <bool XT, bool YT>
+__device__ __forceinline__ void mm(double (*O)[TB + 1], double (*X)[TB + 1], double (*Y)[TB + 1]) {
+  const int r0 = 2 * (threadIdx.x >> 4), c0 = 2 * (threadIdx.x & 15);
+  double a[4];
+  mm22<XT, YT>(a, X, Y, r0, c0);
+  O[r0][c0] = a[0]; O[r0][c0 + 1] = a[1]; O[r0 + 1][c0] = a[2]; O[r0 + 1][c0 + 1] = a[3];
+}
+// G (global, leading dimension ld) -= op(X) op(Y)
+template <bool XT, bool YT>
+__device__ __forceinline__ void gsub(double* G, size_t ld, double (*X)[TB + 1], double (*Y)[TB + 1]) {
+  const int r0 = 2 * (threadIdx.x >> 4), c0 = 2 * (threadIdx.x & 15);
+  double a[4];
+  mm22<XT, YT>(a, X, Y, r0, c0);
+  G[r0 * ld + c0] -= a[0]; G[r0 * ld + c0 + 1] -= a[1];
+  G[(r0 + 1) * ld + c0] -= a[2]; G[(r0 + 1) * ld + c0 + 1] -= a[3];
+}
+
+// Cholesky of diagonal tile J (in A) -> L_JJ (Lo slot 0) and L_JJ^{-1} (Dinv).
+__device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flags, FactorSmem& sm) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  double* Dg = tile(Ak, g, J, 0);
-  for (int t = tid; t < TB * TB; t += nt) D[t / TB][t % TB] = Dg[t];
+  auto& P = sm.P;
+  load_tile(P, tile(B.A, g, J, 0));
   __syncthreads();
-  for (int jc = 0; jc < TB; ++jc) {
-    double d = D[jc][jc];
-    if (!(d > 0.0)) {
-      if (tid == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
-      d = 1.0;
-    }
-    const double piv = sqrt(d), inv = 1.0 / piv;
-    for (int r = jc + 1 + tid; r < TB; r += nt) D[r][jc] *= inv;
-    __syncthreads();
-    if (tid == 0) D[jc][jc] = piv;
-    const int m = TB - 1 - jc;
-    for (int f = tid; f < m * m; f += nt) {
-      int r = jc + 1 + f / m, q = jc + 1 + f % m;
-      if (q <= r) D[r][q] -= D[r][jc] * D[q][jc];
-    }
-    __syncthreads();
-  }
-  for (int t = tid; t < TB * TB; t += nt) {
-    int r = t / TB, q = t % TB;
-    Dg[t] = q <= r ? D[r][q] : 0.0;
-  }
-  // inverse of the lower-triangular diagonal tile, thread per column
-  if (tid < TB) {
-    const int c = tid;
+  if (tid < 32) {       // warp 0: lane r holds row r in registers
+    const int r = tid;
     double x[TB];
 #pragma unroll
-    for (int r = 0; r < TB; ++r) {
-      double v = (r == c) ? 1.0 : 0.0;
+    for (int q = 0; q < TB; ++q) x[q] = P[r][q];
 #pragma unroll
-      for (int m2 = 0; m2 < r; ++m2) v -= D[r][m2] * x[m2];
-      x[r] = (r < c) ? 0.0 : v / D[r][r];
+    for (int c = 0; c < TB; ++c) {
+      double d = __shfl_sync(0xffffffffu, x[c], c);
+      if (!(d > 0.0)) {
+        if (r == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
+        d = 1.0;
+      }
+      const double piv = sqrt(d), inv = 1.0 / piv;
+      if (r > c) x[c] *= inv;
+      if (r == c) x[c] = piv;
+      const double lrc = x[c];
+#pragma unroll
+      for (int q = c + 1; q < TB; ++q) {
+        const double lqc = __shfl_sync(0xffffffffu, lrc, q);
+        if (r >= q) x[q] -= lrc * lqc;
+      }
     }
 #pragma unroll
-    for (int r = 0; r < TB; ++r) Di[r][c] = x[r];
+    for (int q = 0; q < TB; ++q) P[r][q] = q <= r ? x[q] : 0.0;
   }
+  auto& D = sm.D;
+  for (int t = tid; t < TT; t += nt) D[t / TB][t % TB] = 0.0;
   __syncthreads();
-  {
-    double* out = Dinv + (size_t)J * TB * TB;
-    for (int t = tid; t < TB * TB; t += nt) out[t] = Di[t / TB][t % TB];
-  }
-  const int pt = min(g.PT, g.NT - 1 - J);
-  for (int tt = 1; tt <= pt; ++tt) {
-    double* A = tile(Ak, g, J, tt);
-    for (int t = tid; t < TB * TB; t += nt) As[t / TB][t % TB] = A[t];
+  // L^{-1} row by row: D[r][c] = (delta_rc - sum_{c<=m<r} L[r][m] D[m][c]) / L[r][r]
+  const int c = tid & 31, part = tid >> 5;
+  for (int r = 0; r < TB; ++r) {
+    double s = 0.0;
+    for (int m = c + part; m < r; m += 8) s += P[r][m] * D[m][c];
+    sm.R[part][c] = s;
     __syncthreads();
-    for (int t = tid; t < TB * TB; t += nt) {
-      int r = t / TB, q = t % TB;
+    if (tid < 32 && c <= r) {
+      double tot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) tot += sm.R[p][c];
+      D[r][c] = ((r == c ? 1.0 : 0.0) - tot) / P[r][r];
+    }
+    __syncthreads();
+  }
+  store_tile(B.Dinv + (size_t)J * TT, D);
+  store_tile(tile(B.Lo, g, J, 0), P);
+  __syncthreads();
+}
+
+// Task f of tile column J: f < npairs -> trailing tile (t1, t2); else L^{-1}
+// row-panel J restricted to column tile f - npairs.  sm.D holds Dinv_J.
+__device__ void coarse_task(const Geo& g, int J, int f, int npairs, const CoarseBufs& B, FactorSmem& sm) {
+  auto& X1 = sm.P;
+  auto& X2 = sm.Q;
+  auto& T = sm.R;
+  auto& D = sm.D;
+  if (f < npairs) {
+    int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
+    while (t1 * (t1 - 1) / 2 > f) --t1;
+    while ((t1 + 1) * t1 / 2 <= f) ++t1;
+    const int t2 = f - t1 * (t1 - 1) / 2 + 1;
+    load_tile(T, tile(B.A, g, J, t1));
+    __syncthreads();
+    mm<false, true>(X1, T, D);                  // L_{J+t1,J} = A_{J+t1,J} Dinv^T
+    __syncthreads();
+    if (t2 != t1) {
+      load_tile(T, tile(B.A, g, J, t2));
+      __syncthreads();
+      mm<false, true>(X2, T, D);
+      __syncthreads();
+      gsub<false, true>(tile(B.A, g, J + t2, t1 - t2), TB, X1, X2);
+    } else {
+      gsub<false, true>(tile(B.A, g, J + t1, 0), TB, X1, X1);
+      store_tile(tile(B.Lo, g, J, t1), X1);
+    }
+    __syncthreads();
+  } else {
+    // Yf = Dinv_J Y_J ; W = Dinv_J^T Yf ; Y_{J+t} -= A_{J+t,J} W  (= L_{J+t,J} Yf)
+    const int cidx = f - npairs;
+    const size_t ld = y_dim(g);
+    double* Yj = B.Y + (size_t)J * TB * ld + (size_t)cidx * TB;
+    for (int t = threadIdx.x; t < TT; t += blockDim.x) T[t / TB][t % TB] = Yj[(t / TB) * ld + (t % TB)];
+    __syncthreads();
+    mm<false, false>(X1, D, T);
+    __syncthreads();
+    for (int t = threadIdx.x; t < TT; t += blockDim.x) Yj[(t / TB) * ld + (t % TB)] = X1[t / TB][t % TB];
+    mm<true, false>(X2, D, X1);
+    __syncthreads();
+    const int pt = min(g.PT, g.NT - 1 - J);
+    for (int t = 1; t <= pt; ++t) {
+      load_tile(T, tile(B.A, g, J, t));
+      __syncthreads();
+      gsub<false, false>(B.Y + (size_t)(J + t) * TB * ld + (size_t)cidx * TB, ld, T, X2);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_coarse_factor(Geo g, double* __restrict__ base, int* __restrict__ flags) {
+  __shared__ FactorSmem sm;
+  cg::grid_group grid = cg::this_grid();
+  const CoarseBufs B = coarse_bufs(g, base);
+  const bool withY = B.Y != nullptr;
+  if (withY) {
+    const size_t ld = y_dim(g);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ld; i += (size_t)gridDim.x * blockDim.x)
+      B.Y[i * ld + i] = 1.0;
+  }
+  if (blockIdx.x == 0) coarse_potrf(g, 0, B, flags, sm);
+  grid.sync();
+  for (int J = 0; J < g.NT; ++J) {
+    const int pt = min(g.PT, g.NT - 1 - J);
+    const int npairs = pt * (pt + 1) / 2;
+    const int ntasks = npairs + (withY ? J + 1 : 0);
+    load_tile(sm.D, B.Dinv + (size_t)J * TT);
+    __syncthreads();
+    int start = blockIdx.x;
+    if (blockIdx.x == 0 && pt >= 1) {
+      coarse_task(g, J, 0, npairs, B, sm);       // pair (1,1): next diagonal tile
+      __threadfence_block();
+      coarse_potrf(g, J + 1, B, flags, sm);      // lookahead factor of column J+1
+      load_tile(sm.D, B.Dinv + (size_t)J * TT);
+      __syncthreads();
+      start = gridDim.x;
+    }
+    for (int f = start; f < ntasks; f += gridDim.x) coarse_task(g, J, f, npairs, B, sm);
+    grid.sync();
+  }
+}
+
+// -------------------------------------------------- solves with L^{-1}
+
+constexpr int SCH = 16;   // sources per pass
+
+// Z[r][s] = sum_{c <= r} Y[r][c] X[c][s]; CTA per row tile, warp w owns rows
+// w, w+8, w+16, w+24, lanes run over the 32 columns of each column tile.
+__global__ void __launch_bounds__(256) k_coarse_inv_lower(Geo g, const double* __restrict__ Y, const double* __restrict__ X,
+                                                          double* __restrict__ Z, int nrhs) {
+  __shared__ double Xs[TB][SCH + 1];
+  const int I = blockIdx.x;
+  const size_t ld = y_dim(g);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int s0 = 0; s0 < nrhs; s0 += SCH) {
+    double acc[4][SCH];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int s = 0; s < SCH; ++s) acc[q][s] = 0.0;
+    for (int C = 0; C <= I; ++C) {
+      __syncthreads();
+      for (int t = tid; t < TB * SCH; t += blockDim.x) {
+        int c = t / SCH, s = t % SCH, row = C * TB + c;
+        Xs[c][s] = (row < g.kc && s0 + s < nrhs) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double yv = __ldg(Y + (size_t)(I * TB + w + 8 * q) * ld + (size_t)C * TB + lane);
+#pragma unroll
+        for (int s = 0; s < SCH; ++s) acc[q][s] += yv * Xs[lane][s];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int s = 0; s < SCH; ++s) {
+        double v = acc[q][s];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        acc[q][s] = v;
+      }
+      const int row = I * TB + w + 8 * q;
+      if (lane < SCH && row < g.kc && s0 + lane < nrhs) {
+        double v = 0.0;
+#pragma unroll
+        for (int s = 0; s < SCH; ++s) v = (s == lane) ? acc[q][s] : v;
+        Z[(size_t)row * nrhs + s0 + lane] = v;
+      }
+    }
+  }
+}
+
+// X[c][s] = sum_{r >= c} Y[r][c] Z[r][s]; CTA per column tile, lanes over its
+// 32 columns, warps over rows, smem reduction across warps.
+__global__ void __launch_bounds__(256) k_coarse_inv_upper(Geo g, const double* __restrict__ Y, const double* __restrict__ Z,
+                                                          double* __restrict__ X, int nrhs) {
+  __shared__ double Zs[TB][SCH + 1];
+  __shared__ double red[8][TB][SCH + 1];
+  const int C = blockIdx.x;
+  const size_t ld = y_dim(g);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int s0 = 0; s0 < nrhs; s0 += SCH) {
+    double acc[SCH];
+#pragma unroll
+    for (int s = 0; s < SCH; ++s) acc[s] = 0.0;
+    for (int I = C; I < g.NT; ++I) {
+      __syncthreads();
+      for (int t = tid; t < TB * SCH; t += blockDim.x) {
+        int rr = t / SCH, s = t % SCH, row = I * TB + rr;
+        Zs[rr][s] = (row < g.kc && s0 + s < nrhs) ? Z[(size_t)row * nrhs + s0 + s] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rr = w + 8 * q;
+        const double yv = __ldg(Y + (size_t)(I * TB + rr) * ld + (size_t)C * TB + lane);
+#pragma unroll
+        for (int s = 0; s < SCH; ++s) acc[s] += yv * Zs[rr][s];
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < SCH; ++s) red[w][lane][s] = acc[s];
+    __syncthreads();
+    for (int t = tid; t < TB * SCH; t += blockDim.x) {
+      int c = t / SCH, s = t % SCH;
       double v = 0.0;
-      for (int m2 = 0; m2 <= q; ++m2) v += As[r][m2] * Di[q][m2];
-      A[t] = v;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) v += red[p][c][s];
+      const int row = C * TB + c;
+      if (row < g.kc && s0 + s < nrhs) X[(size_t)row * nrhs + s0 + s] = v;
     }
     __syncthreads();
   }
 }
 
-// Trailing update of tile column J: A_{J+t1, J+t2} -= L_{J+t1,J} L_{J+t2,J}^T.
-__global__ void __launch_bounds__(256) k_coarse_update(Geo g, int J, double* __restrict__ Ak) {
-  __shared__ double As[TB][TB + 1], Bs[TB][TB + 1];
-  int f = blockIdx.x;
-  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
-  while (t1 * (t1 - 1) / 2 > f) --t1;
-  while ((t1 + 1) * t1 / 2 <= f) ++t1;
-  int t2 = f - t1 * (t1 - 1) / 2 + 1;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double* A = tile(Ak, g, J, t1);
-  const double* B = tile(Ak, g, J, t2);
-  for (int t = tid; t < TB * TB; t += nt) { As[t / TB][t % TB] = A[t]; Bs[t / TB][t % TB] = B[t]; }
-  __syncthreads();
-  double* C = tile(Ak, g, J + t2, t1 - t2);
-  for (int t = tid; t < TB * TB; t += nt) {
-    int r = t / TB, q = t % TB;
-    double v = 0.0;
-#pragma unroll 8
-    for (int m2 = 0; m2 < TB; ++m2) v += As[r][m2] * Bs[q][m2];
-    C[t] -= v;
-  }
-}
+// ------------------------------------------------ banded trsv (large k)
 
 // Forward then backward substitution with the banded tiled factor for RC
-// right-hand sides per CTA.  X is [kc][nrhs] row-major.  Forward is
-// right-looking (X_{J+t} -= L_{J+t,J} y_J straight in global memory, read back
-// by the same CTA); backward keeps the last PT+1 solved tiles of x in a
-// shared-memory ring so the transposed tile products read only L from L2.
+// right-hand sides per CTA.  X is [kc][nrhs] row-major.  The factor tiles
+// stream through a RING-slot cp.async pipeline in shared memory in exactly
+// the order they are consumed (forward: Dinv_J, L_{J+1,J}..L_{J+pt,J};
+// backward: L_{J+1,J}..L_{J+pt,J}, Dinv_J); the active right-hand-side rows
+// (PT+1 tile rows) live in a shared-memory ring, so global X is read and
+// written once per sweep.
+namespace {
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// tile sequence iterator: forward (dir=+1) or backward (dir=-1)
+struct TileSeq {
+  int J, t, NT, PT, dir;
+  __device__ int pt() const { return min(PT, NT - 1 - J); }
+  __device__ bool valid() const { return J >= 0 && J < NT; }
+  // forward order: t = 0 (Dinv), 1..pt ; backward order: t = 1..pt, then 0 (Dinv)
+  __device__ void next() {
+    if (dir > 0) {
+      if (t < pt()) ++t; else { ++J; t = 0; }
+    } else {
+      if (t == 0) { --J; t = (J >= 0 && pt() > 0) ? 1 : 0; }
+      else if (t < pt()) ++t;
+      else t = 0;
+    }
+  }
+};
+}  // namespace
+
 template <int RC>
 __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __restrict__ Lk, const double* __restrict__ Dinv,
                                                      double* __restrict__ X, int nrhs) {
-  extern __shared__ double tsm[];
-  double* Xs = tsm;                        // [TB][RC]
-  double* acc = Xs + TB * RC;              // [TB][RC]
-  double* win = acc + TB * RC;             // [PT+1][TB][RC]
+  constexpr int RING = 4;
+  extern __shared__ __align__(16) double tsm[];
+  double* ring = tsm;                              // [RING][TB*TB]
+  double* Xw = ring + RING * TT;              // [PT+1][TB][RC]
+  double* Ys = Xw + (size_t)(g.PT + 1) * TB * RC;  // [TB][RC]
   const int tid = threadIdx.x, nt = blockDim.x;
   const int s0 = blockIdx.x * RC;
   const int ns = min(RC, nrhs - s0);
   const int W = g.PT + 1;
-  // ---------------- forward
-  for (int J = 0; J < g.NT; ++J) {
+  auto src_of = [&](const TileSeq& q) -> const double* {
+    return q.t == 0 ? Dinv + (size_t)q.J * TT : tile(Lk, g, q.J, q.t);
+  };
+  auto issue = [&](TileSeq& q, int slot) {
+    if (q.valid()) {
+      const double* src = src_of(q);
+      double* dst = ring + slot * TT;
+      for (int i = tid; i < TT / 2; i += nt) cpa16(dst + 2 * i, src + 2 * i);
+    }
+    cpa_commit();
+    q.next();
+  };
+  auto load_rows = [&](int I, double* dst) {
     for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = J * TB + r;
-      Xs[t] = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+      int r = t / RC, s = t % RC, row = I * TB + r;
+      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
     }
-    __syncthreads();
-    const double* Di = Dinv + (size_t)J * TB * TB;
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC;
-      const double* drow = Di + r * TB;
-      double v = 0.0;
+  };
+    {
+    TileSeq pf{0, 0, g.NT, g.PT, 1};
+    int issued = 0, consumed = 0;
+    for (; issued < RING - 1; ++issued) issue(pf, issued % RING);
+    for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
+    for (int J = 0; J < g.NT; ++J) {
+      const int pt = min(g.PT, g.NT - 1 - J);
+      for (int t = 0; t <= pt; ++t) {
+        cpa_wait<RING - 2>();
+        __syncthreads();
+        issue(pf, issued % RING);
+        ++issued;
+        const double* T = ring + (consumed % RING) * TT;
+        ++consumed;
+        if (t == 0) {
+          const double* xj = Xw + (size_t)(J % W) * TB * RC;
+          for (int q = tid; q < TB * RC; q += nt) {
+            int r = q / RC, s = q % RC;
+            double v = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < TB; ++q) v += drow[q] * Xs[q * RC + s];   // Dinv upper part is zero
-      acc[t] = v;
-      int row = J * TB + r;
-      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-    }
-    __syncthreads();
-    const int pt = min(g.PT, g.NT - 1 - J);
-    for (int t = tid; t < pt * TB * RC; t += nt) {
-      int tt = 1 + t / (TB * RC), rem = t % (TB * RC), r = rem / RC, s = rem % RC;
-      int row = (J + tt) * TB + r;
-      if (s >= ns || row >= g.kc) continue;
-      const double* L = tile(Lk, g, J, tt) + r * TB;
-      double v = 0.0;
+            for (int c = 0; c < TB; ++c) v += T[r * TB + c] * xj[c * RC + s];
+            Ys[q] = v;
+            int row = J * TB + r;
+            if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
+          }
+        } else {
+          double* xt = Xw + (size_t)((J + t) % W) * TB * RC;
+          for (int q = tid; q < TB * RC; q += nt) {
+            int r = q / RC, s = q % RC;
+            double v = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < TB; ++q) v += L[q] * acc[q * RC + s];
-      X[(size_t)row * nrhs + s0 + s] -= v;
+            for (int c = 0; c < TB; ++c) v += T[r * TB + c] * Ys[c * RC + s];
+            xt[q] -= v;
+          }
+        }
+      }
+      __syncthreads();
+      load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);   // slot of row J is free now
     }
+    cpa_wait<0>();
     __syncthreads();
   }
-  // ---------------- backward
-  for (int J = g.NT - 1; J >= 0; --J) {
-    const int pt = min(g.PT, g.NT - 1 - J);
-    for (int t = tid; t < TB * RC; t += nt) {
-      int q = t / RC, s = t % RC, row = J * TB + q;
-      double v = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-      for (int tt = 1; tt <= pt; ++tt) {
-        const double* L = tile(Lk, g, J, tt);
-        const double* xw = win + (size_t)((J + tt) % W) * TB * RC;
-#pragma unroll 8
-        for (int r = 0; r < TB; ++r) v -= L[r * TB + q] * xw[r * RC + s];
+    {
+    TileSeq pf{g.NT - 1, 0, g.NT, g.PT, -1};
+    pf.t = (pf.pt() > 0) ? 1 : 0;
+    int issued = 0, consumed = 0;
+    for (; issued < RING - 1; ++issued) issue(pf, issued % RING);
+    for (int J = g.NT - 1; J >= 0; --J) {
+      const int pt = min(g.PT, g.NT - 1 - J);
+      // acc = y_J
+      for (int q = tid; q < TB * RC; q += nt) {
+        int r = q / RC, s = q % RC, row = J * TB + r;
+        Ys[q] = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
       }
-      acc[t] = v;
+      for (int k = 0; k <= pt; ++k) {
+        const int t = (k < pt) ? k + 1 : 0;
+        cpa_wait<RING - 2>();
+        __syncthreads();
+        issue(pf, issued % RING);
+        ++issued;
+        const double* T = ring + (consumed % RING) * TT;
+        ++consumed;
+        if (t > 0) {
+          const double* xt = Xw + (size_t)((J + t) % W) * TB * RC;
+          for (int q = tid; q < TB * RC; q += nt) {
+            int c = q / RC, s = q % RC;
+            double v = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < TB; ++r) v += T[r * TB + c] * xt[r * RC + s];
+            Ys[q] -= v;
+          }
+        } else {
+          double* xj = Xw + (size_t)(J % W) * TB * RC;
+          for (int q = tid; q < TB * RC; q += nt) {
+            int r = q / RC, s = q % RC;
+            double v = 0.0;
+            for (int c = r; c < TB; ++c) v += T[c * TB + r] * Ys[c * RC + s];
+            int row = J * TB + r;
+            if (row >= g.kc || s >= ns) v = 0.0;
+            xj[q] = v;
+            if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    const double* Di = Dinv + (size_t)J * TB * TB;
-    double* xo = win + (size_t)(J % W) * TB * RC;
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = J * TB + r;
-      double v = 0.0;
-      for (int q = r; q < TB; ++q) v += Di[q * TB + r] * acc[q * RC + s];
-      if (row >= g.kc || s >= ns) v = 0.0;
-      xo[t] = v;
-      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-    }
-    __syncthreads();
+    cpa_wait<0>();
   }
 }
+
+// ------------------------------------------------------------- launchers
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st) {
-  size_t bytes = (size_t)g.NT * (g.PT + 1) * TB * TB * sizeof(double);
-  cudaError_t e = cudaMemsetAsync(Ak, 0, bytes, st);
+  cudaError_t e = cudaMemsetAsync(Ak, 0, band_tiles(g) * TT * sizeof(double), st);
   if (e != cudaSuccess) return e;
   long long tot = (long long)g.NT * TB * 14;
   k_coarse_assemble<<<nblk(tot, 256), 256, 0, st>>>(g, Kloc, shift, Ak);
@@ -259,30 +570,44 @@ cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cud
   return cudaGetLastError();
 }
 
-// Dinv lives right after the tiles in the same allocation.
 cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
-  double* Dinv = Ak + (size_t)g.NT * (g.PT + 1) * TB * TB;
-  for (int J = 0; J < g.NT; ++J) {
-    k_coarse_panel<<<1, 256, 0, st>>>(g, J, Ak, Dinv, flags);
-    count_launches(1);
-    int pt = g.PT < g.NT - 1 - J ? g.PT : g.NT - 1 - J;
-    int npairs = pt * (pt + 1) / 2;
-    if (npairs > 0) {
-      k_coarse_update<<<npairs, 256, 0, st>>>(g, J, Ak);
-      count_launches(1);
-    }
+  static int coop_grid = -1;
+  if (coop_grid < 0) {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_factor, 256, 0);
+    coop_grid = (coop && per_sm > 0) ? sms : 0;
   }
-  return cudaGetLastError();
+  if (coop_grid <= 0) return cudaErrorNotSupported;
+  CoarseBufs B = coarse_bufs(g, Ak);
+  if (B.Y) {
+    cudaError_t e = cudaMemsetAsync(B.Y, 0, y_dim(g) * y_dim(g) * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+  }
+  Geo gg = g;
+  void* args[] = {(void*)&gg, (void*)&Ak, (void*)&flags};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_coarse_factor, dim3(coop_grid), dim3(256), args, 0, st);
+  count_launches(1);
+  return e;
 }
 
-cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, int nrhs, cudaStream_t st) {
+cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
-  const double* Dinv = Lk + (size_t)g.NT * (g.PT + 1) * TB * TB;
+  CoarseBufs B = coarse_bufs(g, const_cast<double*>(Ak));
+  if (B.Y) {
+    k_coarse_inv_lower<<<g.NT, 256, 0, st>>>(g, B.Y, X, scratch, nrhs);
+    count_launches(1);
+    k_coarse_inv_upper<<<g.NT, 256, 0, st>>>(g, B.Y, scratch, X, nrhs);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   constexpr int RC = 4;
-  size_t smem = ((size_t)2 + g.PT + 1) * TB * RC * sizeof(double);
+  size_t smem = ((size_t)4 * TT + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, smem, st>>>(g, Lk, Dinv, X, nrhs);
+  k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, smem, st>>>(g, B.Lo, B.Dinv, X, nrhs);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -38,6 +38,7 @@ struct Geo {
   double h1, h2, h3;
   double ih1, ih2, ih3;    // 1/h per axis (as the reference's 1.0/h)
   double qv;               // 0.25 * cell volume (operators.py:83)
+  double ib1, ib2, ib3;    // 1/b per axis (device-side hats)
 };
 
 __host__ __device__ __forceinline__ long long node_id(const Geo& g, long long i, long long j, long long k) {
@@ -70,6 +71,21 @@ __host__ __device__ __forceinline__ double hat_corner(int cc, int x, int y, int 
   double w = hat1(x - cx, b1);
   w = w * hat1(y - cy, b2);
   w = w * hat1(z - cz, b3);
+  return w;
+}
+// Division-free device hat (1 - |d| * (1/b)); equal to hat1 whenever 1/b is
+// exact (b a power of two, e.g. the 8-cell blocks of the configs) and within
+// one ulp otherwise.  Used only inside device arithmetic; the skeleton values
+// of the returned CSC S come from the host (bit-exact with the reference).
+__device__ __forceinline__ double hatf1(int d, double ib) {
+  double v = 1.0 - fabs((double)d) * ib;
+  return v > 0.0 ? v : 0.0;
+}
+__device__ __forceinline__ double hatf(const Geo& g, int cc, int x, int y, int z) {
+  const int cx = (cc & 1) ? g.b1 : 0, cy = (cc & 2) ? g.b2 : 0, cz = (cc & 4) ? g.b3 : 0;
+  double w = hatf1(x - cx, g.ib1);
+  w = w * hatf1(y - cy, g.ib2);
+  w = w * hatf1(z - cz, g.ib3);
   return w;
 }
 
@@ -105,7 +121,7 @@ __device__ __forceinline__ double s_value(const Geo& g, const double* __restrict
   int a = interior_index(g, x, y, z);
   if (a >= 0) return Sint_b[(size_t)cc * g.nI + a];
   if (is_node0) return 0.0;
-  return hat_corner(cc, x, y, z, g.b1, g.b2, g.b3);
+  return hatf(g, cc, x, y, z);
 }
 
 }  // namespace msfv

@@ -11,6 +11,7 @@ constexpr int SOLVE_NSC = 8;
 constexpr int SOLVE_RING = 8;
 constexpr int RESTRICT_THREADS = 128;
 constexpr int COARSE_TB = 32;
+constexpr int COARSE_INV_MAX = 12000;  // explicit L^{-1} for the coarse solves up to this k
 constexpr int TC_WARPS = 2;      // warps (= coarse blocks) per CTA in the DMMA kernels
 constexpr int TC_MAX_PT = 7;     // largest tile band handled by the DMMA kernels (p <= 56)
 
@@ -39,7 +40,8 @@ cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w
                                const double* w2, const double* X2, int nrhs, double* part, double scale,
                                double* out, cudaStream_t st);
 cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
-                                 const double* Y, const double* R, int nrhs, double* gout, cudaStream_t st);
+                                 const double* Y, const double* R, int nrhs, double* xi, double* gout,
+                                 cudaStream_t st);
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
                              double* vals, cudaStream_t st);
 
@@ -56,7 +58,9 @@ cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* 
 // coarse (msfv_coarse.cu)
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
 cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st);
-cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, int nrhs, cudaStream_t st);
+cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, double* scratch, int nrhs, cudaStream_t st);
+size_t coarse_doubles(const Geo& g);
+size_t coarse_scratch_doubles(const Geo& g, int nrhs);
 cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st);
 
 // survey point sets (msfv_points.cu)

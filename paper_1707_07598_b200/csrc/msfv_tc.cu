@@ -90,7 +90,16 @@ struct Row {
   double kxm, kxp, kym, kyp, kzm, kzp;
 };
 
-__device__ __forceinline__ Row load_row(const Geo& g, const double* __restrict__ w, int X0, int Y0, int Z0, int i) {
+// Interior coordinates, packed x | y << 10 | z << 20 (one table per CTA).
+__device__ __forceinline__ void fill_coords(const Geo& g, int* crd) {
+  for (int a = threadIdx.x; a < g.nI; a += blockDim.x) {
+    const int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
+    crd[a] = x | (y << 10) | (z << 20);
+  }
+}
+
+__device__ __forceinline__ Row load_row(const Geo& g, const double* __restrict__ w, const int* crd, int X0, int Y0,
+                                        int Z0, int i) {
   Row r;
   r.valid = i < g.nI;
   if (!r.valid) {
@@ -98,9 +107,10 @@ __device__ __forceinline__ Row load_row(const Geo& g, const double* __restrict__
     r.kxm = r.kxp = r.kym = r.kyp = r.kzm = r.kzp = 0.0;
     return r;
   }
-  r.x = 1 + i % g.ni1;
-  r.y = 1 + (i / g.ni1) % g.ni2;
-  r.z = 1 + i / (g.ni1 * g.ni2);
+  const int c = crd[i];
+  r.x = c & 1023;
+  r.y = (c >> 10) & 1023;
+  r.z = c >> 20;
   const long long I = X0 + r.x, J = Y0 + r.y, K = Z0 + r.z;
   r.kxm = __ldg(w + ex_id(g, I - 1, J, K)) * g.ih1 * g.ih1;
   r.kxp = __ldg(w + ex_id(g, I, J, K)) * g.ih1 * g.ih1;
@@ -128,12 +138,12 @@ __device__ __forceinline__ double a_entry(const Geo& g, const Row& r, int i, int
 __device__ __forceinline__ double rhs_entry(const Geo& g, const Row& r, int cc) {
   if (!r.valid) return 0.0;
   double v = 0.0;
-  if (r.x == 1) v += r.kxm * hat_corner(cc, 0, r.y, r.z, g.b1, g.b2, g.b3);
-  if (r.x == g.ni1) v += r.kxp * hat_corner(cc, g.b1, r.y, r.z, g.b1, g.b2, g.b3);
-  if (r.y == 1) v += r.kym * hat_corner(cc, r.x, 0, r.z, g.b1, g.b2, g.b3);
-  if (r.y == g.ni2) v += r.kyp * hat_corner(cc, r.x, g.b2, r.z, g.b1, g.b2, g.b3);
-  if (r.z == 1) v += r.kzm * hat_corner(cc, r.x, r.y, 0, g.b1, g.b2, g.b3);
-  if (r.z == g.ni3) v += r.kzp * hat_corner(cc, r.x, r.y, g.b3, g.b1, g.b2, g.b3);
+  if (r.x == 1) v += r.kxm * hatf(g, cc, 0, r.y, r.z);
+  if (r.x == g.ni1) v += r.kxp * hatf(g, cc, g.b1, r.y, r.z);
+  if (r.y == 1) v += r.kym * hatf(g, cc, r.x, 0, r.z);
+  if (r.y == g.ni2) v += r.kyp * hatf(g, cc, r.x, g.b2, r.z);
+  if (r.z == 1) v += r.kzm * hatf(g, cc, r.x, r.y, 0);
+  if (r.z == g.ni3) v += r.kzp * hatf(g, cc, r.x, r.y, g.b3);
   return v;
 }
 
@@ -191,6 +201,9 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
            double* __restrict__ Ysc, double* __restrict__ Kloc, int* __restrict__ flags) {
   __shared__ double Dsh[TC_WARPS][64];
   __shared__ double Ish[TC_WARPS][64];
+  extern __shared__ int crd[];
+  fill_coords(g, crd);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int jb = blockIdx.x * TC_WARPS + wid;
   if (jb >= g.nbl) return;
@@ -216,7 +229,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 #pragma unroll
     for (int a = 0; a <= PT; ++a) {
       const int i = 8 * a + m;
-      Row rw = load_row(g, w, X0, Y0, Z0, i);
+      Row rw = load_row(g, w, crd, X0, Y0, Z0, i);
 #pragma unroll
       for (int b = 0; b <= PT; ++b) {
         if (b <= a) {
@@ -231,7 +244,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
     for (int J = 0; J < NTI; ++J) {
       // prefetch the stencil row entering the window at the end of this step
       const int inext = 8 * (J + 1 + PT) + m;
-      Row rn = load_row(g, w, X0, Y0, Z0, inext);
+      Row rn = load_row(g, w, crd, X0, Y0, Z0, inext);
 
       const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, rl, ql, flags);
       F2 X[PT + 1];
@@ -309,42 +322,41 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   }
 
   // ---- local Galerkin block: K = sum_e (w_e/h^2) dS_e dS_e^T as a DMMA reduction
+  // over the owned edges, 4 edges (k) x 8 corners (m, n) per instruction: lane
+  // (corner cc = lane/4, edge slot lane%4) supplies A[cc][e] = k_e dS_e[cc] and
+  // B[e][cc] = dS_e[cc].
   const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
-  const int ox = g.b1 * (g.b2 + ly) * (g.b3 + lz);
-  const int oy = (g.b1 + lx) * g.b2 * (g.b3 + lz);
-  const int oz = (g.b1 + lx) * (g.b2 + ly) * g.b3;
-  const int tot = ox + oy + oz;
   const bool has0 = (jb == 0);
-  const int cc = lane >> 2;
+  const int cc = lane >> 2, slot = lane & 3;
   const double* Sb = Sint + (size_t)jb * 8 * g.nI + (size_t)cc * g.nI;
+  auto sval = [&](int x, int y, int z) -> double {
+    const int a = interior_index(g, x, y, z);
+    if (a >= 0) return __ldcg(Sb + a);
+    if (has0 && x == 0 && y == 0 && z == 0) return 0.0;
+    return hatf(g, cc, x, y, z);
+  };
   F2 K = {0.0, 0.0};
-  for (int base = 0; base < tot; base += 4) {
-    const int f = base + (lane & 3);
-    double a = 0.0, b = 0.0;
-    if (f < tot) {
-      int ax, x, y, z;
-      long long e;
-      double ihs;
-      if (f < ox) {
-        ax = 0; x = f % g.b1; int r = f / g.b1; y = r % (g.b2 + ly); z = r / (g.b2 + ly);
-        e = ex_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih1 * g.ih1;
-      } else if (f < ox + oy) {
-        ax = 1; int q = f - ox; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % g.b2; z = r / g.b2;
-        e = ey_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih2 * g.ih2;
-      } else {
-        ax = 2; int q = f - ox - oy; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % (g.b2 + ly); z = r / (g.b2 + ly);
-        e = ez_id(g, X0 + x, Y0 + y, Z0 + z); ihs = g.ih3 * g.ih3;
+#pragma unroll 1
+  for (int ax = 0; ax < 3; ++ax) {
+    const int xm = g.b1 + (ax == 0 ? 0 : lx), ym = g.b2 + (ax == 1 ? 0 : ly), zm = g.b3 + (ax == 2 ? 0 : lz);
+    const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
+    for (int z = 0; z < zm; ++z) {
+      for (int y = 0; y < ym; ++y) {
+        for (int x0 = 0; x0 < xm; x0 += 4) {
+          const int x = x0 + slot;
+          double a = 0.0, b = 0.0;
+          if (x < xm) {
+            const long long e = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
+                                        : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
+            const double s0 = sval(x, y, z);
+            const double s1 = sval(x + (ax == 0), y + (ax == 1), z + (ax == 2));
+            b = s1 - s0;
+            a = (__ldg(w + e) * ihs) * b;
+          }
+          mma884(K.x, K.y, a, b);
+        }
       }
-      const int x1 = x + (ax == 0), y1 = y + (ax == 1), z1 = z + (ax == 2);
-      const int a0 = interior_index(g, x, y, z), a1 = interior_index(g, x1, y1, z1);
-      const double s0 = a0 >= 0 ? __ldcg(Sb + a0)
-                                : ((has0 && x == 0 && y == 0 && z == 0) ? 0.0
-                                                                        : hat_corner(cc, x, y, z, g.b1, g.b2, g.b3));
-      const double s1 = a1 >= 0 ? __ldcg(Sb + a1) : hat_corner(cc, x1, y1, z1, g.b1, g.b2, g.b3);
-      b = s1 - s0;
-      a = (__ldg(w + e) * ihs) * b;
     }
-    mma884(K.x, K.y, a, b);
   }
   Kloc[(size_t)jb * 64 + m * 8 + n0] = K.x;
   Kloc[(size_t)jb * 64 + m * 8 + n0 + 1] = K.y;
@@ -357,6 +369,9 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 template <int PT>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs) {
+  extern __shared__ int crd[];
+  fill_coords(g, crd);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int jb = blockIdx.x * TC_WARPS + wid;
   if (jb >= g.nbl) return;
@@ -366,8 +381,8 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
   const int m = lane >> 2, n0 = 2 * (lane & 3);
   auto node_of = [&](int a) -> long long {
-    const int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
-    return node_id(g, X0 + x, Y0 + y, Z0 + z);
+    const int c = crd[a];
+    return node_id(g, X0 + (c & 1023), Y0 + ((c >> 10) & 1023), Z0 + (c >> 20));
   };
   const double* LTb = LT + (size_t)jb * NTI * (PT + 1) * 64;
   for (int s0 = 0; s0 < nrhs; s0 += 8) {
@@ -455,7 +470,7 @@ template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc,
                                      double* Kloc, int* flags, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
-  k_basis_tc<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
+  k_basis_tc<PT><<<grid, TC_WARPS * 32, (size_t)g.nI * sizeof(int), st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -463,7 +478,7 @@ template <int PT>
 static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                      cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
-  k_block_solve_tc<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, LT, rhs, out, nrhs);
+  k_block_solve_tc<PT><<<grid, TC_WARPS * 32, (size_t)g.nI * sizeof(int), st>>>(g, LT, rhs, out, nrhs);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -196,7 +196,9 @@ class Engine:
         """In place: X (k, nrhs) contiguous device tensor."""
         assert X.is_contiguous() and X.shape[0] == self.k
         with phase("coarse_solve"):
-            _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), X.shape[1], stream()), "coarse_solve")
+            scratch = self.empty(max(self.k * X.shape[1], 1))
+            _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), ptr(scratch), X.shape[1], stream()),
+                       "coarse_solve")
         return X
 
     def receive(self, pts, Sint, Y=None, Xfield=None, nrhs=None):
@@ -256,9 +258,10 @@ class Engine:
     def cell_gradient(self, sigma, U, Z, Y, R):
         nrhs = U.shape[1]
         g = self.empty(self.Nm)
+        xi = self.empty(self.E)
         with phase("cell_gradient"):
-            _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs, ptr(g),
-                                                 stream()), "cell_gradient")
+            _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs,
+                                                 ptr(xi), ptr(g), stream()), "cell_gradient")
         return g
 
     def basis_csc(self, Sint, src, hatv):
