@@ -39,17 +39,13 @@ __global__ void k_edge_weights(Geo g, const double* __restrict__ cv, double* __r
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= g.E) return;
   int ax;
-  long long r;
-  long long i, j, k;
+  int i, j, k;
   if (e < g.Ex) {
-    ax = 0; r = e;
-    i = r % g.n1; r /= g.n1; j = r % (g.n2 + 1); k = r / (g.n2 + 1);
+    ax = 0; decode3(e, g.n1, g.n2 + 1, i, j, k);
   } else if (e < g.Ex + g.Ey) {
-    ax = 1; r = e - g.Ex;
-    i = r % (g.n1 + 1); r /= (g.n1 + 1); j = r % g.n2; k = r / g.n2;
+    ax = 1; decode3(e - g.Ex, g.n1 + 1, g.n2, i, j, k);
   } else {
-    ax = 2; r = e - g.Ex - g.Ey;
-    i = r % (g.n1 + 1); r /= (g.n1 + 1); j = r % (g.n2 + 1); k = r / (g.n2 + 1);
+    ax = 2; decode3(e - g.Ex - g.Ey, g.n1 + 1, g.n2 + 1, i, j, k);
   }
   double sum = 0.0;
   // transverse axes t1 < t2; outer loop on t2 (higher stride) gives ascending cell ids
@@ -452,9 +448,11 @@ __global__ void k_residual(Geo g, const double* __restrict__ src, double alpha,
   long long ii = t >> lg;
   const int j = (int)(t & ((1 << lg) - 1));
   if (ii >= (long long)g.nbl * g.nI) return;
-  int jb = (int)(ii / g.nI), a = (int)(ii % g.nI);
-  int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
-  int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
+  const int jb = (int)((unsigned)ii / (unsigned)g.nI), a = (int)((unsigned)ii - (unsigned)jb * (unsigned)g.nI);
+  int bi, bj, bk, x, y, z;
+  decode3(jb, g.nb1, g.nb2, bi, bj, bk);
+  decode3(a, g.ni1, g.ni2, x, y, z);
+  x += 1; y += 1; z += 1;
   long long I = (long long)bi * g.b1 + x, J = (long long)bj * g.b2 + y, K = (long long)bk * g.b3 + z;
   long long nd = node_id(g, I, J, K);
   const double c1 = g.ih1 * g.ih1, c2 = g.ih2 * g.ih2, c3 = g.ih3 * g.ih3;
@@ -480,35 +478,50 @@ __global__ void k_residual(Geo g, const double* __restrict__ src, double alpha,
   }
 }
 
-// field(node, s) = sum_cc S(node, cc) Y[col(cc), s]  (node 0 -> 0); a lane
-// group per node evaluates the node's S row once and strides over sources.
+// field(node, s) = sum_cc S(node, cc) Y[col(cc), s]  (node 0 -> 0).  A lane
+// group per node strides over the sources; with groups of >= 8 lanes each of
+// the first 8 lanes evaluates one corner of the node's S row and the group
+// shares them by shuffles.
 __global__ void k_prolong(Geo g, const double* __restrict__ Sint, const double* __restrict__ Y,
                           int nrhs, int lg, double* __restrict__ out) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long nd = t >> lg;
-  const int j = (int)(t & ((1 << lg) - 1));
+  const int G = 1 << lg;
+  const int j = (int)(t & (G - 1));
+  const bool valid = nd < g.Nn && nd > 0;
+  int bi = 0, bj = 0, bk = 0, x = 0, y = 0, z = 0;
+  if (valid) {
+    int I, J, K;
+    decode3(nd, g.n1 + 1, g.n2 + 1, I, J, K);
+    bi = own1i(I, g.b1, g.nb1); bj = own1i(J, g.b2, g.nb2); bk = own1i(K, g.b3, g.nb3);
+    x = I - bi * g.b1; y = J - bj * g.b2; z = K - bk * g.b3;
+  }
+  const double* Sb = Sint + (size_t)block_of(g, bi, bj, bk) * 8 * g.nI;
+  double sv[8];
+  int col[8];
+  if (G >= 8) {
+    const int my = j & 7;
+    const double s1 = valid ? s_value(g, Sb, my, x, y, z, false) : 0.0;
+    const int c1 = corner_col(g, bi, bj, bk, my);
+    const int base = (threadIdx.x & 31) & ~(G - 1);
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      sv[cc] = __shfl_sync(0xffffffffu, s1, base + cc);
+      col[cc] = __shfl_sync(0xffffffffu, c1, base + cc);
+    }
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      sv[cc] = valid ? s_value(g, Sb, cc, x, y, z, false) : 0.0;
+      col[cc] = corner_col(g, bi, bj, bk, cc);
+    }
+  }
   if (nd >= g.Nn) return;
   double* o = out + nd * nrhs;
-  if (nd == 0) {
-    for (int s = j; s < nrhs; s += (1 << lg)) o[s] = 0.0;
-    return;
-  }
-  long long I = nd % (g.n1 + 1), r = nd / (g.n1 + 1), J = r % (g.n2 + 1), K = r / (g.n2 + 1);
-  int bi = own1(I, g.b1, g.nb1), bj = own1(J, g.b2, g.nb2), bk = own1(K, g.b3, g.nb3);
-  int x = (int)(I - (long long)bi * g.b1), y = (int)(J - (long long)bj * g.b2), z = (int)(K - (long long)bk * g.b3);
-  int jb = block_of(g, bi, bj, bk);
-  const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  double sv[8];
-  const double* yc[8];
-#pragma unroll
-  for (int cc = 0; cc < 8; ++cc) {
-    sv[cc] = s_value(g, Sb, cc, x, y, z, false);
-    yc[cc] = Y + (size_t)corner_col(g, bi, bj, bk, cc) * nrhs;
-  }
-  for (int s = j; s < nrhs; s += (1 << lg)) {
+  for (int s = j; s < nrhs; s += G) {
     double v = 0.0;
 #pragma unroll
-    for (int cc = 0; cc < 8; ++cc) v += sv[cc] * __ldg(yc[cc] + s);
+    for (int cc = 0; cc < 8; ++cc) v += sv[cc] * __ldg(Y + (size_t)col[cc] * nrhs + s);
     o[s] = v;
   }
 }
@@ -590,8 +603,8 @@ __global__ void k_edge_xi(Geo g, const double* __restrict__ U, const double* __r
   long long nd = t >> lg;
   const int j = (int)(t & ((1 << lg) - 1));
   const bool valid = nd < g.Nn;
-  long long i = 0, jj = 0, k = 0;
-  if (valid) { i = nd % (g.n1 + 1); long long r = nd / (g.n1 + 1); jj = r % (g.n2 + 1); k = r / (g.n2 + 1); }
+  int i = 0, jj = 0, k = 0;
+  if (valid) decode3(nd, g.n1 + 1, g.n2 + 1, i, jj, k);
   const bool hx = valid && i < g.n1, hy = valid && jj < g.n2, hz = valid && k < g.n3;
   const long long nx = nd + 1, ny = nd + (g.n1 + 1), nz = nd + (long long)(g.n1 + 1) * (g.n2 + 1);
   double ax = 0.0, ay = 0.0, az = 0.0;
@@ -633,7 +646,8 @@ __global__ void k_cell_gather(Geo g, const double* __restrict__ sigma, const dou
                               double* __restrict__ gout) {
   long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (c >= g.Nm) return;
-  long long i = c % g.n1, r = c / g.n1, j = r % g.n2, k = r / g.n2;
+  int i, j, k;
+  decode3(c, g.n1, g.n2, i, j, k);
   double tot = 0.0;
   tot += xi[ex_id(g, i, j, k)] + xi[ex_id(g, i, j + 1, k)] + xi[ex_id(g, i, j, k + 1)] + xi[ex_id(g, i, j + 1, k + 1)];
   tot += xi[ey_id(g, i, j, k)] + xi[ey_id(g, i + 1, j, k)] + xi[ey_id(g, i, j, k + 1)] + xi[ey_id(g, i + 1, j, k + 1)];

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,9 +79,15 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.ih1 = 1.0 / h[0]; g.ih2 = 1.0 / h[1]; g.ih3 = 1.0 / h[2];
   g.qv = 0.25 * (h[0] * h[1] * h[2]);
   g.ib1 = 1.0 / g.b1; g.ib2 = 1.0 / g.b2; g.ib3 = 1.0 / g.b3;
+  {
+    // dense coarse L^{-1}: default up to COARSE_INV_MAX coarse nodes; MSFV_COARSE_INV=0/1 overrides
+    const char* ev = getenv("MSFV_COARSE_INV");
+    g.coarse_inv = ev ? (atoi(ev) != 0) : (g.kc <= COARSE_INV_MAX);
+  }
   if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
+  if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
   msfv_plan* pl = new msfv_plan;
   pl->g = g;
   *out = pl;

@@ -46,7 +46,7 @@ struct CoarseBufs {
 };
 
 __host__ __device__ __forceinline__ size_t band_tiles(const Geo& g) { return (size_t)g.NT * (g.PT + 1); }
-__host__ __device__ __forceinline__ bool coarse_has_inverse(const Geo& g) { return g.kc <= COARSE_INV_MAX; }
+__host__ __device__ __forceinline__ bool coarse_has_inverse(const Geo& g) { return g.coarse_inv != 0; }
 __host__ __device__ __forceinline__ size_t y_dim(const Geo& g) { return (size_t)g.NT * TB; }
 
 __host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double* base) {
@@ -165,55 +165,68 @@ __device__ __forceinline__ void gsub(double* G, size_t ld, double (*X)[TB + 1], 
   G[(r0 + 1) * ld + c0] -= a[2]; G[(r0 + 1) * ld + c0 + 1] -= a[3];
 }
 
-// Cholesky of diagonal tile J (in A) -> L_JJ (Lo slot 0) and L_JJ^{-1} (Dinv).
+// Cholesky of diagonal tile J (in A) -> L_JJ (Lo slot 0) and L_JJ^{-1} (Dinv),
+// by warp 0 alone: lane r owns row r of L in registers (right-looking with
+// shuffles; compile-time unrolled by template recursion so the row stays in
+// registers), then lane c owns column c of L^{-1} (forward substitution with
+// broadcast shared-memory reads of L).  rsqrt keeps the pivot chain short.
+template <int C>
+__device__ __forceinline__ void potrf_row_step(double (&x)[TB], double& invd, int r, bool& bad) {
+  if constexpr (C < TB) {
+    double d = __shfl_sync(0xffffffffu, x[C], C);
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    const double inv = rsqrt(d);
+    if (r > C) x[C] *= inv;
+    if (r == C) { x[C] = d * inv; invd = inv; }
+    const double lrc = x[C];
+#pragma unroll
+    for (int q = C + 1; q < TB; ++q) {
+      const double lqc = __shfl_sync(0xffffffffu, lrc, q);
+      if (r >= q) x[q] -= lrc * lqc;
+    }
+    potrf_row_step<C + 1>(x, invd, r, bad);
+  }
+}
+template <int R>
+__device__ __forceinline__ void inv_col_step(double (&d)[TB], int c, const double (*P)[TB + 1], const double* invd) {
+  if constexpr (R < TB) {
+    double a0 = (R == c) ? 1.0 : 0.0, a1 = 0.0;
+#pragma unroll
+    for (int m = 0; m + 1 < R; m += 2) {
+      a0 -= P[R][m] * d[m];
+      a1 -= P[R][m + 1] * d[m + 1];
+    }
+    if (R & 1) a0 -= P[R][R - 1] * d[R - 1];
+    d[R] = (R < c) ? 0.0 : (a0 + a1) * invd[R];
+    inv_col_step<R + 1>(d, c, P, invd);
+  }
+}
+
 __device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flags, FactorSmem& sm) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
   auto& P = sm.P;
+  auto& D = sm.D;
   load_tile(P, tile(B.A, g, J, 0));
   __syncthreads();
-  if (tid < 32) {       // warp 0: lane r holds row r in registers
+  if (tid < 32) {
     const int r = tid;
     double x[TB];
 #pragma unroll
     for (int q = 0; q < TB; ++q) x[q] = P[r][q];
-#pragma unroll
-    for (int c = 0; c < TB; ++c) {
-      double d = __shfl_sync(0xffffffffu, x[c], c);
-      if (!(d > 0.0)) {
-        if (r == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
-        d = 1.0;
-      }
-      const double piv = sqrt(d), inv = 1.0 / piv;
-      if (r > c) x[c] *= inv;
-      if (r == c) x[c] = piv;
-      const double lrc = x[c];
-#pragma unroll
-      for (int q = c + 1; q < TB; ++q) {
-        const double lqc = __shfl_sync(0xffffffffu, lrc, q);
-        if (r >= q) x[q] -= lrc * lqc;
-      }
-    }
+    double invd = 1.0;
+    bool bad = false;
+    potrf_row_step<0>(x, invd, r, bad);
+    if (bad && r == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
 #pragma unroll
     for (int q = 0; q < TB; ++q) P[r][q] = q <= r ? x[q] : 0.0;
-  }
-  auto& D = sm.D;
-  for (int t = tid; t < TT; t += nt) D[t / TB][t % TB] = 0.0;
-  __syncthreads();
-  // L^{-1} row by row: D[r][c] = (delta_rc - sum_{c<=m<r} L[r][m] D[m][c]) / L[r][r]
-  const int c = tid & 31, part = tid >> 5;
-  for (int r = 0; r < TB; ++r) {
-    double s = 0.0;
-    for (int m = c + part; m < r; m += 8) s += P[r][m] * D[m][c];
-    sm.R[part][c] = s;
-    __syncthreads();
-    if (tid < 32 && c <= r) {
-      double tot = 0.0;
+    sm.Q[0][r] = invd;                // 1 / L[r][r]
+    __syncwarp();
+    double d[TB];
+    inv_col_step<0>(d, r, P, sm.Q[0]);
 #pragma unroll
-      for (int p = 0; p < 8; ++p) tot += sm.R[p][c];
-      D[r][c] = ((r == c ? 1.0 : 0.0) - tot) / P[r][r];
-    }
-    __syncthreads();
+    for (int rr = 0; rr < TB; ++rr) D[rr][r] = d[rr];
   }
+  __syncthreads();
   store_tile(B.Dinv + (size_t)J * TT, D);
   store_tile(tile(B.Lo, g, J, 0), P);
   __syncthreads();
@@ -286,16 +299,18 @@ __global__ void __launch_bounds__(256) k_coarse_factor(Geo g, double* __restrict
     const int ntasks = npairs + (withY ? J + 1 : 0);
     load_tile(sm.D, B.Dinv + (size_t)J * TT);
     __syncthreads();
-    int start = blockIdx.x;
     if (blockIdx.x == 0 && pt >= 1) {
       coarse_task(g, J, 0, npairs, B, sm);       // pair (1,1): next diagonal tile
       __threadfence_block();
       coarse_potrf(g, J + 1, B, flags, sm);      // lookahead factor of column J+1
-      load_tile(sm.D, B.Dinv + (size_t)J * TT);
-      __syncthreads();
-      start = gridDim.x;
     }
-    for (int f = start; f < ntasks; f += gridDim.x) coarse_task(g, J, f, npairs, B, sm);
+    // the other CTAs share everything except the lookahead pair
+    const int first = (pt >= 1) ? 1 : 0;
+    const int nw = gridDim.x > 1 ? gridDim.x - 1 : 1;
+    if (gridDim.x == 1 || blockIdx.x > 0) {
+      const int me = gridDim.x > 1 ? blockIdx.x - 1 : 0;
+      for (int f = first + me; f < ntasks; f += nw) coarse_task(g, J, f, npairs, B, sm);
+    }
     grid.sync();
   }
 }
@@ -551,6 +566,266 @@ __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __rest
   }
 }
 
+// Step-buffered variant: all PT+1 factor tiles of a column step are staged
+// in shared memory at once (double-buffered with cp.async one step ahead; row
+// stride TB+2 doubles to avoid bank conflicts), so each step is two
+// barrier-separated GEMV phases over all 256 threads.
+constexpr int TS = TB + 2;            // padded smem row stride (16-byte granules)
+constexpr int TTS = TB * TS;
+template <int RC>
+__global__ void __launch_bounds__(256) k_coarse_trsv_step(Geo g, const double* __restrict__ Lk,
+                                                          const double* __restrict__ Dinv, double* __restrict__ X,
+                                                          int nrhs) {
+  extern __shared__ __align__(16) double tsm[];
+  const int W = g.PT + 1;
+  double* buf[2] = {tsm, tsm + (size_t)W * TTS};                // slot 0 = Dinv_J, slot t = L_{J+t,J}
+  double* Xw = tsm + (size_t)2 * W * TTS;                         // [PT+1][TB][RC] rhs ring
+  double* Ys = Xw + (size_t)W * TB * RC;                          // [TB][RC]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int s0 = blockIdx.x * RC;
+  const int ns = min(RC, nrhs - s0);
+  auto cp_tile = [&](double* dst, const double* src) {
+    for (int i = tid; i < TT / 2; i += nt) {
+      const int r = (2 * i) / TB, c = (2 * i) % TB;
+      cpa16(dst + r * TS + c, src + 2 * i);
+    }
+  };
+  auto issue = [&](int J, double* dst) {
+    if (J >= 0 && J < g.NT) {
+      const int pt = min(g.PT, g.NT - 1 - J);
+      cp_tile(dst, Dinv + (size_t)J * TT);
+      for (int t = 1; t <= pt; ++t) cp_tile(dst + (size_t)t * TTS, tile(Lk, g, J, t));
+    }
+    cpa_commit();
+  };
+  auto load_rows = [&](int I, double* dst) {
+    for (int t = tid; t < TB * RC; t += nt) {
+      int r = t / RC, s = t % RC, row = I * TB + r;
+      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+    }
+  };
+  // ---------------- forward: y_J = Dinv_J x_J ; x_{J+t} -= L_{J+t,J} y_J
+  issue(0, buf[0]);
+  issue(1, buf[1]);
+  for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
+  for (int J = 0; J < g.NT; ++J) {
+    const int pt = min(g.PT, g.NT - 1 - J);
+    double* T = buf[J & 1];
+    cpa_wait<1>();
+    __syncthreads();
+    const double* xj = Xw + (size_t)(J % W) * TB * RC;
+    for (int q = tid; q < TB * RC; q += nt) {
+      const int r = q / RC, s = q % RC;
+      const double* tr = T + r * TS;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < TB; c += 2) { v0 += tr[c] * xj[c * RC + s]; v1 += tr[c + 1] * xj[(c + 1) * RC + s]; }
+      const double v = v0 + v1;
+      Ys[q] = v;
+      const int row = J * TB + r;
+      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
+    }
+    __syncthreads();
+    for (int q = tid; q < pt * TB * RC; q += nt) {
+      const int tt = 1 + q / (TB * RC), rem = q % (TB * RC), r = rem / RC, s = rem % RC;
+      const double* L = T + (size_t)tt * TTS + r * TS;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < TB; c += 2) { v0 += L[c] * Ys[c * RC + s]; v1 += L[c + 1] * Ys[(c + 1) * RC + s]; }
+      Xw[(size_t)((J + tt) % W) * TB * RC + rem] -= v0 + v1;
+    }
+    __syncthreads();
+    load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);
+    issue(J + 2, buf[J & 1]);
+  }
+  cpa_wait<0>();
+  __syncthreads();
+  // ---------------- backward: x_J = Dinv_J^T (y_J - sum_t L_{J+t,J}^T x_{J+t})
+  issue(g.NT - 1, buf[0]);
+  issue(g.NT - 2, buf[1]);
+  constexpr int SPLIT = 256 / (TB * RC) > 0 ? 256 / (TB * RC) : 1;   // threads per output
+  for (int it = 0; it < g.NT; ++it) {
+    const int J = g.NT - 1 - it;
+    const int pt = min(g.PT, g.NT - 1 - J);
+    double* T = buf[it & 1];
+    cpa_wait<1>();
+    __syncthreads();
+    {
+      const int q = tid / SPLIT, part = tid % SPLIT;
+      double v0 = 0.0, v1 = 0.0;
+      if (q < TB * RC) {
+        const int c = q / RC, s = q % RC;
+        for (int tt = 1 + part; tt <= pt; tt += SPLIT) {
+          const double* L = T + (size_t)tt * TTS + c;
+          const double* xt = Xw + (size_t)((J + tt) % W) * TB * RC + s;
+#pragma unroll 8
+          for (int r = 0; r < TB; r += 2) { v0 += L[r * TS] * xt[r * RC]; v1 += L[(r + 1) * TS] * xt[(r + 1) * RC]; }
+        }
+      }
+      double v = v0 + v1;
+#pragma unroll
+      for (int off = SPLIT / 2; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off, SPLIT);
+      if (q < TB * RC && part == 0) {
+        const int c = q / RC, s = q % RC, row = J * TB + c;
+        const double y = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+        Ys[q] = y - v;
+      }
+    }
+    __syncthreads();
+    double* xo = Xw + (size_t)(J % W) * TB * RC;
+    for (int q = tid; q < TB * RC; q += nt) {
+      const int r = q / RC, s = q % RC, row = J * TB + r;
+      double v = 0.0;
+      for (int c = r; c < TB; ++c) v += T[c * TS + r] * Ys[c * RC + s];
+      if (row >= g.kc || s >= ns) v = 0.0;
+      xo[q] = v;
+      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
+    }
+    __syncthreads();
+    issue(J - 2, buf[it & 1]);
+  }
+  cpa_wait<0>();
+}
+
+// FP64 tensor-core (DMMA m8n8k4) variant of the step-buffered solve: 8
+// right-hand sides per CTA (one n8 tile), 8 warps.  Per column step the
+// tile GEMVs become m8n8k4 MMAs fed from the padded shared-memory tiles.
+namespace {
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_coarse_trsv_tc(Geo g, const double* __restrict__ Lk,
+                                                        const double* __restrict__ Dinv, double* __restrict__ X,
+                                                        int nrhs) {
+  constexpr int RC = 8;
+  extern __shared__ __align__(16) double tsm[];
+  const int W = g.PT + 1;
+  double* buf[2] = {tsm, tsm + (size_t)W * TTS};                // slot 0 = Dinv_J, slot t = L_{J+t,J}
+  double* Xw = tsm + (size_t)2 * W * TTS;                         // [PT+1][TB][RC] rhs ring (row-major)
+  double* Ys = Xw + (size_t)W * TB * RC;                          // [TB][RC]
+  double* Pt = Ys + TB * RC;                                      // [8 warps][64] partial accumulators
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int s0 = blockIdx.x * RC;
+  const int ns = min(RC, nrhs - s0);
+  const int gm = lane >> 2, gk = lane & 3, cn = 2 * (lane & 3);   // fragment coordinates
+  auto cp_tile = [&](double* dst, const double* src) {
+    for (int i = tid; i < TT / 2; i += nt) {
+      const int r = (2 * i) / TB, c = (2 * i) % TB;
+      cpa16(dst + r * TS + c, src + 2 * i);
+    }
+  };
+  auto issue = [&](int J, double* dst) {
+    if (J >= 0 && J < g.NT) {
+      const int pt = min(g.PT, g.NT - 1 - J);
+      cp_tile(dst, Dinv + (size_t)J * TT);
+      for (int t = 1; t <= pt; ++t) cp_tile(dst + (size_t)t * TTS, tile(Lk, g, J, t));
+    }
+    cpa_commit();
+  };
+  auto load_rows = [&](int I, double* dst) {
+    for (int t = tid; t < TB * RC; t += nt) {
+      int r = t / RC, s = t % RC, row = I * TB + r;
+      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
+    }
+  };
+  // C(8x8 tile mi of a [32][RC] block) += op(T)(rows 8mi..) * B(32 x RC block);  T in smem (stride TS)
+  auto mma_rows = [&](double& c0, double& c1, const double* T, bool trans, int mi, const double* Bm, double sign) {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = 4 * kk + gk;
+      const double a = trans ? T[k * TS + 8 * mi + gm] : T[(8 * mi + gm) * TS + k];
+      const double b = Bm[k * RC + gm];              // B[k][n] with n = gm
+      dmma(c0, c1, sign * a, b);
+    }
+  };
+  // ---------------- forward
+  issue(0, buf[0]);
+  issue(1, buf[1]);
+  for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
+  for (int J = 0; J < g.NT; ++J) {
+    const int pt = min(g.PT, g.NT - 1 - J);
+    const double* T = buf[J & 1];
+    cpa_wait<1>();
+    __syncthreads();
+    if (wid < 4) {                                   // y_J = Dinv_J x_J
+      double c0 = 0.0, c1 = 0.0;
+      mma_rows(c0, c1, T, false, wid, Xw + (size_t)(J % W) * TB * RC, 1.0);
+      const int r = 8 * wid + gm;
+      Ys[r * RC + cn] = c0;
+      Ys[r * RC + cn + 1] = c1;
+      const int row = J * TB + r;
+      if (row < g.kc) {
+        if (cn < ns) X[(size_t)row * nrhs + s0 + cn] = c0;
+        if (cn + 1 < ns) X[(size_t)row * nrhs + s0 + cn + 1] = c1;
+      }
+    }
+    __syncthreads();
+    for (int item = wid; item < pt * 4; item += 8) {  // x_{J+t} -= L_{J+t,J} y_J
+      const int tt = 1 + item / 4, mi = item % 4;
+      double* xt = Xw + (size_t)((J + tt) % W) * TB * RC;
+      const int r = 8 * mi + gm;
+      double c0 = xt[r * RC + cn], c1 = xt[r * RC + cn + 1];
+      mma_rows(c0, c1, T + (size_t)tt * TTS, false, mi, Ys, -1.0);
+      xt[r * RC + cn] = c0;
+      xt[r * RC + cn + 1] = c1;
+    }
+    __syncthreads();
+    load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);
+    issue(J + 2, buf[J & 1]);
+  }
+  cpa_wait<0>();
+  __syncthreads();
+  // ---------------- backward
+  issue(g.NT - 1, buf[0]);
+  issue(g.NT - 2, buf[1]);
+  for (int it = 0; it < g.NT; ++it) {
+    const int J = g.NT - 1 - it;
+    const int pt = min(g.PT, g.NT - 1 - J);
+    const double* T = buf[it & 1];
+    cpa_wait<1>();
+    __syncthreads();
+    {                                                // partial sums of L_{J+t,J}^T x_{J+t}
+      const int mi = wid & 3, half = wid >> 2;
+      double c0 = 0.0, c1 = 0.0;
+      for (int tt = 1 + half; tt <= pt; tt += 2)
+        mma_rows(c0, c1, T + (size_t)tt * TTS, true, mi, Xw + (size_t)((J + tt) % W) * TB * RC, 1.0);
+      Pt[wid * 64 + lane * 2] = c0;
+      Pt[wid * 64 + lane * 2 + 1] = c1;
+    }
+    __syncthreads();
+    if (wid < 4) {
+      const int r = 8 * wid + gm, row = J * TB + r;
+      double y0 = 0.0, y1 = 0.0;
+      if (row < g.kc) {
+        if (cn < ns) y0 = X[(size_t)row * nrhs + s0 + cn];
+        if (cn + 1 < ns) y1 = X[(size_t)row * nrhs + s0 + cn + 1];
+      }
+      Ys[r * RC + cn] = y0 - Pt[wid * 64 + lane * 2] - Pt[(wid + 4) * 64 + lane * 2];
+      Ys[r * RC + cn + 1] = y1 - Pt[wid * 64 + lane * 2 + 1] - Pt[(wid + 4) * 64 + lane * 2 + 1];
+    }
+    __syncthreads();
+    if (wid < 4) {                                   // x_J = Dinv_J^T acc
+      double c0 = 0.0, c1 = 0.0;
+      mma_rows(c0, c1, T, true, wid, Ys, 1.0);
+      const int r = 8 * wid + gm, row = J * TB + r;
+      if (row >= g.kc) { c0 = 0.0; c1 = 0.0; }
+      double* xo = Xw + (size_t)(J % W) * TB * RC;
+      xo[r * RC + cn] = cn < ns ? c0 : 0.0;
+      xo[r * RC + cn + 1] = cn + 1 < ns ? c1 : 0.0;
+      if (row < g.kc) {
+        if (cn < ns) X[(size_t)row * nrhs + s0 + cn] = c0;
+        if (cn + 1 < ns) X[(size_t)row * nrhs + s0 + cn + 1] = c1;
+      }
+    }
+    __syncthreads();
+    issue(J - 2, buf[it & 1]);
+  }
+  cpa_wait<0>();
+}
+
 // ------------------------------------------------------------- launchers
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -604,6 +879,24 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
     return cudaGetLastError();
   }
   constexpr int RC = 4;
+  const size_t step_smem = ((size_t)3 * (g.PT + 1) * TT / TB * TB + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
+  const size_t smem_s = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
+  (void)step_smem;
+  const size_t smem_tc = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * 8 + 8 * 64) * sizeof(double);
+  if (smem_tc <= 220 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc);
+    if (e != cudaSuccess) return e;
+    k_coarse_trsv_tc<<<nblk(nrhs, 8), 256, smem_tc, st>>>(g, B.Lo, B.Dinv, X, nrhs);
+    count_launches(1);
+    return cudaGetLastError();
+  }
+  if (smem_s <= 200 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_step<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+    if (e != cudaSuccess) return e;
+    k_coarse_trsv_step<RC><<<nblk(nrhs, RC), 256, smem_s, st>>>(g, B.Lo, B.Dinv, X, nrhs);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   size_t smem = ((size_t)4 * TT + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

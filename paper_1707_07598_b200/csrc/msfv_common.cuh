@@ -39,6 +39,7 @@ struct Geo {
   double ih1, ih2, ih3;    // 1/h per axis (as the reference's 1.0/h)
   double qv;               // 0.25 * cell volume (operators.py:83)
   double ib1, ib2, ib3;    // 1/b per axis (device-side hats)
+  int coarse_inv;          // 1: keep a dense L^{-1} of the coarse factor for the solves
 };
 
 __host__ __device__ __forceinline__ long long node_id(const Geo& g, long long i, long long j, long long k) {
@@ -94,6 +95,21 @@ __device__ __forceinline__ double hatf(const Geo& g, int cc, int x, int y, int z
 __host__ __device__ __forceinline__ int own1(long long X, int b, int nb) {
   long long q = X / b;
   return (int)(q < nb - 1 ? q : nb - 1);
+}
+
+// 32-bit decode of a linear index (all index spaces here are < 2^31; 64-bit
+// division is a long instruction sequence on the GPU).
+__host__ __device__ __forceinline__ void decode3(long long idx, int d1, int d2, int& i, int& j, int& k) {
+  const unsigned u = (unsigned)idx;
+  const unsigned q = u / (unsigned)d1;
+  i = (int)(u - q * (unsigned)d1);
+  const unsigned q2 = q / (unsigned)d2;
+  j = (int)(q - q2 * (unsigned)d2);
+  k = (int)q2;
+}
+__host__ __device__ __forceinline__ int own1i(int X, int b, int nb) {
+  const int q = (int)((unsigned)X / (unsigned)b);
+  return q < nb - 1 ? q : nb - 1;
 }
 
 __host__ __device__ __forceinline__ int block_of(const Geo& g, int bi, int bj, int bk) {

@@ -147,42 +147,63 @@ __device__ __forceinline__ double rhs_entry(const Geo& g, const Row& r, int cc) 
   return v;
 }
 
-// Cholesky of one 8x8 SPD tile (accumulator layout) in per-warp shared
-// memory; returns L^{-1} as an A-frag.  Lane (rq) owns one strictly-lower
-// trailing entry (r, q) of the rank-1 updates.
-__device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, int lane, int rl, int ql,
-                                         int* flags) {
+// Cholesky of one 8x8 SPD tile (accumulator layout); returns L^{-1} as an
+// A-frag.  Lanes 0..7 own rows of L in registers (shuffle right-looking
+// factorization, rsqrt pivots), then columns of L^{-1}; shared memory is used
+// only to re-layout the tile.
+template <int C>
+__device__ __forceinline__ void p8_step(double (&x)[8], double& invd, int r, bool& bad) {
+  if constexpr (C < 8) {
+    double d = __shfl_sync(FULL, x[C], C);
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    const double inv = rsqrt(d);
+    if (r > C) x[C] *= inv;
+    if (r == C) { x[C] = d * inv; invd = inv; }
+    const double lrc = x[C];
+#pragma unroll
+    for (int q = C + 1; q < 8; ++q) {
+      const double lqc = __shfl_sync(FULL, lrc, q);
+      if (r >= q) x[q] -= lrc * lqc;
+    }
+    p8_step<C + 1>(x, invd, r, bad);
+  }
+}
+template <int R>
+__device__ __forceinline__ void i8_step(double (&d)[8], int c, const double* Ds, const double* invd) {
+  if constexpr (R < 8) {
+    double acc = (R == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < R; ++m) acc -= Ds[R * 8 + m] * d[m];
+    d[R] = (R < c) ? 0.0 : acc * invd[R];
+    i8_step<R + 1>(d, c, Ds, invd);
+  }
+}
+
+__device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, int lane, int* flags) {
   const int m = lane >> 2, n0 = 2 * (lane & 3);
   Ds[m * 8 + n0] = t.x;
   Ds[m * 8 + n0 + 1] = t.y;
   __syncwarp();
+  const int r = lane & 7;
+  double x[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    double d = Ds[c * 9];
-    if (!(d > 0.0)) {
-      if (lane == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
-      d = 1.0;
-    }
-    const double piv = sqrt(d), inv = 1.0 / piv;
-    __syncwarp();
-    if (lane > c && lane < 8) Ds[lane * 8 + c] *= inv;
-    if (lane == c) Ds[c * 9] = piv;
-    __syncwarp();
-    if (ql > c) Ds[rl * 8 + ql] -= Ds[rl * 8 + c] * Ds[ql * 8 + c];
-    __syncwarp();
-  }
+  for (int q = 0; q < 8; ++q) x[q] = Ds[r * 8 + q];
+  bool bad = false;
+  double invd = 1.0;
+  p8_step<0>(x, invd, r, bad);
+  if (bad && lane == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
+  __syncwarp();
   if (lane < 8) {
-    const int c = lane;
-    double x[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      double v = (r == c) ? 1.0 : 0.0;
+    for (int q = 0; q < 8; ++q) Ds[r * 8 + q] = x[q];
+    Is[64 + r] = invd;
+  }
+  __syncwarp();
+  if (lane < 8) {
+    double d[8];
+    i8_step<0>(d, lane, Ds, Is + 64);
 #pragma unroll
-      for (int q = 0; q < r; ++q) v -= Ds[r * 8 + q] * x[q];
-      x[r] = (r < c) ? 0.0 : v / Ds[r * 9];
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) Is[r * 8 + c] = x[r];
+    for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = d[rr];
   }
   __syncwarp();
   const int k = lane & 3;
@@ -200,11 +221,13 @@ __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
            double* __restrict__ Ysc, double* __restrict__ Kloc, int* __restrict__ flags) {
   __shared__ double Dsh[TC_WARPS][64];
-  __shared__ double Ish[TC_WARPS][64];
-  extern __shared__ int crd[];
+  __shared__ double Ish[TC_WARPS][72];
+  extern __shared__ __align__(16) double tcsm[];
+  int* crd = reinterpret_cast<int*>(tcsm + (size_t)TC_WARPS * g.nI * 8);
   fill_coords(g, crd);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Sx = tcsm + (size_t)wid * g.nI * 8;     // this block's interior basis values [a][corner]
   const int jb = blockIdx.x * TC_WARPS + wid;
   if (jb >= g.nbl) return;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
@@ -213,15 +236,17 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   const int m = lane >> 2, n0 = 2 * (lane & 3);
   double* Ds = Dsh[wid];
   double* Is = Ish[wid];
-  // this lane's fixed strictly-lower (r, q) entry of the 8x8 rank-1 updates
-  int rl = 0, ql = -1;   // lanes 28..31 own no entry
+  // tile offsets (I - K) that can hold stencil entries: d in {0, 1, ni1, p}
+  unsigned omask = 1u;
   {
-    int idx = 0;
-    for (int r = 1; r < 8; ++r)
-      for (int q = 1; q <= r; ++q, ++idx)
-        if (idx == lane) { rl = r; ql = q; }
+    const int ds[3] = {g.ni1 >= 2 ? 1 : 0, g.ni2 >= 2 ? g.ni1 : 0, g.ni3 >= 2 ? g.p : 0};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int d = ds[q];
+      if (d <= 0) continue;
+      for (int o = (d - 7 + 7) / 8; o <= (d + 7) / 8; ++o) omask |= 1u << o;
+    }
   }
-
   if (NTI > 0) {
     F2 W[PT + 1][PT + 1];
     F2 R[PT + 1];
@@ -232,7 +257,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       Row rw = load_row(g, w, crd, X0, Y0, Z0, i);
 #pragma unroll
       for (int b = 0; b <= PT; ++b) {
-        if (b <= a) {
+        if (b <= a && ((omask >> (a - b)) & 1u)) {
           const int l = 8 * b + n0;
           W[a][b] = {a_entry(g, rw, i, l), a_entry(g, rw, i, l + 1)};
         } else {
@@ -246,7 +271,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       const int inext = 8 * (J + 1 + PT) + m;
       Row rn = load_row(g, w, crd, X0, Y0, Z0, inext);
 
-      const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, rl, ql, flags);
+      const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, flags);
       F2 X[PT + 1];
 #pragma unroll
       for (int t = 1; t <= PT; ++t) {
@@ -288,85 +313,172 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
         const int In = J + 1 + PT;
 #pragma unroll
         for (int b = 0; b <= PT; ++b) {
-          const int l = 8 * (In - PT + b) + n0;
-          W[PT][b] = {a_entry(g, rn, inext, l), a_entry(g, rn, inext, l + 1)};
+          if ((omask >> (PT - b)) & 1u) {
+            const int l = 8 * (In - PT + b) + n0;
+            W[PT][b] = {a_entry(g, rn, inext, l), a_entry(g, rn, inext, l + 1)};
+          } else {
+            W[PT][b] = {0.0, 0.0};
+          }
         }
         R[PT] = {rhs_entry(g, rn, n0), rhs_entry(g, rn, n0 + 1)};
       }
     }
     __syncwarp();
-    // ---- backward substitution L^T x = y, window of solved tiles as B-frags
+    // ---- backward substitution L^T x = y, window of solved tiles as B-frags;
+    // the next step's factor tiles are prefetched into registers.
     F2 Xw[PT > 0 ? PT : 1];
 #pragma unroll
     for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
-    for (int J = NTI - 1; J >= 0; --J) {
+    F2 nLt[PT + 1], nY;
+    {
+      const int J = NTI - 1;
       const double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
-      F2 acc = ld2cg(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2);
+#pragma unroll
+      for (int t = 0; t <= PT; ++t) nLt[t] = (t == 0 || J + t < NTI) ? ld2cg(Lt + t * 64 + lane * 2) : F2{0.0, 0.0};
+      nY = ld2cg(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2);
+    }
+    for (int J = NTI - 1; J >= 0; --J) {
+      F2 cLt[PT + 1];
+#pragma unroll
+      for (int t = 0; t <= PT; ++t) cLt[t] = nLt[t];
+      F2 acc = nY;
+      if (J > 0) {
+        const double* Lt = LT + ((size_t)jb * NTI + J - 1) * (PT + 1) * 64;
+#pragma unroll
+        for (int t = 0; t <= PT; ++t) nLt[t] = (t == 0 || J - 1 + t < NTI) ? ld2cg(Lt + t * 64 + lane * 2) : F2{0.0, 0.0};
+        nY = ld2cg(Ysc + ((size_t)jb * NTI + J - 1) * 64 + lane * 2);
+      }
 #pragma unroll
       for (int t = 1; t <= PT; ++t) {
-        if (J + t < NTI) mma(acc, neg(a_to_t(ld2cg(Lt + t * 64 + lane * 2), lane)), Xw[t - 1]);
+        if (J + t < NTI) mma(acc, neg(a_to_t(cLt[t], lane)), Xw[t - 1]);
       }
       F2 xj = {0.0, 0.0};
-      mma(xj, a_to_t(ld2cg(Lt + lane * 2), lane), c_to_b(acc, lane));
+      mma(xj, a_to_t(cLt[0], lane), c_to_b(acc, lane));
       const int a0 = 8 * J + m;
       if (a0 < g.nI) {
         Sint[((size_t)jb * 8 + n0) * g.nI + a0] = xj.x;
         Sint[((size_t)jb * 8 + n0 + 1) * g.nI + a0] = xj.y;
+        st2(Sx + a0 * 8 + n0, xj);
       }
 #pragma unroll
       for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
       if (PT > 0) Xw[0] = c_to_b(xj, lane);
     }
     __syncwarp();
-    __threadfence_block();
   }
 
-  // ---- local Galerkin block: K = sum_e (w_e/h^2) dS_e dS_e^T as a DMMA reduction
-  // over the owned edges, 4 edges (k) x 8 corners (m, n) per instruction: lane
-  // (corner cc = lane/4, edge slot lane%4) supplies A[cc][e] = k_e dS_e[cc] and
-  // B[e][cc] = dS_e[cc].
+  // ---- local Galerkin block K_j = sum_{owned e} (w_e/h^2) dS_e dS_e^T (interior part).
+  // Edges touching the interior contribute S_I^T(A S)_I + S_B^T(A^I S)_B and
+  // (A S)_I = 0 is the local problem just solved, so only the boundary-interior
+  // edges remain: k_e S(x_e) (S(x_e) - S(i_e))^T.  Skeleton-only owned edges
+  // contribute k_e dH dH^T with the model-independent hats.  DMMA reduction,
+  // 4 edges (k) x 8 corners per instruction: lane (corner cc = lane/4, edge
+  // slot lane%4).
   const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
   const bool has0 = (jb == 0);
   const int cc = lane >> 2, slot = lane & 3;
-  const double* Sb = Sint + (size_t)jb * 8 * g.nI + (size_t)cc * g.nI;
-  auto sval = [&](int x, int y, int z) -> double {
-    const int a = interior_index(g, x, y, z);
-    if (a >= 0) return __ldcg(Sb + a);
-    if (has0 && x == 0 && y == 0 && z == 0) return 0.0;
-    return hatf(g, cc, x, y, z);
-  };
   F2 K = {0.0, 0.0};
+  // (1) boundary-interior edges, face by face
 #pragma unroll 1
+  for (int face = 0; face < 6; ++face) {
+    const int ax = face >> 1, hi = face & 1;
+    const int nu = ax == 0 ? g.ni2 : g.ni1, nv = ax == 2 ? g.ni2 : g.ni3;
+    const int tot = nu * nv;
+    const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
+    for (int base = 0; base < tot; base += 4) {
+      const int f = base + slot;
+      double a = 0.0, b = 0.0;
+      if (f < tot) {
+        const int u = 1 + f % nu, v = 1 + f / nu;
+        int xb, yb, zb, xi, yi, zi, xe, ye, ze;
+        if (ax == 0) {
+          xb = hi ? g.b1 : 0; yb = u; zb = v; xi = hi ? g.b1 - 1 : 1; yi = u; zi = v;
+        } else if (ax == 1) {
+          xb = u; yb = hi ? g.b2 : 0; zb = v; xi = u; yi = hi ? g.b2 - 1 : 1; zi = v;
+        } else {
+          xb = u; yb = v; zb = hi ? g.b3 : 0; xi = u; yi = v; zi = hi ? g.b3 - 1 : 1;
+        }
+        xe = min(xb, xi); ye = min(yb, yi); ze = min(zb, zi);
+        const long long e = ax == 0 ? ex_id(g, X0 + xe, Y0 + ye, Z0 + ze)
+                                    : (ax == 1 ? ey_id(g, X0 + xe, Y0 + ye, Z0 + ze) : ez_id(g, X0 + xe, Y0 + ye, Z0 + ze));
+        const double sb = hatf(g, cc, xb, yb, zb);
+        const double si = Sx[interior_index(g, xi, yi, zi) * 8 + cc];
+        b = sb - si;
+        a = (__ldg(w + e) * ihs) * sb;
+      }
+      mma884(K.x, K.y, a, b);
+    }
+  }
+  // (2) skeleton-only owned edges: added by k_skel_galerkin (model-independent hats)
+  Kloc[(size_t)jb * 64 + m * 8 + n0] = K.x;
+  Kloc[(size_t)jb * 64 + m * 8 + n0 + 1] = K.y;
+}
+
+// ------------------------------------------------------- skeleton Galerkin
+
+// Kloc[j] += sum over the skeleton-only edges owned by block j of
+// (w_e/h^2) dH_e dH_e^T, where dH_e are the (model-independent) hat
+// differences across the edge.  Runs after k_basis_tc (fixed summation order).
+__global__ void __launch_bounds__(64) k_skel_galerkin(Geo g, const double* __restrict__ w, double* __restrict__ Kloc) {
+  __shared__ double red[36][65];
+  const int jb = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
+  const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
+  const bool has0 = (jb == 0);
+  double acc[36];
+#pragma unroll
+  for (int q = 0; q < 36; ++q) acc[q] = 0.0;
   for (int ax = 0; ax < 3; ++ax) {
     const int xm = g.b1 + (ax == 0 ? 0 : lx), ym = g.b2 + (ax == 1 ? 0 : ly), zm = g.b3 + (ax == 2 ? 0 : lz);
+    const int bax = ax == 0 ? g.b1 : (ax == 1 ? g.b2 : g.b3);
     const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
-    for (int z = 0; z < zm; ++z) {
-      for (int y = 0; y < ym; ++y) {
-        for (int x0 = 0; x0 < xm; x0 += 4) {
-          const int x = x0 + slot;
-          double a = 0.0, b = 0.0;
-          if (x < xm) {
-            const long long e = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
-                                        : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
-            const double s0 = sval(x, y, z);
-            const double s1 = sval(x + (ax == 0), y + (ax == 1), z + (ax == 2));
-            b = s1 - s0;
-            a = (__ldg(w + e) * ihs) * b;
-          }
-          mma884(K.x, K.y, a, b);
-        }
+    const int tot = xm * ym * zm;
+    for (int f = tid; f < tot; f += blockDim.x) {
+      const int x = f % xm, q = f / xm, y = q % ym, z = q / ym;
+      bool skel;
+      if (ax == 0) skel = (y == 0 || y == g.b2 || z == 0 || z == g.b3);
+      else if (ax == 1) skel = (x == 0 || x == g.b1 || z == 0 || z == g.b3);
+      else skel = (x == 0 || x == g.b1 || y == 0 || y == g.b2);
+      if (!(skel || bax == 1)) continue;
+      const int x1 = x + (ax == 0), y1 = y + (ax == 1), z1 = z + (ax == 2);
+      const long long e = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
+                                  : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
+      const double kc = __ldg(w + e) * ihs;
+      const bool n0 = has0 && x == 0 && y == 0 && z == 0;
+      double dh[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) dh[cc] = hatf(g, cc, x1, y1, z1) - (n0 ? 0.0 : hatf(g, cc, x, y, z));
+#pragma unroll
+      for (int c1 = 0; c1 < 8; ++c1) {
+        const double kd = kc * dh[c1];
+#pragma unroll
+        for (int c2 = 0; c2 <= c1; ++c2) acc[c1 * (c1 + 1) / 2 + c2] += kd * dh[c2];
       }
     }
   }
-  Kloc[(size_t)jb * 64 + m * 8 + n0] = K.x;
-  Kloc[(size_t)jb * 64 + m * 8 + n0 + 1] = K.y;
+#pragma unroll
+  for (int q = 0; q < 36; ++q) red[q][tid] = acc[q];
+  __syncthreads();
+  if (tid < 36) {
+    double v = 0.0;
+    for (int t = 0; t < blockDim.x; ++t) v += red[tid][t];
+    int c1 = 0;
+    while ((c1 + 1) * (c1 + 2) / 2 <= tid) ++c1;
+    const int c2 = tid - c1 * (c1 + 1) / 2;
+    Kloc[(size_t)jb * 64 + c1 * 8 + c2] += v;
+    if (c1 != c2) Kloc[(size_t)jb * 64 + c2 * 8 + c1] += v;
+  }
 }
 
 // ------------------------------------------------------------ block solve
 
 // out = blockdiag(A_II^{-1}) rhs on block interiors (full node fields); out
-// may alias rhs.  y is parked in out between the sweeps.
-template <int PT>
+// may alias rhs.  NCH chunks of 8 right-hand sides ride through one sweep so
+// each factor tile is read once per NCH*8 sources; the next step's tiles are
+// prefetched into registers.  y is parked in out between the sweeps.
+template <int PT, int NCH>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs) {
   extern __shared__ int crd[];
@@ -385,64 +497,101 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
     return node_id(g, X0 + (c & 1023), Y0 + ((c >> 10) & 1023), Z0 + (c >> 20));
   };
   const double* LTb = LT + (size_t)jb * NTI * (PT + 1) * 64;
-  for (int s0 = 0; s0 < nrhs; s0 += 8) {
-    const int sA = s0 + n0, sB = s0 + n0 + 1;
-    auto load_tile = [&](const double* src, int I) -> F2 {
-      const int a = 8 * I + m;
-      F2 v = {0.0, 0.0};
-      if (a < g.nI) {
-        const long long nd = node_of(a);
-        if (sA < nrhs) v.x = src[nd * nrhs + sA];
-        if (sB < nrhs) v.y = src[nd * nrhs + sB];
-      }
-      return v;
-    };
-    auto store_tile = [&](int I, const F2& v) {
-      const int a = 8 * I + m;
-      if (a < g.nI) {
-        const long long nd = node_of(a);
-        if (sA < nrhs) out[nd * nrhs + sA] = v.x;
-        if (sB < nrhs) out[nd * nrhs + sB] = v.y;
-      }
-    };
-    F2 R[PT + 1];
+  auto load_step = [&](int J, F2* Lt) {
+    const double* p = LTb + (size_t)J * (PT + 1) * 64 + lane * 2;
 #pragma unroll
-    for (int a = 0; a <= PT; ++a) R[a] = load_tile(rhs, a);
+    for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld2(p + t * 64) : F2{0.0, 0.0};
+  };
+  for (int s0 = 0; s0 < nrhs; s0 += 8 * NCH) {
+    auto load_tile = [&](const double* src, int I, F2* v) {
+      const int a = 8 * I + m;
+      long long nd = (a < g.nI) ? node_of(a) : -1;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int sA = s0 + 8 * ch + n0;
+        v[ch] = {0.0, 0.0};
+        if (nd >= 0) {
+          if (sA < nrhs) v[ch].x = src[nd * nrhs + sA];
+          if (sA + 1 < nrhs) v[ch].y = src[nd * nrhs + sA + 1];
+        }
+      }
+    };
+    auto store_tile = [&](int I, const F2* v) {
+      const int a = 8 * I + m;
+      if (a >= g.nI) return;
+      const long long nd = node_of(a);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int sA = s0 + 8 * ch + n0;
+        if (sA < nrhs) out[nd * nrhs + sA] = v[ch].x;
+        if (sA + 1 < nrhs) out[nd * nrhs + sA + 1] = v[ch].y;
+      }
+    };
+    F2 R[PT + 1][NCH];
+#pragma unroll
+    for (int a = 0; a <= PT; ++a) load_tile(rhs, a, R[a]);
+    F2 nL[PT + 1];
+    load_step(0, nL);
     // forward: y_J = L_JJ^{-1} r_J ; r_{J+t} -= L_{J+t,J} y_J
     for (int J = 0; J < NTI; ++J) {
-      const double* Lt = LTb + (size_t)J * (PT + 1) * 64;
-      const F2 Li = ld2(Lt + lane * 2);
-      F2 Yc = {0.0, 0.0};
-      mma(Yc, Li, c_to_b(R[0], lane));
-      const F2 Yb = c_to_b(Yc, lane);
+      F2 cL[PT + 1];
 #pragma unroll
-      for (int t = 1; t <= PT; ++t)
-        if (J + t < NTI) mma(R[t], neg(ld2(Lt + t * 64 + lane * 2)), Yb);
-      const F2 nxt = load_tile(rhs, J + 1 + PT);   // read ahead before y_J lands (out may alias rhs)
+      for (int t = 0; t <= PT; ++t) cL[t] = nL[t];
+      if (J + 1 < NTI) load_step(J + 1, nL);
+      F2 nxt[NCH];
+      load_tile(rhs, J + 1 + PT, nxt);            // read ahead before y_J lands (out may alias rhs)
+      F2 Yc[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        Yc[ch] = {0.0, 0.0};
+        mma(Yc[ch], cL[0], c_to_b(R[0][ch], lane));
+        const F2 Yb = c_to_b(Yc[ch], lane);
+#pragma unroll
+        for (int t = 1; t <= PT; ++t)
+          if (J + t < NTI) mma(R[t][ch], neg(cL[t]), Yb);
+      }
       __syncwarp();
       store_tile(J, Yc);
 #pragma unroll
-      for (int a = 1; a <= PT; ++a) R[a - 1] = R[a];
-      R[PT] = nxt;
+      for (int a = 1; a <= PT; ++a)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) R[a - 1][ch] = R[a][ch];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) R[PT][ch] = nxt[ch];
     }
     __syncwarp();
     // backward: x_J = L_JJ^{-T} (y_J - sum_t L_{J+t,J}^T x_{J+t})
-    F2 Xw[PT > 0 ? PT : 1];
+    F2 Xw[PT > 0 ? PT : 1][NCH];
 #pragma unroll
-    for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
+    for (int t = 0; t < (PT > 0 ? PT : 1); ++t)
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) Xw[t][ch] = {0.0, 0.0};
+    load_step(NTI - 1, nL);
     for (int J = NTI - 1; J >= 0; --J) {
-      const double* Lt = LTb + (size_t)J * (PT + 1) * 64;
-      F2 acc = load_tile(out, J);
+      F2 cT[PT + 1];
 #pragma unroll
-      for (int t = 1; t <= PT; ++t)
-        if (J + t < NTI) mma(acc, neg(a_to_t(ld2(Lt + t * 64 + lane * 2), lane)), Xw[t - 1]);
-      F2 xj = {0.0, 0.0};
-      mma(xj, a_to_t(ld2(Lt + lane * 2), lane), c_to_b(acc, lane));
+      for (int t = 0; t <= PT; ++t) cT[t] = a_to_t(nL[t], lane);   // transposed tiles
+      if (J > 0) load_step(J - 1, nL);
+      F2 acc[NCH];
+      load_tile(out, J, acc);
+      F2 xj[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+        for (int t = 1; t <= PT; ++t)
+          if (J + t < NTI) mma(acc[ch], neg(cT[t]), Xw[t - 1][ch]);
+        xj[ch] = {0.0, 0.0};
+        mma(xj[ch], cT[0], c_to_b(acc[ch], lane));
+      }
       __syncwarp();
       store_tile(J, xj);
 #pragma unroll
-      for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
-      if (PT > 0) Xw[0] = c_to_b(xj, lane);
+      for (int t = PT - 1; t >= 1; --t)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) Xw[t][ch] = Xw[t - 1][ch];
+      if (PT > 0)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) Xw[0][ch] = c_to_b(xj[ch], lane);
     }
     __syncwarp();
   }
@@ -470,7 +619,14 @@ template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc,
                                      double* Kloc, int* flags, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
-  k_basis_tc<PT><<<grid, TC_WARPS * 32, (size_t)g.nI * sizeof(int), st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
+  const size_t smem = (size_t)TC_WARPS * g.nI * 8 * sizeof(double) + (size_t)g.nI * sizeof(int);
+  cudaError_t e = cudaFuncSetAttribute(k_basis_tc<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_basis_tc<PT><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
+  count_launches(1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_skel_galerkin<<<g.nbl, 64, 0, st>>>(g, w, Kloc);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -478,7 +634,11 @@ template <int PT>
 static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                      cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
-  k_block_solve_tc<PT><<<grid, TC_WARPS * 32, (size_t)g.nI * sizeof(int), st>>>(g, LT, rhs, out, nrhs);
+  const size_t smem = (size_t)g.nI * sizeof(int);
+  if (nrhs > 8)
+    k_block_solve_tc<PT, 2><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs);
+  else
+    k_block_solve_tc<PT, 1><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs);
   count_launches(1);
   return cudaGetLastError();
 }
