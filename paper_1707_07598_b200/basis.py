@@ -98,43 +98,49 @@ def generate_bc_lagrange(partition):
                            count=partition.n_coarse_nodes)
 
 
-class _CscTemplate:
+def csc_pattern(partition):
     """Model-independent CSC pattern of S and the gather map from the device
-    block layout into it (basis.py:574-594)."""
+    block layout into it (basis.py:574-594), host side.
+
+    Returns (indices, indptr, src, hatv): src[t] >= 0 indexes the device
+    array Sint[block][corner][interior]; src[t] == -1 marks a skeleton entry
+    whose value is the hat hatv[t] (bit-exact with the reference)."""
+    n = partition.mesh.n_nodes - 1
+    k = partition.n_coarse_nodes
+    r_s, c_s, v_s = _skeleton_hat_entries(partition)
+    nI = (partition.b1 - 1) * (partition.b2 - 1) * (partition.b3 - 1)
+    rows, cols = [r_s], [c_s]
+    src = [np.full(r_s.size, -1, dtype=np.int64)]
+    hv = [v_s]
+    if nI > 0:
+        nb1, nb2, _ = partition.nb
+        inter = np.stack(partition.interiors) - 1             # [block, a] pinned ids
+        nbl = inter.shape[0]
+        blk = np.arange(nbl)
+        bi, bj, bk = blk % nb1, (blk // nb1) % nb2, blk // (nb1 * nb2)
+        for cc in range(8):
+            col = (bi + (cc & 1)) + (nb1 + 1) * ((bj + ((cc >> 1) & 1)) + (nb2 + 1) * (bk + ((cc >> 2) & 1)))
+            rows.append(inter.ravel())
+            cols.append(np.repeat(col, nI))
+            src.append(((blk[:, None] * 8 + cc) * nI + np.arange(nI)[None, :]).ravel())
+            hv.append(np.zeros(nbl * nI))
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    src, hv = np.concatenate(src), np.concatenate(hv)
+    order = np.argsort(cols.astype(np.int64) * n + rows, kind="stable")
+    indices = rows[order].astype(np.int32)
+    indptr = np.searchsorted(cols[order], np.arange(k + 1)).astype(np.int32)
+    return indices, indptr, src[order], hv[order]
+
+
+class _CscTemplate:
+    """csc_pattern uploaded for one engine."""
 
     def __init__(self, partition, engine):
         import torch
-        n = partition.mesh.n_nodes - 1
-        k = partition.n_coarse_nodes
-        r_s, c_s, v_s = _skeleton_hat_entries(partition)
-        nI = engine.nI
-        rows = [r_s]
-        cols = [c_s]
-        src = [np.full(r_s.size, -1, dtype=np.int64)]
-        hv = [v_s]
-        if nI > 0:
-            nb1, nb2, nb3 = partition.nb
-            inter = np.stack(partition.interiors) - 1             # [block, a] pinned ids
-            nbl = inter.shape[0]
-            bi = np.arange(nbl) % nb1
-            bj = (np.arange(nbl) // nb1) % nb2
-            bk = np.arange(nbl) // (nb1 * nb2)
-            for cc in range(8):
-                col = (bi + (cc & 1)) + (nb1 + 1) * ((bj + ((cc >> 1) & 1)) + (nb2 + 1) * (bk + ((cc >> 2) & 1)))
-                rows.append(inter.ravel())
-                cols.append(np.repeat(col, nI))
-                src.append(((np.arange(nbl)[:, None] * 8 + cc) * nI + np.arange(nI)[None, :]).ravel())
-                hv.append(np.zeros(nbl * nI))
-        rows = np.concatenate(rows)
-        cols = np.concatenate(cols)
-        src = np.concatenate(src)
-        hv = np.concatenate(hv)
-        order = np.argsort(cols.astype(np.int64) * n + rows, kind="stable")
-        self.indices = rows[order].astype(np.int32)
-        self.indptr = np.searchsorted(cols[order], np.arange(k + 1)).astype(np.int32)
-        self.shape = (n, k)
-        self.src = torch.from_numpy(src[order]).to(engine.device)
-        self.hatv = torch.from_numpy(hv[order]).to(engine.device)
+        self.indices, self.indptr, src, hv = csc_pattern(partition)
+        self.shape = (partition.mesh.n_nodes - 1, partition.n_coarse_nodes)
+        self.src = torch.from_numpy(src).to(engine.device)
+        self.hatv = torch.from_numpy(hv).to(engine.device)
 
 
 class MultiscaleBasis:

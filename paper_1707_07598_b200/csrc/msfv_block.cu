@@ -41,11 +41,11 @@ __global__ void k_edge_weights(Geo g, const double* __restrict__ cv, double* __r
   int ax;
   int i, j, k;
   if (e < g.Ex) {
-    ax = 0; decode3(e, g.n1, g.n2 + 1, i, j, k);
+    ax = 0; decode3f(e, g.n1, g.r_n1, g.n2 + 1, g.r_n2p, i, j, k);
   } else if (e < g.Ex + g.Ey) {
-    ax = 1; decode3(e - g.Ex, g.n1 + 1, g.n2, i, j, k);
+    ax = 1; decode3f(e - g.Ex, g.n1 + 1, g.r_n1p, g.n2, g.r_n2, i, j, k);
   } else {
-    ax = 2; decode3(e - g.Ex - g.Ey, g.n1 + 1, g.n2 + 1, i, j, k);
+    ax = 2; decode3f(e - g.Ex - g.Ey, g.n1 + 1, g.r_n1p, g.n2 + 1, g.r_n2p, i, j, k);
   }
   double sum = 0.0;
   // transverse axes t1 < t2; outer loop on t2 (higher stride) gives ascending cell ids
@@ -448,10 +448,10 @@ __global__ void k_residual(Geo g, const double* __restrict__ src, double alpha,
   long long ii = t >> lg;
   const int j = (int)(t & ((1 << lg) - 1));
   if (ii >= (long long)g.nbl * g.nI) return;
-  const int jb = (int)((unsigned)ii / (unsigned)g.nI), a = (int)((unsigned)ii - (unsigned)jb * (unsigned)g.nI);
+  const int jb = fdiv(ii, g.nI, g.r_nI), a = (int)(ii - (long long)jb * g.nI);
   int bi, bj, bk, x, y, z;
-  decode3(jb, g.nb1, g.nb2, bi, bj, bk);
-  decode3(a, g.ni1, g.ni2, x, y, z);
+  decode3f(jb, g.nb1, g.r_nb1, g.nb2, g.r_nb2, bi, bj, bk);
+  decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
   x += 1; y += 1; z += 1;
   long long I = (long long)bi * g.b1 + x, J = (long long)bj * g.b2 + y, K = (long long)bk * g.b3 + z;
   long long nd = node_id(g, I, J, K);
@@ -492,8 +492,9 @@ __global__ void k_prolong(Geo g, const double* __restrict__ Sint, const double* 
   int bi = 0, bj = 0, bk = 0, x = 0, y = 0, z = 0;
   if (valid) {
     int I, J, K;
-    decode3(nd, g.n1 + 1, g.n2 + 1, I, J, K);
-    bi = own1i(I, g.b1, g.nb1); bj = own1i(J, g.b2, g.nb2); bk = own1i(K, g.b3, g.nb3);
+    decode3f(nd, g.n1 + 1, g.r_n1p, g.n2 + 1, g.r_n2p, I, J, K);
+    bi = min(fdiv(I, g.b1, g.r_b1), g.nb1 - 1); bj = min(fdiv(J, g.b2, g.r_b2), g.nb2 - 1);
+    bk = min(fdiv(K, g.b3, g.r_b3), g.nb3 - 1);
     x = I - bi * g.b1; y = J - bj * g.b2; z = K - bk * g.b3;
   }
   const double* Sb = Sint + (size_t)block_of(g, bi, bj, bk) * 8 * g.nI;
@@ -604,7 +605,7 @@ __global__ void k_edge_xi(Geo g, const double* __restrict__ U, const double* __r
   const int j = (int)(t & ((1 << lg) - 1));
   const bool valid = nd < g.Nn;
   int i = 0, jj = 0, k = 0;
-  if (valid) decode3(nd, g.n1 + 1, g.n2 + 1, i, jj, k);
+  if (valid) decode3f(nd, g.n1 + 1, g.r_n1p, g.n2 + 1, g.r_n2p, i, jj, k);
   const bool hx = valid && i < g.n1, hy = valid && jj < g.n2, hz = valid && k < g.n3;
   const long long nx = nd + 1, ny = nd + (g.n1 + 1), nz = nd + (long long)(g.n1 + 1) * (g.n2 + 1);
   double ax = 0.0, ay = 0.0, az = 0.0;
@@ -647,7 +648,7 @@ __global__ void k_cell_gather(Geo g, const double* __restrict__ sigma, const dou
   long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (c >= g.Nm) return;
   int i, j, k;
-  decode3(c, g.n1, g.n2, i, j, k);
+  decode3f(c, g.n1, g.r_n1, g.n2, g.r_n2, i, j, k);
   double tot = 0.0;
   tot += xi[ex_id(g, i, j, k)] + xi[ex_id(g, i, j + 1, k)] + xi[ex_id(g, i, j, k + 1)] + xi[ex_id(g, i, j + 1, k + 1)];
   tot += xi[ey_id(g, i, j, k)] + xi[ey_id(g, i + 1, j, k)] + xi[ey_id(g, i, j, k + 1)] + xi[ey_id(g, i + 1, j, k + 1)];

@@ -79,6 +79,10 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.ih1 = 1.0 / h[0]; g.ih2 = 1.0 / h[1]; g.ih3 = 1.0 / h[2];
   g.qv = 0.25 * (h[0] * h[1] * h[2]);
   g.ib1 = 1.0 / g.b1; g.ib2 = 1.0 / g.b2; g.ib3 = 1.0 / g.b3;
+  g.r_n1 = 1.0f / g.n1; g.r_n2 = 1.0f / g.n2; g.r_n1p = 1.0f / (g.n1 + 1); g.r_n2p = 1.0f / (g.n2 + 1);
+  g.r_b1 = 1.0f / g.b1; g.r_b2 = 1.0f / g.b2; g.r_b3 = 1.0f / g.b3;
+  g.r_ni1 = g.ni1 > 0 ? 1.0f / g.ni1 : 0.0f; g.r_ni2 = g.ni2 > 0 ? 1.0f / g.ni2 : 0.0f;
+  g.r_nI = g.nI > 0 ? 1.0f / g.nI : 0.0f; g.r_nb1 = 1.0f / g.nb1; g.r_nb2 = 1.0f / g.nb2;
   {
     // dense coarse L^{-1}: default up to COARSE_INV_MAX coarse nodes; MSFV_COARSE_INV=0/1 overrides
     const char* ev = getenv("MSFV_COARSE_INV");

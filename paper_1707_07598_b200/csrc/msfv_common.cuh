@@ -40,7 +40,26 @@ struct Geo {
   double qv;               // 0.25 * cell volume (operators.py:83)
   double ib1, ib2, ib3;    // 1/b per axis (device-side hats)
   int coarse_inv;          // 1: keep a dense L^{-1} of the coarse factor for the solves
+  // float reciprocals for division-free index decoding (see fdiv)
+  float r_n1, r_n2, r_n1p, r_n2p, r_b1, r_b2, r_b3, r_ni1, r_ni2, r_nI, r_nb1, r_nb2;
 };
+
+// floor(x / d) for 0 <= x < 2^31 from a float reciprocal, corrected to exact.
+__host__ __device__ __forceinline__ int fdiv(long long x, int d, float rd) {
+  long long q = (long long)((float)x * rd);
+  long long r = x - q * d;
+  while (r < 0) { --q; r += d; }
+  while (r >= d) { ++q; r -= d; }
+  return (int)q;
+}
+// idx -> (i, j, k) for an (d1, d2, *) box, x fastest
+__host__ __device__ __forceinline__ void decode3f(long long idx, int d1, float r1, int d2, float r2, int& i, int& j,
+                                                  int& k) {
+  const int q = fdiv(idx, d1, r1);
+  i = (int)(idx - (long long)q * d1);
+  k = fdiv(q, d2, r2);
+  j = q - k * d2;
+}
 
 __host__ __device__ __forceinline__ long long node_id(const Geo& g, long long i, long long j, long long k) {
   return i + (long long)(g.n1 + 1) * (j + (long long)(g.n2 + 1) * k);

@@ -374,8 +374,6 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   // contribute k_e dH dH^T with the model-independent hats.  DMMA reduction,
   // 4 edges (k) x 8 corners per instruction: lane (corner cc = lane/4, edge
   // slot lane%4).
-  const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
-  const bool has0 = (jb == 0);
   const int cc = lane >> 2, slot = lane & 3;
   F2 K = {0.0, 0.0};
   // (1) boundary-interior edges, face by face

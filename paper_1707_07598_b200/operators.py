@@ -89,8 +89,6 @@ class DiffusionOperator:
     """
 
     def __init__(self, mesh, m, pieces=None, engine=None):
-        from .engine import require_cuda
-        require_cuda()
         if hasattr(m, "detach"):       # torch tensor (host or device)
             m_np = None
             if m.numel() != mesh.n_cells:
@@ -112,6 +110,8 @@ class DiffusionOperator:
     def device_state(self, engine):
         if self._dev is not None and self._dev[0] is engine:
             return self._dev
+        from .engine import require_cuda
+        require_cuda()
         src = self._m_src if self._m_host is None else self._m_host
         m_dev = engine.to_device(src).reshape(-1)
         sigma, w, fl = engine.operator(m_dev)

@@ -1,0 +1,57 @@
+"""BASELINE.json 3D configs on the GPU path against the CPU oracle on the
+same seeded inputs (north_star tolerance: 1e-10 relative on u (T), P u_c
+(S T), D, misfit and gradient).  The oracle is pinned to the reference by
+tests/test_oracle_golden.py."""
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def run_both(cfg, slab=None):
+    import paper_1707_07598_b200 as gp
+    from paper_1707_07598_b200.models import CONFIGS, build_survey, config_model, gaussian_field
+    from oracle import msfv_oracle as orc
+    c = CONFIGS[cfg]
+    n, b = c["n"], c["b"]
+    nz = slab or n
+    mesh = gp.create_mesh(n, n, nz, 1 / n, 1 / n, 1 / n)
+    part = gp.create_partition(mesh, b, b, b)
+    survey = build_survey(mesh, c["n_src"], c["n_rec"])
+    m = config_model(mesh, c, 0) if slab is None else gaussian_field(mesh, c["field"][0], c["field"][1], 0)
+    prob = gp.AdaptiveReducedProblem(gp.BasisBuilder(part), survey)
+    d_obs = prob.simulate(m + 0.1)[0]
+    D, st = prob.simulate(m)
+    phi, r = gp.misfit_ssd(D, d_obs)
+    J = prob.jacobian(st)
+    g = J.rapply(r)
+    dm = np.random.default_rng(1).normal(size=m.size)
+    jv = J.apply(dm)
+    US = st.basis.S @ st.T
+
+    omesh = orc.Mesh(n, n, nz, 1 / n, 1 / n, 1 / n)
+    oprob = orc.AdaptiveProblem(orc.make_partition(omesh, b, b, b), orc.Survey(survey.P, survey.Q))
+    D0, st0 = oprob.simulate(m)
+    phi0, r0 = orc.misfit(D0, d_obs)
+    J0 = oprob.jacobian(st0)
+    errs = {"T": rel(st.T, st0.T), "ST": rel(US, st0.basis.S @ st0.T), "D": rel(D, D0),
+            "phi": abs(phi - phi0) / abs(phi0), "g": rel(g, J0.rapply(r0)), "Jv": rel(jv, J0.apply(dm)),
+            "S": rel(st.basis.S.data, st0.basis.S.data)}
+    assert np.array_equal(st.basis.S.indices, st0.basis.S.indices)
+    assert np.array_equal(st.basis.S.indptr, st0.basis.S.indptr)
+    return errs
+
+
+def test_config3_matches_oracle():
+    errs = run_both(3)
+    assert all(v <= TOL for v in errs.values()), errs
+
+
+def test_config4_matches_oracle():
+    # 128^3, 4096 local solves, sigma contrast ~2e6 (the north_star target config)
+    errs = run_both(4)
+    assert all(v <= TOL for v in errs.values()), errs
