@@ -75,4 +75,4 @@ def test_edge_weights_last_ulp():
     op = gp.assemble_operator(mesh, g["m"])
     builder.assemble(op)
     w = op.edge_weights
-    assert np.max(np.abs(w - g["w"]) / np.abs(g["w"])) <= 4e-16
+    assert np.max(np.abs(w - g["w"]) / np.abs(g["w"])) <= 1e-15
