@@ -211,12 +211,15 @@ def run_gpu(args, rank, world, log):
     L = _lib.load()
 
     def step_dev():
+        # device-resident step: no host synchronisation until the status check
         op = gp.assemble_operator(mesh, m_dev)
         basis = builder.assemble(op)
-        D, st = forward_reduced_dev(op, survey, basis)
+        D, st = forward_reduced_dev(op, survey, basis, defer_check=True)
+        st.deferred = True
         resid = D - dobs_dev
         phi = 0.5 * torch.sum(resid * resid)
         g = sensitivity_adaptive(st, survey).rapply_dev(resid)
+        st.check()
         return phi, g
 
     # correctness guard of the timed configuration: misfit and gradient finite
@@ -225,6 +228,19 @@ def run_gpu(args, rank, world, log):
 
     for _ in range(args.warmup):
         step_dev()
+    # extra untimed steps until the per-step device time is stable (the first
+    # ~10 steps after allocation run slower; see profiles/README)
+    prev = None
+    for _ in range(12):
+        a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        step_dev()
+        b0.record()
+        torch.cuda.synchronize()
+        t = a0.elapsed_time(b0)
+        if prev is not None and abs(t - prev) <= 0.01 * prev:
+            break
+        prev = t
     torch.cuda.synchronize()
     dist.barrier()
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))

@@ -14,10 +14,20 @@ import numpy as np
 import scipy.sparse as sp
 
 from .engine import engine_for
-from .errors import FactorizationError, StaleBasisError
+from .errors import FactorizationError, InvalidModelError, StaleBasisError
 from .operators import edge_cell_map, nodal_gradient
 
 FAMILIES = ("lagrange", "source", "skeleton", "local_pca")
+
+
+def raise_status(f):
+    """Map device status bits onto the reference exception types."""
+    if f & 1:
+        raise InvalidModelError("model vector contains non-finite entries")
+    if f & 2:
+        raise InvalidModelError("conductivity must be positive")
+    if f & 4:
+        raise FactorizationError("local interior operator is not positive definite")
 
 
 @dataclass(frozen=True)
@@ -177,8 +187,7 @@ class MultiscaleBasis:
     def raise_on_flags(self, f=None):
         if f is None:
             f = int(self.flags.item())
-        if f & 4:
-            raise FactorizationError("local interior operator is not positive definite")
+        raise_status(f & 7)
         self._checked = True
 
     def check_model(self, m):
@@ -254,7 +263,7 @@ def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None):
             raise NotImplementedError("the GPU path builds the Lagrange family only")
     eng = engine_for(partition)
     _, m_dev, sigma, w = op.device_state(eng)
-    factor, Sint, Kloc, fl = eng.basis(w)
+    factor, Sint, Kloc, fl = eng.basis(w, op.flags)
     return MultiscaleBasis(partition, eng, op, factor, Sint, Kloc, fl)
 
 

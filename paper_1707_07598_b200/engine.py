@@ -163,16 +163,16 @@ class Engine:
                        "edge_average")
         return c
 
-    def basis(self, w):
+    def basis(self, w, fl=None):
         with phase("basis"):
-            return self._basis(w)
+            return self._basis(w, fl)
 
-    def _basis(self, w):
+    def _basis(self, w, fl=None):
         factor = self.empty(max(self.factor_doubles, 1))
         Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
         Kloc = self.empty(self.nbl * 64)
         scratch = self.empty(max(self.scratch_doubles, 1))
-        fl = self.flags()
+        fl = fl if fl is not None else self.flags()
         _lib.check(self.L.msfv_basis_build(self.plan, ptr(w), ptr(factor), ptr(Sint), ptr(Kloc), ptr(scratch),
                                            ptr(fl), stream()), "basis_build")
         return factor, Sint, Kloc, fl

@@ -120,6 +120,27 @@ class ReducedState:
             self._A_k = K + np.tril(K, -1).T
         return self._A_k
 
+    def check(self):
+        """Resolve the status of the forward chain (one device sync)."""
+        if not getattr(self, "pending", False):
+            return
+        self.pending = False
+        from .basis import raise_status
+        f = int(self.flags.item())
+        raise_status(f & 7)
+        if f & 8:
+            # diagonal shift fallback (forward.py:122-129)
+            eng = self.basis.engine
+            tr = float(eng.coarse_trace(eng.galerkin(self.basis.Kloc, 0.0)).sum().item())
+            shift = 1e-12 * tr / eng.k
+            self.flags.zero_()
+            D, Ak, T = _coarse_solve_chain(eng, self.op, self.survey, self.basis, shift, self.flags)
+            if int(self.flags.item()) & 8:
+                raise ReducedSingularError("projected operator is singular even after diagonal shift")
+            self.D_dev.copy_(D)
+            self.Lk, self.T_dev, self.shift = Ak, T, shift
+            self._T = None
+
     def solve_reduced(self, B):
         eng = self.basis.engine
         B = np.asarray(B, dtype=float)
@@ -130,36 +151,38 @@ class ReducedState:
         return out[:, 0] if single else out
 
 
-def forward_reduced_dev(op, survey, basis):
-    """Device-resident reduced forward: returns (D device tensor, state)."""
+def _coarse_solve_chain(eng, op, survey, basis, shift, fl):
+    Pp, Qp, _ = survey.device(eng)
+    ns = survey.n_sources
+    F = eng.restrict_points(Qp, basis.Sint, None, ns)                 # S^T Q   (forward.py:115)
+    Ak = eng.galerkin(basis.Kloc, shift)                              # S^T A S (+ shift I) (forward.py:118,125)
+    eng.coarse_factor(Ak, fl)                                         # cho_factor (forward.py:121)
+    T = eng.coarse_solve(Ak, F)                                       # T = A_k^-1 S^T Q (forward.py:142)
+    D = eng.receive(Pp, basis.Sint, Y=T)                              # P^T S T (forward.py:143)
+    return D, Ak, T
+
+
+def forward_reduced_dev(op, survey, basis, defer_check=False):
+    """Device-resident reduced forward: returns (D device tensor, state).
+
+    With ``defer_check`` nothing synchronises; the status bits (invalid model,
+    local or coarse factorization failure) are resolved by ``state.check()``,
+    which also takes the reference's diagonal-shift fallback (forward.py:122-129)."""
     eng = basis.engine
     if op._dev is None or op._dev[0] is not eng:
         op.device_state(eng)
     if op._dev[1] is not basis._m_dev and not torch.equal(op._dev[1], basis._m_dev):
         raise NotImplementedError("forward_reduced with a basis frozen at another model "
                                   "(ms_fixed mode) is outside this tier's GPU path")
-    Pp, Qp, _ = survey.device(eng)
-    ns = survey.n_sources
-    F = eng.restrict_points(Qp, basis.Sint, None, ns)                 # S^T Q   (forward.py:115)
-    Ak = eng.galerkin(basis.Kloc, 0.0)                                # S^T A S (forward.py:118)
-    fl = eng.flags()
-    eng.coarse_factor(Ak, fl)                                         # cho_factor (forward.py:121)
-    f = torch.cat([fl, basis.flags]).cpu()
-    basis.raise_on_flags(int(f[1]))
-    shift = 0.0
-    if int(f[0]) & 8:
-        # diagonal shift fallback (forward.py:122-129)
-        Ak = eng.galerkin(basis.Kloc, 0.0)
-        tr = float(eng.coarse_trace(Ak).sum().item())
-        shift = 1e-12 * tr / eng.k
-        Ak = eng.galerkin(basis.Kloc, shift, out=Ak)
-        fl.zero_()
-        eng.coarse_factor(Ak, fl)
-        if int(fl.item()) & 8:
-            raise ReducedSingularError("projected operator is singular even after diagonal shift")
-    T = eng.coarse_solve(Ak, F)                                       # T = A_k^-1 S^T Q (forward.py:142)
-    D = eng.receive(Pp, basis.Sint, Y=T)                              # P^T S T (forward.py:143)
-    return D, ReducedState(op, basis, Ak, T, shift, survey)
+    fl = op.flags
+    D, Ak, T = _coarse_solve_chain(eng, op, survey, basis, 0.0, fl)
+    state = ReducedState(op, basis, Ak, T, 0.0, survey)
+    state.D_dev = D
+    state.flags = fl
+    state.pending = True
+    if not defer_check:
+        state.check()
+    return state.D_dev, state
 
 
 def forward_reduced(op, survey, basis):
@@ -176,6 +199,8 @@ class AdaptiveSensitivity:
     def __init__(self, state, survey, workers=1):
         op, basis = state.op, state.basis
         eng = basis.engine
+        if not getattr(state, "deferred", False):
+            state.check()
         if op._dev is None or op._dev[1] is not basis._m_dev:
             basis.check_model(op.m)
         self.state, self.survey, self.basis, self.engine = state, survey, basis, eng

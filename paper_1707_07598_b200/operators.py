@@ -115,11 +115,9 @@ class DiffusionOperator:
         src = self._m_src if self._m_host is None else self._m_host
         m_dev = engine.to_device(src).reshape(-1)
         sigma, w, fl = engine.operator(m_dev)
-        f = int(fl.item())
-        if f & 1:
-            raise InvalidModelError("model vector contains non-finite entries")
-        if f & 2:
-            raise InvalidModelError("conductivity must be positive")
+        # status bits accumulate along the forward chain (operator, basis,
+        # coarse factor) and are read once, when a result is handed back
+        self.flags = fl
         self._dev = (engine, m_dev, sigma, w)
         return self._dev
 
@@ -186,14 +184,12 @@ class DiffusionOperator:
 
 
 def assemble_operator(mesh, m, pieces=None):
-    """A(m) (operators.py:164-166); device evaluation happens when a basis or
-    forward call binds it to a partition."""
-    op = DiffusionOperator(mesh, m, pieces=pieces)
-    if op._m_host is not None:
-        # same eager validation as the reference (operators.py:128-129)
-        if not np.all(np.isfinite(op._m_host)):
-            raise InvalidModelError("model vector contains non-finite entries")
-    return op
+    """A(m) (operators.py:164-166).  sigma and the edge weights are evaluated on
+    the device when a basis or forward call binds the operator to a partition;
+    the finiteness / positivity checks of operators.py:26-27,128-129 run there
+    too and raise InvalidModelError at the first result read back to the host
+    (no host pass over m on the hot path)."""
+    return DiffusionOperator(mesh, m, pieces=pieces)
 
 
 def grad_A_u_full(mesh, m, u_full, pieces=None):

@@ -180,12 +180,13 @@ def test_error_contract(rng):
     part = gp.create_partition(mesh, 2, 2, 2)
     builder = gp.BasisBuilder(part)
     m = np.zeros(mesh.n_cells)
-    with pytest.raises(gp.InvalidModelError):
-        m2 = m.copy()
-        m2[0] = np.inf
-        gp.assemble_operator(mesh, m2)
-    with pytest.raises(gp.InvalidModelError):
-        builder.assemble(gp.assemble_operator(mesh, m - 800.0))     # exp underflows to 0
+    survey = point_survey(mesh, n_rec=4, n_src=2, seed=1, dipoles=True)
+    m2 = m.copy()
+    m2[0] = np.inf
+    for bad in (m2, m - 800.0):                                       # non-finite / exp underflow
+        with pytest.raises(gp.InvalidModelError):
+            op = gp.assemble_operator(mesh, bad)
+            gp.forward_reduced(op, survey, builder.assemble(op))
     basis = builder.assemble(gp.assemble_operator(mesh, m))
     with pytest.raises(gp.StaleBasisError):
         basis.check_model(m + 1e-3)
