@@ -255,7 +255,7 @@ int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, dou
   CHECK_PLAN(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g)) return cuda_check(launch_basis_tc(g, w, factor, Sint, scratch, Kloc, flags, st), "basis_build");
+  if (tc_supported(g)) return cuda_check(launch_basis_tc(g, w, factor, Sint, Kloc, flags, st), "basis_build");
   double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
   return cuda_check(launch_basis(g, w, factor, Lr, Sint, Kloc, flags, st), "basis_build");
 }

@@ -50,7 +50,7 @@ int tc_band(const Geo& g);
 bool tc_supported(const Geo& g);
 size_t tc_factor_doubles(const Geo& g);
 size_t tc_scratch_doubles(const Geo& g);
-cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc, double* Kloc,
+cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st);
 cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                   cudaStream_t st);

@@ -36,40 +36,12 @@ __device__ __forceinline__ void mma884(double& c0, double& c1, double a, double 
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
-// C (accumulator layout) += A (A-frag) * B (B-frag), k = 8
+// D += X Y^T for C-layout tiles X, Y (k = 8, see ld_t)
 __device__ __forceinline__ void mma(F2& c, const F2& a, const F2& b) {
   mma884(c.x, c.y, a.x, b.x);
   mma884(c.x, c.y, a.y, b.y);
 }
 __device__ __forceinline__ F2 neg(const F2& f) { return {-f.x, -f.y}; }
-
-// accumulator tile T -> A-frag of T
-__device__ __forceinline__ F2 c_to_a(const F2& c, int lane) {
-  const int m = lane >> 2, k = lane & 3;
-  const int s0 = (m << 2) | (k >> 1), s1 = (m << 2) | (2 + (k >> 1));
-  double x0 = __shfl_sync(FULL, c.x, s0), y0 = __shfl_sync(FULL, c.y, s0);
-  double x1 = __shfl_sync(FULL, c.x, s1), y1 = __shfl_sync(FULL, c.y, s1);
-  const bool odd = k & 1;
-  return {odd ? y0 : x0, odd ? y1 : x1};
-}
-// accumulator tile T -> B-frag of T (B[k][n] = T[k][n])
-__device__ __forceinline__ F2 c_to_b(const F2& c, int lane) {
-  const int k = lane & 3, n = lane >> 2;
-  const int s0 = (k << 2) | (n >> 1), s1 = ((k + 4) << 2) | (n >> 1);
-  double x0 = __shfl_sync(FULL, c.x, s0), y0 = __shfl_sync(FULL, c.y, s0);
-  double x1 = __shfl_sync(FULL, c.x, s1), y1 = __shfl_sync(FULL, c.y, s1);
-  const bool odd = n & 1;
-  return {odd ? y0 : x0, odd ? y1 : x1};
-}
-// A-frag of T -> A-frag of T^T (equivalently the B-frag of T)
-__device__ __forceinline__ F2 a_to_t(const F2& f, int lane) {
-  const int k = lane & 3, n = lane >> 2;
-  const int s0 = (k << 2) | (n & 3), s1 = ((k + 4) << 2) | (n & 3);
-  double p0 = __shfl_sync(FULL, f.x, s0), q0 = __shfl_sync(FULL, f.y, s0);
-  double p1 = __shfl_sync(FULL, f.x, s1), q1 = __shfl_sync(FULL, f.y, s1);
-  const bool hi = n >= 4;
-  return {hi ? q0 : p0, hi ? q1 : p1};
-}
 
 __device__ __forceinline__ F2 ld2(const double* p) {
   double2 v = *reinterpret_cast<const double2*>(p);
@@ -83,13 +55,6 @@ __device__ __forceinline__ void st2(double* p, const F2& f) {
   *reinterpret_cast<double2*>(p) = make_double2(f.x, f.y);
 }
 
-// Stencil row of interior node i of a block: the six edge conductances / h^2.
-struct Row {
-  bool valid;
-  int x, y, z;
-  double kxm, kxp, kym, kyp, kzm, kzp;
-};
-
 // Interior coordinates, packed x | y << 10 | z << 20 (one table per CTA).
 __device__ __forceinline__ void fill_coords(const Geo& g, int* crd) {
   for (int a = threadIdx.x; a < g.nI; a += blockDim.x) {
@@ -98,59 +63,116 @@ __device__ __forceinline__ void fill_coords(const Geo& g, int* crd) {
   }
 }
 
-__device__ __forceinline__ Row load_row(const Geo& g, const double* __restrict__ w, const int* crd, int X0, int Y0,
-                                        int Z0, int i) {
-  Row r;
-  r.valid = i < g.nI;
-  if (!r.valid) {
-    r.x = r.y = r.z = 0;
-    r.kxm = r.kxp = r.kym = r.kyp = r.kzm = r.kzp = 0.0;
-    return r;
+// Transposed-operand DMMA form.  With BOTH operands in accumulator (C) layout,
+// mma(D, X, Y) computes D += X Y^T: chunk h of the k dimension is the column
+// set {2k + h}, i.e. slot h of the C layout, for X and Y alike.  Every product
+// the Cholesky and the substitutions need (X_t = A_t L^-T, A -= X_a X_b^T,
+// y^T = r^T L^-T, r^T -= y^T X^T, x^T = (.) L^-1) is of that form once the
+// right-hand sides are carried transposed, so no register shuffles are needed.
+// Tiles are stored row-major (the C layout at lane*2); ld_t loads the C layout
+// of a stored tile's transpose.
+__device__ __forceinline__ F2 ld_t(const double* p, int lane) {
+  const int m = lane >> 2, q = lane & 3;
+  return {__ldcg(p + 16 * q + m), __ldcg(p + 16 * q + 8 + m)};
+}
+
+// Per-block stencil table in shared memory: one row of AROW doubles per
+// interior node, padding rows (up to 8*NTI) are identity:
+//   [A_ii, A_{i,i-1}, A_{i,i-ni1}, A_{i,i-p}, 0]
+// Coinciding offsets (ni1 == 1 or ni2 == 1) are merged into the first slot
+// that the selector (sel_code) tests.  The Lagrange right-hand sides -A_IB x_B
+// (basis.py:548) of the 8 corners are written to the block's Sint rows, which
+// then park the forward-substitution result y and finally hold S_I.  The
+// conductances of the boundary-interior edges go to Fk (face-major, (u, v)
+// in-face order) for the local Galerkin block.
+constexpr int AROW = 5;
+
+__device__ __forceinline__ int face_off(const Geo& g, int face) {
+  const int ax = face >> 1;
+  const int a0 = 0, a1 = 2 * g.ni2 * g.ni3, a2 = a1 + 2 * g.ni1 * g.ni3;
+  const int sz = ax == 0 ? g.ni2 * g.ni3 : (ax == 1 ? g.ni1 * g.ni3 : g.ni1 * g.ni2);
+  return (ax == 0 ? a0 : (ax == 1 ? a1 : a2)) + (face & 1) * sz;
+}
+
+__device__ __forceinline__ void stencil_table(const Geo& g, const double* __restrict__ w, int X0, int Y0, int Z0,
+                                              int NR, double* As, double* Fk, double* Sb, int lane) {
+  const double s1 = g.ih1 * g.ih1, s2 = g.ih2 * g.ih2, s3 = g.ih3 * g.ih3;
+  for (int i = lane; i < NR; i += 32) {
+    double* row = As + i * AROW;
+    if (i >= g.nI) {
+      row[0] = 1.0;
+      row[1] = row[2] = row[3] = row[4] = 0.0;
+      continue;
+    }
+    int x, y, z;
+    decode3f(i, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+    ++x; ++y; ++z;
+    const long long I = X0 + x, J = Y0 + y, K = Z0 + z;
+    const double kxm = __ldg(w + ex_id(g, I - 1, J, K)) * s1;
+    const double kxp = __ldg(w + ex_id(g, I, J, K)) * s1;
+    const double kym = __ldg(w + ey_id(g, I, J - 1, K)) * s2;
+    const double kyp = __ldg(w + ey_id(g, I, J, K)) * s2;
+    const double kzm = __ldg(w + ez_id(g, I, J, K - 1)) * s3;
+    const double kzp = __ldg(w + ez_id(g, I, J, K)) * s3;
+    const double v1 = x > 1 ? -kxm : 0.0, v2 = y > 1 ? -kym : 0.0, v3 = z > 1 ? -kzm : 0.0;
+    const int D2 = g.ni1, D3 = g.p;
+    row[0] = ((((kxm + kxp) + kym) + kyp) + kzm) + kzp;
+    row[1] = v1 + (D2 == 1 ? v2 : 0.0) + (D3 == 1 ? v3 : 0.0);
+    row[2] = v2 + (D3 == D2 ? v3 : 0.0);
+    row[3] = v3;
+    row[4] = 0.0;
+    // boundary-face conductances (x == 1 and x == ni1 may both hold)
+    if (x == 1) Fk[face_off(g, 0) + (z - 1) * g.ni2 + (y - 1)] = kxm;
+    if (x == g.ni1) Fk[face_off(g, 1) + (z - 1) * g.ni2 + (y - 1)] = kxp;
+    if (y == 1) Fk[face_off(g, 2) + (z - 1) * g.ni1 + (x - 1)] = kym;
+    if (y == g.ni2) Fk[face_off(g, 3) + (z - 1) * g.ni1 + (x - 1)] = kyp;
+    if (z == 1) Fk[face_off(g, 4) + (y - 1) * g.ni1 + (x - 1)] = kzm;
+    if (z == g.ni3) Fk[face_off(g, 5) + (y - 1) * g.ni1 + (x - 1)] = kzp;
+    // Lagrange rhs of corner cc: sum over boundary faces of k_f * hat_cc(face
+    // point); the face-normal hat factor is exactly 1 or 0
+    const double fx0 = x == 1 ? kxm : 0.0, fx1 = x == g.ni1 ? kxp : 0.0;
+    const double fy0 = y == 1 ? kym : 0.0, fy1 = y == g.ni2 ? kyp : 0.0;
+    const double fz0 = z == 1 ? kzm : 0.0, fz1 = z == g.ni3 ? kzp : 0.0;
+    const double hx0 = hatf1(x, g.ib1), hx1 = hatf1(x - g.b1, g.ib1);
+    const double hy0 = hatf1(y, g.ib2), hy1 = hatf1(y - g.b2, g.ib2);
+    const double hz0 = hatf1(z, g.ib3), hz1 = hatf1(z - g.b3, g.ib3);
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const bool cx = cc & 1, cy = cc & 2, cz = cc & 4;
+      const double hx = cx ? hx1 : hx0, hy = cy ? hy1 : hy0, hz = cz ? hz1 : hz0;
+      double v = 0.0;
+      v += (cx ? 0.0 : fx0) * (hy * hz);
+      v += (cx ? fx1 : 0.0) * (hy * hz);
+      v += (cy ? 0.0 : fy0) * (hx * hz);
+      v += (cy ? fy1 : 0.0) * (hx * hz);
+      v += (cz ? 0.0 : fz0) * (hx * hy);
+      v += (cz ? fz1 : 0.0) * (hx * hy);
+      Sb[(size_t)cc * g.nI + i] = v;
+    }
   }
-  const int c = crd[i];
-  r.x = c & 1023;
-  r.y = (c >> 10) & 1023;
-  r.z = c >> 20;
-  const long long I = X0 + r.x, J = Y0 + r.y, K = Z0 + r.z;
-  r.kxm = __ldg(w + ex_id(g, I - 1, J, K)) * g.ih1 * g.ih1;
-  r.kxp = __ldg(w + ex_id(g, I, J, K)) * g.ih1 * g.ih1;
-  r.kym = __ldg(w + ey_id(g, I, J - 1, K)) * g.ih2 * g.ih2;
-  r.kyp = __ldg(w + ey_id(g, I, J, K)) * g.ih2 * g.ih2;
-  r.kzm = __ldg(w + ez_id(g, I, J, K - 1)) * g.ih3 * g.ih3;
-  r.kzp = __ldg(w + ez_id(g, I, J, K)) * g.ih3 * g.ih3;
-  return r;
 }
 
-// A_II[i][l] for l <= i (padding rows are identity).
-__device__ __forceinline__ double a_entry(const Geo& g, const Row& r, int i, int l) {
-  if (!r.valid) return i == l ? 1.0 : 0.0;
-  if (l > i) return 0.0;
-  const int d = i - l;
-  if (d == 0) return ((((r.kxm + r.kxp) + r.kym) + r.kyp) + r.kzm) + r.kzp;
-  double v = 0.0;
-  if (d == 1 && r.x > 1) v -= r.kxm;
-  if (d == g.ni1 && r.y > 1) v -= r.kym;
-  if (d == g.p && r.z > 1) v -= r.kzm;
-  return v;
+// Stencil-table slot of A(i, i - d) (4 = structural zero).
+__device__ __forceinline__ unsigned sel_code(const Geo& g, int d) {
+  return d == 0 ? 0u : d == 1 ? 1u : d == g.ni1 ? 2u : d == g.p ? 3u : 4u;
 }
 
-// Lagrange right-hand side -A_IB x_B (basis.py:548) of node row r, corner cc.
-__device__ __forceinline__ double rhs_entry(const Geo& g, const Row& r, int cc) {
-  if (!r.valid) return 0.0;
-  double v = 0.0;
-  if (r.x == 1) v += r.kxm * hatf(g, cc, 0, r.y, r.z);
-  if (r.x == g.ni1) v += r.kxp * hatf(g, cc, g.b1, r.y, r.z);
-  if (r.y == 1) v += r.kym * hatf(g, cc, r.x, 0, r.z);
-  if (r.y == g.ni2) v += r.kyp * hatf(g, cc, r.x, g.b2, r.z);
-  if (r.z == 1) v += r.kzm * hatf(g, cc, r.x, r.y, 0);
-  if (r.z == g.ni3) v += r.kzp * hatf(g, cc, r.x, r.y, g.b3);
-  return v;
+// Transposed right-hand-side tile I of corner column c = lane/4 (rows 8I+2q, +1).
+__device__ __forceinline__ F2 ld_rt(const Geo& g, const double* Sb, int I, int lane) {
+  const int c = lane >> 2, r0 = 8 * I + 2 * (lane & 3);
+  const double* p = Sb + (size_t)c * g.nI + r0;
+  return {r0 < g.nI ? __ldcg(p) : 0.0, r0 + 1 < g.nI ? __ldcg(p + 1) : 0.0};
+}
+__device__ __forceinline__ void st_rt(const Geo& g, double* Sb, int I, int lane, const F2& v) {
+  const int c = lane >> 2, r0 = 8 * I + 2 * (lane & 3);
+  double* p = Sb + (size_t)c * g.nI + r0;
+  if (r0 < g.nI) p[0] = v.x;
+  if (r0 + 1 < g.nI) p[1] = v.y;
 }
 
-// Cholesky of one 8x8 SPD tile (accumulator layout); returns L^{-1} as an
-// A-frag.  Lanes 0..7 own rows of L in registers (shuffle right-looking
-// factorization, rsqrt pivots), then columns of L^{-1}; shared memory is used
-// only to re-layout the tile.
+// Cholesky of one 8x8 SPD tile (C layout); returns L^{-1} in C layout.  Lanes
+// 0..7 own rows of L in registers (shuffle right-looking factorization, rsqrt
+// pivots), then columns of L^{-1}; shared memory re-lays the tile.
 template <int C>
 __device__ __forceinline__ void p8_step(double (&x)[8], double& invd, int r, bool& bad) {
   if constexpr (C < 8) {
@@ -180,9 +202,7 @@ __device__ __forceinline__ void i8_step(double (&d)[8], int c, const double* Ds,
 }
 
 __device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, int lane, int* flags) {
-  const int m = lane >> 2, n0 = 2 * (lane & 3);
-  Ds[m * 8 + n0] = t.x;
-  Ds[m * 8 + n0 + 1] = t.y;
+  st2(Ds + lane * 2, t);
   __syncwarp();
   const int r = lane & 7;
   double x[8];
@@ -206,8 +226,7 @@ __device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, in
     for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = d[rr];
   }
   __syncwarp();
-  const int k = lane & 3;
-  F2 li = {Is[m * 8 + k], Is[m * 8 + 4 + k]};
+  const F2 li = ld2(Is + lane * 2);
   __syncwarp();
   return li;
 }
@@ -219,73 +238,80 @@ __device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, in
 template <int PT>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
-           double* __restrict__ Ysc, double* __restrict__ Kloc, int* __restrict__ flags) {
-  __shared__ double Dsh[TC_WARPS][64];
-  __shared__ double Ish[TC_WARPS][72];
+           double* __restrict__ Kloc, int* __restrict__ flags) {
+  __shared__ __align__(16) double Dsh[TC_WARPS][64];
+  __shared__ __align__(16) double Ish[TC_WARPS][72];
   extern __shared__ __align__(16) double tcsm[];
-  int* crd = reinterpret_cast<int*>(tcsm + (size_t)TC_WARPS * g.nI * 8);
-  fill_coords(g, crd);
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* Sx = tcsm + (size_t)wid * g.nI * 8;     // this block's interior basis values [a][corner]
   const int jb = blockIdx.x * TC_WARPS + wid;
   if (jb >= g.nbl) return;
+  const int NTI = (g.nI + 7) >> 3, NR = 8 * NTI;
+  const int NF = face_off(g, 5) + g.ni1 * g.ni2;
+  double* As = tcsm + (size_t)wid * (NR * AROW + NF);
+  double* Fk = As + NR * AROW;
+  double* Sb = Sint + (size_t)jb * 8 * g.nI;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int NTI = (g.nI + 7) >> 3;
-  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  const int m = lane >> 2, q = lane & 3;
   double* Ds = Dsh[wid];
   double* Is = Ish[wid];
+  stencil_table(g, w, X0, Y0, Z0, NR, As, Fk, Sb, lane);
+  __syncwarp();
   // tile offsets (I - K) that can hold stencil entries: d in {0, 1, ni1, p}
   unsigned omask = 1u;
   {
     const int ds[3] = {g.ni1 >= 2 ? 1 : 0, g.ni2 >= 2 ? g.ni1 : 0, g.ni3 >= 2 ? g.p : 0};
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int d = ds[q];
+    for (int s = 0; s < 3; ++s) {
+      const int d = ds[s];
       if (d <= 0) continue;
-      for (int o = (d - 7 + 7) / 8; o <= (d + 7) / 8; ++o) omask |= 1u << o;
+      for (int o = d / 8; o <= (d + 7) / 8; ++o) omask |= 1u << o;
     }
   }
+  // per-lane table slots of the entering row: element (b, s) of W[PT][b]
+  // is A(i, i - d) with d = 8 (PT - b) + m - 2q - s
+  unsigned long long sel = 0;
+#pragma unroll
+  for (int b = 0; b <= PT; ++b)
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      sel |= (unsigned long long)sel_code(g, 8 * (PT - b) + m - 2 * q - s) << (6 * b + 3 * s);
+  // tile (I, I - (PT - b)) of A, C layout, from the stencil table
+  auto fetch = [&](int I, int b) -> F2 {
+    const double* row = As + (8 * I + m) * AROW;
+    return {row[(sel >> (6 * b)) & 7u], row[(sel >> (6 * b + 3)) & 7u]};
+  };
+  F2 G = {0.0, 0.0};                   // sum_J y_J^T y_J  (= R^T S_I, see the Galerkin block)
   if (NTI > 0) {
     F2 W[PT + 1][PT + 1];
-    F2 R[PT + 1];
-    // ---- initial window: tile rows 0..PT
+    F2 Rt[PT + 1];
 #pragma unroll
     for (int a = 0; a <= PT; ++a) {
-      const int i = 8 * a + m;
-      Row rw = load_row(g, w, crd, X0, Y0, Z0, i);
 #pragma unroll
       for (int b = 0; b <= PT; ++b) {
-        if (b <= a && ((omask >> (a - b)) & 1u)) {
-          const int l = 8 * b + n0;
-          W[a][b] = {a_entry(g, rw, i, l), a_entry(g, rw, i, l + 1)};
-        } else {
-          W[a][b] = {0.0, 0.0};
-        }
+        W[a][b] = {0.0, 0.0};
+        if (b <= a && ((omask >> (a - b)) & 1u)) W[a][b] = fetch(a, PT - a + b);
       }
-      R[a] = {rhs_entry(g, rw, n0), rhs_entry(g, rw, n0 + 1)};
+      Rt[a] = ld_rt(g, Sb, a, lane);
     }
     for (int J = 0; J < NTI; ++J) {
-      // prefetch the stencil row entering the window at the end of this step
-      const int inext = 8 * (J + 1 + PT) + m;
-      Row rn = load_row(g, w, crd, X0, Y0, Z0, inext);
-
+      const int In = J + 1 + PT;       // tile row entering the window after this step
+      const F2 nR = In < NTI ? ld_rt(g, Sb, In, lane) : F2{0.0, 0.0};
       const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, flags);
       F2 X[PT + 1];
 #pragma unroll
       for (int t = 1; t <= PT; ++t) {
-        F2 c = {0.0, 0.0};
-        mma(c, c_to_a(W[t][0], lane), Li);     // X_t = A_t L^{-T}
-        X[t] = c_to_a(c, lane);
+        X[t] = {0.0, 0.0};
+        mma(X[t], W[t][0], Li);                // X_t = A_t L^{-T}
       }
-      // fused forward substitution for the 8 Lagrange columns
-      F2 Yc = {0.0, 0.0};
-      mma(Yc, Li, c_to_b(R[0], lane));         // y_J = L_JJ^{-1} r_J
+      // fused forward substitution of the 8 Lagrange columns (transposed)
+      F2 Yt = {0.0, 0.0};
+      mma(Yt, Rt[0], Li);                      // y^T = r^T L^{-T}
+      mma(G, Yt, Yt);
       {
-        const F2 Yb = c_to_b(Yc, lane);
+        const F2 nY = neg(Yt);
 #pragma unroll
-        for (int t = 1; t <= PT; ++t) mma(R[t], neg(X[t]), Yb);
+        for (int t = 1; t <= PT; ++t) mma(Rt[t], nY, X[t]);   // r_t^T -= y^T X_t^T
       }
       // trailing update of the register window
 #pragma unroll
@@ -294,75 +320,60 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 #pragma unroll
         for (int b = 1; b <= a; ++b) mma(W[a][b], nXa, X[b]);
       }
-      // factor tiles and y to global memory
       {
-        double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
-        st2(Lt + lane * 2, Li);
+        double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64 + lane * 2;
+        st2(Lt, Li);
 #pragma unroll
-        for (int t = 1; t <= PT; ++t) st2(Lt + t * 64 + lane * 2, X[t]);
-        st2(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2, Yc);
+        for (int t = 1; t <= PT; ++t) st2(Lt + t * 64, X[t]);
+        st_rt(g, Sb, J, lane, Yt);             // y parks in the consumed rhs rows
       }
       // slide the window by one tile
 #pragma unroll
       for (int a = 1; a <= PT; ++a) {
 #pragma unroll
         for (int b = 1; b <= a; ++b) W[a - 1][b - 1] = W[a][b];
-        R[a - 1] = R[a];
+        Rt[a - 1] = Rt[a];
       }
-      {
-        const int In = J + 1 + PT;
 #pragma unroll
-        for (int b = 0; b <= PT; ++b) {
-          if ((omask >> (PT - b)) & 1u) {
-            const int l = 8 * (In - PT + b) + n0;
-            W[PT][b] = {a_entry(g, rn, inext, l), a_entry(g, rn, inext, l + 1)};
-          } else {
-            W[PT][b] = {0.0, 0.0};
-          }
-        }
-        R[PT] = {rhs_entry(g, rn, n0), rhs_entry(g, rn, n0 + 1)};
-      }
+      for (int b = 0; b <= PT; ++b)
+        W[PT][b] = (In < NTI && ((omask >> (PT - b)) & 1u)) ? fetch(In, b) : F2{0.0, 0.0};
+      Rt[PT] = nR;
     }
     __syncwarp();
-    // ---- backward substitution L^T x = y, window of solved tiles as B-frags;
-    // the next step's factor tiles are prefetched into registers.
+    // ---- backward substitution x_J^T = (y_J^T - sum_t x_{J+t}^T X_t) L_JJ^{-1};
+    // the window keeps -x^T of the last PT tiles; the next step's transposed
+    // factor tiles and y are prefetched into registers.
     F2 Xw[PT > 0 ? PT : 1];
 #pragma unroll
     for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
-    F2 nLt[PT + 1], nY;
-    {
-      const int J = NTI - 1;
-      const double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
+    F2 nLt[2][PT + 1], nY[2];
+    auto load_bwd = [&](int J, F2 (&Lt)[PT + 1], F2& Y) {
+      const double* p = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
 #pragma unroll
-      for (int t = 0; t <= PT; ++t) nLt[t] = (t == 0 || J + t < NTI) ? ld2cg(Lt + t * 64 + lane * 2) : F2{0.0, 0.0};
-      nY = ld2cg(Ysc + ((size_t)jb * NTI + J) * 64 + lane * 2);
-    }
+      for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld_t(p + t * 64, lane) : F2{0.0, 0.0};
+      Y = ld_rt(g, Sb, J, lane);
+    };
+    load_bwd(NTI - 1, nLt[0], nY[0]);
+    if (NTI > 1) load_bwd(NTI - 2, nLt[1], nY[1]);
     for (int J = NTI - 1; J >= 0; --J) {
       F2 cLt[PT + 1];
 #pragma unroll
-      for (int t = 0; t <= PT; ++t) cLt[t] = nLt[t];
-      F2 acc = nY;
-      if (J > 0) {
-        const double* Lt = LT + ((size_t)jb * NTI + J - 1) * (PT + 1) * 64;
-#pragma unroll
-        for (int t = 0; t <= PT; ++t) nLt[t] = (t == 0 || J - 1 + t < NTI) ? ld2cg(Lt + t * 64 + lane * 2) : F2{0.0, 0.0};
-        nY = ld2cg(Ysc + ((size_t)jb * NTI + J - 1) * 64 + lane * 2);
+      for (int t = 0; t <= PT; ++t) {
+        cLt[t] = nLt[0][t];
+        nLt[0][t] = nLt[1][t];
       }
+      F2 acc = nY[0];
+      nY[0] = nY[1];
+      if (J > 1) load_bwd(J - 2, nLt[1], nY[1]);
 #pragma unroll
-      for (int t = 1; t <= PT; ++t) {
-        if (J + t < NTI) mma(acc, neg(a_to_t(cLt[t], lane)), Xw[t - 1]);
-      }
+      for (int t = 1; t <= PT; ++t)
+        if (J + t < NTI) mma(acc, Xw[t - 1], cLt[t]);
       F2 xj = {0.0, 0.0};
-      mma(xj, a_to_t(cLt[0], lane), c_to_b(acc, lane));
-      const int a0 = 8 * J + m;
-      if (a0 < g.nI) {
-        Sint[((size_t)jb * 8 + n0) * g.nI + a0] = xj.x;
-        Sint[((size_t)jb * 8 + n0 + 1) * g.nI + a0] = xj.y;
-        st2(Sx + a0 * 8 + n0, xj);
-      }
+      mma(xj, acc, cLt[0]);
+      st_rt(g, Sb, J, lane, xj);
 #pragma unroll
       for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
-      if (PT > 0) Xw[0] = c_to_b(xj, lane);
+      if (PT > 0) Xw[0] = neg(xj);
     }
     __syncwarp();
   }
@@ -370,46 +381,42 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   // ---- local Galerkin block K_j = sum_{owned e} (w_e/h^2) dS_e dS_e^T (interior part).
   // Edges touching the interior contribute S_I^T(A S)_I + S_B^T(A^I S)_B and
   // (A S)_I = 0 is the local problem just solved, so only the boundary-interior
-  // edges remain: k_e S(x_e) (S(x_e) - S(i_e))^T.  Skeleton-only owned edges
-  // contribute k_e dH dH^T with the model-independent hats.  DMMA reduction,
-  // 4 edges (k) x 8 corners per instruction: lane (corner cc = lane/4, edge
-  // slot lane%4).
+  // edges remain: sum_e k_e h(x_e) (h(x_e) - S_I(i_e))^T = B - R^T S_I with
+  // B = sum_e k_e h h^T and R the Lagrange rhs; R^T S_I = R^T A_II^-1 R = Y^T Y
+  // with Y = L^-1 R, accumulated during the forward sweep (G).  Skeleton-only
+  // owned edges (model-independent hats) are added by k_skel_galerkin.
+  // B is a DMMA reduction, 4 edges (k) x 8 corners per instruction: lane
+  // (corner cc = lane/4, edge slot lane%4).
   const int cc = lane >> 2, slot = lane & 3;
+  const int cx = cc & 1, cy = (cc >> 1) & 1, cz = (cc >> 2) & 1;
   F2 K = {0.0, 0.0};
-  // (1) boundary-interior edges, face by face
 #pragma unroll 1
   for (int face = 0; face < 6; ++face) {
     const int ax = face >> 1, hi = face & 1;
     const int nu = ax == 0 ? g.ni2 : g.ni1, nv = ax == 2 ? g.ni2 : g.ni3;
     const int tot = nu * nv;
-    const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
+    // hat factors: face normal exactly 0/1, in-face axes u, v
+    const bool on = (ax == 0 ? cx : (ax == 1 ? cy : cz)) == hi;
+    const int cu = ax == 0 ? cy * g.b2 : cx * g.b1, cv = ax == 2 ? cy * g.b2 : cz * g.b3;
+    const double ibu = ax == 0 ? g.ib2 : g.ib1, ibv = ax == 2 ? g.ib2 : g.ib3;
+    const double* F = Fk + face_off(g, face);
+    int u = 1 + slot, v = 1;
+    while (u > nu) { u -= nu; ++v; }
     for (int base = 0; base < tot; base += 4) {
       const int f = base + slot;
       double a = 0.0, b = 0.0;
-      if (f < tot) {
-        const int u = 1 + f % nu, v = 1 + f / nu;
-        int xb, yb, zb, xi, yi, zi, xe, ye, ze;
-        if (ax == 0) {
-          xb = hi ? g.b1 : 0; yb = u; zb = v; xi = hi ? g.b1 - 1 : 1; yi = u; zi = v;
-        } else if (ax == 1) {
-          xb = u; yb = hi ? g.b2 : 0; zb = v; xi = u; yi = hi ? g.b2 - 1 : 1; zi = v;
-        } else {
-          xb = u; yb = v; zb = hi ? g.b3 : 0; xi = u; yi = v; zi = hi ? g.b3 - 1 : 1;
-        }
-        xe = min(xb, xi); ye = min(yb, yi); ze = min(zb, zi);
-        const long long e = ax == 0 ? ex_id(g, X0 + xe, Y0 + ye, Z0 + ze)
-                                    : (ax == 1 ? ey_id(g, X0 + xe, Y0 + ye, Z0 + ze) : ez_id(g, X0 + xe, Y0 + ye, Z0 + ze));
-        const double sb = hatf(g, cc, xb, yb, zb);
-        const double si = Sx[interior_index(g, xi, yi, zi) * 8 + cc];
-        b = sb - si;
-        a = (__ldg(w + e) * ihs) * sb;
+      if (f < tot && on) {
+        b = hatf1(u - cu, ibu) * hatf1(v - cv, ibv);
+        a = F[f] * b;
       }
       mma884(K.x, K.y, a, b);
+      u += 4;
+      while (u > nu) { u -= nu; ++v; }
     }
   }
-  // (2) skeleton-only owned edges: added by k_skel_galerkin (model-independent hats)
-  Kloc[(size_t)jb * 64 + m * 8 + n0] = K.x;
-  Kloc[(size_t)jb * 64 + m * 8 + n0 + 1] = K.y;
+  K.x -= G.x;
+  K.y -= G.y;
+  st2(Kloc + (size_t)jb * 64 + lane * 2, K);
 }
 
 // ------------------------------------------------------- skeleton Galerkin
@@ -475,7 +482,9 @@ __global__ void __launch_bounds__(64) k_skel_galerkin(Geo g, const double* __res
 // out = blockdiag(A_II^{-1}) rhs on block interiors (full node fields); out
 // may alias rhs.  NCH chunks of 8 right-hand sides ride through one sweep so
 // each factor tile is read once per NCH*8 sources; the next step's tiles are
-// prefetched into registers.  y is parked in out between the sweeps.
+// prefetched into registers.  Right-hand sides are carried transposed (lane
+// 4c+q: rows 8I+2q, 8I+2q+1 of column c) so every product is X Y^T of two
+// C-layout tiles (see ld_t).  y is parked in out between the sweeps.
 template <int PT, int NCH>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs) {
@@ -489,64 +498,69 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
   if (NTI == 0) return;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  const int c = lane >> 2, q = lane & 3;
   auto node_of = [&](int a) -> long long {
-    const int c = crd[a];
-    return node_id(g, X0 + (c & 1023), Y0 + ((c >> 10) & 1023), Z0 + (c >> 20));
+    if (a >= g.nI) return -1;
+    const int v = crd[a];
+    return node_id(g, X0 + (v & 1023), Y0 + ((v >> 10) & 1023), Z0 + (v >> 20));
   };
   const double* LTb = LT + (size_t)jb * NTI * (PT + 1) * 64;
-  auto load_step = [&](int J, F2* Lt) {
+  auto load_fwd = [&](int J, F2* Lt) {
     const double* p = LTb + (size_t)J * (PT + 1) * 64 + lane * 2;
 #pragma unroll
     for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld2(p + t * 64) : F2{0.0, 0.0};
   };
+  auto load_bwd = [&](int J, F2* Lt) {
+    const double* p = LTb + (size_t)J * (PT + 1) * 64;
+#pragma unroll
+    for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld_t(p + t * 64, lane) : F2{0.0, 0.0};
+  };
   for (int s0 = 0; s0 < nrhs; s0 += 8 * NCH) {
     auto load_tile = [&](const double* src, int I, F2* v) {
-      const int a = 8 * I + m;
-      long long nd = (a < g.nI) ? node_of(a) : -1;
+      const long long n0 = node_of(8 * I + 2 * q), n1 = node_of(8 * I + 2 * q + 1);
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const int sA = s0 + 8 * ch + n0;
+        const int col = s0 + 8 * ch + c;
         v[ch] = {0.0, 0.0};
-        if (nd >= 0) {
-          if (sA < nrhs) v[ch].x = src[nd * nrhs + sA];
-          if (sA + 1 < nrhs) v[ch].y = src[nd * nrhs + sA + 1];
+        if (col < nrhs) {
+          if (n0 >= 0) v[ch].x = src[n0 * nrhs + col];
+          if (n1 >= 0) v[ch].y = src[n1 * nrhs + col];
         }
       }
     };
     auto store_tile = [&](int I, const F2* v) {
-      const int a = 8 * I + m;
-      if (a >= g.nI) return;
-      const long long nd = node_of(a);
+      const long long n0 = node_of(8 * I + 2 * q), n1 = node_of(8 * I + 2 * q + 1);
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const int sA = s0 + 8 * ch + n0;
-        if (sA < nrhs) out[nd * nrhs + sA] = v[ch].x;
-        if (sA + 1 < nrhs) out[nd * nrhs + sA + 1] = v[ch].y;
+        const int col = s0 + 8 * ch + c;
+        if (col < nrhs) {
+          if (n0 >= 0) out[n0 * nrhs + col] = v[ch].x;
+          if (n1 >= 0) out[n1 * nrhs + col] = v[ch].y;
+        }
       }
     };
     F2 R[PT + 1][NCH];
 #pragma unroll
     for (int a = 0; a <= PT; ++a) load_tile(rhs, a, R[a]);
     F2 nL[PT + 1];
-    load_step(0, nL);
-    // forward: y_J = L_JJ^{-1} r_J ; r_{J+t} -= L_{J+t,J} y_J
+    load_fwd(0, nL);
+    // forward: y_J^T = r_J^T L_JJ^{-T} ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
     for (int J = 0; J < NTI; ++J) {
       F2 cL[PT + 1];
 #pragma unroll
       for (int t = 0; t <= PT; ++t) cL[t] = nL[t];
-      if (J + 1 < NTI) load_step(J + 1, nL);
+      if (J + 1 < NTI) load_fwd(J + 1, nL);
       F2 nxt[NCH];
       load_tile(rhs, J + 1 + PT, nxt);            // read ahead before y_J lands (out may alias rhs)
       F2 Yc[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         Yc[ch] = {0.0, 0.0};
-        mma(Yc[ch], cL[0], c_to_b(R[0][ch], lane));
-        const F2 Yb = c_to_b(Yc[ch], lane);
+        mma(Yc[ch], R[0][ch], cL[0]);
+        const F2 nY = neg(Yc[ch]);
 #pragma unroll
         for (int t = 1; t <= PT; ++t)
-          if (J + t < NTI) mma(R[t][ch], neg(cL[t]), Yb);
+          if (J + t < NTI) mma(R[t][ch], nY, cL[t]);
       }
       __syncwarp();
       store_tile(J, Yc);
@@ -558,18 +572,19 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
       for (int ch = 0; ch < NCH; ++ch) R[PT][ch] = nxt[ch];
     }
     __syncwarp();
-    // backward: x_J = L_JJ^{-T} (y_J - sum_t L_{J+t,J}^T x_{J+t})
+    // backward: x_J^T = (y_J^T - sum_t x_{J+t}^T L_{J+t,J}) L_JJ^{-1}; the
+    // window keeps -x^T
     F2 Xw[PT > 0 ? PT : 1][NCH];
 #pragma unroll
     for (int t = 0; t < (PT > 0 ? PT : 1); ++t)
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) Xw[t][ch] = {0.0, 0.0};
-    load_step(NTI - 1, nL);
+    load_bwd(NTI - 1, nL);
     for (int J = NTI - 1; J >= 0; --J) {
       F2 cT[PT + 1];
 #pragma unroll
-      for (int t = 0; t <= PT; ++t) cT[t] = a_to_t(nL[t], lane);   // transposed tiles
-      if (J > 0) load_step(J - 1, nL);
+      for (int t = 0; t <= PT; ++t) cT[t] = nL[t];
+      if (J > 0) load_bwd(J - 1, nL);
       F2 acc[NCH];
       load_tile(out, J, acc);
       F2 xj[NCH];
@@ -577,9 +592,9 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
       for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
         for (int t = 1; t <= PT; ++t)
-          if (J + t < NTI) mma(acc[ch], neg(cT[t]), Xw[t - 1][ch]);
+          if (J + t < NTI) mma(acc[ch], Xw[t - 1][ch], cT[t]);
         xj[ch] = {0.0, 0.0};
-        mma(xj[ch], cT[0], c_to_b(acc[ch], lane));
+        mma(xj[ch], acc[ch], cT[0]);
       }
       __syncwarp();
       store_tile(J, xj);
@@ -589,7 +604,7 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
         for (int ch = 0; ch < NCH; ++ch) Xw[t][ch] = Xw[t - 1][ch];
       if (PT > 0)
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) Xw[0][ch] = c_to_b(xj[ch], lane);
+        for (int ch = 0; ch < NCH; ++ch) Xw[0][ch] = neg(xj[ch]);
     }
     __syncwarp();
   }
@@ -611,16 +626,17 @@ size_t tc_factor_doubles(const Geo& g) {
   const size_t nti = (g.nI + 7) / 8;
   return (size_t)g.nbl * nti * (tc_band(g) + 1) * 64;
 }
-size_t tc_scratch_doubles(const Geo& g) { return (size_t)g.nbl * ((g.nI + 7) / 8) * 64; }
+size_t tc_scratch_doubles(const Geo&) { return 0; }
 
 template <int PT>
-static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc,
+static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
                                      double* Kloc, int* flags, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
-  const size_t smem = (size_t)TC_WARPS * g.nI * 8 * sizeof(double) + (size_t)g.nI * sizeof(int);
+  const size_t nf = 2 * ((size_t)g.ni2 * g.ni3 + (size_t)g.ni1 * g.ni3 + (size_t)g.ni1 * g.ni2);
+  const size_t smem = (size_t)TC_WARPS * (((g.nI + 7) / 8) * 8 * AROW + nf) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_basis_tc<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_basis_tc<PT><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Ysc, Kloc, flags);
+  k_basis_tc<PT><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -641,17 +657,17 @@ static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const doubl
   return cudaGetLastError();
 }
 
-cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Ysc, double* Kloc,
+cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st) {
   switch (tc_band(g)) {
-    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Ysc, Kloc, flags, st);
-    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Ysc, Kloc, flags, st);
+    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, st);
+    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, st);
+    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Kloc, flags, st);
+    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Kloc, flags, st);
+    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Kloc, flags, st);
+    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Kloc, flags, st);
+    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Kloc, flags, st);
+    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Kloc, flags, st);
     default: return cudaErrorInvalidValue;
   }
 }
