@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MSFV_ABI_VERSION 1
+#define MSFV_ABI_VERSION 2
 
 enum msfv_status {
   MSFV_OK = 0,
@@ -150,6 +150,29 @@ MSFV_API int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const d
  * xi: nedges doubles of scratch (the per-edge sums). */
 MSFV_API int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
                        const double* Y, const double* R, int32_t nrhs, double* xi, double* g, void* stream);
+
+/* Interior-only survey fields.  The Lagrange columns solve their local
+ * problems, (A S)_I = 0, so interior_solve(Q - A S T) = blockdiag(A_II^-1) Q_I
+ * and interior_solve(P W - A S y) = blockdiag(A_II^-1) (P W)_I
+ * (forward.py:240-246,278): nonzero only on the blocks whose interiors hold
+ * survey nodes.  Compact fields hold nblocks x nI x nrhs doubles (slot-major).
+ * msfv_points_interior_blocks: number of such blocks of a point set. */
+MSFV_API int msfv_points_interior_blocks(const msfv_points* pts, int64_t* nblocks);
+/* rhs_c = (M Z)_I on the interior slots (Z = NULL: the identity, i.e. M itself) */
+MSFV_API int msfv_points_interior_scatter(const msfv_plan* plan, const msfv_points* pts, const double* Z, int32_t nrhs,
+                                 double* rhs_c, void* stream);
+/* out_c = blockdiag(A_II^-1) rhs_c on the interior slots (out_c may alias rhs_c) */
+MSFV_API int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, const double* factor,
+                               const double* rhs_c, double* out_c, int32_t nrhs, void* stream);
+/* Fused per-block rapply gradient (forward.py:270-281, the msfv_cell_gradient
+ * sum without node fields): g = -sigma C^T xi with
+ *   xi_e = sum_s [dU (dZ + dY) + dR dY] / h_e^2,  U = S T, Y = S y,
+ * Z / R the compact interior fields of pz / pr (NULL when the point set has no
+ * interior blocks).  MSFV_UNSUPPORTED when the block closure does not fit in
+ * shared memory. */
+MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
+                        const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
+                        const msfv_points* pr, const double* Rc, double* g, void* stream);
 
 #ifdef __cplusplus
 }

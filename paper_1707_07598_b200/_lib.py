@@ -63,6 +63,10 @@ SIGNATURES = {
     "msfv_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_restrict_op": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),
     "msfv_cell_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P]),
+    "msfv_points_interior_blocks": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "msfv_points_interior_scatter": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
+    "msfv_points_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P]),
+    "msfv_block_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
 }
 
 _LIB = None

@@ -173,6 +173,26 @@ int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const i
   }
   uptr.push_back(nnz);
   long long nu = (long long)unode.size();
+  // blocks with survey entries on interior nodes (compact per-block fields of
+  // the interior-only solves): slot per block, compact row per unique node
+  std::vector<int> islot(g.nbl, -1), iblk;
+  std::vector<long long> urow(nu, -1);
+  for (long long u = 0; u < nu; ++u) {
+    const long long nd = unode[u];
+    const long long t = uent[uptr[u]];
+    int x, y, z;
+    x = loc[t] & 1023; y = (loc[t] >> 10) & 1023; z = (loc[t] >> 20) & 1023;
+    (void)nd;
+    const int a = interior_index(g, x, y, z);
+    if (a < 0) continue;
+    const int jb = blk[t];
+    if (islot[jb] < 0) {
+      islot[jb] = (int)iblk.size();
+      iblk.push_back(jb);
+    }
+    urow[u] = (long long)islot[jb] * g.nI + a;
+  }
+  const int nib = (int)iblk.size();
 
   // one device allocation for all tables
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
@@ -187,7 +207,10 @@ int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const i
   size_t o_uptr = o_cent + al(cent.size() * 8);
   size_t o_unode = o_uptr + al((nu + 1) * 8);
   size_t o_uent = o_unode + al(nu * 8);
-  size_t total = o_uent + al(nnz * 8) + 256;
+  size_t o_islot = o_uent + al(nnz * 8);
+  size_t o_iblk = o_islot + al((size_t)g.nbl * 4);
+  size_t o_urow = o_iblk + al((size_t)nib * 4);
+  size_t total = o_urow + al(nu * 8) + 256;
   char* mem = nullptr;
   cudaError_t e = cudaMalloc(&mem, total);
   if (e != cudaSuccess) return cuda_check(e, "cudaMalloc(points)");
@@ -201,7 +224,8 @@ int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const i
                       up(o_blk, blk.data(), nnz * 4),          up(o_loc, loc.data(), nnz * 4),
                       up(o_cptr, cptr.data(), (g.kc + 1) * 8), up(o_cent, cent.data(), cent.size() * 8),
                       up(o_uptr, uptr.data(), (nu + 1) * 8),   up(o_unode, unode.data(), nu * 8),
-                      up(o_uent, uent.data(), nnz * 8)};
+                      up(o_uent, uent.data(), nnz * 8),        up(o_islot, islot.data(), (size_t)g.nbl * 4),
+                      up(o_iblk, iblk.data(), (size_t)nib * 4), up(o_urow, urow.data(), nu * 8)};
   for (cudaError_t x : es)
     if (x != cudaSuccess) {
       cudaFree(mem);
@@ -223,6 +247,10 @@ int msfv_points_create(const msfv_plan* plan, int64_t nnz, int32_t ncol, const i
   P->d.uptr = (const long long*)(mem + o_uptr);
   P->d.unode = (const long long*)(mem + o_unode);
   P->d.uent = (const long long*)(mem + o_uent);
+  P->d.nib = nib;
+  P->d.islot = (const int*)(mem + o_islot);
+  P->d.iblk = (const int*)(mem + o_iblk);
+  P->d.urow = (const long long*)(mem + o_urow);
   *out = P;
   return MSFV_OK;
 }
@@ -346,6 +374,43 @@ int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double*
   CHECK_PLAN(plan);
   return cuda_check(launch_cell_gradient(plan->g, sigma, U, Z, Y, R, nrhs, xi, g, (cudaStream_t)stream),
                     "cell_gradient");
+}
+
+int msfv_points_interior_blocks(const msfv_points* pts, int64_t* nblocks) {
+  if (!pts || !nblocks) return fail(MSFV_SHAPE, "null points");
+  *nblocks = pts->d.nib;
+  return MSFV_OK;
+}
+
+int msfv_points_interior_scatter(const msfv_plan* plan, const msfv_points* pts, const double* Z, int32_t nrhs,
+                                 double* rhs_c, void* stream) {
+  CHECK_PLAN(plan);
+  if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior scatter arguments");
+  return cuda_check(launch_points_scatter_interior(plan->g, pts->d, Z, nrhs, rhs_c, (cudaStream_t)stream),
+                    "points_interior_scatter");
+}
+
+int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, const double* factor,
+                               const double* rhs_c, double* out_c, int32_t nrhs, void* stream) {
+  CHECK_PLAN(plan);
+  if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
+  const Geo& g = plan->g;
+  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "compact interior solve needs the tensor-core band path");
+  return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk, pts->d.nib),
+                    "points_interior_solve");
+}
+
+int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
+                        const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
+                        const msfv_points* pr, const double* Rc, double* g, void* stream) {
+  CHECK_PLAN(plan);
+  if (nrhs < 0) return fail(MSFV_SHAPE, "bad gradient arguments");
+  const Geo& gg = plan->g;
+  if (!grad_supported(gg, nrhs)) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
+  const bool hz = pz && pz->d.nib > 0 && Zc, hr = pr && pr->d.nib > 0 && Rc;
+  return cuda_check(launch_grad_block(gg, Sint, T, y, nrhs, sigma, hz ? pz->d.islot : nullptr, Zc,
+                                      hr ? pr->d.islot : nullptr, Rc, g, (cudaStream_t)stream),
+                    "block_gradient");
 }
 
 }  // extern "C"

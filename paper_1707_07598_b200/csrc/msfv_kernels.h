@@ -53,7 +53,7 @@ size_t tc_scratch_doubles(const Geo& g);
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st);
 cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
-                                  cudaStream_t st);
+                                  cudaStream_t st, const int* blist = nullptr, int nlist = 0);
 
 // coarse (msfv_coarse.cu)
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
@@ -79,6 +79,10 @@ struct PointsDev {
   const long long* uptr;     // [nu+1]
   const long long* unode;    // [nu]
   const long long* uent;     // [nnz] entry ids grouped by node
+  int nib;                   // blocks with entries on interior nodes
+  const int* islot;          // [nbl] compact slot of a block or -1
+  const int* iblk;           // [nib] block of a slot
+  const long long* urow;     // [nu] compact row slot*nI + a of a unique node or -1
 };
 cudaError_t launch_points_receive(const Geo& g, const PointsDev& P, const double* Sint, const double* Y,
                                   const double* Xf, int nrhs, double* out, cudaStream_t st);
@@ -86,5 +90,16 @@ cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const doubl
                                    int nrhs, double* out, cudaStream_t st);
 cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* field,
                                   cudaStream_t st);
+// compact interior fields of the survey's interior blocks (zeroed, then scattered)
+cudaError_t launch_points_scatter_interior(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* rhs_c,
+                                           cudaStream_t st);
+
+// fused per-block gradient (msfv_grad.cu)
+constexpr int GRAD_THREADS = 256;
+size_t grad_smem_doubles(const Geo& g, int nrhs);
+bool grad_supported(const Geo& g, int nrhs);
+cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T, const double* Y, int nrhs,
+                              const double* sigma, const int* zslot, const double* Zc, const int* rslot,
+                              const double* Rc, double* gout, cudaStream_t st);
 
 }  // namespace msfv

@@ -84,6 +84,25 @@ __global__ void k_points_scatter(Geo g, PointsDev P, const double* __restrict__ 
   field[P.unode[u] * nrhs + s] = v;
 }
 
+// rhs_c[urow(node)][s] = sum_{t at node} val_t Z[col_t][s] for the interior nodes
+__global__ void k_points_scatter_interior(Geo g, PointsDev P, const double* __restrict__ Z, int nrhs,
+                                          double* __restrict__ rhs_c) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.nu * nrhs) return;
+  int s = (int)(i % nrhs);
+  long long u = i / nrhs;
+  const long long row = P.urow[u];
+  if (row < 0) return;
+  double v = 0.0;
+  for (long long e = P.uptr[u]; e < P.uptr[u + 1]; ++e) {
+    long long t = P.uent[e];
+    int col = P.col[t];
+    double z = Z ? Z[(size_t)col * nrhs + s] : (col == s ? 1.0 : 0.0);
+    v += P.val[t] * z;
+  }
+  rhs_c[row * nrhs + s] = v;
+}
+
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t launch_points_receive(const Geo& g, const PointsDev& P, const double* Sint, const double* Y,
@@ -107,6 +126,16 @@ cudaError_t launch_points_scatter(const Geo& g, const PointsDev& P, const double
   long long tot = P.nu * nrhs;
   if (tot == 0) return cudaSuccess;
   k_points_scatter<<<nblk(tot, 128), 128, 0, st>>>(g, P, Z, nrhs, field);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_points_scatter_interior(const Geo& g, const PointsDev& P, const double* Z, int nrhs, double* rhs_c,
+                                           cudaStream_t st) {
+  if (P.nib == 0 || nrhs == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(rhs_c, 0, (size_t)P.nib * g.nI * nrhs * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  k_points_scatter_interior<<<nblk(P.nu * nrhs, 128), 128, 0, st>>>(g, P, Z, nrhs, rhs_c);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -90,6 +90,9 @@ class Points:
                                         ctypes.byref(h)), "points_create")
         self.handle = h
         self._fin = weakref.finalize(self, L.msfv_points_destroy, h)
+        nib = ctypes.c_int64()
+        _lib.check(L.msfv_points_interior_blocks(h, ctypes.byref(nib)), "points_interior_blocks")
+        self.interior_blocks = int(nib.value)     # blocks with survey nodes in their interior
 
 
 class Engine:
@@ -262,6 +265,32 @@ class Engine:
         with phase("cell_gradient"):
             _lib.check(self.L.msfv_cell_gradient(self.plan, ptr(sigma), ptr(U), ptr(Z), ptr(Y), ptr(R), nrhs,
                                                  ptr(xi), ptr(g), stream()), "cell_gradient")
+        return g
+
+    def interior_fields(self, pts, factor, Z=None, nrhs=None):
+        """Compact blockdiag(A_II^-1) (M Z)_I on the point set's interior blocks
+        (None when it has none)."""
+        nrhs = nrhs if nrhs is not None else (Z.shape[1] if Z is not None else pts.ncol)
+        if pts.interior_blocks == 0:
+            return None
+        rc = self.empty(pts.interior_blocks * self.nI * max(nrhs, 1))
+        with phase("interior_solve"):
+            _lib.check(self.L.msfv_points_interior_scatter(self.plan, pts.handle, ptr(Z), nrhs, ptr(rc), stream()),
+                       "points_interior_scatter")
+            _lib.check(self.L.msfv_points_interior_solve(self.plan, pts.handle, ptr(factor), ptr(rc), ptr(rc), nrhs,
+                                                         stream()), "points_interior_solve")
+        return rc
+
+    def block_gradient(self, sigma, Sint, T, y, pz=None, Zc=None, pr=None, Rc=None):
+        """Fused per-block rapply gradient; raises NotImplementedError when the
+        block closure does not fit in shared memory."""
+        nrhs = T.shape[1]
+        g = self.empty(self.Nm)
+        with phase("block_gradient"):
+            _lib.check(self.L.msfv_block_gradient(self.plan, ptr(sigma), ptr(Sint), ptr(T), ptr(y), nrhs,
+                                                  None if pz is None else pz.handle, ptr(Zc),
+                                                  None if pr is None else pr.handle, ptr(Rc), ptr(g), stream()),
+                       "block_gradient")
         return g
 
     def basis_csc(self, Sint, src, hatv):

@@ -206,12 +206,32 @@ class AdaptiveSensitivity:
         self.state, self.survey, self.basis, self.engine = state, survey, basis, eng
         self.workers = workers
         _, _, self.sigma, self.w = op._dev
-        self.Pp, self.Qp, Qf = survey.device(eng)
-        ns = survey.n_sources
-        self.U = eng.prolong(basis.Sint, state.T_dev)                               # S T (forward.py:241)
-        R = eng.residual(Qf, 1.0, self.w, self.U, -1.0, ns)                         # Q - A U (forward.py:243)
-        self.ZR = eng.interior_solve(basis.factor, R)                         # interior_solve(R) (:246)
-        self.UR = self.U + self.ZR
+        self.Pp, self.Qp, self._Qf = survey.device(eng)
+        # interior_solve(Q - A S T) = blockdiag(A_II^-1) Q_I since (A S)_I = 0
+        # (Lagrange local problems, basis.py:548): compact, on the source blocks only
+        self.Rc = eng.interior_fields(self.Qp, basis.factor, None, survey.n_sources)
+        self._U = self._ZR = self._UR = None
+
+    # node fields of the forward state (J v only; rapply works block-locally)
+    @property
+    def U(self):
+        if self._U is None:
+            self._U = self.engine.prolong(self.basis.Sint, self.state.T_dev)               # S T (forward.py:241)
+        return self._U
+
+    @property
+    def ZR(self):
+        if self._ZR is None:
+            eng, ns = self.engine, self.survey.n_sources
+            R = eng.residual(self._Qf, 1.0, self.w, self.U, -1.0, ns)                     # Q - A U (forward.py:243)
+            self._ZR = eng.interior_solve(self.basis.factor, R)                           # interior_solve(R) (:246)
+        return self._ZR
+
+    @property
+    def UR(self):
+        if self._UR is None:
+            self._UR = self.U + self.ZR
+        return self._UR
 
     # ---------------------------------------------------------- device API
     def rapply_dev(self, W):
@@ -220,6 +240,13 @@ class AdaptiveSensitivity:
         W = eng.to_device(W)
         y = eng.restrict_points(self.Pp, b.Sint, W, ns)                             # S^T P W (forward.py:276)
         eng.coarse_solve(self.state.Lk, y)
+        # z = interior_solve(P W - A S y) = blockdiag(A_II^-1)(P W)_I (forward.py:278)
+        Zc = eng.interior_fields(self.Pp, b.factor, W, ns)
+        try:
+            return eng.block_gradient(self.sigma, b.Sint, self.state.T_dev, y, self.Pp, Zc, self.Qp, self.Rc)
+        except NotImplementedError:
+            pass
+        # blocks too large for the fused kernel: node-field form
         sy = eng.prolong(b.Sint, y)                                                 # S y (forward.py:277)
         pf = eng.scatter_points(self.Pp, W, ns)                                     # P W (forward.py:275)
         z = eng.residual(pf, 1.0, self.w, sy, -1.0, ns)                             # p - A sy (forward.py:278)

@@ -38,7 +38,7 @@ def test_plan_info_without_gpu():
     if not os.path.exists(_lib.LIB_PATH):
         pytest.skip("libmsfv.so not built")
     L = _lib.load()
-    assert L.msfv_abi_version() == 1
+    assert L.msfv_abi_version() == 2
     plan = ctypes.c_void_p()
     rc = L.msfv_plan_create((ctypes.c_int32 * 3)(128, 128, 128), (ctypes.c_double * 3)(1 / 128, 1 / 128, 1 / 128),
                             (ctypes.c_int32 * 3)(8, 8, 8), ctypes.byref(plan))
