@@ -14,6 +14,8 @@
 //                           place by the factorization (trailing tiles).
 //   Dinv  NT tiles          L_JJ^{-1}
 //   Lo    NT*(PT+1) tiles   the factor: slot 0 = L_JJ, slot t = L_{J+t,J}
+//   LF,LB NT*(PT+1) tiles   solve copies (slot 0 = L_JJ^{-1}) in DMMA fragment
+//                           order, forward and transposed (k_coarse_pack)
 //   Y     (NT*TB)^2         dense L^{-1} (row-major, lower part), only when
 //                           k <= COARSE_INV_MAX: a solve becomes two streaming
 //                           products instead of 2*NT dependent tile steps.
@@ -42,6 +44,8 @@ struct CoarseBufs {
   double* A;
   double* Dinv;
   double* Lo;
+  double* LF;  // solve copy of (Dinv_J, L_{J+t,J}) in forward fragment order (k_coarse_pack)
+  double* LB;  // the same tiles in backward (transposed) fragment order
   double* Y;   // may be null
 };
 
@@ -54,12 +58,14 @@ __host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double*
   b.A = base;
   b.Dinv = b.A + band_tiles(g) * TT;
   b.Lo = b.Dinv + (size_t)g.NT * TT;
-  b.Y = coarse_has_inverse(g) ? b.Lo + band_tiles(g) * TT : nullptr;
+  b.LF = b.Lo + band_tiles(g) * TT;
+  b.LB = b.LF + band_tiles(g) * TT;
+  b.Y = coarse_has_inverse(g) ? b.LB + band_tiles(g) * TT : nullptr;
   return b;
 }
 
 size_t coarse_doubles(const Geo& g) {
-  size_t n = 2 * band_tiles(g) * TT + (size_t)g.NT * TT;
+  size_t n = 4 * band_tiles(g) * TT + (size_t)g.NT * TT;
   if (coarse_has_inverse(g)) n += y_dim(g) * y_dim(g);
   return n;
 }
@@ -687,143 +693,229 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_step(Geo g, const double* _
   cpa_wait<0>();
 }
 
-// FP64 tensor-core (DMMA m8n8k4) variant of the step-buffered solve: 8
-// right-hand sides per CTA (one n8 tile), 8 warps.  Per column step the
-// tile GEMVs become m8n8k4 MMAs fed from the padded shared-memory tiles.
 namespace {
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_coarse_trsv_tc(Geo g, const double* __restrict__ Lk,
-                                                        const double* __restrict__ Dinv, double* __restrict__ X,
-                                                        int nrhs) {
-  constexpr int RC = 8;
-  extern __shared__ __align__(16) double tsm[];
-  const int W = g.PT + 1;
-  double* buf[2] = {tsm, tsm + (size_t)W * TTS};                // slot 0 = Dinv_J, slot t = L_{J+t,J}
-  double* Xw = tsm + (size_t)2 * W * TTS;                         // [PT+1][TB][RC] rhs ring (row-major)
-  double* Ys = Xw + (size_t)W * TB * RC;                          // [TB][RC]
-  double* Pt = Ys + TB * RC;                                      // [8 warps][64] partial accumulators
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  const int s0 = blockIdx.x * RC;
-  const int ns = min(RC, nrhs - s0);
-  const int gm = lane >> 2, gk = lane & 3, cn = 2 * (lane & 3);   // fragment coordinates
-  auto cp_tile = [&](double* dst, const double* src) {
-    for (int i = tid; i < TT / 2; i += nt) {
-      const int r = (2 * i) / TB, c = (2 * i) % TB;
-      cpa16(dst + r * TS + c, src + 2 * i);
-    }
-  };
-  auto issue = [&](int J, double* dst) {
-    if (J >= 0 && J < g.NT) {
-      const int pt = min(g.PT, g.NT - 1 - J);
-      cp_tile(dst, Dinv + (size_t)J * TT);
-      for (int t = 1; t <= pt; ++t) cp_tile(dst + (size_t)t * TTS, tile(Lk, g, J, t));
-    }
-    cpa_commit();
-  };
-  auto load_rows = [&](int I, double* dst) {
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = I * TB + r;
-      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-    }
-  };
-  // C(8x8 tile mi of a [32][RC] block) += op(T)(rows 8mi..) * B(32 x RC block);  T in smem (stride TS)
-  auto mma_rows = [&](double& c0, double& c1, const double* T, bool trans, int mi, const double* Bm, double sign) {
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = 4 * kk + gk;
-      const double a = trans ? T[k * TS + 8 * mi + gm] : T[(8 * mi + gm) * TS + k];
-      const double b = Bm[k * RC + gm];              // B[k][n] with n = gm
-      dmma(c0, c1, sign * a, b);
-    }
-  };
-  // ---------------- forward
-  issue(0, buf[0]);
-  issue(1, buf[1]);
-  for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
-  for (int J = 0; J < g.NT; ++J) {
-    const int pt = min(g.PT, g.NT - 1 - J);
-    const double* T = buf[J & 1];
-    cpa_wait<1>();
-    __syncthreads();
-    if (wid < 4) {                                   // y_J = Dinv_J x_J
-      double c0 = 0.0, c1 = 0.0;
-      mma_rows(c0, c1, T, false, wid, Xw + (size_t)(J % W) * TB * RC, 1.0);
-      const int r = 8 * wid + gm;
-      Ys[r * RC + cn] = c0;
-      Ys[r * RC + cn + 1] = c1;
-      const int row = J * TB + r;
-      if (row < g.kc) {
-        if (cn < ns) X[(size_t)row * nrhs + s0 + cn] = c0;
-        if (cn + 1 < ns) X[(size_t)row * nrhs + s0 + cn + 1] = c1;
-      }
-    }
-    __syncthreads();
-    for (int item = wid; item < pt * 4; item += 8) {  // x_{J+t} -= L_{J+t,J} y_J
-      const int tt = 1 + item / 4, mi = item % 4;
-      double* xt = Xw + (size_t)((J + tt) % W) * TB * RC;
-      const int r = 8 * mi + gm;
-      double c0 = xt[r * RC + cn], c1 = xt[r * RC + cn + 1];
-      mma_rows(c0, c1, T + (size_t)tt * TTS, false, mi, Ys, -1.0);
-      xt[r * RC + cn] = c0;
-      xt[r * RC + cn + 1] = c1;
-    }
-    __syncthreads();
-    load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);
-    issue(J + 2, buf[J & 1]);
+// ----------------------------------------------------------- bulk solves
+//
+// Solve-side copies of the factor.  Both sweeps carry the right-hand sides
+// transposed (8 sources x 32 rows per tile row, as four 8x8 accumulator-layout
+// pieces), so every product is D += X Y^T of two accumulator-layout 8x8
+// pieces (chunk h of k = columns {2k+h}, the layout's slot h).  A 32x32 tile T
+// is stored as 16 pieces of 64 doubles at lane*2 (one 512-byte conflict-free
+// warp load each):
+//   LF piece (mi, kb) = T  block (mi, kb)          (forward:  y^T = r^T Dinv^T, r^T -= y^T L^T)
+//   LB piece (nb, kb) = T^T block (nb, kb)         (backward: x^T = (y^T - x^T L) Dinv)
+// with slot 0 of tile column J holding Dinv_J.  Tiles below the band end are 0.
+__global__ void k_coarse_pack(Geo g, const double* __restrict__ Lo, const double* __restrict__ Dinv,
+                              double* __restrict__ LF, double* __restrict__ LB) {
+  const int J = blockIdx.x / (g.PT + 1), t = blockIdx.x % (g.PT + 1);
+  const bool valid = t == 0 || J + t < g.NT;
+  const double* src = t == 0 ? Dinv + (size_t)J * TT : tile(Lo, g, J, t);
+  double* f = LF + (size_t)blockIdx.x * TT;
+  double* b = LB + (size_t)blockIdx.x * TT;
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int p = e >> 6, w = e & 63, lane = w >> 1, sl = w & 1, m = lane >> 2, q = lane & 3;
+    const int hi = p >> 2, kb = p & 3;
+    f[e] = valid ? src[(8 * hi + m) * TB + 8 * kb + 2 * q + sl] : 0.0;
+    b[e] = valid ? src[(8 * kb + 2 * q + sl) * TB + 8 * hi + m] : 0.0;
   }
-  cpa_wait<0>();
+}
+
+namespace {
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+// D += X Y^T, X / Y accumulator-layout pieces given as (x0, x1) / (y0, y1)
+__device__ __forceinline__ void mma_xyt(double& c0, double& c1, double x0, double x1, double y0, double y1) {
+  dmma(c0, c1, x0, y0);
+  dmma(c0, c1, x1, y1);
+}
+}  // namespace
+
+// Forward then backward substitution for 8 right-hand sides per CTA.  Each
+// step's factor tiles (one contiguous (PT+1)-tile column of LF / LB) arrive
+// with one bulk TMA copy into a double-buffered stage; the active
+// right-hand-side rows live in a shared-memory ring of transposed pieces.
+__global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* __restrict__ LF,
+                                                          const double* __restrict__ LB, double* __restrict__ X,
+                                                          int nrhs) {
+  extern __shared__ __align__(128) double bsm[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  const int W = g.PT + 1;
+  const size_t col_dbl = (size_t)W * TT;
+  const unsigned col_bytes = (unsigned)(col_dbl * sizeof(double));
+  double* Rt = bsm + 2 * col_dbl;            // [W][4][64] rhs ring (transposed pieces)
+  double* Ys = Rt + (size_t)W * 256;          // [4][64]
+  double* Pt = Ys + 256;                      // [8][64]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c = lane >> 2, q = lane & 3;
+  const int s0 = blockIdx.x * 8;
+  const int col = s0 + c;
+  const bool cok = col < nrhs;
+  // rows (8 pi + 2q, +1) of tile row R, source column col
+  auto ldx = [&](int R, int pi, double& a, double& b) {
+    const int r0 = R * TB + 8 * pi + 2 * q;
+    a = (cok && R < g.NT && r0 < g.kc) ? X[(size_t)r0 * nrhs + col] : 0.0;
+    b = (cok && R < g.NT && r0 + 1 < g.kc) ? X[(size_t)(r0 + 1) * nrhs + col] : 0.0;
+  };
+  auto stx = [&](int R, int pi, double a, double b) {
+    const int r0 = R * TB + 8 * pi + 2 * q;
+    if (cok && r0 < g.kc) X[(size_t)r0 * nrhs + col] = a;
+    if (cok && r0 + 1 < g.kc) X[(size_t)(r0 + 1) * nrhs + col] = b;
+  };
+  auto piece = [&](const double* base, int p) -> const double* { return base + p * 64 + 2 * lane; };
+  if (tid == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
-  // ---------------- backward
-  issue(g.NT - 1, buf[0]);
-  issue(g.NT - 2, buf[1]);
-  for (int it = 0; it < g.NT; ++it) {
-    const int J = g.NT - 1 - it;
+  unsigned ph = 0u;                           // parity bit per stage
+
+  // ---------------- forward: y_J^T = r_J^T Dinv_J^T ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
+  if (tid == 0) {
+    bulk_load(bsm, LF, col_bytes, &bar[0]);
+    if (g.NT > 1) bulk_load((bsm + col_dbl), LF + col_dbl, col_bytes, &bar[1]);
+  }
+  for (int i = tid; i < W * 4 * 32; i += blockDim.x) {       // rows 0..PT
+    const int R = i / 128, pi = (i / 32) & 3, ln = i & 31;
+    if (ln == lane) {
+      double a, b;
+      ldx(R, pi, a, b);
+      Rt[(R * 4 + pi) * 64 + 2 * lane] = a;
+      Rt[(R * 4 + pi) * 64 + 2 * lane + 1] = b;
+    }
+  }
+  __syncthreads();
+  for (int J = 0; J < g.NT; ++J) {
+    const int s = J & 1;
     const int pt = min(g.PT, g.NT - 1 - J);
-    const double* T = buf[it & 1];
-    cpa_wait<1>();
-    __syncthreads();
-    {                                                // partial sums of L_{J+t,J}^T x_{J+t}
-      const int mi = wid & 3, half = wid >> 2;
+    mbar_wait(&bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    const double* T = (bsm + s * col_dbl);
+    const double* RJ = Rt + (size_t)(J % W) * 256;
+    if (wid < 4) {
+      const int mi = wid;
       double c0 = 0.0, c1 = 0.0;
-      for (int tt = 1 + half; tt <= pt; tt += 2)
-        mma_rows(c0, c1, T + (size_t)tt * TTS, true, mi, Xw + (size_t)((J + tt) % W) * TB * RC, 1.0);
-      Pt[wid * 64 + lane * 2] = c0;
-      Pt[wid * 64 + lane * 2 + 1] = c1;
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const double* x = piece(RJ, kb);
+        const double* y = piece(T, mi * 4 + kb);
+        mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
+      }
+      Ys[mi * 64 + 2 * lane] = c0;
+      Ys[mi * 64 + 2 * lane + 1] = c1;
+      stx(J, mi, c0, c1);
+    }
+    __syncthreads();
+    for (int p = wid; p < pt * 4; p += 8) {
+      const int t = 1 + (p >> 2), mi = p & 3;
+      double* acc = Rt + (size_t)(((J + t) % W) * 4 + mi) * 64 + 2 * lane;
+      double c0 = acc[0], c1 = acc[1];
+      const double* Tt = T + (size_t)t * TT;
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const double* x = piece(Ys, kb);
+        const double* y = piece(Tt, mi * 4 + kb);
+        mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
+      }
+      acc[0] = c0;
+      acc[1] = c1;
+    }
+    __syncthreads();
+    if (tid == 0 && J + 2 < g.NT) bulk_load((bsm + s * col_dbl), LF + (size_t)(J + 2) * col_dbl, col_bytes, &bar[s]);
+    if (wid < 4) {                                            // row J + 1 + PT enters the ring
+      double a, b;
+      ldx(J + 1 + g.PT, wid, a, b);
+      double* d = Rt + (size_t)((J % W) * 4 + wid) * 64 + 2 * lane;
+      d[0] = a;
+      d[1] = b;
+    }
+  }
+  __syncthreads();
+
+  // ---------------- backward: x_J^T = (y_J^T - sum_t x_{J+t}^T L_{J+t,J}) Dinv_J
+  for (int i = tid; i < W * 256; i += blockDim.x) Rt[i] = 0.0;
+  if (tid == 0) {
+    bulk_load(bsm, LB + (size_t)(g.NT - 1) * col_dbl, col_bytes, &bar[0]);
+    if (g.NT > 1) bulk_load((bsm + col_dbl), LB + (size_t)(g.NT - 2) * col_dbl, col_bytes, &bar[1]);
+  }
+  __syncthreads();
+  for (int it = 0; it < g.NT; ++it) {
+    const int J = g.NT - 1 - it, s = it & 1;
+    const int pt = min(g.PT, g.NT - 1 - J);
+    double ya = 0.0, yb = 0.0;
+    if (wid < 4) ldx(J, wid, ya, yb);
+    mbar_wait(&bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    const double* T = (bsm + s * col_dbl);
+    {
+      const int nb = wid & 3, half = wid >> 2;
+      double c0 = 0.0, c1 = 0.0;
+      for (int t = 1 + half; t <= pt; t += 2) {
+        const double* xr = Rt + (size_t)((J + t) % W) * 256;
+        const double* Tt = T + (size_t)t * TT;
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          const double* x = piece(xr, kb);
+          const double* y = piece(Tt, nb * 4 + kb);
+          mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
+        }
+      }
+      Pt[wid * 64 + 2 * lane] = c0;
+      Pt[wid * 64 + 2 * lane + 1] = c1;
     }
     __syncthreads();
     if (wid < 4) {
-      const int r = 8 * wid + gm, row = J * TB + r;
-      double y0 = 0.0, y1 = 0.0;
-      if (row < g.kc) {
-        if (cn < ns) y0 = X[(size_t)row * nrhs + s0 + cn];
-        if (cn + 1 < ns) y1 = X[(size_t)row * nrhs + s0 + cn + 1];
-      }
-      Ys[r * RC + cn] = y0 - Pt[wid * 64 + lane * 2] - Pt[(wid + 4) * 64 + lane * 2];
-      Ys[r * RC + cn + 1] = y1 - Pt[wid * 64 + lane * 2 + 1] - Pt[(wid + 4) * 64 + lane * 2 + 1];
+      const int nb = wid;
+      Ys[nb * 64 + 2 * lane] = (ya + Pt[nb * 64 + 2 * lane]) + Pt[(nb + 4) * 64 + 2 * lane];
+      Ys[nb * 64 + 2 * lane + 1] = (yb + Pt[nb * 64 + 2 * lane + 1]) + Pt[(nb + 4) * 64 + 2 * lane + 1];
     }
     __syncthreads();
-    if (wid < 4) {                                   // x_J = Dinv_J^T acc
+    if (wid < 4) {
+      const int nb = wid;
       double c0 = 0.0, c1 = 0.0;
-      mma_rows(c0, c1, T, true, wid, Ys, 1.0);
-      const int r = 8 * wid + gm, row = J * TB + r;
-      if (row >= g.kc) { c0 = 0.0; c1 = 0.0; }
-      double* xo = Xw + (size_t)(J % W) * TB * RC;
-      xo[r * RC + cn] = cn < ns ? c0 : 0.0;
-      xo[r * RC + cn + 1] = cn + 1 < ns ? c1 : 0.0;
-      if (row < g.kc) {
-        if (cn < ns) X[(size_t)row * nrhs + s0 + cn] = c0;
-        if (cn + 1 < ns) X[(size_t)row * nrhs + s0 + cn + 1] = c1;
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const double* x = piece(Ys, kb);
+        const double* y = piece(T, nb * 4 + kb);
+        mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
       }
+      const int r0 = J * TB + 8 * nb + 2 * q;
+      if (r0 >= g.kc) c0 = 0.0;
+      if (r0 + 1 >= g.kc) c1 = 0.0;
+      double* xo = Rt + (size_t)((J % W) * 4 + nb) * 64 + 2 * lane;
+      xo[0] = cok ? c0 : 0.0;
+      xo[1] = cok ? c1 : 0.0;
+      stx(J, nb, c0, c1);
     }
     __syncthreads();
-    issue(J - 2, buf[it & 1]);
+    if (tid == 0 && J - 2 >= 0) bulk_load((bsm + s * col_dbl), LB + (size_t)(J - 2) * col_dbl, col_bytes, &bar[s]);
   }
-  cpa_wait<0>();
 }
 
 // ------------------------------------------------------------- launchers
@@ -865,7 +957,10 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   void* args[] = {(void*)&gg, (void*)&Ak, (void*)&flags};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_coarse_factor, dim3(coop_grid), dim3(256), args, 0, st);
   count_launches(1);
-  return e;
+  if (e != cudaSuccess) return e;
+  k_coarse_pack<<<(unsigned)band_tiles(g), 256, 0, st>>>(g, B.Lo, B.Dinv, B.LF, B.LB);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
@@ -879,17 +974,15 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
     return cudaGetLastError();
   }
   constexpr int RC = 4;
-  const size_t step_smem = ((size_t)3 * (g.PT + 1) * TT / TB * TB + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
-  const size_t smem_s = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
-  (void)step_smem;
-  const size_t smem_tc = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * 8 + 8 * 64) * sizeof(double);
-  if (smem_tc <= 220 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc);
+  const size_t smem_b = ((size_t)2 * (g.PT + 1) * TT + ((size_t)g.PT + 1) * 256 + 256 + 8 * 64) * sizeof(double);
+  if (smem_b <= 220 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
     if (e != cudaSuccess) return e;
-    k_coarse_trsv_tc<<<nblk(nrhs, 8), 256, smem_tc, st>>>(g, B.Lo, B.Dinv, X, nrhs);
+    k_coarse_trsv_bulk<<<nblk(nrhs, 8), 256, smem_b, st>>>(g, B.LF, B.LB, X, nrhs);
     count_launches(1);
     return cudaGetLastError();
   }
+  const size_t smem_s = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
   if (smem_s <= 200 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_step<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
     if (e != cudaSuccess) return e;

@@ -73,18 +73,17 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   const int zs = zslot ? zslot[jb] : -1, rs = rslot ? rslot[jb] : -1;
   const int NE = NEx + NEy + NEz;
   for (int e = tid; e < NE; e += blockDim.x) {
-    int ax, x, y, z, step;
+    int x, y, z, step;
     double ihs;
     if (e < NEx) {
-      ax = 0; x = e % g.b1; const int r = e / g.b1; y = r % B2; z = r / B2; step = 1; ihs = g.ih1 * g.ih1;
+      x = e % g.b1; const int r = e / g.b1; y = r % B2; z = r / B2; step = 1; ihs = g.ih1 * g.ih1;
     } else if (e < NEx + NEy) {
       const int f = e - NEx;
-      ax = 1; x = f % B1; const int r = f / B1; y = r % g.b2; z = r / g.b2; step = B1; ihs = g.ih2 * g.ih2;
+      x = f % B1; const int r = f / B1; y = r % g.b2; z = r / g.b2; step = B1; ihs = g.ih2 * g.ih2;
     } else {
       const int f = e - NEx - NEy;
-      ax = 2; x = f % B1; const int r = f / B1; y = r % B2; z = r / B2; step = B1 * B2; ihs = g.ih3 * g.ih3;
+      x = f % B1; const int r = f / B1; y = r % B2; z = r / B2; step = B1 * B2; ihs = g.ih3 * g.ih3;
     }
-    (void)ax;
     const int na = x + B1 * (y + B2 * z), nb = na + step;
     double d[8];
 #pragma unroll

@@ -47,10 +47,6 @@ __device__ __forceinline__ F2 ld2(const double* p) {
   double2 v = *reinterpret_cast<const double2*>(p);
   return {v.x, v.y};
 }
-__device__ __forceinline__ F2 ld2cg(const double* p) {
-  double2 v = __ldcg(reinterpret_cast<const double2*>(p));
-  return {v.x, v.y};
-}
 __device__ __forceinline__ void st2(double* p, const F2& f) {
   *reinterpret_cast<double2*>(p) = make_double2(f.x, f.y);
 }
