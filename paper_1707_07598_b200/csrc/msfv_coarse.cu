@@ -756,27 +756,30 @@ __device__ __forceinline__ void mma_xyt(double& c0, double& c1, double x0, doubl
 }
 }  // namespace
 
-// Forward then backward substitution for 8 right-hand sides per CTA.  Each
-// step's factor tiles (one contiguous (PT+1)-tile column of LF / LB) arrive
-// with one bulk TMA copy into a double-buffered stage; the active
+// Forward then backward substitution for 8 right-hand sides per CTA.  The
+// factor tiles of a step (tile column J of LF / LB) are cut into nch chunks
+// of up to CHT contiguous tiles; the chunk sequence (forward: J ascending,
+// chunks in order; backward: J descending, chunks reversed so the Dinv chunk
+// comes last) streams through a ring of TRSV_STAGES shared-memory stages, one
+// bulk TMA copy per chunk, prefetched TRSV_STAGES-1 chunks ahead.  The active
 // right-hand-side rows live in a shared-memory ring of transposed pieces.
+constexpr int TRSV_MAX_STAGES = 3;
+
 __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* __restrict__ LF,
                                                           const double* __restrict__ LB, double* __restrict__ X,
-                                                          int nrhs) {
+                                                          int nrhs, int CHT, int NS) {
   extern __shared__ __align__(128) double bsm[];
-  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ __align__(8) unsigned long long bar[TRSV_MAX_STAGES];
   const int W = g.PT + 1;
-  const size_t col_dbl = (size_t)W * TT;
-  const unsigned col_bytes = (unsigned)(col_dbl * sizeof(double));
-  double* Rt = bsm + 2 * col_dbl;            // [W][4][64] rhs ring (transposed pieces)
-  double* Ys = Rt + (size_t)W * 256;          // [4][64]
-  double* Pt = Ys + 256;                      // [8][64]
+  const int nch = (W + CHT - 1) / CHT;
+  const size_t stage_dbl = (size_t)CHT * TT;
+  double* Rt = bsm + NS * stage_dbl;   // [W][4][64] rhs ring (transposed pieces)
+  double* Ys = Rt + (size_t)W * 256;             // [4][64]
+  double* Pt = Ys + 256;                         // [8][64]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int c = lane >> 2, q = lane & 3;
-  const int s0 = blockIdx.x * 8;
-  const int col = s0 + c;
+  const int col = blockIdx.x * 8 + c;
   const bool cok = col < nrhs;
-  // rows (8 pi + 2q, +1) of tile row R, source column col
   auto ldx = [&](int R, int pi, double& a, double& b) {
     const int r0 = R * TB + 8 * pi + 2 * q;
     a = (cok && R < g.NT && r0 < g.kc) ? X[(size_t)r0 * nrhs + col] : 0.0;
@@ -788,22 +791,37 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
     if (cok && r0 + 1 < g.kc) X[(size_t)(r0 + 1) * nrhs + col] = b;
   };
   auto piece = [&](const double* base, int p) -> const double* { return base + p * 64 + 2 * lane; };
+  auto ring = [&](int jm, int t) { const int r = jm + t; return r >= W ? r - W : r; };   // (J + t) % W, jm = J % W
+  const int nf = g.NT * nch, total = 2 * nf;
+  auto decode = [&](int i, int& J, int& ch) {
+    if (i < nf) {
+      J = i / nch;
+      ch = i - J * nch;
+    } else {
+      const int k = i - nf;
+      J = g.NT - 1 - k / nch;
+      ch = nch - 1 - (k - (k / nch) * nch);
+    }
+  };
+  auto issue = [&](int i) {
+    if (i >= total) return;
+    int J, ch;
+    decode(i, J, ch);
+    const int nt = min(CHT, W - ch * CHT);
+    const double* src = (i < nf ? LF : LB) + ((size_t)J * W + (size_t)ch * CHT) * TT;
+    bulk_load(bsm + (size_t)(i % NS) * stage_dbl, src, (unsigned)(nt * TT * sizeof(double)),
+              &bar[i % NS]);
+  };
   if (tid == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s]);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  unsigned ph = 0u;                           // parity bit per stage
-
-  // ---------------- forward: y_J^T = r_J^T Dinv_J^T ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
-  if (tid == 0) {
-    bulk_load(bsm, LF, col_bytes, &bar[0]);
-    if (g.NT > 1) bulk_load((bsm + col_dbl), LF + col_dbl, col_bytes, &bar[1]);
-  }
-  for (int i = tid; i < W * 4 * 32; i += blockDim.x) {       // rows 0..PT
-    const int R = i / 128, pi = (i / 32) & 3, ln = i & 31;
-    if (ln == lane) {
+  if (tid == 0)
+    for (int i = 0; i < NS - 1; ++i) issue(i);
+  for (int i = tid; i < W * 128; i += blockDim.x) {         // rows 0..PT enter the ring
+    const int R = i / 128, pi = (i / 32) & 3;
+    if ((i & 31) == lane) {
       double a, b;
       ldx(R, pi, a, b);
       Rt[(R * 4 + pi) * 64 + 2 * lane] = a;
@@ -811,111 +829,156 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
     }
   }
   __syncthreads();
-  for (int J = 0; J < g.NT; ++J) {
-    const int s = J & 1;
+  double p0 = 0.0, p1 = 0.0;        // backward partial sums of this warp, across the step's chunks
+  double ya = 0.0, yb = 0.0;
+  for (int i = 0; i < total; ++i) {
+    if (tid == 0) issue(i + NS - 1);
+    int J, ch;
+    decode(i, J, ch);
+    const int jm = J % W;
     const int pt = min(g.PT, g.NT - 1 - J);
-    mbar_wait(&bar[s], (ph >> s) & 1u);
-    ph ^= 1u << s;
-    const double* T = (bsm + s * col_dbl);
-    const double* RJ = Rt + (size_t)(J % W) * 256;
-    if (wid < 4) {
-      const int mi = wid;
-      double c0 = 0.0, c1 = 0.0;
+    const int t0 = ch * CHT, t1 = min(W, t0 + CHT) - 1;
+    const double* T = bsm + (size_t)(i % NS) * stage_dbl;     // local tile (t - t0)
+    if (i == nf) {                                           // backward: the ring keeps x^T
+      for (int k = tid; k < W * 256; k += blockDim.x) Rt[k] = 0.0;
+      __syncthreads();
+    }
+    if (i >= nf && ch == nch - 1) {                         // first chunk of a backward step
+      p0 = p1 = 0.0;
+      if (wid < 4) ldx(J, wid, ya, yb);
+    }
+    double ra = 0.0, rb = 0.0;
+    if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + g.PT, wid, ra, rb);   // in flight during the step
+    mbar_wait(&bar[i % NS], (unsigned)(i / NS) & 1u);
+    if (i < nf) {
+      // ---------- forward: y_J^T = r_J^T Dinv_J^T ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
+      if (ch == 0) {
+        if (wid < 4) {
+          const int mi = wid;
+          const double* RJ = Rt + (size_t)jm * 256;
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-        const double* x = piece(RJ, kb);
-        const double* y = piece(T, mi * 4 + kb);
-        mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
+          for (int kb = 0; kb < 4; kb += 2) {
+            const double* x = piece(RJ, kb);
+            const double* y = piece(T, mi * 4 + kb);
+            const double* x2 = piece(RJ, kb + 1);
+            const double* y2 = piece(T, mi * 4 + kb + 1);
+            mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
+            mma_xyt(e0, e1, x2[0], x2[1], y2[0], y2[1]);
+          }
+          c0 += e0;
+          c1 += e1;
+          Ys[mi * 64 + 2 * lane] = c0;
+          Ys[mi * 64 + 2 * lane + 1] = c1;
+          stx(J, mi, c0, c1);
+        }
+        __syncthreads();
       }
-      Ys[mi * 64 + 2 * lane] = c0;
-      Ys[mi * 64 + 2 * lane + 1] = c1;
-      stx(J, mi, c0, c1);
-    }
-    __syncthreads();
-    for (int p = wid; p < pt * 4; p += 8) {
-      const int t = 1 + (p >> 2), mi = p & 3;
-      double* acc = Rt + (size_t)(((J + t) % W) * 4 + mi) * 64 + 2 * lane;
-      double c0 = acc[0], c1 = acc[1];
-      const double* Tt = T + (size_t)t * TT;
+      const int ta = max(t0, 1), tb = min(t1, pt);
+      {
+        const int np = (tb - ta + 1) * 4;
+        for (int p = wid; p < np; p += 8) {
+          const int t = ta + (p >> 2), mi = p & 3;
+          double* acc = Rt + (size_t)(ring(jm, t) * 4 + mi) * 64 + 2 * lane;
+          double c0 = acc[0], c1 = acc[1];
+          const double* Tt = T + (size_t)(t - t0) * TT;
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-        const double* x = piece(Ys, kb);
-        const double* y = piece(Tt, mi * 4 + kb);
-        mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
-      }
-      acc[0] = c0;
-      acc[1] = c1;
-    }
-    __syncthreads();
-    if (tid == 0 && J + 2 < g.NT) bulk_load((bsm + s * col_dbl), LF + (size_t)(J + 2) * col_dbl, col_bytes, &bar[s]);
-    if (wid < 4) {                                            // row J + 1 + PT enters the ring
-      double a, b;
-      ldx(J + 1 + g.PT, wid, a, b);
-      double* d = Rt + (size_t)((J % W) * 4 + wid) * 64 + 2 * lane;
-      d[0] = a;
-      d[1] = b;
-    }
-  }
-  __syncthreads();
-
-  // ---------------- backward: x_J^T = (y_J^T - sum_t x_{J+t}^T L_{J+t,J}) Dinv_J
-  for (int i = tid; i < W * 256; i += blockDim.x) Rt[i] = 0.0;
-  if (tid == 0) {
-    bulk_load(bsm, LB + (size_t)(g.NT - 1) * col_dbl, col_bytes, &bar[0]);
-    if (g.NT > 1) bulk_load((bsm + col_dbl), LB + (size_t)(g.NT - 2) * col_dbl, col_bytes, &bar[1]);
-  }
-  __syncthreads();
-  for (int it = 0; it < g.NT; ++it) {
-    const int J = g.NT - 1 - it, s = it & 1;
-    const int pt = min(g.PT, g.NT - 1 - J);
-    double ya = 0.0, yb = 0.0;
-    if (wid < 4) ldx(J, wid, ya, yb);
-    mbar_wait(&bar[s], (ph >> s) & 1u);
-    ph ^= 1u << s;
-    const double* T = (bsm + s * col_dbl);
-    {
-      const int nb = wid & 3, half = wid >> 2;
-      double c0 = 0.0, c1 = 0.0;
-      for (int t = 1 + half; t <= pt; t += 2) {
-        const double* xr = Rt + (size_t)((J + t) % W) * 256;
-        const double* Tt = T + (size_t)t * TT;
-#pragma unroll
-        for (int kb = 0; kb < 4; ++kb) {
-          const double* x = piece(xr, kb);
-          const double* y = piece(Tt, nb * 4 + kb);
-          mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
+          for (int kb = 0; kb < 4; ++kb) {
+            const double* x = piece(Ys, kb);
+            const double* y = piece(Tt, mi * 4 + kb);
+            mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
+          }
+          acc[0] = c0;
+          acc[1] = c1;
         }
       }
-      Pt[wid * 64 + 2 * lane] = c0;
-      Pt[wid * 64 + 2 * lane + 1] = c1;
-    }
-    __syncthreads();
-    if (wid < 4) {
-      const int nb = wid;
-      Ys[nb * 64 + 2 * lane] = (ya + Pt[nb * 64 + 2 * lane]) + Pt[(nb + 4) * 64 + 2 * lane];
-      Ys[nb * 64 + 2 * lane + 1] = (yb + Pt[nb * 64 + 2 * lane + 1]) + Pt[(nb + 4) * 64 + 2 * lane + 1];
-    }
-    __syncthreads();
-    if (wid < 4) {
-      const int nb = wid;
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-        const double* x = piece(Ys, kb);
-        const double* y = piece(T, nb * 4 + kb);
-        mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
+      __syncthreads();
+      if (ch == nch - 1 && wid < 4) {                        // row J + 1 + PT enters the ring
+        const double a = ra, b = rb;
+        double* d = Rt + (size_t)(jm * 4 + wid) * 64 + 2 * lane;
+        d[0] = a;
+        d[1] = b;
       }
-      const int r0 = J * TB + 8 * nb + 2 * q;
-      if (r0 >= g.kc) c0 = 0.0;
-      if (r0 + 1 >= g.kc) c1 = 0.0;
-      double* xo = Rt + (size_t)((J % W) * 4 + nb) * 64 + 2 * lane;
-      xo[0] = cok ? c0 : 0.0;
-      xo[1] = cok ? c1 : 0.0;
-      stx(J, nb, c0, c1);
+    } else {
+      // ---------- backward: x_J^T = (y_J^T - sum_t x_{J+t}^T L_{J+t,J}) Dinv_J
+      {
+        const int nb = wid & 3, half = wid >> 2;
+        const int ta = max(t0, 1), tb = min(t1, pt);
+        double e0 = 0.0, e1 = 0.0;
+        for (int t = ta + ((ta & 1) != half ? 1 : 0); t <= tb; t += 2) {
+          const double* xr = Rt + (size_t)ring(jm, t) * 256;
+          const double* Tt = T + (size_t)(t - t0) * TT;
+#pragma unroll
+          for (int kb = 0; kb < 4; kb += 2) {
+            const double* x = piece(xr, kb);
+            const double* y = piece(Tt, nb * 4 + kb);
+            const double* x2 = piece(xr, kb + 1);
+            const double* y2 = piece(Tt, nb * 4 + kb + 1);
+            mma_xyt(p0, p1, x[0], x[1], y[0], y[1]);
+            mma_xyt(e0, e1, x2[0], x2[1], y2[0], y2[1]);
+          }
+        }
+        p0 += e0;
+        p1 += e1;
+      }
+      if (ch == 0) {
+        Pt[wid * 64 + 2 * lane] = p0;
+        Pt[wid * 64 + 2 * lane + 1] = p1;
+        __syncthreads();
+        if (wid < 4) {
+          const int nb = wid;
+          Ys[nb * 64 + 2 * lane] = (ya + Pt[nb * 64 + 2 * lane]) + Pt[(nb + 4) * 64 + 2 * lane];
+          Ys[nb * 64 + 2 * lane + 1] = (yb + Pt[nb * 64 + 2 * lane + 1]) + Pt[(nb + 4) * 64 + 2 * lane + 1];
+        }
+        __syncthreads();
+        if (wid < 4) {
+          const int nb = wid;
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+          for (int kb = 0; kb < 4; kb += 2) {
+            const double* x = piece(Ys, kb);
+            const double* y = piece(T, nb * 4 + kb);
+            const double* x2 = piece(Ys, kb + 1);
+            const double* y2 = piece(T, nb * 4 + kb + 1);
+            mma_xyt(c0, c1, x[0], x[1], y[0], y[1]);
+            mma_xyt(e0, e1, x2[0], x2[1], y2[0], y2[1]);
+          }
+          c0 += e0;
+          c1 += e1;
+          const int r0 = J * TB + 8 * nb + 2 * q;
+          if (r0 >= g.kc) c0 = 0.0;
+          if (r0 + 1 >= g.kc) c1 = 0.0;
+          double* xo = Rt + (size_t)(jm * 4 + nb) * 64 + 2 * lane;   // ring keeps -x^T
+          xo[0] = cok ? -c0 : 0.0;
+          xo[1] = cok ? -c1 : 0.0;
+          stx(J, nb, c0, c1);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (tid == 0 && J - 2 >= 0) bulk_load((bsm + s * col_dbl), LB + (size_t)(J - 2) * col_dbl, col_bytes, &bar[s]);
   }
+}
+
+// One whole tile column per stage (2 stages) when it fits, else chunks
+// through 3 stages.
+static void trsv_bulk_shape(const Geo& g, int& cht, int& ns, size_t& smem) {
+  const int W = g.PT + 1;
+  const size_t fixed = ((size_t)W * 256 + 256 + 8 * 64) * sizeof(double);
+  const size_t budget = 220 * 1024, tile_b = (size_t)TT * sizeof(double);
+  cht = 0;
+  ns = 0;
+  smem = 0;
+  if (fixed + 2 * W * tile_b <= budget) {
+    cht = W;
+    ns = 2;
+  } else {
+    if (fixed + (size_t)TRSV_MAX_STAGES * tile_b > budget) return;
+    const int maxc = (int)((budget - fixed) / (TRSV_MAX_STAGES * tile_b));
+    const int nch = (W + maxc - 1) / maxc;
+    cht = (W + nch - 1) / nch;
+    ns = TRSV_MAX_STAGES;
+  }
+  smem = fixed + (size_t)ns * cht * tile_b;
 }
 
 // ------------------------------------------------------------- launchers
@@ -974,11 +1037,13 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
     return cudaGetLastError();
   }
   constexpr int RC = 4;
-  const size_t smem_b = ((size_t)2 * (g.PT + 1) * TT + ((size_t)g.PT + 1) * 256 + 256 + 8 * 64) * sizeof(double);
-  if (smem_b <= 220 * 1024) {
+  int cht = 0, ns = 0;
+  size_t smem_b = 0;
+  trsv_bulk_shape(g, cht, ns, smem_b);
+  if (cht > 0) {
     cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
     if (e != cudaSuccess) return e;
-    k_coarse_trsv_bulk<<<nblk(nrhs, 8), 256, smem_b, st>>>(g, B.LF, B.LB, X, nrhs);
+    k_coarse_trsv_bulk<<<nblk(nrhs, 8), 256, smem_b, st>>>(g, B.LF, B.LB, X, nrhs, cht, ns);
     count_launches(1);
     return cudaGetLastError();
   }
