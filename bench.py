@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gn", action="store_true", help="skip the Gauss-Newton iteration timing")
     return ap.parse_args()
 
 
@@ -266,6 +267,39 @@ def run_gpu(args, rank, world, log):
     ms = dist.max_over_ranks(ms, dev)
     log(f"device step {ms:.3f} ms")
 
+    # config-4 Gauss-Newton iteration (BASELINE configs[3]): forward, gradient
+    # and 5 CG steps, each one J v and one J^T (J v), device-resident
+    def gn_iter_dev():
+        op = gp.assemble_operator(mesh, m_dev)
+        basis = builder.assemble(op)
+        D, st = forward_reduced_dev(op, survey, basis, defer_check=True)
+        st.deferred = True
+        resid = D - dobs_dev
+        J = sensitivity_adaptive(st, survey)
+        v = J.rapply_dev(resid)
+        for _ in range(5):
+            jv = J.apply_dev(v)
+            v = J.rapply_dev(jv)
+        st.check()
+        return v
+
+    gn = None
+    if not args.no_gn:
+        for _ in range(args.warmup):
+            gn_iter_dev()
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0e, g1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0e.record()
+        for _ in range(args.steps):
+            gn_iter_dev()
+        g1e.record()
+        torch.cuda.synchronize()
+        gn_ms = dist.max_over_ranks(g0e.elapsed_time(g1e) / args.steps, dev)
+        gn = {"ms_per_iter": round(gn_ms, 4), "cg_steps": 5,
+              "what": "forward + gradient + 5 x (J v, J^T J v) (device-resident)"}
+        log(f"GN iteration {gn_ms:.3f} ms")
+
     # per-phase breakdown (one extra instrumented step)
     PhaseTimer.start()
     step_dev()
@@ -316,7 +350,7 @@ def run_gpu(args, rank, world, log):
     return {
         "ms": ms, "launches": launches, "clocks": clk, "phases": phases, "e2e": e2e, "roofline": roof,
         "block_solves_per_s": eng.nbl / t_basis, "nbl": eng.nbl,
-        "interior_solve_ms": phases.get("interior_solve"),
+        "interior_solve_ms": phases.get("interior_solve"), "gn": gn,
     }
 
 
@@ -363,6 +397,7 @@ def main():
             "gpu_launches_per_step": res["launches"] / args.steps, "clocks": res["clocks"],
             "local_block_solves_per_s": round(res["block_solves_per_s"], 1),
             "phases_ms": {k: round(v, 4) for k, v in res["phases"].items()},
+            "gn_iteration": res["gn"],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -173,6 +173,14 @@ MSFV_API int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points
 MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
                         const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
                         const msfv_points* pr, const double* Rc, double* g, void* stream);
+/* Coarse right-hand side of J v for surveys without interior receivers
+ * (forward.py:258-269): out = xdm - S^T(gdm + A ydm) = -EP^T((G U + G R) o c)
+ * with U = S T, R the compact interior field of pr (NULL: none) and c = Csig dm
+ * (msfv_edge_average).  The S^T A ydm term vanishes because (A S)_I = 0 and
+ * ydm lives on block interiors.  part: nblocks*8*nrhs doubles of scratch;
+ * out: k x nrhs. */
+MSFV_API int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
+                       const msfv_points* pr, const double* Rc, double* part, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -736,6 +736,12 @@ cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w
   count_launches(1);
   return cudaGetLastError();
 }
+cudaError_t launch_gather_corners(const Geo& g, const double* part, int nrhs, double scale, double* out,
+                                  cudaStream_t st) {
+  k_gather_corners<<<nblk((long long)g.kc * nrhs, 256), 256, 0, st>>>(g, part, nrhs, scale, out);
+  count_launches(1);
+  return cudaGetLastError();
+}
 cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
                                  const double* Y, const double* R, int nrhs, double* xi, double* gout,
                                  cudaStream_t st) {

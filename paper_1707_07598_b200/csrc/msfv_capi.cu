@@ -413,4 +413,18 @@ int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double
                     "block_gradient");
 }
 
+int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
+                       const msfv_points* pr, const double* Rc, double* part, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (nrhs < 0) return fail(MSFV_SHAPE, "bad J v arguments");
+  const Geo& g = plan->g;
+  if (jv_smem_doubles(g, nrhs) * sizeof(double) > 200 * 1024)
+    return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool hr = pr && pr->d.nib > 0 && Rc;
+  int rc = cuda_check(launch_jv_block(g, Sint, c, T, nrhs, hr ? pr->d.islot : nullptr, Rc, part, st), "jv_block");
+  if (rc) return rc;
+  return cuda_check(launch_gather_corners(g, part, nrhs, -1.0, out, st), "jv_gather");
+}
+
 }  // extern "C"

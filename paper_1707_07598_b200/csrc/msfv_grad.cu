@@ -20,6 +20,27 @@
 
 namespace msfv {
 
+// Basis values of block jb's 8 columns on its closure nodes (x fastest,
+// (b1+1)(b2+1)(b3+1) nodes x 8): interior from Sint, skeleton from the hats,
+// 0 at the pinned node.
+__device__ __forceinline__ void stage_closure(const Geo& g, int jb, const double* __restrict__ Sint, double* Sn) {
+  const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
+  const double* Sb = Sint + (size_t)jb * 8 * g.nI;
+  for (int i = threadIdx.x; i < 8 * g.nI; i += blockDim.x) {
+    const int cc = i / g.nI, a = i - cc * g.nI;
+    int x, y, z;
+    decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+    Sn[((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8 + cc] = __ldg(Sb + i);
+  }
+  for (int n = threadIdx.x; n < NN; n += blockDim.x) {
+    const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
+    if (x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3) continue;
+    const bool node0 = jb == 0 && n == 0;     // pinned node: no row of S
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) Sn[n * 8 + cc] = node0 ? 0.0 : hatf(g, cc, x, y, z);
+  }
+}
+
 size_t grad_smem_doubles(const Geo& g, int nrhs) {
   const size_t B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1;
   const size_t ne = (size_t)g.b1 * B2 * B3 + B1 * g.b2 * B3 + B1 * B2 * g.b3;
@@ -48,20 +69,7 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
     Tj[i] = T[col * nrhs + s];
     Yj[i] = Y[col * nrhs + s];
   }
-  const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  for (int i = tid; i < 8 * g.nI; i += blockDim.x) {
-    const int cc = i / g.nI, a = i - cc * g.nI;
-    int x, y, z;
-    decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
-    Sn[((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8 + cc] = __ldg(Sb + i);
-  }
-  for (int n = tid; n < NN; n += blockDim.x) {
-    const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
-    if (x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3) continue;
-    const bool node0 = jb == 0 && n == 0;     // pinned node: no row of S
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) Sn[n * 8 + cc] = node0 ? 0.0 : hatf(g, cc, x, y, z);
-  }
+  stage_closure(g, jb, Sint, Sn);
   __syncthreads();
   if (tid < 64) {
     const int c = tid >> 3, c2 = tid & 7;
@@ -138,6 +146,117 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
     const long long cid = cell_id(g, X0 + x, Y0 + y, Z0 + z);
     gout[cid] = -sigma[cid] * (g.qv * tot);
   }
+}
+
+// Coarse right-hand side of J v (forward.py:258-269) for surveys without
+// interior receivers.  With c = Csig dm, U = S T and R = interior_solve(Q - A U):
+//   rhs = xdm - S^T(gdm + A ydm) = -EP^T((G U + G R) o c)       (S^T A ydm = (A S)^T ydm = 0)
+// and EP^T diag(c) G S T = sum_j  K_c(j) T_j,  K_c(j) = sum_{e owned by j} (c_e/h_e^2) dS_e dS_e^T,
+// i.e. the Galerkin block of the conductances c.  part[j][cc][s] holds block
+// j's share (gathered to coarse nodes by k_gather_corners with scale -1).
+// Edge ownership: the edge's lower node is owned by j (node ownership of
+// k_restrict_op).  K_c is a DMMA reduction (lane = corner cc, edge slot).
+__global__ void __launch_bounds__(GRAD_THREADS)
+k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cvec, const double* __restrict__ T,
+           int nrhs, const int* __restrict__ rslot, const double* __restrict__ Rc, double* __restrict__ part) {
+  extern __shared__ __align__(16) double gsm[];
+  const int jb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
+  const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
+  const int ox = g.b1 + (bi == g.nb1 - 1), oy = g.b2 + (bj == g.nb2 - 1), oz = g.b3 + (bk == g.nb3 - 1);
+  const int NOx = g.b1 * oy * oz, NOy = ox * g.b2 * oz, NOz = ox * oy * g.b3, NO = NOx + NOy + NOz;
+  double* Sn = gsm;                       // [NN][8]
+  double* Kw = Sn + (size_t)NN * 8;       // [8 warps][64]
+  double* Tj = Kw + 8 * 64;               // [8][nrhs]
+  stage_closure(g, jb, Sint, Sn);
+  for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
+    const int cc = i / nrhs, s = i - cc * nrhs;
+    Tj[i] = T[(size_t)corner_col(g, bi, bj, bk, cc) * nrhs + s];
+  }
+  __syncthreads();
+  // owned edge f -> (local lower node, step, global edge id, 1/h^2)
+  auto edge = [&](int f, int& na, int& step, long long& eid, double& ihs) {
+    int x, y, z;
+    if (f < NOx) {
+      x = f % g.b1; const int r = f / g.b1; y = r % oy; z = r / oy;
+      step = 1; ihs = g.ih1 * g.ih1; eid = ex_id(g, X0 + x, Y0 + y, Z0 + z);
+    } else if (f < NOx + NOy) {
+      const int h = f - NOx;
+      x = h % ox; const int r = h / ox; y = r % g.b2; z = r / g.b2;
+      step = B1; ihs = g.ih2 * g.ih2; eid = ey_id(g, X0 + x, Y0 + y, Z0 + z);
+    } else {
+      const int h = f - NOx - NOy;
+      x = h % ox; const int r = h / ox; y = r % oy; z = r / oy;
+      step = B1 * B2; ihs = g.ih3 * g.ih3; eid = ez_id(g, X0 + x, Y0 + y, Z0 + z);
+    }
+    na = x + B1 * (y + B2 * z);
+  };
+  const int cc = lane >> 2, slot = lane & 3;
+  double k0 = 0.0, k1 = 0.0;
+  for (int base = 4 * wid; base < NO; base += 32) {
+    const int f = base + slot;
+    double a = 0.0, b = 0.0;
+    if (f < NO) {
+      int na, step;
+      long long eid;
+      double ihs;
+      edge(f, na, step, eid, ihs);
+      b = Sn[(na + step) * 8 + cc] - Sn[na * 8 + cc];
+      a = (__ldg(cvec + eid) * ihs) * b;
+    }
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(k0), "+d"(k1)
+        : "d"(a), "d"(b));
+  }
+  Kw[wid * 64 + 2 * lane] = k0;
+  Kw[wid * 64 + 2 * lane + 1] = k1;
+  __syncthreads();
+  if (tid < 64) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += Kw[w * 64 + tid];
+    Kw[tid] = v;                         // warp 0's slot now holds K_c (row-major 8x8)
+  }
+  __syncthreads();
+  const int rs = rslot ? rslot[jb] : -1;
+  const double* Rb = rs >= 0 ? Rc + (size_t)rs * g.nI * nrhs : nullptr;
+  for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
+    const int c1 = i / nrhs, s = i - c1 * nrhs;
+    double v = 0.0;
+#pragma unroll
+    for (int c2 = 0; c2 < 8; ++c2) v += Kw[c1 * 8 + c2] * Tj[c2 * nrhs + s];
+    if (Rb) {
+      // source blocks: + sum_e (c_e/h^2) dS_c1(e) dR_s(e), R interior-only
+      for (int f = 0; f < NO; ++f) {
+        int na, step;
+        long long eid;
+        double ihs;
+        edge(f, na, step, eid, ihs);
+        const int nb = na + step;
+        const int xa = na % B1, ya = (na / B1) % B2, za = na / (B1 * B2);
+        const int xb = nb % B1, yb = (nb / B1) % B2, zb = nb / (B1 * B2);
+        const int ia = interior_index(g, xa, ya, za), ib = interior_index(g, xb, yb, zb);
+        const double dr = (ib >= 0 ? Rb[(size_t)ib * nrhs + s] : 0.0) - (ia >= 0 ? Rb[(size_t)ia * nrhs + s] : 0.0);
+        if (dr == 0.0) continue;
+        v += (__ldg(cvec + eid) * ihs) * (Sn[nb * 8 + c1] - Sn[na * 8 + c1]) * dr;
+      }
+    }
+    part[((size_t)jb * 8 + c1) * nrhs + s] = v;
+  }
+}
+
+size_t jv_smem_doubles(const Geo& g, int nrhs) {
+  return (size_t)(g.b1 + 1) * (g.b2 + 1) * (g.b3 + 1) * 8 + 8 * 64 + 8 * (size_t)nrhs;
+}
+
+cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec, const double* T, int nrhs,
+                            const int* rslot, const double* Rc, double* part, cudaStream_t st) {
+  const size_t smem = jv_smem_doubles(g, nrhs) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_jv_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_jv_block<<<g.nbl, GRAD_THREADS, smem, st>>>(g, Sint, cvec, T, nrhs, rslot, Rc, part);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 bool grad_supported(const Geo& g, int nrhs) { return grad_smem_doubles(g, nrhs) * sizeof(double) <= 200 * 1024; }

@@ -293,6 +293,18 @@ class Engine:
                        "block_gradient")
         return g
 
+    def jv_coarse_rhs(self, Sint, c, T, pr=None, Rc=None):
+        """-EP^T((G U + G R) o c) on the coarse nodes (k x nrhs); raises
+        NotImplementedError when the block closure does not fit in shared memory."""
+        nrhs = T.shape[1]
+        part = self.empty(self.nbl * 8 * max(nrhs, 1))
+        out = self.empty(self.k, nrhs)
+        with phase("jv_rhs"):
+            _lib.check(self.L.msfv_jv_coarse_rhs(self.plan, ptr(Sint), ptr(c), ptr(T), nrhs,
+                                                 None if pr is None else pr.handle, ptr(Rc), ptr(part), ptr(out),
+                                                 stream()), "jv_coarse_rhs")
+        return out
+
     def basis_csc(self, Sint, src, hatv):
         vals = self.empty(src.numel())
         _lib.check(self.L.msfv_basis_csc(src.numel(), ptr(Sint), ptr(src), ptr(hatv), ptr(vals), stream()),

@@ -258,6 +258,16 @@ class AdaptiveSensitivity:
         ns = self.survey.n_sources
         dm = eng.to_device(dm).reshape(-1)
         c = eng.edge_average(self.sigma, dm)                                        # Csig dm (forward.py:259)
+        if self.Pp.interior_blocks == 0:
+            # receivers on the skeleton: P^T ydm = 0 and S^T A ydm = (A S)^T ydm = 0,
+            # so only the coarse rhs -EP^T(G UR o c) remains (block-local)
+            try:
+                dt = eng.jv_coarse_rhs(b.Sint, c, self.state.T_dev, self.Qp, self.Rc)
+            except NotImplementedError:
+                dt = None
+            if dt is not None:
+                eng.coarse_solve(self.state.Lk, dt)                                 # forward.py:267
+                return eng.receive(self.Pp, b.Sint, Y=dt)                           # P^T S dt (:268)
         ydm = eng.residual(None, 0.0, c, self.U, -1.0, ns)                          # -G^T(gu c)
         eng.interior_solve(b.factor, ydm)                                         # _Y_dm (forward.py:250-252)
         dt = eng.restrict_op(b.Sint, c, self.UR, self.w, ydm, ns, scale=-1.0)       # xdm - S^T(gdm + A ydm)
