@@ -793,24 +793,40 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
   auto piece = [&](const double* base, int p) -> const double* { return base + p * 64 + 2 * lane; };
   auto ring = [&](int jm, int t) { const int r = jm + t; return r >= W ? r - W : r; };   // (J + t) % W, jm = J % W
   const int nf = g.NT * nch, total = 2 * nf;
-  auto decode = [&](int i, int& J, int& ch) {
-    if (i < nf) {
-      J = i / nch;
-      ch = i - J * nch;
-    } else {
-      const int k = i - nf;
-      J = g.NT - 1 - k / nch;
-      ch = nch - 1 - (k - (k / nch) * nch);
+  // chunk sequence iterator (no integer division in the loop)
+  struct It {
+    int J, ch, jm;
+    bool fwd;
+  };
+  auto advance = [&](It& c) {
+    if (c.fwd) {
+      if (++c.ch == nch) {
+        c.ch = 0;
+        ++c.J;
+        c.jm = c.jm + 1 == W ? 0 : c.jm + 1;
+        if (c.J == g.NT) {
+          c.fwd = false;
+          c.J = g.NT - 1;
+          c.ch = nch - 1;
+          c.jm = (g.NT - 1) % W;
+        }
+      }
+    } else if (--c.ch < 0) {
+      c.ch = nch - 1;
+      --c.J;
+      c.jm = c.jm == 0 ? W - 1 : c.jm - 1;
     }
   };
-  auto issue = [&](int i) {
-    if (i >= total) return;
-    int J, ch;
-    decode(i, J, ch);
-    const int nt = min(CHT, W - ch * CHT);
-    const double* src = (i < nf ? LF : LB) + ((size_t)J * W + (size_t)ch * CHT) * TT;
-    bulk_load(bsm + (size_t)(i % NS) * stage_dbl, src, (unsigned)(nt * TT * sizeof(double)),
-              &bar[i % NS]);
+  It ld = {0, 0, 0, true};          // next chunk to load
+  int ld_i = 0, ld_st = 0;
+  auto issue_next = [&]() {
+    if (ld_i >= total) return;
+    const int nt = min(CHT, W - ld.ch * CHT);
+    const double* src = (ld.fwd ? LF : LB) + ((size_t)ld.J * W + (size_t)ld.ch * CHT) * TT;
+    bulk_load(bsm + (size_t)ld_st * stage_dbl, src, (unsigned)(nt * TT * sizeof(double)), &bar[ld_st]);
+    advance(ld);
+    ++ld_i;
+    ld_st = ld_st + 1 == NS ? 0 : ld_st + 1;
   };
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bar[s]);
@@ -818,7 +834,7 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
   }
   __syncthreads();
   if (tid == 0)
-    for (int i = 0; i < NS - 1; ++i) issue(i);
+    for (int i = 0; i < NS - 1; ++i) issue_next();
   for (int i = tid; i < W * 128; i += blockDim.x) {         // rows 0..PT enter the ring
     const int R = i / 128, pi = (i / 32) & 3;
     if ((i & 31) == lane) {
@@ -831,14 +847,15 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
   __syncthreads();
   double p0 = 0.0, p1 = 0.0;        // backward partial sums of this warp, across the step's chunks
   double ya = 0.0, yb = 0.0;
-  for (int i = 0; i < total; ++i) {
-    if (tid == 0) issue(i + NS - 1);
-    int J, ch;
-    decode(i, J, ch);
-    const int jm = J % W;
+  It cu = {0, 0, 0, true};
+  int st = 0;
+  unsigned par = 0u;
+  for (int i = 0; i < total; ++i, advance(cu), st = st + 1 == NS ? 0 : st + 1) {
+    if (tid == 0) issue_next();
+    const int J = cu.J, ch = cu.ch, jm = cu.jm;
     const int pt = min(g.PT, g.NT - 1 - J);
     const int t0 = ch * CHT, t1 = min(W, t0 + CHT) - 1;
-    const double* T = bsm + (size_t)(i % NS) * stage_dbl;     // local tile (t - t0)
+    const double* T = bsm + (size_t)st * stage_dbl;           // local tile (t - t0)
     if (i == nf) {                                           // backward: the ring keeps x^T
       for (int k = tid; k < W * 256; k += blockDim.x) Rt[k] = 0.0;
       __syncthreads();
@@ -849,7 +866,8 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
     }
     double ra = 0.0, rb = 0.0;
     if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + g.PT, wid, ra, rb);   // in flight during the step
-    mbar_wait(&bar[i % NS], (unsigned)(i / NS) & 1u);
+    mbar_wait(&bar[st], (par >> st) & 1u);
+    par ^= 1u << st;
     if (i < nf) {
       // ---------- forward: y_J^T = r_J^T Dinv_J^T ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
       if (ch == 0) {
