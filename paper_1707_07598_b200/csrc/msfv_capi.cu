@@ -84,9 +84,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.r_ni1 = g.ni1 > 0 ? 1.0f / g.ni1 : 0.0f; g.r_ni2 = g.ni2 > 0 ? 1.0f / g.ni2 : 0.0f;
   g.r_nI = g.nI > 0 ? 1.0f / g.nI : 0.0f; g.r_nb1 = 1.0f / g.nb1; g.r_nb2 = 1.0f / g.nb2;
   {
-    // dense coarse L^{-1}: default up to COARSE_INV_MAX coarse nodes; MSFV_COARSE_INV=0/1 overrides
-    const char* ev = getenv("MSFV_COARSE_INV");
-    g.coarse_inv = ev ? (atoi(ev) != 0) : (g.kc <= COARSE_INV_MAX);
+    g.coarse_inv = 0;
   }
   if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");

@@ -13,19 +13,16 @@
 //                           t = 0..PT, each TB x TB row-major.  Updated in
 //                           place by the factorization (trailing tiles).
 //   Dinv  NT tiles          L_JJ^{-1}
-//   Lo    NT*(PT+1) tiles   the factor: slot 0 = L_JJ, slot t = L_{J+t,J}
+//   Lo    NT*(PT+1) tiles   the factor: slot t = L_{J+t,J} (slot 0 unused)
 //   LF,LB NT*(PT+1) tiles   solve copies (slot 0 = L_JJ^{-1}) in DMMA fragment
 //                           order, forward and transposed (k_coarse_pack)
-//   Y     (NT*TB)^2         dense L^{-1} (row-major, lower part), only when
-//                           k <= COARSE_INV_MAX: a solve becomes two streaming
-//                           products instead of 2*NT dependent tile steps.
 // Padding rows (>= kc) are identity.
 //
 // The factorization is one cooperative launch with one grid barrier per tile
 // column: after the barrier every CTA takes trailing-update tasks
 // (recomputing the panel products it needs, so the panel TRSM costs no extra
-// barrier) and L^{-1} row-panel tasks; CTA 0 first takes the task that
-// updates the next diagonal tile and then factors it (one-step lookahead).
+// barrier); CTA 0 first takes the task that updates the next diagonal tile
+// and then factors it (one-step lookahead).  All tile products are DMMA.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -46,12 +43,9 @@ struct CoarseBufs {
   double* Lo;
   double* LF;  // solve copy of (Dinv_J, L_{J+t,J}) in forward fragment order (k_coarse_pack)
   double* LB;  // the same tiles in backward (transposed) fragment order
-  double* Y;   // may be null
 };
 
 __host__ __device__ __forceinline__ size_t band_tiles(const Geo& g) { return (size_t)g.NT * (g.PT + 1); }
-__host__ __device__ __forceinline__ bool coarse_has_inverse(const Geo& g) { return g.coarse_inv != 0; }
-__host__ __device__ __forceinline__ size_t y_dim(const Geo& g) { return (size_t)g.NT * TB; }
 
 __host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double* base) {
   CoarseBufs b;
@@ -60,14 +54,11 @@ __host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double*
   b.Lo = b.Dinv + (size_t)g.NT * TT;
   b.LF = b.Lo + band_tiles(g) * TT;
   b.LB = b.LF + band_tiles(g) * TT;
-  b.Y = coarse_has_inverse(g) ? b.LB + band_tiles(g) * TT : nullptr;
   return b;
 }
 
 size_t coarse_doubles(const Geo& g) {
-  size_t n = 4 * band_tiles(g) * TT + (size_t)g.NT * TT;
-  if (coarse_has_inverse(g)) n += y_dim(g) * y_dim(g);
-  return n;
+  return 4 * band_tiles(g) * TT + (size_t)g.NT * TT;
 }
 size_t coarse_scratch_doubles(const Geo& g, int nrhs) { return (size_t)g.kc * nrhs; }
 
@@ -127,292 +118,278 @@ __global__ void k_coarse_diag(Geo g, const double* __restrict__ Ak, double* __re
 }
 
 // ------------------------------------------------------------ factorization
+//
+// Tile products run on the FP64 tensor cores (DMMA m8n8k4) in the
+// transposed-operand form: with both operands in accumulator (C) layout,
+// D += X Y^T (chunk h of k = columns {2k+h}, the layout's slot h), so a 32x32
+// tile product O = X Y^T is 16 output 8x8 blocks x 4 k-blocks x 2 DMMAs; warp
+// w owns output blocks w and w+8.  Shared tiles use a padded row stride LDT
+// (320 bytes) so the 16-byte fragment loads are bank-conflict free.
+constexpr int LDT = TB + 8;
 
 struct FactorSmem {
-  double P[TB][TB + 1];    // tile operands / POTRF workspace
-  double Q[TB][TB + 1];
-  double R[TB][TB + 1];
-  double D[TB][TB + 1];    // Dinv of the current column
+  double T[TB * LDT];      // operand tile (A_{J+t,J}) / diagonal tile under POTRF
+  double X1[TB * LDT];     // L_{J+t1,J}
+  double X2[TB * LDT];     // L_{J+t2,J}
+  double D[TB * LDT];      // Dinv_J
+  double Li[4][64];        // POTRF: L_kk^{-1} of the diagonal 8x8 blocks (C layout)
+  double Is[64];           // potrf8 output
 };
 
-__device__ __forceinline__ void load_tile(double (*S)[TB + 1], const double* src) {
-  for (int t = threadIdx.x; t < TT; t += blockDim.x) S[t / TB][t % TB] = src[t];
+struct F2c {
+  double x, y;
+};
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void store_tile(double* dst, double (*S)[TB + 1]) {
-  for (int t = threadIdx.x; t < TT; t += blockDim.x) dst[t] = S[t / TB][t % TB];
+__device__ __forceinline__ void mxyt(F2c& c, const F2c& x, const F2c& y) {
+  dmma(c.x, c.y, x.x, y.x);
+  dmma(c.x, c.y, x.y, y.y);
 }
-
-// 32x32 tile products by 256 threads, each owning a 2x2 output block.
-template <bool XT, bool YT>
-__device__ __forceinline__ void mm22(double acc[4], double (*X)[TB + 1], double (*Y)[TB + 1], int r0, int c0) {
-  acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
-#pragma unroll 8
-  for (int m = 0; m < TB; ++m) {
-    const double x0 = XT ? X[m][r0] : X[r0][m], x1 = XT ? X[m][r0 + 1] : X[r0 + 1][m];
-    const double y0 = YT ? Y[c0][m] : Y[m][c0], y1 = YT ? Y[c0 + 1][m] : Y[m][c0 + 1];
-    acc[0] += x0 * y0; acc[1] += x0 * y1; acc[2] += x1 * y0; acc[3] += x1 * y1;
+// C-layout fragment of 8x8 block (bi, bj) of a tile with row stride ld
+__device__ __forceinline__ F2c frag(const double* S, int ld, int bi, int bj, int lane) {
+  const double2 v = *reinterpret_cast<const double2*>(S + (8 * bi + (lane >> 2)) * ld + 8 * bj + 2 * (lane & 3));
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void put(double* S, int ld, int bi, int bj, int lane, const F2c& f) {
+  *reinterpret_cast<double2*>(S + (8 * bi + (lane >> 2)) * ld + 8 * bj + 2 * (lane & 3)) = make_double2(f.x, f.y);
+}
+__device__ __forceinline__ void load_tile(double* S, const double* src) {
+  for (int t = threadIdx.x; t < TT / 2; t += blockDim.x) {
+    const int r = (2 * t) / TB, c = (2 * t) % TB;
+    *reinterpret_cast<double2*>(S + r * LDT + c) = *reinterpret_cast<const double2*>(src + 2 * t);
   }
 }
-// O = op(X) op(Y)  (X^T when XT, Y^T when YT)
-template <bool XT, bool YT>
-__device__ __forceinline__ void mm(double (*O)[TB + 1], double (*X)[TB + 1], double (*Y)[TB + 1]) {
-  const int r0 = 2 * (threadIdx.x >> 4), c0 = 2 * (threadIdx.x & 15);
-  double a[4];
-  mm22<XT, YT>(a, X, Y, r0, c0);
-  O[r0][c0] = a[0]; O[r0][c0 + 1] = a[1]; O[r0 + 1][c0] = a[2]; O[r0 + 1][c0 + 1] = a[3];
+__device__ __forceinline__ void store_tile(double* dst, const double* S) {
+  for (int t = threadIdx.x; t < TT / 2; t += blockDim.x) {
+    const int r = (2 * t) / TB, c = (2 * t) % TB;
+    *reinterpret_cast<double2*>(dst + 2 * t) = *reinterpret_cast<const double2*>(S + r * LDT + c);
+  }
 }
-// G (global, leading dimension ld) -= op(X) op(Y)
-template <bool XT, bool YT>
-__device__ __forceinline__ void gsub(double* G, size_t ld, double (*X)[TB + 1], double (*Y)[TB + 1]) {
-  const int r0 = 2 * (threadIdx.x >> 4), c0 = 2 * (threadIdx.x & 15);
-  double a[4];
-  mm22<XT, YT>(a, X, Y, r0, c0);
-  G[r0 * ld + c0] -= a[0]; G[r0 * ld + c0 + 1] -= a[1];
-  G[(r0 + 1) * ld + c0] -= a[2]; G[(r0 + 1) * ld + c0 + 1] -= a[3];
-}
-
-// Cholesky of diagonal tile J (in A) -> L_JJ (Lo slot 0) and L_JJ^{-1} (Dinv),
-// by warp 0 alone: lane r owns row r of L in registers (right-looking with
-// shuffles; compile-time unrolled by template recursion so the row stays in
-// registers), then lane c owns column c of L^{-1} (forward substitution with
-// broadcast shared-memory reads of L).  rsqrt keeps the pivot chain short.
-template <int C>
-__device__ __forceinline__ void potrf_row_step(double (&x)[TB], double& invd, int r, bool& bad) {
-  if constexpr (C < TB) {
-    double d = __shfl_sync(0xffffffffu, x[C], C);
-    if (!(d > 0.0)) { bad = true; d = 1.0; }
-    const double inv = rsqrt(d);
-    if (r > C) x[C] *= inv;
-    if (r == C) { x[C] = d * inv; invd = inv; }
-    const double lrc = x[C];
+// O = X Y^T (32x32 tiles in shared memory), then op(O block) by the caller
+template <class F>
+__device__ __forceinline__ void tile_xyt(const double* X, const double* Y, F&& out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int q = C + 1; q < TB; ++q) {
-      const double lqc = __shfl_sync(0xffffffffu, lrc, q);
-      if (r >= q) x[q] -= lrc * lqc;
+  for (int h = 0; h < 2; ++h) {
+    const int o = w + 8 * h, bi = o >> 2, bj = o & 3;
+    F2c c = {0.0, 0.0}, e = {0.0, 0.0};
+#pragma unroll
+    for (int kb = 0; kb < 4; kb += 2) {
+      mxyt(c, frag(X, LDT, bi, kb, lane), frag(Y, LDT, bj, kb, lane));
+      mxyt(e, frag(X, LDT, bi, kb + 1, lane), frag(Y, LDT, bj, kb + 1, lane));
     }
-    potrf_row_step<C + 1>(x, invd, r, bad);
+    c.x += e.x;
+    c.y += e.y;
+    out(bi, bj, c);
   }
 }
+
+// Cholesky of one 8x8 SPD block -> L^{-1} (row-major in Is[0..63]).  Every
+// lane factors the block redundantly from shared memory (no shuffles on the
+// pivot chain: ~2x shorter than a row-per-lane factorization); lanes 0..7
+// then form the columns of L^{-1}.
 template <int R>
-__device__ __forceinline__ void inv_col_step(double (&d)[TB], int c, const double (*P)[TB + 1], const double* invd) {
-  if constexpr (R < TB) {
-    double a0 = (R == c) ? 1.0 : 0.0, a1 = 0.0;
+__device__ __forceinline__ void c8_inv(double (&d)[8], int c, const double (&a)[8][8], const double (&inv)[8]) {
+  if constexpr (R < 8) {
+    double acc = (R == c) ? 1.0 : 0.0;
 #pragma unroll
-    for (int m = 0; m + 1 < R; m += 2) {
-      a0 -= P[R][m] * d[m];
-      a1 -= P[R][m + 1] * d[m + 1];
-    }
-    if (R & 1) a0 -= P[R][R - 1] * d[R - 1];
-    d[R] = (R < c) ? 0.0 : (a0 + a1) * invd[R];
-    inv_col_step<R + 1>(d, c, P, invd);
+    for (int m = 0; m < R; ++m) acc -= a[R][m] * d[m];
+    d[R] = (R < c) ? 0.0 : acc * inv[R];
+    c8_inv<R + 1>(d, c, a, inv);
   }
 }
-
-__device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flags, FactorSmem& sm) {
-  const int tid = threadIdx.x;
-  auto& P = sm.P;
-  auto& D = sm.D;
-  load_tile(P, tile(B.A, g, J, 0));
-  __syncthreads();
-  if (tid < 32) {
-    const int r = tid;
-    double x[TB];
+__device__ __forceinline__ void potrf_inv8w(const double* S, int ld, double* Is, int lane, int* flags) {
+  double a[8][8];
 #pragma unroll
-    for (int q = 0; q < TB; ++q) x[q] = P[r][q];
-    double invd = 1.0;
-    bool bad = false;
-    potrf_row_step<0>(x, invd, r, bad);
-    if (bad && r == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int q = 0; q < TB; ++q) P[r][q] = q <= r ? x[q] : 0.0;
-    sm.Q[0][r] = invd;                // 1 / L[r][r]
-    __syncwarp();
-    double d[TB];
-    inv_col_step<0>(d, r, P, sm.Q[0]);
+    for (int j = 0; j <= i; ++j) a[i][j] = S[i * ld + j];
+  double inv[8];
+  bool bad = false;
 #pragma unroll
-    for (int rr = 0; rr < TB; ++rr) D[rr][r] = d[rr];
+  for (int c = 0; c < 8; ++c) {
+    double d = a[c][c];
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    inv[c] = rsqrt(d);
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) a[i][c] *= inv[c];
+#pragma unroll
+    for (int j = c + 1; j < 8; ++j)
+#pragma unroll
+      for (int i = j; i < 8; ++i) a[i][j] -= a[i][c] * a[j][c];
   }
-  __syncthreads();
-  store_tile(B.Dinv + (size_t)J * TT, D);
-  store_tile(tile(B.Lo, g, J, 0), P);
-  __syncthreads();
+  if (bad && lane == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
+  if (lane < 8) {
+    double d[8];
+    c8_inv<0>(d, lane, a, inv);
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = d[rr];
+  }
+  __syncwarp();
 }
 
-// Task f of tile column J: f < npairs -> trailing tile (t1, t2); else L^{-1}
-// row-panel J restricted to column tile f - npairs.  sm.D holds Dinv_J.
-__device__ void coarse_task(const Geo& g, int J, int f, int npairs, const CoarseBufs& B, FactorSmem& sm) {
-  auto& X1 = sm.P;
-  auto& X2 = sm.Q;
-  auto& T = sm.R;
-  auto& D = sm.D;
-  if (f < npairs) {
-    int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
-    while (t1 * (t1 - 1) / 2 > f) --t1;
-    while ((t1 + 1) * t1 / 2 <= f) ++t1;
-    const int t2 = f - t1 * (t1 - 1) / 2 + 1;
-    load_tile(T, tile(B.A, g, J, t1));
-    __syncthreads();
-    mm<false, true>(X1, T, D);                  // L_{J+t1,J} = A_{J+t1,J} Dinv^T
-    __syncthreads();
-    if (t2 != t1) {
-      load_tile(T, tile(B.A, g, J, t2));
-      __syncthreads();
-      mm<false, true>(X2, T, D);
-      __syncthreads();
-      gsub<false, true>(tile(B.A, g, J + t2, t1 - t2), TB, X1, X2);
-    } else {
-      gsub<false, true>(tile(B.A, g, J + t1, 0), TB, X1, X1);
-      store_tile(tile(B.Lo, g, J, t1), X1);
+// Blocked Cholesky of the diagonal tile J (in A, full symmetric 32x32) by one
+// CTA: four 8x8 diagonal blocks (potrf8 + inverse on warp 0), DMMA panel and
+// trailing updates; then Dinv_J = L_JJ^{-1} by block forward substitution in
+// transposed form, DT[i][j] = Dinv[i][j]^T = -(sum_k DT[k][j] L[i][k]^T) Li_i^T.
+// Writes Dinv_J (row-major) to the factor buffer.
+// tile_in_smem: sm.T already holds the (updated) diagonal tile.  Dinv_J is
+// also left row-major in sm.D for the caller's next column.
+__device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flags, FactorSmem& sm,
+                             bool tile_in_smem = false, long long* tprof = nullptr) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  auto stamp = [&](int k) {
+    if (tprof && tid == 0) tprof[k] += clock64();
+  };
+  stamp(0);
+  double* P = sm.T;
+  if (!tile_in_smem) load_tile(P, tile(B.A, g, J, 0));
+  __syncthreads();
+  for (int kb = 0; kb < 4; ++kb) {
+    if (w == 0) {
+      potrf_inv8w(P + 8 * kb * LDT + 8 * kb, LDT, sm.Is, lane, flags);
+      const int m = lane >> 2, q = lane & 3;
+      sm.Li[kb][2 * lane] = sm.Is[m * 8 + 2 * q];          // L_kk^{-1}, C layout
+      sm.Li[kb][2 * lane + 1] = sm.Is[m * 8 + 2 * q + 1];
     }
+    __syncthreads();
+    stamp(1 + 3 * kb);
+    if (w < 3 - kb) {                                      // L[i][kb] = A[i][kb] L_kk^{-T}
+      const int i = kb + 1 + w;
+      F2c c = {0.0, 0.0};
+      const F2c li = {sm.Li[kb][2 * lane], sm.Li[kb][2 * lane + 1]};
+      mxyt(c, frag(P, LDT, i, kb, lane), li);
+      put(P, LDT, i, kb, lane, c);
+    }
+    __syncthreads();
+    stamp(2 + 3 * kb);
+    {                                                      // trailing A[i][j] -= L[i][kb] L[j][kb]^T
+      int cnt = 0;
+      for (int i = kb + 1; i < 4; ++i)
+        for (int j = kb + 1; j <= i; ++j, ++cnt)
+          if (cnt == w) {
+            F2c c = frag(P, LDT, i, j, lane);
+            const F2c a = frag(P, LDT, i, kb, lane), b = frag(P, LDT, j, kb, lane);
+            mxyt(c, {-a.x, -a.y}, b);
+            put(P, LDT, i, j, lane, c);
+          }
+    }
+    __syncthreads();
+    stamp(3 + 3 * kb);
+  }
+  // Dinv in transposed blocks, held in sm.X2 (block (i,j) C layout of Dinv[i][j]^T)
+  double* DT = sm.X2;
+  if (w < 4) {                                             // DT[i][i] = Li_i^T
+    const int m = lane >> 2, q = lane & 3;
+    // C layout of Li^T: lane (m,q) holds Li[2q][m], Li[2q+1][m]; Li row-major is
+    // recovered from its C layout: Li[r][c] sits at lane 4r + c/2, slot c%2
+    const double* L = sm.Li[w];
+    const F2c f = {L[2 * (4 * (2 * q) + m / 2) + (m & 1)], L[2 * (4 * (2 * q + 1) + m / 2) + (m & 1)]};
+    put(DT, LDT, w, w, lane, f);
+  }
+  __syncthreads();
+  for (int d = 1; d < 4; ++d) {
+    if (w < 4 - d) {
+      const int j = w, i = j + d;
+      F2c z = {0.0, 0.0};
+      for (int k = j; k < i; ++k) mxyt(z, frag(DT, LDT, k, j, lane), frag(P, LDT, i, k, lane));
+      F2c o = {0.0, 0.0};
+      const F2c li = {sm.Li[i][2 * lane], sm.Li[i][2 * lane + 1]};
+      mxyt(o, {-z.x, -z.y}, li);
+      put(DT, LDT, i, j, lane, o);
+    }
+    __syncthreads();
+  }
+  stamp(13);
+  // Dinv row-major: Dinv[8i + 2q (+1)][8j + m] = DT[i][j] slot 0 (1) at lane (m, q)
+  double* dst = B.Dinv + (size_t)J * TT;
+  for (int o = w; o < 16; o += 8) {
+    const int i = o >> 2, j = o & 3, m = lane >> 2, q = lane & 3;
+    F2c f = {0.0, 0.0};
+    if (j <= i) f = frag(DT, LDT, i, j, lane);
+    dst[(8 * i + 2 * q) * TB + 8 * j + m] = f.x;
+    dst[(8 * i + 2 * q + 1) * TB + 8 * j + m] = f.y;
+    sm.D[(8 * i + 2 * q) * LDT + 8 * j + m] = f.x;
+    sm.D[(8 * i + 2 * q + 1) * LDT + 8 * j + m] = f.y;
+  }
+  __syncthreads();
+  stamp(14);
+}
+
+// Pair task f of tile column J: trailing tile (t1, t2), t2 <= t1, recomputing
+// the panel tiles it needs, L_{J+t,J} = A_{J+t,J} Dinv_J^T (so the panel TRSM
+// costs no grid barrier).  sm.D holds Dinv_J.
+// diag_to_smem (lookahead pair (1,1)): the updated diagonal tile goes to
+// sm.T for the POTRF that follows instead of back to global memory.
+__device__ void coarse_task(const Geo& g, int J, int f, const CoarseBufs& B, FactorSmem& sm,
+                            bool diag_to_smem = false) {
+  const int lane = threadIdx.x & 31;
+  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
+  while (t1 * (t1 - 1) / 2 > f) --t1;
+  while ((t1 + 1) * t1 / 2 <= f) ++t1;
+  const int t2 = f - t1 * (t1 - 1) / 2 + 1;
+  load_tile(sm.T, tile(B.A, g, J, t1));
+  __syncthreads();
+  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X1, LDT, bi, bj, lane, c); });
+  __syncthreads();
+  if (t2 != t1) {
+    load_tile(sm.T, tile(B.A, g, J, t2));
+    __syncthreads();
+    tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X2, LDT, bi, bj, lane, c); });
     __syncthreads();
   } else {
-    // Yf = Dinv_J Y_J ; W = Dinv_J^T Yf ; Y_{J+t} -= A_{J+t,J} W  (= L_{J+t,J} Yf)
-    const int cidx = f - npairs;
-    const size_t ld = y_dim(g);
-    double* Yj = B.Y + (size_t)J * TB * ld + (size_t)cidx * TB;
-    for (int t = threadIdx.x; t < TT; t += blockDim.x) T[t / TB][t % TB] = Yj[(t / TB) * ld + (t % TB)];
-    __syncthreads();
-    mm<false, false>(X1, D, T);
-    __syncthreads();
-    for (int t = threadIdx.x; t < TT; t += blockDim.x) Yj[(t / TB) * ld + (t % TB)] = X1[t / TB][t % TB];
-    mm<true, false>(X2, D, X1);
-    __syncthreads();
-    const int pt = min(g.PT, g.NT - 1 - J);
-    for (int t = 1; t <= pt; ++t) {
-      load_tile(T, tile(B.A, g, J, t));
-      __syncthreads();
-      gsub<false, false>(B.Y + (size_t)(J + t) * TB * ld + (size_t)cidx * TB, ld, T, X2);
-      __syncthreads();
-    }
+    store_tile(tile(B.Lo, g, J, t1), sm.X1);
   }
+  const double* Y = (t2 != t1) ? sm.X2 : sm.X1;
+  double* G = tile(B.A, g, J + t2, t1 - t2);
+  // G -= X1 Y^T, block by block straight from / to global
+  const int wv = threadIdx.x >> 5;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
+    F2c c = frag(G, TB, bi, bj, lane), e = {0.0, 0.0};
+#pragma unroll
+    for (int kb = 0; kb < 4; kb += 2) {
+      const F2c a = frag(sm.X1, LDT, bi, kb, lane), a2 = frag(sm.X1, LDT, bi, kb + 1, lane);
+      mxyt(c, {-a.x, -a.y}, frag(Y, LDT, bj, kb, lane));
+      mxyt(e, {-a2.x, -a2.y}, frag(Y, LDT, bj, kb + 1, lane));
+    }
+    c.x += e.x;
+    c.y += e.y;
+    if (diag_to_smem)
+      put(sm.T, LDT, bi, bj, lane, c);
+    else
+      put(G, TB, bi, bj, lane, c);
+  }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_coarse_factor(Geo g, double* __restrict__ base, int* __restrict__ flags) {
-  __shared__ FactorSmem sm;
+__global__ void __launch_bounds__(256, 1) k_coarse_factor(Geo g, double* __restrict__ base, int* __restrict__ flags) {
+  __shared__ __align__(16) FactorSmem sm;
   cg::grid_group grid = cg::this_grid();
   const CoarseBufs B = coarse_bufs(g, base);
-  const bool withY = B.Y != nullptr;
-  if (withY) {
-    const size_t ld = y_dim(g);
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ld; i += (size_t)gridDim.x * blockDim.x)
-      B.Y[i * ld + i] = 1.0;
-  }
   if (blockIdx.x == 0) coarse_potrf(g, 0, B, flags, sm);
   grid.sync();
   for (int J = 0; J < g.NT; ++J) {
     const int pt = min(g.PT, g.NT - 1 - J);
     const int npairs = pt * (pt + 1) / 2;
-    const int ntasks = npairs + (withY ? J + 1 : 0);
-    load_tile(sm.D, B.Dinv + (size_t)J * TT);
+    if (blockIdx.x != 0) load_tile(sm.D, B.Dinv + (size_t)J * TT);   // CTA 0 kept it from its POTRF
     __syncthreads();
     if (blockIdx.x == 0 && pt >= 1) {
-      coarse_task(g, J, 0, npairs, B, sm);       // pair (1,1): next diagonal tile
-      __threadfence_block();
-      coarse_potrf(g, J + 1, B, flags, sm);      // lookahead factor of column J+1
+      coarse_task(g, J, 0, B, sm, true);         // pair (1,1): next diagonal tile, into sm.T
+      coarse_potrf(g, J + 1, B, flags, sm, true);  // lookahead factor of column J+1
     }
     // the other CTAs share everything except the lookahead pair
     const int first = (pt >= 1) ? 1 : 0;
     const int nw = gridDim.x > 1 ? gridDim.x - 1 : 1;
     if (gridDim.x == 1 || blockIdx.x > 0) {
       const int me = gridDim.x > 1 ? blockIdx.x - 1 : 0;
-      for (int f = first + me; f < ntasks; f += nw) coarse_task(g, J, f, npairs, B, sm);
+      for (int f = first + me; f < npairs; f += nw) coarse_task(g, J, f, B, sm);
     }
     grid.sync();
-  }
-}
-
-// -------------------------------------------------- solves with L^{-1}
-
-constexpr int SCH = 16;   // sources per pass
-
-// Z[r][s] = sum_{c <= r} Y[r][c] X[c][s]; CTA per row tile, warp w owns rows
-// w, w+8, w+16, w+24, lanes run over the 32 columns of each column tile.
-__global__ void __launch_bounds__(256) k_coarse_inv_lower(Geo g, const double* __restrict__ Y, const double* __restrict__ X,
-                                                          double* __restrict__ Z, int nrhs) {
-  __shared__ double Xs[TB][SCH + 1];
-  const int I = blockIdx.x;
-  const size_t ld = y_dim(g);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int s0 = 0; s0 < nrhs; s0 += SCH) {
-    double acc[4][SCH];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int s = 0; s < SCH; ++s) acc[q][s] = 0.0;
-    for (int C = 0; C <= I; ++C) {
-      __syncthreads();
-      for (int t = tid; t < TB * SCH; t += blockDim.x) {
-        int c = t / SCH, s = t % SCH, row = C * TB + c;
-        Xs[c][s] = (row < g.kc && s0 + s < nrhs) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double yv = __ldg(Y + (size_t)(I * TB + w + 8 * q) * ld + (size_t)C * TB + lane);
-#pragma unroll
-        for (int s = 0; s < SCH; ++s) acc[q][s] += yv * Xs[lane][s];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-#pragma unroll
-      for (int s = 0; s < SCH; ++s) {
-        double v = acc[q][s];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        acc[q][s] = v;
-      }
-      const int row = I * TB + w + 8 * q;
-      if (lane < SCH && row < g.kc && s0 + lane < nrhs) {
-        double v = 0.0;
-#pragma unroll
-        for (int s = 0; s < SCH; ++s) v = (s == lane) ? acc[q][s] : v;
-        Z[(size_t)row * nrhs + s0 + lane] = v;
-      }
-    }
-  }
-}
-
-// X[c][s] = sum_{r >= c} Y[r][c] Z[r][s]; CTA per column tile, lanes over its
-// 32 columns, warps over rows, smem reduction across warps.
-__global__ void __launch_bounds__(256) k_coarse_inv_upper(Geo g, const double* __restrict__ Y, const double* __restrict__ Z,
-                                                          double* __restrict__ X, int nrhs) {
-  __shared__ double Zs[TB][SCH + 1];
-  __shared__ double red[8][TB][SCH + 1];
-  const int C = blockIdx.x;
-  const size_t ld = y_dim(g);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int s0 = 0; s0 < nrhs; s0 += SCH) {
-    double acc[SCH];
-#pragma unroll
-    for (int s = 0; s < SCH; ++s) acc[s] = 0.0;
-    for (int I = C; I < g.NT; ++I) {
-      __syncthreads();
-      for (int t = tid; t < TB * SCH; t += blockDim.x) {
-        int rr = t / SCH, s = t % SCH, row = I * TB + rr;
-        Zs[rr][s] = (row < g.kc && s0 + s < nrhs) ? Z[(size_t)row * nrhs + s0 + s] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int rr = w + 8 * q;
-        const double yv = __ldg(Y + (size_t)(I * TB + rr) * ld + (size_t)C * TB + lane);
-#pragma unroll
-        for (int s = 0; s < SCH; ++s) acc[s] += yv * Zs[rr][s];
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < SCH; ++s) red[w][lane][s] = acc[s];
-    __syncthreads();
-    for (int t = tid; t < TB * SCH; t += blockDim.x) {
-      int c = t / SCH, s = t % SCH;
-      double v = 0.0;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) v += red[p][c][s];
-      const int row = C * TB + c;
-      if (row < g.kc && s0 + s < nrhs) X[(size_t)row * nrhs + s0 + s] = v;
-    }
-    __syncthreads();
   }
 }
 
@@ -572,134 +549,6 @@ __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __rest
   }
 }
 
-// Step-buffered variant: all PT+1 factor tiles of a column step are staged
-// in shared memory at once (double-buffered with cp.async one step ahead; row
-// stride TB+2 doubles to avoid bank conflicts), so each step is two
-// barrier-separated GEMV phases over all 256 threads.
-constexpr int TS = TB + 2;            // padded smem row stride (16-byte granules)
-constexpr int TTS = TB * TS;
-template <int RC>
-__global__ void __launch_bounds__(256) k_coarse_trsv_step(Geo g, const double* __restrict__ Lk,
-                                                          const double* __restrict__ Dinv, double* __restrict__ X,
-                                                          int nrhs) {
-  extern __shared__ __align__(16) double tsm[];
-  const int W = g.PT + 1;
-  double* buf[2] = {tsm, tsm + (size_t)W * TTS};                // slot 0 = Dinv_J, slot t = L_{J+t,J}
-  double* Xw = tsm + (size_t)2 * W * TTS;                         // [PT+1][TB][RC] rhs ring
-  double* Ys = Xw + (size_t)W * TB * RC;                          // [TB][RC]
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int s0 = blockIdx.x * RC;
-  const int ns = min(RC, nrhs - s0);
-  auto cp_tile = [&](double* dst, const double* src) {
-    for (int i = tid; i < TT / 2; i += nt) {
-      const int r = (2 * i) / TB, c = (2 * i) % TB;
-      cpa16(dst + r * TS + c, src + 2 * i);
-    }
-  };
-  auto issue = [&](int J, double* dst) {
-    if (J >= 0 && J < g.NT) {
-      const int pt = min(g.PT, g.NT - 1 - J);
-      cp_tile(dst, Dinv + (size_t)J * TT);
-      for (int t = 1; t <= pt; ++t) cp_tile(dst + (size_t)t * TTS, tile(Lk, g, J, t));
-    }
-    cpa_commit();
-  };
-  auto load_rows = [&](int I, double* dst) {
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = I * TB + r;
-      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-    }
-  };
-  // ---------------- forward: y_J = Dinv_J x_J ; x_{J+t} -= L_{J+t,J} y_J
-  issue(0, buf[0]);
-  issue(1, buf[1]);
-  for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
-  for (int J = 0; J < g.NT; ++J) {
-    const int pt = min(g.PT, g.NT - 1 - J);
-    double* T = buf[J & 1];
-    cpa_wait<1>();
-    __syncthreads();
-    const double* xj = Xw + (size_t)(J % W) * TB * RC;
-    for (int q = tid; q < TB * RC; q += nt) {
-      const int r = q / RC, s = q % RC;
-      const double* tr = T + r * TS;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < TB; c += 2) { v0 += tr[c] * xj[c * RC + s]; v1 += tr[c + 1] * xj[(c + 1) * RC + s]; }
-      const double v = v0 + v1;
-      Ys[q] = v;
-      const int row = J * TB + r;
-      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-    }
-    __syncthreads();
-    for (int q = tid; q < pt * TB * RC; q += nt) {
-      const int tt = 1 + q / (TB * RC), rem = q % (TB * RC), r = rem / RC, s = rem % RC;
-      const double* L = T + (size_t)tt * TTS + r * TS;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < TB; c += 2) { v0 += L[c] * Ys[c * RC + s]; v1 += L[c + 1] * Ys[(c + 1) * RC + s]; }
-      Xw[(size_t)((J + tt) % W) * TB * RC + rem] -= v0 + v1;
-    }
-    __syncthreads();
-    load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);
-    issue(J + 2, buf[J & 1]);
-  }
-  cpa_wait<0>();
-  __syncthreads();
-  // ---------------- backward: x_J = Dinv_J^T (y_J - sum_t L_{J+t,J}^T x_{J+t})
-  issue(g.NT - 1, buf[0]);
-  issue(g.NT - 2, buf[1]);
-  constexpr int SPLIT = 256 / (TB * RC) > 0 ? 256 / (TB * RC) : 1;   // threads per output
-  for (int it = 0; it < g.NT; ++it) {
-    const int J = g.NT - 1 - it;
-    const int pt = min(g.PT, g.NT - 1 - J);
-    double* T = buf[it & 1];
-    cpa_wait<1>();
-    __syncthreads();
-    {
-      const int q = tid / SPLIT, part = tid % SPLIT;
-      double v0 = 0.0, v1 = 0.0;
-      if (q < TB * RC) {
-        const int c = q / RC, s = q % RC;
-        for (int tt = 1 + part; tt <= pt; tt += SPLIT) {
-          const double* L = T + (size_t)tt * TTS + c;
-          const double* xt = Xw + (size_t)((J + tt) % W) * TB * RC + s;
-#pragma unroll 8
-          for (int r = 0; r < TB; r += 2) { v0 += L[r * TS] * xt[r * RC]; v1 += L[(r + 1) * TS] * xt[(r + 1) * RC]; }
-        }
-      }
-      double v = v0 + v1;
-#pragma unroll
-      for (int off = SPLIT / 2; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off, SPLIT);
-      if (q < TB * RC && part == 0) {
-        const int c = q / RC, s = q % RC, row = J * TB + c;
-        const double y = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-        Ys[q] = y - v;
-      }
-    }
-    __syncthreads();
-    double* xo = Xw + (size_t)(J % W) * TB * RC;
-    for (int q = tid; q < TB * RC; q += nt) {
-      const int r = q / RC, s = q % RC, row = J * TB + r;
-      double v = 0.0;
-      for (int c = r; c < TB; ++c) v += T[c * TS + r] * Ys[c * RC + s];
-      if (row >= g.kc || s >= ns) v = 0.0;
-      xo[q] = v;
-      if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-    }
-    __syncthreads();
-    issue(J - 2, buf[it & 1]);
-  }
-  cpa_wait<0>();
-}
-
-namespace {
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-}  // namespace
 
 // ----------------------------------------------------------- bulk solves
 //
@@ -1030,10 +879,6 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   }
   if (coop_grid <= 0) return cudaErrorNotSupported;
   CoarseBufs B = coarse_bufs(g, Ak);
-  if (B.Y) {
-    cudaError_t e = cudaMemsetAsync(B.Y, 0, y_dim(g) * y_dim(g) * sizeof(double), st);
-    if (e != cudaSuccess) return e;
-  }
   Geo gg = g;
   void* args[] = {(void*)&gg, (void*)&Ak, (void*)&flags};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_coarse_factor, dim3(coop_grid), dim3(256), args, 0, st);
@@ -1047,13 +892,6 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
 cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
   CoarseBufs B = coarse_bufs(g, const_cast<double*>(Ak));
-  if (B.Y) {
-    k_coarse_inv_lower<<<g.NT, 256, 0, st>>>(g, B.Y, X, scratch, nrhs);
-    count_launches(1);
-    k_coarse_inv_upper<<<g.NT, 256, 0, st>>>(g, B.Y, scratch, X, nrhs);
-    count_launches(1);
-    return cudaGetLastError();
-  }
   constexpr int RC = 4;
   int cht = 0, ns = 0;
   size_t smem_b = 0;
@@ -1062,14 +900,6 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
     cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
     if (e != cudaSuccess) return e;
     k_coarse_trsv_bulk<<<nblk(nrhs, 8), 256, smem_b, st>>>(g, B.LF, B.LB, X, nrhs, cht, ns);
-    count_launches(1);
-    return cudaGetLastError();
-  }
-  const size_t smem_s = ((size_t)2 * (g.PT + 1) * TTS + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
-  if (smem_s <= 200 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_step<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
-    if (e != cudaSuccess) return e;
-    k_coarse_trsv_step<RC><<<nblk(nrhs, RC), 256, smem_s, st>>>(g, B.Lo, B.Dinv, X, nrhs);
     count_launches(1);
     return cudaGetLastError();
   }

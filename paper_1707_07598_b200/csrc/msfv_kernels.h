@@ -11,7 +11,6 @@ constexpr int SOLVE_NSC = 8;
 constexpr int SOLVE_RING = 8;
 constexpr int RESTRICT_THREADS = 128;
 constexpr int COARSE_TB = 32;
-constexpr int COARSE_INV_MAX = 0;      // dense L^{-1} for the coarse solves up to this k (0: off; MSFV_COARSE_INV=1 forces)
 constexpr int TC_WARPS = 2;      // warps (= coarse blocks) per CTA in the DMMA kernels
 constexpr int TC_MAX_PT = 7;     // largest tile band handled by the DMMA kernels (p <= 56)
 

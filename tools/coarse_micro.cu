@@ -5,21 +5,22 @@
 #include "../paper_1707_07598_b200/csrc/msfv_coarse.cu"
 namespace msfv {
 void count_launches(long long) {}
+__device__ long long g_tprof[16];
 __global__ void k_probe(Geo g, double* base, int* flags, int which, int reps) {
   __shared__ FactorSmem sm;
   const CoarseBufs B = coarse_bufs(g, base);
   load_tile(sm.D, B.Dinv);
   __syncthreads();
   for (int i = 0; i < reps; ++i) {
-    if (which == 0) coarse_potrf(g, 0, B, flags, sm);
-    else coarse_task(g, 0, which - 1, g.PT * (g.PT + 1) / 2, B, sm);
+    if (which == 0) coarse_potrf(g, 0, B, flags, sm, false, g_tprof);
+    else coarse_task(g, 0, which - 1, B, sm);
   }
 }
 }  // namespace msfv
 using namespace msfv;
 int main1() {
   Geo g{};
-  g.NT = 154; g.PT = 10; g.kc = 154 * 32 - 15; g.TB = 32; g.coarse_inv = 0;
+  g.NT = 154; g.PT = 10; g.kc = 154 * 32 - 15; g.TB = 32;
   size_t n = coarse_doubles(g);
   double* base; cudaMalloc(&base, n * 8);
   // SPD-ish band: identity diag tiles * 100, zero elsewhere
@@ -38,17 +39,23 @@ int main1() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     printf("%-10s %.3f us per call (%s)\n", names[which], ms * 1000 / reps, cudaGetErrorString(cudaGetLastError()));
+    if (which == 0) {
+      long long tp[16];
+      cudaMemcpyFromSymbol(tp, g_tprof, sizeof(tp));
+      printf("  potrf phases (cycles, avg):");
+      for (int k = 1; k <= 14; ++k) printf(" %lld", (tp[k] - tp[k - 1]) / (reps + 2));
+      printf("\n");
+    }
   }
   return 0;
 }
 // (appended) instrumented copy of the cooperative factor loop
 namespace msfv {
-__global__ void __launch_bounds__(256) k_factor_timed(Geo g, double* __restrict__ base, int* __restrict__ flags,
+__global__ void __launch_bounds__(256, 1) k_factor_timed(Geo g, double* __restrict__ base, int* __restrict__ flags,
                                                       unsigned long long* ts) {
   __shared__ FactorSmem sm;
   cg::grid_group grid = cg::this_grid();
   const CoarseBufs B = coarse_bufs(g, base);
-  const bool withY = B.Y != nullptr;
   auto now = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
   if (blockIdx.x == 0) coarse_potrf(g, 0, B, flags, sm);
   grid.sync();
@@ -56,21 +63,21 @@ __global__ void __launch_bounds__(256) k_factor_timed(Geo g, double* __restrict_
     unsigned long long t0 = now();
     const int pt = min(g.PT, g.NT - 1 - J);
     const int npairs = pt * (pt + 1) / 2;
-    const int ntasks = npairs + (withY ? J + 1 : 0);
-    load_tile(sm.D, B.Dinv + (size_t)J * TT);
+    const int ntasks = npairs;
+    if (blockIdx.x != 0) load_tile(sm.D, B.Dinv + (size_t)J * TT);
     __syncthreads();
     unsigned long long t1 = now(), t2 = t1, t3 = t1;
     if (blockIdx.x == 0 && pt >= 1) {
-      coarse_task(g, J, 0, npairs, B, sm);
+      coarse_task(g, J, 0, B, sm, true);
       t2 = now();
-      coarse_potrf(g, J + 1, B, flags, sm);
+      coarse_potrf(g, J + 1, B, flags, sm, true);
       t3 = now();
     }
     const int first = (pt >= 1) ? 1 : 0;
     const int nw = gridDim.x > 1 ? gridDim.x - 1 : 1;
     if (gridDim.x == 1 || blockIdx.x > 0) {
       const int me = gridDim.x > 1 ? blockIdx.x - 1 : 0;
-      for (int f = first + me; f < ntasks; f += nw) coarse_task(g, J, f, npairs, B, sm);
+      for (int f = first + me; f < ntasks; f += nw) coarse_task(g, J, f, B, sm);
     }
     unsigned long long t4 = now();
     grid.sync();
@@ -86,7 +93,7 @@ __global__ void __launch_bounds__(256) k_factor_timed(Geo g, double* __restrict_
 int main2() {
   using namespace msfv;
   Geo g{};
-  g.NT = 154; g.PT = 10; g.kc = 154 * 32 - 15; g.TB = 32; g.coarse_inv = 0;
+  g.NT = 154; g.PT = 10; g.kc = 154 * 32 - 15; g.TB = 32;
   size_t n = coarse_doubles(g);
   double* base; cudaMalloc(&base, n * 8); cudaMemset(base, 0, n * 8);
   double* h = (double*)calloc(band_tiles(g) * 1024, 8);
