@@ -181,6 +181,31 @@ MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, con
  * out: k x nrhs. */
 MSFV_API int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
                        const msfv_points* pr, const double* Rc, double* part, double* out, void* stream);
+/* ---- Table-3 operators: materialized basis derivatives (basis.py:684-800) ----
+ * apply_Yk: W = G_p^T diag(G_p S v) Csig restricted to block interiors and the
+ * block's cells; Y_k = -blockdiag(A_II^-1) W as an n x N_m CSR.
+ *   msfv_yk_rhs: rhs_c[nblocks][nI][b1*b2*b3] = W (zeroed first) from Sv = S v
+ *     (a node field, msfv_prolong) and sigma; mask[nblocks][ceil(b1b2b3/32)]
+ *     marks the non-zero columns (the reference's Wd.any(axis=0)).
+ *   msfv_block_solve_compact: out_c = blockdiag(A_II^-1) rhs_c for all blocks
+ *     (compact layout, block-major).
+ *   msfv_yk_rowcount: entries per pinned row; msfv_yk_scatter: CSR (int32
+ *     indices, ascending) of -out_c with the row pointer from the counts.
+ * apply_Xk: z = interior_solve(w) (msfv_interior_solve, node field).
+ *   msfv_xk_present: blocks with z != 0 (the reference's np.any(a_j));
+ *   msfv_xk_rowcount: entries per coarse row; msfv_xk_values: CSR values and
+ *   ascending column indices. */
+MSFV_API int msfv_yk_rhs(const msfv_plan* plan, const double* sigma, const double* Sv, double* rhs_c, uint32_t* mask,
+                void* stream);
+MSFV_API int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const double* rhs_c, double* out_c,
+                             int32_t nrhs, void* stream);
+MSFV_API int msfv_yk_rowcount(const msfv_plan* plan, const uint32_t* mask, int64_t* counts, void* stream);
+MSFV_API int msfv_yk_scatter(const msfv_plan* plan, const uint32_t* mask, const double* sol_c, const int64_t* indptr,
+                    int32_t* indices, double* vals, void* stream);
+MSFV_API int msfv_xk_present(const msfv_plan* plan, const double* z, int32_t* present, void* stream);
+MSFV_API int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* counts, void* stream);
+MSFV_API int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
+                   const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream);
 
 #ifdef __cplusplus
 }

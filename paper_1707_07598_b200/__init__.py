@@ -19,6 +19,7 @@ from .inversion import (
     misfit_ssd, Objective, GNConfig, projected_gauss_newton, AdaptiveReducedProblem,
     cell_gradient, project_bounds, add_noise, tikhonov_reg, InversionTrace,
 )
+from .table3 import apply_Yk, apply_Xk, apply_Yk_dev, apply_Xk_dev
 from .errors import (
     InvalidModelError, FactorizationError, SolverBreakdown,
     StaleBasisError, ReducedSingularError,

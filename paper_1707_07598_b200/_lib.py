@@ -68,6 +68,13 @@ SIGNATURES = {
     "msfv_points_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P]),
     "msfv_block_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "msfv_jv_coarse_rhs": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
+    "msfv_yk_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "msfv_block_solve_compact": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv_yk_rowcount": (ctypes.c_int, [_P, _P, _P, _P]),
+    "msfv_yk_scatter": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "msfv_xk_present": (ctypes.c_int, [_P, _P, _P, _P]),
+    "msfv_xk_rowcount": (ctypes.c_int, [_P, _P, _P, _P]),
+    "msfv_xk_values": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _LIB = None

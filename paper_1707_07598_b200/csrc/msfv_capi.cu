@@ -394,7 +394,7 @@ int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, co
   if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
   const Geo& g = plan->g;
   if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "compact interior solve needs the tensor-core band path");
-  return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk, pts->d.nib),
+  return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk, pts->d.nib, 1),
                     "points_interior_solve");
 }
 
@@ -423,6 +423,61 @@ int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* 
   int rc = cuda_check(launch_jv_block(g, Sint, c, T, nrhs, hr ? pr->d.islot : nullptr, Rc, part, st), "jv_block");
   if (rc) return rc;
   return cuda_check(launch_gather_corners(g, part, nrhs, -1.0, out, st), "jv_gather");
+}
+
+int msfv_yk_rhs(const msfv_plan* plan, const double* sigma, const double* Sv, double* rhs_c, uint32_t* mask,
+                void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t ncb = (size_t)g.b1 * g.b2 * g.b3, words = (ncb + 31) / 32;
+  cudaError_t e = cudaMemsetAsync(rhs_c, 0, (size_t)g.nbl * g.nI * ncb * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(mask, 0, (size_t)g.nbl * words * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return cuda_check(e, "yk_rhs memset");
+  return cuda_check(launch_yk_rhs(g, sigma, Sv, rhs_c, mask, st), "yk_rhs");
+}
+
+int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const double* rhs_c, double* out_c,
+                             int32_t nrhs, void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "compact block solve needs the tensor-core band path");
+  return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
+                    "block_solve_compact");
+}
+
+int msfv_yk_rowcount(const msfv_plan* plan, const uint32_t* mask, int64_t* counts, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_yk_rowcount(plan->g, mask, (long long*)counts, (cudaStream_t)stream), "yk_rowcount");
+}
+
+int msfv_yk_scatter(const msfv_plan* plan, const uint32_t* mask, const double* sol_c, const int64_t* indptr,
+                    int32_t* indices, double* vals, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_yk_scatter(plan->g, mask, sol_c, (const long long*)indptr, indices, vals,
+                                      (cudaStream_t)stream), "yk_scatter");
+}
+
+int msfv_xk_present(const msfv_plan* plan, const double* z, int32_t* present, void* stream) {
+  CHECK_PLAN(plan);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(present, 0, (size_t)plan->g.nbl * sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_check(e, "xk_present memset");
+  return cuda_check(launch_xk_present(plan->g, z, present, st), "xk_present");
+}
+
+int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* counts, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_xk_rowcount(plan->g, present, (long long*)counts, (cudaStream_t)stream), "xk_rowcount");
+}
+
+int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
+                   const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  if (xk_smem_bytes(g) > 200 * 1024) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
+  return cuda_check(launch_xk_values(g, sigma, Sint, z, present, (const long long*)indptr, indices, vals,
+                                     (cudaStream_t)stream), "xk_values");
 }
 
 }  // extern "C"

@@ -52,7 +52,7 @@ size_t tc_scratch_doubles(const Geo& g);
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st);
 cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
-                                  cudaStream_t st, const int* blist = nullptr, int nlist = 0);
+                                  cudaStream_t st, const int* blist = nullptr, int nlist = 0, int compact = 0);
 
 // coarse (msfv_coarse.cu)
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
@@ -103,6 +103,17 @@ cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T,
 size_t jv_smem_doubles(const Geo& g, int nrhs);
 cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec, const double* T, int nrhs,
                             const int* rslot, const double* Rc, double* part, cudaStream_t st);
+// Table-3 operators (msfv_table3.cu)
+cudaError_t launch_yk_rhs(const Geo& g, const double* sigma, const double* Sv, double* rhs, unsigned* mask,
+                          cudaStream_t st);
+cudaError_t launch_yk_rowcount(const Geo& g, const unsigned* mask, long long* counts, cudaStream_t st);
+cudaError_t launch_yk_scatter(const Geo& g, const unsigned* mask, const double* sol, const long long* indptr,
+                              int* indices, double* vals, cudaStream_t st);
+cudaError_t launch_xk_present(const Geo& g, const double* zf, int* present, cudaStream_t st);
+cudaError_t launch_xk_rowcount(const Geo& g, const int* present, long long* counts, cudaStream_t st);
+size_t xk_smem_bytes(const Geo& g);
+cudaError_t launch_xk_values(const Geo& g, const double* sigma, const double* Sint, const double* zf, const int* present,
+                             const long long* indptr, int* indices, double* vals, cudaStream_t st);
 cudaError_t launch_gather_corners(const Geo& g, const double* part, int nrhs, double scale, double* out,
                                   cudaStream_t st);
 

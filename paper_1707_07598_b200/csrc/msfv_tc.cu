@@ -481,18 +481,19 @@ __global__ void __launch_bounds__(64) k_skel_galerkin(Geo g, const double* __res
 // prefetched into registers.  Right-hand sides are carried transposed (lane
 // 4c+q: rows 8I+2q, 8I+2q+1 of column c) so every product is X Y^T of two
 // C-layout tiles (see ld_t).  y is parked in out between the sweeps.
-// With blist != nullptr the warps run over the nlist listed blocks and rhs/out
-// are compact per-block interior fields (row slot*nI + a).
+// With compact != 0 the warps run over nlist blocks (blist[slot], or slot
+// itself when blist is null) and rhs/out are compact per-block interior
+// fields (row slot*nI + a).
 template <int PT, int NCH>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs,
-                 const int* __restrict__ blist, int nlist) {
+                 const int* __restrict__ blist, int nlist, int compact) {
   extern __shared__ int crd[];
   fill_coords(g, crd);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int widx = blockIdx.x * TC_WARPS + wid;
-  if (widx >= (blist ? nlist : g.nbl)) return;
+  if (widx >= (compact ? nlist : g.nbl)) return;
   const int jb = blist ? blist[widx] : widx;
   const int NTI = (g.nI + 7) >> 3;
   if (NTI == 0) return;
@@ -501,7 +502,7 @@ k_block_solve_tc(Geo g, const double* __restrict__ LT, const double* rhs, double
   const int c = lane >> 2, q = lane & 3;
   auto node_of = [&](int a) -> long long {
     if (a >= g.nI) return -1;
-    if (blist) return (long long)widx * g.nI + a;
+    if (compact) return (long long)widx * g.nI + a;
     const int v = crd[a];
     return node_id(g, X0 + (v & 1023), Y0 + ((v >> 10) & 1023), Z0 + (v >> 20));
   };
@@ -647,14 +648,14 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
 }
 template <int PT>
 static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
-                                     const int* blist, int nlist, cudaStream_t st) {
-  const int nw = blist ? nlist : g.nbl;
+                                     const int* blist, int nlist, int compact, cudaStream_t st) {
+  const int nw = compact ? nlist : g.nbl;
   const unsigned grid = (unsigned)((nw + TC_WARPS - 1) / TC_WARPS);
   const size_t smem = (size_t)g.nI * sizeof(int);
   if (nrhs > 8)
-    k_block_solve_tc<PT, 2><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs, blist, nlist);
+    k_block_solve_tc<PT, 2><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs, blist, nlist, compact);
   else
-    k_block_solve_tc<PT, 1><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs, blist, nlist);
+    k_block_solve_tc<PT, 1><<<grid, TC_WARPS * 32, smem, st>>>(g, LT, rhs, out, nrhs, blist, nlist, compact);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -675,17 +676,17 @@ cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* S
 }
 
 cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
-                                  cudaStream_t st, const int* blist, int nlist) {
-  if (g.nI == 0 || nrhs == 0 || (blist && nlist == 0)) return cudaSuccess;
+                                  cudaStream_t st, const int* blist, int nlist, int compact) {
+  if (g.nI == 0 || nrhs == 0 || (compact && nlist == 0)) return cudaSuccess;
   switch (tc_band(g)) {
-    case 0: return launch_solve_tc_t<0>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 1: return launch_solve_tc_t<1>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 2: return launch_solve_tc_t<2>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 3: return launch_solve_tc_t<3>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 4: return launch_solve_tc_t<4>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 5: return launch_solve_tc_t<5>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 6: return launch_solve_tc_t<6>(g, LT, rhs, out, nrhs, blist, nlist, st);
-    case 7: return launch_solve_tc_t<7>(g, LT, rhs, out, nrhs, blist, nlist, st);
+    case 0: return launch_solve_tc_t<0>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 1: return launch_solve_tc_t<1>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 2: return launch_solve_tc_t<2>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 3: return launch_solve_tc_t<3>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 4: return launch_solve_tc_t<4>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 5: return launch_solve_tc_t<5>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 6: return launch_solve_tc_t<6>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
+    case 7: return launch_solve_tc_t<7>(g, LT, rhs, out, nrhs, blist, nlist, compact, st);
     default: return cudaErrorInvalidValue;
   }
 }

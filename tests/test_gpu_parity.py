@@ -76,3 +76,44 @@ def test_edge_weights_last_ulp():
     builder.assemble(op)
     w = op.edge_weights
     assert np.max(np.abs(w - g["w"]) / np.abs(g["w"])) <= 1e-15
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_table3_operators_match_reference(name):
+    """apply_Yk / apply_Xk (basis.py:684-800): CSR pattern bit-exact, values <= 1e-10."""
+    g = load_golden(name)
+    if "v" not in g:
+        pytest.skip("fixture without Table-3 vectors (see test_table3_operators_match_oracle)")
+    gp, mesh, part, survey, builder = build_gpu(g)
+    op = gp.assemble_operator(mesh, g["m"])
+    basis = builder.assemble(op)
+    Y = gp.apply_Yk(basis, g["v"], g["m"])
+    assert np.array_equal(Y.indptr, g["Y_indptr"]), "Y_k indptr differs"
+    assert np.array_equal(Y.indices, g["Y_indices"]), "Y_k indices differ"
+    assert rel(Y.data, g["Y_data"]) <= TOL
+    X = gp.apply_Xk(basis, g["wv"], g["m"])
+    assert np.array_equal(X.indptr, g["X_indptr"]), "X_k indptr differs"
+    assert np.array_equal(X.indices, g["X_indices"]), "X_k indices differ"
+    assert rel(X.data, g["X_data"]) <= TOL
+    # stale-model contract (basis.py:333-337)
+    with pytest.raises(gp.StaleBasisError):
+        gp.apply_Yk(basis, g["v"], g["m"] + 1.0)
+
+
+def test_table3_operators_match_oracle(rng):
+    """apply_Yk / apply_Xk at 8^3-cell blocks (the BASELINE block size) against the oracle."""
+    from oracle import msfv_oracle as oracle
+    g = load_golden("c16_b8")
+    gp, mesh, part, survey, builder = build_gpu(g)
+    m = g["m"]
+    op = gp.assemble_operator(mesh, m)
+    basis = builder.assemble(op)
+    omesh = oracle.Mesh(*[int(x) for x in g["cells"]], *[float(x) for x in g["h"]])
+    obasis = oracle.build_basis(oracle.assemble(omesh, m), oracle.make_partition(omesh, *[int(x) for x in g["blocks"]]))
+    v = rng.standard_normal(basis.k)
+    w = rng.standard_normal(basis.n)
+    for got, ref in ((gp.apply_Yk(basis, v, m), oracle.apply_Yk(obasis, v, m)),
+                     (gp.apply_Xk(basis, w, m), oracle.apply_Xk(obasis, w, m))):
+        assert np.array_equal(got.indptr, ref.indptr)
+        assert np.array_equal(got.indices, ref.indices)
+        assert rel(got.data, ref.data) <= TOL
