@@ -119,7 +119,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline
 
-def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None):
+def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None, workers=1):
     """Time the CPU oracle forward+gradient on a z-slab of the config (same
     x/y extent, survey and per-block work; nz = 2 blocks) and return
     (seconds per slab iteration, scale factor to the full config, description)."""
@@ -127,6 +127,7 @@ def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None):
     import numpy as np
     from oracle import msfv_oracle as orc
     from paper_1707_07598_b200.models import CONFIGS, gaussian_field
+    orc.WORKERS = workers             # per-block loops on `workers` threads (reference: workers=os.cpu_count())
     c = CONFIGS[cfg_id]
     n, b = c["n"], c["b"]
     nz = 2 * b
@@ -148,7 +149,8 @@ def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None):
         if log:
             log(f"oracle slab iteration {it}: {dt:.2f} s")
     scale = n / nz
-    desc = (f"oracle port (numpy/scipy restatement of msinv, 1 thread, OPENBLAS_NUM_THREADS=1) forward+misfit+gradient "
+    desc = (f"oracle port (numpy/scipy restatement of msinv, {workers} worker thread(s) over blocks, "
+            f"OPENBLAS_NUM_THREADS=1) forward+misfit+gradient "
             f"on a {n}x{n}x{nz} z-slab ({part.n_blocks} of {(n // b) ** 3} blocks, same survey layout); "
             f"seconds scaled x{scale:g} to the full config (coarse solve scaled linearly, which understates CPU cost)")
     return float(np.median(ts)), scale, desc
@@ -367,12 +369,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=args.steps, warm=args.warmup, log=log)
+        workers = os.cpu_count() or 1
+        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=args.steps, warm=args.warmup, log=log,
+                                          workers=workers)
         v = t * scale
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc,
                                  "sample_seconds": t},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)

@@ -34,6 +34,20 @@ class OracleError(RuntimeError):
     pass
 
 
+# Thread count of the per-block loops (the reference's `workers`,
+# parallel.py:21-49).  LAPACK releases the GIL, so blocks run concurrently;
+# results are collected in block order, hence bitwise independent of WORKERS.
+WORKERS = 1
+
+
+def run_indexed(fn, n):
+    if WORKERS <= 1 or n <= 1:
+        return [fn(j) for j in range(n)]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=WORKERS) as ex:
+        return list(ex.map(fn, range(n), chunksize=max(1, n // (4 * WORKERS))))
+
+
 # --------------------------------------------------------------------- mesh
 
 @dataclass(frozen=True)
@@ -339,33 +353,40 @@ class Basis:
         """blockdiag(A_II^-1) on interiors, zero on the skeleton (basis.py:339-353)."""
         w = np.asarray(w, dtype=float)
         out = np.zeros_like(w)
-        for I, f in zip(self.I, self.factors):
-            if I.size:
-                out[I] = sla.cho_solve(f, w[I], check_finite=False)
+
+        def task(j):
+            I = self.I[j]
+            return sla.cho_solve(self.factors[j], w[I], check_finite=False) if I.size else None
+
+        for I, sol in zip(self.I, run_indexed(task, len(self.I))):
+            if sol is not None:
+                out[I] = sol
         return out
 
 
 def build_basis(op, part, cache=None):
     """Per-block Cholesky + solve, scatter into reference CSC order
-    (basis.py:511-616; _BlockFactor basis.py:258-298, dense path)."""
+    (basis.py:511-616; _BlockFactor basis.py:258-298, dense path).  The
+    per-block factor/solve runs on WORKERS threads (ordered, like
+    parallel.run_indexed, parallel.py:21-49)."""
     n = part.mesh.n_nodes - 1
     if cache is None:
         cache = build_cache(part, op.G, op.C)
     A = op.A
-    factors, sols = [], []
-    for j in range(part.n_blocks):
+
+    def task(j):
         I, B, cols = cache.I[j], cache.B[j], cache.cols[j]
         if I.size == 0:
-            factors.append(None)
-            sols.append(np.zeros((0, cols.size)))
-            continue
+            return None, np.zeros((0, cols.size))
         AI = A[I]
         A_II = AI[:, I].toarray()
         rhs = -(AI[:, B] @ cache.xb[j])                           # basis.py:548 (rhs0 = 0)
         f = sla.cho_factor(A_II, lower=True, check_finite=False)    # basis.py:275
-        factors.append(f)
-        sols.append(sla.cho_solve(f, rhs, check_finite=False) if cols.size
-                    else np.zeros((I.size, 0)))
+        return f, (sla.cho_solve(f, rhs, check_finite=False) if cols.size else np.zeros((I.size, 0)))
+
+    res = run_indexed(task, part.n_blocks)
+    factors = [r[0] for r in res]
+    sols = [r[1] for r in res]
     vcoo = cache.values.tocoo()
     flat = np.concatenate([vcoo.data] + [s.ravel() for s in sols])
     if cache.s_perm is None:                                         # basis.py:576-592
