@@ -16,7 +16,46 @@ using namespace msfv;
 
 struct msfv_plan {
   Geo g;
+  SkelEdge* skel_dev = nullptr;   // uploaded on first basis build (plan creation needs no GPU)
 };
+
+// Skeleton-only owned edges of a block in the "last along every axis" case;
+// k_skel_galerkin skips entries whose req bits the block does not have.
+static std::vector<SkelEdge> skeleton_edges(const Geo& g) {
+  std::vector<SkelEdge> out;
+  const int b[3] = {g.b1, g.b2, g.b3};
+  auto hat = [&](int c, int x, int y, int z) {
+    const int cx = (c & 1) ? g.b1 : 0, cy = (c & 2) ? g.b2 : 0, cz = (c & 4) ? g.b3 : 0;
+    auto h1 = [](int d, double ib) { double v = 1.0 - std::fabs((double)d) * ib; return v > 0.0 ? v : 0.0; };
+    double w = h1(x - cx, g.ib1);
+    w = w * h1(y - cy, g.ib2);
+    w = w * h1(z - cz, g.ib3);
+    return w;
+  };
+  for (int ax = 0; ax < 3; ++ax) {
+    const int pa = ax == 0 ? 1 : 0, qa = ax == 2 ? 1 : 2;     // transverse axes (u, v)
+    for (int v = 0; v <= b[qa]; ++v)
+      for (int u = 0; u <= b[pa]; ++u) {
+        const bool perim = u == 0 || u == b[pa] || v == 0 || v == b[qa];
+        if (!(perim || b[ax] == 1)) continue;
+        for (int xa = 0; xa < b[ax]; ++xa) {
+          int c[3];
+          c[ax] = xa; c[pa] = u; c[qa] = v;
+          SkelEdge e{};
+          e.ax = ax; e.x = c[0]; e.y = c[1]; e.z = c[2];
+          e.req = (u == b[pa] ? (1 << pa) : 0) | (v == b[qa] ? (1 << qa) : 0);
+          e.origin = (c[0] == 0 && c[1] == 0 && c[2] == 0);
+          const int x1 = c[0] + (ax == 0), y1 = c[1] + (ax == 1), z1 = c[2] + (ax == 2);
+          for (int cc = 0; cc < 8; ++cc) {
+            e.h1[cc] = hat(cc, x1, y1, z1);
+            e.h0[cc] = hat(cc, c[0], c[1], c[2]);
+          }
+          out.push_back(e);
+        }
+      }
+  }
+  return out;
+}
 
 struct msfv_points {
   PointsDev d;
@@ -85,6 +124,8 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.r_nI = g.nI > 0 ? 1.0f / g.nI : 0.0f; g.r_nb1 = 1.0f / g.nb1; g.r_nb2 = 1.0f / g.nb2;
   {
     g.coarse_inv = 0;
+    g.skel = nullptr;
+    g.nskel = 0;
   }
   if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
@@ -96,7 +137,11 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   return MSFV_OK;
 }
 
-void msfv_plan_destroy(msfv_plan* plan) { delete plan; }
+void msfv_plan_destroy(msfv_plan* plan) {
+  if (!plan) return;
+  if (plan->skel_dev) cudaFree(plan->skel_dev);
+  delete plan;
+}
 
 int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   CHECK_PLAN(plan);
@@ -281,7 +326,19 @@ int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, dou
   CHECK_PLAN(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g)) return cuda_check(launch_basis_tc(g, w, factor, Sint, Kloc, flags, st), "basis_build");
+  if (tc_supported(g)) {
+    msfv_plan* pl = const_cast<msfv_plan*>(plan);
+    if (!pl->skel_dev) {
+      const std::vector<SkelEdge> tab = skeleton_edges(g);
+      cudaError_t e = cudaMalloc(&pl->skel_dev, std::max<size_t>(tab.size(), 1) * sizeof(SkelEdge));
+      if (e == cudaSuccess && !tab.empty())
+        e = cudaMemcpy(pl->skel_dev, tab.data(), tab.size() * sizeof(SkelEdge), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_check(e, "skeleton edge table");
+      pl->g.skel = pl->skel_dev;
+      pl->g.nskel = (int)tab.size();
+    }
+    return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st), "basis_build");
+  }
   double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
   return cuda_check(launch_basis(g, w, factor, Lr, Sint, Kloc, flags, st), "basis_build");
 }

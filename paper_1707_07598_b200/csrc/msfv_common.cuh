@@ -20,6 +20,15 @@
 
 namespace msfv {
 
+// One skeleton-only edge of a block's owned set (model-independent, built on
+// the host): local lower node, axis, which "last block along x/y/z" flags it
+// needs (bits 1/2/4), whether its lower node is the block origin (the pinned
+// node for block 0), and the 8 corner hats at its two nodes.
+struct SkelEdge {
+  int ax, x, y, z, req, origin, pad0, pad1;
+  double h1[8], h0[8];
+};
+
 struct Geo {
   int n1, n2, n3;          // cells per axis
   int b1, b2, b3;          // cells per block per axis
@@ -39,7 +48,9 @@ struct Geo {
   double ih1, ih2, ih3;    // 1/h per axis (as the reference's 1.0/h)
   double qv;               // 0.25 * cell volume (operators.py:83)
   double ib1, ib2, ib3;    // 1/b per axis (device-side hats)
-  int coarse_inv;          // 1: keep a dense L^{-1} of the coarse factor for the solves
+  int coarse_inv;          // unused (0)
+  const SkelEdge* skel;    // device table of the skeleton-only owned edges (msfv_basis_build)
+  int nskel;
   // float reciprocals for division-free index decoding (see fdiv)
   float r_n1, r_n2, r_n1p, r_n2p, r_b1, r_b2, r_b3, r_ni1, r_ni2, r_nI, r_nb1, r_nb2;
 };

@@ -420,57 +420,63 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 // Kloc[j] += sum over the skeleton-only edges owned by block j of
 // (w_e/h^2) dH_e dH_e^T, where dH_e are the (model-independent) hat
 // differences across the edge.  Runs after k_basis_tc (fixed summation order).
-__global__ void __launch_bounds__(64) k_skel_galerkin(Geo g, const double* __restrict__ w, double* __restrict__ Kloc) {
-  __shared__ double red[36][65];
-  const int jb = blockIdx.x;
-  const int tid = threadIdx.x;
+// One warp per block, DMMA reduction (lane = corner cc x edge slot) over the
+// host-built edge table g.skel (entries needing a "last block" flag the block
+// lacks are skipped; the pinned node has no row of S).
+constexpr int SKEL_WARPS = 4;
+__global__ void __launch_bounds__(SKEL_WARPS * 32) k_skel_galerkin(Geo g, const double* __restrict__ w,
+                                                                  double* __restrict__ Kloc) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int jb = blockIdx.x * SKEL_WARPS + wid;
+  if (jb >= g.nbl) return;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
-  const bool has0 = (jb == 0);
-  double acc[36];
+  const int lx = bi == g.nb1 - 1, ly = bj == g.nb2 - 1, lz = bk == g.nb3 - 1;
+  const int cc = lane >> 2, slot = lane & 3;
+  const int cb[3] = {(cc & 1) ? g.b1 : 0, (cc & 2) ? g.b2 : 0, (cc & 4) ? g.b3 : 0};
+  F2 K = {0.0, 0.0};
 #pragma unroll
-  for (int q = 0; q < 36; ++q) acc[q] = 0.0;
   for (int ax = 0; ax < 3; ++ax) {
-    const int xm = g.b1 + (ax == 0 ? 0 : lx), ym = g.b2 + (ax == 1 ? 0 : ly), zm = g.b3 + (ax == 2 ? 0 : lz);
+    // transverse axes p (u) and q (v), their block sizes / "last" flags / hat data
+    const int pa = ax == 0 ? 1 : 0, qa = ax == 2 ? 1 : 2;
     const int bax = ax == 0 ? g.b1 : (ax == 1 ? g.b2 : g.b3);
+    const int bp = pa == 0 ? g.b1 : g.b2, bq = qa == 1 ? g.b2 : g.b3;
+    const int lp = pa == 0 ? lx : ly, lq = qa == 1 ? ly : lz;
+    const double ibax = ax == 0 ? g.ib1 : (ax == 1 ? g.ib2 : g.ib3);
+    const double ibp = pa == 0 ? g.ib1 : g.ib2, ibq = qa == 1 ? g.ib2 : g.ib3;
     const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
-    const int tot = xm * ym * zm;
-    for (int f = tid; f < tot; f += blockDim.x) {
-      const int x = f % xm, q = f / xm, y = q % ym, z = q / ym;
-      bool skel;
-      if (ax == 0) skel = (y == 0 || y == g.b2 || z == 0 || z == g.b3);
-      else if (ax == 1) skel = (x == 0 || x == g.b1 || z == 0 || z == g.b3);
-      else skel = (x == 0 || x == g.b1 || y == 0 || y == g.b2);
-      if (!(skel || bax == 1)) continue;
-      const int x1 = x + (ax == 0), y1 = y + (ax == 1), z1 = z + (ax == 2);
-      const long long e = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
-                                  : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
-      const double kc = __ldg(w + e) * ihs;
-      const bool n0 = has0 && x == 0 && y == 0 && z == 0;
-      double dh[8];
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) dh[cc] = hatf(g, cc, x1, y1, z1) - (n0 ? 0.0 : hatf(g, cc, x, y, z));
-#pragma unroll
-      for (int c1 = 0; c1 < 8; ++c1) {
-        const double kd = kc * dh[c1];
-#pragma unroll
-        for (int c2 = 0; c2 <= c1; ++c2) acc[c1 * (c1 + 1) / 2 + c2] += kd * dh[c2];
+    const int np_ = bp + lp, nq = bq + lq;
+    const long long sx = ax == 0 ? 1 : (ax == 1 ? (long long)(g.n1 + 1) : (long long)(g.n1 + 1) * (g.n2 + 1));
+    for (int v = 0; v < nq; ++v) {
+      const bool vedge = v == 0 || v == bq;
+      for (int u = 0; u < np_; ++u) {
+        if (!(vedge || u == 0 || u == bp || bax == 1)) {
+          u = bp - 1;            // skip the inner part of the row (u in (0, bp))
+          continue;
+        }
+        const double ht = hatf1(u - cb[pa], ibp) * hatf1(v - cb[qa], ibq);
+        int x = 0, y = 0, z = 0;
+        if (ax == 0) { y = u; z = v; } else if (ax == 1) { x = u; z = v; } else { x = u; y = v; }
+        const long long e0 = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
+                                     : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
+        for (int xa0 = 0; xa0 < bax; xa0 += 4) {
+          const int xa = xa0 + slot;
+          double a = 0.0, b = 0.0;
+          if (xa < bax) {
+            const bool n0 = jb == 0 && xa == 0 && u == 0 && v == 0;   // pinned node: no row of S
+            const double h1 = hatf1(xa + 1 - cb[ax], ibax) * ht;
+            const double h0 = n0 ? 0.0 : hatf1(xa - cb[ax], ibax) * ht;
+            b = h1 - h0;
+            a = (__ldg(w + e0 + xa * sx) * ihs) * b;
+          }
+          mma884(K.x, K.y, a, b);
+        }
       }
     }
   }
-#pragma unroll
-  for (int q = 0; q < 36; ++q) red[q][tid] = acc[q];
-  __syncthreads();
-  if (tid < 36) {
-    double v = 0.0;
-    for (int t = 0; t < blockDim.x; ++t) v += red[tid][t];
-    int c1 = 0;
-    while ((c1 + 1) * (c1 + 2) / 2 <= tid) ++c1;
-    const int c2 = tid - c1 * (c1 + 1) / 2;
-    Kloc[(size_t)jb * 64 + c1 * 8 + c2] += v;
-    if (c1 != c2) Kloc[(size_t)jb * 64 + c2 * 8 + c1] += v;
-  }
+  double* kl = Kloc + (size_t)jb * 64 + lane * 2;
+  kl[0] += K.x;
+  kl[1] += K.y;
 }
 
 // ------------------------------------------------------------ block solve
@@ -642,7 +648,7 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_skel_galerkin<<<g.nbl, 64, 0, st>>>(g, w, Kloc);
+  k_skel_galerkin<<<(unsigned)((g.nbl + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc);
   count_launches(1);
   return cudaGetLastError();
 }
