@@ -342,9 +342,21 @@ def run_gpu(args, rank, world, log):
     t_basis = phases.get("basis", float("nan")) / 1e3
     peak, peak_src = fp64_peak()
     achieved = fl_block * eng.nbl / t_basis / 1e12
-    roof = {"kernel": "k_basis (per-block A_II band Cholesky + 8-RHS solve + local Galerkin)",
+    traffic, traffic_src = None, None
+    try:
+        # dram__bytes_read.sum + dram__bytes_write.sum of k_basis_tc from the
+        # committed ncu --set full capture of this configuration
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu.json")))["full"]
+        kb = next(v for k, v in prof.items() if "k_basis_tc" in k)
+        if args.config == 4:
+            traffic = int(kb["dram_read_B"] + kb["dram_write_B"])
+            traffic_src = "profiles/r01_ncu.json (ncu --set full, k_basis_tc, bytes per launch)"
+    except Exception:  # noqa: BLE001
+        pass
+    roof = {"kernel": "k_basis_tc + k_skel_galerkin (per-block A_II band Cholesky, 8-RHS solve, local Galerkin)",
             "bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes", "traffic_source": traffic_src,
+            "algorithmic_bytes": int(eng.nbl * (eng.factor_doubles / eng.nbl * 8 + 8 * eng.nI * 8 + 64 * 8)),
             "flops_per_block": fl_block, "blocks_per_launch": eng.nbl, "launch_ms": round(t_basis * 1e3, 4),
             "peak_source": peak_src,
             "note": "FP64 bound: tcgen05 has no f64 kind; the kernel runs on DMMA (mma.sync m8n8k4 f64); "

@@ -15,10 +15,15 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 mesh, part, survey, m = config_problem(cfg)
 builder = gp.BasisBuilder(part)
 m_dev = torch.from_numpy(m).cuda()
+with_jv = len(sys.argv) > 3 and sys.argv[3] == "jv"
 for _ in range(steps):
     op = gp.assemble_operator(mesh, m_dev)
     basis = builder.assemble(op)
     D, st = forward_reduced_dev(op, survey, basis)
-    g = sensitivity_adaptive(st, survey).rapply_dev(D)
+    J = sensitivity_adaptive(st, survey)
+    g = J.rapply_dev(D)
+    if with_jv:                     # one CG-step pair of the config-4 GN iteration
+        jv = J.apply_dev(g)
+        g = J.rapply_dev(jv)
 torch.cuda.synchronize()
 print("profile_step done", float(g.norm()))
