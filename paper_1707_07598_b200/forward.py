@@ -75,6 +75,15 @@ class Survey:
 
 
 def _host(t):
+    """Device tensor -> numpy.  Large results go through a page-locked buffer
+    (torch's caching host allocator) so the copy runs at full link speed; the
+    returned array owns that buffer."""
+    if t.is_cuda and t.numel() * t.element_size() >= (1 << 20):
+        import torch
+        buf = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        buf.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return buf.numpy()
     return t.cpu().numpy()
 
 
