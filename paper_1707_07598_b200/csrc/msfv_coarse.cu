@@ -616,7 +616,7 @@ constexpr int TRSV_MAX_STAGES = 3;
 
 __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* __restrict__ LF,
                                                           const double* __restrict__ LB, double* __restrict__ X,
-                                                          int nrhs, int CHT, int NS) {
+                                                          int nrhs, int CHT, int NS, long long* tprof = nullptr) {
   extern __shared__ __align__(128) double bsm[];
   __shared__ __align__(8) unsigned long long bar[TRSV_MAX_STAGES];
   const int W = g.PT + 1;
@@ -715,8 +715,14 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
     }
     double ra = 0.0, rb = 0.0;
     if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + g.PT, wid, ra, rb);   // in flight during the step
+    long long tclk = 0, tw = 0;
+    if (tprof && tid == 0) tclk = clock64();
     mbar_wait(&bar[st], (par >> st) & 1u);
     par ^= 1u << st;
+    if (tprof && tid == 0) {
+      tw = clock64();
+      tprof[i < nf ? 0 : 3] += tw - tclk;
+    }
     if (i < nf) {
       // ---------- forward: y_J^T = r_J^T Dinv_J^T ; r_{J+t}^T -= y_J^T L_{J+t,J}^T
       if (ch == 0) {
@@ -740,23 +746,45 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
           stx(J, mi, c0, c1);
         }
         __syncthreads();
+        if (tprof && tid == 0) tprof[1] += clock64() - tw;
       }
       const int ta = max(t0, 1), tb = min(t1, pt);
       {
-        const int np = (tb - ta + 1) * 4;
-        for (int p = wid; p < np; p += 8) {
-          const int t = ta + (p >> 2), mi = p & 3;
-          double* acc = Rt + (size_t)(ring(jm, t) * 4 + mi) * 64 + 2 * lane;
-          double c0 = acc[0], c1 = acc[1];
-          const double* Tt = T + (size_t)(t - t0) * TT;
+        // each warp owns pieces wid, wid+8, ...: up to UP of them run as
+        // independent DMMA chains (kb outermost) so the chains overlap
+        constexpr int UP = 5;
+        double ny[4][2];
 #pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {
-            const double* x = piece(Ys, kb);
-            const double* y = piece(Tt, mi * 4 + kb);
-            mma_xyt(c0, c1, -x[0], -x[1], y[0], y[1]);
+        for (int kb = 0; kb < 4; ++kb) {
+          ny[kb][0] = -Ys[kb * 64 + 2 * lane];
+          ny[kb][1] = -Ys[kb * 64 + 2 * lane + 1];
+        }
+        const int np = (tb - ta + 1) * 4;
+        for (int p0 = wid; p0 < np; p0 += 8 * UP) {
+          double acc[UP][2];
+          double* ap[UP];
+          const double* tp[UP];
+#pragma unroll
+          for (int q = 0; q < UP; ++q) {
+            const int p = p0 + 8 * q;
+            const bool v = p < np;
+            const int t = ta + (v ? (p >> 2) : 0), mi = p & 3;
+            ap[q] = Rt + (size_t)(ring(jm, t) * 4 + mi) * 64 + 2 * lane;
+            tp[q] = T + (size_t)(t - t0) * TT + mi * 4 * 64 + 2 * lane;
+            acc[q][0] = v ? ap[q][0] : 0.0;
+            acc[q][1] = v ? ap[q][1] : 0.0;
           }
-          acc[0] = c0;
-          acc[1] = c1;
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+            for (int q = 0; q < UP; ++q)
+              if (p0 + 8 * q < np) mma_xyt(acc[q][0], acc[q][1], ny[kb][0], ny[kb][1], tp[q][kb * 64], tp[q][kb * 64 + 1]);
+#pragma unroll
+          for (int q = 0; q < UP; ++q)
+            if (p0 + 8 * q < np) {
+              ap[q][0] = acc[q][0];
+              ap[q][1] = acc[q][1];
+            }
         }
       }
       __syncthreads();
@@ -771,18 +799,31 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
       {
         const int nb = wid & 3, half = wid >> 2;
         const int ta = max(t0, 1), tb = min(t1, pt);
+        // up to UB tiles of this warp's parity as independent DMMA chains
+        constexpr int UB = 3;
         double e0 = 0.0, e1 = 0.0;
-        for (int t = ta + ((ta & 1) != half ? 1 : 0); t <= tb; t += 2) {
-          const double* xr = Rt + (size_t)ring(jm, t) * 256;
-          const double* Tt = T + (size_t)(t - t0) * TT;
+        const int tstart = ta + ((ta & 1) != half ? 1 : 0);
+        for (int tq = tstart; tq <= tb; tq += 2 * UB) {
+          double ac[UB][2];
+          const double* xp[UB];
+          const double* yp[UB];
 #pragma unroll
-          for (int kb = 0; kb < 4; kb += 2) {
-            const double* x = piece(xr, kb);
-            const double* y = piece(Tt, nb * 4 + kb);
-            const double* x2 = piece(xr, kb + 1);
-            const double* y2 = piece(Tt, nb * 4 + kb + 1);
-            mma_xyt(p0, p1, x[0], x[1], y[0], y[1]);
-            mma_xyt(e0, e1, x2[0], x2[1], y2[0], y2[1]);
+          for (int q = 0; q < UB; ++q) {
+            const int t = min(tq + 2 * q, tb);
+            xp[q] = Rt + (size_t)ring(jm, t) * 256 + 2 * lane;
+            yp[q] = T + (size_t)(t - t0) * TT + nb * 4 * 64 + 2 * lane;
+            ac[q][0] = ac[q][1] = 0.0;
+          }
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+            for (int q = 0; q < UB; ++q)
+              if (tq + 2 * q <= tb)
+                mma_xyt(ac[q][0], ac[q][1], xp[q][kb * 64], xp[q][kb * 64 + 1], yp[q][kb * 64], yp[q][kb * 64 + 1]);
+#pragma unroll
+          for (int q = 0; q < UB; ++q) {
+            e0 += ac[q][0];
+            e1 += ac[q][1];
           }
         }
         p0 += e0;
@@ -823,6 +864,7 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
       }
       __syncthreads();
     }
+    if (tprof && tid == 0) tprof[i < nf ? 2 : 5] += clock64() - tclk;
   }
 }
 
