@@ -181,6 +181,10 @@ MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, con
  * out: k x nrhs. */
 MSFV_API int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
                        const msfv_points* pr, const double* Rc, double* part, double* out, void* stream);
+/* Dense natural-order A_k (+ shift I), both triangles, k x k doubles: the
+ * reference's `ReducedState.A_k` attribute (forward.py:62-75,101-102). */
+MSFV_API int msfv_coarse_dense(const msfv_plan* plan, const double* Kloc, double shift, double* out, void* stream);
+
 /* ---- Table-3 operators: materialized basis derivatives (basis.py:684-800) ----
  * apply_Yk: W = G_p^T diag(G_p S v) Csig restricted to block interiors and the
  * block's cells; Y_k = -blockdiag(A_II^-1) W as an n x N_m CSR.

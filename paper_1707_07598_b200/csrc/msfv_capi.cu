@@ -123,7 +123,9 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.r_ni1 = g.ni1 > 0 ? 1.0f / g.ni1 : 0.0f; g.r_ni2 = g.ni2 > 0 ? 1.0f / g.ni2 : 0.0f;
   g.r_nI = g.nI > 0 ? 1.0f / g.nI : 0.0f; g.r_nb1 = 1.0f / g.nb1; g.r_nb2 = 1.0f / g.nb2;
   {
-    g.coarse_inv = 0;
+    // coarse nested dissection: on for k >= 1000 (MSFV_COARSE_ND=0/1 overrides)
+    const char* ev = getenv("MSFV_COARSE_ND");
+    g.coarse_nd = ev ? (atoi(ev) != 0) : (g.kc >= 1000);
     g.skel = nullptr;
     g.nskel = 0;
   }
@@ -157,7 +159,7 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_K] = g.kc;
   v[MSFV_INFO_AK_DOUBLES] = (int64_t)coarse_doubles(g);
   v[MSFV_INFO_BASIS_SMEM] = (int64_t)basis_smem_bytes(g);
-  v[MSFV_INFO_NT] = g.NT;
+  v[MSFV_INFO_NT] = coarse_tile_rows(g);
   v[MSFV_INFO_PT] = g.PT;
   v[MSFV_INFO_TB] = g.TB;
   v[MSFV_INFO_PC] = g.pc;
@@ -535,6 +537,11 @@ int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sin
   if (xk_smem_bytes(g) > 200 * 1024) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
   return cuda_check(launch_xk_values(g, sigma, Sint, z, present, (const long long*)indptr, indices, vals,
                                      (cudaStream_t)stream), "xk_values");
+}
+
+int msfv_coarse_dense(const msfv_plan* plan, const double* Kloc, double shift, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  return cuda_check(launch_coarse_dense(plan->g, Kloc, shift, out, (cudaStream_t)stream), "coarse_dense");
 }
 
 }  // extern "C"

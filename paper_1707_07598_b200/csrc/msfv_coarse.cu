@@ -1,31 +1,44 @@
 // Coarse (Galerkin) system: assembly of A_k = P^T A P from the per-block 8x8
-// contributions, banded tiled Cholesky, and the coarse solves.
+// contributions, its Cholesky factorization and the coarse solves.
 //
 // Reference: forward.py:101-142 forms A_k densely and calls LAPACK dpotrf
 // (cho_factor) for k <= 5000, SuperLU above.  A_k couples coarse nodes only
 // within a 27-point stencil, so in lexicographic coarse order its half
 // bandwidth is pc = (nb1+1)(nb2+1) + (nb1+1) + 1 and Cholesky fill stays
-// inside that band: the banded factorization below is the same Cholesky
-// factor as the reference's dense one, computed without the zero blocks.
+// inside that band: the banded factorization below is the Cholesky factor of
+// the (permuted) matrix, computed without the zero blocks.
 //
-// Buffer layout (one allocation of MSFV_INFO_AK_DOUBLES doubles):
-//   A     NT*(PT+1) tiles   lower band of A_k; tile column J holds (J+t, J),
-//                           t = 0..PT, each TB x TB row-major.  Updated in
-//                           place by the factorization (trailing tiles).
+// Nested dissection by coarse z-planes (coarse_nd): the middle plane zs is a
+// separator C; the planes below (part 0, natural order) and above (part 1,
+// planes in reverse order so the plane next to C comes last) are independent
+// banded systems factored concurrently, half the sequential depth of the
+// single band.  With L_q the part factors, the coupling blocks are
+// Z_q = L_q^{-1} A_{q,C} (non-zero only from the part's last plane on, since
+// A_{q,C} couples C to that plane), the separator Schur complement is
+// S = A_CC - Z_0^T Z_0 - Z_1^T Z_1 (dense P x P, P = plane size), factored as a
+// dense band.  Solves: forward sweeps on both parts, x_C -= Z^T y, full
+// separator solve, y -= Z x_C, backward sweeps.  Without coarse_nd the whole
+// system is one band (b[0]).
+//
+// Per band (one allocation, see coarse_layout):
+//   A     NT*(PT+1) tiles   lower band; tile column J holds (J+t, J), t = 0..PT,
+//                           each TB x TB row-major.  Updated in place.
 //   Dinv  NT tiles          L_JJ^{-1}
 //   Lo    NT*(PT+1) tiles   the factor: slot t = L_{J+t,J} (slot 0 unused)
 //   LF,LB NT*(PT+1) tiles   solve copies (slot 0 = L_JJ^{-1}) in DMMA fragment
 //                           order, forward and transposed (k_coarse_pack)
-// Padding rows (>= kc) are identity.
+// Padding rows (>= n) are identity.
 //
-// The factorization is one cooperative launch with one grid barrier per tile
-// column: after the barrier every CTA takes trailing-update tasks
-// (recomputing the panel products it needs, so the panel TRSM costs no extra
-// barrier); CTA 0 first takes the task that updates the next diagonal tile
-// and then factors it (one-step lookahead).  All tile products are DMMA.
+// The band factorization is one cooperative launch with one grid barrier per
+// tile column (both parts advance together): every CTA takes trailing-update
+// tasks (recomputing the panel products it needs, so the panel TRSM costs no
+// extra barrier); CTA b first takes the task that updates band b's next
+// diagonal tile and then factors it (one-step lookahead).  All tile products
+// are DMMA.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
 
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
@@ -37,84 +50,184 @@ namespace msfv {
 constexpr int TB = COARSE_TB;
 constexpr int TT = TB * TB;
 
-struct CoarseBufs {
+struct Band {
   double* A;
   double* Dinv;
   double* Lo;
-  double* LF;  // solve copy of (Dinv_J, L_{J+t,J}) in forward fragment order (k_coarse_pack)
-  double* LB;  // the same tiles in backward (transposed) fragment order
+  double* LF;
+  double* LB;
+  int n;        // valid rows
+  int NT, PT;   // tile rows, band tiles
 };
 
-__host__ __device__ __forceinline__ size_t band_tiles(const Geo& g) { return (size_t)g.NT * (g.PT + 1); }
+struct Coarse {
+  int nd;               // 1: z-plane nested dissection, 0: one band
+  int P, zs, planes;    // coarse plane size, separator plane, planes
+  int nb;               // bands in use (1 or 3)
+  Band b[3];            // part 0, part 1, separator (b[0] = whole system when !nd)
+  int J0[2];            // first tile row of each part's last plane
+  double* Z[2];         // rows [J0*TB, NT*TB) of Z_q, row-major, P columns
+  size_t total;         // doubles
+};
 
-__host__ __device__ __forceinline__ CoarseBufs coarse_bufs(const Geo& g, double* base) {
-  CoarseBufs b;
-  b.A = base;
-  b.Dinv = b.A + band_tiles(g) * TT;
-  b.Lo = b.Dinv + (size_t)g.NT * TT;
-  b.LF = b.Lo + band_tiles(g) * TT;
-  b.LB = b.LF + band_tiles(g) * TT;
-  return b;
+__host__ __device__ __forceinline__ Band make_band(double* base, size_t& off, int n, int ptcap) {
+  Band B;
+  B.n = n;
+  B.NT = (n + TB - 1) / TB;
+  B.PT = ptcap < B.NT - 1 ? ptcap : B.NT - 1;
+  const size_t bt = (size_t)B.NT * (B.PT + 1) * TT;
+  B.A = base ? base + off : nullptr;        off += bt;
+  B.Dinv = base ? base + off : nullptr;     off += (size_t)B.NT * TT;
+  B.Lo = base ? base + off : nullptr;       off += bt;
+  B.LF = base ? base + off : nullptr;       off += bt;
+  B.LB = base ? base + off : nullptr;       off += bt;
+  return B;
 }
 
-size_t coarse_doubles(const Geo& g) {
-  return 4 * band_tiles(g) * TT + (size_t)g.NT * TT;
+__host__ __device__ __forceinline__ Coarse coarse_layout(const Geo& g, double* base) {
+  Coarse L{};
+  L.P = (g.nb1 + 1) * (g.nb2 + 1);
+  L.planes = g.nb3 + 1;
+  L.nd = g.coarse_nd != 0 && L.planes >= 3;
+  const int ptcap = (g.pc + TB - 1) / TB;
+  size_t off = 0;
+  if (!L.nd) {
+    L.nb = 1;
+    L.b[0] = make_band(base, off, g.kc, ptcap);
+    L.total = off;
+    return L;
+  }
+  L.nb = 3;
+  L.zs = (L.planes - 1) / 2;
+  const int n0 = L.zs * L.P, n1 = (L.planes - 1 - L.zs) * L.P;
+  L.b[0] = make_band(base, off, n0, ptcap);
+  L.b[1] = make_band(base, off, n1, ptcap);
+  L.b[2] = make_band(base, off, L.P, INT_MAX);
+  for (int q = 0; q < 2; ++q) {
+    L.J0[q] = (L.b[q].n - L.P) / TB;
+    L.Z[q] = base ? base + off : nullptr;
+    off += (size_t)(L.b[q].NT - L.J0[q]) * TB * L.P;
+  }
+  L.total = off;
+  return L;
 }
-size_t coarse_scratch_doubles(const Geo& g, int nrhs) { return (size_t)g.kc * nrhs; }
 
-__device__ __forceinline__ double* tile(double* A, const Geo& g, int J, int t) {
-  return A + ((size_t)J * (g.PT + 1) + t) * TT;
+__device__ __forceinline__ double* btile(double* A, const Band& B, int J, int t) {
+  return A + ((size_t)J * (B.PT + 1) + t) * TT;
 }
-__device__ __forceinline__ const double* tile(const double* A, const Geo& g, int J, int t) {
-  return A + ((size_t)J * (g.PT + 1) + t) * TT;
+__device__ __forceinline__ const double* btile(const double* A, const Band& B, int J, int t) {
+  return A + ((size_t)J * (B.PT + 1) + t) * TT;
 }
 
-// Thread per (coarse row c, lower neighbour o): A_k[c][c'] = sum over blocks
-// having both as corners (fixed order) of Kloc, + shift on the diagonal.
-__global__ void k_coarse_assemble(Geo g, const double* __restrict__ Kloc, double shift, double* __restrict__ Ak) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long tot = (long long)g.NT * TB * 14;
-  if (t >= tot) return;
-  int o = (int)(t % 14);
-  int c = (int)(t / 14);
-  if (c >= g.kc) {
-    if (o == 0) {
-      int J = c / TB, r = c % TB;
-      tile(Ak, g, J, 0)[r * TB + r] = 1.0;    // padding rows: identity
-    }
+// natural coarse index -> (band, local row)
+__device__ __forceinline__ void coarse_map(const Coarse& L, int c, int& part, int& local) {
+  if (!L.nd) {
+    part = 0;
+    local = c;
     return;
   }
-  // enumerate the 14 lexicographically-lower offsets (dz, dy, dx) <= 0
+  const int ck = c / L.P, w = c - ck * L.P;
+  if (ck < L.zs) { part = 0; local = c; }
+  else if (ck > L.zs) { part = 1; local = (L.planes - 1 - ck) * L.P + w; }
+  else { part = 2; local = w; }
+}
+
+size_t coarse_doubles(const Geo& g) { return coarse_layout(g, nullptr).total; }
+size_t coarse_scratch_doubles(const Geo& g, int nrhs) {
+  const Coarse L = coarse_layout(g, nullptr);
+  size_t rows = 0;
+  for (int b = 0; b < L.nb; ++b) rows += (size_t)L.b[b].NT * TB;
+  return rows * nrhs;
+}
+int coarse_tile_rows(const Geo& g) {
+  const Coarse L = coarse_layout(g, nullptr);
+  int r = 0;
+  for (int b = 0; b < L.nb; ++b) r += L.b[b].NT;
+  return r;
+}
+
+// A_k[c][c2] for the o-th lexicographically lower stencil neighbour c2 of c:
+// sum over blocks having both as corners (fixed order) of Kloc, + shift on the
+// diagonal.  Returns false when the neighbour is outside the grid.
+__device__ __forceinline__ bool coarse_entry(const Geo& g, const double* __restrict__ Kloc, double shift, int c, int o,
+                                             int& c2, double& v) {
   int dz, dy, dx;
   if (o < 9) { dz = -1; dy = o / 3 - 1; dx = o % 3 - 1; }
   else if (o < 12) { dz = 0; dy = -1; dx = (o - 9) - 1; }
   else { dz = 0; dy = 0; dx = (o - 12) - 1; }
-  int ci = c % (g.nb1 + 1), r = c / (g.nb1 + 1), cj = r % (g.nb2 + 1), ck = r / (g.nb2 + 1);
-  int di = ci + dx, dj = cj + dy, dk = ck + dz;
-  if (di < 0 || dj < 0 || dk < 0 || di > g.nb1 || dj > g.nb2 || dk > g.nb3) return;
-  int c2 = coarse_of(g, di, dj, dk);
-  double v = 0.0;
+  const int ci = c % (g.nb1 + 1), r = c / (g.nb1 + 1), cj = r % (g.nb2 + 1), ck = r / (g.nb2 + 1);
+  const int di = ci + dx, dj = cj + dy, dk = ck + dz;
+  if (di < 0 || dj < 0 || dk < 0 || di > g.nb1 || dj > g.nb2 || dk > g.nb3) return false;
+  c2 = coarse_of(g, di, dj, dk);
+  v = 0.0;
   for (int bk = max(ck, dk) - 1; bk <= min(ck, dk); ++bk) {
     if (bk < 0 || bk >= g.nb3) continue;
     for (int bj = max(cj, dj) - 1; bj <= min(cj, dj); ++bj) {
       if (bj < 0 || bj >= g.nb2) continue;
       for (int bi = max(ci, di) - 1; bi <= min(ci, di); ++bi) {
         if (bi < 0 || bi >= g.nb1) continue;
-        int l1 = (ci - bi) + 2 * (cj - bj) + 4 * (ck - bk);
-        int l2 = (di - bi) + 2 * (dj - bj) + 4 * (dk - bk);
+        const int l1 = (ci - bi) + 2 * (cj - bj) + 4 * (ck - bk);
+        const int l2 = (di - bi) + 2 * (dj - bj) + 4 * (dk - bk);
         v += Kloc[(size_t)block_of(g, bi, bj, bk) * 64 + l1 * 8 + l2];
       }
     }
   }
   if (c2 == c) v += shift;
-  int I = c / TB, J = c2 / TB;
-  tile(Ak, g, J, I - J)[(c % TB) * TB + (c2 % TB)] = v;
+  return true;
 }
 
-__global__ void k_coarse_diag(Geo g, const double* __restrict__ Ak, double* __restrict__ diag) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+// Thread per (coarse row c, lower neighbour o); scatters into the permuted bands
+// and coupling blocks.  Then padding rows of every band get identity.
+__global__ void k_coarse_assemble(Geo g, Coarse L, const double* __restrict__ Kloc, double shift) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long main = (long long)g.kc * 14;
+  if (t >= main) {
+    const long long u = t - main;              // padding: band u / TB, row n + u % TB
+    const int b = (int)(u / TB), r = (int)(u % TB);
+    if (b < L.nb) {
+      const Band& B = L.b[b];
+      const int row = B.n + r;
+      if (row < B.NT * TB) btile(B.A, B, row / TB, 0)[(row % TB) * (TB + 1)] = 1.0;
+    }
+    return;
+  }
+  const int o = (int)(t % 14), c = (int)(t / 14);
+  int c2;
+  double v;
+  if (!coarse_entry(g, Kloc, shift, c, o, c2, v)) return;
+  int p1, l1, p2, l2;
+  coarse_map(L, c, p1, l1);
+  coarse_map(L, c2, p2, l2);
+  if (p1 == p2) {
+    const Band& B = L.b[p1];
+    const int r = max(l1, l2), s = min(l1, l2);
+    btile(B.A, B, s / TB, r / TB - s / TB)[(r % TB) * TB + (s % TB)] = v;
+  } else {
+    // part q node lr (in its last plane) couples to separator node ls
+    const int q = p1 == 2 ? p2 : p1, lr = p1 == 2 ? l2 : l1, ls = p1 == 2 ? l1 : l2;
+    L.Z[q][(size_t)(lr - L.J0[q] * TB) * L.P + ls] = v;
+  }
+}
+
+__global__ void k_coarse_diag(Geo g, Coarse L, double* __restrict__ diag) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.kc) return;
-  diag[c] = tile(Ak, g, c / TB, 0)[(c % TB) * TB + (c % TB)];
+  int p, l;
+  coarse_map(L, c, p, l);
+  const Band& B = L.b[p];
+  diag[c] = btile(B.A, B, l / TB, 0)[(l % TB) * (TB + 1)];
+}
+
+// Dense natural-order A_k (both triangles), for the host-side `A_k` attribute.
+__global__ void k_coarse_dense(Geo g, const double* __restrict__ Kloc, double shift, double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)g.kc * 14) return;
+  const int o = (int)(t % 14), c = (int)(t / 14);
+  int c2;
+  double v;
+  if (!coarse_entry(g, Kloc, shift, c, o, c2, v)) return;
+  out[(size_t)c * g.kc + c2] = v;
+  out[(size_t)c2 * g.kc + c] = v;
 }
 
 // ------------------------------------------------------------ factorization
@@ -238,7 +351,7 @@ __device__ __forceinline__ void potrf_inv8w(const double* S, int ld, double* Is,
 // Writes Dinv_J (row-major) to the factor buffer.
 // tile_in_smem: sm.T already holds the (updated) diagonal tile.  Dinv_J is
 // also left row-major in sm.D for the caller's next column.
-__device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flags, FactorSmem& sm,
+__device__ void coarse_potrf(const Band& B, int J, int* flags, FactorSmem& sm,
                              bool tile_in_smem = false, long long* tprof = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   auto stamp = [&](int k) {
@@ -246,7 +359,7 @@ __device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flag
   };
   stamp(0);
   double* P = sm.T;
-  if (!tile_in_smem) load_tile(P, tile(B.A, g, J, 0));
+  if (!tile_in_smem) load_tile(P, btile(B.A, B, J, 0));
   __syncthreads();
   for (int kb = 0; kb < 4; ++kb) {
     if (w == 0) {
@@ -324,27 +437,27 @@ __device__ void coarse_potrf(const Geo& g, int J, const CoarseBufs& B, int* flag
 // costs no grid barrier).  sm.D holds Dinv_J.
 // diag_to_smem (lookahead pair (1,1)): the updated diagonal tile goes to
 // sm.T for the POTRF that follows instead of back to global memory.
-__device__ void coarse_task(const Geo& g, int J, int f, const CoarseBufs& B, FactorSmem& sm,
+__device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm,
                             bool diag_to_smem = false) {
   const int lane = threadIdx.x & 31;
   int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
   while (t1 * (t1 - 1) / 2 > f) --t1;
   while ((t1 + 1) * t1 / 2 <= f) ++t1;
   const int t2 = f - t1 * (t1 - 1) / 2 + 1;
-  load_tile(sm.T, tile(B.A, g, J, t1));
+  load_tile(sm.T, btile(B.A, B, J, t1));
   __syncthreads();
   tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X1, LDT, bi, bj, lane, c); });
   __syncthreads();
   if (t2 != t1) {
-    load_tile(sm.T, tile(B.A, g, J, t2));
+    load_tile(sm.T, btile(B.A, B, J, t2));
     __syncthreads();
     tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X2, LDT, bi, bj, lane, c); });
     __syncthreads();
   } else {
-    store_tile(tile(B.Lo, g, J, t1), sm.X1);
+    store_tile(btile(B.Lo, B, J, t1), sm.X1);
   }
   const double* Y = (t2 != t1) ? sm.X2 : sm.X1;
-  double* G = tile(B.A, g, J + t2, t1 - t2);
+  double* G = btile(B.A, B, J + t2, t1 - t2);
   // G -= X1 Y^T, block by block straight from / to global
   const int wv = threadIdx.x >> 5;
 #pragma unroll
@@ -367,188 +480,134 @@ __device__ void coarse_task(const Geo& g, int J, int f, const CoarseBufs& B, Fac
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256, 1) k_coarse_factor(Geo g, double* __restrict__ base, int* __restrict__ flags) {
+// One cooperative launch factors up to two independent bands in lockstep
+// (one grid barrier per tile column).
+struct FactorJob {
+  Band b[2];
+  int nb;
+};
+
+__global__ void __launch_bounds__(256, 1) k_coarse_factor(FactorJob job, int* __restrict__ flags) {
   __shared__ __align__(16) FactorSmem sm;
   cg::grid_group grid = cg::this_grid();
-  const CoarseBufs B = coarse_bufs(g, base);
-  if (blockIdx.x == 0) coarse_potrf(g, 0, B, flags, sm);
+  const int nb = job.nb;
+  const int mine = blockIdx.x < nb ? (int)blockIdx.x : -1;        // lookahead band of this CTA
+  if (mine >= 0) coarse_potrf(mine ? job.b[1] : job.b[0], 0, flags, sm);
   grid.sync();
-  for (int J = 0; J < g.NT; ++J) {
-    const int pt = min(g.PT, g.NT - 1 - J);
-    const int npairs = pt * (pt + 1) / 2;
-    if (blockIdx.x != 0) load_tile(sm.D, B.Dinv + (size_t)J * TT);   // CTA 0 kept it from its POTRF
-    __syncthreads();
-    if (blockIdx.x == 0 && pt >= 1) {
-      coarse_task(g, J, 0, B, sm, true);         // pair (1,1): next diagonal tile, into sm.T
-      coarse_potrf(g, J + 1, B, flags, sm, true);  // lookahead factor of column J+1
+  int ntmax = 0;
+  for (int b = 0; b < nb; ++b) ntmax = max(ntmax, job.b[b].NT);
+  const int nw = (int)gridDim.x - nb > 0 ? (int)gridDim.x - nb : (int)gridDim.x;
+  const int me = (int)gridDim.x - nb > 0 ? (int)blockIdx.x - nb : (int)blockIdx.x;
+  for (int J = 0; J < ntmax; ++J) {
+    if (mine >= 0) {
+      const Band B = mine ? job.b[1] : job.b[0];
+      if (J < B.NT - 1) {
+        coarse_task(B, J, 0, sm, true);           // pair (1,1): next diagonal tile, into sm.T
+        coarse_potrf(B, J + 1, flags, sm, true);  // lookahead factor of column J+1 (keeps Dinv in sm.D)
+      }
     }
-    // the other CTAs share everything except the lookahead pair
-    const int first = (pt >= 1) ? 1 : 0;
-    const int nw = gridDim.x > 1 ? gridDim.x - 1 : 1;
-    if (gridDim.x == 1 || blockIdx.x > 0) {
-      const int me = gridDim.x > 1 ? blockIdx.x - 1 : 0;
-      for (int f = first + me; f < npairs; f += nw) coarse_task(g, J, f, B, sm);
+    if (me >= 0) {
+      // trailing tasks of all bands (minus each band's lookahead pair) in one index space
+      int first[2] = {0, 0}, ntask[2] = {0, 0};
+      for (int b = 0; b < nb; ++b) {
+        const Band& B = job.b[b];
+        const int pt = J < B.NT ? min(B.PT, B.NT - 1 - J) : 0;
+        first[b] = pt >= 1 ? 1 : 0;
+        ntask[b] = pt * (pt + 1) / 2 - first[b];
+      }
+      int loaded = -1;
+      for (int gi = me; gi < ntask[0] + ntask[1]; gi += nw) {
+        const int b = gi < ntask[0] ? 0 : 1;
+        const int f = gi - (b ? ntask[0] : 0);
+        const Band B = b ? job.b[1] : job.b[0];
+        if (loaded != b) {
+          load_tile(sm.D, B.Dinv + (size_t)J * TT);
+          __syncthreads();
+          loaded = b;
+        }
+        coarse_task(B, J, first[b] + f, sm);
+      }
     }
     grid.sync();
   }
 }
 
-// ------------------------------------------------ banded trsv (large k)
-
-// Forward then backward substitution with the banded tiled factor for RC
-// right-hand sides per CTA.  X is [kc][nrhs] row-major.  The factor tiles
-// stream through a RING-slot cp.async pipeline in shared memory in exactly
-// the order they are consumed (forward: Dinv_J, L_{J+1,J}..L_{J+pt,J};
-// backward: L_{J+1,J}..L_{J+pt,J}, Dinv_J); the active right-hand-side rows
-// (PT+1 tile rows) live in a shared-memory ring, so global X is read and
-// written once per sweep.
-namespace {
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// tile sequence iterator: forward (dir=+1) or backward (dir=-1)
-struct TileSeq {
-  int J, t, NT, PT, dir;
-  __device__ int pt() const { return min(PT, NT - 1 - J); }
-  __device__ bool valid() const { return J >= 0 && J < NT; }
-  // forward order: t = 0 (Dinv), 1..pt ; backward order: t = 1..pt, then 0 (Dinv)
-  __device__ void next() {
-    if (dir > 0) {
-      if (t < pt()) ++t; else { ++J; t = 0; }
-    } else {
-      if (t == 0) { --J; t = (J >= 0 && pt() > 0) ? 1 : 0; }
-      else if (t < pt()) ++t;
-      else t = 0;
-    }
-  }
-};
-}  // namespace
-
-template <int RC>
-__global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __restrict__ Lk, const double* __restrict__ Dinv,
-                                                     double* __restrict__ X, int nrhs) {
-  constexpr int RING = 4;
-  extern __shared__ __align__(16) double tsm[];
-  double* ring = tsm;                              // [RING][TB*TB]
-  double* Xw = ring + RING * TT;              // [PT+1][TB][RC]
-  double* Ys = Xw + (size_t)(g.PT + 1) * TB * RC;  // [TB][RC]
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int s0 = blockIdx.x * RC;
-  const int ns = min(RC, nrhs - s0);
-  const int W = g.PT + 1;
-  auto src_of = [&](const TileSeq& q) -> const double* {
-    return q.t == 0 ? Dinv + (size_t)q.J * TT : tile(Lk, g, q.J, q.t);
-  };
-  auto issue = [&](TileSeq& q, int slot) {
-    if (q.valid()) {
-      const double* src = src_of(q);
-      double* dst = ring + slot * TT;
-      for (int i = tid; i < TT / 2; i += nt) cpa16(dst + 2 * i, src + 2 * i);
-    }
-    cpa_commit();
-    q.next();
-  };
-  auto load_rows = [&](int I, double* dst) {
-    for (int t = tid; t < TB * RC; t += nt) {
-      int r = t / RC, s = t % RC, row = I * TB + r;
-      dst[t] = (I < g.NT && s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-    }
-  };
-    {
-    TileSeq pf{0, 0, g.NT, g.PT, 1};
-    int issued = 0, consumed = 0;
-    for (; issued < RING - 1; ++issued) issue(pf, issued % RING);
-    for (int I = 0; I <= g.PT; ++I) load_rows(I, Xw + (size_t)(I % W) * TB * RC);
-    for (int J = 0; J < g.NT; ++J) {
-      const int pt = min(g.PT, g.NT - 1 - J);
-      for (int t = 0; t <= pt; ++t) {
-        cpa_wait<RING - 2>();
-        __syncthreads();
-        issue(pf, issued % RING);
-        ++issued;
-        const double* T = ring + (consumed % RING) * TT;
-        ++consumed;
-        if (t == 0) {
-          const double* xj = Xw + (size_t)(J % W) * TB * RC;
-          for (int q = tid; q < TB * RC; q += nt) {
-            int r = q / RC, s = q % RC;
-            double v = 0.0;
-#pragma unroll 8
-            for (int c = 0; c < TB; ++c) v += T[r * TB + c] * xj[c * RC + s];
-            Ys[q] = v;
-            int row = J * TB + r;
-            if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-          }
-        } else {
-          double* xt = Xw + (size_t)((J + t) % W) * TB * RC;
-          for (int q = tid; q < TB * RC; q += nt) {
-            int r = q / RC, s = q % RC;
-            double v = 0.0;
-#pragma unroll 8
-            for (int c = 0; c < TB; ++c) v += T[r * TB + c] * Ys[c * RC + s];
-            xt[q] -= v;
-          }
-        }
+// S_CC -= sum_q Z_q^T Z_q on the separator band (dense), CTA per lower 32x32 tile.
+// DMMA in the transposed-operand form: D[i][j] += sum_r Z[r][i] Z[r][j].
+__global__ void __launch_bounds__(256) k_schur_update(Coarse L) {
+  const Band& C = L.b[2];
+  int I = 0, K = blockIdx.x;                      // blockIdx -> lower tile (I, K), I >= K
+  while (K > I) { K -= I + 1; ++I; }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = lane >> 2, q = lane & 3;
+  double* G = btile(C.A, C, K, I - K);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = w + 8 * h, bi = o >> 2, bj = o & 3;
+    const int i = I * TB + 8 * bi + m, j = K * TB + 8 * bj + m;       // row of X / row of Y at this lane
+    double c0 = 0.0, c1 = 0.0;
+    for (int p = 0; p < 2; ++p) {
+      const double* Z = L.Z[p];
+      const int rows = (L.b[p].NT - L.J0[p]) * TB;
+      for (int r0 = 0; r0 < rows; r0 += 8) {
+        const int ra = r0 + 2 * q;
+        const double x0 = i < L.P ? Z[(size_t)ra * L.P + i] : 0.0, x1 = i < L.P ? Z[(size_t)(ra + 1) * L.P + i] : 0.0;
+        const double y0 = j < L.P ? Z[(size_t)ra * L.P + j] : 0.0, y1 = j < L.P ? Z[(size_t)(ra + 1) * L.P + j] : 0.0;
+        dmma(c0, c1, x0, y0);
+        dmma(c0, c1, x1, y1);
       }
-      __syncthreads();
-      load_rows(J + 1 + g.PT, Xw + (size_t)(J % W) * TB * RC);   // slot of row J is free now
     }
-    cpa_wait<0>();
-    __syncthreads();
-  }
-    {
-    TileSeq pf{g.NT - 1, 0, g.NT, g.PT, -1};
-    pf.t = (pf.pt() > 0) ? 1 : 0;
-    int issued = 0, consumed = 0;
-    for (; issued < RING - 1; ++issued) issue(pf, issued % RING);
-    for (int J = g.NT - 1; J >= 0; --J) {
-      const int pt = min(g.PT, g.NT - 1 - J);
-      // acc = y_J
-      for (int q = tid; q < TB * RC; q += nt) {
-        int r = q / RC, s = q % RC, row = J * TB + r;
-        Ys[q] = (s < ns && row < g.kc) ? X[(size_t)row * nrhs + s0 + s] : 0.0;
-      }
-      for (int k = 0; k <= pt; ++k) {
-        const int t = (k < pt) ? k + 1 : 0;
-        cpa_wait<RING - 2>();
-        __syncthreads();
-        issue(pf, issued % RING);
-        ++issued;
-        const double* T = ring + (consumed % RING) * TT;
-        ++consumed;
-        if (t > 0) {
-          const double* xt = Xw + (size_t)((J + t) % W) * TB * RC;
-          for (int q = tid; q < TB * RC; q += nt) {
-            int c = q / RC, s = q % RC;
-            double v = 0.0;
-#pragma unroll 8
-            for (int r = 0; r < TB; ++r) v += T[r * TB + c] * xt[r * RC + s];
-            Ys[q] -= v;
-          }
-        } else {
-          double* xj = Xw + (size_t)(J % W) * TB * RC;
-          for (int q = tid; q < TB * RC; q += nt) {
-            int r = q / RC, s = q % RC;
-            double v = 0.0;
-            for (int c = r; c < TB; ++c) v += T[c * TB + r] * Ys[c * RC + s];
-            int row = J * TB + r;
-            if (row >= g.kc || s >= ns) v = 0.0;
-            xj[q] = v;
-            if (s < ns && row < g.kc) X[(size_t)row * nrhs + s0 + s] = v;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    cpa_wait<0>();
+    // C-layout output: lane (m, q) holds D[8bi+m][8bj+2q], [..+1]
+    double* gp = G + (8 * bi + m) * TB + 8 * bj + 2 * q;
+    gp[0] -= c0;
+    gp[1] -= c1;
   }
 }
 
+// x_C[ls][s] -= sum_q sum_r Z_q[r][ls] y_q[J0_q*TB + r][s]
+__global__ void k_schur_rhs(Coarse L, const double* __restrict__ y0, const double* __restrict__ y1,
+                            double* __restrict__ xc, int nrhs) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)L.P * nrhs) return;
+  const int ls = (int)(t / nrhs), s = (int)(t % nrhs);
+  double v = xc[t];
+  for (int p = 0; p < 2; ++p) {
+    const double* Z = L.Z[p];
+    const double* y = (p == 0 ? y0 : y1) + (size_t)L.J0[p] * TB * nrhs;
+    const int rows = min((L.b[p].NT - L.J0[p]) * TB, L.b[p].n - L.J0[p] * TB);
+    for (int r = 0; r < rows; ++r) v -= Z[(size_t)r * L.P + ls] * y[(size_t)r * nrhs + s];
+  }
+  xc[t] = v;
+}
+
+// y_q[J0_q*TB + r][s] -= sum_ls Z_q[r][ls] x_C[ls][s]
+__global__ void k_schur_back(Coarse L, double* __restrict__ y0, double* __restrict__ y1,
+                             const double* __restrict__ xc, int nrhs) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long r0 = (long long)(L.b[0].NT - L.J0[0]) * TB, r1 = (long long)(L.b[1].NT - L.J0[1]) * TB;
+  if (t >= (r0 + r1) * nrhs) return;
+  const int p = t < r0 * nrhs ? 0 : 1;
+  const long long u = p == 0 ? t : t - r0 * nrhs;
+  const int r = (int)(u / nrhs), s = (int)(u % nrhs);
+  if (L.J0[p] * TB + r >= L.b[p].n) return;
+  const double* Z = L.Z[p] + (size_t)r * L.P;
+  double* y = (p == 0 ? y0 : y1) + ((size_t)L.J0[p] * TB + r) * nrhs + s;
+  double v = *y;
+  for (int ls = 0; ls < L.P; ++ls) v -= Z[ls] * xc[(size_t)ls * nrhs + s];
+  *y = v;
+}
+
+// natural X <-> part-local vectors (dir 0: gather, 1: scatter)
+__global__ void k_coarse_permute(Geo g, Coarse L, double* __restrict__ X, double* __restrict__ x0,
+                                 double* __restrict__ x1, double* __restrict__ xc, int nrhs, int dir) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)g.kc * nrhs) return;
+  const int c = (int)(t / nrhs), s = (int)(t % nrhs);
+  int p, l;
+  coarse_map(L, c, p, l);
+  double* d = (p == 0 ? x0 : (p == 1 ? x1 : xc)) + (size_t)l * nrhs + s;
+  if (dir == 0) *d = X[t];
+  else X[t] = *d;
+}
 
 // ----------------------------------------------------------- bulk solves
 //
@@ -561,13 +620,12 @@ __global__ void __launch_bounds__(256) k_coarse_trsv(Geo g, const double* __rest
 //   LF piece (mi, kb) = T  block (mi, kb)          (forward:  y^T = r^T Dinv^T, r^T -= y^T L^T)
 //   LB piece (nb, kb) = T^T block (nb, kb)         (backward: x^T = (y^T - x^T L) Dinv)
 // with slot 0 of tile column J holding Dinv_J.  Tiles below the band end are 0.
-__global__ void k_coarse_pack(Geo g, const double* __restrict__ Lo, const double* __restrict__ Dinv,
-                              double* __restrict__ LF, double* __restrict__ LB) {
-  const int J = blockIdx.x / (g.PT + 1), t = blockIdx.x % (g.PT + 1);
-  const bool valid = t == 0 || J + t < g.NT;
-  const double* src = t == 0 ? Dinv + (size_t)J * TT : tile(Lo, g, J, t);
-  double* f = LF + (size_t)blockIdx.x * TT;
-  double* b = LB + (size_t)blockIdx.x * TT;
+__global__ void k_coarse_pack(Band B) {
+  const int J = blockIdx.x / (B.PT + 1), t = blockIdx.x % (B.PT + 1);
+  const bool valid = t == 0 || J + t < B.NT;
+  const double* src = t == 0 ? B.Dinv + (size_t)J * TT : btile(B.Lo, B, J, t);
+  double* f = B.LF + (size_t)blockIdx.x * TT;
+  double* b = B.LB + (size_t)blockIdx.x * TT;
   for (int e = threadIdx.x; e < TT; e += blockDim.x) {
     const int p = e >> 6, w = e & 63, lane = w >> 1, sl = w & 1, m = lane >> 2, q = lane & 3;
     const int hi = p >> 2, kb = p & 3;
@@ -605,8 +663,24 @@ __device__ __forceinline__ void mma_xyt(double& c0, double& c1, double x0, doubl
 }
 }  // namespace
 
-// Forward then backward substitution for 8 right-hand sides per CTA.  The
-// factor tiles of a step (tile column J of LF / LB) are cut into nch chunks
+
+// One sweep job: a band's solve copies, its right-hand sides (row r of the
+// band at X[r*nrhs]), first tile row J0 and mode (1 forward, 2 backward).
+struct SweepJob {
+  const double* LF;
+  const double* LB;
+  double* X;
+  int NT, PT, n, nrhs, J0, mode;
+};
+struct SweepJobs {
+  SweepJob j[2];
+  int groups;   // CTAs (8 right-hand sides each) per job
+};
+
+// Banded substitution sweeps for 8 right-hand sides per CTA, one launch
+// serving up to two independent jobs (e.g. the two nested-dissection parts);
+// each job sweeps forward from tile row J0 (mode bit 1) and/or backward down
+// to J0 (mode bit 2).  The factor tiles of a step (tile column J of LF / LB) are cut into nch chunks
 // of up to CHT contiguous tiles; the chunk sequence (forward: J ascending,
 // chunks in order; backward: J descending, chunks reversed so the Dinv chunk
 // comes last) streams through a ring of TRSV_STAGES shared-memory stages, one
@@ -614,12 +688,17 @@ __device__ __forceinline__ void mma_xyt(double& c0, double& c1, double x0, doubl
 // right-hand-side rows live in a shared-memory ring of transposed pieces.
 constexpr int TRSV_MAX_STAGES = 3;
 
-__global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* __restrict__ LF,
-                                                          const double* __restrict__ LB, double* __restrict__ X,
-                                                          int nrhs, int CHT, int NS, long long* tprof = nullptr) {
+__global__ void __launch_bounds__(256) k_coarse_trsv_bulk(SweepJobs jobs, int CHT, int NS,
+                                                          long long* tprof = nullptr) {
   extern __shared__ __align__(128) double bsm[];
   __shared__ __align__(8) unsigned long long bar[TRSV_MAX_STAGES];
-  const int W = g.PT + 1;
+  const SweepJob& job = jobs.j[blockIdx.x / jobs.groups];
+  const int group = blockIdx.x % jobs.groups;
+  const double* __restrict__ LF = job.LF;
+  const double* __restrict__ LB = job.LB;
+  double* __restrict__ X = job.X;
+  const int NTj = job.NT, nrow = job.n, nrhs = job.nrhs, J0 = job.J0, mode = job.mode, PTj = job.PT;
+  const int W = PTj + 1;
   const int nch = (W + CHT - 1) / CHT;
   const size_t stage_dbl = (size_t)CHT * TT;
   double* Rt = bsm + NS * stage_dbl;   // [W][4][64] rhs ring (transposed pieces)
@@ -627,21 +706,22 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
   double* Pt = Ys + 256;                         // [8][64]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int c = lane >> 2, q = lane & 3;
-  const int col = blockIdx.x * 8 + c;
+  const int col = group * 8 + c;
   const bool cok = col < nrhs;
   auto ldx = [&](int R, int pi, double& a, double& b) {
     const int r0 = R * TB + 8 * pi + 2 * q;
-    a = (cok && R < g.NT && r0 < g.kc) ? X[(size_t)r0 * nrhs + col] : 0.0;
-    b = (cok && R < g.NT && r0 + 1 < g.kc) ? X[(size_t)(r0 + 1) * nrhs + col] : 0.0;
+    a = (cok && R < NTj && r0 < nrow) ? X[(size_t)r0 * nrhs + col] : 0.0;
+    b = (cok && R < NTj && r0 + 1 < nrow) ? X[(size_t)(r0 + 1) * nrhs + col] : 0.0;
   };
   auto stx = [&](int R, int pi, double a, double b) {
     const int r0 = R * TB + 8 * pi + 2 * q;
-    if (cok && r0 < g.kc) X[(size_t)r0 * nrhs + col] = a;
-    if (cok && r0 + 1 < g.kc) X[(size_t)(r0 + 1) * nrhs + col] = b;
+    if (cok && r0 < nrow) X[(size_t)r0 * nrhs + col] = a;
+    if (cok && r0 + 1 < nrow) X[(size_t)(r0 + 1) * nrhs + col] = b;
   };
   auto piece = [&](const double* base, int p) -> const double* { return base + p * 64 + 2 * lane; };
   auto ring = [&](int jm, int t) { const int r = jm + t; return r >= W ? r - W : r; };   // (J + t) % W, jm = J % W
-  const int nf = g.NT * nch, total = 2 * nf;
+  const int nsteps = (NTj - J0) * nch;
+  const int nf = (mode & 1) ? nsteps : 0, total = nf + ((mode & 2) ? nsteps : 0);
   // chunk sequence iterator (no integer division in the loop)
   struct It {
     int J, ch, jm;
@@ -653,11 +733,11 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
         c.ch = 0;
         ++c.J;
         c.jm = c.jm + 1 == W ? 0 : c.jm + 1;
-        if (c.J == g.NT) {
+        if (c.J == NTj) {
           c.fwd = false;
-          c.J = g.NT - 1;
+          c.J = NTj - 1;
           c.ch = nch - 1;
-          c.jm = (g.NT - 1) % W;
+          c.jm = (NTj - 1) % W;
         }
       }
     } else if (--c.ch < 0) {
@@ -666,7 +746,8 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
       c.jm = c.jm == 0 ? W - 1 : c.jm - 1;
     }
   };
-  It ld = {0, 0, 0, true};          // next chunk to load
+  const It start = (mode & 1) ? It{J0, 0, J0 % W, true} : It{NTj - 1, nch - 1, (NTj - 1) % W, false};
+  It ld = start;                    // next chunk to load
   int ld_i = 0, ld_st = 0;
   auto issue_next = [&]() {
     if (ld_i >= total) return;
@@ -684,25 +765,26 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
   __syncthreads();
   if (tid == 0)
     for (int i = 0; i < NS - 1; ++i) issue_next();
-  for (int i = tid; i < W * 128; i += blockDim.x) {         // rows 0..PT enter the ring
-    const int R = i / 128, pi = (i / 32) & 3;
-    if ((i & 31) == lane) {
-      double a, b;
-      ldx(R, pi, a, b);
-      Rt[(R * 4 + pi) * 64 + 2 * lane] = a;
-      Rt[(R * 4 + pi) * 64 + 2 * lane + 1] = b;
+  if (mode & 1)
+    for (int i = tid; i < W * 128; i += blockDim.x) {       // rows J0..J0+PT enter the ring
+      const int R = J0 + i / 128, pi = (i / 32) & 3;
+      if ((i & 31) == lane) {
+        double a, b;
+        ldx(R, pi, a, b);
+        Rt[((R % W) * 4 + pi) * 64 + 2 * lane] = a;
+        Rt[((R % W) * 4 + pi) * 64 + 2 * lane + 1] = b;
+      }
     }
-  }
   __syncthreads();
   double p0 = 0.0, p1 = 0.0;        // backward partial sums of this warp, across the step's chunks
   double ya = 0.0, yb = 0.0;
-  It cu = {0, 0, 0, true};
+  It cu = start;
   int st = 0;
   unsigned par = 0u;
   for (int i = 0; i < total; ++i, advance(cu), st = st + 1 == NS ? 0 : st + 1) {
     if (tid == 0) issue_next();
     const int J = cu.J, ch = cu.ch, jm = cu.jm;
-    const int pt = min(g.PT, g.NT - 1 - J);
+    const int pt = min(PTj, NTj - 1 - J);
     const int t0 = ch * CHT, t1 = min(W, t0 + CHT) - 1;
     const double* T = bsm + (size_t)st * stage_dbl;           // local tile (t - t0)
     if (i == nf) {                                           // backward: the ring keeps x^T
@@ -714,7 +796,7 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
       if (wid < 4) ldx(J, wid, ya, yb);
     }
     double ra = 0.0, rb = 0.0;
-    if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + g.PT, wid, ra, rb);   // in flight during the step
+    if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + PTj, wid, ra, rb);   // in flight during the step
     long long tclk = 0, tw = 0;
     if (tprof && tid == 0) tclk = clock64();
     mbar_wait(&bar[st], (par >> st) & 1u);
@@ -854,8 +936,8 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
           c0 += e0;
           c1 += e1;
           const int r0 = J * TB + 8 * nb + 2 * q;
-          if (r0 >= g.kc) c0 = 0.0;
-          if (r0 + 1 >= g.kc) c1 = 0.0;
+          if (r0 >= nrow) c0 = 0.0;
+          if (r0 + 1 >= nrow) c1 = 0.0;
           double* xo = Rt + (size_t)(jm * 4 + nb) * 64 + 2 * lane;   // ring keeps -x^T
           xo[0] = cok ? -c0 : 0.0;
           xo[1] = cok ? -c1 : 0.0;
@@ -870,8 +952,8 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(Geo g, const double* _
 
 // One whole tile column per stage (2 stages) when it fits, else chunks
 // through 3 stages.
-static void trsv_bulk_shape(const Geo& g, int& cht, int& ns, size_t& smem) {
-  const int W = g.PT + 1;
+static void trsv_bulk_shape(int PT, int& cht, int& ns, size_t& smem) {
+  const int W = PT + 1;
   const size_t fixed = ((size_t)W * 256 + 256 + 8 * 64) * sizeof(double);
   const size_t budget = 220 * 1024, tile_b = (size_t)TT * sizeof(double);
   cht = 0;
@@ -895,21 +977,37 @@ static void trsv_bulk_shape(const Geo& g, int& cht, int& ns, size_t& smem) {
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(Ak, 0, band_tiles(g) * TT * sizeof(double), st);
-  if (e != cudaSuccess) return e;
-  long long tot = (long long)g.NT * TB * 14;
-  k_coarse_assemble<<<nblk(tot, 256), 256, 0, st>>>(g, Kloc, shift, Ak);
+  const Coarse L = coarse_layout(g, Ak);
+  for (int b = 0; b < L.nb; ++b) {
+    cudaError_t e = cudaMemsetAsync(L.b[b].A, 0, (size_t)L.b[b].NT * (L.b[b].PT + 1) * TT * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+  }
+  if (L.nd)
+    for (int q = 0; q < 2; ++q) {
+      cudaError_t e = cudaMemsetAsync(L.Z[q], 0, (size_t)(L.b[q].NT - L.J0[q]) * TB * L.P * sizeof(double), st);
+      if (e != cudaSuccess) return e;
+    }
+  const long long tot = (long long)g.kc * 14 + (long long)L.nb * TB;
+  k_coarse_assemble<<<nblk(tot, 256), 256, 0, st>>>(g, L, Kloc, shift);
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st) {
-  k_coarse_diag<<<nblk(g.kc, 256), 256, 0, st>>>(g, Ak, diag);
+  k_coarse_diag<<<nblk(g.kc, 256), 256, 0, st>>>(g, coarse_layout(g, const_cast<double*>(Ak)), diag);
   count_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
+cudaError_t launch_coarse_dense(const Geo& g, const double* Kloc, double shift, double* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, (size_t)g.kc * g.kc * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  k_coarse_dense<<<nblk((long long)g.kc * 14, 256), 256, 0, st>>>(g, Kloc, shift, out);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_factor_job(const FactorJob& job, int* flags, cudaStream_t st) {
   static int coop_grid = -1;
   if (coop_grid < 0) {
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
@@ -920,35 +1018,109 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
     coop_grid = (coop && per_sm > 0) ? sms : 0;
   }
   if (coop_grid <= 0) return cudaErrorNotSupported;
-  CoarseBufs B = coarse_bufs(g, Ak);
-  Geo gg = g;
-  void* args[] = {(void*)&gg, (void*)&Ak, (void*)&flags};
+  FactorJob j = job;
+  void* args[] = {(void*)&j, (void*)&flags};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_coarse_factor, dim3(coop_grid), dim3(256), args, 0, st);
   count_launches(1);
   if (e != cudaSuccess) return e;
-  k_coarse_pack<<<(unsigned)band_tiles(g), 256, 0, st>>>(g, B.Lo, B.Dinv, B.LF, B.LB);
+  for (int b = 0; b < job.nb; ++b) {
+    k_coarse_pack<<<(unsigned)(job.b[b].NT * (job.b[b].PT + 1)), 256, 0, st>>>(job.b[b]);
+    count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_sweeps(const SweepJobs& jobs, int njobs, int nrhs, cudaStream_t st) {
+  if (nrhs == 0) return cudaSuccess;
+  int ptmax = 0;
+  for (int k = 0; k < njobs; ++k) ptmax = std::max(ptmax, jobs.j[k].PT);
+  int cht = 0, ns = 0;
+  size_t smem = 0;
+  trsv_bulk_shape(ptmax, cht, ns, smem);
+  if (cht <= 0) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  SweepJobs J = jobs;
+  J.groups = (nrhs + 7) / 8;
+  k_coarse_trsv_bulk<<<(unsigned)(njobs * J.groups), 256, smem, st>>>(J, cht, ns, nullptr);
   count_launches(1);
   return cudaGetLastError();
 }
 
+static SweepJob sweep_job(const Band& B, double* X, int nrhs, int J0, int mode) {
+  SweepJob s;
+  s.LF = B.LF;
+  s.LB = B.LB;
+  s.X = X;
+  s.NT = B.NT;
+  s.PT = B.PT;
+  s.n = B.n;
+  s.nrhs = nrhs;
+  s.J0 = J0;
+  s.mode = mode;
+  return s;
+}
+
+cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
+  const Coarse L = coarse_layout(g, Ak);
+  FactorJob job{};
+  job.b[0] = L.b[0];
+  if (!L.nd) {
+    job.nb = 1;
+    return launch_factor_job(job, flags, st);
+  }
+  job.b[1] = L.b[1];
+  job.nb = 2;
+  cudaError_t e = launch_factor_job(job, flags, st);                // both parts
+  if (e != cudaSuccess) return e;
+  SweepJobs zj{};
+  for (int q = 0; q < 2; ++q)                                       // Z_q = L_q^{-1} A_{q,C}
+    zj.j[q] = sweep_job(L.b[q], L.Z[q] - (size_t)L.J0[q] * TB * L.P, L.P, L.J0[q], 1);
+  e = launch_sweeps(zj, 2, L.P, st);
+  if (e != cudaSuccess) return e;
+  const int ntc = L.b[2].NT;
+  k_schur_update<<<(unsigned)(ntc * (ntc + 1) / 2), 256, 0, st>>>(L);  // S = A_CC - sum Z^T Z
+  count_launches(1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  FactorJob jc{};
+  jc.b[0] = L.b[2];
+  jc.nb = 1;
+  return launch_factor_job(jc, flags, st);
+}
+
 cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
-  CoarseBufs B = coarse_bufs(g, const_cast<double*>(Ak));
-  constexpr int RC = 4;
-  int cht = 0, ns = 0;
-  size_t smem_b = 0;
-  trsv_bulk_shape(g, cht, ns, smem_b);
-  if (cht > 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    if (e != cudaSuccess) return e;
-    k_coarse_trsv_bulk<<<nblk(nrhs, 8), 256, smem_b, st>>>(g, B.LF, B.LB, X, nrhs, cht, ns);
-    count_launches(1);
-    return cudaGetLastError();
+  const Coarse L = coarse_layout(g, const_cast<double*>(Ak));
+  SweepJobs sj{};
+  if (!L.nd) {
+    sj.j[0] = sweep_job(L.b[0], X, nrhs, 0, 3);
+    return launch_sweeps(sj, 1, nrhs, st);
   }
-  size_t smem = ((size_t)4 * TT + ((size_t)g.PT + 2) * TB * RC) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_coarse_trsv<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  double* x0 = scratch;
+  double* x1 = x0 + (size_t)L.b[0].NT * TB * nrhs;
+  double* xc = x1 + (size_t)L.b[1].NT * TB * nrhs;
+  const long long tot = (long long)g.kc * nrhs;
+  k_coarse_permute<<<nblk(tot, 256), 256, 0, st>>>(g, L, X, x0, x1, xc, nrhs, 0);
+  count_launches(1);
+  sj.j[0] = sweep_job(L.b[0], x0, nrhs, 0, 1);
+  sj.j[1] = sweep_job(L.b[1], x1, nrhs, 0, 1);
+  cudaError_t e = launch_sweeps(sj, 2, nrhs, st);                   // y_q = L_q^{-1} b_q
   if (e != cudaSuccess) return e;
-  k_coarse_trsv<RC><<<nblk(nrhs, RC), 256, smem, st>>>(g, B.Lo, B.Dinv, X, nrhs);
+  k_schur_rhs<<<nblk((long long)L.P * nrhs, 128), 128, 0, st>>>(L, x0, x1, xc, nrhs);
+  count_launches(1);
+  SweepJobs cj{};
+  cj.j[0] = sweep_job(L.b[2], xc, nrhs, 0, 3);                      // x_C = S^{-1}(b_C - sum Z^T y)
+  e = launch_sweeps(cj, 1, nrhs, st);
+  if (e != cudaSuccess) return e;
+  const long long rz = (long long)((L.b[0].NT - L.J0[0]) + (L.b[1].NT - L.J0[1])) * TB * nrhs;
+  k_schur_back<<<nblk(rz, 128), 128, 0, st>>>(L, x0, x1, xc, nrhs);   // y_q -= Z_q x_C
+  count_launches(1);
+  sj.j[0].mode = 2;
+  sj.j[1].mode = 2;
+  e = launch_sweeps(sj, 2, nrhs, st);                               // x_q = L_q^{-T} y_q
+  if (e != cudaSuccess) return e;
+  k_coarse_permute<<<nblk(tot, 256), 256, 0, st>>>(g, L, X, x0, x1, xc, nrhs, 1);
   count_launches(1);
   return cudaGetLastError();
 }

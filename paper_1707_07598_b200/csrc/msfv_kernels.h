@@ -61,6 +61,8 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Lk, double* X, doubl
 size_t coarse_doubles(const Geo& g);
 size_t coarse_scratch_doubles(const Geo& g, int nrhs);
 cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st);
+cudaError_t launch_coarse_dense(const Geo& g, const double* Kloc, double shift, double* out, cudaStream_t st);
+int coarse_tile_rows(const Geo& g);
 
 // survey point sets (msfv_points.cu)
 struct PointsDev {

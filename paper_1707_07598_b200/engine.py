@@ -186,6 +186,12 @@ class Engine:
             _lib.check(self.L.msfv_galerkin(self.plan, ptr(Kloc), float(shift), ptr(Ak), stream()), "galerkin")
         return Ak
 
+    def coarse_dense(self, Kloc, shift=0.0):
+        """Dense natural-order A_k (+ shift I) for the host-side A_k attribute."""
+        out = self.empty(self.k, self.k)
+        _lib.check(self.L.msfv_coarse_dense(self.plan, ptr(Kloc), float(shift), ptr(out), stream()), "coarse_dense")
+        return out
+
     def coarse_trace(self, Ak):
         d = self.empty(self.k)
         _lib.check(self.L.msfv_coarse_diag(self.plan, ptr(Ak), ptr(d), stream()), "coarse_diag")
@@ -199,7 +205,7 @@ class Engine:
         """In place: X (k, nrhs) contiguous device tensor."""
         assert X.is_contiguous() and X.shape[0] == self.k
         with phase("coarse_solve"):
-            scratch = self.empty(max(self.k * X.shape[1], 1))
+            scratch = self.empty(max(self.NT * self.TB * X.shape[1], 1))
             _lib.check(self.L.msfv_coarse_solve(self.plan, ptr(Lk), ptr(X), ptr(scratch), X.shape[1], stream()),
                        "coarse_solve")
         return X

@@ -117,16 +117,7 @@ class ReducedState:
         """Dense projected operator (forward.py:102), re-assembled on demand."""
         if self._A_k is None:
             eng = self.basis.engine
-            Ak = eng.galerkin(self.basis.Kloc, self.shift)
-            tiles = _host(Ak)[: eng.NT * (eng.PT + 1) * eng.TB * eng.TB]
-            tiles = tiles.reshape(eng.NT, eng.PT + 1, eng.TB, eng.TB)
-            K = np.zeros((eng.NT * eng.TB, eng.NT * eng.TB))
-            for J in range(eng.NT):
-                for t in range(min(eng.PT, eng.NT - 1 - J) + 1):
-                    I = J + t
-                    K[I * eng.TB:(I + 1) * eng.TB, J * eng.TB:(J + 1) * eng.TB] = tiles[J, t]
-            K = np.tril(K[: eng.k, : eng.k])
-            self._A_k = K + np.tril(K, -1).T
+            self._A_k = _host(eng.coarse_dense(self.basis.Kloc, self.shift))
         return self._A_k
 
     def check(self):

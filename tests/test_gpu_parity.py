@@ -117,3 +117,28 @@ def test_table3_operators_match_oracle(rng):
         assert np.array_equal(got.indptr, ref.indptr)
         assert np.array_equal(got.indices, ref.indices)
         assert rel(got.data, ref.data) <= TOL
+
+
+@pytest.mark.parametrize("name", ["c16_b8", "c32_b8"])
+def test_coarse_nested_dissection_matches_reference(name, monkeypatch):
+    """The z-plane nested-dissection coarse solver (default for k >= 1000)
+    forced on small golden cases: same T, D, misfit, gradient, J v, J^T w."""
+    import paper_1707_07598_b200.engine as E
+    monkeypatch.setenv("MSFV_COARSE_ND", "1")
+    saved = dict(E._ENGINES)
+    E._ENGINES.clear()
+    try:
+        g = load_golden(name)
+        gp, mesh, part, survey, builder = build_gpu(g)
+        op = gp.assemble_operator(mesh, g["m"])
+        basis = builder.assemble(op)
+        D, state = gp.forward_reduced(op, survey, basis)
+        J = gp.sensitivity_adaptive(state, survey)
+        errs = {"T": rel(state.T, g["T"]), "D": rel(D, g["D"]), "g": rel(J.rapply(g["resid"]), g["g"]),
+                "Jv": rel(J.apply(g["dm"]), g["Jv"]), "JtW": rel(J.rapply(g["W"]), g["JtW"]),
+                "A_k": rel(state.A_k, g["A_k"])}
+        bad = {k: v for k, v in errs.items() if not v <= TOL}
+        assert not bad, f"{name}: {errs}"
+    finally:
+        E._ENGINES.clear()
+        E._ENGINES.update(saved)
