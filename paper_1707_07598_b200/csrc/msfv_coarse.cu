@@ -532,68 +532,125 @@ __global__ void __launch_bounds__(256, 1) k_coarse_factor(FactorJob job, int* __
   }
 }
 
-// S_CC -= sum_q Z_q^T Z_q on the separator band (dense), CTA per lower 32x32 tile.
-// DMMA in the transposed-operand form: D[i][j] += sum_r Z[r][i] Z[r][j].
+// S_CC -= sum_q Z_q^T Z_q on the separator band (dense), CTA per lower 32x32
+// tile.  DMMA in the transposed-operand form, D[i][j] += sum_r Z[r][i] Z[r][j]:
+// warp w takes the 8-row chunks w, w+8, ... of both parts for all 16 output
+// blocks of the tile (4 X and 4 Y fragments per chunk feed 16 MMA pairs);
+// the 8 warp partials are summed in a fixed order through shared memory.
 __global__ void __launch_bounds__(256) k_schur_update(Coarse L) {
+  extern __shared__ __align__(16) double red[];   // [8 warps][16 blocks][64]
   const Band& C = L.b[2];
   int I = 0, K = blockIdx.x;                      // blockIdx -> lower tile (I, K), I >= K
   while (K > I) { K -= I + 1; ++I; }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = lane >> 2, q = lane & 3;
-  double* G = btile(C.A, C, K, I - K);
+  double acc[16][2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int o = w + 8 * h, bi = o >> 2, bj = o & 3;
-    const int i = I * TB + 8 * bi + m, j = K * TB + 8 * bj + m;       // row of X / row of Y at this lane
-    double c0 = 0.0, c1 = 0.0;
-    for (int p = 0; p < 2; ++p) {
-      const double* Z = L.Z[p];
-      const int rows = (L.b[p].NT - L.J0[p]) * TB;
-      for (int r0 = 0; r0 < rows; r0 += 8) {
-        const int ra = r0 + 2 * q;
-        const double x0 = i < L.P ? Z[(size_t)ra * L.P + i] : 0.0, x1 = i < L.P ? Z[(size_t)(ra + 1) * L.P + i] : 0.0;
-        const double y0 = j < L.P ? Z[(size_t)ra * L.P + j] : 0.0, y1 = j < L.P ? Z[(size_t)(ra + 1) * L.P + j] : 0.0;
-        dmma(c0, c1, x0, y0);
-        dmma(c0, c1, x1, y1);
-      }
+  for (int o = 0; o < 16; ++o) acc[o][0] = acc[o][1] = 0.0;
+  const int nc0 = (L.b[0].NT - L.J0[0]) * TB / 8, nc1 = (L.b[1].NT - L.J0[1]) * TB / 8;
+  for (int ch = w; ch < nc0 + nc1; ch += 8) {
+    const int p = ch < nc0 ? 0 : 1;
+    const double* Z = L.Z[p] + (size_t)(8 * (ch - (p ? nc0 : 0)) + 2 * q) * L.P;
+    double x[4][2], y[4][2];
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const int i = I * TB + 8 * bb + m, j = K * TB + 8 * bb + m;
+      x[bb][0] = i < L.P ? Z[i] : 0.0;
+      x[bb][1] = i < L.P ? Z[L.P + i] : 0.0;
+      y[bb][0] = j < L.P ? Z[j] : 0.0;
+      y[bb][1] = j < L.P ? Z[L.P + j] : 0.0;
     }
-    // C-layout output: lane (m, q) holds D[8bi+m][8bj+2q], [..+1]
-    double* gp = G + (8 * bi + m) * TB + 8 * bj + 2 * q;
-    gp[0] -= c0;
-    gp[1] -= c1;
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      dmma(acc[o][0], acc[o][1], x[o >> 2][0], y[o & 3][0]);
+      dmma(acc[o][0], acc[o][1], x[o >> 2][1], y[o & 3][1]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < 16; ++o) {
+    red[(w * 16 + o) * 64 + 2 * lane] = acc[o][0];
+    red[(w * 16 + o) * 64 + 2 * lane + 1] = acc[o][1];
+  }
+  __syncthreads();
+  double* G = btile(C.A, C, K, I - K);
+  for (int e = threadIdx.x; e < 16 * 64; e += blockDim.x) {
+    const int o = e >> 6, idx = e & 63, ln = idx >> 1, sl = idx & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += red[(ww * 16 + o) * 64 + idx];
+    const int bi = o >> 2, bj = o & 3, mm = ln >> 2, qq = ln & 3;
+    G[(8 * bi + mm) * TB + 8 * bj + 2 * qq + sl] -= v;
   }
 }
 
-// x_C[ls][s] -= sum_q sum_r Z_q[r][ls] y_q[J0_q*TB + r][s]
-__global__ void k_schur_rhs(Coarse L, const double* __restrict__ y0, const double* __restrict__ y1,
-                            double* __restrict__ xc, int nrhs) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)L.P * nrhs) return;
-  const int ls = (int)(t / nrhs), s = (int)(t % nrhs);
-  double v = xc[t];
-  for (int p = 0; p < 2; ++p) {
-    const double* Z = L.Z[p];
-    const double* y = (p == 0 ? y0 : y1) + (size_t)L.J0[p] * TB * nrhs;
-    const int rows = min((L.b[p].NT - L.J0[p]) * TB, L.b[p].n - L.J0[p] * TB);
-    for (int r = 0; r < rows; ++r) v -= Z[(size_t)r * L.P + ls] * y[(size_t)r * nrhs + s];
+// x_C[ls][s] -= sum_q sum_r Z_q[r][ls] y_q[J0_q*TB + r][s]: CTA per 8 separator
+// rows x 8 sources, 8 warps over the 8-row chunks of both parts (DMMA,
+// D[ls][s] += sum_r Z[r][ls] y[r][s]), fixed-order warp reduction.
+__global__ void __launch_bounds__(256) k_schur_rhs(Coarse L, const double* __restrict__ y0,
+                                                   const double* __restrict__ y1, double* __restrict__ xc, int nrhs) {
+  __shared__ double red[8][64];
+  const int ls0 = blockIdx.x * 8, s0 = blockIdx.y * 8;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = lane >> 2, q = lane & 3;
+  const int nc0 = (L.b[0].NT - L.J0[0]) * TB / 8, nc1 = (L.b[1].NT - L.J0[1]) * TB / 8;
+  const int ls = ls0 + m, s = s0 + m;
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  int u = 0;
+  for (int ch = w; ch < nc0 + nc1; ch += 8, u ^= 1) {
+    const int p = ch < nc0 ? 0 : 1;
+    const int r = 8 * (ch - (p ? nc0 : 0)) + 2 * q;
+    const double* Z = L.Z[p] + (size_t)r * L.P;
+    const double* y = (p == 0 ? y0 : y1) + ((size_t)L.J0[p] * TB + r) * nrhs;
+    const double x0 = ls < L.P ? Z[ls] : 0.0, x1 = ls < L.P ? Z[L.P + ls] : 0.0;
+    const double v0 = s < nrhs ? y[s] : 0.0, v1 = s < nrhs ? y[nrhs + s] : 0.0;
+    dmma(c[u][0], c[u][1], x0, v0);
+    dmma(c[u][0], c[u][1], x1, v1);
   }
-  xc[t] = v;
+  red[w][2 * lane] = c[0][0] + c[1][0];
+  red[w][2 * lane + 1] = c[0][1] + c[1][1];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int idx = threadIdx.x, ln = idx >> 1, sl = idx & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += red[ww][idx];
+    const int r = ls0 + (ln >> 2), cidx = s0 + 2 * (ln & 3) + sl;
+    if (r < L.P && cidx < nrhs) xc[(size_t)r * nrhs + cidx] -= v;
+  }
 }
 
-// y_q[J0_q*TB + r][s] -= sum_ls Z_q[r][ls] x_C[ls][s]
-__global__ void k_schur_back(Coarse L, double* __restrict__ y0, double* __restrict__ y1,
-                             const double* __restrict__ xc, int nrhs) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long r0 = (long long)(L.b[0].NT - L.J0[0]) * TB, r1 = (long long)(L.b[1].NT - L.J0[1]) * TB;
-  if (t >= (r0 + r1) * nrhs) return;
-  const int p = t < r0 * nrhs ? 0 : 1;
-  const long long u = p == 0 ? t : t - r0 * nrhs;
-  const int r = (int)(u / nrhs), s = (int)(u % nrhs);
-  if (L.J0[p] * TB + r >= L.b[p].n) return;
-  const double* Z = L.Z[p] + (size_t)r * L.P;
-  double* y = (p == 0 ? y0 : y1) + ((size_t)L.J0[p] * TB + r) * nrhs + s;
-  double v = *y;
-  for (int ls = 0; ls < L.P; ++ls) v -= Z[ls] * xc[(size_t)ls * nrhs + s];
-  *y = v;
+// y_q[J0_q*TB + r][s] -= sum_ls Z_q[r][ls] x_C[ls][s]: CTA per 8 part rows x
+// 8 sources, 8 warps over the 8-column chunks of Z (DMMA,
+// D[r][s] += sum_ls Z[r][ls] x_C[ls][s]), fixed-order warp reduction.
+__global__ void __launch_bounds__(256) k_schur_back(Coarse L, double* __restrict__ y0, double* __restrict__ y1,
+                                                    const double* __restrict__ xc, int nrhs) {
+  __shared__ double red[8][64];
+  const int rb = blockIdx.x * 8, s0 = blockIdx.y * 8;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = lane >> 2, q = lane & 3;
+  const int r0 = (L.b[0].NT - L.J0[0]) * TB;
+  const int p = rb < r0 ? 0 : 1;
+  const int rloc = (p == 0 ? rb : rb - r0) + m;                // Z row of this lane
+  const double* Z = L.Z[p] + (size_t)rloc * L.P;
+  const int s = s0 + m;
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  int u = 0;
+  for (int ls = 8 * w + 2 * q; ls < L.P + 6; ls += 64, u ^= 1) {
+    const double x0 = ls < L.P ? Z[ls] : 0.0, x1 = ls + 1 < L.P ? Z[ls + 1] : 0.0;
+    const double v0 = (ls < L.P && s < nrhs) ? xc[(size_t)ls * nrhs + s] : 0.0;
+    const double v1 = (ls + 1 < L.P && s < nrhs) ? xc[(size_t)(ls + 1) * nrhs + s] : 0.0;
+    dmma(c[u][0], c[u][1], x0, v0);
+    dmma(c[u][0], c[u][1], x1, v1);
+  }
+  red[w][2 * lane] = c[0][0] + c[1][0];
+  red[w][2 * lane + 1] = c[0][1] + c[1][1];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int idx = threadIdx.x, ln = idx >> 1, sl = idx & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += red[ww][idx];
+    const int r = (p == 0 ? rb : rb - r0) + (ln >> 2), cidx = s0 + 2 * (ln & 3) + sl;
+    if (L.J0[p] * TB + r < L.b[p].n && cidx < nrhs)
+      ((p == 0 ? y0 : y1) + ((size_t)L.J0[p] * TB + r) * nrhs)[cidx] -= v;
+  }
 }
 
 // natural X <-> part-local vectors (dir 0: gather, 1: scatter)
@@ -1079,7 +1136,10 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   e = launch_sweeps(zj, 2, L.P, st);
   if (e != cudaSuccess) return e;
   const int ntc = L.b[2].NT;
-  k_schur_update<<<(unsigned)(ntc * (ntc + 1) / 2), 256, 0, st>>>(L);  // S = A_CC - sum Z^T Z
+  const int red_bytes = 8 * 16 * 64 * (int)sizeof(double);
+  e = cudaFuncSetAttribute(k_schur_update, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
+  if (e != cudaSuccess) return e;
+  k_schur_update<<<(unsigned)(ntc * (ntc + 1) / 2), 256, red_bytes, st>>>(L);  // S = A_CC - sum Z^T Z
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1107,14 +1167,14 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
   sj.j[1] = sweep_job(L.b[1], x1, nrhs, 0, 1);
   cudaError_t e = launch_sweeps(sj, 2, nrhs, st);                   // y_q = L_q^{-1} b_q
   if (e != cudaSuccess) return e;
-  k_schur_rhs<<<nblk((long long)L.P * nrhs, 128), 128, 0, st>>>(L, x0, x1, xc, nrhs);
+  k_schur_rhs<<<dim3(nblk(L.P, 8), nblk(nrhs, 8)), 256, 0, st>>>(L, x0, x1, xc, nrhs);
   count_launches(1);
   SweepJobs cj{};
   cj.j[0] = sweep_job(L.b[2], xc, nrhs, 0, 3);                      // x_C = S^{-1}(b_C - sum Z^T y)
   e = launch_sweeps(cj, 1, nrhs, st);
   if (e != cudaSuccess) return e;
-  const long long rz = (long long)((L.b[0].NT - L.J0[0]) + (L.b[1].NT - L.J0[1])) * TB * nrhs;
-  k_schur_back<<<nblk(rz, 128), 128, 0, st>>>(L, x0, x1, xc, nrhs);   // y_q -= Z_q x_C
+  const long long rz = (long long)((L.b[0].NT - L.J0[0]) + (L.b[1].NT - L.J0[1])) * TB;
+  k_schur_back<<<dim3(nblk(rz, 8), nblk(nrhs, 8)), 256, 0, st>>>(L, x0, x1, xc, nrhs);  // y_q -= Z_q x_C
   count_launches(1);
   sj.j[0].mode = 2;
   sj.j[1].mode = 2;
