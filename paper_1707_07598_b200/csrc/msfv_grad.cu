@@ -26,11 +26,21 @@ namespace msfv {
 __device__ __forceinline__ void stage_closure(const Geo& g, int jb, const double* __restrict__ Sint, double* Sn) {
   const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
   const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  for (int i = threadIdx.x; i < 8 * g.nI; i += blockDim.x) {
-    const int cc = i / g.nI, a = i - cc * g.nI;
-    int x, y, z;
-    decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
-    Sn[((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8 + cc] = __ldg(Sb + i);
+  // four loads in flight per thread before the scattered shared-memory stores
+  const int tot = 8 * g.nI, step = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < tot; i0 += 4 * step) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = i0 + u * step < tot ? __ldg(Sb + i0 + u * step) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * step;
+      if (i >= tot) break;
+      const int cc = i / g.nI, a = i - cc * g.nI;
+      int x, y, z;
+      decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+      Sn[((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8 + cc] = v[u];
+    }
   }
   for (int n = threadIdx.x; n < NN; n += blockDim.x) {
     const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
@@ -80,9 +90,9 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   __syncthreads();
   const int zs = zslot ? zslot[jb] : -1, rs = rslot ? rslot[jb] : -1;
   const int NE = NEx + NEy + NEz;
-  for (int e = tid; e < NE; e += blockDim.x) {
-    int x, y, z, step;
-    double ihs;
+  // edge e -> lower closure node, step to the upper node, 1/h^2
+  auto edge = [&](int e, int& na, int& step, double& ihs) {
+    int x, y, z;
     if (e < NEx) {
       x = e % g.b1; const int r = e / g.b1; y = r % B2; z = r / B2; step = 1; ihs = g.ih1 * g.ih1;
     } else if (e < NEx + NEy) {
@@ -92,20 +102,55 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
       const int f = e - NEx - NEy;
       x = f % B1; const int r = f / B1; y = r % B2; z = r / B2; step = B1 * B2; ihs = g.ih3 * g.ih3;
     }
-    const int na = x + B1 * (y + B2 * z), nb = na + step;
-    double d[8];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) d[cc] = Sn[nb * 8 + cc] - Sn[na * 8 + cc];
-    double v = 0.0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      double t = 0.0;
-#pragma unroll
-      for (int c2 = 0; c2 < 8; ++c2) t += M[c * 8 + c2] * d[c2];
-      v += d[c] * t;
+    na = x + B1 * (y + B2 * z);
+  };
+  if (zs < 0 && rs < 0) {
+    // xi_e = dS_e^T M dS_e for 8 edges per warp step: D (8 edges x 8 corners,
+    // accumulator layout) times M on the DMMA (D += X Y^T with Y = M^T), then
+    // the row-wise product with D and a 4-lane reduction.
+    const int lane = tid & 31, wv = tid >> 5, m = lane >> 2, q = lane & 3;
+    const double mt0 = M[(2 * q) * 8 + m], mt1 = M[(2 * q + 1) * 8 + m];   // C layout of M^T
+    for (int e0 = 8 * wv; e0 < NE; e0 += 8 * (blockDim.x >> 5)) {
+      const int e = e0 + m;
+      double d0 = 0.0, d1 = 0.0, ihs = 0.0;
+      if (e < NE) {
+        int na, step;
+        edge(e, na, step, ihs);
+        const int nb = na + step;
+        const double2 sb = *reinterpret_cast<const double2*>(Sn + nb * 8 + 2 * q);
+        const double2 sa = *reinterpret_cast<const double2*>(Sn + na * 8 + 2 * q);
+        d0 = sb.x - sa.x;
+        d1 = sb.y - sa.y;
+      }
+      double c0 = 0.0, c1 = 0.0;
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c0), "+d"(c1) : "d"(d0), "d"(mt0));
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c0), "+d"(c1) : "d"(d1), "d"(mt1));
+      double v = c0 * d0 + c1 * d1;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (q == 0 && e < NE) xi[e] = v * ihs;
     }
-    if (zs >= 0 || rs >= 0) {
-      // interior-source / receiver blocks: dU dZ + dR dY per source
+  } else {
+    // interior-source / receiver blocks: scalar path with dU dZ + dR dY per source
+    for (int e = tid; e < NE; e += blockDim.x) {
+      int na, step;
+      double ihs;
+      edge(e, na, step, ihs);
+      const int nb = na + step;
+      double d[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) d[cc] = Sn[nb * 8 + cc] - Sn[na * 8 + cc];
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double t = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < 8; ++c2) t += M[c * 8 + c2] * d[c2];
+        v += d[c] * t;
+      }
+      const int x = na % B1, r = na / B1, y = r % B2, z = r / B2;
       const int xb = x + (step == 1), yb = y + (step == B1), zb = z + (step == B1 * B2);
       const int ia = interior_index(g, x, y, z), ib = interior_index(g, xb, yb, zb);
       for (int s = 0; s < nrhs; ++s) {
@@ -126,8 +171,8 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
         }
         v += du * dz + dr * dy;
       }
+      xi[e] = v * ihs;
     }
-    xi[e] = v * ihs;
   }
   __syncthreads();
   const double* xx = xi;
