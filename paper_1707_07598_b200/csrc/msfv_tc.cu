@@ -227,6 +227,106 @@ __device__ __forceinline__ F2 potrf_inv8(const F2& t, double* Ds, double* Is, in
   return li;
 }
 
+// ---- software-pipelined POTRF: the factorization of the next diagonal tile
+// runs with the current step's other trailing DMMAs interleaved between its
+// pivots (one warp's in-order stream then overlaps the pivot chain latency
+// with tensor-core work).  Trailing pairs (a, b), 2 <= a <= PT, 1 <= b <= a,
+// in descending rows so X tiles die early.
+__host__ __device__ constexpr int tr_a(int PT, int k) {
+  for (int a = PT; a >= 2; --a) {
+    if (k < a) return a;
+    k -= a;
+  }
+  return 1;
+}
+__host__ __device__ constexpr int tr_b(int PT, int k) {
+  for (int a = PT; a >= 2; --a) {
+    if (k < a) return k + 1;
+    k -= a;
+  }
+  return 1;
+}
+template <int PT, int LO, int HI>
+__device__ __forceinline__ void trail(F2 (&W)[PT + 1][PT + 1], const F2 (&X)[PT + 1]) {
+  if constexpr (LO < HI) {
+    constexpr int a = tr_a(PT, LO), b = tr_b(PT, LO);
+    mma(W[a][b], neg(X[a]), X[b]);
+    trail<PT, LO + 1, HI>(W, X);
+  }
+}
+constexpr int PIPE_STAGES = 17;   // after load, after each of 8 pivots, after each of 8 inverse rows
+template <int PT>
+struct TrailPipe {
+  F2 (&W)[PT + 1][PT + 1];
+  const F2 (&X)[PT + 1];
+  template <int K>
+  __device__ __forceinline__ void at() {
+    constexpr int NP = PT * (PT + 1) / 2 - 1;
+    trail<PT, (K * NP) / PIPE_STAGES, ((K + 1) * NP) / PIPE_STAGES>(W, X);
+  }
+};
+template <int C, class P>
+__device__ __forceinline__ void p8_pipe(double (&x)[8], double& invd, int r, bool& bad, P& pipe) {
+  if constexpr (C < 8) {
+    double d = __shfl_sync(FULL, x[C], C);
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    const double inv = rsqrt(d);
+    if (r > C) x[C] *= inv;
+    if (r == C) { x[C] = d * inv; invd = inv; }
+    const double lrc = x[C];
+#pragma unroll
+    for (int q = C + 1; q < 8; ++q) {
+      const double lqc = __shfl_sync(FULL, lrc, q);
+      if (r >= q) x[q] -= lrc * lqc;
+    }
+    pipe.template at<C + 1>();
+    p8_pipe<C + 1>(x, invd, r, bad, pipe);
+  }
+}
+template <int R, class P>
+__device__ __forceinline__ void i8_pipe(double (&d)[8], int c, const double* Ds, const double* invd, P& pipe) {
+  if constexpr (R < 8) {
+    double acc = (R == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < R; ++m) acc -= Ds[R * 8 + m] * d[m];
+    d[R] = (R < c) ? 0.0 : acc * invd[R];
+    pipe.template at<9 + R>();
+    i8_pipe<R + 1>(d, c, Ds, invd, pipe);
+  }
+}
+// potrf_inv8 with the pipe's DMMA groups interleaved (all lanes convergent)
+template <class P>
+__device__ __forceinline__ F2 potrf_inv8_pipe(const F2& t, double* Ds, double* Is, int lane, int* flags, P& pipe) {
+  st2(Ds + lane * 2, t);
+  __syncwarp();
+  const int r = lane & 7;
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = Ds[r * 8 + q];
+  pipe.template at<0>();
+  bool bad = false;
+  double invd = 1.0;
+  p8_pipe<0>(x, invd, r, bad, pipe);
+  if (bad && lane == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
+  __syncwarp();
+  if (lane < 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) Ds[r * 8 + q] = x[q];
+    Is[64 + r] = invd;
+  }
+  __syncwarp();
+  double d[8];
+  i8_pipe<0>(d, r, Ds, Is + 64, pipe);
+  if (lane < 8) {
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = d[rr];
+  }
+  __syncwarp();
+  const F2 li = ld2(Is + lane * 2);
+  __syncwarp();
+  return li;
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- basis
@@ -290,15 +390,18 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       }
       Rt[a] = ld_rt(g, Sb, a, lane);
     }
+    F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, flags);
     for (int J = 0; J < NTI; ++J) {
       const int In = J + 1 + PT;       // tile row entering the window after this step
       const F2 nR = In < NTI ? ld_rt(g, Sb, In, lane) : F2{0.0, 0.0};
-      const F2 Li = potrf_inv8(W[0][0], Ds, Is, lane, flags);
       F2 X[PT + 1];
+      double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64 + lane * 2;
+      st2(Lt, Li);
 #pragma unroll
       for (int t = 1; t <= PT; ++t) {
         X[t] = {0.0, 0.0};
         mma(X[t], W[t][0], Li);                // X_t = A_t L^{-T}
+        st2(Lt + t * 64, X[t]);
       }
       // fused forward substitution of the 8 Lagrange columns (transposed)
       F2 Yt = {0.0, 0.0};
@@ -309,19 +412,17 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 #pragma unroll
         for (int t = 1; t <= PT; ++t) mma(Rt[t], nY, X[t]);   // r_t^T -= y^T X_t^T
       }
-      // trailing update of the register window
-#pragma unroll
-      for (int a = 1; a <= PT; ++a) {
-        const F2 nXa = neg(X[a]);
-#pragma unroll
-        for (int b = 1; b <= a; ++b) mma(W[a][b], nXa, X[b]);
-      }
-      {
-        double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64 + lane * 2;
-        st2(Lt, Li);
-#pragma unroll
-        for (int t = 1; t <= PT; ++t) st2(Lt + t * 64, X[t]);
-        st_rt(g, Sb, J, lane, Yt);             // y parks in the consumed rhs rows
+      st_rt(g, Sb, J, lane, Yt);               // y parks in the consumed rhs rows
+      // trailing update: the next diagonal tile first, then its POTRF with
+      // the remaining tile updates interleaved between the pivots
+      if constexpr (PT >= 1) {
+        mma(W[1][1], neg(X[1]), X[1]);
+        TrailPipe<PT> pipe{W, X};
+        if (J + 1 < NTI) {
+          Li = potrf_inv8_pipe(W[1][1], Ds, Is, lane, flags, pipe);
+        } else {
+          trail<PT, 0, PT * (PT + 1) / 2 - 1>(W, X);
+        }
       }
       // slide the window by one tile
 #pragma unroll
