@@ -26,35 +26,35 @@ namespace msfv {
 __device__ __forceinline__ void stage_closure(const Geo& g, int jb, const double* __restrict__ Sint, double* Sn) {
   const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
   const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  // four loads in flight per thread before the scattered shared-memory stores
-  const int tot = 8 * g.nI, step = blockDim.x;
-  for (int i0 = threadIdx.x; i0 < tot; i0 += 4 * step) {
-    double v[4];
+  // interior: one coordinate decode per node, the 8 corner loads in flight together
+  for (int a = threadIdx.x; a < g.nI; a += blockDim.x) {
+    double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = i0 + u * step < tot ? __ldg(Sb + i0 + u * step) : 0.0;
+    for (int cc = 0; cc < 8; ++cc) v[cc] = __ldg(Sb + (size_t)cc * g.nI + a);
+    int x, y, z;
+    decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+    double* d = Sn + ((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * step;
-      if (i >= tot) break;
-      const int cc = i / g.nI, a = i - cc * g.nI;
-      int x, y, z;
-      decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
-      Sn[((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8 + cc] = v[u];
-    }
+    for (int cc = 0; cc < 8; cc += 2) *reinterpret_cast<double2*>(d + cc) = make_double2(v[cc], v[cc + 1]);
   }
+  // skeleton: separable hats (6 one-dimensional values per node)
   for (int n = threadIdx.x; n < NN; n += blockDim.x) {
     const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
     if (x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3) continue;
     const bool node0 = jb == 0 && n == 0;     // pinned node: no row of S
+    const double hx[2] = {hatf1(x, g.ib1), hatf1(x - g.b1, g.ib1)};
+    const double hy[2] = {hatf1(y, g.ib2), hatf1(y - g.b2, g.ib2)};
+    const double hz[2] = {hatf1(z, g.ib3), hatf1(z - g.b3, g.ib3)};
 #pragma unroll
-    for (int cc = 0; cc < 8; ++cc) Sn[n * 8 + cc] = node0 ? 0.0 : hatf(g, cc, x, y, z);
+    for (int cc = 0; cc < 8; ++cc)
+      Sn[n * 8 + cc] = node0 ? 0.0 : (hx[cc & 1] * hy[(cc >> 1) & 1]) * hz[cc >> 2];
   }
 }
 
 size_t grad_smem_doubles(const Geo& g, int nrhs) {
   const size_t B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1;
   const size_t ne = (size_t)g.b1 * B2 * B3 + B1 * g.b2 * B3 + B1 * B2 * g.b3;
-  return B1 * B2 * B3 * 8 + ne + 16 * (size_t)nrhs + 64;
+  return B1 * B2 * B3 * 8 + ne + 16 * (size_t)nrhs + 64 + (ne + 1) / 2;   // + packed edge table (ints)
 }
 
 __global__ void __launch_bounds__(GRAD_THREADS)
@@ -72,6 +72,7 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   double* Tj = xi + NEx + NEy + NEz;      // [8][nrhs]
   double* Yj = Tj + 8 * nrhs;             // [8][nrhs]
   double* M = Yj + 8 * nrhs;              // [8][8]
+  int* Et = reinterpret_cast<int*>(M + 64);  // [NE] lower closure node | axis << 24
 
   for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
     const int cc = i / nrhs, s = i - cc * nrhs;
@@ -105,6 +106,14 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
     na = x + B1 * (y + B2 * z);
   };
   if (zs < 0 && rs < 0) {
+    for (int e = tid; e < NE; e += blockDim.x) {
+      int na, step;
+      double ihs;
+      edge(e, na, step, ihs);
+      Et[e] = na | ((e < NEx ? 0 : (e < NEx + NEy ? 1 : 2)) << 24);
+    }
+    __syncthreads();
+    const double ihx[3] = {g.ih1 * g.ih1, g.ih2 * g.ih2, g.ih3 * g.ih3};
     // xi_e = dS_e^T M dS_e for 8 edges per warp step: D (8 edges x 8 corners,
     // accumulator layout) times M on the DMMA (D += X Y^T with Y = M^T), then
     // the row-wise product with D and a 4-lane reduction.
@@ -114,9 +123,9 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
       const int e = e0 + m;
       double d0 = 0.0, d1 = 0.0, ihs = 0.0;
       if (e < NE) {
-        int na, step;
-        edge(e, na, step, ihs);
-        const int nb = na + step;
+        const int pk = Et[e], ax = pk >> 24, na = pk & 0xFFFFFF;
+        const int nb = na + (ax == 0 ? 1 : (ax == 1 ? B1 : B1 * B2));
+        ihs = ax == 0 ? ihx[0] : (ax == 1 ? ihx[1] : ihx[2]);
         const double2 sb = *reinterpret_cast<const double2*>(Sn + nb * 8 + 2 * q);
         const double2 sa = *reinterpret_cast<const double2*>(Sn + na * 8 + 2 * q);
         d0 = sb.x - sa.x;
