@@ -246,18 +246,29 @@ k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cv
     }
     na = x + B1 * (y + B2 * z);
   };
+  // owned-edge table: lower node | step code << 24 and c_e / h_e^2 (one decode
+  // and one load of c per edge)
+  int* Et = reinterpret_cast<int*>(Tj + 8 * nrhs);
+  double* Ce = reinterpret_cast<double*>(Et + ((NO + 1) & ~1));
+  for (int f = tid; f < NO; f += blockDim.x) {
+    int na, step;
+    long long eid;
+    double ihs;
+    edge(f, na, step, eid, ihs);
+    Et[f] = na | ((step == 1 ? 0 : (step == B1 ? 1 : 2)) << 24);
+    Ce[f] = __ldg(cvec + eid) * ihs;
+  }
+  __syncthreads();
   const int cc = lane >> 2, slot = lane & 3;
   double k0 = 0.0, k1 = 0.0;
   for (int base = 4 * wid; base < NO; base += 32) {
     const int f = base + slot;
     double a = 0.0, b = 0.0;
     if (f < NO) {
-      int na, step;
-      long long eid;
-      double ihs;
-      edge(f, na, step, eid, ihs);
-      b = Sn[(na + step) * 8 + cc] - Sn[na * 8 + cc];
-      a = (__ldg(cvec + eid) * ihs) * b;
+      const int pk = Et[f], sc = pk >> 24, na = pk & 0xFFFFFF;
+      const int nb = na + (sc == 0 ? 1 : (sc == 1 ? B1 : B1 * B2));
+      b = Sn[nb * 8 + cc] - Sn[na * 8 + cc];
+      a = Ce[f] * b;
     }
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(k0), "+d"(k1)
@@ -300,7 +311,9 @@ k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cv
 }
 
 size_t jv_smem_doubles(const Geo& g, int nrhs) {
-  return (size_t)(g.b1 + 1) * (g.b2 + 1) * (g.b3 + 1) * 8 + 8 * 64 + 8 * (size_t)nrhs;
+  const size_t B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1;
+  const size_t ne = (size_t)g.b1 * B2 * B3 + B1 * g.b2 * B3 + B1 * B2 * g.b3;   // >= owned edges
+  return B1 * B2 * B3 * 8 + 8 * 64 + 8 * (size_t)nrhs + (ne + 2) / 2 + ne;
 }
 
 cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec, const double* T, int nrhs,
