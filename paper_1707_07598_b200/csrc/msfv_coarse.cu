@@ -361,61 +361,83 @@ __device__ void coarse_potrf(const Band& B, int J, int* flags, FactorSmem& sm,
   double* P = sm.T;
   if (!tile_in_smem) load_tile(P, btile(B.A, B, J, 0));
   __syncthreads();
-  for (int kb = 0; kb < 4; ++kb) {
-    if (w == 0) {
-      potrf_inv8w(P + 8 * kb * LDT + 8 * kb, LDT, sm.Is, lane, flags);
-      const int m = lane >> 2, q = lane & 3;
-      sm.Li[kb][2 * lane] = sm.Is[m * 8 + 2 * q];          // L_kk^{-1}, C layout
-      sm.Li[kb][2 * lane + 1] = sm.Is[m * 8 + 2 * q + 1];
-    }
-    __syncthreads();
-    stamp(1 + 3 * kb);
-    if (w < 3 - kb) {                                      // L[i][kb] = A[i][kb] L_kk^{-T}
-      const int i = kb + 1 + w;
-      F2c c = {0.0, 0.0};
-      const F2c li = {sm.Li[kb][2 * lane], sm.Li[kb][2 * lane + 1]};
-      mxyt(c, frag(P, LDT, i, kb, lane), li);
-      put(P, LDT, i, kb, lane, c);
-    }
-    __syncthreads();
-    stamp(2 + 3 * kb);
-    {                                                      // trailing A[i][j] -= L[i][kb] L[j][kb]^T
-      int cnt = 0;
-      for (int i = kb + 1; i < 4; ++i)
-        for (int j = kb + 1; j <= i; ++j, ++cnt)
-          if (cnt == w) {
-            F2c c = frag(P, LDT, i, j, lane);
-            const F2c a = frag(P, LDT, i, kb, lane), b = frag(P, LDT, j, kb, lane);
-            mxyt(c, {-a.x, -a.y}, b);
-            put(P, LDT, i, j, lane, c);
-          }
-    }
-    __syncthreads();
-    stamp(3 + 3 * kb);
-  }
-  // Dinv in transposed blocks, held in sm.X2 (block (i,j) C layout of Dinv[i][j]^T)
+  // The whole chain runs on warp 0 (warp barriers only): four 8x8 POTRF +
+  // inverse steps, each followed by its panel and trailing DMMA updates, then
+  // Dinv in transposed blocks (sm.X2, block (i,j) = C layout of Dinv[i][j]^T):
+  // DT[i][j] = -(sum_k DT[k][j] L[i][k]^T) Li_i^T.
   double* DT = sm.X2;
-  if (w < 4) {                                             // DT[i][i] = Li_i^T
+  if (w == 0) {
     const int m = lane >> 2, q = lane & 3;
-    // C layout of Li^T: lane (m,q) holds Li[2q][m], Li[2q+1][m]; Li row-major is
-    // recovered from its C layout: Li[r][c] sits at lane 4r + c/2, slot c%2
-    const double* L = sm.Li[w];
-    const F2c f = {L[2 * (4 * (2 * q) + m / 2) + (m & 1)], L[2 * (4 * (2 * q + 1) + m / 2) + (m & 1)]};
-    put(DT, LDT, w, w, lane, f);
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      potrf_inv8w(P + 8 * kb * LDT + 8 * kb, LDT, sm.Is, lane, flags);
+      const F2c li = {sm.Is[m * 8 + 2 * q], sm.Is[m * 8 + 2 * q + 1]};     // L_kk^{-1}, C layout
+      sm.Li[kb][2 * lane] = li.x;
+      sm.Li[kb][2 * lane + 1] = li.y;
+      stamp(1 + 3 * kb);
+      // panel L[i][kb] = A[i][kb] L_kk^{-T} and trailing A[i][j] -= L[i][kb] L[j][kb]^T,
+      // all operands loaded before any store (independent DMMA chains)
+      F2c pl[4], tr[4][4];
+#pragma unroll
+      for (int i = kb + 1; i < 4; ++i) {
+        pl[i] = frag(P, LDT, i, kb, lane);
+#pragma unroll
+        for (int j = kb + 1; j <= i; ++j) tr[i][j] = frag(P, LDT, i, j, lane);
+      }
+#pragma unroll
+      for (int i = kb + 1; i < 4; ++i) {
+        F2c c = {0.0, 0.0};
+        mxyt(c, pl[i], li);
+        pl[i] = c;
+      }
+#pragma unroll
+      for (int i = kb + 1; i < 4; ++i)
+#pragma unroll
+        for (int j = kb + 1; j <= i; ++j) mxyt(tr[i][j], {-pl[i].x, -pl[i].y}, pl[j]);
+#pragma unroll
+      for (int i = kb + 1; i < 4; ++i) {
+        put(P, LDT, i, kb, lane, pl[i]);
+#pragma unroll
+        for (int j = kb + 1; j <= i; ++j) put(P, LDT, i, j, lane, tr[i][j]);
+      }
+      __syncwarp();
+      stamp(3 + 3 * kb);
+    }
+    for (int i = 0; i < 4; ++i) {                          // DT[i][i] = Li_i^T
+      // C layout of Li^T: lane (m,q) holds Li[2q][m], Li[2q+1][m]; Li[r][c] sits
+      // at lane 4r + c/2, slot c%2 of its C layout
+      const double* L = sm.Li[i];
+      const F2c f = {L[2 * (4 * (2 * q) + m / 2) + (m & 1)], L[2 * (4 * (2 * q + 1) + m / 2) + (m & 1)]};
+      put(DT, LDT, i, i, lane, f);
+    }
+    __syncwarp();
+    // block forward substitution by diagonals; Li and L blocks in registers
+    F2c lb[4][4], dt[4][4], lid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      lid[i] = {sm.Li[i][2 * lane], sm.Li[i][2 * lane + 1]};
+#pragma unroll
+      for (int k = 0; k < i; ++k) lb[i][k] = frag(P, LDT, i, k, lane);
+      dt[i][i] = frag(DT, LDT, i, i, lane);
+    }
+#pragma unroll
+    for (int d = 1; d < 4; ++d)
+#pragma unroll
+      for (int j = 0; j + d < 4; ++j) {
+        const int i = j + d;
+        F2c z = {0.0, 0.0};
+#pragma unroll
+        for (int k = j; k < i; ++k) mxyt(z, dt[k][j], lb[i][k]);
+        F2c o = {0.0, 0.0};
+        mxyt(o, {-z.x, -z.y}, lid[i]);
+        dt[i][j] = o;
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) put(DT, LDT, i, j, lane, dt[i][j]);
   }
   __syncthreads();
-  for (int d = 1; d < 4; ++d) {
-    if (w < 4 - d) {
-      const int j = w, i = j + d;
-      F2c z = {0.0, 0.0};
-      for (int k = j; k < i; ++k) mxyt(z, frag(DT, LDT, k, j, lane), frag(P, LDT, i, k, lane));
-      F2c o = {0.0, 0.0};
-      const F2c li = {sm.Li[i][2 * lane], sm.Li[i][2 * lane + 1]};
-      mxyt(o, {-z.x, -z.y}, li);
-      put(DT, LDT, i, j, lane, o);
-    }
-    __syncthreads();
-  }
   stamp(13);
   // Dinv row-major: Dinv[8i + 2q (+1)][8j + m] = DT[i][j] slot 0 (1) at lane (m, q)
   double* dst = B.Dinv + (size_t)J * TT;
