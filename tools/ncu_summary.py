@@ -1,7 +1,7 @@
 """Summarize an ncu launch list (--metrics gpu__time_duration.sum --csv) and a
 --set full report into profiles/ (markdown rows + JSON).
 
-usage: python tools/ncu_summary.py LAUNCHES.csv REPORT.ncu-rep OUT_PREFIX
+usage: python tools/ncu_summary.py LAUNCHES.csv REPORT.ncu-rep[,REPORT2.ncu-rep...] OUT_PREFIX
 """
 import collections
 import csv
@@ -60,14 +60,17 @@ def full(path):
                     pass
         if "dmma_cycles" in m and m.get("smsp_cycles"):
             m["dmma_pipe_pct"] = 100.0 * m["dmma_cycles"] / m["smsp_cycles"]
-        res[name] = m          # last instance wins (steady-state step)
+        if name not in res or m.get("duration_ns", 0) > res[name].get("duration_ns", 0):
+            res[name] = m      # the longest instance of each kernel (its dominant launch)
     return res
 
 
 def main():
     lp, rp, pre = sys.argv[1:4]
     L = launches(lp)
-    F = full(rp)
+    F = collections.OrderedDict()
+    for r in rp.split(","):
+        F.update(full(r))
     tot = sum(t for _, t in L.values())
     md = ["| kernel | launches | ms (cold, serialized) | share |", "|---|---|---|---|"]
     for k, (n, t) in sorted(L.items(), key=lambda kv: -kv[1][1]):
