@@ -163,12 +163,24 @@ class MultiscaleBasis:
         self._model = None
         self._m_dev = op._dev[1]
         self.factor, self.Sint, self.Kloc, self.flags = factor, Sint, Kloc, flags
-        self.families = np.full(partition.n_coarse_nodes, "lagrange")
-        self.labels = [("coarse_node", int(cn)) for cn in partition.coarse_nodes]
+        self._families = None
+        self._labels = None
         self.cache = None
         self._S = None
         self._EP = None
         self._checked = False
+
+    @property
+    def families(self):
+        if self._families is None:
+            self._families = np.full(self.partition.n_coarse_nodes, "lagrange")
+        return self._families
+
+    @property
+    def labels(self):
+        if self._labels is None:
+            self._labels = [("coarse_node", int(cn)) for cn in self.partition.coarse_nodes]
+        return self._labels
 
     @property
     def model(self):
