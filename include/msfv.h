@@ -107,6 +107,15 @@ MSFV_API int msfv_edge_average(const msfv_plan* plan, const double* sigma, const
  * scratch: MSFV_INFO_SCRATCH_DOUBLES doubles.  flags |= LOCAL_NOT_SPD. */
 MSFV_API int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                      double* scratch, int32_t* flags, void* stream);
+/* The same build in two launches (tensor-core geometries only): the forward
+ * part (factors, Galerkin blocks, and y = L^{-1} R parked in Sint) and the
+ * backward sweeps (Sint = S_I).  The Galerkin blocks do not need the backward
+ * sweeps, so the coarse factorization can run while msfv_basis_backward
+ * executes on another stream (a small persistent grid that leaves a CTA slot
+ * per SM for the cooperative factorization). */
+MSFV_API int msfv_basis_forward(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                       int32_t* flags, void* stream);
+MSFV_API int msfv_basis_backward(const msfv_plan* plan, const double* factor, double* Sint, void* stream);
 /* Values of S in the reference CSC pattern (basis.py:574-594):
  * vals[t] = src[t] >= 0 ? Sint[src[t]] : hatv[t]  (src, hatv device arrays). */
 MSFV_API int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,

@@ -50,6 +50,8 @@ SIGNATURES = {
     "msfv_operator": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "msfv_edge_average": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "msfv_basis_build": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "msfv_basis_forward": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "msfv_basis_backward": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_basis_csc": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P]),
     "msfv_galerkin": (ctypes.c_int, [_P, _P, _D, _P, _P]),
     "msfv_coarse_diag": (ctypes.c_int, [_P, _P, _P, _P]),

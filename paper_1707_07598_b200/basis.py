@@ -162,13 +162,51 @@ class MultiscaleBasis:
         self.op = op
         self._model = None
         self._m_dev = op._dev[1]
-        self.factor, self.Sint, self.Kloc, self.flags = factor, Sint, Kloc, flags
+        self.factor, self._Sint, self.Kloc, self.flags = factor, Sint, Kloc, flags
+        self._sint_event = None          # set when the backward sweeps run on the side stream
+        self._bwd_pending = False        # split build: backward sweeps not launched yet
         self._families = None
         self._labels = None
         self.cache = None
         self._S = None
         self._EP = None
         self._checked = False
+
+    def start_backward(self):
+        """Launch the deferred backward sweeps (split build) on the side stream,
+        ordered after everything already queued on the current stream."""
+        if not self._bwd_pending:
+            return
+        import torch
+        eng = self.engine
+        self._bwd_pending = False
+        main, side = torch.cuda.current_stream(), eng.side_stream
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            eng.basis_backward(self.factor, self._Sint)
+        self.factor.record_stream(side)
+        self._Sint.record_stream(side)
+        done = torch.cuda.Event()
+        done.record(side)
+        self._sint_event = done
+
+    @property
+    def Sint(self):
+        """Interior basis values; orders the current stream after the backward
+        sweeps (split build)."""
+        if self._bwd_pending:
+            self.start_backward()
+        if self._sint_event is not None:
+            import torch
+            torch.cuda.current_stream().wait_event(self._sint_event)
+        return self._Sint
+
+    def sint_for(self, pts):
+        """Sint for a survey-point kernel: the backward sweeps are awaited only
+        when the point set has interior nodes (skeleton values are hats)."""
+        return self.Sint if pts.interior_blocks else self._Sint
 
     @property
     def families(self):
@@ -275,6 +313,15 @@ def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None):
             raise NotImplementedError("the GPU path builds the Lagrange family only")
     eng = engine_for(partition)
     _, m_dev, sigma, w = op.device_state(eng)
+    if eng.tensor_core:
+        # forward part (factor, forward sweep, Galerkin) now; the backward
+        # sweeps that complete S_I are deferred to start_backward(), which the
+        # forward chain calls after the coarse factorization so they overlap
+        # the latency-bound coarse sweeps on the engine's side stream
+        factor, Sint, Kloc, fl = eng.basis_forward(w, op.flags)
+        basis = MultiscaleBasis(partition, eng, op, factor, Sint, Kloc, fl)
+        basis._bwd_pending = True
+        return basis
     factor, Sint, Kloc, fl = eng.basis(w, op.flags)
     return MultiscaleBasis(partition, eng, op, factor, Sint, Kloc, fl)
 

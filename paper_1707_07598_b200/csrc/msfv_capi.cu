@@ -323,8 +323,8 @@ int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* 
   return cuda_check(launch_edge_weights(plan->g, tmp, c, st), "edge_average");
 }
 
-int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
-                     double* scratch, int32_t* flags, void* stream) {
+static int basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                       double* scratch, int32_t* flags, void* stream, bool bwd) {
   CHECK_PLAN(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
@@ -339,10 +339,28 @@ int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, dou
       pl->g.skel = pl->skel_dev;
       pl->g.nskel = (int)tab.size();
     }
-    return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st), "basis_build");
+    return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, bwd), "basis_build");
   }
   double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
   return cuda_check(launch_basis(g, w, factor, Lr, Sint, Kloc, flags, st), "basis_build");
+}
+
+int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                     double* scratch, int32_t* flags, void* stream) {
+  return basis_build(plan, w, factor, Sint, Kloc, scratch, flags, stream, true);
+}
+
+int msfv_basis_forward(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                       int32_t* flags, void* stream) {
+  CHECK_PLAN(plan);
+  if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  return basis_build(plan, w, factor, Sint, Kloc, nullptr, flags, stream, false);
+}
+
+int msfv_basis_backward(const msfv_plan* plan, const double* factor, double* Sint, void* stream) {
+  CHECK_PLAN(plan);
+  if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  return cuda_check(launch_basis_bwd(plan->g, factor, Sint, (cudaStream_t)stream), "basis_backward");
 }
 
 int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const double* hatv, double* vals,

@@ -331,7 +331,53 @@ __device__ __forceinline__ F2 potrf_inv8_pipe(const F2& t, double* Ds, double* I
 
 // ----------------------------------------------------------------- basis
 
+// Backward substitution of block jb: Sb holds y = L^{-1} R (parked by the
+// forward sweep) and receives S_I = L^{-T} y:
+//   x_J^T = (y_J^T - sum_t x_{J+t}^T X_t) L_JJ^{-1};
+// the window keeps -x^T of the last PT tiles; the next steps' transposed
+// factor tiles and y are prefetched into registers.
 template <int PT>
+__device__ __forceinline__ void backward_sweep(const Geo& g, const double* __restrict__ LT, double* Sb, int jb,
+                                               int lane) {
+  const int NTI = (g.nI + 7) >> 3;
+  if (NTI == 0) return;
+    F2 Xw[PT > 0 ? PT : 1];
+#pragma unroll
+    for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
+    F2 nLt[2][PT + 1], nY[2];
+    auto load_bwd = [&](int J, F2 (&Lt)[PT + 1], F2& Y) {
+      const double* p = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
+#pragma unroll
+      for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld_t(p + t * 64, lane) : F2{0.0, 0.0};
+      Y = ld_rt(g, Sb, J, lane);
+    };
+    load_bwd(NTI - 1, nLt[0], nY[0]);
+    if (NTI > 1) load_bwd(NTI - 2, nLt[1], nY[1]);
+    for (int J = NTI - 1; J >= 0; --J) {
+      F2 cLt[PT + 1];
+#pragma unroll
+      for (int t = 0; t <= PT; ++t) {
+        cLt[t] = nLt[0][t];
+        nLt[0][t] = nLt[1][t];
+      }
+      F2 acc = nY[0];
+      nY[0] = nY[1];
+      if (J > 1) load_bwd(J - 2, nLt[1], nY[1]);
+#pragma unroll
+      for (int t = 1; t <= PT; ++t)
+        if (J + t < NTI) mma(acc, Xw[t - 1], cLt[t]);
+      F2 xj = {0.0, 0.0};
+      mma(xj, acc, cLt[0]);
+      st_rt(g, Sb, J, lane, xj);
+#pragma unroll
+      for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
+      if (PT > 0) Xw[0] = neg(xj);
+    }
+  __syncwarp();
+}
+
+
+template <int PT, bool BWD>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
            double* __restrict__ Kloc, int* __restrict__ flags) {
@@ -437,41 +483,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       Rt[PT] = nR;
     }
     __syncwarp();
-    // ---- backward substitution x_J^T = (y_J^T - sum_t x_{J+t}^T X_t) L_JJ^{-1};
-    // the window keeps -x^T of the last PT tiles; the next step's transposed
-    // factor tiles and y are prefetched into registers.
-    F2 Xw[PT > 0 ? PT : 1];
-#pragma unroll
-    for (int t = 0; t < (PT > 0 ? PT : 1); ++t) Xw[t] = {0.0, 0.0};
-    F2 nLt[2][PT + 1], nY[2];
-    auto load_bwd = [&](int J, F2 (&Lt)[PT + 1], F2& Y) {
-      const double* p = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64;
-#pragma unroll
-      for (int t = 0; t <= PT; ++t) Lt[t] = (t == 0 || J + t < NTI) ? ld_t(p + t * 64, lane) : F2{0.0, 0.0};
-      Y = ld_rt(g, Sb, J, lane);
-    };
-    load_bwd(NTI - 1, nLt[0], nY[0]);
-    if (NTI > 1) load_bwd(NTI - 2, nLt[1], nY[1]);
-    for (int J = NTI - 1; J >= 0; --J) {
-      F2 cLt[PT + 1];
-#pragma unroll
-      for (int t = 0; t <= PT; ++t) {
-        cLt[t] = nLt[0][t];
-        nLt[0][t] = nLt[1][t];
-      }
-      F2 acc = nY[0];
-      nY[0] = nY[1];
-      if (J > 1) load_bwd(J - 2, nLt[1], nY[1]);
-#pragma unroll
-      for (int t = 1; t <= PT; ++t)
-        if (J + t < NTI) mma(acc, Xw[t - 1], cLt[t]);
-      F2 xj = {0.0, 0.0};
-      mma(xj, acc, cLt[0]);
-      st_rt(g, Sb, J, lane, xj);
-#pragma unroll
-      for (int t = PT - 1; t >= 1; --t) Xw[t] = Xw[t - 1];
-      if (PT > 0) Xw[0] = neg(xj);
-    }
+    if constexpr (BWD) backward_sweep<PT>(g, LT, Sb, jb, lane);
     __syncwarp();
   }
 
@@ -514,6 +526,17 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   K.x -= G.x;
   K.y -= G.y;
   st2(Kloc + (size_t)jb * 64 + lane * 2, K);
+}
+
+// Backward sweeps only (S_I from the parked y): a small persistent grid (one
+// 2-warp CTA per two SMs) so it can run beside the cooperative coarse
+// factorization, which needs a CTA slot on every SM.
+template <int PT>
+__global__ void __launch_bounds__(TC_WARPS * 32) k_basis_bwd(Geo g, const double* __restrict__ LT,
+                                                             double* __restrict__ Sint) {
+  const int lane = threadIdx.x & 31;
+  for (int jb = blockIdx.x * TC_WARPS + (threadIdx.x >> 5); jb < g.nbl; jb += gridDim.x * TC_WARPS)
+    backward_sweep<PT>(g, LT, Sint + (size_t)jb * 8 * g.nI, jb, lane);
 }
 
 // ------------------------------------------------------- skeleton Galerkin
@@ -739,13 +762,18 @@ size_t tc_scratch_doubles(const Geo&) { return 0; }
 
 template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
-                                     double* Kloc, int* flags, cudaStream_t st) {
+                                     double* Kloc, int* flags, bool bwd, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
   const size_t nf = 2 * ((size_t)g.ni2 * g.ni3 + (size_t)g.ni1 * g.ni3 + (size_t)g.ni1 * g.ni2);
   const size_t smem = (size_t)TC_WARPS * (((g.nI + 7) / 8) * 8 * AROW + nf) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_basis_tc<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_basis_tc<PT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_basis_tc<PT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_basis_tc<PT><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+  if (bwd)
+    k_basis_tc<PT, true><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+  else
+    k_basis_tc<PT, false><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -768,16 +796,42 @@ static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const doubl
 }
 
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
-                            int* flags, cudaStream_t st) {
+                            int* flags, cudaStream_t st, bool bwd) {
   switch (tc_band(g)) {
-    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, st);
-    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, st);
-    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Kloc, flags, st);
-    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Kloc, flags, st);
-    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Kloc, flags, st);
-    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Kloc, flags, st);
-    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Kloc, flags, st);
-    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Kloc, flags, st);
+    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int PT>
+static cudaError_t launch_basis_bwd_t(const Geo& g, const double* LT, double* Sint, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // leaves a few SMs to the coarse sweeps it runs beside
+  const int grid = std::max(1, std::min((g.nbl + TC_WARPS - 1) / TC_WARPS, sms - 12));
+  k_basis_bwd<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, LT, Sint);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_basis_bwd(const Geo& g, const double* LT, double* Sint, cudaStream_t st) {
+  switch (tc_band(g)) {
+    case 0: return launch_basis_bwd_t<0>(g, LT, Sint, st);
+    case 1: return launch_basis_bwd_t<1>(g, LT, Sint, st);
+    case 2: return launch_basis_bwd_t<2>(g, LT, Sint, st);
+    case 3: return launch_basis_bwd_t<3>(g, LT, Sint, st);
+    case 4: return launch_basis_bwd_t<4>(g, LT, Sint, st);
+    case 5: return launch_basis_bwd_t<5>(g, LT, Sint, st);
+    case 6: return launch_basis_bwd_t<6>(g, LT, Sint, st);
+    case 7: return launch_basis_bwd_t<7>(g, LT, Sint, st);
     default: return cudaErrorInvalidValue;
   }
 }

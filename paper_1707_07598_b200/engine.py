@@ -180,6 +180,27 @@ class Engine:
                                            ptr(fl), stream()), "basis_build")
         return factor, Sint, Kloc, fl
 
+    def basis_forward(self, w, fl=None):
+        """Split build, part 1: factors, Galerkin blocks, y = L^-1 R parked in Sint."""
+        with phase("basis"):
+            factor = self.empty(max(self.factor_doubles, 1))
+            Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
+            Kloc = self.empty(self.nbl * 64)
+            fl = fl if fl is not None else self.flags()
+            _lib.check(self.L.msfv_basis_forward(self.plan, ptr(w), ptr(factor), ptr(Sint), ptr(Kloc), ptr(fl),
+                                                 stream()), "basis_forward")
+        return factor, Sint, Kloc, fl
+
+    def basis_backward(self, factor, Sint):
+        """Split build, part 2 (on the current stream): Sint = S_I."""
+        _lib.check(self.L.msfv_basis_backward(self.plan, ptr(factor), ptr(Sint), stream()), "basis_backward")
+
+    @property
+    def side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
     def galerkin(self, Kloc, shift=0.0, out=None):
         Ak = out if out is not None else self.empty(self.ak_doubles)
         with phase("galerkin"):

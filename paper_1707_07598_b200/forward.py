@@ -154,11 +154,12 @@ class ReducedState:
 def _coarse_solve_chain(eng, op, survey, basis, shift, fl):
     Pp, Qp, _ = survey.device(eng)
     ns = survey.n_sources
-    F = eng.restrict_points(Qp, basis.Sint, None, ns)                 # S^T Q   (forward.py:115)
+    F = eng.restrict_points(Qp, basis.sint_for(Qp), None, ns)        # S^T Q   (forward.py:115)
     Ak = eng.galerkin(basis.Kloc, shift)                              # S^T A S (+ shift I) (forward.py:118,125)
     eng.coarse_factor(Ak, fl)                                         # cho_factor (forward.py:121)
+    basis.start_backward()                                            # S_I sweeps overlap the coarse solve
     T = eng.coarse_solve(Ak, F)                                       # T = A_k^-1 S^T Q (forward.py:142)
-    D = eng.receive(Pp, basis.Sint, Y=T)                              # P^T S T (forward.py:143)
+    D = eng.receive(Pp, basis.sint_for(Pp), Y=T)                      # P^T S T (forward.py:143)
     return D, Ak, T
 
 
@@ -238,7 +239,7 @@ class AdaptiveSensitivity:
         eng, b = self.engine, self.basis
         ns = self.survey.n_sources
         W = eng.to_device(W)
-        y = eng.restrict_points(self.Pp, b.Sint, W, ns)                             # S^T P W (forward.py:276)
+        y = eng.restrict_points(self.Pp, b.sint_for(self.Pp), W, ns)                # S^T P W (forward.py:276)
         eng.coarse_solve(self.state.Lk, y)
         # z = interior_solve(P W - A S y) = blockdiag(A_II^-1)(P W)_I (forward.py:278)
         Zc = eng.interior_fields(self.Pp, b.factor, W, ns)
@@ -267,7 +268,7 @@ class AdaptiveSensitivity:
                 dt = None
             if dt is not None:
                 eng.coarse_solve(self.state.Lk, dt)                                 # forward.py:267
-                return eng.receive(self.Pp, b.Sint, Y=dt)                           # P^T S dt (:268)
+                return eng.receive(self.Pp, b.sint_for(self.Pp), Y=dt)              # P^T S dt (:268)
         ydm = eng.residual(None, 0.0, c, self.U, -1.0, ns)                          # -G^T(gu c)
         eng.interior_solve(b.factor, ydm)                                         # _Y_dm (forward.py:250-252)
         dt = eng.restrict_op(b.Sint, c, self.UR, self.w, ydm, ns, scale=-1.0)       # xdm - S^T(gdm + A ydm)
