@@ -19,6 +19,7 @@
 // slot t = L_{J+t,J}.   Fragment layouts (m8n8k4 f64):
 //   A[m][k] at lane 4m+k ; B[k][n] at lane 4n+k ; C[m][n] at lane 4m+n/2, slot n%2
 // An 8x8 tile in "A-frag" form is two A fragments (k = 0..3 and 4..7).
+#include <cstdlib>
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
 
@@ -531,11 +532,12 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 // Backward sweeps only (S_I from the parked y): a small persistent grid (one
 // 2-warp CTA per two SMs) so it can run beside the cooperative coarse
 // factorization, which needs a CTA slot on every SM.
+constexpr int BWD_WARPS = 8;   // one 256-thread CTA per SM (register-limited)
 template <int PT>
-__global__ void __launch_bounds__(TC_WARPS * 32) k_basis_bwd(Geo g, const double* __restrict__ LT,
-                                                             double* __restrict__ Sint) {
+__global__ void __launch_bounds__(BWD_WARPS * 32) k_basis_bwd(Geo g, const double* __restrict__ LT,
+                                                              double* __restrict__ Sint) {
   const int lane = threadIdx.x & 31;
-  for (int jb = blockIdx.x * TC_WARPS + (threadIdx.x >> 5); jb < g.nbl; jb += gridDim.x * TC_WARPS)
+  for (int jb = blockIdx.x * BWD_WARPS + (threadIdx.x >> 5); jb < g.nbl; jb += gridDim.x * BWD_WARPS)
     backward_sweep<PT>(g, LT, Sint + (size_t)jb * 8 * g.nI, jb, lane);
 }
 
@@ -815,9 +817,16 @@ static cudaError_t launch_basis_bwd_t(const Geo& g, const double* LT, double* Si
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // leaves a few SMs to the coarse sweeps it runs beside
-  const int grid = std::max(1, std::min((g.nbl + TC_WARPS - 1) / TC_WARPS, sms - 12));
-  k_basis_bwd<PT><<<grid, TC_WARPS * 32, 0, st>>>(g, LT, Sint);
+  // persistent, one 8-warp CTA on all but a few SMs: the register file of a
+  // busy SM is then full, so the latency-bound coarse sweeps this kernel runs
+  // beside land on the SMs left free
+  static int free_sms = -1;
+  if (free_sms < 0) {
+    const char* e = getenv("MSFV_BWD_FREE_SMS");
+    free_sms = e ? std::max(0, atoi(e)) : 12;
+  }
+  const int grid = std::max(1, std::min((g.nbl + BWD_WARPS - 1) / BWD_WARPS, sms - free_sms));
+  k_basis_bwd<PT><<<grid, BWD_WARPS * 32, 0, st>>>(g, LT, Sint);
   count_launches(1);
   return cudaGetLastError();
 }
