@@ -27,6 +27,10 @@
 //   Lo    NT*(PT+1) tiles   the factor: slot t = L_{J+t,J} (slot 0 unused)
 //   LF,LB NT*(PT+1) tiles   solve copies (slot 0 = L_JJ^{-1}) in DMMA fragment
 //                           order, forward and transposed (k_coarse_pack)
+//   SF,SB NT*(PT+1) tiles   block-row-scaled solve copies for the cluster
+//                           sweeps (k_coarse_pack_scaled): SF[J][t] =
+//                           Dinv_{J+t} L_{J+t,J}, SB[J][t] = Dinv_{J-t}^T
+//                           L_{J,J-t}^T, slot 0 = Dinv_J / Dinv_J^T
 // Padding rows (>= n) are identity.
 //
 // The band factorization is one cooperative launch with one grid barrier per
@@ -38,6 +42,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 
 #include "msfv_common.cuh"
@@ -56,6 +61,8 @@ struct Band {
   double* Lo;
   double* LF;
   double* LB;
+  double* SF;   // scaled solve copies for the cluster sweeps (k_coarse_pack_scaled)
+  double* SB;
   int n;        // valid rows
   int NT, PT;   // tile rows, band tiles
 };
@@ -81,6 +88,8 @@ __host__ __device__ __forceinline__ Band make_band(double* base, size_t& off, in
   B.Lo = base ? base + off : nullptr;       off += bt;
   B.LF = base ? base + off : nullptr;       off += bt;
   B.LB = base ? base + off : nullptr;       off += bt;
+  B.SF = base ? base + off : nullptr;       off += bt;
+  B.SB = base ? base + off : nullptr;       off += bt;
   return B;
 }
 
@@ -872,10 +881,14 @@ __global__ void __launch_bounds__(256) k_coarse_trsv_bulk(SweepJobs jobs, int CH
     }
     if (i >= nf && ch == nch - 1) {                         // first chunk of a backward step
       p0 = p1 = 0.0;
+#ifndef TRSV_SKIP_LDX
       if (wid < 4) ldx(J, wid, ya, yb);
+#endif
     }
     double ra = 0.0, rb = 0.0;
+#ifndef TRSV_SKIP_LDX
     if (i < nf && ch == nch - 1 && wid < 4) ldx(J + 1 + PTj, wid, ra, rb);   // in flight during the step
+#endif
     long long tclk = 0, tw = 0;
     if (tprof && tid == 0) tclk = clock64();
     mbar_wait(&bar[st], (par >> st) & 1u);
@@ -1051,6 +1064,440 @@ static void trsv_bulk_shape(int PT, int& cht, int& ns, size_t& smem) {
   smem = fixed + (size_t)ns * cht * tile_b;
 }
 
+// ------------------------------------------------ cluster-parallel sweeps
+//
+// Block-row-scaled forms of the two triangular systems:
+//   forward   (Dinv L) y = Dinv b,        tiles SF[J][t] = Dinv_{J+t} L_{J+t,J}
+//   backward  (Dinv^T L^T) x = Dinv^T y,  tiles SB[J][t] = Dinv_{J-t}^T L_{J,J-t}^T
+// have identity diagonal blocks, so a right-looking sweep needs no diagonal
+// solve: once row J is final, every row J+t (J-t) subtracts M_t * row_J, and
+// the next row is final after ONE tile product.  Rows are spread over the C
+// CTAs of a thread-block cluster (row R owned by CTA R mod C, each CTA holding
+// its rows' accumulators in a shared-memory ring and streaming only its own
+// tiles), so a step costs one tile product plus one DSMEM broadcast of the
+// final row instead of a whole tile column on one SM.
+//
+// Broadcast protocol (all in shared memory, no grid barrier): the owner of
+// the row final at global step u writes its 8x32 transposed value with
+// st.async into slot u % CS_NB of every CTA's Ybuf, completing 2 KB of
+// transaction bytes on that CTA's full[slot] barrier (armed by the receiver
+// one use ahead).  A receiver releases a slot (remote arrive on empty[slot] of
+// the CTA that will write its next use) as soon as the row is in registers.
+// Warp w always owns 8-row piece w of every row, so the ring needs no
+// CTA-wide synchronisation; one __syncthreads per step guards tile-stage reuse.
+__global__ void __launch_bounds__(256) k_coarse_pack_scaled(Band B) {
+  constexpr int LD = TB + 1;                             // padded rows: conflict-free columns
+  __shared__ double Ms[TB * LD], Ds[TB * LD];
+  const int J = blockIdx.x / (B.PT + 1), t = blockIdx.x % (B.PT + 1);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // output (r = ty + 8i, col = tx)
+  for (int dir = 0; dir < 2; ++dir) {
+    const int R = dir == 0 ? J + t : J - t;              // row block whose Dinv scales
+    const bool valid = R >= 0 && R < B.NT;
+    double* out = (dir == 0 ? B.SF : B.SB) + (size_t)blockIdx.x * TT;
+    __syncthreads();
+    if (valid) {
+      const double* L = t == 0 ? nullptr : btile(B.Lo, B, dir == 0 ? J : R, t);
+      for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+        const int r = e / TB, cc = e % TB;
+        Ds[r * LD + cc] = B.Dinv[(size_t)R * TT + e];
+        Ms[r * LD + cc] = L ? L[e] : (r == cc ? 1.0 : 0.0);
+      }
+    }
+    __syncthreads();
+    // forward: (Dinv M)[r][col]; backward: (M Dinv)^T[r][col] = sum_k M[col][k] Dinv[k][r]
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (valid) {
+#pragma unroll 8
+      for (int kk = 0; kk < TB; ++kk) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = ty + 8 * i;
+          v[i] = dir == 0 ? fma(Ds[r * LD + kk], Ms[kk * LD + tx], v[i]) : fma(Ms[tx * LD + kk], Ds[kk * LD + r], v[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {                        // element (r, tx) -> piece layout
+      const int r = ty + 8 * i, p = (r >> 3) * 4 + (tx >> 3), lane = (r & 7) * 4 + ((tx & 7) >> 1);
+      out[p * 64 + lane * 2 + (tx & 1)] = v[i];
+    }
+  }
+}
+
+constexpr int CS_CWARPS = 4;                      // compute warps
+constexpr int CS_THREADS = (CS_CWARPS + 1) * 32;  // + one producer warp
+constexpr int CS_NB = 4;      // broadcast slots
+constexpr int CS_MAXNS = 3;   // tile stages (2 when 3 do not fit)
+constexpr int CS_MAXC = 8;
+
+struct CsJob {
+  const double* SF;
+  const double* SB;
+  double* X;
+  int NT, PT, n, nrhs, J0, mode;   // mode bit 1 forward (rows J0..NT-1), bit 2 backward (NT-1..J0)
+};
+struct CsJobs {
+  CsJob j[2];
+  int groups;   // clusters (8 right-hand sides each) per job
+  int C;        // CTAs per cluster
+  int SLT;      // tiles per stage
+  int NS;       // tile stages
+};
+
+namespace {
+__device__ __forceinline__ unsigned cs_mapa(unsigned a, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// CTA-scope acquire: the st.async / bulk-copy data completes through the
+// barrier's transaction count (async proxy); a cluster-scope acquire would
+// also invalidate L1 (CCTL.IVALL) on every wait.
+__device__ __forceinline__ void cs_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cs_arm(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// Relaxed remote arrive: a release at cluster scope compiles to a GPU-wide
+// MEMBAR that waits for the thread's outstanding global stores.  The only
+// accesses it must order are the shared-memory reads of the slot, which the
+// caller makes complete first through a register dependency (dep == 0).
+__device__ __forceinline__ void cs_remote_arrive(unsigned rbar, unsigned dep) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(rbar + dep) : "memory");
+}
+// 0, computed from v so that it cannot issue before v's loads complete
+__device__ __forceinline__ unsigned cs_dep(double v) {
+  unsigned z;
+  asm volatile("{\n .reg .b32 lo, hi;\n mov.b64 {lo, hi}, %1;\n and.b32 %0, lo, 0;\n}\n" : "=r"(z) : "d"(v));
+  return z;
+}
+__device__ __forceinline__ void cs_st_async(unsigned raddr, double a, double b, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void cs_bulk(double* dst, const double* src, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"((unsigned)(TT * sizeof(double))), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cs_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ int cs_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return (int)r;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(CS_THREADS) k_coarse_sweep_cluster(CsJobs jobs) {
+  extern __shared__ __align__(128) double csm[];
+  __shared__ __align__(8) unsigned long long full[CS_NB], empty[CS_NB], tbar[CS_MAXNS], tfree[CS_MAXNS];
+  const int C = jobs.C, cm = C - 1, SLT = jobs.SLT, NS = jobs.NS;
+  const int cl = blockIdx.x / C, k = cs_rank();
+  const bool j1 = cl >= jobs.groups;                          // (no dynamic param indexing)
+  CsJob job;
+#define CS_SEL(f) job.f = j1 ? jobs.j[1].f : jobs.j[0].f
+  CS_SEL(SF); CS_SEL(SB); CS_SEL(X); CS_SEL(NT); CS_SEL(PT); CS_SEL(n); CS_SEL(nrhs); CS_SEL(J0); CS_SEL(mode);
+#undef CS_SEL
+  const int group = j1 ? cl - jobs.groups : cl;
+  const int NT = job.NT, PT = job.PT, W = PT + 1, J0 = job.J0, nrow = job.n, nrhs = job.nrhs;
+  const int nV = NT - J0;
+  const int nph = ((job.mode & 1) ? 1 : 0) + ((job.mode & 2) ? 1 : 0);
+  const int total = nph * nV;
+  const bool fwd0 = (job.mode & 1) != 0;
+  double* __restrict__ X = job.X;
+  double* stage = csm;                                          // [NS][SLT][TT]
+  double* ring = stage + (size_t)NS * SLT * TT;                 // [W][4][64]
+  double* ybuf = ring + (size_t)W * 256;                        // [CS_NB][4][64]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int q = lane & 3, col = group * 8 + (lane >> 2);
+  const bool cok = col < nrhs;
+  const unsigned full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+  const unsigned tbar0 = smem_u32(&tbar[0]), tfree0 = smem_u32(&tfree[0]);
+  const unsigned ybuf0 = smem_u32(ybuf);
+
+  // step u: direction, local index v, band row R; this CTA's rows updated at
+  // step u are R +- t for t = t1, t1 + C, ... <= tmax; `entry`: the row of
+  // local step v + PT + 1 (band row Re) enters this CTA's ring at step u
+  struct Step {
+    bool fwd, entry;
+    int v, R, t1, tmax, Re;
+  };
+  auto geom = [&](int u) {
+    Step s;
+    s.fwd = fwd0 && u < nV;
+    s.v = u < nV ? u : u - nV;
+    s.R = s.fwd ? J0 + s.v : NT - 1 - s.v;
+    s.t1 = (s.fwd ? k - s.R : s.R - k) & cm;
+    if (s.t1 == 0) s.t1 = C;
+    s.tmax = min(PT, nV - 1 - s.v);
+    s.Re = s.fwd ? s.R + W : s.R - W;
+    s.entry = s.v + W < nV && (s.Re & cm) == k;
+    return s;
+  };
+  auto row_of = [&](int u) {
+    const int v = u < nV ? u : u - nV;
+    return (fwd0 && u < nV) ? J0 + v : NT - 1 - v;
+  };
+  auto ldx = [&](int R, int pi, double& a, double& b) {
+    const int r0 = R * TB + 8 * pi + 2 * q;
+    a = (cok && r0 < nrow) ? X[(size_t)r0 * nrhs + col] : 0.0;
+    b = (cok && r0 + 1 < nrow) ? X[(size_t)(r0 + 1) * nrhs + col] : 0.0;
+  };
+  auto stx = [&](int R, int pi, double a, double b) {
+    const int r0 = R * TB + 8 * pi + 2 * q;
+    if (cok && r0 < nrow) X[(size_t)r0 * nrhs + col] = a;
+    if (cok && r0 + 1 < nrow) X[(size_t)(r0 + 1) * nrhs + col] = b;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < CS_NB; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(full0 + 8u * s));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8u * s), "r"(CS_CWARPS * C));
+    }
+    for (int s = 0; s < NS; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tbar0 + 8u * s));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tfree0 + 8u * s), "r"(CS_CWARPS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < CS_NB && s < total; ++s) cs_arm(full0 + 8u * s, 256u * sizeof(double));
+  }
+  cs_cluster_sync();
+
+  if (w == CS_CWARPS) {
+    // ---------------- producer warp: this CTA's tiles of every step, NS ahead
+    if (lane == 0) {
+      int st = 0;
+      unsigned it = 0;
+      for (int u = 0; u < total; ++u) {
+        if (it > 0) cs_wait(tfree0 + 8u * st, (it - 1) & 1u);
+        const Step s = geom(u);
+        const int nt = (s.t1 <= s.tmax ? (s.tmax - s.t1) / C + 1 : 0) + (s.entry ? 1 : 0);
+        const unsigned bar = tbar0 + 8u * st;
+        cs_arm(bar, (unsigned)(nt * TT * sizeof(double)));
+        const double* T = s.fwd ? job.SF : job.SB;
+        double* dst = stage + (size_t)st * SLT * TT;
+        int i = 0;
+        for (int t = s.t1; t <= s.tmax; t += C, ++i)
+          cs_bulk(dst + (size_t)i * TT, T + ((size_t)s.R * W + t) * TT, bar);
+        if (s.entry) cs_bulk(dst + (size_t)i * TT, T + (size_t)s.Re * W * TT, bar);
+        if (++st == NS) {
+          st = 0;
+          ++it;
+        }
+      }
+    }
+  } else {
+    // ---------------- compute warps: warp w owns piece w of every row
+    unsigned eph = 0u;               // empty-barrier parity per slot
+    auto publish = [&](int u, double a, double b) {      // row of step u is final
+      stx(row_of(u), w, a, b);
+      const int s = u & (CS_NB - 1);
+      if (u >= CS_NB) {
+        cs_wait(empty0 + 8u * s, (eph >> s) & 1u);
+        eph ^= 1u << s;
+      }
+      const unsigned la = ybuf0 + (unsigned)((s * 256 + w * 64 + 2 * lane) * sizeof(double));
+      const unsigned lb = full0 + 8u * s;
+      for (int c = 0; c < C; ++c) cs_st_async(cs_mapa(la, c), a, b, cs_mapa(lb, c));
+    };
+    auto prod = [&](const double* tp, const double (&x)[4][2], double& c0, double& c1) {
+      double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+      for (int kb = 0; kb < 4; kb += 2) {
+        mma_xyt(c0, c1, x[kb][0], x[kb][1], tp[kb * 64], tp[kb * 64 + 1]);
+        mma_xyt(e0, e1, x[kb + 1][0], x[kb + 1][1], tp[(kb + 1) * 64], tp[(kb + 1) * 64 + 1]);
+      }
+      c0 += e0;
+      c1 += e1;
+    };
+    int st = 0;
+    unsigned it = 0;
+    int vs = 0;                      // v % W
+    for (int u = 0; u < total; ++u) {
+      const Step s = geom(u);
+      if (s.v == 0) {
+        // phase prologue: rows of local steps 0..PT enter (Dinv from global);
+        // the first one is final at once
+        vs = 0;
+        asm volatile("bar.sync 1, %0;\n" ::"r"(CS_CWARPS * 32) : "memory");   // phase-1 results visible
+        const double* T = s.fwd ? job.SF : job.SB;
+        for (int vv = 0; vv < W && vv < nV; ++vv) {
+          const int R = s.fwd ? s.R + vv : s.R - vv;
+          if ((R & cm) != k) continue;
+          double bv[4][2], m[4][2];
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            ldx(R, kb, bv[kb][0], bv[kb][1]);
+            m[kb][0] = T[(size_t)R * W * TT + (w * 4 + kb) * 64 + 2 * lane];
+            m[kb][1] = T[(size_t)R * W * TT + (w * 4 + kb) * 64 + 2 * lane + 1];
+          }
+          double c0 = 0.0, c1 = 0.0;
+          double mm[4][2];
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            mm[kb][0] = m[kb][0];
+            mm[kb][1] = m[kb][1];
+          }
+          // acc = M0 b: operands (b^T, M0 pieces)
+          {
+            double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < 4; kb += 2) {
+              mma_xyt(c0, c1, bv[kb][0], bv[kb][1], mm[kb][0], mm[kb][1]);
+              mma_xyt(e0, e1, bv[kb + 1][0], bv[kb + 1][1], mm[kb + 1][0], mm[kb + 1][1]);
+            }
+            c0 += e0;
+            c1 += e1;
+          }
+          if (vv == 0) publish(u, c0, c1);
+          else {
+            ring[(vv * 4 + w) * 64 + 2 * lane] = c0;
+            ring[(vv * 4 + w) * 64 + 2 * lane + 1] = c1;
+          }
+        }
+      }
+      double bv[4][2];
+      if (s.entry) {                                       // in flight during the step
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) ldx(s.Re, kb, bv[kb][0], bv[kb][1]);
+      }
+      cs_wait(tbar0 + 8u * st, it & 1u);
+      const int ys = u & (CS_NB - 1);
+      cs_wait(full0 + 8u * ys, (unsigned)((u >> 2) & 1));
+      double ny[4][2];
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        ny[kb][0] = -ybuf[ys * 256 + kb * 64 + 2 * lane];
+        ny[kb][1] = -ybuf[ys * 256 + kb * 64 + 2 * lane + 1];
+      }
+      if (tid == 0 && u + CS_NB < total) cs_arm(full0 + 8u * ys, 256u * sizeof(double));
+      if (lane == 0 && u + CS_NB < total) {
+        double d = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) d += ny[kb][0] + ny[kb][1];
+        cs_remote_arrive(cs_mapa(empty0 + 8u * ys, row_of(u + CS_NB) & cm), cs_dep(d));
+      }
+      const double* Tst = stage + (size_t)st * SLT * TT + w * 4 * 64 + 2 * lane;
+      int t = s.t1, i = 0;
+      if (t == 1 && t <= s.tmax) {                         // critical: row of step u+1 becomes final
+        const int rs = vs + 1 == W ? 0 : vs + 1;
+        const double* ap = ring + (rs * 4 + w) * 64 + 2 * lane;
+        double c0 = ap[0], c1 = ap[1];
+        prod(Tst, ny, c0, c1);
+        publish(u + 1, c0, c1);
+        t += C;
+        ++i;
+      }
+      for (; t + C <= s.tmax; t += 2 * C, i += 2) {        // two independent tile products
+        int ra = vs + t, rb = vs + t + C;
+        ra -= ra >= W ? W : 0;
+        rb -= rb >= W ? W : 0;
+        double* apa = ring + (ra * 4 + w) * 64 + 2 * lane;
+        double* apb = ring + (rb * 4 + w) * 64 + 2 * lane;
+        double a0 = apa[0], a1 = apa[1], b0 = apb[0], b1 = apb[1];
+        prod(Tst + (size_t)i * TT, ny, a0, a1);
+        prod(Tst + (size_t)(i + 1) * TT, ny, b0, b1);
+        apa[0] = a0;
+        apa[1] = a1;
+        apb[0] = b0;
+        apb[1] = b1;
+      }
+      if (t <= s.tmax) {
+        int ra = vs + t;
+        ra -= ra >= W ? W : 0;
+        double* apa = ring + (ra * 4 + w) * 64 + 2 * lane;
+        double a0 = apa[0], a1 = apa[1];
+        prod(Tst + (size_t)i * TT, ny, a0, a1);
+        apa[0] = a0;
+        apa[1] = a1;
+        ++i;
+      }
+      if (s.entry) {                                       // ring slot of the finished row v
+        double c0 = 0.0, c1 = 0.0;
+        const double* tp = Tst + (size_t)i * TT;
+        double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < 4; kb += 2) {
+          mma_xyt(c0, c1, bv[kb][0], bv[kb][1], tp[kb * 64], tp[kb * 64 + 1]);
+          mma_xyt(e0, e1, bv[kb + 1][0], bv[kb + 1][1], tp[(kb + 1) * 64], tp[(kb + 1) * 64 + 1]);
+        }
+        double* ap = ring + (vs * 4 + w) * 64 + 2 * lane;
+        ap[0] = c0 + e0;
+        ap[1] = c1 + e1;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tfree0 + 8u * st) : "memory");
+      if (++st == NS) {
+        st = 0;
+        ++it;
+      }
+      vs = vs + 1 == W ? 0 : vs + 1;
+    }
+  }
+  cs_cluster_sync();
+}
+
+static cudaError_t launch_cluster_sweeps(const CsJobs& jobs, int njobs, int nrhs, cudaStream_t st) {
+  if (nrhs == 0) return cudaSuccess;
+  CsJobs J = jobs;
+  int ptmax = 0;
+  for (int k = 0; k < njobs; ++k) ptmax = std::max(ptmax, J.j[k].PT);
+  J.groups = (nrhs + 7) / 8;
+  J.C = 1;
+  while (J.C * 2 <= std::min(CS_MAXC, ptmax)) J.C *= 2;      // power of two
+  J.SLT = (ptmax + J.C - 1) / J.C + 1;
+  const size_t fixed = ((size_t)(ptmax + 1) * 256 + CS_NB * 256) * sizeof(double);
+  const size_t stage_b = (size_t)J.SLT * TT * sizeof(double);
+  const size_t budget = 225 * 1024;
+  J.NS = fixed + CS_MAXNS * stage_b <= budget ? CS_MAXNS : 2;
+  const size_t smem = fixed + J.NS * stage_b;
+  if (smem > budget) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_coarse_sweep_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(njobs * J.groups * J.C));
+  cfg.blockDim = dim3(CS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)J.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k_coarse_sweep_cluster, J);
+  count_launches(1);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+static CsJob cs_job(const Band& B, double* X, int nrhs, int J0, int mode) {
+  CsJob s;
+  s.SF = B.SF;
+  s.SB = B.SB;
+  s.X = X;
+  s.NT = B.NT;
+  s.PT = B.PT;
+  s.n = B.n;
+  s.nrhs = nrhs;
+  s.J0 = J0;
+  s.mode = mode;
+  return s;
+}
+
 // ------------------------------------------------------------- launchers
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -1104,7 +1551,8 @@ static cudaError_t launch_factor_job(const FactorJob& job, int* flags, cudaStrea
   if (e != cudaSuccess) return e;
   for (int b = 0; b < job.nb; ++b) {
     k_coarse_pack<<<(unsigned)(job.b[b].NT * (job.b[b].PT + 1)), 256, 0, st>>>(job.b[b]);
-    count_launches(1);
+    k_coarse_pack_scaled<<<(unsigned)(job.b[b].NT * (job.b[b].PT + 1)), 256, 0, st>>>(job.b[b]);
+    count_launches(2);
   }
   return cudaGetLastError();
 }
@@ -1140,6 +1588,15 @@ static SweepJob sweep_job(const Band& B, double* X, int nrhs, int J0, int mode) 
   return s;
 }
 
+static bool cluster_sweeps_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MSFV_CLUSTER_SWEEP");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
 cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
   const Coarse L = coarse_layout(g, Ak);
   FactorJob job{};
@@ -1152,10 +1609,15 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   job.nb = 2;
   cudaError_t e = launch_factor_job(job, flags, st);                // both parts
   if (e != cudaSuccess) return e;
-  SweepJobs zj{};
-  for (int q = 0; q < 2; ++q)                                       // Z_q = L_q^{-1} A_{q,C}
-    zj.j[q] = sweep_job(L.b[q], L.Z[q] - (size_t)L.J0[q] * TB * L.P, L.P, L.J0[q], 1);
-  e = launch_sweeps(zj, 2, L.P, st);
+  if (cluster_sweeps_enabled()) {                                   // Z_q = L_q^{-1} A_{q,C}
+    CsJobs zj{};
+    for (int q = 0; q < 2; ++q) zj.j[q] = cs_job(L.b[q], L.Z[q] - (size_t)L.J0[q] * TB * L.P, L.P, L.J0[q], 1);
+    e = launch_cluster_sweeps(zj, 2, L.P, st);
+  } else {
+    SweepJobs zj{};
+    for (int q = 0; q < 2; ++q) zj.j[q] = sweep_job(L.b[q], L.Z[q] - (size_t)L.J0[q] * TB * L.P, L.P, L.J0[q], 1);
+    e = launch_sweeps(zj, 2, L.P, st);
+  }
   if (e != cudaSuccess) return e;
   const int ntc = L.b[2].NT;
   const int red_bytes = 8 * 16 * 64 * (int)sizeof(double);
@@ -1171,36 +1633,41 @@ cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStrea
   return launch_factor_job(jc, flags, st);
 }
 
+
+// Solve sweeps of one or two bands: cluster-parallel (scaled copies) by
+// default, the one-CTA-per-8-rhs kernel when MSFV_CLUSTER_SWEEP=0.
+static cudaError_t solve_sweeps(const Band* B, double* const* X, int nj, int nrhs, int mode, cudaStream_t st) {
+  if (cluster_sweeps_enabled()) {
+    CsJobs cj{};
+    for (int k = 0; k < nj; ++k) cj.j[k] = cs_job(B[k], X[k], nrhs, 0, mode);
+    return launch_cluster_sweeps(cj, nj, nrhs, st);
+  }
+  SweepJobs sj{};
+  for (int k = 0; k < nj; ++k) sj.j[k] = sweep_job(B[k], X[k], nrhs, 0, mode);
+  return launch_sweeps(sj, nj, nrhs, st);
+}
+
 cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
   const Coarse L = coarse_layout(g, const_cast<double*>(Ak));
-  SweepJobs sj{};
-  if (!L.nd) {
-    sj.j[0] = sweep_job(L.b[0], X, nrhs, 0, 3);
-    return launch_sweeps(sj, 1, nrhs, st);
-  }
+  if (!L.nd) return solve_sweeps(&L.b[0], &X, 1, nrhs, 3, st);
   double* x0 = scratch;
   double* x1 = x0 + (size_t)L.b[0].NT * TB * nrhs;
   double* xc = x1 + (size_t)L.b[1].NT * TB * nrhs;
+  double* xp[2] = {x0, x1};
   const long long tot = (long long)g.kc * nrhs;
   k_coarse_permute<<<nblk(tot, 256), 256, 0, st>>>(g, L, X, x0, x1, xc, nrhs, 0);
   count_launches(1);
-  sj.j[0] = sweep_job(L.b[0], x0, nrhs, 0, 1);
-  sj.j[1] = sweep_job(L.b[1], x1, nrhs, 0, 1);
-  cudaError_t e = launch_sweeps(sj, 2, nrhs, st);                   // y_q = L_q^{-1} b_q
+  cudaError_t e = solve_sweeps(L.b, xp, 2, nrhs, 1, st);             // y_q = L_q^{-1} b_q
   if (e != cudaSuccess) return e;
   k_schur_rhs<<<dim3(nblk(L.P, 8), nblk(nrhs, 8)), 256, 0, st>>>(L, x0, x1, xc, nrhs);
   count_launches(1);
-  SweepJobs cj{};
-  cj.j[0] = sweep_job(L.b[2], xc, nrhs, 0, 3);                      // x_C = S^{-1}(b_C - sum Z^T y)
-  e = launch_sweeps(cj, 1, nrhs, st);
+  e = solve_sweeps(&L.b[2], &xc, 1, nrhs, 3, st);                    // x_C = S^{-1}(b_C - sum Z^T y)
   if (e != cudaSuccess) return e;
   const long long rz = (long long)((L.b[0].NT - L.J0[0]) + (L.b[1].NT - L.J0[1])) * TB;
   k_schur_back<<<dim3(nblk(rz, 8), nblk(nrhs, 8)), 256, 0, st>>>(L, x0, x1, xc, nrhs);  // y_q -= Z_q x_C
   count_launches(1);
-  sj.j[0].mode = 2;
-  sj.j[1].mode = 2;
-  e = launch_sweeps(sj, 2, nrhs, st);                               // x_q = L_q^{-T} y_q
+  e = solve_sweeps(L.b, xp, 2, nrhs, 2, st);                         // x_q = L_q^{-T} y_q
   if (e != cudaSuccess) return e;
   k_coarse_permute<<<nblk(tot, 256), 256, 0, st>>>(g, L, X, x0, x1, xc, nrhs, 1);
   count_launches(1);
