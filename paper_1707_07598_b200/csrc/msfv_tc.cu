@@ -378,7 +378,197 @@ __device__ __forceinline__ void backward_sweep(const Geo& g, const double* __res
 }
 
 
-template <int PT, bool BWD>
+// ---- lean main loop (compile-time stencil tile mask OM: bit o set when tile
+// offset o below the diagonal can hold stencil entries; 0xC3 = {0,1,6,7} for
+// 7x7x7 interiors).  Differences from the generic loop:
+//  * the window slide costs no register moves: every trailing update writes
+//    its result straight into the shifted slot (D != C form of the DMMA);
+//  * the diagonal 8x8 POTRF is predicate-free (rows above the pivot carry
+//    junk in their upper part, never read) with a MUFU-seeded rsqrt and one
+//    cubic correction instead of the library's special-case branches;
+//  * L_JJ^{-1} is a right-looking column solve (chain of 8 FMA+MUL pairs)
+//    over a column-major copy of L in shared memory;
+//  * only the tile offsets in OM are fetched from the stencil table.
+__device__ __forceinline__ void mma_to(F2& d, const F2& c, const F2& a, const F2& b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+      : "=d"(d.x), "=d"(d.y)
+      : "d"(a.x), "d"(b.x), "d"(c.x), "d"(c.y));
+  mma884(d.x, d.y, a.y, b.y);
+}
+// 1/sqrt(d) for a positive normal d: MUFU seed (>= 2^-22) and one cubic
+// Newton-type step y (1 + e/2 + 3e^2/8), e = 1 - d y^2 (relative error ~2^-60
+// before rounding).
+__device__ __forceinline__ double rsq(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double e = fma(-d * y, y, 1.0);
+  const double t = fma(0.375, e, 0.5);
+  return fma(y * e, t, y);
+}
+template <int PT>
+struct TrailPipe2 {
+  F2 (&Wn)[PT + 1][PT + 1];
+  const F2 (&W)[PT + 1][PT + 1];
+  const F2 (&X)[PT + 1];
+  template <int K>
+  __device__ __forceinline__ void at() {
+    constexpr int NP = PT * (PT + 1) / 2 - 1;
+    run<(K * NP) / PIPE_STAGES, ((K + 1) * NP) / PIPE_STAGES>();
+  }
+  template <int LO, int HI>
+  __device__ __forceinline__ void run() {
+    if constexpr (LO < HI) {
+      constexpr int a = tr_a(PT, LO), b = tr_b(PT, LO);
+      mma_to(Wn[a - 1][b - 1], W[a][b], neg(X[a]), X[b]);
+      run<LO + 1, HI>();
+    }
+  }
+};
+template <int C, class P>
+__device__ __forceinline__ void p8_lean(double (&x)[8], bool& bad, double* Is, int lane, P& pipe) {
+  if constexpr (C < 8) {
+    double d = __shfl_sync(FULL, x[C], C);
+    if (!(d > 0.0)) { bad = true; d = 1.0; }
+    const double inv = rsq(d);
+    x[C] *= inv;                      // L(r, C) on rows r >= C (sqrt(d) on r == C)
+    if (lane == 0) Is[C] = inv;
+#pragma unroll
+    for (int q = C + 1; q < 8; ++q) x[q] = fma(-x[C], __shfl_sync(FULL, x[C], q), x[q]);
+    pipe.template at<C + 1>();
+    p8_lean<C + 1>(x, bad, Is, lane, pipe);
+  }
+}
+template <int K, class P>
+__device__ __forceinline__ void inv_lean(double (&acc)[8], const double* Ds, const double* Is, P& pipe) {
+  if constexpr (K < 8) {
+    acc[K] *= Is[K];
+#pragma unroll
+    for (int R = K + 1; R < 8; ++R) acc[R] = fma(-Ds[K * 8 + R], acc[K], acc[R]);
+    pipe.template at<9 + K>();
+    inv_lean<K + 1>(acc, Ds, Is, pipe);
+  }
+}
+// returns L^{-1} (C layout) of the SPD 8x8 tile t (C layout); Ds: 64 doubles,
+// Is: 72 doubles of warp-private shared memory
+template <class P>
+__device__ __forceinline__ F2 potrf_inv8_lean(const F2& t, double* Ds, double* Is, int lane, int* flags, P& pipe) {
+  st2(Ds + lane * 2, t);
+  __syncwarp();
+  const int r = lane & 7;
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double2 v = reinterpret_cast<const double2*>(Ds + r * 8)[k];
+    x[2 * k] = v.x;
+    x[2 * k + 1] = v.y;
+  }
+  pipe.template at<0>();
+  bool bad = false;
+  p8_lean<0>(x, bad, Is, lane, pipe);
+  if (bad && lane == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
+  __syncwarp();
+  if (lane < 8) {                     // column-major copy of L: Ds[q * 8 + r] = L(r, q)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) Ds[q * 8 + r] = x[q];
+  }
+  __syncwarp();
+  // column c = r of L^{-1}, right-looking: z_k = acc_k / L(k,k); acc_R -= L(R,k) z_k
+  double acc[8];
+#pragma unroll
+  for (int R = 0; R < 8; ++R) acc[R] = R == r ? 1.0 : 0.0;
+  inv_lean<0>(acc, Ds, Is, pipe);
+  if (lane < 8) {
+#pragma unroll
+    for (int R = 0; R < 8; ++R) Is[8 + R * 8 + r] = acc[R];
+  }
+  __syncwarp();
+  const F2 li = ld2(Is + 8 + lane * 2);
+  __syncwarp();
+  return li;
+}
+
+struct NoPipe {
+  template <int K>
+  __device__ __forceinline__ void at() {}
+};
+template <int PT, unsigned OM>
+__device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* As, double* Sb, double* LT, int jb,
+                                                    int lane, double* Ds, double* Is, int* flags, F2& G) {
+  const int NTI = (g.nI + 7) >> 3;
+  const int m = lane >> 2, q = lane & 3;
+  // per-lane stencil slots (3 bits each) of element (b, s) of W[PT][b]:
+  // A(i, i - d), d = 8 (PT - b) + m - 2q - s
+  unsigned long long sel = 0;
+#pragma unroll
+  for (int b = 0; b <= PT; ++b)
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      sel |= (unsigned long long)sel_code(g, 8 * (PT - b) + m - 2 * q - s) << (6 * b + 3 * s);
+  auto fetch = [&](int I, int b) -> F2 {
+    const double* row = As + (8 * I + m) * AROW;
+    return {row[(sel >> (6 * b)) & 7u], row[(sel >> (6 * b + 3)) & 7u]};
+  };
+  F2 W[PT + 1][PT + 1];
+  F2 Rt[PT + 1];
+#pragma unroll
+  for (int a = 0; a <= PT; ++a) {
+#pragma unroll
+    for (int b = 0; b <= PT; ++b) {
+      W[a][b] = {0.0, 0.0};
+      if (b <= a && ((OM >> (a - b)) & 1u) && a < NTI) W[a][b] = fetch(a, PT - a + b);
+    }
+    Rt[a] = ld_rt(g, Sb, a, lane);
+  }
+  NoPipe nop;
+  F2 Li = potrf_inv8_lean(W[0][0], Ds, Is, lane, flags, nop);
+#pragma unroll 1
+  for (int J = 0; J < NTI; ++J) {
+    const int In = J + 1 + PT;       // tile row entering the window after this step
+    const F2 nR = In < NTI ? ld_rt(g, Sb, In, lane) : F2{0.0, 0.0};
+    F2 X[PT + 1];
+    double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64 + lane * 2;
+    st2(Lt, Li);
+#pragma unroll
+    for (int t = 1; t <= PT; ++t) {
+      X[t] = {0.0, 0.0};
+      mma(X[t], W[t][0], Li);        // X_t = A_t L^{-T}
+      st2(Lt + t * 64, X[t]);
+    }
+    F2 Wn[PT + 1][PT + 1];
+    F2 Rn[PT + 1];
+    // fused forward substitution of the 8 Lagrange columns (transposed)
+    F2 Yt = {0.0, 0.0};
+    mma(Yt, Rt[0], Li);              // y^T = r^T L^{-T}
+    mma(G, Yt, Yt);
+    {
+      const F2 nY = neg(Yt);
+#pragma unroll
+      for (int t = 1; t <= PT; ++t) mma_to(Rn[t - 1], Rt[t], nY, X[t]);
+    }
+    st_rt(g, Sb, J, lane, Yt);       // y parks in the consumed rhs rows
+    Rn[PT] = nR;
+    if constexpr (PT >= 1) {
+      mma_to(Wn[0][0], W[1][1], neg(X[1]), X[1]);
+      TrailPipe2<PT> pipe{Wn, W, X};
+      if (J + 1 < NTI) {
+        Li = potrf_inv8_lean(Wn[0][0], Ds, Is, lane, flags, pipe);
+      } else {
+        pipe.template run<0, PT * (PT + 1) / 2 - 1>();
+      }
+    }
+#pragma unroll
+    for (int b = 0; b <= PT; ++b)
+      Wn[PT][b] = (In < NTI && ((OM >> (PT - b)) & 1u)) ? fetch(In, b) : F2{0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a <= PT; ++a) {
+#pragma unroll
+      for (int b = 0; b <= a; ++b) W[a][b] = Wn[a][b];
+      Rt[a] = Rn[a];
+    }
+  }
+}
+
+template <int PT, bool BWD, unsigned OM>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
            double* __restrict__ Kloc, int* __restrict__ flags) {
@@ -425,7 +615,14 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
     return {row[(sel >> (6 * b)) & 7u], row[(sel >> (6 * b + 3)) & 7u]};
   };
   F2 G = {0.0, 0.0};                   // sum_J y_J^T y_J  (= R^T S_I, see the Galerkin block)
-  if (NTI > 0) {
+  if constexpr (OM != 0) {
+    if (NTI > 0) {
+      factor_forward_lean<PT, OM>(g, As, Sb, LT, jb, lane, Ds, Is, flags, G);
+      __syncwarp();
+      if constexpr (BWD) backward_sweep<PT>(g, LT, Sb, jb, lane);
+      __syncwarp();
+    }
+  } else if (NTI > 0) {
     F2 W[PT + 1][PT + 1];
     F2 Rt[PT + 1];
 #pragma unroll
@@ -762,20 +959,46 @@ size_t tc_factor_doubles(const Geo& g) {
 }
 size_t tc_scratch_doubles(const Geo&) { return 0; }
 
-template <int PT>
-static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
-                                     double* Kloc, int* flags, bool bwd, cudaStream_t st) {
+template <int PT, unsigned OM>
+static cudaError_t launch_basis_tc_k(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
+                                     int* flags, bool bwd, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
   const size_t nf = 2 * ((size_t)g.ni2 * g.ni3 + (size_t)g.ni1 * g.ni3 + (size_t)g.ni1 * g.ni2);
   const size_t smem = (size_t)TC_WARPS * (((g.nI + 7) / 8) * 8 * AROW + nf) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_basis_tc<PT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(k_basis_tc<PT, true, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_basis_tc<PT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_basis_tc<PT, false, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (bwd)
-    k_basis_tc<PT, true><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, true, OM><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
   else
-    k_basis_tc<PT, false><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, false, OM><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+  return cudaSuccess;
+}
+// lean main loop for 7x7x7 interiors (every 3D BASELINE config: 8^3-cell
+// blocks); MSFV_BASIS_GENERIC=1 forces the generic loop
+static bool use_lean(const Geo& g) {
+  static int gen = -1;
+  if (gen < 0) {
+    const char* e = getenv("MSFV_BASIS_GENERIC");
+    gen = e && atoi(e) ? 1 : 0;
+  }
+  return !gen && g.ni1 == 7 && g.ni2 == 7 && g.ni3 == 7;
+}
+template <int PT>
+static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
+                                     double* Kloc, int* flags, bool bwd, cudaStream_t st) {
+  cudaError_t e;
+  if constexpr (PT == 7) {
+    if (use_lean(g))
+      e = launch_basis_tc_k<7, 0xC3u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    else
+      e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+  } else {
+    e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+  }
+  if (e != cudaSuccess) return e;
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
