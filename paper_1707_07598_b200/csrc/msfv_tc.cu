@@ -487,13 +487,93 @@ __device__ __forceinline__ F2 potrf_inv8_lean(const F2& t, double* Ds, double* I
   return li;
 }
 
+// 1D bulk copy shared -> global (async proxy) for the factor tiles: the
+// registers are free once the tiles are in shared memory (a plain STG keeps
+// its source registers locked until the LSU drains them, which stalled the
+// next step's DMMAs writing the same registers).
+__device__ __forceinline__ void bulk_s2g(double* gdst, const double* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Transposed Lagrange right-hand-side tile I (corner lane/4, rows 8I+2q, +1)
+// evaluated from the face conductances in shared memory, in the summation
+// order of stencil_table (bit-identical to the parked copy in Sint): the
+// first window of the factorization does not wait on a global round trip of
+// the values stencil_table has just stored.
+__device__ __forceinline__ double rhs_value(const Geo& g, const double* Fk, int i, int cc) {
+  if (i >= g.nI) return 0.0;
+  int x, y, z;
+  decode3f(i, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+  ++x; ++y; ++z;
+  const bool cx = cc & 1, cy = cc & 2, cz = cc & 4;
+  const double hx = cx ? hatf1(x - g.b1, g.ib1) : hatf1(x, g.ib1);
+  const double hy = cy ? hatf1(y - g.b2, g.ib2) : hatf1(y, g.ib2);
+  const double hz = cz ? hatf1(z - g.b3, g.ib3) : hatf1(z, g.ib3);
+  const double fx0 = x == 1 ? Fk[face_off(g, 0) + (z - 1) * g.ni2 + (y - 1)] : 0.0;
+  const double fx1 = x == g.ni1 ? Fk[face_off(g, 1) + (z - 1) * g.ni2 + (y - 1)] : 0.0;
+  const double fy0 = y == 1 ? Fk[face_off(g, 2) + (z - 1) * g.ni1 + (x - 1)] : 0.0;
+  const double fy1 = y == g.ni2 ? Fk[face_off(g, 3) + (z - 1) * g.ni1 + (x - 1)] : 0.0;
+  const double fz0 = z == 1 ? Fk[face_off(g, 4) + (y - 1) * g.ni1 + (x - 1)] : 0.0;
+  const double fz1 = z == g.ni3 ? Fk[face_off(g, 5) + (y - 1) * g.ni1 + (x - 1)] : 0.0;
+  double v = 0.0;
+  v += (cx ? 0.0 : fx0) * (hy * hz);
+  v += (cx ? fx1 : 0.0) * (hy * hz);
+  v += (cy ? 0.0 : fy0) * (hx * hz);
+  v += (cy ? fy1 : 0.0) * (hx * hz);
+  v += (cz ? 0.0 : fz0) * (hx * hy);
+  v += (cz ? fz1 : 0.0) * (hx * hy);
+  return v;
+}
+__device__ __forceinline__ F2 rhs_rt(const Geo& g, const double* Fk, int I, int lane) {
+  const int c = lane >> 2, r0 = 8 * I + 2 * (lane & 3);
+  return {rhs_value(g, Fk, r0, c), rhs_value(g, Fk, r0 + 1, c)};
+}
+
+// B = sum over the six boundary faces of k_f h h^T for 7x7 faces: per face
+// row v two DMMAs (u = 1..4 | 5..7, lane slot = u offset), the hats separable
+// (same products as the generic loop, summed in row order).
+__device__ __forceinline__ void galerkin_faces7(const Geo& g, const double* Fk, int lane, F2& K) {
+  const int cc = lane >> 2, slot = lane & 3;
+  const int cx = cc & 1, cy = (cc >> 1) & 1, cz = (cc >> 2) & 1;
+#pragma unroll
+  for (int face = 0; face < 6; ++face) {
+    const int ax = face >> 1, hi = face & 1;
+    const bool on = (ax == 0 ? cx : (ax == 1 ? cy : cz)) == hi;
+    const int cu = ax == 0 ? cy * g.b2 : cx * g.b1, cv = ax == 2 ? cy * g.b2 : cz * g.b3;
+    const double ibu = ax == 0 ? g.ib2 : g.ib1, ibv = ax == 2 ? g.ib2 : g.ib3;
+    const double* F = Fk + 49 * face;
+    const double hu0 = on ? hatf1(1 + slot - cu, ibu) : 0.0;
+    const double hu1 = (on && slot < 3) ? hatf1(5 + slot - cu, ibu) : 0.0;
+#pragma unroll
+    for (int v = 1; v <= 7; ++v) {
+      const double hv = hatf1(v - cv, ibv);
+      const double b0 = hu0 * hv, b1 = hu1 * hv;
+      const double a0 = F[(v - 1) * 7 + slot] * b0;
+      const double a1 = slot < 3 ? F[(v - 1) * 7 + 4 + slot] * b1 : 0.0;
+      mma884(K.x, K.y, a0, b0);
+      mma884(K.x, K.y, a1, b1);
+    }
+  }
+}
+
 struct NoPipe {
   template <int K>
   __device__ __forceinline__ void at() {}
 };
-template <int PT, unsigned OM>
-__device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* As, double* Sb, double* LT, int jb,
-                                                    int lane, double* Ds, double* Is, int* flags, F2& G) {
+template <int PT, unsigned OM, int RF>
+__device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* As, const double* Fk, double* Sb,
+                                                    double* LT, int jb,
+                                                    int lane, double* Ds, double* Is, double* Lst, int* flags,
+                                                    F2& G) {
   const int NTI = (g.nI + 7) >> 3;
   const int m = lane >> 2, q = lane & 3;
   // per-lane stencil slots (3 bits each) of element (b, s) of W[PT][b]:
@@ -517,23 +597,30 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
       W[a][b] = {0.0, 0.0};
       if (b <= a && ((OM >> (a - b)) & 1u) && a < NTI) W[a][b] = fetch(a, PT - a + b);
     }
-    Rt[a] = ld_rt(g, Sb, a, lane);
+    Rt[a] = RF ? rhs_rt(g, Fk, a, lane) : ld_rt(g, Sb, a, lane);
   }
   NoPipe nop;
   F2 Li = potrf_inv8_lean(W[0][0], Ds, Is, lane, flags, nop);
 #pragma unroll 1
   for (int J = 0; J < NTI; ++J) {
     const int In = J + 1 + PT;       // tile row entering the window after this step
-    const F2 nR = In < NTI ? ld_rt(g, Sb, In, lane) : F2{0.0, 0.0};
+    const F2 nR = In < NTI ? (RF == 2 ? rhs_rt(g, Fk, In, lane) : ld_rt(g, Sb, In, lane)) : F2{0.0, 0.0};
     F2 X[PT + 1];
-    double* Lt = LT + ((size_t)jb * NTI + J) * (PT + 1) * 64 + lane * 2;
-    st2(Lt, Li);
+    // factor tiles of this step: staged in shared memory (double buffer),
+    // one bulk copy to LT
+    double* Ls = Lst + (J & 1) * (PT + 1) * 64;
+    if (lane == 0) bulk_wait_read<1>();          // the copy that last read this buffer is done
+    __syncwarp();
+    st2(Ls + lane * 2, Li);
 #pragma unroll
     for (int t = 1; t <= PT; ++t) {
       X[t] = {0.0, 0.0};
       mma(X[t], W[t][0], Li);        // X_t = A_t L^{-T}
-      st2(Lt + t * 64, X[t]);
+      st2(Ls + t * 64 + lane * 2, X[t]);
     }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) bulk_s2g(LT + ((size_t)jb * NTI + J) * (PT + 1) * 64, Ls, (PT + 1) * 64 * sizeof(double));
     F2 Wn[PT + 1][PT + 1];
     F2 Rn[PT + 1];
     // fused forward substitution of the 8 Lagrange columns (transposed)
@@ -566,9 +653,11 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
       Rt[a] = Rn[a];
     }
   }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
 }
 
-template <int PT, bool BWD, unsigned OM>
+template <int PT, bool BWD, unsigned OM, int RF>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
            double* __restrict__ Kloc, int* __restrict__ flags) {
@@ -580,7 +669,8 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   if (jb >= g.nbl) return;
   const int NTI = (g.nI + 7) >> 3, NR = 8 * NTI;
   const int NF = face_off(g, 5) + g.ni1 * g.ni2;
-  double* As = tcsm + (size_t)wid * (NR * AROW + NF);
+  const int AFE = (NR * AROW + NF + 1) & ~1;   // stencil table + face conductances, even
+  double* As = tcsm + (size_t)wid * (AFE + (OM ? 2 * (PT + 1) * 64 : 0));
   double* Fk = As + NR * AROW;
   double* Sb = Sint + (size_t)jb * 8 * g.nI;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
@@ -617,7 +707,8 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   F2 G = {0.0, 0.0};                   // sum_J y_J^T y_J  (= R^T S_I, see the Galerkin block)
   if constexpr (OM != 0) {
     if (NTI > 0) {
-      factor_forward_lean<PT, OM>(g, As, Sb, LT, jb, lane, Ds, Is, flags, G);
+      double* Lst = As + AFE;                    // 2 x (PT + 1) tiles, 16-byte aligned
+      factor_forward_lean<PT, OM, RF>(g, As, Fk, Sb, LT, jb, lane, Ds, Is, Lst, flags, G);
       __syncwarp();
       if constexpr (BWD) backward_sweep<PT>(g, LT, Sb, jb, lane);
       __syncwarp();
@@ -697,6 +788,9 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   const int cc = lane >> 2, slot = lane & 3;
   const int cx = cc & 1, cy = (cc >> 1) & 1, cz = (cc >> 2) & 1;
   F2 K = {0.0, 0.0};
+  if constexpr (OM != 0) {
+    galerkin_faces7(g, Fk, lane, K);
+  } else {
 #pragma unroll 1
   for (int face = 0; face < 6; ++face) {
     const int ax = face >> 1, hi = face & 1;
@@ -720,6 +814,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       u += 4;
       while (u > nu) { u -= nu; ++v; }
     }
+  }
   }
   K.x -= G.x;
   K.y -= G.y;
@@ -796,6 +891,108 @@ __global__ void __launch_bounds__(SKEL_WARPS * 32) k_skel_galerkin(Geo g, const 
         }
       }
     }
+  }
+  double* kl = Kloc + (size_t)jb * 64 + lane * 2;
+  kl[0] += K.x;
+  kl[1] += K.y;
+}
+
+// Skeleton Galerkin by lines: along an owned skeleton line (axis ax,
+// transverse position (u, v)) every hat difference is the same,
+// dH_c = s_c ht_c / b_ax with s_c = +-1 (the hats are linear along the
+// line) and ht_c the transverse hat product, so the line contributes
+// (sum_e w_e / h^2) dH dH^T: the edge weights of a line are summed first and
+// the 8x8 block is a DMMA reduction over lines.  Lines are enumerated as in
+// the edge loop above (v = 0 all u; 0 < v < bq: u in {0, bp (last block)};
+// v = bq (last block) all u).  The pinned node (block 0, first edge of each
+// axis' (0,0) line) has no row of S: that edge is its own record with
+// dH = H(node 1).  Lanes own lines; records go through shared memory.
+// Requires every block extent >= 2 (the edge loop handles extent 1).
+constexpr int SKL_WARPS = 4;
+__host__ __device__ inline int skel_lines_axis(int bp, int bq, int lp, int lq) {
+  return (bp + lp) + (bq - 1) * (1 + lp) + lq * (bp + lp);
+}
+__global__ void __launch_bounds__(SKL_WARPS * 32) k_skel_lines(Geo g, const double* __restrict__ w,
+                                                              double* __restrict__ Kloc, int rec_max) {
+  extern __shared__ __align__(16) double skl[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int jb = blockIdx.x * SKL_WARPS + wid;
+  if (jb >= g.nbl) return;
+  double* ra = skl + (size_t)wid * rec_max * 16;   // record r: a[8] at 16r, b[8] at 16r + 8
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
+  const int lx = bi == g.nb1 - 1, ly = bj == g.nb2 - 1, lz = bk == g.nb3 - 1;
+  const int nl0 = skel_lines_axis(g.b2, g.b3, ly, lz);
+  const int nl1 = skel_lines_axis(g.b1, g.b3, lx, lz);
+  const int nl2 = skel_lines_axis(g.b1, g.b2, lx, ly);
+  const int NL = nl0 + nl1 + nl2, NR = NL + (jb == 0 ? 3 : 0);
+  for (int r = lane; r < NR; r += 32) {
+    int ax, L;
+    if (r < NL) {
+      ax = r < nl0 ? 0 : (r < nl0 + nl1 ? 1 : 2);
+      L = r - (ax == 0 ? 0 : (ax == 1 ? nl0 : nl0 + nl1));
+    } else {
+      ax = r - NL;                                  // pinned-node records
+      L = 0;
+    }
+    const int pa = ax == 0 ? 1 : 0, qa = ax == 2 ? 1 : 2;
+    const int bax = ax == 0 ? g.b1 : (ax == 1 ? g.b2 : g.b3);
+    const int bp = pa == 0 ? g.b1 : g.b2, bq = qa == 1 ? g.b2 : g.b3;
+    const int lp = pa == 0 ? lx : ly;
+    const double ibax = ax == 0 ? g.ib1 : (ax == 1 ? g.ib2 : g.ib3);
+    const double ibp = pa == 0 ? g.ib1 : g.ib2, ibq = qa == 1 ? g.ib2 : g.ib3;
+    const double ihs = ax == 0 ? g.ih1 * g.ih1 : (ax == 1 ? g.ih2 * g.ih2 : g.ih3 * g.ih3);
+    const long long sx = ax == 0 ? 1 : (ax == 1 ? (long long)(g.n1 + 1) : (long long)(g.n1 + 1) * (g.n2 + 1));
+    const int np_ = bp + lp, nU = 1 + lp;
+    int u, v;
+    if (L < np_) {
+      v = 0;
+      u = L;
+    } else if (L < np_ + (bq - 1) * nU) {
+      const int L2 = L - np_;
+      v = 1 + L2 / nU;
+      u = (L2 % nU) ? bp : 0;
+    } else {
+      v = bq;
+      u = L - np_ - (bq - 1) * nU;
+    }
+    int x = 0, y = 0, z = 0;
+    if (ax == 0) { y = u; z = v; } else if (ax == 1) { x = u; z = v; } else { x = u; y = v; }
+    const long long e0 = ax == 0 ? ex_id(g, X0 + x, Y0 + y, Z0 + z)
+                                 : (ax == 1 ? ey_id(g, X0 + x, Y0 + y, Z0 + z) : ez_id(g, X0 + x, Y0 + y, Z0 + z));
+    const bool pin_line = jb == 0 && u == 0 && v == 0;
+    double wsum, scale;
+    if (r < NL) {
+      wsum = 0.0;
+#pragma unroll 8
+      for (int xa = pin_line ? 1 : 0; xa < bax; ++xa) wsum += __ldg(w + e0 + xa * sx);
+      scale = ibax;                                 // |dH| along the line, times s_c below
+    } else {
+      wsum = __ldg(w + e0);
+      scale = 0.0;                                  // pinned edge: H(node 1) (set per corner)
+    }
+    const double wl = wsum * ihs;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cbp = ((pa == 0 ? c & 1 : (c >> 1) & 1)) ? bp : 0;
+      const int cbq = ((qa == 1 ? (c >> 1) & 1 : (c >> 2) & 1)) ? bq : 0;
+      const int cba = (ax == 0 ? c & 1 : (ax == 1 ? (c >> 1) & 1 : (c >> 2) & 1));
+      const double ht = hatf1(u - cbp, ibp) * hatf1(v - cbq, ibq);
+      double d;
+      if (r < NL) d = (cba ? scale : -scale) * ht;
+      else d = hatf1(1 - (cba ? bax : 0), ibax) * ht;
+      ra[16 * r + c] = wl * d;
+      ra[16 * r + 8 + c] = d;
+    }
+  }
+  __syncwarp();
+  const int cc = lane >> 2, slot = lane & 3;
+  F2 K = {0.0, 0.0};
+  for (int r0 = 0; r0 < NR; r0 += 4) {
+    const int r = r0 + slot;
+    const double a = r < NR ? ra[16 * r + cc] : 0.0;
+    const double b = r < NR ? ra[16 * r + 8 + cc] : 0.0;
+    mma884(K.x, K.y, a, b);
   }
   double* kl = Kloc + (size_t)jb * 64 + lane * 2;
   kl[0] += K.x;
@@ -959,40 +1156,45 @@ size_t tc_factor_doubles(const Geo& g) {
 }
 size_t tc_scratch_doubles(const Geo&) { return 0; }
 
-template <int PT, unsigned OM>
+template <int PT, unsigned OM, int RF = 0>
 static cudaError_t launch_basis_tc_k(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                                      int* flags, bool bwd, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
   const size_t nf = 2 * ((size_t)g.ni2 * g.ni3 + (size_t)g.ni1 * g.ni3 + (size_t)g.ni1 * g.ni2);
-  const size_t smem = (size_t)TC_WARPS * (((g.nI + 7) / 8) * 8 * AROW + nf) * sizeof(double);
+  const size_t smem =
+      (size_t)TC_WARPS * (((((g.nI + 7) / 8) * 8 * AROW + nf + 1) & ~(size_t)1) + (OM ? 2 * (PT + 1) * 64 : 0)) *
+      sizeof(double);
   cudaError_t e =
-      cudaFuncSetAttribute(k_basis_tc<PT, true, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_basis_tc<PT, true, OM, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_basis_tc<PT, false, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_basis_tc<PT, false, OM, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (bwd)
-    k_basis_tc<PT, true, OM><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, true, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
   else
-    k_basis_tc<PT, false, OM><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, false, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
   return cudaSuccess;
 }
 // lean main loop for 7x7x7 interiors (every 3D BASELINE config: 8^3-cell
-// blocks); MSFV_BASIS_GENERIC=1 forces the generic loop
-static bool use_lean(const Geo& g) {
-  static int gen = -1;
-  if (gen < 0) {
-    const char* e = getenv("MSFV_BASIS_GENERIC");
-    gen = e && atoi(e) ? 1 : 0;
-  }
-  return !gen && g.ni1 == 7 && g.ni2 == 7 && g.ni3 == 7;
+// blocks); MSFV_BASIS_VARIANT=0 forces the generic loop (1..3: rhs tiles from
+// Sint / first window evaluated in place / all evaluated in place)
+static int basis_variant(const Geo& g) {
+  const char* e = getenv("MSFV_BASIS_VARIANT");
+  const int v = e ? atoi(e) : 1;
+  return g.ni1 == 7 && g.ni2 == 7 && g.ni3 == 7 ? v : 0;
 }
 template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
                                      double* Kloc, int* flags, bool bwd, cudaStream_t st) {
   cudaError_t e;
   if constexpr (PT == 7) {
-    if (use_lean(g))
-      e = launch_basis_tc_k<7, 0xC3u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    const int v = basis_variant(g);
+    if (v == 1)
+      e = launch_basis_tc_k<7, 0xC3u, 0>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    else if (v == 2)
+      e = launch_basis_tc_k<7, 0xC3u, 1>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    else if (v == 3)
+      e = launch_basis_tc_k<7, 0xC3u, 2>(g, w, LT, Sint, Kloc, flags, bwd, st);
     else
       e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st);
   } else {
@@ -1002,7 +1204,17 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_skel_galerkin<<<(unsigned)((g.nbl + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc);
+  if (g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2 && !getenv("MSFV_SKEL_GENERIC")) {
+    const int rec_max = skel_lines_axis(g.b2, g.b3, 1, 1) + skel_lines_axis(g.b1, g.b3, 1, 1) +
+                        skel_lines_axis(g.b1, g.b2, 1, 1) + 3;
+    const size_t sm = (size_t)SKL_WARPS * rec_max * 16 * sizeof(double);
+    if (sm > 48 * 1024) {
+      cudaError_t e2 = cudaFuncSetAttribute(k_skel_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e2 != cudaSuccess) return e2;
+    }
+    k_skel_lines<<<(unsigned)((g.nbl + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, sm, st>>>(g, w, Kloc, rec_max);
+  } else
+    k_skel_galerkin<<<(unsigned)((g.nbl + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc);
   count_launches(1);
   return cudaGetLastError();
 }
