@@ -220,6 +220,76 @@ MSFV_API int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int
 MSFV_API int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
                    const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream);
 
+/* ==== 2D path (BASELINE.json configs 1-2) =================================
+ * The reference package is 3D only; these entry points run the
+ * same adaptive MSFV algorithm with d = 2: cells n1 x n2,
+ * blocks b1 x b2 (>= 2 cells each), bilinear Lagrange hats, x- then y-edges,
+ * C = V/2 per touching cell, node 0 pinned.  Fields are row-major
+ * [pinned node][nrhs] (n = (n1+1)(n2+1) - 1 rows); coarse fields [k][nrhs] in
+ * coarse-node order; edge fields [E][nrhs]; cell fields [n1 n2].
+ *   Sb      [blocks][4 corners][nI]      interior basis values S_I
+ *   factor  [blocks][nI][b1]             band Cholesky of A_II (row, offset)
+ *   Kloc    [blocks][16]                 local Galerkin blocks
+ *   Ab, Lk  [k][k_x + 2]                 lower band of A_k / its factor
+ * Replaces: assemble_operator (operators.py:123-141), assemble_basis
+ * (basis.py:511-616), forward_reduced (forward.py:105-144),
+ * MultiscaleBasis.interior_solve (basis.py:339-353) and the products of
+ * AdaptiveSensitivity (forward.py:224-281). */
+typedef struct msfv2d_plan msfv2d_plan;
+enum msfv2d_info {
+  MSFV2D_INFO_NN = 0,
+  MSFV2D_INFO_N = 1,
+  MSFV2D_INFO_NCELLS = 2,
+  MSFV2D_INFO_NEDGES = 3,
+  MSFV2D_INFO_NBLOCKS = 4,
+  MSFV2D_INFO_NI = 5,
+  MSFV2D_INFO_K = 6,
+  MSFV2D_INFO_FACTOR_DOUBLES = 7,
+  MSFV2D_INFO_BAND_DOUBLES = 8,
+  MSFV2D_INFO_COUNT = 9
+};
+MSFV_API int msfv2d_plan_create(const int32_t* cells, const double* h, const int32_t* blocks, msfv2d_plan** out);
+MSFV_API void msfv2d_plan_destroy(msfv2d_plan* plan);
+MSFV_API int msfv2d_plan_info(const msfv2d_plan* plan, int64_t* info, int32_t n);
+/* sigma = exp(m) (flags |= NONFINITE on non-finite m), w = C sigma   operators.py:23-28,136 */
+MSFV_API int msfv2d_operator(const msfv2d_plan* plan, const double* m, double* sigma, double* w, int32_t* flags,
+                             void* stream);
+/* per-block band Cholesky + 4 Lagrange solves, local Galerkin blocks   basis.py:537-563 */
+MSFV_API int msfv2d_basis(const msfv2d_plan* plan, const double* w, double* factor, double* Sb, double* Kloc,
+                          int32_t* flags, void* stream);
+/* A_k band (+ shift on the diagonal)   forward.py:117-118,123 */
+MSFV_API int msfv2d_galerkin(const msfv2d_plan* plan, const double* Kloc, double shift, double* Ab, void* stream);
+/* band Cholesky of A_k (flags |= COARSE_NOT_SPD)   forward.py:119-129 */
+MSFV_API int msfv2d_coarse_factor(const msfv2d_plan* plan, const double* Ab, double* Lk, int32_t* flags,
+                                  void* stream);
+/* X <- A_k^-1 X (k x nrhs, in place)   forward.py:72-75 */
+MSFV_API int msfv2d_coarse_solve(const msfv2d_plan* plan, const double* Lk, double* X, int32_t nrhs, void* stream);
+/* out = blockdiag(A_II^-1) rhs on interiors, 0 on the skeleton   basis.py:339-353 */
+MSFV_API int msfv2d_interior_solve(const msfv2d_plan* plan, const double* factor, const double* rhs, double* out,
+                                   int32_t nrhs, void* stream);
+/* out = S Y ; out = S^T X ; out = A X ; out = G_p X ; out = G_p^T (a o c) */
+MSFV_API int msfv2d_prolong(const msfv2d_plan* plan, const double* Sb, const double* Y, double* out, int32_t nrhs,
+                            void* stream);
+MSFV_API int msfv2d_restrict(const msfv2d_plan* plan, const double* Sb, const double* X, double* out, int32_t nrhs,
+                             void* stream);
+MSFV_API int msfv2d_apply_A(const msfv2d_plan* plan, const double* w, const double* X, double* out, int32_t nrhs,
+                            void* stream);
+MSFV_API int msfv2d_grad(const msfv2d_plan* plan, const double* X, double* out, int32_t nrhs, void* stream);
+MSFV_API int msfv2d_gradT(const msfv2d_plan* plan, const double* a, const double* c, double* out, int32_t nrhs,
+                          void* stream);
+/* c = C (sigma o dm) ; out = -(C diag sigma)^T sum_s e[:, s]   forward.py:259,281 */
+MSFV_API int msfv2d_edge_average(const msfv2d_plan* plan, const double* sigma, const double* dm, double* c,
+                                 void* stream);
+MSFV_API int msfv2d_cell_adjoint(const msfv2d_plan* plan, const double* sigma, const double* e, double* out,
+                                 int32_t nrhs, void* stream);
+/* out = beta out + M X for a CSR M (int64 row pointer, int32 columns): survey products */
+MSFV_API int msfv2d_spmm(int64_t nrows, const int64_t* ptr, const int32_t* col, const double* val, const double* X,
+                         int32_t nrhs, double beta, double* out, void* stream);
+/* out = alpha a + b ; out = a o b + c o d + e o f (elementwise; b, c..f nullable) */
+MSFV_API int msfv2d_axpby(int64_t n, double alpha, const double* a, const double* b, double* out, void* stream);
+MSFV_API int msfv2d_fma3(int64_t n, const double* a, const double* b, const double* c, const double* d,
+                         const double* e, const double* f, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -287,8 +287,8 @@ class Cache:
     s_perm: np.ndarray = None
 
 
-def build_cache(part, G, C):
-    values = lagrange_values(part)
+def build_cache(part, G, C, values=None):
+    values = lagrange_values(part) if values is None else values
     vcsr = values.tocsr()
     n = part.mesh.n_nodes - 1
     I_l, B_l, cols_l, xb_l = [], [], [], []

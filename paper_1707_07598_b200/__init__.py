@@ -20,6 +20,10 @@ from .inversion import (
     cell_gradient, project_bounds, add_noise, tikhonov_reg, InversionTrace,
 )
 from .table3 import apply_Yk, apply_Xk, apply_Yk_dev, apply_Xk_dev
+from .planar import (
+    Mesh2D, Partition2D, create_mesh_2d, create_partition_2d, AdaptiveReducedProblem2D,
+    ReducedState2D, Sensitivity2D, cell_survey_2d, config_problem_2d,
+)
 from .errors import (
     InvalidModelError, FactorizationError, SolverBreakdown,
     StaleBasisError, ReducedSingularError,

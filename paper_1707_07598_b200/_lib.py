@@ -78,6 +78,26 @@ SIGNATURES = {
     "msfv_xk_present": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_xk_rowcount": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_xk_values": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    # 2D path (BASELINE configs 1-2)
+    "msfv2d_plan_create": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_P)]),
+    "msfv2d_plan_destroy": (None, [_P]),
+    "msfv2d_plan_info": (ctypes.c_int, [_P, _P, _I32]),
+    "msfv2d_operator": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "msfv2d_basis": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "msfv2d_galerkin": (ctypes.c_int, [_P, _P, _D, _P, _P]),
+    "msfv2d_coarse_factor": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "msfv2d_coarse_solve": (ctypes.c_int, [_P, _P, _P, _I32, _P]),
+    "msfv2d_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_prolong": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_restrict": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_apply_A": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_grad": (ctypes.c_int, [_P, _P, _P, _I32, _P]),
+    "msfv2d_gradT": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_edge_average": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "msfv2d_cell_adjoint": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
+    "msfv2d_spmm": (ctypes.c_int, [_I64, _P, _P, _P, _P, _I32, _D, _P, _P]),
+    "msfv2d_axpby": (ctypes.c_int, [_I64, _D, _P, _P, _P, _P]),
+    "msfv2d_fma3": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _LIB = None

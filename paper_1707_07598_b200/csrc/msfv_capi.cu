@@ -68,6 +68,9 @@ static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+namespace msfv {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace msfv
 static int cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return MSFV_OK;
   return fail(MSFV_CUDA, std::string(what) + ": " + cudaGetErrorString(e));

@@ -1,5 +1,6 @@
 // Internal launcher declarations (not part of the public C-ABI).
 #pragma once
+#include <string>
 #include <cuda_runtime.h>
 #include "msfv_common.cuh"
 
@@ -20,6 +21,8 @@ constexpr int FLAG_LOCAL_NOT_SPD = 4;
 constexpr int FLAG_COARSE_NOT_SPD = 8;
 
 void count_launches(long long n);
+// record msg as msfv_last_error() and return code (msfv_capi.cu)
+int set_error(int code, const std::string& msg);
 long long launch_count();
 
 size_t basis_smem_bytes(const Geo& g);
