@@ -141,6 +141,53 @@ __device__ void band_solve(const double* L, int nI, int p, double* X, int nr) {
     __syncthreads();
   }
 }
+// Same solve, one warp per right-hand-side column (half band p <= 31): lane r
+// keeps row j + r (forward) / j - r (backward) of the column in a register
+// window that slides by one shuffle per pivot, so a pivot costs one
+// broadcast, one FMA and one shift instead of two CTA barriers.
+// rinv[j] = 1 / L(j, j).
+__device__ void band_solve_warp(const double* __restrict__ L, const double* __restrict__ rinv, int nI, int p,
+                                double* __restrict__ X, int nr) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P1 = p + 1;
+  for (int s = wid; s < nr; s += nw) {
+    // forward: the entering row and 1/L(j,j) are prefetched one pivot ahead
+    double v = (lane <= p && lane < nI) ? X[lane * nr + s] : 0.0;
+    double nx = (lane == p && p + 1 < nI) ? X[(p + 1) * nr + s] : 0.0;
+    double ri = rinv[0];
+    for (int j = 0; j < nI; ++j) {
+      const double nx2 = (lane == p && j + 2 + p < nI) ? X[(j + 2 + p) * nr + s] : 0.0;
+      const double ri2 = j + 1 < nI ? rinv[j + 1] : 0.0;
+      const double lv = (lane >= 1 && lane <= p && j + lane < nI) ? L[(j + lane) * P1 + lane] : 0.0;
+      const double x = __shfl_sync(FULL, v, 0) * ri;
+      if (lane == 0) X[j * nr + s] = x;
+      v = fma(-lv, x, v);
+      v = __shfl_down_sync(FULL, v, 1);
+      if (lane == p) v = nx;
+      nx = nx2;
+      ri = ri2;
+    }
+    __syncwarp();
+    v = (lane <= p && nI - 1 - lane >= 0) ? X[(nI - 1 - lane) * nr + s] : 0.0;
+    nx = (lane == p && nI - 2 - p >= 0) ? X[(nI - 2 - p) * nr + s] : 0.0;
+    ri = rinv[nI - 1];
+    for (int j = nI - 1; j >= 0; --j) {
+      const double nx2 = (lane == p && j - 2 - p >= 0) ? X[(j - 2 - p) * nr + s] : 0.0;
+      const double ri2 = j >= 1 ? rinv[j - 1] : 0.0;
+      const double lv = (lane >= 1 && lane <= p && j - lane >= 0) ? L[j * P1 + lane] : 0.0;
+      const double x = __shfl_sync(FULL, v, 0) * ri;
+      if (lane == 0) X[j * nr + s] = x;
+      v = fma(-lv, x, v);
+      v = __shfl_down_sync(FULL, v, 1);
+      if (lane == p) v = nx;
+      nx = nx2;
+      ri = ri2;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
 __device__ void fill_pairs(short2* tab, int p) {
   for (int t = threadIdx.x; t < p * (p + 1) / 2; t += blockDim.x) {
     int r = 1, rem = t;
@@ -161,7 +208,8 @@ __global__ void __launch_bounds__(B2_THREADS) k2_basis(G2 g, const double* __res
   const int nI = g.nI, p = g.p, P1 = p + 1;
   double* L = sm2;                    // nI * P1
   double* X = L + nI * P1;            // nI * 4
-  double* sinv = X + nI * 4;
+  double* rinv = X + nI * 4;          // nI
+  double* sinv = rinv + nI;
   short2* tab = reinterpret_cast<short2*>(sinv + 2);
   const int bi = blk % g.nb1, bj = blk / g.nb1, X0 = bi * g.b1, Y0 = bj * g.b2;
   fill_pairs(tab, p);
@@ -187,7 +235,12 @@ __global__ void __launch_bounds__(B2_THREADS) k2_basis(G2 g, const double* __res
   }
   __syncthreads();
   band_potrf(L, nI, p, tab, flags, sinv);
-  band_solve(L, nI, p, X, 4);
+  for (int a = threadIdx.x; a < nI; a += blockDim.x) rinv[a] = 1.0 / L[a * P1];
+  __syncthreads();
+  if (p <= 31)
+    band_solve_warp(L, rinv, nI, p, X, 4);
+  else
+    band_solve(L, nI, p, X, 4);
   for (int t = threadIdx.x; t < nI * P1; t += blockDim.x) fac[(size_t)blk * nI * P1 + t] = L[t];
   for (int t = threadIdx.x; t < nI * 4; t += blockDim.x) {
     const int a = t >> 2, c = t & 3;
@@ -197,7 +250,7 @@ __global__ void __launch_bounds__(B2_THREADS) k2_basis(G2 g, const double* __res
 
 // blockdiag(A_II^-1) on the interior rows of a node field (nr columns);
 // skeleton rows of `out` are zeroed (basis.py:339-353)
-__global__ void __launch_bounds__(B2_THREADS) k2_interior_solve(G2 g, const double* __restrict__ fac,
+__global__ void __launch_bounds__(512) k2_interior_solve(G2 g, const double* __restrict__ fac,
                                                                const double* __restrict__ rhs,
                                                                double* __restrict__ out, int nr) {
   extern __shared__ __align__(16) double sm2[];
@@ -205,6 +258,7 @@ __global__ void __launch_bounds__(B2_THREADS) k2_interior_solve(G2 g, const doub
   const int nI = g.nI, P1 = g.p + 1;
   double* L = sm2;
   double* X = L + nI * P1;
+  double* rinv = X + nI * nr;
   const int bi = blk % g.nb1, bj = blk / g.nb1, X0 = bi * g.b1, Y0 = bj * g.b2;
   for (int t = threadIdx.x; t < nI * P1; t += blockDim.x) L[t] = fac[(size_t)blk * nI * P1 + t];
   for (int t = threadIdx.x; t < nI * nr; t += blockDim.x) {
@@ -213,7 +267,12 @@ __global__ void __launch_bounds__(B2_THREADS) k2_interior_solve(G2 g, const doub
     X[t] = rhs[node * nr + s];
   }
   __syncthreads();
-  band_solve(L, nI, g.p, X, nr);
+  for (int a = threadIdx.x; a < nI; a += blockDim.x) rinv[a] = 1.0 / L[a * P1];
+  __syncthreads();
+  if (g.p <= 31)
+    band_solve_warp(L, rinv, nI, g.p, X, nr);
+  else
+    band_solve(L, nI, g.p, X, nr);
   for (int t = threadIdx.x; t < nI * nr; t += blockDim.x) {
     const int a = t / nr, s = t % nr;
     const long long node = nid(g, X0 + 1 + a % g.ni1, Y0 + 1 + a / g.ni1) - 1;
@@ -349,10 +408,16 @@ __global__ void k2_coarse_solve(G2 g, const double* __restrict__ Lk, double* __r
   const int P1 = g.pc + 1;
   double* L = sm2;
   double* Y = L + (size_t)g.kc * P1;
+  double* rinv = Y + (size_t)g.kc * nr;
   for (int t = threadIdx.x; t < g.kc * P1; t += blockDim.x) L[t] = Lk[t];
   for (int t = threadIdx.x; t < g.kc * nr; t += blockDim.x) Y[t] = X[t];
   __syncthreads();
-  band_solve(L, g.kc, g.pc, Y, nr);
+  for (int a = threadIdx.x; a < g.kc; a += blockDim.x) rinv[a] = 1.0 / L[a * P1];
+  __syncthreads();
+  if (g.pc <= 31)
+    band_solve_warp(L, rinv, g.kc, g.pc, Y, nr);
+  else
+    band_solve(L, g.kc, g.pc, Y, nr);
   for (int t = threadIdx.x; t < g.kc * nr; t += blockDim.x) X[t] = Y[t];
 }
 
@@ -378,15 +443,18 @@ __global__ void k2_prolong(G2 g, const double* __restrict__ Sb, const double* __
 // out[c][s] = sum_i S(i, c) X[i][s] over the support of column c, ascending node order
 __global__ void k2_restrict(G2 g, const double* __restrict__ Sb, const double* __restrict__ X,
                             double* __restrict__ out, int nr) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= (long long)g.kc * nr) return;
   const int c = (int)(t / nr), s = (int)(t % nr);
   const int cx = c % g.kx, cy = c / g.kx;
   const int i0 = max(cx * g.b1 - g.b1 + 1, 0), i1 = min(cx * g.b1 + g.b1 - 1, g.n1);
   const int j0 = max(cy * g.b2 - g.b2 + 1, 0), j1 = min(cy * g.b2 + g.b2 - 1, g.n2);
+  const int wi = i1 - i0 + 1, tot = wi * (j1 - j0 + 1);
   double v = 0.0;
-  for (int j = j0; j <= j1; ++j)
-    for (int i = i0; i <= i1; ++i) {
+  for (int q = lane; q < tot; q += 32) {
+    const int i = i0 + q % wi, j = j0 + q / wi;
+    {
       if (i == 0 && j == 0) continue;
       // the block of c's support holding (i, j) (on a shared line either works)
       const int bi = i < cx * g.b1 ? cx - 1 : (i > cx * g.b1 ? cx : (cx < g.nb1 ? cx : cx - 1));
@@ -395,7 +463,10 @@ __global__ void k2_restrict(G2 g, const double* __restrict__ Sb, const double* _
       const double sv = sval(g, Sb, bi, bj, lc, i, j);
       if (sv != 0.0) v += sv * X[(nid(g, i, j) - 1) * nr + s];
     }
-  out[t] = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) out[t] = v;
 }
 // out = A X (pinned node fields): sum over the 4 incident edges of k (x_n - x_m)
 __global__ void k2_apply_A(G2 g, const double* __restrict__ w, const double* __restrict__ X, double* __restrict__ out,
@@ -534,7 +605,7 @@ struct msfv2d_plan {
 namespace {
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 size_t basis_smem(const G2& g) {
-  return ((size_t)g.nI * (g.p + 1) + (size_t)g.nI * 4 + 2) * sizeof(double) +
+  return ((size_t)g.nI * (g.p + 1) + (size_t)g.nI * 5 + 2) * sizeof(double) +
          (size_t)(g.p * (g.p + 1) / 2 + 2) * sizeof(short2);
 }
 size_t coarse_smem(const G2& g, int nr) {
@@ -654,10 +725,10 @@ MSFV_API int msfv2d_coarse_factor(const msfv2d_plan* p, const double* Ab, double
 MSFV_API int msfv2d_coarse_solve(const msfv2d_plan* p, const double* Lk, double* X, int32_t nrhs, void* stream) {
   if (!p || nrhs < 1) return msfv::set_error(MSFV_SHAPE, "null plan / nrhs");
   const G2& g = p->g;
-  const size_t sm = ((size_t)g.kc * (g.pc + 1) + (size_t)g.kc * nrhs) * sizeof(double);
+  const size_t sm = ((size_t)g.kc * (g.pc + 2) + (size_t)g.kc * nrhs) * sizeof(double);
   int rc = smem_attr((const void*)k2_coarse_solve, sm, "2d coarse solve");
   if (rc) return rc;
-  k2_coarse_solve<<<1, 256, sm, (cudaStream_t)stream>>>(g, Lk, X, nrhs);
+  k2_coarse_solve<<<1, 512, sm, (cudaStream_t)stream>>>(g, Lk, X, nrhs);
   return launched("2d coarse solve");
 }
 MSFV_API int msfv2d_interior_solve(const msfv2d_plan* p, const double* factor, const double* rhs, double* out,
@@ -665,11 +736,11 @@ MSFV_API int msfv2d_interior_solve(const msfv2d_plan* p, const double* factor, c
   if (!p || nrhs < 1) return msfv::set_error(MSFV_SHAPE, "null plan / nrhs");
   const G2& g = p->g;
   auto st = (cudaStream_t)stream;
-  const size_t sm = ((size_t)g.nI * (g.p + 1) + (size_t)g.nI * nrhs) * sizeof(double);
+  const size_t sm = ((size_t)g.nI * (g.p + 2) + (size_t)g.nI * nrhs) * sizeof(double);
   int rc = smem_attr((const void*)k2_interior_solve, sm, "2d interior solve");
   if (rc) return rc;
   k2_zero_skeleton<<<nblk(g.n * nrhs), 256, 0, st>>>(g, out, nrhs);
-  k2_interior_solve<<<g.nbl, B2_THREADS, sm, st>>>(g, factor, rhs, out, nrhs);
+  k2_interior_solve<<<g.nbl, 512, sm, st>>>(g, factor, rhs, out, nrhs);
   return launched("2d interior solve", 2);
 }
 MSFV_API int msfv2d_prolong(const msfv2d_plan* p, const double* Sb, const double* Y, double* out, int32_t nrhs,
@@ -681,7 +752,7 @@ MSFV_API int msfv2d_prolong(const msfv2d_plan* p, const double* Sb, const double
 MSFV_API int msfv2d_restrict(const msfv2d_plan* p, const double* Sb, const double* X, double* out, int32_t nrhs,
                              void* stream) {
   if (!p) return msfv::set_error(MSFV_SHAPE, "null plan");
-  k2_restrict<<<nblk((long long)p->g.kc * nrhs, 64), 64, 0, (cudaStream_t)stream>>>(p->g, Sb, X, out, nrhs);
+  k2_restrict<<<nblk((long long)p->g.kc * nrhs * 32, 128), 128, 0, (cudaStream_t)stream>>>(p->g, Sb, X, out, nrhs);
   return launched("2d restrict");
 }
 MSFV_API int msfv2d_apply_A(const msfv2d_plan* p, const double* w, const double* X, double* out, int32_t nrhs,
