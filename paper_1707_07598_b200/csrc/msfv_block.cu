@@ -62,6 +62,36 @@ __global__ void k_edge_weights(Geo g, const double* __restrict__ cv, double* __r
   w[e] = sum;
 }
 
+// Same sums on a line grid: blockIdx.z = axis, blockIdx.y = the edge line
+// (the two transverse indices), threads along x, so there is no index
+// division and the four cell loads of a warp are coalesced rows.
+constexpr int EW_THREADS = 128;
+__global__ void __launch_bounds__(EW_THREADS) k_edge_weights_lines(Geo g, const double* __restrict__ cv,
+                                                                  double* __restrict__ w) {
+  const int ax = blockIdx.z;
+  const int nx = ax == 0 ? g.n1 : g.n1 + 1;                  // edges along x in a line
+  const int ny = ax == 1 ? g.n2 : g.n2 + 1;                  // lines per z plane
+  const int i = blockIdx.x * EW_THREADS + threadIdx.x;
+  if (i >= nx) return;
+  const int j = blockIdx.y % ny, k = blockIdx.y / ny;
+  if (k >= (ax == 2 ? g.n3 : g.n3 + 1)) return;
+  const long long e = (ax == 0 ? 0 : (ax == 1 ? g.Ex : g.Ex + g.Ey)) + i + (long long)nx * (j + (long long)ny * k);
+  double sum = 0.0;
+#pragma unroll
+  for (int d2 = -1; d2 <= 0; ++d2) {
+#pragma unroll
+    for (int d1 = -1; d1 <= 0; ++d1) {
+      int ci = i, cj = j, ck = k;
+      if (ax == 0) { cj += d1; ck += d2; }
+      else if (ax == 1) { ci += d1; ck += d2; }
+      else { ci += d1; cj += d2; }
+      if (ci < 0 || cj < 0 || ck < 0 || ci >= g.n1 || cj >= g.n2 || ck >= g.n3) continue;
+      sum = __dadd_rn(sum, __dmul_rn(g.qv, __ldg(cv + cell_id(g, ci, cj, ck))));
+    }
+  }
+  w[e] = sum;
+}
+
 // ------------------------------------------------------------------ basis
 
 // Closed-box edge weights of a block, staged in shared memory.
@@ -687,7 +717,13 @@ cudaError_t launch_mul(long long n, const double* a, const double* b, double* ou
   return cudaGetLastError();
 }
 cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st) {
-  k_edge_weights<<<nblk(g.E, 256), 256, 0, st>>>(g, cv, w);
+  const unsigned lines = (unsigned)((long long)(g.n2 + 1) * (g.n3 + 1));
+  if (lines < 65535u) {
+    const dim3 grid(nblk(g.n1 + 1, EW_THREADS), lines, 3);
+    k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w);
+  } else {
+    k_edge_weights<<<nblk(g.E, 256), 256, 0, st>>>(g, cv, w);
+  }
   count_launches(1);
   return cudaGetLastError();
 }
