@@ -182,6 +182,13 @@ MSFV_API int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points
 MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
                         const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
                         const msfv_points* pr, const double* Rc, double* g, void* stream);
+/* Same, for the blocks of the z-slab bk0 <= bk < bk1 only (they own the cells
+ * with bk0*b3 <= k < bk1*b3, a contiguous range of g): lets the host copy
+ * finished slabs of g back while the next slab is computed. */
+MSFV_API int msfv_block_gradient_slab(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
+                             const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
+                             const msfv_points* pr, const double* Rc, int32_t bk0, int32_t bk1, double* g,
+                             void* stream);
 /* Coarse right-hand side of J v for surveys without interior receivers
  * (forward.py:258-269): out = xdm - S^T(gdm + A ydm) = -EP^T((G U + G R) o c)
  * with U = S T, R the compact interior field of pr (NULL: none) and c = Csig dm

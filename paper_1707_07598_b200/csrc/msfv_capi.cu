@@ -491,6 +491,22 @@ int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double
                     "block_gradient");
 }
 
+int msfv_block_gradient_slab(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
+                             const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
+                             const msfv_points* pr, const double* Rc, int32_t bk0, int32_t bk1, double* g,
+                             void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& gg = plan->g;
+  if (nrhs < 0 || bk0 < 0 || bk1 > gg.nb3 || bk0 > bk1) return fail(MSFV_SHAPE, "bad gradient slab arguments");
+  if (!grad_supported(gg, nrhs)) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
+  const bool hz = pz && pz->d.nib > 0 && Zc, hr = pr && pr->d.nib > 0 && Rc;
+  const int per = gg.nb1 * gg.nb2;
+  return cuda_check(launch_grad_block(gg, Sint, T, y, nrhs, sigma, hz ? pz->d.islot : nullptr, Zc,
+                                      hr ? pr->d.islot : nullptr, Rc, g, (cudaStream_t)stream, bk0 * per,
+                                      (bk1 - bk0) * per),
+                    "block_gradient_slab");
+}
+
 int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
                        const msfv_points* pr, const double* Rc, double* part, double* out, void* stream) {
   CHECK_PLAN(plan);

@@ -60,9 +60,9 @@ size_t grad_smem_doubles(const Geo& g, int nrhs) {
 __global__ void __launch_bounds__(GRAD_THREADS)
 k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ T, const double* __restrict__ Y,
              int nrhs, const double* __restrict__ sigma, const int* __restrict__ zslot, const double* __restrict__ Zc,
-             const int* __restrict__ rslot, const double* __restrict__ Rc, double* __restrict__ gout) {
+             const int* __restrict__ rslot, const double* __restrict__ Rc, double* __restrict__ gout, int jb0) {
   extern __shared__ __align__(16) double gsm[];
-  const int jb = blockIdx.x, tid = threadIdx.x;
+  const int jb = jb0 + blockIdx.x, tid = threadIdx.x;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
   const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
@@ -330,11 +330,13 @@ bool grad_supported(const Geo& g, int nrhs) { return grad_smem_doubles(g, nrhs) 
 
 cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T, const double* Y, int nrhs,
                               const double* sigma, const int* zslot, const double* Zc, const int* rslot,
-                              const double* Rc, double* gout, cudaStream_t st) {
+                              const double* Rc, double* gout, cudaStream_t st, int jb0, int nb) {
   const size_t smem = grad_smem_doubles(g, nrhs) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_grad_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_grad_block<<<g.nbl, GRAD_THREADS, smem, st>>>(g, Sint, T, Y, nrhs, sigma, zslot, Zc, rslot, Rc, gout);
+  if (nb < 0) nb = g.nbl - jb0;
+  if (nb <= 0) return cudaSuccess;
+  k_grad_block<<<nb, GRAD_THREADS, smem, st>>>(g, Sint, T, Y, nrhs, sigma, zslot, Zc, rslot, Rc, gout, jb0);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -105,7 +105,7 @@ size_t grad_smem_doubles(const Geo& g, int nrhs);
 bool grad_supported(const Geo& g, int nrhs);
 cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T, const double* Y, int nrhs,
                               const double* sigma, const int* zslot, const double* Zc, const int* rslot,
-                              const double* Rc, double* gout, cudaStream_t st);
+                              const double* Rc, double* gout, cudaStream_t st, int jb0 = 0, int nb = -1);
 size_t jv_smem_doubles(const Geo& g, int nrhs);
 cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec, const double* T, int nrhs,
                             const int* rslot, const double* Rc, double* part, cudaStream_t st);

@@ -320,6 +320,42 @@ class Engine:
                        "block_gradient")
         return g
 
+    def block_gradient_to_host(self, sigma, Sint, T, y, pz=None, Zc=None, pr=None, Rc=None, chunks=4):
+        """block_gradient with the result copied to a page-locked host array
+        slab by slab: the copy of slab i runs on a side stream while slab
+        i + 1 is computed.  Returns the numpy view of the host buffer."""
+        nrhs = T.shape[1]
+        g = self.empty(self.Nm)
+        host = torch.empty(self.Nm, dtype=F64, pin_memory=True)
+        nb3 = self.cells[2] // self.blocks[2]
+        cur = torch.cuda.current_stream()
+        cp = self.copy_stream
+        bounds = [round(i * nb3 / chunks) for i in range(chunks + 1)]
+        per_slab = self.Nm // nb3
+        with phase("block_gradient"):
+            for c in range(chunks):
+                b0, b1 = bounds[c], bounds[c + 1]
+                if b1 <= b0:
+                    continue
+                _lib.check(self.L.msfv_block_gradient_slab(
+                    self.plan, ptr(sigma), ptr(Sint), ptr(T), ptr(y), nrhs, None if pz is None else pz.handle,
+                    ptr(Zc), None if pr is None else pr.handle, ptr(Rc), b0, b1, ptr(g), stream()),
+                    "block_gradient_slab")
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                cp.wait_event(ev)
+                with torch.cuda.stream(cp):
+                    host[b0 * per_slab:b1 * per_slab].copy_(g[b0 * per_slab:b1 * per_slab], non_blocking=True)
+        g.record_stream(cp)
+        cp.synchronize()
+        return host.numpy()
+
+    @property
+    def copy_stream(self):
+        if getattr(self, "_copy", None) is None:
+            self._copy = torch.cuda.Stream(device=self.device)
+        return self._copy
+
     def jv_coarse_rhs(self, Sint, c, T, pr=None, Rc=None):
         """-EP^T((G U + G R) o c) on the coarse nodes (k x nrhs); raises
         NotImplementedError when the block closure does not fit in shared memory."""

@@ -282,7 +282,17 @@ class AdaptiveSensitivity:
 
     def rapply(self, W):
         W = np.asarray(W, dtype=float) if not hasattr(W, "detach") else W
-        return _host(self.rapply_dev(W))
+        eng, b = self.engine, self.basis
+        ns = self.survey.n_sources
+        Wd = eng.to_device(W)
+        y = eng.restrict_points(self.Pp, b.sint_for(self.Pp), Wd, ns)
+        eng.coarse_solve(self.state.Lk, y)
+        Zc = eng.interior_fields(self.Pp, b.factor, Wd, ns)
+        try:
+            # fused gradient, copied back slab by slab behind the computation
+            return eng.block_gradient_to_host(self.sigma, b.Sint, self.state.T_dev, y, self.Pp, Zc, self.Qp, self.Rc)
+        except NotImplementedError:
+            return _host(self.rapply_dev(W))
 
 
 def sensitivity_adaptive(state, survey, workers=1):
