@@ -128,7 +128,8 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   {
     // coarse nested dissection: on for k >= 1000 (MSFV_COARSE_ND=0/1 overrides)
     const char* ev = getenv("MSFV_COARSE_ND");
-    g.coarse_nd = ev ? (atoi(ev) != 0) : (g.kc >= 1000);
+    g.coarse_nd = ev ? std::min(2, std::max(0, atoi(ev))) : (g.kc >= 1000 ? 1 : 0);
+    g.mf = nullptr;
     g.skel = nullptr;
     g.nskel = 0;
   }
@@ -136,6 +137,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
+  if (g.coarse_nd == 2) mf_attach(g);
   msfv_plan* pl = new msfv_plan;
   pl->g = g;
   *out = pl;
@@ -145,6 +147,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
 void msfv_plan_destroy(msfv_plan* plan) {
   if (!plan) return;
   if (plan->skel_dev) cudaFree(plan->skel_dev);
+  mf_release(plan->g);
   delete plan;
 }
 

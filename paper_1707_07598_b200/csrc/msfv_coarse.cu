@@ -42,6 +42,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <array>
+#include <vector>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 
@@ -141,14 +144,18 @@ __device__ __forceinline__ void coarse_map(const Coarse& L, int c, int& part, in
   else { part = 2; local = w; }
 }
 
-size_t coarse_doubles(const Geo& g) { return coarse_layout(g, nullptr).total; }
+size_t mf_doubles(const Geo& g);
+int mf_tile_rows(const Geo& g);
+size_t coarse_doubles(const Geo& g) { return g.coarse_nd == 2 ? mf_doubles(g) : coarse_layout(g, nullptr).total; }
 size_t coarse_scratch_doubles(const Geo& g, int nrhs) {
+  if (g.coarse_nd == 2) return (size_t)mf_tile_rows(g) * TB * nrhs;
   const Coarse L = coarse_layout(g, nullptr);
   size_t rows = 0;
   for (int b = 0; b < L.nb; ++b) rows += (size_t)L.b[b].NT * TB;
   return rows * nrhs;
 }
 int coarse_tile_rows(const Geo& g) {
+  if (g.coarse_nd == 2) return mf_tile_rows(g);
   const Coarse L = coarse_layout(g, nullptr);
   int r = 0;
   for (int b = 0; b < L.nb; ++b) r += L.b[b].NT;
@@ -1502,7 +1509,15 @@ static CsJob cs_job(const Band& B, double* X, int nrhs, int J0, int mode) {
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+cudaError_t launch_mf_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
+cudaError_t launch_mf_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st);
+cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st);
+cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st);
+size_t mf_doubles(const Geo& g);
+int mf_tile_rows(const Geo& g);
+
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st) {
+  if (g.coarse_nd == 2) return launch_mf_assemble(g, Kloc, shift, Ak, st);
   const Coarse L = coarse_layout(g, Ak);
   for (int b = 0; b < L.nb; ++b) {
     cudaError_t e = cudaMemsetAsync(L.b[b].A, 0, (size_t)L.b[b].NT * (L.b[b].PT + 1) * TT * sizeof(double), st);
@@ -1520,6 +1535,7 @@ cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shif
 }
 
 cudaError_t launch_coarse_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st) {
+  if (g.coarse_nd == 2) return launch_mf_diag(g, Ak, diag, st);
   k_coarse_diag<<<nblk(g.kc, 256), 256, 0, st>>>(g, coarse_layout(g, const_cast<double*>(Ak)), diag);
   count_launches(1);
   return cudaGetLastError();
@@ -1598,6 +1614,7 @@ static bool cluster_sweeps_enabled() {
 }
 
 cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
+  if (g.coarse_nd == 2) return launch_mf_factor(g, Ak, flags, st);
   const Coarse L = coarse_layout(g, Ak);
   FactorJob job{};
   job.b[0] = L.b[0];
@@ -1649,6 +1666,7 @@ static cudaError_t solve_sweeps(const Band* B, double* const* X, int nj, int nrh
 
 cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
+  if (g.coarse_nd == 2) return launch_mf_solve(g, Ak, X, scratch, nrhs, st);
   const Coarse L = coarse_layout(g, const_cast<double*>(Ak));
   if (!L.nd) return solve_sweeps(&L.b[0], &X, 1, nrhs, 3, st);
   double* x0 = scratch;
@@ -1673,5 +1691,804 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
   count_launches(1);
   return cudaGetLastError();
 }
+
+
+// ============================================================================
+// Multifrontal nested dissection of the coarse system (coarse_nd == 2).
+//
+// The coarse grid (kx x ky x kz nodes, 27-point stencil) is dissected
+// recursively: a box is split by the coordinate plane through the middle of
+// its longest extent; boxes of <= MF_LEAF nodes are leaves.  A tree node
+// eliminates E (its separator plane, or the whole leaf box); its front is
+// [E | B], B = the nodes of ancestor separators adjacent to its box, each part
+// padded to whole 32-row tiles (E padding = identity, B padding = 0).  Fronts
+// are dense bands of full width (PT = NT - 1), so the tile-task Cholesky of
+// the banded path factors them unchanged: the first NE tile columns are
+// eliminated, the trailing tiles are left holding the update matrix
+// U = F_BB - L_BE L_BE^T, which the parent extend-adds.  All fronts of one
+// tree level are factored in one cooperative launch (grid barrier per tile
+// column), the sequential depth is the sum over levels of NE instead of the
+// band's NT (config 4: 23 tile columns instead of 73 + 10).  Solves walk the
+// levels up (y_E = L_EE^-1 v_E, v_B -= L_BE y_E) and down
+// (x_E = L_EE^-T (y_E - L_BE^T x_B)); contributions move between fronts by
+// gathers through host-built index maps, so every sum has a fixed order.
+// ============================================================================
+
+constexpr int MF_LEAF = 64;
+constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
+
+struct MfFront {
+  int nE, nB, NE, NT;     // real E / B sizes, tile counts (NT = NE + ceil(nB/TB))
+  long long aoff;         // band storage offset (A, Dinv, Lo)
+  long long voff;         // solve workspace row offset
+  int c[2];               // children (-1: none)
+  int goff;               // gid table offset (NT*TB entries, -1 = padding)
+  int moff[2];            // child maps (NT*TB entries: child-local row or -1)
+};
+
+struct MfPlan {
+  std::vector<MfFront> fr;
+  std::vector<int> lvl, lvl_off;     // fronts per level (leaves first), CSR offsets
+  std::vector<int> gid, maps;
+  size_t a27 = 0, total = 0, vrows = 0;
+  int maxNT = 0;
+  // device copies (uploaded on first use)
+  MfFront* d_fr = nullptr;
+  int* d_lvl = nullptr;
+  int* d_gid = nullptr;
+  int* d_maps = nullptr;
+};
+
+__host__ __device__ __forceinline__ Band mf_band(double* base, const MfFront& f) {
+  Band B{};
+  B.n = f.NT * TB;
+  B.NT = f.NT;
+  B.PT = f.NT - 1;
+  const size_t bt = (size_t)f.NT * f.NT * TT;
+  B.A = base + f.aoff;
+  B.Dinv = B.A + bt;
+  B.Lo = B.Dinv + (size_t)f.NT * TT;
+  B.LF = B.LB = B.SF = B.SB = nullptr;
+  return B;
+}
+
+static void mf_dissect(MfPlan& P, int kx, int ky, int kz, int lo[3], int hi[3], std::vector<int>& anc_seps,
+                       std::vector<std::vector<int>>& Elist, std::vector<std::vector<int>>& Blist,
+                       std::vector<int>& height, std::vector<std::array<int, 2>>& kids, int& out_id) {
+  auto id = [&](int x, int y, int z) { return x + kx * (y + ky * z); };
+  const int ext[3] = {hi[0] - lo[0] + 1, hi[1] - lo[1] + 1, hi[2] - lo[2] + 1};
+  const long long vol = (long long)ext[0] * ext[1] * ext[2];
+  std::vector<int> E;
+  std::array<int, 2> ch = {-1, -1};
+  int h = 0;
+  if (vol <= MF_LEAF || (ext[0] < 3 && ext[1] < 3 && ext[2] < 3)) {
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) E.push_back(id(x, y, z));
+  } else {
+    int ax = 2;
+    if (ext[1] > ext[ax]) ax = 1;
+    if (ext[0] > ext[ax]) ax = 0;
+    const int mid = (lo[ax] + hi[ax]) / 2;
+    int slo[3] = {lo[0], lo[1], lo[2]}, shi[3] = {hi[0], hi[1], hi[2]};
+    slo[ax] = shi[ax] = mid;
+    for (int z = slo[2]; z <= shi[2]; ++z)
+      for (int y = slo[1]; y <= shi[1]; ++y)
+        for (int x = slo[0]; x <= shi[0]; ++x) E.push_back(id(x, y, z));
+    // the separator's own nodes are ancestors of both halves
+    const size_t mark = anc_seps.size();
+    anc_seps.insert(anc_seps.end(), E.begin(), E.end());
+    for (int side = 0; side < 2; ++side) {
+      int clo[3] = {lo[0], lo[1], lo[2]}, chi[3] = {hi[0], hi[1], hi[2]};
+      if (side == 0) chi[ax] = mid - 1; else clo[ax] = mid + 1;
+      if (clo[ax] > chi[ax]) continue;
+      int cid;
+      mf_dissect(P, kx, ky, kz, clo, chi, anc_seps, Elist, Blist, height, kids, cid);
+      ch[side] = cid;
+      h = std::max(h, height[cid] + 1);
+    }
+    anc_seps.resize(mark);
+  }
+  // B: ancestor separator nodes adjacent (27-point) to the box
+  std::vector<int> B;
+  for (int u : anc_seps) {
+    const int x = u % kx, y = (u / kx) % ky, z = u / (kx * ky);
+    if (x >= lo[0] - 1 && x <= hi[0] + 1 && y >= lo[1] - 1 && y <= hi[1] + 1 && z >= lo[2] - 1 && z <= hi[2] + 1)
+      B.push_back(u);
+  }
+  out_id = (int)Elist.size();
+  Elist.push_back(E);
+  Blist.push_back(B);
+  height.push_back(h);
+  kids.push_back(ch);
+}
+
+static MfPlan* mf_build(const Geo& g) {
+  auto* P = new MfPlan;
+  const int kx = g.nb1 + 1, ky = g.nb2 + 1, kz = g.nb3 + 1;
+  std::vector<std::vector<int>> Elist, Blist;
+  std::vector<int> height, anc;
+  std::vector<std::array<int, 2>> kids;
+  int lo[3] = {0, 0, 0}, hi[3] = {kx - 1, ky - 1, kz - 1}, root;
+  mf_dissect(*P, kx, ky, kz, lo, hi, anc, Elist, Blist, height, kids, root);
+  const int nf = (int)Elist.size();     // postorder: children before parents
+  // B in elimination order (ancestor fronts come later in postorder; within a
+  // front E is lexicographic)
+  std::vector<int> pos(g.kc, -1);
+  {
+    int p = 0;
+    for (int f = 0; f < nf; ++f)
+      for (int u : Elist[f]) pos[u] = p++;
+  }
+  for (auto& B : Blist) std::sort(B.begin(), B.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+  P->fr.resize(nf);
+  size_t aoff = 0, voff = 0;
+  for (int f = 0; f < nf; ++f) {
+    MfFront& F = P->fr[f];
+    F.nE = (int)Elist[f].size();
+    F.nB = (int)Blist[f].size();
+    F.NE = (F.nE + TB - 1) / TB;
+    F.NT = F.NE + (F.nB + TB - 1) / TB;
+    F.aoff = (long long)aoff;
+    aoff += (size_t)F.NT * F.NT * TT * 2 + (size_t)F.NT * TT;
+    F.voff = (long long)voff;
+    voff += (size_t)F.NT * TB;
+    F.c[0] = kids[f][0];
+    F.c[1] = kids[f][1];
+    P->maxNT = std::max(P->maxNT, F.NT);
+    F.goff = (int)P->gid.size();
+    for (int r = 0; r < F.NT * TB; ++r) {
+      int v = -1;
+      if (r < F.NE * TB) { if (r < F.nE) v = Elist[f][r]; }
+      else if (r - F.NE * TB < F.nB) v = Blist[f][r - F.NE * TB];
+      P->gid.push_back(v);
+    }
+  }
+  for (int f = 0; f < nf; ++f) {
+    MfFront& F = P->fr[f];
+    for (int s = 0; s < 2; ++s) {
+      F.moff[s] = -1;
+      const int c = F.c[s];
+      if (c < 0) continue;
+      const MfFront& C = P->fr[c];
+      std::vector<int> where(g.kc, -1);       // node -> child-local row of the child's B part
+      for (int i = 0; i < C.nB; ++i) where[Blist[c][i]] = C.NE * TB + i;
+      F.moff[s] = (int)P->maps.size();
+      for (int r = 0; r < F.NT * TB; ++r) {
+        const int u = P->gid[F.goff + r];
+        P->maps.push_back(u >= 0 ? where[u] : -1);
+      }
+    }
+  }
+  // levels by height (leaves = 0)
+  int hmax = 0;
+  for (int f = 0; f < nf; ++f) hmax = std::max(hmax, height[f]);
+  P->lvl_off.push_back(0);
+  for (int h = 0; h <= hmax; ++h) {
+    for (int f = 0; f < nf; ++f)
+      if (height[f] == h) P->lvl.push_back(f);
+    P->lvl_off.push_back((int)P->lvl.size());
+  }
+  P->a27 = aoff;
+  P->total = aoff + (size_t)g.kc * 14;
+  P->vrows = voff;
+  if (getenv("MSFV_MF_DEBUG")) {
+    for (size_t l = 0; l + 1 < P->lvl_off.size(); ++l) {
+      int ne = 0, nt = 0, nemax = 0;
+      for (int i = P->lvl_off[l]; i < P->lvl_off[l + 1]; ++i) {
+        ne += P->fr[P->lvl[i]].nE;
+        nt = std::max(nt, P->fr[P->lvl[i]].NT);
+        nemax = std::max(nemax, P->fr[P->lvl[i]].NE);
+      }
+      fprintf(stderr, "mf level %zu: %d fronts, sum nE %d, max NE %d tiles, max NT %d tiles\n", l,
+              P->lvl_off[l + 1] - P->lvl_off[l], ne, nemax, nt);
+    }
+  }
+  return P;
+}
+
+static const MfPlan* mf_plan(const Geo& g) { return static_cast<const MfPlan*>(g.mf); }
+
+static cudaError_t mf_upload(const Geo& g) {
+  MfPlan* P = const_cast<MfPlan*>(mf_plan(g));
+  if (P->d_fr) return cudaSuccess;
+  cudaError_t e = cudaMalloc(&P->d_fr, P->fr.size() * sizeof(MfFront));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_lvl, P->lvl.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_gid, P->gid.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_maps, std::max<size_t>(P->maps.size(), 1) * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_fr, P->fr.data(), P->fr.size() * sizeof(MfFront), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_lvl, P->lvl.data(), P->lvl.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_gid, P->gid.data(), P->gid.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !P->maps.empty())
+    e = cudaMemcpy(P->d_maps, P->maps.data(), P->maps.size() * sizeof(int), cudaMemcpyHostToDevice);
+  return e;
+}
+
+void mf_release(Geo& g) {
+  auto* P = const_cast<MfPlan*>(mf_plan(g));
+  if (!P) return;
+  if (P->d_fr) cudaFree(P->d_fr);
+  if (P->d_lvl) cudaFree(P->d_lvl);
+  if (P->d_gid) cudaFree(P->d_gid);
+  if (P->d_maps) cudaFree(P->d_maps);
+  delete P;
+  g.mf = nullptr;
+}
+void mf_attach(Geo& g) { g.mf = mf_build(g); }
+
+struct MfDev {
+  const MfFront* fr;
+  const int* lvl;
+  const int* gid;
+  const int* maps;
+  double* base;
+};
+
+// A27[c][o]: the 14 lexicographically lower stencil entries of row c
+__global__ void k_mf_a27(Geo g, const double* __restrict__ Kloc, double shift, double* __restrict__ A27) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)g.kc * 14) return;
+  const int o = (int)(t % 14), c = (int)(t / 14);
+  int c2;
+  double v;
+  A27[t] = coarse_entry(g, Kloc, shift, c, o, c2, v) ? v : 0.0;
+}
+__device__ __forceinline__ double mf_a(const Geo& g, const double* __restrict__ A27, int a, int b) {
+  const int c = max(a, b), c2 = min(a, b);
+  const int kx = g.nb1 + 1, ky = g.nb2 + 1;
+  const int dx = c2 % kx - c % kx, dy = (c2 / kx) % ky - (c / kx) % ky, dz = c2 / (kx * ky) - c / (kx * ky);
+  if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) return 0.0;
+  int o;
+  if (dz == -1) o = (dy + 1) * 3 + (dx + 1);
+  else if (dz == 0 && dy == -1) o = 9 + dx + 1;
+  else o = 12 + dx + 1;
+  return A27[(size_t)c * 14 + o];
+}
+// U element (r, c) (child-local, both in the child's B part) of a factored child
+__device__ __forceinline__ double mf_u(const Band& C, int r, int c) {
+  const int a = max(r, c), b = min(r, c);
+  return btile(C.A, C, b / TB, a / TB - b / TB)[(a % TB) * TB + (b % TB)];
+}
+// Front assembly of the fronts lvl[l0 .. l0 + gridDim.y): original entries with
+// a row or column in E, plus the children's update matrices (gathers).
+__global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__ A27) {
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.y]];
+  const Band B = mf_band(d.base, F);
+  const long long ntile = (long long)F.NT * F.NT;
+  const int* gid = d.gid + F.goff;
+  Band C0{}, C1{};
+  if (F.c[0] >= 0) C0 = mf_band(d.base, d.fr[F.c[0]]);
+  if (F.c[1] >= 0) C1 = mf_band(d.base, d.fr[F.c[1]]);
+  const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntile * TT;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int tile = (int)(t / TT), e = (int)(t % TT);
+    const int J = tile / F.NT, tt = tile % F.NT;
+    if (J + tt >= F.NT) continue;
+    const int r = (J + tt) * TB + e / TB, c = J * TB + e % TB;
+    const int gr = gid[r], gc = gid[c];
+    double v = 0.0;
+    if (gr < 0 || gc < 0) {
+      v = (r == c && r < F.NE * TB) ? 1.0 : 0.0;
+    } else {
+      if (r < F.nE || c < F.nE) v = mf_a(g, A27, gr, gc);
+      if (m0) {
+        const int a = m0[r], b = m0[c];
+        if (a >= 0 && b >= 0) v += mf_u(C0, a, b);
+      }
+      if (m1) {
+        const int a = m1[r], b = m1[c];
+        if (a >= 0 && b >= 0) v += mf_u(C1, a, b);
+      }
+    }
+    btile(B.A, B, J, tt)[e] = v;
+  }
+}
+
+// Partial Cholesky (first NE tile columns) of all fronts of one level, one
+// grid barrier per tile column: CTA f (< nf) factors front f's diagonal tiles
+// (one-column lookahead), the other CTAs take the trailing tile tasks of all
+// fronts in one index space.
+struct MfJob {
+  MfDev d;
+  int l0, nf, jmax;
+};
+constexpr int MF_MAXF = 1024;
+__global__ void __launch_bounds__(256, 1) k_mf_factor(MfJob job, int* __restrict__ flags) {
+  __shared__ __align__(16) FactorSmem sm;
+  __shared__ int pre[MF_MAXF + 1];
+  cg::grid_group grid = cg::this_grid();
+  const int nf = job.nf, G = (int)gridDim.x;
+  const bool split = nf < G;
+  auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
+  for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
+  grid.sync();
+  const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
+  for (int J = 0; J < job.jmax; ++J) {
+    for (int i = blockIdx.x; i < nf && (split ? blockIdx.x < nf : true); i += G) {
+      const MfFront F = front(i);
+      if (J + 1 < F.NE) {
+        const Band B = mf_band(job.d.base, F);
+        load_tile(sm.D, B.Dinv + (size_t)J * TT);
+        __syncthreads();
+        coarse_task(B, J, 0, sm, true);
+        coarse_potrf(B, J + 1, flags, sm, true);
+      }
+    }
+    if (me >= 0) {
+      // prefix of the task counts (each CTA builds the same table)
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const MfFront F = front(i);
+        int n = 0;
+        if (J < F.NE) {
+          const int pt = F.NT - 1 - J;
+          const int first = (pt >= 1 && J + 1 < F.NE) ? 1 : 0;
+          n = pt >= 1 ? pt * (pt + 1) / 2 - first : 0;
+        }
+        pre[i + 1] = n;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pre[0] = 0;
+        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+      }
+      __syncthreads();
+      const int total = pre[nf];
+      int loaded = -1, fi = 0;
+      for (int gi = me; gi < total; gi += nw) {
+        while (pre[fi + 1] <= gi) ++fi;
+        const MfFront F = front(fi);
+        const Band B = mf_band(job.d.base, F);
+        const int first = (J + 1 < F.NE) ? 1 : 0;
+        if (loaded != fi) {
+          load_tile(sm.D, B.Dinv + (size_t)J * TT);
+          __syncthreads();
+          loaded = fi;
+        }
+        coarse_task(B, J, first + (gi - pre[fi]), sm);
+      }
+    }
+    grid.sync();
+  }
+}
+
+// Forward solve of the fronts of one level, CTA per front:
+// v = [X(E) ; 0] + children's v_B (gathers), y_J = Dinv_J v_J,
+// v_I -= L_{I,J} y_J; V keeps y_E and the update v_B for the parent.
+__global__ void __launch_bounds__(256) k_mf_fwd(MfDev d, int l0, const double* __restrict__ X, double* __restrict__ V,
+                                                int nrhs) {
+  extern __shared__ __align__(16) double ys[];     // TB x nrhs
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  double* v = V + (size_t)F.voff * nrhs;
+  const int rows = F.NT * TB;
+  const double* v0 = F.c[0] >= 0 ? V + (size_t)d.fr[F.c[0]].voff * nrhs : nullptr;
+  const double* v1 = F.c[1] >= 0 ? V + (size_t)d.fr[F.c[1]].voff * nrhs : nullptr;
+  const int* m0 = v0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = v1 ? d.maps + F.moff[1] : nullptr;
+  for (int t = threadIdx.x; t < rows * nrhs; t += blockDim.x) {
+    const int r = t / nrhs, s = t % nrhs;
+    double a = (r < F.nE) ? X[(size_t)gid[r] * nrhs + s] : 0.0;
+    if (m0 && m0[r] >= 0) a += v0[(size_t)m0[r] * nrhs + s];
+    if (m1 && m1[r] >= 0) a += v1[(size_t)m1[r] * nrhs + s];
+    v[t] = a;
+  }
+  __syncthreads();
+  for (int J = 0; J < F.NE; ++J) {
+    const double* Di = B.Dinv + (size_t)J * TT;
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int i = t / nrhs, s = t % nrhs;
+      double a = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < TB; ++k) a += Di[i * TB + k] * v[(size_t)(J * TB + k) * nrhs + s];
+      ys[t] = a;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) v[(size_t)J * TB * nrhs + t] = ys[t];
+    for (int t = threadIdx.x; t < (F.NT - 1 - J) * TB * nrhs; t += blockDim.x) {
+      const int rr = t / nrhs, s = t % nrhs, I = J + 1 + rr / TB, i = rr % TB;
+      const double* Lt = btile(B.Lo, B, J, I - J) + i * TB;
+      double a = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < TB; ++k) a += Lt[k] * ys[k * nrhs + s];
+      v[(size_t)(I * TB + i) * nrhs + s] -= a;
+    }
+    __syncthreads();
+  }
+}
+// Backward solve, CTA per front (levels root first): x_B from X (solved
+// ancestors), x_J = Dinv_J^T (y_J - sum_{I>J} L_{I,J}^T x_I), x_E -> X.
+__global__ void __launch_bounds__(256) k_mf_bwd(MfDev d, int l0, double* __restrict__ X, double* __restrict__ V,
+                                                int nrhs) {
+  extern __shared__ __align__(16) double ys[];     // TB x nrhs
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  double* v = V + (size_t)F.voff * nrhs;
+  for (int t = threadIdx.x; t < (F.NT - F.NE) * TB * nrhs; t += blockDim.x) {
+    const int r = F.NE * TB + t / nrhs, s = t % nrhs;
+    v[(size_t)r * nrhs + s] = gid[r] >= 0 ? X[(size_t)gid[r] * nrhs + s] : 0.0;
+  }
+  __syncthreads();
+  for (int J = F.NE - 1; J >= 0; --J) {
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int j = t / nrhs, s = t % nrhs;
+      double a = v[(size_t)(J * TB + j) * nrhs + s];
+      for (int I = J + 1; I < F.NT; ++I) {
+        const double* Lt = btile(B.Lo, B, J, I - J);
+#pragma unroll 8
+        for (int i = 0; i < TB; ++i) a -= Lt[i * TB + j] * v[(size_t)(I * TB + i) * nrhs + s];
+      }
+      ys[t] = a;
+    }
+    __syncthreads();
+    const double* Di = B.Dinv + (size_t)J * TT;
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int j = t / nrhs, s = t % nrhs;
+      double a = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < TB; ++k) a += Di[k * TB + j] * ys[k * nrhs + s];
+      v[(size_t)(J * TB + j) * nrhs + s] = a;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < F.nE * nrhs; t += blockDim.x) {
+    const int r = t / nrhs, s = t % nrhs;
+    X[(size_t)gid[r] * nrhs + s] = v[t];
+  }
+}
+
+// Shared-memory versions (the front vector, Dinv_J and L's tile column J
+// staged per step; coalesced tile loads, no global round trips in the dot
+// products).  smem: V rows*nrhs + (NT-1) tiles + 1 tile + TB*nrhs.
+// Dinv_J and L's tile column J (contiguous) arrive by two bulk copies on one
+// mbarrier (issued by thread 0; the caller waits on the returned phase).
+__device__ __forceinline__ void mf_stage_tma(double* Dj, double* Ls, const Band& B, int J, int nb,
+                                             unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    const unsigned bd = TT * sizeof(double), bl = (unsigned)nb * TT * sizeof(double);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bd + bl)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(Dj)),
+                 "l"(B.Dinv + (size_t)J * TT), "r"(bd), "r"(smem_u32(bar))
+                 : "memory");
+    if (nb > 0)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       smem_u32(Ls)),
+                   "l"(btile(B.Lo, B, J, 1)), "r"(bl), "r"(smem_u32(bar))
+                   : "memory");
+  }
+}
+__global__ void __launch_bounds__(256) k_mf_fwd_s(MfDev d, int l0, const double* __restrict__ X,
+                                                  double* __restrict__ Vg, int nrhs, int ntmax) {
+  extern __shared__ __align__(16) double sh[];
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  const int rows = F.NT * TB;
+  double* V = sh;                                   // rows x nrhs
+  double* Ls = V + (size_t)ntmax * TB * nrhs;       // (NT-1) tiles
+  double* Dj = Ls + (size_t)(ntmax - 1) * TT;       // 1 tile
+  double* ys = Dj + TT;                             // TB x nrhs
+  const bool pairs = !(nrhs & 1) && nrhs <= 64 && (int)blockDim.x % (nrhs >> 1) == 0;
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  unsigned phase = 0;
+  const double* v0 = F.c[0] >= 0 ? Vg + (size_t)d.fr[F.c[0]].voff * nrhs : nullptr;
+  const double* v1 = F.c[1] >= 0 ? Vg + (size_t)d.fr[F.c[1]].voff * nrhs : nullptr;
+  const int* m0 = v0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = v1 ? d.maps + F.moff[1] : nullptr;
+  // gather indices first (coalesced), then the values with several loads in
+  // flight per thread
+  int* ix = reinterpret_cast<int*>(ys + TB * nrhs);   // 3 x rows
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    ix[r] = r < F.nE ? gid[r] : -1;
+    ix[rows + r] = m0 ? m0[r] : -1;
+    ix[2 * rows + r] = m1 ? m1[r] : -1;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int t = threadIdx.x; t < rows * nrhs; t += blockDim.x) {
+    const int r = t / nrhs, s = t % nrhs;
+    const int a0 = ix[r], a1 = ix[rows + r], a2 = ix[2 * rows + r];
+    double a = a0 >= 0 ? __ldcg(X + (size_t)a0 * nrhs + s) : 0.0;
+    if (a1 >= 0) a += __ldcg(v0 + (size_t)a1 * nrhs + s);
+    if (a2 >= 0) a += __ldcg(v1 + (size_t)a2 * nrhs + s);
+    V[t] = a;
+  }
+  __syncthreads();
+  for (int J = 0; J < F.NE; ++J) {
+    const int nb = F.NT - 1 - J;
+    mf_stage_tma(Dj, Ls, B, J, nb, &bar);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    if (pairs) {
+      // 2 rows x 2 right-hand sides per thread, double2 shared loads
+      const int ncp = nrhs >> 1, cp = threadIdx.x % ncp, rp = threadIdx.x / ncp, rstep = 2 * (blockDim.x / ncp);
+      const double* vJ = V + (size_t)J * TB * nrhs;
+      for (int r0 = 2 * rp; r0 < TB; r0 += rstep) {
+        double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll
+        for (int k = 0; k < TB; k += 2) {
+          const double2 l0 = *reinterpret_cast<const double2*>(Dj + r0 * TB + k);
+          const double2 l1 = *reinterpret_cast<const double2*>(Dj + (r0 + 1) * TB + k);
+          const double2 y0 = *reinterpret_cast<const double2*>(vJ + k * nrhs + 2 * cp);
+          const double2 y1 = *reinterpret_cast<const double2*>(vJ + (k + 1) * nrhs + 2 * cp);
+          a00 = fma(l0.x, y0.x, fma(l0.y, y1.x, a00));
+          a01 = fma(l0.x, y0.y, fma(l0.y, y1.y, a01));
+          a10 = fma(l1.x, y0.x, fma(l1.y, y1.x, a10));
+          a11 = fma(l1.x, y0.y, fma(l1.y, y1.y, a11));
+        }
+        *reinterpret_cast<double2*>(ys + r0 * nrhs + 2 * cp) = make_double2(a00, a01);
+        *reinterpret_cast<double2*>(ys + (r0 + 1) * nrhs + 2 * cp) = make_double2(a10, a11);
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) V[(size_t)J * TB * nrhs + t] = ys[t];
+      double* vN = V + (size_t)(J + 1) * TB * nrhs;
+      for (int r0 = 2 * rp; r0 < nb * TB; r0 += rstep) {
+        double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll
+        for (int k = 0; k < TB; k += 2) {
+          const double2 l0 = *reinterpret_cast<const double2*>(Ls + (size_t)r0 * TB + k);
+          const double2 l1 = *reinterpret_cast<const double2*>(Ls + (size_t)(r0 + 1) * TB + k);
+          const double2 y0 = *reinterpret_cast<const double2*>(ys + k * nrhs + 2 * cp);
+          const double2 y1 = *reinterpret_cast<const double2*>(ys + (k + 1) * nrhs + 2 * cp);
+          a00 = fma(l0.x, y0.x, fma(l0.y, y1.x, a00));
+          a01 = fma(l0.x, y0.y, fma(l0.y, y1.y, a01));
+          a10 = fma(l1.x, y0.x, fma(l1.y, y1.x, a10));
+          a11 = fma(l1.x, y0.y, fma(l1.y, y1.y, a11));
+        }
+        double2* o0 = reinterpret_cast<double2*>(vN + (size_t)r0 * nrhs + 2 * cp);
+        double2* o1 = reinterpret_cast<double2*>(vN + (size_t)(r0 + 1) * nrhs + 2 * cp);
+        const double2 p0 = *o0, p1 = *o1;
+        *o0 = make_double2(p0.x - a00, p0.y - a01);
+        *o1 = make_double2(p1.x - a10, p1.y - a11);
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int i = t / nrhs, s = t % nrhs;
+      const double* vj = V + (size_t)J * TB * nrhs + s;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; k += 2) {
+        a = fma(Dj[i * TB + k], vj[k * nrhs], a);
+        b = fma(Dj[i * TB + k + 1], vj[(k + 1) * nrhs], b);
+      }
+      ys[t] = a + b;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) V[(size_t)J * TB * nrhs + t] = ys[t];
+    for (int t = threadIdx.x; t < nb * TB * nrhs; t += blockDim.x) {
+      const int rr = t / nrhs, s = t % nrhs;
+      const double* Lr = Ls + (size_t)rr * TB;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; k += 2) {
+        a = fma(Lr[k], ys[k * nrhs + s], a);
+        b = fma(Lr[k + 1], ys[(k + 1) * nrhs + s], b);
+      }
+      V[(size_t)((J + 1) * TB + rr) * nrhs + s] -= a + b;
+    }
+    __syncthreads();
+  }
+  double* v = Vg + (size_t)F.voff * nrhs;
+  for (int t = threadIdx.x; t < rows * nrhs; t += blockDim.x) v[t] = V[t];
+}
+__global__ void __launch_bounds__(256) k_mf_bwd_s(MfDev d, int l0, double* __restrict__ X, const double* __restrict__ Vg,
+                                                  int nrhs, int ntmax) {
+  extern __shared__ __align__(16) double sh[];
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  const int rows = F.NT * TB;
+  double* V = sh;
+  double* Ls = V + (size_t)ntmax * TB * nrhs;
+  double* Dj = Ls + (size_t)(ntmax - 1) * TT;
+  double* ys = Dj + TT;
+  const bool pairs = !(nrhs & 1) && nrhs <= 64 && ((int)blockDim.x / 2) % (nrhs >> 1) == 0;
+  double* ps = ys + TB * nrhs + (3 * ntmax * TB + 1) / 2;   // 2 x TB x nrhs partial sums (after ix)
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  unsigned phase = 0;
+  const double* v = Vg + (size_t)F.voff * nrhs;
+  int* ix = reinterpret_cast<int*>(ys + TB * nrhs);
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) ix[r] = gid[r];
+  __syncthreads();
+#pragma unroll 4
+  for (int t = threadIdx.x; t < rows * nrhs; t += blockDim.x) {
+    const int r = t / nrhs, s = t % nrhs;
+    const int a0 = ix[r];
+    V[t] = r < F.NE * TB ? __ldcg(v + t) : (a0 >= 0 ? __ldcg(X + (size_t)a0 * nrhs + s) : 0.0);
+  }
+  __syncthreads();
+  for (int J = F.NE - 1; J >= 0; --J) {
+    const int nb = F.NT - 1 - J;
+    mf_stage_tma(Dj, Ls, B, J, nb, &bar);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    if (pairs) {
+      // r = y_J - L^T x: 2 columns x 2 right-hand sides per thread, the
+      // row sum split over the two thread halves (partials through Dj's
+      // neighbour buffer ps), then x_J = Dinv_J^T r
+      const int ncp = nrhs >> 1, half = blockDim.x / 2, th = threadIdx.x % half, hs = threadIdx.x / half;
+      const int cp = th % ncp, jp = th / ncp, jstep = 2 * (half / ncp);
+      const double* vb = V + (size_t)(J + 1) * TB * nrhs;
+      const int R = nb * TB, r0 = hs ? R / 2 : 0, r1 = hs ? R : R / 2;
+      for (int j0 = 2 * jp; j0 < TB; j0 += jstep) {
+        double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+        for (int rr = r0; rr < r1; ++rr) {
+          const double2 l = *reinterpret_cast<const double2*>(Ls + (size_t)rr * TB + j0);
+          const double2 x = *reinterpret_cast<const double2*>(vb + (size_t)rr * nrhs + 2 * cp);
+          a00 = fma(l.x, x.x, a00);
+          a01 = fma(l.x, x.y, a01);
+          a10 = fma(l.y, x.x, a10);
+          a11 = fma(l.y, x.y, a11);
+        }
+        double* pp = ps + (size_t)hs * TB * nrhs;
+        *reinterpret_cast<double2*>(pp + j0 * nrhs + 2 * cp) = make_double2(a00, a01);
+        *reinterpret_cast<double2*>(pp + (j0 + 1) * nrhs + 2 * cp) = make_double2(a10, a11);
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x)
+        ys[t] = V[(size_t)J * TB * nrhs + t] - (ps[t] + ps[TB * nrhs + t]);
+      __syncthreads();
+      {
+        const int cq = threadIdx.x % ncp, jq = threadIdx.x / ncp, js = 2 * ((int)blockDim.x / ncp);
+        for (int j0 = 2 * jq; j0 < TB; j0 += js) {
+          double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll
+          for (int k = 0; k < TB; ++k) {
+            const double2 dd = *reinterpret_cast<const double2*>(Dj + k * TB + j0);
+            const double2 rr = *reinterpret_cast<const double2*>(ys + k * nrhs + 2 * cq);
+            a00 = fma(dd.x, rr.x, a00);
+            a01 = fma(dd.x, rr.y, a01);
+            a10 = fma(dd.y, rr.x, a10);
+            a11 = fma(dd.y, rr.y, a11);
+          }
+          *reinterpret_cast<double2*>(V + (size_t)(J * TB + j0) * nrhs + 2 * cq) = make_double2(a00, a01);
+          *reinterpret_cast<double2*>(V + (size_t)(J * TB + j0 + 1) * nrhs + 2 * cq) = make_double2(a10, a11);
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int j = t / nrhs, s = t % nrhs;
+      const double* vb = V + (size_t)(J + 1) * TB * nrhs + s;
+      double a = V[(size_t)(J * TB + j) * nrhs + s], b = 0.0;
+      for (int rr = 0; rr < nb * TB; rr += 2) {
+        a = fma(-Ls[(size_t)rr * TB + j], vb[(size_t)rr * nrhs], a);
+        b = fma(-Ls[(size_t)(rr + 1) * TB + j], vb[(size_t)(rr + 1) * nrhs], b);
+      }
+      ys[t] = a + b;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TB * nrhs; t += blockDim.x) {
+      const int j = t / nrhs, s = t % nrhs;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; k += 2) {
+        a = fma(Dj[k * TB + j], ys[k * nrhs + s], a);
+        b = fma(Dj[(k + 1) * TB + j], ys[(k + 1) * nrhs + s], b);
+      }
+      V[(size_t)(J * TB + j) * nrhs + s] = a + b;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < F.nE * nrhs; t += blockDim.x) {
+    const int r = t / nrhs, s = t % nrhs;
+    X[(size_t)gid[r] * nrhs + s] = V[t];
+  }
+}
+
+static MfDev mf_dev(const Geo& g, double* base) {
+  const MfPlan* P = mf_plan(g);
+  return MfDev{P->d_fr, P->d_lvl, P->d_gid, P->d_maps, base};
+}
+
+cudaError_t launch_mf_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st) {
+  cudaError_t e = mf_upload(g);
+  if (e != cudaSuccess) return e;
+  k_mf_a27<<<nblk((long long)g.kc * 14, 256), 256, 0, st>>>(g, Kloc, shift, Ak + mf_plan(g)->a27);
+  count_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_mf_diag(const Geo& g, const double* Ak, double* diag, cudaStream_t st) {
+  // diagonal entries are A27[c][13]
+  cudaError_t e = cudaMemcpy2DAsync(diag, sizeof(double), Ak + mf_plan(g)->a27 + 13, 14 * sizeof(double),
+                                    sizeof(double), g.kc, cudaMemcpyDeviceToDevice, st);
+  return e;
+}
+cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st) {
+  cudaError_t e = mf_upload(g);
+  if (e != cudaSuccess) return e;
+  const MfPlan* P = mf_plan(g);
+  static int coop_grid = -1;
+  if (coop_grid < 0) {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
+    coop_grid = (coop && per_sm > 0) ? sms : 0;
+  }
+  if (coop_grid <= 0) return cudaErrorNotSupported;
+  const MfDev d = mf_dev(g, Ak);
+  for (size_t l = 0; l + 1 < P->lvl_off.size(); ++l) {
+    const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0;
+    if (nf <= 0) continue;
+    if (nf > MF_MAXF) return cudaErrorInvalidValue;
+    int jmax = 0, ntmax = 0;
+    for (int i = 0; i < nf; ++i) {
+      jmax = std::max(jmax, P->fr[P->lvl[l0 + i]].NE);
+      ntmax = std::max(ntmax, P->fr[P->lvl[l0 + i]].NT);
+    }
+    const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * ntmax * TT + 255) / 256);
+    k_mf_assemble<<<dim3(gx, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
+    count_launches(1);
+    MfJob job{d, l0, nf, jmax};
+    void* args[] = {(void*)&job, (void*)&flags};
+    e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
+    count_launches(1);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
+  if (nrhs == 0) return cudaSuccess;
+  cudaError_t e = mf_upload(g);
+  if (e != cudaSuccess) return e;
+  const MfPlan* P = mf_plan(g);
+  const MfDev d = mf_dev(g, const_cast<double*>(Ak));
+  const size_t sm = (size_t)TB * nrhs * sizeof(double);
+  if (sm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_mf_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  const int nl = (int)P->lvl_off.size() - 1;
+  auto level_nt = [&](int l) {
+    int nt = 1;
+    for (int i = P->lvl_off[l]; i < P->lvl_off[l + 1]; ++i) nt = std::max(nt, P->fr[P->lvl[i]].NT);
+    return nt;
+  };
+  auto smem_s = [&](int nt) {
+    return ((size_t)nt * TB * nrhs + (size_t)nt * TT + (size_t)3 * TB * nrhs) * sizeof(double) +
+           (size_t)3 * nt * TB * sizeof(int) + 16;
+  };
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_mf_fwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (getenv("MSFV_MF_DEBUG"))
+    fprintf(stderr, "mf solve nrhs %d, smem(max level) %zu\n", nrhs, smem_s(level_nt(nl - 2 >= 0 ? nl - 2 : 0)));
+  for (int l = 0; l < nl; ++l) {
+    const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
+    if (smem_s(nt) <= MF_SMEM_MAX)
+      k_mf_fwd_s<<<nf, 256, smem_s(nt), st>>>(d, l0, X, scratch, nrhs, nt);
+    else
+      k_mf_fwd<<<nf, 256, sm, st>>>(d, l0, X, scratch, nrhs);
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
+    if (smem_s(nt) <= MF_SMEM_MAX)
+      k_mf_bwd_s<<<nf, 256, smem_s(nt), st>>>(d, l0, X, scratch, nrhs, nt);
+    else
+      k_mf_bwd<<<nf, 256, sm, st>>>(d, l0, X, scratch, nrhs);
+  }
+  count_launches(2 * nl);
+  return cudaGetLastError();
+}
+size_t mf_doubles(const Geo& g) { return mf_plan(g)->total; }
+int mf_tile_rows(const Geo& g) { return (int)(mf_plan(g)->vrows / TB); }
 
 }  // namespace msfv

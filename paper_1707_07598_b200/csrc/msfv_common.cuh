@@ -48,7 +48,8 @@ struct Geo {
   double ih1, ih2, ih3;    // 1/h per axis (as the reference's 1.0/h)
   double qv;               // 0.25 * cell volume (operators.py:83)
   double ib1, ib2, ib3;    // 1/b per axis (device-side hats)
-  int coarse_nd;           // 1: z-plane nested dissection of the coarse system (msfv_coarse.cu)
+  int coarse_nd;           // 1: z-plane nested dissection, 2: multifrontal nested dissection (msfv_coarse.cu)
+  const void* mf;          // host-side multifrontal plan (coarse_nd == 2), owned by the msfv_plan
   const SkelEdge* skel;    // device table of the skeleton-only owned edges (msfv_basis_build)
   int nskel;
   // float reciprocals for division-free index decoding (see fdiv)

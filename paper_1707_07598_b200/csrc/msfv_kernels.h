@@ -23,6 +23,9 @@ constexpr int FLAG_COARSE_NOT_SPD = 8;
 void count_launches(long long n);
 // record msg as msfv_last_error() and return code (msfv_capi.cu)
 int set_error(int code, const std::string& msg);
+// multifrontal coarse plan (msfv_coarse.cu): built at plan creation when coarse_nd == 2
+void mf_attach(Geo& g);
+void mf_release(Geo& g);
 long long launch_count();
 
 size_t basis_smem_bytes(const Geo& g);
