@@ -127,8 +127,11 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   g.r_nI = g.nI > 0 ? 1.0f / g.nI : 0.0f; g.r_nb1 = 1.0f / g.nb1; g.r_nb2 = 1.0f / g.nb2;
   {
     // coarse nested dissection: on for k >= 1000 (MSFV_COARSE_ND=0/1 overrides)
+    // coarse solver: one band below 1000 unknowns, multifrontal nested
+    // dissection where its fronts fit the kernels (config 4), z-plane nested
+    // dissection of the band otherwise (config 5); MSFV_COARSE_ND=0/1/2 overrides
     const char* ev = getenv("MSFV_COARSE_ND");
-    g.coarse_nd = ev ? std::min(2, std::max(0, atoi(ev))) : (g.kc >= 1000 ? 1 : 0);
+    g.coarse_nd = ev ? std::min(2, std::max(0, atoi(ev))) : (g.kc >= 1000 ? 2 : 0);
     g.mf = nullptr;
     g.skel = nullptr;
     g.nskel = 0;
@@ -137,7 +140,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
     return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
-  if (g.coarse_nd == 2) mf_attach(g);
+  if (g.coarse_nd == 2 && !mf_attach(g)) g.coarse_nd = g.kc >= 1000 ? 1 : 0;
   msfv_plan* pl = new msfv_plan;
   pl->g = g;
   *out = pl;

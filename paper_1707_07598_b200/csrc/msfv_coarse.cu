@@ -148,7 +148,7 @@ size_t mf_doubles(const Geo& g);
 int mf_tile_rows(const Geo& g);
 size_t coarse_doubles(const Geo& g) { return g.coarse_nd == 2 ? mf_doubles(g) : coarse_layout(g, nullptr).total; }
 size_t coarse_scratch_doubles(const Geo& g, int nrhs) {
-  if (g.coarse_nd == 2) return (size_t)mf_tile_rows(g) * TB * nrhs;
+  if (g.coarse_nd == 2) return (size_t)mf_tile_rows(g) * TB * nrhs;   // mf_tile_rows already counts Vin + Vout
   const Coarse L = coarse_layout(g, nullptr);
   size_t rows = 0;
   for (int b = 0; b < L.nb; ++b) rows += (size_t)L.b[b].NT * TB;
@@ -1715,7 +1715,18 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 // ============================================================================
 
 constexpr int MF_LEAF = 64;
+constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative kernels
+constexpr int MF_GR = 16;       // rows per item of the G products
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
+// explicit front inverse blocks (G) for one-product-per-front solves; MSFV_MF_G=0 keeps the staged sweeps
+static bool mf_use_g() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MSFV_MF_G");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v == 1;
+}
 
 struct MfFront {
   int nE, nB, NE, NT;     // real E / B sizes, tile counts (NT = NE + ceil(nB/TB))
@@ -1724,6 +1735,7 @@ struct MfFront {
   int c[2];               // children (-1: none)
   int goff;               // gid table offset (NT*TB entries, -1 = padding)
   int moff[2];            // child maps (NT*TB entries: child-local row or -1)
+  long long goff2;        // G = [L_EE^-1 ; -L_BE L_EE^-1] (NT*TB x NE*TB) then G^T, row-major
 };
 
 struct MfPlan {
@@ -1737,6 +1749,7 @@ struct MfPlan {
   int* d_lvl = nullptr;
   int* d_gid = nullptr;
   int* d_maps = nullptr;
+  int* d_lvloff = nullptr;
 };
 
 __host__ __device__ __forceinline__ Band mf_band(double* base, const MfFront& f) {
@@ -1869,6 +1882,11 @@ static MfPlan* mf_build(const Geo& g) {
       if (height[f] == h) P->lvl.push_back(f);
     P->lvl_off.push_back((int)P->lvl.size());
   }
+  for (int f = 0; f < nf; ++f) {
+    MfFront& F = P->fr[f];
+    F.goff2 = (long long)aoff;
+    aoff += (size_t)2 * F.NT * F.NE * TT;
+  }
   P->a27 = aoff;
   P->total = aoff + (size_t)g.kc * 14;
   P->vrows = voff;
@@ -1901,6 +1919,9 @@ static cudaError_t mf_upload(const Geo& g) {
   if (e == cudaSuccess) e = cudaMemcpy(P->d_gid, P->gid.data(), P->gid.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !P->maps.empty())
     e = cudaMemcpy(P->d_maps, P->maps.data(), P->maps.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_lvloff, P->lvl_off.size() * sizeof(int));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(P->d_lvloff, P->lvl_off.data(), P->lvl_off.size() * sizeof(int), cudaMemcpyHostToDevice);
   return e;
 }
 
@@ -1911,10 +1932,33 @@ void mf_release(Geo& g) {
   if (P->d_lvl) cudaFree(P->d_lvl);
   if (P->d_gid) cudaFree(P->d_gid);
   if (P->d_maps) cudaFree(P->d_maps);
+  if (P->d_lvloff) cudaFree(P->d_lvloff);
   delete P;
   g.mf = nullptr;
 }
-void mf_attach(Geo& g) { g.mf = mf_build(g); }
+// Multifrontal plan when its kernels fit (the explicit-inverse chain keeps a
+// front's E rows in shared memory; the one-launch solve keeps the largest
+// front's G chunk and vector there, sized for <= 32 right-hand sides).
+bool mf_attach(Geo& g) {
+  MfPlan* P = mf_build(g);
+  int nemax = 0, ntmax = 0;
+  for (const MfFront& F : P->fr) {
+    nemax = std::max(nemax, F.NE);
+    ntmax = std::max(ntmax, F.NT);
+  }
+  const size_t inv_b = ((size_t)nemax * TT + 3 * TT) * sizeof(double);
+  const size_t sol_b = ((size_t)MF_GR * ntmax * TB + (size_t)ntmax * TB * 32 + (size_t)MF_GR * 32) * sizeof(double);
+  const int nl = (int)P->lvl_off.size() - 1;
+  int maxf = 0;
+  for (int l = 0; l < nl; ++l) maxf = std::max(maxf, P->lvl_off[l + 1] - P->lvl_off[l]);
+  if (inv_b > (size_t)MF_SMEM_MAX || sol_b > (size_t)MF_SMEM_MAX - 8192 || maxf > MF_MAXF) {
+    delete P;
+    g.mf = nullptr;
+    return false;
+  }
+  g.mf = P;
+  return true;
+}
 
 struct MfDev {
   const MfFront* fr;
@@ -1994,7 +2038,6 @@ struct MfJob {
   MfDev d;
   int l0, nf, jmax;
 };
-constexpr int MF_MAXF = 1024;
 __global__ void __launch_bounds__(256, 1) k_mf_factor(MfJob job, int* __restrict__ flags) {
   __shared__ __align__(16) FactorSmem sm;
   __shared__ int pre[MF_MAXF + 1];
@@ -2387,6 +2430,406 @@ __global__ void __launch_bounds__(256) k_mf_bwd_s(MfDev d, int l0, double* __res
   }
 }
 
+// Explicit front inverse blocks, after the level's factorization: CTA
+// (front, c) solves L [G_E; G_B](:, block c) = [I; 0](:, block c) by the
+// blocked forward substitution (steps J = c .. NE-1) with the 32 columns in
+// shared memory, then stores G and G^T.  With them a front's forward solve is
+// [y_E; c_B] = G v_E + [0; v_B] and its backward solve x_E = G^T [y_E; x_B]:
+// one matrix product per front, so a coarse solve has the depth of the tree
+// (7 levels at config 4) instead of 23 tile steps.
+constexpr int MF_INV_THREADS = 256;
+// one bulk copy global -> shared on an mbarrier (thread 0 issues; all wait)
+__device__ __forceinline__ void mf_tma1(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+  }
+}
+// 2x2-blocked 32x32 by 32x32 product O = Lt Y, Lt row-major (stride 32),
+// Y / O row-major with stride ld; op(o, value) stores.  256 threads.
+template <class Op>
+__device__ __forceinline__ void mf_tile_mm(const double* Lt, const double* Y, int ld, Op op) {
+  const int cp = threadIdx.x % 16, rp = threadIdx.x / 16, r0 = 2 * rp;
+  double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll 8
+  for (int k = 0; k < TB; k += 2) {
+    const double2 l0 = *reinterpret_cast<const double2*>(Lt + r0 * TB + k);
+    const double2 l1 = *reinterpret_cast<const double2*>(Lt + (r0 + 1) * TB + k);
+    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * ld + 2 * cp);
+    const double2 y1 = *reinterpret_cast<const double2*>(Y + (k + 1) * ld + 2 * cp);
+    a00 = fma(l0.x, y0.x, fma(l0.y, y1.x, a00));
+    a01 = fma(l0.x, y0.y, fma(l0.y, y1.y, a01));
+    a10 = fma(l1.x, y0.x, fma(l1.y, y1.x, a10));
+    a11 = fma(l1.x, y0.y, fma(l1.y, y1.y, a11));
+  }
+  op(r0, 2 * cp, a00, a01);
+  op(r0 + 1, 2 * cp, a10, a11);
+}
+__global__ void __launch_bounds__(MF_INV_THREADS) k_mf_inv(MfDev d, int l0) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int c = blockIdx.y;
+  if (c >= F.NE) return;
+  const Band B = mf_band(d.base, F);
+  const int rows = F.NE * TB;           // the chain runs on the E rows; G_B = -L_BE G_E follows (k_mf_invB)
+  double* V = sh;                       // rows x 32
+  double* ys = V + (size_t)rows * TB;   // 32 x 32
+  double* Tb = ys + TT;                 // 2 tiles: Dinv_J / L tiles, double-buffered
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+  }
+  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
+    const int r = t / TB, q = t % TB;
+    V[t] = (r == c * TB + q) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  unsigned ph[2] = {0, 0};
+  int buf = 0;
+  // sequence of tiles: per step J, Dinv_J then L_{I,J} for I = J+1 .. NT-1
+  auto src_of = [&](int J, int I) -> const double* {
+    return I == J ? B.Dinv + (size_t)J * TT : btile(B.Lo, B, J, I - J);
+  };
+  mf_tma1(Tb, src_of(c, c), TT * sizeof(double), &bar[0]);
+  for (int J = c; J < F.NE; ++J) {
+    for (int I = J; I < F.NE; ++I) {
+      // prefetch the next tile of the sequence into the other buffer
+      int nJ = J, nI = I + 1;
+      if (nI >= F.NE) { nJ = J + 1; nI = nJ; }
+      if (nJ < F.NE) mf_tma1(Tb + (buf ^ 1) * TT, src_of(nJ, nI), TT * sizeof(double), &bar[buf ^ 1]);
+      mbar_wait(&bar[buf], ph[buf]);
+      ph[buf] ^= 1;
+      const double* T = Tb + buf * TT;
+      if (I == J) {
+        mf_tile_mm(T, V + (size_t)J * TT, TB, [&](int r, int q, double x, double y) {
+          *reinterpret_cast<double2*>(ys + r * TB + q) = make_double2(x, y);
+        });
+        __syncthreads();
+        for (int t = threadIdx.x; t < TT; t += blockDim.x) V[(size_t)J * TT + t] = ys[t];
+      } else {
+        double* VI = V + (size_t)I * TT;
+        mf_tile_mm(T, ys, TB, [&](int r, int q, double x, double y) {
+          double2* o = reinterpret_cast<double2*>(VI + r * TB + q);
+          const double2 p = *o;
+          *o = make_double2(p.x - x, p.y - y);
+        });
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  double* G = d.base + F.goff2;
+  const int frows = F.NT * TB;
+  double* GT = G + (size_t)F.NT * F.NE * TT;
+  const int ncol = F.NE * TB;
+  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
+    const int r = t / TB, q = t % TB;
+    G[(size_t)r * ncol + c * TB + q] = V[t];
+  }
+  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
+    const int q = t / rows, r = t % rows;
+    GT[(size_t)(c * TB + q) * frows + r] = V[(size_t)r * TB + q];
+  }
+}
+// G_B = -L_BE G_E: item (front, B tile row I, column block c) sums
+// L_{I,J} G_E[J][c] over J = c .. NE-1 (32x32 tiles through shared memory).
+__global__ void __launch_bounds__(MF_INV_THREADS) k_mf_invB(MfDev d, int l0, int nbmax) {
+  __shared__ __align__(16) double Lt[TT];
+  __shared__ __align__(16) double Gt[TT];
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int NB = F.NT - F.NE;
+  const int I = F.NE + blockIdx.y % nbmax, c = blockIdx.y / nbmax;
+  if (I >= F.NT || c >= F.NE || NB <= 0) return;
+  const Band B = mf_band(d.base, F);
+  const int ncol = F.NE * TB, frows = F.NT * TB;
+  double* G = d.base + F.goff2;
+  double* GT = G + (size_t)F.NT * F.NE * TT;
+  double acc[4] = {0, 0, 0, 0};
+  const int cp = threadIdx.x % 16, r0 = 2 * (threadIdx.x / 16);
+  for (int J = c; J < F.NE; ++J) {
+    const double* Ls = btile(B.Lo, B, J, I - J);
+    for (int t = threadIdx.x; t < TT / 2; t += blockDim.x) {
+      reinterpret_cast<double2*>(Lt)[t] = __ldg(reinterpret_cast<const double2*>(Ls) + t);
+      const int r = (2 * t) / TB, q = (2 * t) % TB;
+      reinterpret_cast<double2*>(Gt)[t] =
+          __ldcg(reinterpret_cast<const double2*>(G + (size_t)(J * TB + r) * ncol + c * TB + q));
+    }
+    __syncthreads();
+    mf_tile_mm(Lt, Gt, TB, [&](int r, int q, double x, double y) {
+      const int h = (r - r0) * 2;
+      acc[h] += x;
+      acc[h + 1] += y;
+    });
+    __syncthreads();
+  }
+  for (int h = 0; h < 2; ++h) {
+    const int r = I * TB + r0 + h, q = c * TB + 2 * cp;
+    G[(size_t)r * ncol + q] = -acc[2 * h];
+    G[(size_t)r * ncol + q + 1] = -acc[2 * h + 1];
+    GT[(size_t)q * frows + r] = -acc[2 * h];
+    GT[(size_t)(q + 1) * frows + r] = -acc[2 * h + 1];
+  }
+}
+
+// Forward solve of one level with G: CTA (front, 16-row chunk): the chunk of
+// G arrives by one bulk copy while v_E is gathered (X on E + the children's
+// c_B); out = G v_E (+ the children's c_B on B rows).
+__global__ void __launch_bounds__(256) k_mf_gfwd(MfDev d, int l0, const double* __restrict__ X,
+                                                 double* __restrict__ Vg, int nrhs) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int rows = F.NT * TB, ncol = F.NE * TB, r0c = blockIdx.y * MF_GR;
+  if (r0c >= rows) return;
+  const int nr = min(MF_GR, rows - r0c);
+  const int* gid = d.gid + F.goff;
+  const double* v0 = F.c[0] >= 0 ? Vg + (size_t)d.fr[F.c[0]].voff * nrhs : nullptr;
+  const double* v1 = F.c[1] >= 0 ? Vg + (size_t)d.fr[F.c[1]].voff * nrhs : nullptr;
+  const int* m0 = v0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = v1 ? d.maps + F.moff[1] : nullptr;
+  double* Gs = sh;                                    // MF_GR x ncol
+  double* vE = Gs + (size_t)MF_GR * ncol;             // ncol x nrhs
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  mf_tma1(Gs, d.base + F.goff2 + (size_t)r0c * ncol, (unsigned)(nr * ncol * sizeof(double)), &bar);
+  auto gat = [&](int r, int s) {
+    double a = (r < F.nE) ? __ldcg(X + (size_t)gid[r] * nrhs + s) : 0.0;
+    if (m0) { const int q = m0[r]; if (q >= 0) a += __ldcg(v0 + (size_t)q * nrhs + s); }
+    if (m1) { const int q = m1[r]; if (q >= 0) a += __ldcg(v1 + (size_t)q * nrhs + s); }
+    return a;
+  };
+#pragma unroll 4
+  for (int t = threadIdx.x; t < ncol * nrhs; t += blockDim.x) vE[t] = gat(t / nrhs, t % nrhs);
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  double* v = Vg + (size_t)F.voff * nrhs;
+  for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) {
+    const int i = t / nrhs, s = t % nrhs, r = r0c + i;
+    const double* Gr = Gs + (size_t)i * ncol;
+    const int kend = r < ncol ? min(ncol, (r / TB + 1) * TB) : ncol;   // L_EE^-1 is block lower triangular
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < kend; k += 2) {
+      a = fma(Gr[k], vE[k * nrhs + s], a);
+      b = fma(Gr[k + 1], vE[(k + 1) * nrhs + s], b);
+    }
+    a += b;
+    if (r >= ncol) a += gat(r, s);
+    v[(size_t)r * nrhs + s] = a;
+  }
+}
+// Backward solve of one level with G^T: CTA (front, 16-row chunk of x_E):
+// z = [y_E ; x_B] gathered, x_E = G^T z -> X.
+__global__ void __launch_bounds__(256) k_mf_gbwd(MfDev d, int l0, double* __restrict__ X,
+                                                 const double* __restrict__ Vg, int nrhs) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int j0 = blockIdx.y * MF_GR;
+  if (j0 >= F.nE) return;
+  const int nj = min(MF_GR, F.nE - j0);
+  const int rows = F.NT * TB, ncol = F.NE * TB;
+  const int rz0 = (j0 / TB) * TB;                    // G^T rows of this chunk vanish before their block
+  const int* gid = d.gid + F.goff;
+  const double* v = Vg + (size_t)F.voff * nrhs;
+  double* Gs = sh;                                   // MF_GR x rows (columns rz0.. used)
+  double* z = Gs + (size_t)MF_GR * rows;             // rows x nrhs
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  mf_tma1(Gs, d.base + F.goff2 + (size_t)F.NT * F.NE * TT + (size_t)j0 * rows,
+          (unsigned)(nj * rows * sizeof(double)), &bar);
+#pragma unroll 4
+  for (int t = threadIdx.x; t < (rows - rz0) * nrhs; t += blockDim.x) {
+    const int r = rz0 + t / nrhs, s = t % nrhs;
+    z[(size_t)r * nrhs + s] = r < ncol ? __ldcg(v + (size_t)r * nrhs + s)
+                                       : (gid[r] >= 0 ? __ldcg(X + (size_t)gid[r] * nrhs + s) : 0.0);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int t = threadIdx.x; t < nj * nrhs; t += blockDim.x) {
+    const int i = t / nrhs, s = t % nrhs, j = j0 + i;
+    const double* Gr = Gs + (size_t)i * rows;
+    double a = 0.0, b = 0.0;
+    for (int r = rz0; r < rows; r += 2) {
+      a = fma(Gr[r], z[(size_t)r * nrhs + s], a);
+      b = fma(Gr[r + 1], z[(size_t)(r + 1) * nrhs + s], b);
+    }
+    X[(size_t)gid[j] * nrhs + s] = a + b;
+  }
+}
+
+// Both sweeps of a coarse solve in one cooperative launch.  Per level:
+// (A) grid-wide gather of every front's input vector into Vin (independent
+// loads on all SMs), grid barrier; (B) (front, 16-row chunk) items: the chunk
+// of G (forward) or G^T (backward) and the input rows it needs arrive by bulk
+// copies, one product, result to Vout (forward) or X (backward); grid barrier.
+struct MfSolveJob {
+  MfDev d;
+  const int* lvl_off;   // device copy of the level offsets
+  int nl;
+  double* X;            // right-hand sides in, solution out (k x nrhs, natural order)
+  double* Vout;         // per-front outputs (y_E | c_B), Σ rows x nrhs
+  double* Vin;          // per-front gathered inputs, Σ rows x nrhs
+  int nrhs;
+};
+__global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ int pre[MF_MAXF + 1];
+  cg::grid_group grid = cg::this_grid();
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  unsigned ph = 0;
+  const MfDev& d = job.d;
+  const int nrhs = job.nrhs;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int li = 0; li < job.nl; ++li) {
+      const int l = pass == 0 ? li : job.nl - 1 - li;
+      const int l0 = job.lvl_off[l], nf = job.lvl_off[l + 1] - l0;
+      // ---- (A) gather: flat index over the level's fronts (rows x nrhs each)
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const MfFront F = d.fr[d.lvl[l0 + i]];
+        pre[i + 1] = F.NT * TB * nrhs;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pre[0] = 0;
+        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+      }
+      __syncthreads();
+      {
+        int fi = 0;
+        for (long long gi = gtid; gi < pre[nf]; gi += gstride) {
+          while (pre[fi + 1] <= gi) ++fi;
+          const MfFront F = d.fr[d.lvl[l0 + fi]];
+          const int e = (int)(gi - pre[fi]), r = e / nrhs, s = e % nrhs;
+          const int g = d.gid[F.goff + r];
+          double a;
+          if (pass == 0) {
+            a = (r < F.nE) ? __ldcg(job.X + (size_t)g * nrhs + s) : 0.0;
+            for (int c = 0; c < 2; ++c) {
+              if (F.c[c] < 0) continue;
+              const int q = d.maps[F.moff[c] + r];
+              if (q >= 0) a += __ldcg(job.Vout + ((size_t)d.fr[F.c[c]].voff + q) * nrhs + s);
+            }
+          } else {
+            a = r < F.NE * TB ? __ldcg(job.Vout + ((size_t)F.voff + r) * nrhs + s)
+                              : (g >= 0 ? __ldcg(job.X + (size_t)g * nrhs + s) : 0.0);
+          }
+          job.Vin[((size_t)F.voff + r) * nrhs + s] = a;
+        }
+      }
+      grid.sync();
+      // ---- (B) products
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const MfFront F = d.fr[d.lvl[l0 + i]];
+        pre[i + 1] = pass == 0 ? (F.NT * TB + MF_GR - 1) / MF_GR : (F.nE + MF_GR - 1) / MF_GR;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pre[0] = 0;
+        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+      }
+      __syncthreads();
+      int fi = 0;
+      for (int gi = blockIdx.x; gi < pre[nf]; gi += gridDim.x) {
+        while (pre[fi + 1] <= gi) ++fi;
+        const MfFront F = d.fr[d.lvl[l0 + fi]];
+        const int rows = F.NT * TB, ncol = F.NE * TB;
+        const double* vin = job.Vin + (size_t)F.voff * nrhs;
+        if (pass == 0) {
+          const int r0c = (gi - pre[fi]) * MF_GR, nr = min(MF_GR, rows - r0c);
+          const int kmax = r0c < ncol ? min(ncol, ((r0c + nr - 1) / TB + 1) * TB) : ncol;
+          double* Gs = sh;
+          double* vs = Gs + (size_t)MF_GR * ncol;
+          double* addv = vs + (size_t)ncol * nrhs;
+          if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bg = (unsigned)(nr * ncol * sizeof(double)), bv = (unsigned)(kmax * nrhs * sizeof(double));
+            const unsigned ba = r0c >= ncol ? (unsigned)(nr * nrhs * sizeof(double)) : 0u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(bg + bv + ba)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(Gs)), "l"(d.base + F.goff2 + (size_t)r0c * ncol), "r"(bg), "r"(smem_u32(&bar))
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(vs)), "l"(vin), "r"(bv), "r"(smem_u32(&bar))
+                         : "memory");
+            if (ba)
+              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                               smem_u32(addv)), "l"(vin + (size_t)r0c * nrhs), "r"(ba), "r"(smem_u32(&bar))
+                           : "memory");
+          }
+          mbar_wait(&bar, ph);
+          ph ^= 1;
+          // rows of the chunk may end at different diagonal blocks: use each row's own bound
+          for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) {
+            const int ii = t / nrhs, s = t % nrhs, r = r0c + ii;
+            const double* Gr = Gs + (size_t)ii * ncol;
+            const int kend = r < ncol ? min(ncol, (r / TB + 1) * TB) : ncol;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int k = 0;
+            for (; k + 3 < kend; k += 4) {
+              a0 = fma(Gr[k], vs[(size_t)k * nrhs + s], a0);
+              a1 = fma(Gr[k + 1], vs[(size_t)(k + 1) * nrhs + s], a1);
+              a2 = fma(Gr[k + 2], vs[(size_t)(k + 2) * nrhs + s], a2);
+              a3 = fma(Gr[k + 3], vs[(size_t)(k + 3) * nrhs + s], a3);
+            }
+            for (; k < kend; ++k) a0 = fma(Gr[k], vs[(size_t)k * nrhs + s], a0);
+            double a = (a0 + a1) + (a2 + a3);
+            if (r >= ncol) a += addv[(size_t)ii * nrhs + s];
+            job.Vout[((size_t)F.voff + r) * nrhs + s] = a;
+          }
+        } else {
+          const int j0 = (gi - pre[fi]) * MF_GR, nj = min(MF_GR, F.nE - j0);
+          const int rz0 = (j0 / TB) * TB;
+          double* Gs = sh;                                 // nj x rows
+          double* zs = Gs + (size_t)MF_GR * rows;          // rows x nrhs (from rz0)
+          if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bg = (unsigned)(nj * rows * sizeof(double)),
+                           bz = (unsigned)((rows - rz0) * nrhs * sizeof(double));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(bg + bz)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(Gs)),
+                         "l"(d.base + F.goff2 + (size_t)F.NT * F.NE * TT + (size_t)j0 * rows), "r"(bg),
+                         "r"(smem_u32(&bar))
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(zs + (size_t)rz0 * nrhs)), "l"(vin + (size_t)rz0 * nrhs), "r"(bz), "r"(smem_u32(&bar))
+                         : "memory");
+          }
+          mbar_wait(&bar, ph);
+          ph ^= 1;
+          for (int t = threadIdx.x; t < nj * nrhs; t += blockDim.x) {
+            const int ii = t / nrhs, s = t % nrhs, j = j0 + ii;
+            const double* Gr = Gs + (size_t)ii * rows;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int r = rz0;
+            for (; r + 3 < rows; r += 4) {
+              a0 = fma(Gr[r], zs[(size_t)r * nrhs + s], a0);
+              a1 = fma(Gr[r + 1], zs[(size_t)(r + 1) * nrhs + s], a1);
+              a2 = fma(Gr[r + 2], zs[(size_t)(r + 2) * nrhs + s], a2);
+              a3 = fma(Gr[r + 3], zs[(size_t)(r + 3) * nrhs + s], a3);
+            }
+            for (; r < rows; ++r) a0 = fma(Gr[r], zs[(size_t)r * nrhs + s], a0);
+            job.X[(size_t)d.gid[F.goff + j] * nrhs + s] = (a0 + a1) + (a2 + a3);
+          }
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+  }
+}
+
 static MfDev mf_dev(const Geo& g, double* base) {
   const MfPlan* P = mf_plan(g);
   return MfDev{P->d_fr, P->d_lvl, P->d_gid, P->d_maps, base};
@@ -2437,6 +2880,27 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
     count_launches(1);
     if (e != cudaSuccess) return e;
+    if (mf_use_g()) {
+      int nemax = 1, nbmax = 0;
+      for (int i = 0; i < nf; ++i) {
+        nemax = std::max(nemax, P->fr[P->lvl[l0 + i]].NE);
+        nbmax = std::max(nbmax, P->fr[P->lvl[l0 + i]].NT - P->fr[P->lvl[l0 + i]].NE);
+      }
+      const size_t smi = ((size_t)nemax * TB * TB + 3 * TT) * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        e = cudaFuncSetAttribute(k_mf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
+      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, st>>>(d, l0);
+      count_launches(1);
+      if (nbmax > 0) {
+        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, st>>>(d, l0, nbmax);
+        count_launches(1);
+      }
+    }
   }
   return cudaGetLastError();
 }
@@ -2469,8 +2933,64 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (getenv("MSFV_MF_DEBUG"))
-    fprintf(stderr, "mf solve nrhs %d, smem(max level) %zu\n", nrhs, smem_s(level_nt(nl - 2 >= 0 ? nl - 2 : 0)));
+  if (mf_use_g() && nrhs <= 64) {
+    // one cooperative launch for both sweeps
+    size_t smc = 0;
+    for (int l = 0; l < nl; ++l) {
+      const int nt = level_nt(l);
+      smc = std::max(smc, ((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs + (size_t)MF_GR * nrhs) * sizeof(double));
+    }
+    static int coop_grid = -1;
+    if (coop_grid < 0) {
+      int dev = 0, sms = 0, coop = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+      if (e != cudaSuccess) return e;
+      coop_grid = coop ? sms : 0;
+    }
+    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 8192 && !getenv("MSFV_MF_NOCOOP")) {
+      MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs};
+      void* args[] = {(void*)&job};
+      e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
+      count_launches(1);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
+  }
+  bool g_fits = true;
+  for (int l = 0; l < nl; ++l) {
+    const int nt = level_nt(l);
+    if (((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs) * sizeof(double) > (size_t)MF_SMEM_MAX) g_fits = false;
+  }
+  if (mf_use_g() && g_fits) {
+    static bool gattr = false;
+    if (!gattr) {
+      e = cudaFuncSetAttribute(k_mf_gfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_gbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+      if (e != cudaSuccess) return e;
+      gattr = true;
+    }
+    for (int l = 0; l < nl; ++l) {
+      const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
+      int ne = 1;
+      for (int i = l0; i < l0 + nf; ++i) ne = std::max(ne, P->fr[P->lvl[i]].NE);
+      const size_t smf = ((size_t)MF_GR * ne * TB + (size_t)ne * TB * nrhs) * sizeof(double);
+      if (smf > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;   // unreachable: checked below
+      k_mf_gfwd<<<dim3(nf, (nt * TB + MF_GR - 1) / MF_GR), 256, smf, st>>>(d, l0, X, scratch, nrhs);
+    }
+    for (int l = nl - 1; l >= 0; --l) {
+      const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
+      int ne = 1;
+      for (int i = l0; i < l0 + nf; ++i) ne = std::max(ne, P->fr[P->lvl[i]].NE);
+      const size_t smb = ((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs) * sizeof(double);
+      if (smb > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
+      k_mf_gbwd<<<dim3(nf, (ne * TB + MF_GR - 1) / MF_GR), 256, smb, st>>>(d, l0, X, scratch, nrhs);
+    }
+    count_launches(2 * nl);
+    return cudaGetLastError();
+  }
   for (int l = 0; l < nl; ++l) {
     const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
     if (smem_s(nt) <= MF_SMEM_MAX)
@@ -2489,6 +3009,6 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
   return cudaGetLastError();
 }
 size_t mf_doubles(const Geo& g) { return mf_plan(g)->total; }
-int mf_tile_rows(const Geo& g) { return (int)(mf_plan(g)->vrows / TB); }
+int mf_tile_rows(const Geo& g) { return (int)(2 * mf_plan(g)->vrows / TB); }   // Vout + Vin workspaces
 
 }  // namespace msfv

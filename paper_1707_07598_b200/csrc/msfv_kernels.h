@@ -24,7 +24,7 @@ void count_launches(long long n);
 // record msg as msfv_last_error() and return code (msfv_capi.cu)
 int set_error(int code, const std::string& msg);
 // multifrontal coarse plan (msfv_coarse.cu): built at plan creation when coarse_nd == 2
-void mf_attach(Geo& g);
+bool mf_attach(Geo& g);   // false (and g.mf = nullptr) when the fronts exceed the kernels' shared memory
 void mf_release(Geo& g);
 long long launch_count();
 
