@@ -1719,6 +1719,14 @@ constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative k
 constexpr int MF_GR = 16;       // rows per item of the G products
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
 // explicit front inverse blocks (G) for one-product-per-front solves; MSFV_MF_G=0 keeps the staged sweeps
+static bool mf_two_phase() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MSFV_MF_2P");
+    v = e ? (atoi(e) != 0) : 0;
+  }
+  return v == 1;
+}
 static bool mf_use_g() {
   static int v = -1;
   if (v < 0) {
@@ -2005,11 +2013,18 @@ __global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__
   if (F.c[1] >= 0) C1 = mf_band(d.base, d.fr[F.c[1]]);
   const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
   const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntile * TT;
+  const long long nlow = (long long)F.NT * (F.NT + 1) / 2;   // lower tiles (J, tt), J + tt < NT
+  (void)ntile;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nlow * TT;
        t += (long long)gridDim.x * blockDim.x) {
-    const int tile = (int)(t / TT), e = (int)(t % TT);
-    const int J = tile / F.NT, tt = tile % F.NT;
-    if (J + tt >= F.NT) continue;
+    const int lt = (int)(t / TT), e = (int)(t % TT);
+    // lt -> (J, tt): column J holds NT - J tiles
+    int J = 0, rem = lt;
+    while (rem >= F.NT - J) {
+      rem -= F.NT - J;
+      ++J;
+    }
+    const int tt = rem;
     const int r = (J + tt) * TB + e / TB, c = J * TB + e % TB;
     const int gr = gid[r], gc = gid[c];
     double v = 0.0;
@@ -2038,7 +2053,117 @@ struct MfJob {
   MfDev d;
   int l0, nf, jmax;
 };
-__global__ void __launch_bounds__(256, 1) k_mf_factor(MfJob job, int* __restrict__ flags) {
+// Panel / update split for the fronts: per tile column, phase P stores the
+// panel tiles L_{J+t,J} = A_{J+t,J} Dinv_J^T once (Lo), grid barrier, phase U
+// applies A_{J+t1,J+t2} -= L_{J+t1,J} L_{J+t2,J}^T with one tile product per
+// task (the banded path's pair tasks recompute both panel tiles: 3 products).
+__device__ void mf_panel_task(const Band& B, int J, int t, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  load_tile(sm.T, btile(B.A, B, J, t));
+  __syncthreads();
+  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X1, LDT, bi, bj, lane, c); });
+  __syncthreads();
+  store_tile(btile(B.Lo, B, J, t), sm.X1);
+  __syncthreads();
+}
+__device__ void mf_update_task(const Band& B, int J, int f, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
+  while (t1 * (t1 - 1) / 2 > f) --t1;
+  while ((t1 + 1) * t1 / 2 <= f) ++t1;
+  const int t2 = f - t1 * (t1 - 1) / 2 + 1;
+  load_tile(sm.X1, btile(B.Lo, B, J, t1));
+  if (t2 != t1) load_tile(sm.X2, btile(B.Lo, B, J, t2));
+  __syncthreads();
+  const double* Y = (t2 != t1) ? sm.X2 : sm.X1;
+  double* G = btile(B.A, B, J + t2, t1 - t2);
+  const int wv = threadIdx.x >> 5;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
+    F2c c = frag(G, TB, bi, bj, lane), e = {0.0, 0.0};
+#pragma unroll
+    for (int kb = 0; kb < 4; kb += 2) {
+      const F2c a = frag(sm.X1, LDT, bi, kb, lane), a2 = frag(sm.X1, LDT, bi, kb + 1, lane);
+      mxyt(c, {-a.x, -a.y}, frag(Y, LDT, bj, kb, lane));
+      mxyt(e, {-a2.x, -a2.y}, frag(Y, LDT, bj, kb + 1, lane));
+    }
+    c.x += e.x;
+    c.y += e.y;
+    put(G, TB, bi, bj, lane, c);
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(256, 1) k_mf_factor2(MfJob job, int* __restrict__ flags) {
+  __shared__ __align__(16) FactorSmem sm;
+  __shared__ int pre[MF_MAXF + 1];
+  cg::grid_group grid = cg::this_grid();
+  const int nf = job.nf, G = (int)gridDim.x;
+  const bool split = nf < G;
+  auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
+  for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
+  grid.sync();
+  const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
+  for (int J = 0; J < job.jmax; ++J) {
+    // lookahead: pair (1,1) and the POTRF of column J+1 (dedicated CTAs)
+    for (int i = blockIdx.x; i < nf && (split ? blockIdx.x < nf : true); i += G) {
+      const MfFront F = front(i);
+      if (J + 1 < F.NE) {
+        const Band B = mf_band(job.d.base, F);
+        load_tile(sm.D, B.Dinv + (size_t)J * TT);
+        __syncthreads();
+        coarse_task(B, J, 0, sm, true);
+        coarse_potrf(B, J + 1, flags, sm, true);
+      }
+    }
+    for (int phase = 0; phase < 2; ++phase) {
+      if (me >= 0) {
+        for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+          const MfFront F = front(i);
+          int n = 0;
+          if (J < F.NE) {
+            const int pt = F.NT - 1 - J;
+            if (phase == 0) {
+              n = pt >= 1 ? pt : 0;
+            } else {
+              const int first = (pt >= 1 && J + 1 < F.NE) ? 1 : 0;
+              n = pt >= 1 ? pt * (pt + 1) / 2 - first : 0;
+            }
+          }
+          pre[i + 1] = n;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          pre[0] = 0;
+          for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+        }
+        __syncthreads();
+        const int total = pre[nf];
+        int loaded = -1, fi = 0;
+        for (int gi = me; gi < total; gi += nw) {
+          while (pre[fi + 1] <= gi) ++fi;
+          const MfFront F = front(fi);
+          const Band B = mf_band(job.d.base, F);
+          if (phase == 0) {
+            if (loaded != fi) {
+              load_tile(sm.D, B.Dinv + (size_t)J * TT);
+              __syncthreads();
+              loaded = fi;
+            }
+            // the lookahead CTA computes panel tile 1 itself; storing it again is harmless
+            mf_panel_task(B, J, 1 + (gi - pre[fi]), sm);
+          } else {
+            const int first = (J + 1 < F.NE) ? 1 : 0;
+            mf_update_task(B, J, first + (gi - pre[fi]), sm);
+          }
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict__ flags) {
   __shared__ __align__(16) FactorSmem sm;
   __shared__ int pre[MF_MAXF + 1];
   cg::grid_group grid = cg::this_grid();
@@ -2858,8 +2983,11 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
-    coop_grid = (coop && per_sm > 0) ? sms : 0;
+    if (mf_two_phase())
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor2, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
+    coop_grid = (coop && per_sm > 0) ? sms * std::min(per_sm, 2) : 0;
   }
   if (coop_grid <= 0) return cudaErrorNotSupported;
   const MfDev d = mf_dev(g, Ak);
@@ -2872,12 +3000,13 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
       jmax = std::max(jmax, P->fr[P->lvl[l0 + i]].NE);
       ntmax = std::max(ntmax, P->fr[P->lvl[l0 + i]].NT);
     }
-    const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * ntmax * TT + 255) / 256);
+    const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * (ntmax + 1) / 2 * TT + 255) / 256);
     k_mf_assemble<<<dim3(gx, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
     count_launches(1);
     MfJob job{d, l0, nf, jmax};
     void* args[] = {(void*)&job, (void*)&flags};
-    e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
+    e = cudaLaunchCooperativeKernel(mf_two_phase() ? (void*)k_mf_factor2 : (void*)k_mf_factor, dim3(coop_grid),
+                                    dim3(256), args, 0, st);
     count_launches(1);
     if (e != cudaSuccess) return e;
     if (mf_use_g()) {
