@@ -510,14 +510,14 @@ def run_gpu(args, rank, world, log):
     try:
         # dram__bytes_read.sum + dram__bytes_write.sum of k_basis_tc from the
         # committed ncu --set full capture of this configuration
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r01b_ncu.json")))["full"]
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r01c_ncu.json")))["full"]
         kb = next(v for k, v in prof.items() if "k_basis_tc" in k)
         if args.config == 4:
             traffic = int(kb["dram_read_B"] + kb["dram_write_B"])
-            traffic_src = "profiles/r01b_ncu.json (ncu --set full, k_basis_tc, bytes per launch)"
+            traffic_src = "profiles/r01c_ncu.json (ncu --set full, k_basis_tc, bytes per launch)"
     except Exception:  # noqa: BLE001
         pass
-    roof = {"kernel": "k_basis_tc<PT,false> + k_skel_galerkin (per-block A_II band Cholesky, 8-RHS forward sweep, "
+    roof = {"kernel": "k_basis_tc<PT,false> + k_skel_lines (per-block A_II band Cholesky, 8-RHS forward sweep, "
                       "local Galerkin; the backward sweeps run concurrently in k_basis_bwd)",
             "bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes", "traffic_source": traffic_src,
