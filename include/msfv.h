@@ -72,7 +72,8 @@ enum msfv_info {
   MSFV_INFO_FACTOR_DOUBLES = 14,  /* size of the per-model local factor buffer  */
   MSFV_INFO_SCRATCH_DOUBLES = 15, /* scratch needed by msfv_basis_build         */
   MSFV_INFO_TC = 16,              /* 1: FP64 tensor-core (DMMA) tile-band path  */
-  MSFV_INFO_COUNT = 17
+  MSFV_INFO_COARSE = 17,          /* coarse solver: 0 band, 1 z-plane ND band, 2 multifrontal ND */
+  MSFV_INFO_COUNT = 18
 };
 
 typedef struct msfv_plan msfv_plan;      /* geometry; model-independent        */

@@ -29,8 +29,8 @@ FLAG_COARSE_NOT_SPD = 8
 
 INFO_NN, INFO_N, INFO_NCELLS, INFO_NEDGES, INFO_NBLOCKS, INFO_NI, INFO_P1S, INFO_K, \
     INFO_AK_DOUBLES, INFO_BASIS_SMEM, INFO_NT, INFO_PT, INFO_TB, INFO_PC, \
-    INFO_FACTOR_DOUBLES, INFO_SCRATCH_DOUBLES, INFO_TC = range(17)
-INFO_COUNT = 17
+    INFO_FACTOR_DOUBLES, INFO_SCRATCH_DOUBLES, INFO_TC, INFO_COARSE = range(18)
+INFO_COUNT = 18
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32

@@ -176,6 +176,7 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)2 * g.nbl * g.nI * g.P1s;
   v[MSFV_INFO_SCRATCH_DOUBLES] = tc ? (int64_t)tc_scratch_doubles(g) : 0;
   v[MSFV_INFO_TC] = tc ? 1 : 0;
+  v[MSFV_INFO_COARSE] = g.coarse_nd;
   for (int i = 0; i < n && i < MSFV_INFO_COUNT; ++i) info[i] = v[i];
   return MSFV_OK;
 }

@@ -1719,6 +1719,16 @@ constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative k
 constexpr int MF_GR = 16;       // rows per item of the G products
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
 // explicit front inverse blocks (G) for one-product-per-front solves; MSFV_MF_G=0 keeps the staged sweeps
+// SMs left to the backward basis sweeps (k_basis_bwd, side stream) while the
+// multifrontal kernels run: the latency-bound coarse work keeps the rest
+int mf_reserved_sms() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MSFV_BWD_SMS");
+    v = e ? std::max(0, atoi(e)) : 32;
+  }
+  return v;
+}
 static bool mf_two_phase() {
   static int v = -1;
   if (v < 0) {
@@ -2987,7 +2997,7 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor2, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
-    coop_grid = (coop && per_sm > 0) ? sms * std::min(per_sm, 2) : 0;
+    coop_grid = (coop && per_sm > 0) ? std::max(1, sms - mf_reserved_sms()) * std::min(per_sm, 2) : 0;
   }
   if (coop_grid <= 0) return cudaErrorNotSupported;
   const MfDev d = mf_dev(g, Ak);
@@ -3077,7 +3087,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
       e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
       if (e != cudaSuccess) return e;
-      coop_grid = coop ? sms : 0;
+      coop_grid = coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     }
     if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 8192 && !getenv("MSFV_MF_NOCOOP")) {
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs};

@@ -24,7 +24,8 @@ void count_launches(long long n);
 // record msg as msfv_last_error() and return code (msfv_capi.cu)
 int set_error(int code, const std::string& msg);
 // multifrontal coarse plan (msfv_coarse.cu): built at plan creation when coarse_nd == 2
-bool mf_attach(Geo& g);   // false (and g.mf = nullptr) when the fronts exceed the kernels' shared memory
+bool mf_attach(Geo& g);
+int mf_reserved_sms();   // SMs the multifrontal kernels leave to the backward basis sweeps   // false (and g.mf = nullptr) when the fronts exceed the kernels' shared memory
 void mf_release(Geo& g);
 long long launch_count();
 

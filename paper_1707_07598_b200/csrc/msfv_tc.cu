@@ -1260,7 +1260,10 @@ static cudaError_t launch_basis_bwd_t(const Geo& g, const double* LT, double* Si
     const char* e = getenv("MSFV_BWD_FREE_SMS");
     free_sms = e ? std::max(0, atoi(e)) : 12;
   }
-  const int grid = std::max(1, std::min((g.nbl + BWD_WARPS - 1) / BWD_WARPS, sms - free_sms));
+  // multifrontal coarse path: the sweeps start right after the forward part
+  // and run on the SMs the coarse kernels leave free (mf_reserved_sms)
+  const int want = g.coarse_nd == 2 ? std::max(1, mf_reserved_sms()) : sms - free_sms;
+  const int grid = std::max(1, std::min((g.nbl + BWD_WARPS - 1) / BWD_WARPS, want));
   k_basis_bwd<PT><<<grid, BWD_WARPS * 32, 0, st>>>(g, LT, Sint);
   count_launches(1);
   return cudaGetLastError();

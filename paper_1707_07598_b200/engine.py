@@ -122,6 +122,7 @@ class Engine:
         self.factor_doubles = info[_lib.INFO_FACTOR_DOUBLES]
         self.scratch_doubles = info[_lib.INFO_SCRATCH_DOUBLES]
         self.tensor_core = bool(info[_lib.INFO_TC])
+        self.coarse_multifrontal = info[_lib.INFO_COARSE] == 2
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._csc = None
 

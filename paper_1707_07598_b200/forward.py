@@ -156,6 +156,8 @@ def _coarse_solve_chain(eng, op, survey, basis, shift, fl):
     ns = survey.n_sources
     F = eng.restrict_points(Qp, basis.sint_for(Qp), None, ns)        # S^T Q   (forward.py:115)
     Ak = eng.galerkin(basis.Kloc, shift)                              # S^T A S (+ shift I) (forward.py:118,125)
+    if eng.coarse_multifrontal:
+        basis.start_backward()                                        # S_I sweeps beside the whole coarse phase
     eng.coarse_factor(Ak, fl)                                         # cho_factor (forward.py:121)
     basis.start_backward()                                            # S_I sweeps overlap the coarse solve
     T = eng.coarse_solve(Ak, F)                                       # T = A_k^-1 S^T Q (forward.py:142)
