@@ -183,6 +183,16 @@ MSFV_API int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points
 MSFV_API int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
                         const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
                         const msfv_points* pr, const double* Rc, double* g, void* stream);
+/* Slab forms of msfv_operator / msfv_basis_forward for pipelining the model
+ * upload: msfv_operator_slab computes sigma on cell planes k0 .. min(k1, n3-1)
+ * and the edge weights of node planes k0..k1 (x-, y-edges) and cell planes
+ * k0..k1-1 (z-edges) -- the edges of the blocks with bk0*b3 = k0, bk1*b3 = k1;
+ * it reads m on cell planes k0 .. min(k1, n3-1) only.  msfv_basis_forward_slab
+ * builds the blocks bk0 <= bk < bk1 (their w must be complete). */
+MSFV_API int msfv_operator_slab(const msfv_plan* plan, const double* m, double* sigma, double* w, int32_t* flags,
+                                int32_t k0, int32_t k1, void* stream);
+MSFV_API int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* factor, double* Sint,
+                                     double* Kloc, int32_t* flags, int32_t bk0, int32_t bk1, void* stream);
 /* Same, for the blocks of the z-slab bk0 <= bk < bk1 only (they own the cells
  * with bk0*b3 <= k < bk1*b3, a contiguous range of g): lets the host copy
  * finished slabs of g back while the next slab is computed. */

@@ -69,6 +69,8 @@ SIGNATURES = {
     "msfv_points_interior_scatter": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_points_interior_solve": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P]),
     "msfv_block_gradient": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
+    "msfv_operator_slab": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _P]),
+    "msfv_basis_forward_slab": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P]),
     "msfv_block_gradient_slab": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I32, _P, _P]),
     "msfv_jv_coarse_rhs": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "msfv_coarse_dense": (ctypes.c_int, [_P, _P, _D, _P, _P]),

@@ -67,14 +67,15 @@ __global__ void k_edge_weights(Geo g, const double* __restrict__ cv, double* __r
 // division and the four cell loads of a warp are coalesced rows.
 constexpr int EW_THREADS = 128;
 __global__ void __launch_bounds__(EW_THREADS) k_edge_weights_lines(Geo g, const double* __restrict__ cv,
-                                                                  double* __restrict__ w) {
+                                                                  double* __restrict__ w, int k0, int k1) {
+  // planes k0 <= k <= k1 for x- and y-edges (node planes), k0 <= k < k1 for z-edges (cell planes)
   const int ax = blockIdx.z;
   const int nx = ax == 0 ? g.n1 : g.n1 + 1;                  // edges along x in a line
   const int ny = ax == 1 ? g.n2 : g.n2 + 1;                  // lines per z plane
   const int i = blockIdx.x * EW_THREADS + threadIdx.x;
   if (i >= nx) return;
-  const int j = blockIdx.y % ny, k = blockIdx.y / ny;
-  if (k >= (ax == 2 ? g.n3 : g.n3 + 1)) return;
+  const int j = blockIdx.y % ny, k = k0 + (int)(blockIdx.y / ny);
+  if (k > (ax == 2 ? k1 - 1 : k1) || k >= (ax == 2 ? g.n3 : g.n3 + 1)) return;
   const long long e = (ax == 0 ? 0 : (ax == 1 ? g.Ex : g.Ex + g.Ey)) + i + (long long)nx * (j + (long long)ny * k);
   double sum = 0.0;
 #pragma unroll
@@ -720,10 +721,18 @@ cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaS
   const unsigned lines = (unsigned)((long long)(g.n2 + 1) * (g.n3 + 1));
   if (lines < 65535u) {
     const dim3 grid(nblk(g.n1 + 1, EW_THREADS), lines, 3);
-    k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w);
+    k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w, 0, g.n3);
   } else {
     k_edge_weights<<<nblk(g.E, 256), 256, 0, st>>>(g, cv, w);
   }
+  count_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_edge_weights_planes(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st) {
+  const unsigned lines = (unsigned)((long long)(g.n2 + 1) * (k1 - k0 + 1));
+  if (k1 < k0 || lines >= 65535u) return cudaErrorInvalidValue;
+  const dim3 grid(nblk(g.n1 + 1, EW_THREADS), lines, 3);
+  k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w, k0, k1);
   count_launches(1);
   return cudaGetLastError();
 }

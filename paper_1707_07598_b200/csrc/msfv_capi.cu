@@ -324,6 +324,20 @@ int msfv_operator(const msfv_plan* plan, const double* m, double* sigma, double*
   return cuda_check(launch_edge_weights(plan->g, sigma, w, st), "edge_weights");
 }
 
+int msfv_operator_slab(const msfv_plan* plan, const double* m, double* sigma, double* w, int32_t* flags, int32_t k0,
+                       int32_t k1, void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  if (k0 < 0 || k1 > g.n3 || k0 >= k1) return fail(MSFV_SHAPE, "bad operator slab");
+  cudaStream_t st = (cudaStream_t)stream;
+  // sigma on cell planes k0 .. min(k1, n3 - 1) (plane k1 feeds the slab's top x/y edges)
+  const long long plane = (long long)g.n1 * g.n2;
+  const int kc1 = std::min(k1 + 1, g.n3);
+  int rc = cuda_check(launch_sigma(plane * (kc1 - k0), m + plane * k0, nullptr, sigma + plane * k0, flags, st), "sigma");
+  if (rc) return rc;
+  return cuda_check(launch_edge_weights_planes(g, sigma, w, k0, k1, st), "edge_weights");
+}
+
 int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* dm, double* tmp, double* c,
                       void* stream) {
   CHECK_PLAN(plan);
@@ -333,6 +347,18 @@ int msfv_edge_average(const msfv_plan* plan, const double* sigma, const double* 
   return cuda_check(launch_edge_weights(plan->g, tmp, c, st), "edge_average");
 }
 
+static int ensure_skel(msfv_plan* pl) {
+  if (pl->skel_dev) return MSFV_OK;
+  const std::vector<SkelEdge> tab = skeleton_edges(pl->g);
+  cudaError_t e = cudaMalloc(&pl->skel_dev, std::max<size_t>(tab.size(), 1) * sizeof(SkelEdge));
+  if (e == cudaSuccess && !tab.empty())
+    e = cudaMemcpy(pl->skel_dev, tab.data(), tab.size() * sizeof(SkelEdge), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_check(e, "skeleton edge table");
+  pl->g.skel = pl->skel_dev;
+  pl->g.nskel = (int)tab.size();
+  return MSFV_OK;
+}
+
 static int basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                        double* scratch, int32_t* flags, void* stream, bool bwd) {
   CHECK_PLAN(plan);
@@ -340,15 +366,8 @@ static int basis_build(const msfv_plan* plan, const double* w, double* factor, d
   cudaStream_t st = (cudaStream_t)stream;
   if (tc_supported(g)) {
     msfv_plan* pl = const_cast<msfv_plan*>(plan);
-    if (!pl->skel_dev) {
-      const std::vector<SkelEdge> tab = skeleton_edges(g);
-      cudaError_t e = cudaMalloc(&pl->skel_dev, std::max<size_t>(tab.size(), 1) * sizeof(SkelEdge));
-      if (e == cudaSuccess && !tab.empty())
-        e = cudaMemcpy(pl->skel_dev, tab.data(), tab.size() * sizeof(SkelEdge), cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return cuda_check(e, "skeleton edge table");
-      pl->g.skel = pl->skel_dev;
-      pl->g.nskel = (int)tab.size();
-    }
+    int rc = ensure_skel(pl);
+    if (rc) return rc;
     return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, bwd), "basis_build");
   }
   double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
@@ -365,6 +384,21 @@ int msfv_basis_forward(const msfv_plan* plan, const double* w, double* factor, d
   CHECK_PLAN(plan);
   if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   return basis_build(plan, w, factor, Sint, Kloc, nullptr, flags, stream, false);
+}
+
+int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
+                            int32_t* flags, int32_t bk0, int32_t bk1, void* stream) {
+  CHECK_PLAN(plan);
+  const Geo& g = plan->g;
+  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  if (bk0 < 0 || bk1 > g.nb3 || bk0 >= bk1) return fail(MSFV_SHAPE, "bad basis slab");
+  msfv_plan* pl = const_cast<msfv_plan*>(plan);
+  int rc = ensure_skel(pl);
+  if (rc) return rc;
+  const int per = g.nb1 * g.nb2;
+  return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, (cudaStream_t)stream, false, bk0 * per,
+                                    bk1 * per),
+                    "basis_forward_slab");
 }
 
 int msfv_basis_backward(const msfv_plan* plan, const double* factor, double* Sint, void* stream) {

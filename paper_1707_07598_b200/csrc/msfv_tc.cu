@@ -660,13 +660,13 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
 template <int PT, bool BWD, unsigned OM, int RF>
 __global__ void __launch_bounds__(TC_WARPS * 32)
 k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double* __restrict__ Sint,
-           double* __restrict__ Kloc, int* __restrict__ flags) {
+           double* __restrict__ Kloc, int* __restrict__ flags, int jb0, int jb1) {
   __shared__ __align__(16) double Dsh[TC_WARPS][64];
   __shared__ __align__(16) double Ish[TC_WARPS][72];
   extern __shared__ __align__(16) double tcsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int jb = blockIdx.x * TC_WARPS + wid;
-  if (jb >= g.nbl) return;
+  const int jb = jb0 + blockIdx.x * TC_WARPS + wid;
+  if (jb >= jb1) return;
   const int NTI = (g.nI + 7) >> 3, NR = 8 * NTI;
   const int NF = face_off(g, 5) + g.ni1 * g.ni2;
   const int AFE = (NR * AROW + NF + 1) & ~1;   // stencil table + face conductances, even
@@ -843,10 +843,10 @@ __global__ void __launch_bounds__(BWD_WARPS * 32) k_basis_bwd(Geo g, const doubl
 // lacks are skipped; the pinned node has no row of S).
 constexpr int SKEL_WARPS = 4;
 __global__ void __launch_bounds__(SKEL_WARPS * 32) k_skel_galerkin(Geo g, const double* __restrict__ w,
-                                                                  double* __restrict__ Kloc) {
+                                                                  double* __restrict__ Kloc, int jb0, int jb1) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int jb = blockIdx.x * SKEL_WARPS + wid;
-  if (jb >= g.nbl) return;
+  const int jb = jb0 + blockIdx.x * SKEL_WARPS + wid;
+  if (jb >= jb1) return;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
   const int lx = bi == g.nb1 - 1, ly = bj == g.nb2 - 1, lz = bk == g.nb3 - 1;
@@ -913,11 +913,12 @@ __host__ __device__ inline int skel_lines_axis(int bp, int bq, int lp, int lq) {
   return (bp + lp) + (bq - 1) * (1 + lp) + lq * (bp + lp);
 }
 __global__ void __launch_bounds__(SKL_WARPS * 32) k_skel_lines(Geo g, const double* __restrict__ w,
-                                                              double* __restrict__ Kloc, int rec_max) {
+                                                              double* __restrict__ Kloc, int rec_max, int jb0,
+                                                              int jb1) {
   extern __shared__ __align__(16) double skl[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int jb = blockIdx.x * SKL_WARPS + wid;
-  if (jb >= g.nbl) return;
+  const int jb = jb0 + blockIdx.x * SKL_WARPS + wid;
+  if (jb >= jb1) return;
   double* ra = skl + (size_t)wid * rec_max * 16;   // record r: a[8] at 16r, b[8] at 16r + 8
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
@@ -1158,8 +1159,9 @@ size_t tc_scratch_doubles(const Geo&) { return 0; }
 
 template <int PT, unsigned OM, int RF = 0>
 static cudaError_t launch_basis_tc_k(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
-                                     int* flags, bool bwd, cudaStream_t st) {
-  const unsigned grid = (unsigned)((g.nbl + TC_WARPS - 1) / TC_WARPS);
+                                     int* flags, bool bwd, cudaStream_t st, int jb0, int jb1) {
+  const unsigned grid = (unsigned)((jb1 - jb0 + TC_WARPS - 1) / TC_WARPS);
+  if (grid == 0) return cudaSuccess;
   const size_t nf = 2 * ((size_t)g.ni2 * g.ni3 + (size_t)g.ni1 * g.ni3 + (size_t)g.ni1 * g.ni2);
   const size_t smem =
       (size_t)TC_WARPS * (((((g.nI + 7) / 8) * 8 * AROW + nf + 1) & ~(size_t)1) + (OM ? 2 * (PT + 1) * 64 : 0)) *
@@ -1170,9 +1172,9 @@ static cudaError_t launch_basis_tc_k(const Geo& g, const double* w, double* LT, 
     e = cudaFuncSetAttribute(k_basis_tc<PT, false, OM, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (bwd)
-    k_basis_tc<PT, true, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, true, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags, jb0, jb1);
   else
-    k_basis_tc<PT, false, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags);
+    k_basis_tc<PT, false, OM, RF><<<grid, TC_WARPS * 32, smem, st>>>(g, w, LT, Sint, Kloc, flags, jb0, jb1);
   return cudaSuccess;
 }
 // lean main loop for 7x7x7 interiors (every 3D BASELINE config: 8^3-cell
@@ -1185,20 +1187,20 @@ static int basis_variant(const Geo& g) {
 }
 template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
-                                     double* Kloc, int* flags, bool bwd, cudaStream_t st) {
+                                     double* Kloc, int* flags, bool bwd, cudaStream_t st, int jb0, int jb1) {
   cudaError_t e;
   if constexpr (PT == 7) {
     const int v = basis_variant(g);
     if (v == 1)
-      e = launch_basis_tc_k<7, 0xC3u, 0>(g, w, LT, Sint, Kloc, flags, bwd, st);
+      e = launch_basis_tc_k<7, 0xC3u, 0>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     else if (v == 2)
-      e = launch_basis_tc_k<7, 0xC3u, 1>(g, w, LT, Sint, Kloc, flags, bwd, st);
+      e = launch_basis_tc_k<7, 0xC3u, 1>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     else if (v == 3)
-      e = launch_basis_tc_k<7, 0xC3u, 2>(g, w, LT, Sint, Kloc, flags, bwd, st);
+      e = launch_basis_tc_k<7, 0xC3u, 2>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     else
-      e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+      e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
   } else {
-    e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    e = launch_basis_tc_k<PT, 0u>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
   }
   if (e != cudaSuccess) return e;
   count_launches(1);
@@ -1212,9 +1214,11 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
       cudaError_t e2 = cudaFuncSetAttribute(k_skel_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e2 != cudaSuccess) return e2;
     }
-    k_skel_lines<<<(unsigned)((g.nbl + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, sm, st>>>(g, w, Kloc, rec_max);
+    k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, sm, st>>>(g, w, Kloc, rec_max,
+                                                                                              jb0, jb1);
   } else
-    k_skel_galerkin<<<(unsigned)((g.nbl + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc);
+    k_skel_galerkin<<<(unsigned)((jb1 - jb0 + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc,
+                                                                                                     jb0, jb1);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -1233,16 +1237,17 @@ static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const doubl
 }
 
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
-                            int* flags, cudaStream_t st, bool bwd) {
+                            int* flags, cudaStream_t st, bool bwd, int jb0, int jb1) {
+  if (jb1 < 0) jb1 = g.nbl;
   switch (tc_band(g)) {
-    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Kloc, flags, bwd, st);
-    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Kloc, flags, bwd, st);
+    case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 2: return launch_basis_tc_t<2>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 3: return launch_basis_tc_t<3>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 4: return launch_basis_tc_t<4>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 5: return launch_basis_tc_t<5>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 6: return launch_basis_tc_t<6>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
+    case 7: return launch_basis_tc_t<7>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -192,6 +192,44 @@ class Engine:
                                                  stream()), "basis_forward")
         return factor, Sint, Kloc, fl
 
+    def build_pipelined(self, m_host, chunks=4):
+        """Model upload in z-slabs on the copy stream with the operator and the
+        forward basis build of each slab queued behind its copy (the upload
+        of slab i + 1 overlaps the build of slab i).  Returns
+        (m_dev, sigma, w, flags, factor, Sint, Kloc)."""
+        n1, n2, n3 = self.cells
+        b3 = self.blocks[2]
+        nb3 = n3 // b3
+        plane = n1 * n2
+        m_dev, sigma, w, fl = self.empty(self.Nm), self.empty(self.Nm), self.empty(self.E), self.flags()
+        factor = self.empty(max(self.factor_doubles, 1))
+        Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
+        Kloc = self.empty(self.nbl * 64)
+        cur, cp = torch.cuda.current_stream(), self.copy_stream
+        chunks = max(1, min(chunks, nb3))
+        bounds = [round(i * nb3 / chunks) for i in range(chunks + 1)]
+        ready = torch.cuda.Event()
+        ready.record(cur)                       # m_dev / flags allocated and zeroed on the current stream
+        cp.wait_event(ready)
+        evs = []
+        with torch.cuda.stream(cp):
+            for c in range(chunks):
+                k0, kc1 = bounds[c] * b3, min(bounds[c + 1] * b3 + 1, n3)
+                m_dev[k0 * plane:kc1 * plane].copy_(m_host[k0 * plane:kc1 * plane], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cp)
+                evs.append(ev)
+        m_dev.record_stream(cp)
+        with phase("operator+basis (pipelined)"):
+            for c in range(chunks):
+                bk0, bk1 = bounds[c], bounds[c + 1]
+                cur.wait_event(evs[c])
+                _lib.check(self.L.msfv_operator_slab(self.plan, ptr(m_dev), ptr(sigma), ptr(w), ptr(fl), bk0 * b3,
+                                                     bk1 * b3, stream()), "operator_slab")
+                _lib.check(self.L.msfv_basis_forward_slab(self.plan, ptr(w), ptr(factor), ptr(Sint), ptr(Kloc),
+                                                          ptr(fl), bk0, bk1, stream()), "basis_forward_slab")
+        return m_dev, sigma, w, fl, factor, Sint, Kloc
+
     def basis_backward(self, factor, Sint):
         """Split build, part 2 (on the current stream): Sint = S_I."""
         _lib.check(self.L.msfv_basis_backward(self.plan, ptr(factor), ptr(Sint), stream()), "basis_backward")
