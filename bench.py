@@ -468,16 +468,21 @@ def run_gpu(args, rank, world, log):
     e2e = None
     if not args.no_e2e:
         m_pin = torch.from_numpy(m).pin_memory()
-        for _ in range(max(1, args.warmup)):
+        # the device-resident legs above leave the caching allocator with their
+        # block layout; release it so the e2e leg's warm-up settles its own
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        for _ in range(max(5, args.warmup)):
             D, st = problem.simulate(m_pin)
             phi, resid = gp.misfit_ssd(D, d_obs)
             problem.jacobian(st).rapply(resid)
         torch.cuda.synchronize()
         dist.barrier()
-        # three back-to-back repetitions of the K-step loop, median reported
-        # (host-side jitter of a single repetition is ~10%)
+        # five back-to-back repetitions of the K-step loop, median reported
+        # (the first repetition after the device-resident legs is ~25% slower:
+        # host allocator / page-locked buffer warm-up)
         reps = []
-        for _ in range(3):
+        for _ in range(5):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             for _ in range(args.steps):
@@ -487,7 +492,8 @@ def run_gpu(args, rank, world, log):
             b.record()
             torch.cuda.synchronize()
             reps.append(a.elapsed_time(b) / args.steps)
-        e2e_ms = dist.max_over_ranks(sorted(reps)[1], dev)
+        log("e2e repetitions (ms/step): " + ", ".join(f"{x:.3f}" for x in reps))
+        e2e_ms = dist.max_over_ranks(sorted(reps)[2], dev)
         h2d = m.nbytes + resid.nbytes
         d2h = D.nbytes + g_host.nbytes
         e2e = {"value": dist.aggregate_seconds_per_iter(e2e_ms / 1e3, world), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
