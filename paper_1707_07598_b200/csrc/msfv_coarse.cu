@@ -1753,6 +1753,8 @@ struct MfFront {
   int c[2];               // children (-1: none)
   int goff;               // gid table offset (NT*TB entries, -1 = padding)
   int moff[2];            // child maps (NT*TB entries: child-local row or -1)
+  int parent, pslot;      // parent front (-1: root) and which of its children this is
+  int upoff;              // up map (NT*TB entries: parent-local row of this front's B rows, else -1)
   long long goff2;        // G = [L_EE^-1 ; -L_BE L_EE^-1] (NT*TB x NE*TB) then G^T, row-major
 };
 
@@ -1889,6 +1891,34 @@ static MfPlan* mf_build(const Geo& g) {
         const int u = P->gid[F.goff + r];
         P->maps.push_back(u >= 0 ? where[u] : -1);
       }
+    }
+  }
+  // parents and up maps (child B row -> parent-local row)
+  for (int f = 0; f < nf; ++f) {
+    P->fr[f].parent = -1;
+    P->fr[f].pslot = 0;
+  }
+  for (int f = 0; f < nf; ++f)
+    for (int sl = 0; sl < 2; ++sl)
+      if (P->fr[f].c[sl] >= 0) {
+        P->fr[P->fr[f].c[sl]].parent = f;
+        P->fr[P->fr[f].c[sl]].pslot = sl;
+      }
+  for (int f = 0; f < nf; ++f) {
+    MfFront& F = P->fr[f];
+    F.upoff = (int)P->maps.size();
+    std::vector<int> prow;
+    if (F.parent >= 0) {
+      const MfFront& Pa = P->fr[F.parent];
+      prow.assign(g.kc, -1);
+      for (int r = 0; r < Pa.NT * TB; ++r) {
+        const int u = P->gid[Pa.goff + r];
+        if (u >= 0) prow[u] = r;
+      }
+    }
+    for (int r = 0; r < F.NT * TB; ++r) {
+      const int u = P->gid[F.goff + r];
+      P->maps.push_back(F.parent >= 0 && r >= F.NE * TB && u >= 0 ? prow[u] : -1);
     }
   }
   // levels by height (leaves = 0)
@@ -2965,6 +2995,208 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   }
 }
 
+// Solve with scatters instead of gather phases (15 grid barriers instead of
+// 29): phase 0 gathers X onto every front's E rows (XE) and zeroes the child
+// slots S0/S1; a forward item sums XE + S0 + S1 for its input rows and
+// writes y_E (Vout) and its c_B rows straight into its parent's slot
+// S_{pslot} at fixed rows (no atomics: each slot row has one writer); a
+// backward item reads [y_E; x_B] (x_B in Zb, written by the parent), writes
+// x_E to X and to its children's Zb rows.  Zb reuses the XE workspace.
+struct MfSolveJob2 {
+  MfDev d;
+  const int* lvl_off;
+  int nl, nfront;
+  long long vrows;
+  double* X;
+  double* W;            // 4 x vrows x nrhs: Vout | XE (Zb) | S0 | S1
+  int nrhs;
+};
+__global__ void __launch_bounds__(256, 1) k_mf_solve_coop2(MfSolveJob2 job) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ int pre[MF_MAXF + 1];
+  cg::grid_group grid = cg::this_grid();
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  unsigned ph = 0;
+  const MfDev& d = job.d;
+  const int nrhs = job.nrhs;
+  const size_t ws = (size_t)job.vrows * nrhs;
+  double* Vout = job.W;
+  double* XE = Vout + ws;
+  double* S0 = XE + ws;
+  double* S1 = S0 + ws;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
+  // ---- phase 0: XE = X on E rows, slots zero
+  (void)gtid;
+  (void)gstride;
+  for (int f = blockIdx.x; f < job.nfront; f += gridDim.x) {
+    const MfFront F = d.fr[f];
+    const size_t vo = (size_t)F.voff * nrhs;
+    const int* gid = d.gid + F.goff;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < F.NT * TB * nrhs; t += blockDim.x) {
+      const int r = t / nrhs, s2 = t % nrhs;
+      XE[vo + t] = r < F.nE ? __ldcg(job.X + (size_t)gid[r] * nrhs + s2) : 0.0;
+      S0[vo + t] = 0.0;
+      S1[vo + t] = 0.0;
+    }
+  }
+  grid.sync();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int li = 0; li < job.nl; ++li) {
+      const int l = pass == 0 ? li : job.nl - 1 - li;
+      const int l0 = job.lvl_off[l], nf = job.lvl_off[l + 1] - l0;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const MfFront F = d.fr[d.lvl[l0 + i]];
+        pre[i + 1] = pass == 0 ? (F.NT * TB + MF_GR - 1) / MF_GR : (F.nE + MF_GR - 1) / MF_GR;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pre[0] = 0;
+        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+      }
+      __syncthreads();
+      int fi = 0;
+      for (int gi = blockIdx.x; gi < pre[nf]; gi += gridDim.x) {
+        while (pre[fi + 1] <= gi) ++fi;
+        const MfFront F = d.fr[d.lvl[l0 + fi]];
+        const int rows = F.NT * TB, ncol = F.NE * TB;
+        const size_t vo = (size_t)F.voff * nrhs;
+        if (pass == 0) {
+          const int r0c = (gi - pre[fi]) * MF_GR, nr = min(MF_GR, rows - r0c);
+          const int kmax = r0c < ncol ? min(ncol, ((r0c + nr - 1) / TB + 1) * TB) : ncol;
+          double* Gs = sh;
+          double* vs = Gs + (size_t)MF_GR * ncol;          // XE rows [0, kmax)
+          double* v0s = vs + (size_t)ncol * nrhs;           // S0 rows [0, kmax)
+          double* v1s = v0s + (size_t)ncol * nrhs;          // S1 rows [0, kmax)
+          double* a0s = v1s + (size_t)ncol * nrhs;          // S0 rows of the chunk (B rows)
+          double* a1s = a0s + (size_t)MF_GR * nrhs;         // S1 rows of the chunk
+          const bool brow = r0c >= ncol;
+          if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bg = (unsigned)(nr * ncol * sizeof(double)), bv = (unsigned)(kmax * nrhs * sizeof(double));
+            const unsigned ba = brow ? (unsigned)(nr * nrhs * sizeof(double)) : 0u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)),
+                         "r"(bg + 3 * bv + 2 * ba)
+                         : "memory");
+            auto cp = [&](void* dst, const void* src, unsigned bytes) {
+              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                               smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(&bar))
+                           : "memory");
+            };
+            cp(Gs, d.base + F.goff2 + (size_t)r0c * ncol, bg);
+            cp(vs, XE + vo, bv);
+            cp(v0s, S0 + vo, bv);
+            cp(v1s, S1 + vo, bv);
+            if (ba) {
+              cp(a0s, S0 + vo + (size_t)r0c * nrhs, ba);
+              cp(a1s, S1 + vo + (size_t)r0c * nrhs, ba);
+            }
+          }
+          mbar_wait(&bar, ph);
+          ph ^= 1;
+          // input = XE + S0 + S1 (fixed order); B rows add S0 + S1
+          for (int t = threadIdx.x; t < kmax * nrhs; t += blockDim.x) vs[t] = (vs[t] + v0s[t]) + v1s[t];
+          double* addv = a0s;
+          if (brow)
+            for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) a0s[t] = a0s[t] + a1s[t];
+          __syncthreads();
+          const int* up = d.maps + F.upoff;
+          double* pslot = nullptr;
+          size_t pvo = 0;
+          if (F.parent >= 0) {
+            pslot = F.pslot ? S1 : S0;
+            pvo = (size_t)d.fr[F.parent].voff * nrhs;
+          }
+          for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) {
+            const int ii = t / nrhs, s2 = t % nrhs, r = r0c + ii;
+            const double* Gr = Gs + (size_t)ii * ncol;
+            const int kend = r < ncol ? min(ncol, (r / TB + 1) * TB) : ncol;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int k = 0;
+            for (; k + 3 < kend; k += 4) {
+              a0 = fma(Gr[k], vs[(size_t)k * nrhs + s2], a0);
+              a1 = fma(Gr[k + 1], vs[(size_t)(k + 1) * nrhs + s2], a1);
+              a2 = fma(Gr[k + 2], vs[(size_t)(k + 2) * nrhs + s2], a2);
+              a3 = fma(Gr[k + 3], vs[(size_t)(k + 3) * nrhs + s2], a3);
+            }
+            for (; k < kend; ++k) a0 = fma(Gr[k], vs[(size_t)k * nrhs + s2], a0);
+            double a = (a0 + a1) + (a2 + a3);
+            if (r < ncol) {
+              Vout[vo + (size_t)r * nrhs + s2] = a;
+            } else {
+              a += addv[(size_t)ii * nrhs + s2];
+              const int q = up[r];
+              if (pslot && q >= 0) pslot[pvo + (size_t)q * nrhs + s2] = a;
+            }
+          }
+        } else {
+          double* Zb = XE;
+          const int j0 = (gi - pre[fi]) * MF_GR, nj = min(MF_GR, F.nE - j0);
+          const int rz0 = (j0 / TB) * TB;
+          double* Gs = sh;
+          double* zs = Gs + (size_t)MF_GR * rows;
+          if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bg = (unsigned)(nj * rows * sizeof(double));
+            const unsigned be = (unsigned)((ncol - rz0) * nrhs * sizeof(double));
+            const unsigned bb = (unsigned)((rows - ncol) * nrhs * sizeof(double));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(bg + be + bb)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(Gs)),
+                         "l"(d.base + F.goff2 + (size_t)F.NT * F.NE * TT + (size_t)j0 * rows), "r"(bg), "r"(smem_u32(&bar))
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(zs + (size_t)rz0 * nrhs)), "l"(Vout + vo + (size_t)rz0 * nrhs), "r"(be),
+                         "r"(smem_u32(&bar))
+                         : "memory");
+            if (bb)
+              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                               smem_u32(zs + (size_t)ncol * nrhs)), "l"(Zb + vo + (size_t)ncol * nrhs), "r"(bb),
+                           "r"(smem_u32(&bar))
+                           : "memory");
+          }
+          mbar_wait(&bar, ph);
+          ph ^= 1;
+          const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
+          const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
+          const size_t c0o = m0 ? (size_t)d.fr[F.c[0]].voff * nrhs : 0, c1o = m1 ? (size_t)d.fr[F.c[1]].voff * nrhs : 0;
+          for (int t = threadIdx.x; t < nj * nrhs; t += blockDim.x) {
+            const int ii = t / nrhs, s2 = t % nrhs, j = j0 + ii;
+            const double* Gr = Gs + (size_t)ii * rows;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int r = rz0;
+            for (; r + 3 < rows; r += 4) {
+              a0 = fma(Gr[r], zs[(size_t)r * nrhs + s2], a0);
+              a1 = fma(Gr[r + 1], zs[(size_t)(r + 1) * nrhs + s2], a1);
+              a2 = fma(Gr[r + 2], zs[(size_t)(r + 2) * nrhs + s2], a2);
+              a3 = fma(Gr[r + 3], zs[(size_t)(r + 3) * nrhs + s2], a3);
+            }
+            for (; r < rows; ++r) a0 = fma(Gr[r], zs[(size_t)r * nrhs + s2], a0);
+            const double x = (a0 + a1) + (a2 + a3);
+            job.X[(size_t)d.gid[F.goff + j] * nrhs + s2] = x;
+            if (m0) { const int q = m0[j]; if (q >= 0) Zb[c0o + (size_t)q * nrhs + s2] = x; }
+            if (m1) { const int q = m1[j]; if (q >= 0) Zb[c1o + (size_t)q * nrhs + s2] = x; }
+          }
+          // this front's x_B rows travel on to its children (first chunk's CTA)
+          if (j0 == 0 && (m0 || m1)) {
+            for (int t = threadIdx.x; t < (rows - ncol) * nrhs; t += blockDim.x) {
+              const int p = ncol + t / nrhs, s2 = t % nrhs;
+              const double x = zs[(size_t)p * nrhs + s2];
+              if (m0) { const int q = m0[p]; if (q >= 0) Zb[c0o + (size_t)q * nrhs + s2] = x; }
+              if (m1) { const int q = m1[p]; if (q >= 0) Zb[c1o + (size_t)q * nrhs + s2] = x; }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+  }
+}
+
 static MfDev mf_dev(const Geo& g, double* base) {
   const MfPlan* P = mf_plan(g);
   return MfDev{P->d_fr, P->d_lvl, P->d_gid, P->d_maps, base};
@@ -3074,10 +3306,12 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
   }
   if (mf_use_g() && nrhs <= 64) {
     // one cooperative launch for both sweeps
-    size_t smc = 0;
+    size_t smc = 0, smc2 = 0;
     for (int l = 0; l < nl; ++l) {
       const int nt = level_nt(l);
       smc = std::max(smc, ((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs + (size_t)MF_GR * nrhs) * sizeof(double));
+      smc2 = std::max(smc2, ((size_t)MF_GR * nt * TB + (size_t)3 * nt * TB * nrhs + (size_t)2 * MF_GR * nrhs) *
+                                sizeof(double));
     }
     static int coop_grid = -1;
     if (coop_grid < 0) {
@@ -3090,6 +3324,20 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       coop_grid = coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     }
     if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 8192 && !getenv("MSFV_MF_NOCOOP")) {
+      if (getenv("MSFV_MF_SCATTER") && smc2 <= (size_t)MF_SMEM_MAX - 8192) {   // scatter variant: fewer barriers, slower at config 4
+        static bool a2 = false;
+        if (!a2) {
+          e = cudaFuncSetAttribute(k_mf_solve_coop2, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+          if (e != cudaSuccess) return e;
+          a2 = true;
+        }
+        MfSolveJob2 job2{d, P->d_lvloff, nl, (int)P->fr.size(), (long long)P->vrows, X, scratch, nrhs};
+        void* args2[] = {(void*)&job2};
+        e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop2, dim3(coop_grid), dim3(256), args2, smc2, st);
+        count_launches(1);
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+      }
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
@@ -3148,6 +3396,6 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
   return cudaGetLastError();
 }
 size_t mf_doubles(const Geo& g) { return mf_plan(g)->total; }
-int mf_tile_rows(const Geo& g) { return (int)(2 * mf_plan(g)->vrows / TB); }   // Vout + Vin workspaces
+int mf_tile_rows(const Geo& g) { return (int)(4 * mf_plan(g)->vrows / TB); }   // Vout, XE/Zb, S0, S1 workspaces
 
 }  // namespace msfv
