@@ -66,31 +66,34 @@ __global__ void k_edge_weights(Geo g, const double* __restrict__ cv, double* __r
 // (the two transverse indices), threads along x, so there is no index
 // division and the four cell loads of a warp are coalesced rows.
 constexpr int EW_THREADS = 128;
-__global__ void __launch_bounds__(EW_THREADS) k_edge_weights_lines(Geo g, const double* __restrict__ cv,
+constexpr int EW_LINES = 4;
+__global__ void __launch_bounds__(EW_THREADS * EW_LINES) k_edge_weights_lines(Geo g, const double* __restrict__ cv,
                                                                   double* __restrict__ w, int k0, int k1) {
   // planes k0 <= k <= k1 for x- and y-edges (node planes), k0 <= k < k1 for z-edges (cell planes)
+  // EW_LINES lines per CTA (blockIdx.y * EW_LINES + threadIdx.y), threads along x
   const int ax = blockIdx.z;
   const int nx = ax == 0 ? g.n1 : g.n1 + 1;                  // edges along x in a line
   const int ny = ax == 1 ? g.n2 : g.n2 + 1;                  // lines per z plane
-  const int i = blockIdx.x * EW_THREADS + threadIdx.x;
-  if (i >= nx) return;
-  const int j = blockIdx.y % ny, k = k0 + (int)(blockIdx.y / ny);
+  const int line = blockIdx.y * EW_LINES + threadIdx.y;
+  const int j = line % ny, k = k0 + line / ny;
   if (k > (ax == 2 ? k1 - 1 : k1) || k >= (ax == 2 ? g.n3 : g.n3 + 1)) return;
-  const long long e = (ax == 0 ? 0 : (ax == 1 ? g.Ex : g.Ex + g.Ey)) + i + (long long)nx * (j + (long long)ny * k);
-  double sum = 0.0;
+  const long long e0 = (ax == 0 ? 0 : (ax == 1 ? g.Ex : g.Ex + g.Ey)) + (long long)nx * (j + (long long)ny * k);
+  for (int i = threadIdx.x; i < nx; i += EW_THREADS) {
+    double sum = 0.0;
 #pragma unroll
-  for (int d2 = -1; d2 <= 0; ++d2) {
+    for (int d2 = -1; d2 <= 0; ++d2) {
 #pragma unroll
-    for (int d1 = -1; d1 <= 0; ++d1) {
-      int ci = i, cj = j, ck = k;
-      if (ax == 0) { cj += d1; ck += d2; }
-      else if (ax == 1) { ci += d1; ck += d2; }
-      else { ci += d1; cj += d2; }
-      if (ci < 0 || cj < 0 || ck < 0 || ci >= g.n1 || cj >= g.n2 || ck >= g.n3) continue;
-      sum = __dadd_rn(sum, __dmul_rn(g.qv, __ldg(cv + cell_id(g, ci, cj, ck))));
+      for (int d1 = -1; d1 <= 0; ++d1) {
+        int ci = i, cj = j, ck = k;
+        if (ax == 0) { cj += d1; ck += d2; }
+        else if (ax == 1) { ci += d1; ck += d2; }
+        else { ci += d1; cj += d2; }
+        if (ci < 0 || cj < 0 || ck < 0 || ci >= g.n1 || cj >= g.n2 || ck >= g.n3) continue;
+        sum = __dadd_rn(sum, __dmul_rn(g.qv, __ldg(cv + cell_id(g, ci, cj, ck))));
+      }
     }
+    w[e0 + i] = sum;
   }
-  w[e] = sum;
 }
 
 // ------------------------------------------------------------------ basis
@@ -718,10 +721,10 @@ cudaError_t launch_mul(long long n, const double* a, const double* b, double* ou
   return cudaGetLastError();
 }
 cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st) {
-  const unsigned lines = (unsigned)((long long)(g.n2 + 1) * (g.n3 + 1));
+  const unsigned lines = (unsigned)(((long long)(g.n2 + 1) * (g.n3 + 1) + EW_LINES - 1) / EW_LINES);
   if (lines < 65535u) {
-    const dim3 grid(nblk(g.n1 + 1, EW_THREADS), lines, 3);
-    k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w, 0, g.n3);
+    const dim3 grid(1, lines, 3);
+    k_edge_weights_lines<<<grid, dim3(EW_THREADS, EW_LINES), 0, st>>>(g, cv, w, 0, g.n3);
   } else {
     k_edge_weights<<<nblk(g.E, 256), 256, 0, st>>>(g, cv, w);
   }
@@ -729,10 +732,10 @@ cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaS
   return cudaGetLastError();
 }
 cudaError_t launch_edge_weights_planes(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st) {
-  const unsigned lines = (unsigned)((long long)(g.n2 + 1) * (k1 - k0 + 1));
+  const unsigned lines = (unsigned)(((long long)(g.n2 + 1) * (k1 - k0 + 1) + EW_LINES - 1) / EW_LINES);
   if (k1 < k0 || lines >= 65535u) return cudaErrorInvalidValue;
-  const dim3 grid(nblk(g.n1 + 1, EW_THREADS), lines, 3);
-  k_edge_weights_lines<<<grid, EW_THREADS, 0, st>>>(g, cv, w, k0, k1);
+  const dim3 grid(1, lines, 3);
+  k_edge_weights_lines<<<grid, dim3(EW_THREADS, EW_LINES), 0, st>>>(g, cv, w, k0, k1);
   count_launches(1);
   return cudaGetLastError();
 }
