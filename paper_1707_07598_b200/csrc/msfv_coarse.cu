@@ -3233,6 +3233,21 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
   }
   if (coop_grid <= 0) return cudaErrorNotSupported;
   const MfDev d = mf_dev(g, Ak);
+  // helper stream + events for the inverse blocks (created once per process)
+  static cudaStream_t inv_stream = nullptr;
+  static cudaEvent_t mf_events[64], mf_done;
+  static int inv_mode = -1;
+  if (inv_mode < 0) {
+    const char* ev = getenv("MSFV_MF_INV_SIDE");
+    inv_mode = ev ? (atoi(ev) != 0) : 0;   // opt-in: no gain at config 4, occasional placement stalls
+    if (inv_mode) {
+      cudaError_t e2 = cudaStreamCreateWithFlags(&inv_stream, cudaStreamNonBlocking);
+      for (int i = 0; i < 64 && e2 == cudaSuccess; ++i) e2 = cudaEventCreateWithFlags(&mf_events[i], cudaEventDisableTiming);
+      if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&mf_done, cudaEventDisableTiming);
+      if (e2 != cudaSuccess) inv_mode = 0;
+    }
+  }
+  const bool inv_side = inv_mode == 1 && P->lvl_off.size() <= 65;
   for (size_t l = 0; l + 1 < P->lvl_off.size(); ++l) {
     const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0;
     if (nf <= 0) continue;
@@ -3265,13 +3280,28 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
         attr = true;
       }
       if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
-      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, st>>>(d, l0);
+      // the inverse blocks of level l run on a helper stream beside the
+      // factorization of level l + 1 (they are needed only by the solves;
+      // their small grids land on the SMs the coarse kernels leave free)
+      cudaStream_t si = st;
+      if (inv_side) {
+        e = cudaEventRecord(mf_events[l], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(inv_stream, mf_events[l], 0);
+        if (e != cudaSuccess) return e;
+        si = inv_stream;
+      }
+      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, si>>>(d, l0);
       count_launches(1);
       if (nbmax > 0) {
-        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, st>>>(d, l0, nbmax);
+        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, si>>>(d, l0, nbmax);
         count_launches(1);
       }
     }
+  }
+  if (inv_side && mf_use_g()) {
+    e = cudaEventRecord(mf_done, inv_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, mf_done, 0);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
