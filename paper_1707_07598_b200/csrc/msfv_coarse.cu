@@ -1770,6 +1770,7 @@ struct MfPlan {
   int* d_gid = nullptr;
   int* d_maps = nullptr;
   int* d_lvloff = nullptr;
+  bool use_g = true;      // explicit inverse blocks fit the kernels' shared memory (else staged sweeps)
 };
 
 __host__ __device__ __forceinline__ Band mf_band(double* base, const MfFront& f) {
@@ -1999,11 +2000,14 @@ bool mf_attach(Geo& g) {
   const int nl = (int)P->lvl_off.size() - 1;
   int maxf = 0;
   for (int l = 0; l < nl; ++l) maxf = std::max(maxf, P->lvl_off[l + 1] - P->lvl_off[l]);
-  if (inv_b > (size_t)MF_SMEM_MAX || sol_b > (size_t)MF_SMEM_MAX - 8192 || maxf > MF_MAXF) {
+  if (maxf > MF_MAXF) {
     delete P;
     g.mf = nullptr;
     return false;
   }
+  // fronts too large for the explicit-inverse kernels (config 5's top levels):
+  // keep the multifrontal factorization, solve with the blocked sweeps
+  P->use_g = inv_b <= (size_t)MF_SMEM_MAX && sol_b <= (size_t)MF_SMEM_MAX - 8192;
   g.mf = P;
   return true;
 }
@@ -3197,6 +3201,181 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop2(MfSolveJob2 job) {
   }
 }
 
+// Blocked sweeps for fronts too large for the explicit inverse (config 5):
+// CTA (front, group of <= MF_CC right-hand sides); the front vector of the
+// group lives in shared memory, L's tile column J streams through a buffer of
+// MF_LCH tiles (bulk copies), 2x2-blocked FMA products.
+constexpr int MF_CC = 8;
+constexpr int MF_LCH = 8;
+__device__ __forceinline__ void mf_tma_tiles(double* dst, const double* src, int ntile, unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    const unsigned bytes = (unsigned)ntile * TT * sizeof(double);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+  }
+}
+__global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double* __restrict__ X,
+                                                  double* __restrict__ Vg, int ld, int ntmax) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int c0 = blockIdx.y * MF_CC, nc = min(MF_CC, ld - c0);
+  if (nc <= 0) return;
+  const Band B = mf_band(d.base, F);
+  const int rows = F.NT * TB;
+  double* V = sh;                                   // rows x MF_CC
+  double* Ls = V + (size_t)ntmax * TB * MF_CC;      // MF_LCH tiles
+  double* Dj = Ls + (size_t)MF_LCH * TT;
+  double* ys = Dj + TT;                             // TB x MF_CC
+  const int* gid = d.gid + F.goff;
+  const double* v0 = F.c[0] >= 0 ? Vg + (size_t)d.fr[F.c[0]].voff * ld : nullptr;
+  const double* v1 = F.c[1] >= 0 ? Vg + (size_t)d.fr[F.c[1]].voff * ld : nullptr;
+  const int* m0 = v0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = v1 ? d.maps + F.moff[1] : nullptr;
+  if (threadIdx.x == 0) mbar_init(&bar);
+#pragma unroll 4
+  for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
+    const int r = t / MF_CC, s = t % MF_CC;
+    double a = 0.0;
+    if (s < nc) {
+      if (r < F.nE) a = __ldcg(X + (size_t)gid[r] * ld + c0 + s);
+      if (m0) { const int q = m0[r]; if (q >= 0) a += __ldcg(v0 + (size_t)q * ld + c0 + s); }
+      if (m1) { const int q = m1[r]; if (q >= 0) a += __ldcg(v1 + (size_t)q * ld + c0 + s); }
+    }
+    V[t] = a;
+  }
+  __syncthreads();
+  unsigned ph = 0;
+  const int cp = threadIdx.x % (MF_CC / 2), rp = threadIdx.x / (MF_CC / 2);   // 2 rows x 2 rhs per thread
+  const int rstep = 2 * (blockDim.x / (MF_CC / 2));
+  for (int J = 0; J < F.NE; ++J) {
+    mf_tma_tiles(Dj, B.Dinv + (size_t)J * TT, 1, &bar);
+    mbar_wait(&bar, ph);
+    ph ^= 1;
+    for (int r0 = 2 * rp; r0 < TB; r0 += rstep) {
+      double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+      const double* vJ = V + (size_t)J * TB * MF_CC;
+#pragma unroll 8
+      for (int k = 0; k < TB; ++k) {
+        const double l0v = Dj[r0 * TB + k], l1v = Dj[(r0 + 1) * TB + k];
+        const double2 y = *reinterpret_cast<const double2*>(vJ + k * MF_CC + 2 * cp);
+        a00 = fma(l0v, y.x, a00);
+        a01 = fma(l0v, y.y, a01);
+        a10 = fma(l1v, y.x, a10);
+        a11 = fma(l1v, y.y, a11);
+      }
+      *reinterpret_cast<double2*>(ys + r0 * MF_CC + 2 * cp) = make_double2(a00, a01);
+      *reinterpret_cast<double2*>(ys + (r0 + 1) * MF_CC + 2 * cp) = make_double2(a10, a11);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TB * MF_CC; t += blockDim.x) V[(size_t)J * TB * MF_CC + t] = ys[t];
+    const int nb = F.NT - 1 - J;
+    for (int tc = 0; tc < nb; tc += MF_LCH) {
+      const int nt = min(MF_LCH, nb - tc);
+      __syncthreads();                                // previous chunk consumed
+      mf_tma_tiles(Ls, btile(B.Lo, B, J, 1 + tc), nt, &bar);
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+      double* vN = V + (size_t)(J + 1 + tc) * TB * MF_CC;
+      for (int r0 = 2 * rp; r0 < nt * TB; r0 += rstep) {
+        double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll 8
+        for (int k = 0; k < TB; ++k) {
+          const double l0v = Ls[(size_t)r0 * TB + k], l1v = Ls[(size_t)(r0 + 1) * TB + k];
+          const double2 y = *reinterpret_cast<const double2*>(ys + k * MF_CC + 2 * cp);
+          a00 = fma(l0v, y.x, a00);
+          a01 = fma(l0v, y.y, a01);
+          a10 = fma(l1v, y.x, a10);
+          a11 = fma(l1v, y.y, a11);
+        }
+        double2* o0 = reinterpret_cast<double2*>(vN + (size_t)r0 * MF_CC + 2 * cp);
+        double2* o1 = reinterpret_cast<double2*>(vN + (size_t)(r0 + 1) * MF_CC + 2 * cp);
+        const double2 p0 = *o0, p1 = *o1;
+        *o0 = make_double2(p0.x - a00, p0.y - a01);
+        *o1 = make_double2(p1.x - a10, p1.y - a11);
+      }
+    }
+    __syncthreads();
+  }
+  double* v = Vg + (size_t)F.voff * ld;
+  for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
+    const int r = t / MF_CC, s = t % MF_CC;
+    if (s < nc) v[(size_t)r * ld + c0 + s] = V[t];
+  }
+}
+__global__ void __launch_bounds__(256) k_mf_bwd_c(MfDev d, int l0, double* __restrict__ X,
+                                                  const double* __restrict__ Vg, int ld, int ntmax) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) unsigned long long bar;
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
+  const int c0 = blockIdx.y * MF_CC, nc = min(MF_CC, ld - c0);
+  if (nc <= 0) return;
+  const Band B = mf_band(d.base, F);
+  const int rows = F.NT * TB;
+  double* V = sh;
+  double* Ls = V + (size_t)ntmax * TB * MF_CC;
+  double* Dj = Ls + (size_t)MF_LCH * TT;
+  double* ys = Dj + TT;                             // TB x MF_CC (sums)
+  const int* gid = d.gid + F.goff;
+  const double* v = Vg + (size_t)F.voff * ld;
+  if (threadIdx.x == 0) mbar_init(&bar);
+#pragma unroll 4
+  for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
+    const int r = t / MF_CC, s = t % MF_CC;
+    double a = 0.0;
+    if (s < nc) {
+      if (r < F.NE * TB) a = __ldcg(v + (size_t)r * ld + c0 + s);
+      else if (gid[r] >= 0) a = __ldcg(X + (size_t)gid[r] * ld + c0 + s);
+    }
+    V[t] = a;
+  }
+  __syncthreads();
+  unsigned ph = 0;
+  // thread (column j, rhs s): one output per thread (32 x 8 = 256)
+  const int j = threadIdx.x / MF_CC, s = threadIdx.x % MF_CC;
+  for (int J = F.NE - 1; J >= 0; --J) {
+    const int nb = F.NT - 1 - J;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int tc = 0; tc < nb; tc += MF_LCH) {
+      const int nt = min(MF_LCH, nb - tc);
+      __syncthreads();
+      mf_tma_tiles(Ls, btile(B.Lo, B, J, 1 + tc), nt, &bar);
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+      if (j < TB) {
+        const double* vb = V + (size_t)(J + 1 + tc) * TB * MF_CC + s;
+        for (int rr = 0; rr < nt * TB; rr += 2) {
+          acc0 = fma(Ls[(size_t)rr * TB + j], vb[(size_t)rr * MF_CC], acc0);
+          acc1 = fma(Ls[(size_t)(rr + 1) * TB + j], vb[(size_t)(rr + 1) * MF_CC], acc1);
+        }
+      }
+    }
+    __syncthreads();
+    mf_tma_tiles(Dj, B.Dinv + (size_t)J * TT, 1, &bar);
+    if (j < TB) ys[j * MF_CC + s] = V[(size_t)(J * TB + j) * MF_CC + s] - (acc0 + acc1);
+    mbar_wait(&bar, ph);
+    ph ^= 1;
+    __syncthreads();
+    if (j < TB) {
+      double a = 0.0, b = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < TB; k += 2) {
+        a = fma(Dj[k * TB + j], ys[k * MF_CC + s], a);
+        b = fma(Dj[(k + 1) * TB + j], ys[(k + 1) * MF_CC + s], b);
+      }
+      V[(size_t)(J * TB + j) * MF_CC + s] = a + b;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < F.nE * MF_CC; t += blockDim.x) {
+    const int r = t / MF_CC, s2 = t % MF_CC;
+    if (s2 < nc) X[(size_t)gid[r] * ld + c0 + s2] = V[t];
+  }
+}
+
 static MfDev mf_dev(const Geo& g, double* base) {
   const MfPlan* P = mf_plan(g);
   return MfDev{P->d_fr, P->d_lvl, P->d_gid, P->d_maps, base};
@@ -3266,7 +3445,7 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
                                     dim3(256), args, 0, st);
     count_launches(1);
     if (e != cudaSuccess) return e;
-    if (mf_use_g()) {
+    if (mf_use_g() && P->use_g) {
       int nemax = 1, nbmax = 0;
       for (int i = 0; i < nf; ++i) {
         nemax = std::max(nemax, P->fr[P->lvl[l0 + i]].NE);
@@ -3298,7 +3477,7 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
       }
     }
   }
-  if (inv_side && mf_use_g()) {
+  if (inv_side && mf_use_g() && P->use_g) {
     e = cudaEventRecord(mf_done, inv_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, mf_done, 0);
     if (e != cudaSuccess) return e;
@@ -3307,6 +3486,7 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
 }
 cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* scratch, int nrhs, cudaStream_t st) {
   if (nrhs == 0) return cudaSuccess;
+  const bool force_c = getenv("MSFV_MF_FORCE_CHUNKED") != nullptr;   // test hook: the blocked sweeps at any size
   cudaError_t e = mf_upload(g);
   if (e != cudaSuccess) return e;
   const MfPlan* P = mf_plan(g);
@@ -3327,14 +3507,19 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
     return ((size_t)nt * TB * nrhs + (size_t)nt * TT + (size_t)3 * TB * nrhs) * sizeof(double) +
            (size_t)3 * nt * TB * sizeof(int) + 16;
   };
+  auto smem_c = [&](int nt) {
+    return ((size_t)nt * TB * MF_CC + (size_t)MF_LCH * TT + TT + (size_t)TB * MF_CC) * sizeof(double);
+  };
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(k_mf_fwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_fwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (mf_use_g() && nrhs <= 64) {
+  if (mf_use_g() && P->use_g && nrhs <= 64 && !force_c) {
     // one cooperative launch for both sweeps
     size_t smc = 0, smc2 = 0;
     for (int l = 0; l < nl; ++l) {
@@ -3376,12 +3561,12 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       return cudaGetLastError();
     }
   }
-  bool g_fits = true;
+  bool g_fits = !force_c;
   for (int l = 0; l < nl; ++l) {
     const int nt = level_nt(l);
     if (((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs) * sizeof(double) > (size_t)MF_SMEM_MAX) g_fits = false;
   }
-  if (mf_use_g() && g_fits) {
+  if (mf_use_g() && P->use_g && g_fits) {
     static bool gattr = false;
     if (!gattr) {
       e = cudaFuncSetAttribute(k_mf_gfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
@@ -3410,15 +3595,19 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
   }
   for (int l = 0; l < nl; ++l) {
     const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
-    if (smem_s(nt) <= MF_SMEM_MAX)
+    if (smem_s(nt) <= MF_SMEM_MAX && !force_c)
       k_mf_fwd_s<<<nf, 256, smem_s(nt), st>>>(d, l0, X, scratch, nrhs, nt);
+    else if (smem_c(nt) <= MF_SMEM_MAX - 8192)
+      k_mf_fwd_c<<<dim3(nf, (nrhs + MF_CC - 1) / MF_CC), 256, smem_c(nt), st>>>(d, l0, X, scratch, nrhs, nt);
     else
       k_mf_fwd<<<nf, 256, sm, st>>>(d, l0, X, scratch, nrhs);
   }
   for (int l = nl - 1; l >= 0; --l) {
     const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
-    if (smem_s(nt) <= MF_SMEM_MAX)
+    if (smem_s(nt) <= MF_SMEM_MAX && !force_c)
       k_mf_bwd_s<<<nf, 256, smem_s(nt), st>>>(d, l0, X, scratch, nrhs, nt);
+    else if (smem_c(nt) <= MF_SMEM_MAX - 8192)
+      k_mf_bwd_c<<<dim3(nf, (nrhs + MF_CC - 1) / MF_CC), 256, smem_c(nt), st>>>(d, l0, X, scratch, nrhs, nt);
     else
       k_mf_bwd<<<nf, 256, sm, st>>>(d, l0, X, scratch, nrhs);
   }

@@ -55,3 +55,27 @@ def test_config4_matches_oracle():
     # 128^3, 4096 local solves, sigma contrast ~2e6 (the north_star target config)
     errs = run_both(4)
     assert all(v <= TOL for v in errs.values()), errs
+
+
+@pytest.mark.gpu
+def test_multifrontal_blocked_sweeps_match_inverse_blocks():
+    """The blocked multifrontal sweeps (used for fronts too large for the
+    explicit inverse blocks, config 5) reproduce the default solves at config 4."""
+    import os
+    import torch
+    import paper_1707_07598_b200 as gp
+    from paper_1707_07598_b200.models import config_problem
+    mesh, part, survey, m = config_problem(4)
+    prob = gp.AdaptiveReducedProblem(gp.BasisBuilder(part), survey)
+    D, st = prob.simulate(m)
+    if not st.basis.engine.coarse_multifrontal:
+        pytest.skip("multifrontal coarse path not selected")
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((st.basis.engine.k, 16))
+    X0 = st.solve_reduced(B)
+    os.environ["MSFV_MF_FORCE_CHUNKED"] = "1"
+    try:
+        X1 = st.solve_reduced(B)
+    finally:
+        del os.environ["MSFV_MF_FORCE_CHUNKED"]
+    assert rel(X1, X0) <= 1e-11
