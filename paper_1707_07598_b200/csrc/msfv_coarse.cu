@@ -3206,7 +3206,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop2(MfSolveJob2 job) {
 // group lives in shared memory, L's tile column J streams through a buffer of
 // MF_LCH tiles (bulk copies), 2x2-blocked FMA products.
 constexpr int MF_CC = 8;
-constexpr int MF_LCH = 8;
+constexpr int MF_LCH = 4;
 __device__ __forceinline__ void mf_tma_tiles(double* dst, const double* src, int ntile, unsigned long long* bar) {
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -3220,22 +3220,26 @@ __device__ __forceinline__ void mf_tma_tiles(double* dst, const double* src, int
 __global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double* __restrict__ X,
                                                   double* __restrict__ Vg, int ld, int ntmax) {
   extern __shared__ __align__(16) double sh[];
-  __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bar[3];     // 0, 1: L chunk buffers, 2: Dinv
   const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
   const int c0 = blockIdx.y * MF_CC, nc = min(MF_CC, ld - c0);
   if (nc <= 0) return;
   const Band B = mf_band(d.base, F);
   const int rows = F.NT * TB;
   double* V = sh;                                   // rows x MF_CC
-  double* Ls = V + (size_t)ntmax * TB * MF_CC;      // MF_LCH tiles
-  double* Dj = Ls + (size_t)MF_LCH * TT;
+  double* Ls = V + (size_t)ntmax * TB * MF_CC;      // 2 x MF_LCH tiles
+  double* Dj = Ls + (size_t)2 * MF_LCH * TT;
   double* ys = Dj + TT;                             // TB x MF_CC
   const int* gid = d.gid + F.goff;
   const double* v0 = F.c[0] >= 0 ? Vg + (size_t)d.fr[F.c[0]].voff * ld : nullptr;
   const double* v1 = F.c[1] >= 0 ? Vg + (size_t)d.fr[F.c[1]].voff * ld : nullptr;
   const int* m0 = v0 ? d.maps + F.moff[0] : nullptr;
   const int* m1 = v1 ? d.maps + F.moff[1] : nullptr;
-  if (threadIdx.x == 0) mbar_init(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    mbar_init(&bar[2]);
+  }
 #pragma unroll 4
   for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
     const int r = t / MF_CC, s = t % MF_CC;
@@ -3248,13 +3252,21 @@ __global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double*
     V[t] = a;
   }
   __syncthreads();
-  unsigned ph = 0;
+  unsigned ph[3] = {0, 0, 0};
+  int buf = 0;
   const int cp = threadIdx.x % (MF_CC / 2), rp = threadIdx.x / (MF_CC / 2);   // 2 rows x 2 rhs per thread
   const int rstep = 2 * (blockDim.x / (MF_CC / 2));
+  // prologue: Dinv_0 and the first L chunk of column 0
+  mf_tma_tiles(Dj, B.Dinv, 1, &bar[2]);
+  if (F.NT > 1) mf_tma_tiles(Ls, btile(B.Lo, B, 0, 1), min(MF_LCH, F.NT - 1), &bar[0]);
+  bool first_issued = true;                         // the prologue issued column 0's first chunk (if any)
   for (int J = 0; J < F.NE; ++J) {
-    mf_tma_tiles(Dj, B.Dinv + (size_t)J * TT, 1, &bar);
-    mbar_wait(&bar, ph);
-    ph ^= 1;
+    const int nb = F.NT - 1 - J;
+    if (nb > 0 && !first_issued) mf_tma_tiles(Ls + (size_t)buf * MF_LCH * TT, btile(B.Lo, B, J, 1), min(MF_LCH, nb),
+                                              &bar[buf]);
+    first_issued = false;
+    mbar_wait(&bar[2], ph[2]);
+    ph[2] ^= 1;
     for (int r0 = 2 * rp; r0 < TB; r0 += rstep) {
       double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
       const double* vJ = V + (size_t)J * TB * MF_CC;
@@ -3270,21 +3282,31 @@ __global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double*
       *reinterpret_cast<double2*>(ys + r0 * MF_CC + 2 * cp) = make_double2(a00, a01);
       *reinterpret_cast<double2*>(ys + (r0 + 1) * MF_CC + 2 * cp) = make_double2(a10, a11);
     }
-    __syncthreads();
+    __syncthreads();                                  // ys complete, Dj consumed
+    if (J + 1 < F.NE) mf_tma_tiles(Dj, B.Dinv + (size_t)(J + 1) * TT, 1, &bar[2]);
     for (int t = threadIdx.x; t < TB * MF_CC; t += blockDim.x) V[(size_t)J * TB * MF_CC + t] = ys[t];
-    const int nb = F.NT - 1 - J;
     for (int tc = 0; tc < nb; tc += MF_LCH) {
       const int nt = min(MF_LCH, nb - tc);
-      __syncthreads();                                // previous chunk consumed
-      mf_tma_tiles(Ls, btile(B.Lo, B, J, 1 + tc), nt, &bar);
-      mbar_wait(&bar, ph);
-      ph ^= 1;
+      // prefetch the next chunk (this column's next, or the next column's first)
+      {
+        int nJ = J, ntc = tc + MF_LCH;
+        if (ntc >= nb) { nJ = J + 1; ntc = 0; }
+        const int nnb = F.NT - 1 - nJ;
+        if (nJ < F.NE && ntc < nnb) {
+          mf_tma_tiles(Ls + (size_t)(buf ^ 1) * MF_LCH * TT, btile(B.Lo, B, nJ, 1 + ntc), min(MF_LCH, nnb - ntc),
+                       &bar[buf ^ 1]);
+          if (nJ != J) first_issued = true;
+        }
+      }
+      mbar_wait(&bar[buf], ph[buf]);
+      ph[buf] ^= 1;
+      const double* Lc = Ls + (size_t)buf * MF_LCH * TT;
       double* vN = V + (size_t)(J + 1 + tc) * TB * MF_CC;
       for (int r0 = 2 * rp; r0 < nt * TB; r0 += rstep) {
         double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
 #pragma unroll 8
         for (int k = 0; k < TB; ++k) {
-          const double l0v = Ls[(size_t)r0 * TB + k], l1v = Ls[(size_t)(r0 + 1) * TB + k];
+          const double l0v = Lc[(size_t)r0 * TB + k], l1v = Lc[(size_t)(r0 + 1) * TB + k];
           const double2 y = *reinterpret_cast<const double2*>(ys + k * MF_CC + 2 * cp);
           a00 = fma(l0v, y.x, a00);
           a01 = fma(l0v, y.y, a01);
@@ -3297,8 +3319,9 @@ __global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double*
         *o0 = make_double2(p0.x - a00, p0.y - a01);
         *o1 = make_double2(p1.x - a10, p1.y - a11);
       }
+      __syncthreads();                                // chunk consumed before its buffer is refilled
+      buf ^= 1;
     }
-    __syncthreads();
   }
   double* v = Vg + (size_t)F.voff * ld;
   for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
@@ -3309,19 +3332,23 @@ __global__ void __launch_bounds__(256) k_mf_fwd_c(MfDev d, int l0, const double*
 __global__ void __launch_bounds__(256) k_mf_bwd_c(MfDev d, int l0, double* __restrict__ X,
                                                   const double* __restrict__ Vg, int ld, int ntmax) {
   extern __shared__ __align__(16) double sh[];
-  __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bar[3];
   const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
   const int c0 = blockIdx.y * MF_CC, nc = min(MF_CC, ld - c0);
   if (nc <= 0) return;
   const Band B = mf_band(d.base, F);
   const int rows = F.NT * TB;
   double* V = sh;
-  double* Ls = V + (size_t)ntmax * TB * MF_CC;
-  double* Dj = Ls + (size_t)MF_LCH * TT;
-  double* ys = Dj + TT;                             // TB x MF_CC (sums)
+  double* Ls = V + (size_t)ntmax * TB * MF_CC;      // 2 x MF_LCH tiles
+  double* Dj = Ls + (size_t)2 * MF_LCH * TT;
+  double* ys = Dj + TT;                             // TB x MF_CC
   const int* gid = d.gid + F.goff;
   const double* v = Vg + (size_t)F.voff * ld;
-  if (threadIdx.x == 0) mbar_init(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    mbar_init(&bar[2]);
+  }
 #pragma unroll 4
   for (int t = threadIdx.x; t < rows * MF_CC; t += blockDim.x) {
     const int r = t / MF_CC, s = t % MF_CC;
@@ -3333,31 +3360,49 @@ __global__ void __launch_bounds__(256) k_mf_bwd_c(MfDev d, int l0, double* __res
     V[t] = a;
   }
   __syncthreads();
-  unsigned ph = 0;
-  // thread (column j, rhs s): one output per thread (32 x 8 = 256)
-  const int j = threadIdx.x / MF_CC, s = threadIdx.x % MF_CC;
+  unsigned ph[3] = {0, 0, 0};
+  int buf = 0;
+  const int j = threadIdx.x / MF_CC, s = threadIdx.x % MF_CC;   // one output per thread (32 x 8)
+  {
+    const int J = F.NE - 1, nb = F.NT - 1 - J;
+    mf_tma_tiles(Dj, B.Dinv + (size_t)J * TT, 1, &bar[2]);
+    if (nb > 0) mf_tma_tiles(Ls, btile(B.Lo, B, J, 1), min(MF_LCH, nb), &bar[0]);
+  }
+  bool first_issued = true;                         // the prologue issued step NE-1's first chunk (if any)
   for (int J = F.NE - 1; J >= 0; --J) {
     const int nb = F.NT - 1 - J;
     double acc0 = 0.0, acc1 = 0.0;
+    if (nb > 0 && !first_issued) mf_tma_tiles(Ls + (size_t)buf * MF_LCH * TT, btile(B.Lo, B, J, 1), min(MF_LCH, nb),
+                                              &bar[buf]);
+    first_issued = false;
     for (int tc = 0; tc < nb; tc += MF_LCH) {
       const int nt = min(MF_LCH, nb - tc);
-      __syncthreads();
-      mf_tma_tiles(Ls, btile(B.Lo, B, J, 1 + tc), nt, &bar);
-      mbar_wait(&bar, ph);
-      ph ^= 1;
+      {
+        int nJ = J, ntc = tc + MF_LCH;
+        if (ntc >= nb) { nJ = J - 1; ntc = 0; }
+        const int nnb = F.NT - 1 - nJ;
+        if (nJ >= 0 && ntc < nnb) {
+          mf_tma_tiles(Ls + (size_t)(buf ^ 1) * MF_LCH * TT, btile(B.Lo, B, nJ, 1 + ntc), min(MF_LCH, nnb - ntc),
+                       &bar[buf ^ 1]);
+          if (nJ != J) first_issued = true;
+        }
+      }
+      mbar_wait(&bar[buf], ph[buf]);
+      ph[buf] ^= 1;
+      const double* Lc = Ls + (size_t)buf * MF_LCH * TT;
       if (j < TB) {
         const double* vb = V + (size_t)(J + 1 + tc) * TB * MF_CC + s;
         for (int rr = 0; rr < nt * TB; rr += 2) {
-          acc0 = fma(Ls[(size_t)rr * TB + j], vb[(size_t)rr * MF_CC], acc0);
-          acc1 = fma(Ls[(size_t)(rr + 1) * TB + j], vb[(size_t)(rr + 1) * MF_CC], acc1);
+          acc0 = fma(Lc[(size_t)rr * TB + j], vb[(size_t)rr * MF_CC], acc0);
+          acc1 = fma(Lc[(size_t)(rr + 1) * TB + j], vb[(size_t)(rr + 1) * MF_CC], acc1);
         }
       }
+      __syncthreads();
+      buf ^= 1;
     }
-    __syncthreads();
-    mf_tma_tiles(Dj, B.Dinv + (size_t)J * TT, 1, &bar);
     if (j < TB) ys[j * MF_CC + s] = V[(size_t)(J * TB + j) * MF_CC + s] - (acc0 + acc1);
-    mbar_wait(&bar, ph);
-    ph ^= 1;
+    mbar_wait(&bar[2], ph[2]);
+    ph[2] ^= 1;
     __syncthreads();
     if (j < TB) {
       double a = 0.0, b = 0.0;
@@ -3368,7 +3413,8 @@ __global__ void __launch_bounds__(256) k_mf_bwd_c(MfDev d, int l0, double* __res
       }
       V[(size_t)(J * TB + j) * MF_CC + s] = a + b;
     }
-    __syncthreads();
+    __syncthreads();                                  // Dj consumed, x_J in V
+    if (J >= 1) mf_tma_tiles(Dj, B.Dinv + (size_t)(J - 1) * TT, 1, &bar[2]);
   }
   for (int t = threadIdx.x; t < F.nE * MF_CC; t += blockDim.x) {
     const int r = t / MF_CC, s2 = t % MF_CC;
@@ -3508,7 +3554,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
            (size_t)3 * nt * TB * sizeof(int) + 16;
   };
   auto smem_c = [&](int nt) {
-    return ((size_t)nt * TB * MF_CC + (size_t)MF_LCH * TT + TT + (size_t)TB * MF_CC) * sizeof(double);
+    return ((size_t)nt * TB * MF_CC + (size_t)2 * MF_LCH * TT + TT + (size_t)TB * MF_CC) * sizeof(double);
   };
   static bool attr = false;
   if (!attr) {
