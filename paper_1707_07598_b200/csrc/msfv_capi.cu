@@ -128,8 +128,9 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   {
     // coarse nested dissection: on for k >= 1000 (MSFV_COARSE_ND=0/1 overrides)
     // coarse solver: one band below 1000 unknowns, multifrontal nested
-    // dissection where its fronts fit the kernels (config 4), z-plane nested
-    // dissection of the band otherwise (config 5); MSFV_COARSE_ND=0/1/2 overrides
+    // dissection above (z-plane nested dissection of the band if the tree has
+    // more fronts per level than the cooperative kernels take);
+    // MSFV_COARSE_ND=0/1/2 overrides
     const char* ev = getenv("MSFV_COARSE_ND");
     g.coarse_nd = ev ? std::min(2, std::max(0, atoi(ev))) : (g.kc >= 1000 ? 2 : 0);
     g.mf = nullptr;
