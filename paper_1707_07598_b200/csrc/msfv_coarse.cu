@@ -1996,7 +1996,7 @@ bool mf_attach(Geo& g) {
     ntmax = std::max(ntmax, F.NT);
   }
   const size_t inv_b = ((size_t)nemax * TT + 3 * TT) * sizeof(double);
-  const size_t sol_b = ((size_t)MF_GR * ntmax * TB + (size_t)ntmax * TB * 32 + (size_t)MF_GR * 32) * sizeof(double);
+  const size_t sol_b = ((size_t)MF_GR * ntmax * TB + (size_t)ntmax * TB * 32 + (size_t)MF_GR * 32) * sizeof(double) + 8192;
   const int nl = (int)P->lvl_off.size() - 1;
   int maxf = 0;
   for (int l = 0; l < nl; ++l) maxf = std::max(maxf, P->lvl_off[l + 1] - P->lvl_off[l]);
@@ -2846,10 +2846,12 @@ struct MfSolveJob {
   double* Vin;          // per-front gathered inputs, Σ rows x nrhs
   int nrhs;
 };
+constexpr int MF_FCACHE = 128;   // front descriptors cached per level in the coop solve
 __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ int pre[MF_MAXF + 1];
+  __shared__ MfFront fc[MF_FCACHE];
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
@@ -2861,9 +2863,12 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
     for (int li = 0; li < job.nl; ++li) {
       const int l = pass == 0 ? li : job.nl - 1 - li;
       const int l0 = job.lvl_off[l], nf = job.lvl_off[l + 1] - l0;
-      // ---- (A) gather: flat index over the level's fronts (rows x nrhs each)
+      // ---- (A) gather: flat index over the level's fronts (rows x nrhs
+      // each); the level's front descriptors are cached in shared memory and
+      // each thread keeps four elements' loads in flight
+      for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc[i] = d.fr[d.lvl[l0 + i]];
       for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const MfFront F = d.fr[d.lvl[l0 + i]];
+        const MfFront F = i < MF_FCACHE ? fc[i] : d.fr[d.lvl[l0 + i]];
         pre[i + 1] = F.NT * TB * nrhs;
       }
       __syncthreads();
@@ -2873,31 +2878,51 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       }
       __syncthreads();
       {
-        int fi = 0;
-        for (long long gi = gtid; gi < pre[nf]; gi += gstride) {
-          while (pre[fi + 1] <= gi) ++fi;
-          const MfFront F = d.fr[d.lvl[l0 + fi]];
-          const int e = (int)(gi - pre[fi]), r = e / nrhs, s = e % nrhs;
-          const int g = d.gid[F.goff + r];
-          double a;
-          if (pass == 0) {
-            a = (r < F.nE) ? __ldcg(job.X + (size_t)g * nrhs + s) : 0.0;
-            for (int c = 0; c < 2; ++c) {
-              if (F.c[c] < 0) continue;
-              const int q = d.maps[F.moff[c] + r];
-              if (q >= 0) a += __ldcg(job.Vout + ((size_t)d.fr[F.c[c]].voff + q) * nrhs + s);
-            }
-          } else {
-            a = r < F.NE * TB ? __ldcg(job.Vout + ((size_t)F.voff + r) * nrhs + s)
-                              : (g >= 0 ? __ldcg(job.X + (size_t)g * nrhs + s) : 0.0);
+        const long long total = pre[nf];
+        auto front_of = [&](long long gi) {
+          int lo = 0, hi = nf - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= gi) lo = mid; else hi = mid - 1;
           }
-          job.Vin[((size_t)F.voff + r) * nrhs + s] = a;
+          return lo;
+        };
+        for (long long base = gtid; base < total; base += 4 * gstride) {
+          double a[4];
+          long long dst[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const long long gi = base + u * gstride;
+            a[u] = 0.0;
+            dst[u] = -1;
+            if (gi >= total) continue;
+            const int fi = front_of(gi);
+            const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
+            const int e = (int)(gi - pre[fi]), r = e / nrhs, s2 = e % nrhs;
+            const int g = d.gid[F.goff + r];
+            if (pass == 0) {
+              double v = (r < F.nE) ? __ldcg(job.X + (size_t)g * nrhs + s2) : 0.0;
+              for (int c = 0; c < 2; ++c) {
+                if (F.c[c] < 0) continue;
+                const int q = d.maps[F.moff[c] + r];
+                if (q >= 0) v += __ldcg(job.Vout + ((size_t)d.fr[F.c[c]].voff + q) * nrhs + s2);
+              }
+              a[u] = v;
+            } else {
+              a[u] = r < F.NE * TB ? __ldcg(job.Vout + ((size_t)F.voff + r) * nrhs + s2)
+                                   : (g >= 0 ? __ldcg(job.X + (size_t)g * nrhs + s2) : 0.0);
+            }
+            dst[u] = ((long long)F.voff + r) * nrhs + s2;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (dst[u] >= 0) job.Vin[dst[u]] = a[u];
         }
       }
       grid.sync();
       // ---- (B) products
       for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const MfFront F = d.fr[d.lvl[l0 + i]];
+        const MfFront F = i < MF_FCACHE ? fc[i] : d.fr[d.lvl[l0 + i]];
         pre[i + 1] = pass == 0 ? (F.NT * TB + MF_GR - 1) / MF_GR : (F.nE + MF_GR - 1) / MF_GR;
       }
       __syncthreads();
@@ -2909,7 +2934,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       int fi = 0;
       for (int gi = blockIdx.x; gi < pre[nf]; gi += gridDim.x) {
         while (pre[fi + 1] <= gi) ++fi;
-        const MfFront F = d.fr[d.lvl[l0 + fi]];
+        const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
         const int rows = F.NT * TB, ncol = F.NE * TB;
         const double* vin = job.Vin + (size_t)F.voff * nrhs;
         if (pass == 0) {
@@ -3580,11 +3605,11 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 16384);
       if (e != cudaSuccess) return e;
       coop_grid = coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     }
-    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 8192 && !getenv("MSFV_MF_NOCOOP")) {
+    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 16384 && !getenv("MSFV_MF_NOCOOP")) {
       if (getenv("MSFV_MF_SCATTER") && smc2 <= (size_t)MF_SMEM_MAX - 8192) {   // scatter variant: fewer barriers, slower at config 4
         static bool a2 = false;
         if (!a2) {
