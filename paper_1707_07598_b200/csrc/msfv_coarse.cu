@@ -2047,6 +2047,33 @@ __device__ __forceinline__ double mf_u(const Band& C, int r, int c) {
 }
 // Front assembly of the fronts lvl[l0 .. l0 + gridDim.y): original entries with
 // a row or column in E, plus the children's update matrices (gathers).
+__device__ __forceinline__ void mf_assemble_elem(const Geo& g, const MfDev& d, const MfFront& F, long long t,
+                                                 const double* __restrict__ A27) {
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  const int lt = (int)(t / TT), e = (int)(t % TT);
+  int J = 0, rem = lt;
+  while (rem >= F.NT - J) {
+    rem -= F.NT - J;
+    ++J;
+  }
+  const int tt = rem;
+  const int r = (J + tt) * TB + e / TB, c = J * TB + e % TB;
+  const int gr = gid[r], gc = gid[c];
+  double v = 0.0;
+  if (gr < 0 || gc < 0) {
+    v = (r == c && r < F.NE * TB) ? 1.0 : 0.0;
+  } else {
+    if (r < F.nE || c < F.nE) v = mf_a(g, A27, gr, gc);
+    for (int k = 0; k < 2; ++k) {
+      if (F.c[k] < 0) continue;
+      const int* mk = d.maps + F.moff[k];
+      const int a = mk[r], b = mk[c];
+      if (a >= 0 && b >= 0) v += mf_u(mf_band(d.base, d.fr[F.c[k]]), a, b);
+    }
+  }
+  btile(B.A, B, J, tt)[e] = v;
+}
 __global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__ A27) {
   const MfFront F = d.fr[d.lvl[l0 + blockIdx.y]];
   const Band B = mf_band(d.base, F);
@@ -2096,6 +2123,8 @@ __global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__
 struct MfJob {
   MfDev d;
   int l0, nf, jmax;
+  Geo g;
+  const double* A27;    // non-null: assemble the level's fronts first (one grid barrier)
 };
 // Panel / update split for the fronts: per tile column, phase P stores the
 // panel tiles L_{J+t,J} = A_{J+t,J} Dinv_J^T once (Lo), grid barrier, phase U
@@ -2214,6 +2243,32 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
   const int nf = job.nf, G = (int)gridDim.x;
   const bool split = nf < G;
   auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
+  if (job.A27) {
+    // level assembly (A_k entries + the children's update matrices), all CTAs
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+      const MfFront F = front(i);
+      pre[i + 1] = F.NT * (F.NT + 1) / 2 * TT;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pre[0] = 0;
+      for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+    }
+    __syncthreads();
+    const long long total = pre[nf];
+    int fi = 0;
+    MfFront F = front(0);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)G * blockDim.x) {
+      bool moved = false;
+      while (pre[fi + 1] <= t) {
+        ++fi;
+        moved = true;
+      }
+      if (moved) F = front(fi);
+      mf_assemble_elem(job.g, job.d, F, t - pre[fi], job.A27);
+    }
+    grid.sync();
+  }
   for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
   grid.sync();
   const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
@@ -3507,10 +3562,15 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
       jmax = std::max(jmax, P->fr[P->lvl[l0 + i]].NE);
       ntmax = std::max(ntmax, P->fr[P->lvl[l0 + i]].NT);
     }
-    const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * (ntmax + 1) / 2 * TT + 255) / 256);
-    k_mf_assemble<<<dim3(gx, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
-    count_launches(1);
-    MfJob job{d, l0, nf, jmax};
+    // assembly inside the cooperative launch (one fewer launch per level) is
+    // slower at config 4/5 (fewer threads on the gathers): opt-in only
+    const bool fold = !mf_two_phase() && getenv("MSFV_MF_FOLD_ASSEMBLY");
+    if (!fold) {
+      const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * (ntmax + 1) / 2 * TT + 255) / 256);
+      k_mf_assemble<<<dim3(gx, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
+      count_launches(1);
+    }
+    MfJob job{d, l0, nf, jmax, g, fold ? Ak + P->a27 : nullptr};
     void* args[] = {(void*)&job, (void*)&flags};
     e = cudaLaunchCooperativeKernel(mf_two_phase() ? (void*)k_mf_factor2 : (void*)k_mf_factor, dim3(coop_grid),
                                     dim3(256), args, 0, st);
