@@ -2074,6 +2074,64 @@ __device__ __forceinline__ void mf_assemble_elem(const Geo& g, const MfDev& d, c
   }
   btile(B.A, B, J, tt)[e] = v;
 }
+// Tile-staged assembly: CTA (lower tile, front); the tile's 32 row and 32
+// column node ids, their coarse coordinates and child-map entries are staged
+// in shared memory once, each thread then assembles 4 elements.
+__global__ void __launch_bounds__(256) k_mf_assemble_t(Geo g, MfDev d, int l0, const double* __restrict__ A27) {
+  __shared__ int rid[2][TB], rco[2][TB], rm0[2][TB], rm1[2][TB];   // [0] rows, [1] columns
+  const MfFront F = d.fr[d.lvl[l0 + blockIdx.y]];
+  const int nlow = F.NT * (F.NT + 1) / 2;
+  if ((int)blockIdx.x >= nlow) return;
+  int J = 0, rem = blockIdx.x;
+  while (rem >= F.NT - J) {
+    rem -= F.NT - J;
+    ++J;
+  }
+  const int tt = rem;
+  const Band B = mf_band(d.base, F);
+  const int* gid = d.gid + F.goff;
+  const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
+  const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
+  const int kx = g.nb1 + 1, ky = g.nb2 + 1;
+  if (threadIdx.x < 2 * TB) {
+    const int w = threadIdx.x / TB, i = threadIdx.x % TB;
+    const int r = (w == 0 ? (J + tt) : J) * TB + i;
+    const int u = gid[r];
+    rid[w][i] = u;
+    rco[w][i] = u >= 0 ? (u % kx) | (((u / kx) % ky) << 10) | ((u / (kx * ky)) << 20) : 0;
+    rm0[w][i] = m0 ? m0[r] : -1;
+    rm1[w][i] = m1 ? m1[r] : -1;
+  }
+  Band C0{}, C1{};
+  if (F.c[0] >= 0) C0 = mf_band(d.base, d.fr[F.c[0]]);
+  if (F.c[1] >= 0) C1 = mf_band(d.base, d.fr[F.c[1]]);
+  __syncthreads();
+  double* T = btile(B.A, B, J, tt);
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int i = e / TB, j = e % TB;
+    const int r = (J + tt) * TB + i, c = J * TB + j;
+    const int gr = rid[0][i], gc = rid[1][j];
+    double v = 0.0;
+    if (gr < 0 || gc < 0) {
+      v = (r == c && r < F.NE * TB) ? 1.0 : 0.0;
+    } else {
+      if (r < F.nE || c < F.nE) {
+        // A_k(gr, gc) from the 14 lower stencil entries of max(gr, gc)
+        const bool sw = gr < gc;
+        const int hi = sw ? gc : gr, pc = sw ? rco[0][i] : rco[1][j], hc = sw ? rco[1][j] : rco[0][i];
+        const int dx = (pc & 1023) - (hc & 1023), dy = ((pc >> 10) & 1023) - ((hc >> 10) & 1023),
+                  dz = (pc >> 20) - (hc >> 20);
+        if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
+          const int o = dz == -1 ? (dy + 1) * 3 + (dx + 1) : (dy == -1 ? 9 + dx + 1 : 12 + dx + 1);
+          v = A27[(size_t)hi * 14 + o];
+        }
+      }
+      if (rm0[0][i] >= 0 && rm0[1][j] >= 0) v += mf_u(C0, rm0[0][i], rm0[1][j]);
+      if (rm1[0][i] >= 0 && rm1[1][j] >= 0) v += mf_u(C1, rm1[0][i], rm1[1][j]);
+    }
+    T[e] = v;
+  }
+}
 __global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__ A27) {
   const MfFront F = d.fr[d.lvl[l0 + blockIdx.y]];
   const Band B = mf_band(d.base, F);
@@ -3566,8 +3624,7 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     // slower at config 4/5 (fewer threads on the gathers): opt-in only
     const bool fold = !mf_two_phase() && getenv("MSFV_MF_FOLD_ASSEMBLY");
     if (!fold) {
-      const unsigned gx = (unsigned)std::min<long long>(4096, ((long long)ntmax * (ntmax + 1) / 2 * TT + 255) / 256);
-      k_mf_assemble<<<dim3(gx, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
+      k_mf_assemble_t<<<dim3(ntmax * (ntmax + 1) / 2, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
       count_launches(1);
     }
     MfJob job{d, l0, nf, jmax, g, fold ? Ak + P->a27 : nullptr};
