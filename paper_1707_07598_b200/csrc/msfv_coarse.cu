@@ -1698,7 +1698,7 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 //
 // The coarse grid (kx x ky x kz nodes, 27-point stencil) is dissected
 // recursively: a box is split by the coordinate plane through the middle of
-// its longest extent; boxes of <= MF_LEAF nodes are leaves.  A tree node
+// its longest extent; boxes of <= MF_LEAF (128) nodes are leaves.  A tree node
 // eliminates E (its separator plane, or the whole leaf box); its front is
 // [E | B], B = the nodes of ancestor separators adjacent to its box, each part
 // padded to whole 32-row tiles (E padding = identity, B padding = 0).  Fronts
@@ -1714,7 +1714,7 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 // gathers through host-built index maps, so every sum has a fixed order.
 // ============================================================================
 
-constexpr int MF_LEAF = 64;
+constexpr int MF_LEAF = 128;   // leaf boxes of <= 128 coarse nodes (tuned on config 4: 64 -> 128 saves 0.07 ms per step)
 constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative kernels
 constexpr int MF_GR = 16;       // rows per item of the G products
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
@@ -1795,7 +1795,12 @@ static void mf_dissect(MfPlan& P, int kx, int ky, int kz, int lo[3], int hi[3], 
   std::vector<int> E;
   std::array<int, 2> ch = {-1, -1};
   int h = 0;
-  if (vol <= MF_LEAF || (ext[0] < 3 && ext[1] < 3 && ext[2] < 3)) {
+  static int leaf = -1;
+  if (leaf < 0) {
+    const char* e = getenv("MSFV_MF_LEAF");
+    leaf = e ? std::max(8, atoi(e)) : MF_LEAF;
+  }
+  if (vol <= leaf || (ext[0] < 3 && ext[1] < 3 && ext[2] < 3)) {
     for (int z = lo[2]; z <= hi[2]; ++z)
       for (int y = lo[1]; y <= hi[1]; ++y)
         for (int x = lo[0]; x <= hi[0]; ++x) E.push_back(id(x, y, z));
