@@ -142,6 +142,7 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
   if (g.coarse_nd == 2 && !mf_attach(g)) g.coarse_nd = g.kc >= 1000 ? 1 : 0;
+  g.gtab8 = grad_template_init(g) ? 1 : 0;
   msfv_plan* pl = new msfv_plan;
   pl->g = g;
   *out = pl;

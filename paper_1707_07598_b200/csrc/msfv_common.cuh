@@ -52,6 +52,7 @@ struct Geo {
   const void* mf;          // host-side multifrontal plan (coarse_nd == 2), owned by the msfv_plan
   const SkelEdge* skel;    // device table of the skeleton-only owned edges (msfv_basis_build)
   int nskel;
+  int gtab8;               // 1: the 8^3 closure template (hats + edge table) is on the device (grad_template_init)
   // float reciprocals for division-free index decoding (see fdiv)
   float r_n1, r_n2, r_n1p, r_n2p, r_b1, r_b2, r_b3, r_ni1, r_ni2, r_nI, r_nb1, r_nb2;
 };

@@ -23,16 +23,25 @@ namespace msfv {
 // Basis values of block jb's 8 columns on its closure nodes (x fastest,
 // (b1+1)(b2+1)(b3+1) nodes x 8): interior from Sint, skeleton from the hats,
 // 0 at the pinned node.
+// BB > 0: cubic blocks of BB cells per axis known at compile time (every
+// index decode folds to multiply/shift); BB == 0: sizes from the Geo.
+template <int BB>
 __device__ __forceinline__ void stage_closure(const Geo& g, int jb, const double* __restrict__ Sint, double* Sn) {
-  const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
-  const double* Sb = Sint + (size_t)jb * 8 * g.nI;
+  const int b1 = BB ? BB : g.b1, b2 = BB ? BB : g.b2, b3 = BB ? BB : g.b3;
+  const int B1 = b1 + 1, B2 = b2 + 1, B3 = b3 + 1, NN = B1 * B2 * B3;
+  const int ni1 = b1 - 1, ni2 = b2 - 1, nI = ni1 * ni2 * (b3 - 1);
+  const double* Sb = Sint + (size_t)jb * 8 * nI;
   // interior: one coordinate decode per node, the 8 corner loads in flight together
-  for (int a = threadIdx.x; a < g.nI; a += blockDim.x) {
+  for (int a = threadIdx.x; a < nI; a += blockDim.x) {
     double v[8];
 #pragma unroll
-    for (int cc = 0; cc < 8; ++cc) v[cc] = __ldg(Sb + (size_t)cc * g.nI + a);
+    for (int cc = 0; cc < 8; ++cc) v[cc] = __ldg(Sb + (size_t)cc * nI + a);
     int x, y, z;
-    decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+    if (BB) {
+      x = a % ni1; const int r = a / ni1; y = r % ni2; z = r / ni2;
+    } else {
+      decode3f(a, g.ni1, g.r_ni1, g.ni2, g.r_ni2, x, y, z);
+    }
     double* d = Sn + ((x + 1) + B1 * ((y + 1) + B2 * (z + 1))) * 8;
 #pragma unroll
     for (int cc = 0; cc < 8; cc += 2) *reinterpret_cast<double2*>(d + cc) = make_double2(v[cc], v[cc + 1]);
@@ -40,33 +49,134 @@ __device__ __forceinline__ void stage_closure(const Geo& g, int jb, const double
   // skeleton: separable hats (6 one-dimensional values per node)
   for (int n = threadIdx.x; n < NN; n += blockDim.x) {
     const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
-    if (x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3) continue;
+    if (x > 0 && x < b1 && y > 0 && y < b2 && z > 0 && z < b3) continue;
     const bool node0 = jb == 0 && n == 0;     // pinned node: no row of S
-    const double hx[2] = {hatf1(x, g.ib1), hatf1(x - g.b1, g.ib1)};
-    const double hy[2] = {hatf1(y, g.ib2), hatf1(y - g.b2, g.ib2)};
-    const double hz[2] = {hatf1(z, g.ib3), hatf1(z - g.b3, g.ib3)};
+    const double hx[2] = {hatf1(x, g.ib1), hatf1(x - b1, g.ib1)};
+    const double hy[2] = {hatf1(y, g.ib2), hatf1(y - b2, g.ib2)};
+    const double hz[2] = {hatf1(z, g.ib3), hatf1(z - b3, g.ib3)};
+    double h[8];
 #pragma unroll
-    for (int cc = 0; cc < 8; ++cc)
-      Sn[n * 8 + cc] = node0 ? 0.0 : (hx[cc & 1] * hy[(cc >> 1) & 1]) * hz[cc >> 2];
+    for (int cc = 0; cc < 8; ++cc) h[cc] = node0 ? 0.0 : (hx[cc & 1] * hy[(cc >> 1) & 1]) * hz[cc >> 2];
+#pragma unroll
+    for (int cc = 0; cc < 8; cc += 2) *reinterpret_cast<double2*>(Sn + n * 8 + cc) = make_double2(h[cc], h[cc + 1]);
   }
+}
+
+// 8^3 blocks: the skeleton part of the closure (hats, identical for every
+// block but the pinned node of block 0) and the closure edge table are one
+// device-resident template; each CTA bulk-copies it into shared memory (TMA,
+// L2-resident after the first CTAs) while its threads fetch the interior
+// values, instead of recomputing 386 hat products and 1944 edge decodes.
+constexpr int TPL_NN = 9 * 9 * 9, TPL_NE = 3 * 8 * 9 * 9, TPL_NEP = 2048;   // edge table padded to 16 warps x 16 steps x 8
+__device__ __align__(16) double g_tpl8_sn[TPL_NN * 8];
+__device__ __align__(16) int g_tpl8_et[TPL_NEP];
+
+bool grad_template_init(const Geo& g) {
+  if (!(g.b1 == 8 && g.b2 == 8 && g.b3 == 8)) return false;
+  static double sn[TPL_NN * 8];
+  static int et[TPL_NEP];   // padding entries: node 0, x axis (results discarded)
+  const double ib = 1.0 / 8;
+  auto hat = [&](int d) { const double v = 1.0 - fabs((double)d) * ib; return v > 0.0 ? v : 0.0; };
+  for (int n = 0; n < TPL_NN; ++n) {
+    const int x = n % 9, y = (n / 9) % 9, z = n / 81;
+    const bool inner = x > 0 && x < 8 && y > 0 && y < 8 && z > 0 && z < 8;
+    const double hx[2] = {hat(x), hat(x - 8)}, hy[2] = {hat(y), hat(y - 8)}, hz[2] = {hat(z), hat(z - 8)};
+    for (int cc = 0; cc < 8; ++cc) sn[n * 8 + cc] = inner ? 0.0 : (hx[cc & 1] * hy[(cc >> 1) & 1]) * hz[cc >> 2];
+  }
+  const int NEx = 8 * 81, NEy = 8 * 81;
+  for (int e = 0; e < TPL_NE; ++e) {
+    int x, y, z, ax;
+    if (e < NEx) { x = e % 8; y = (e / 8) % 9; z = e / 72; ax = 0; }
+    else if (e < NEx + NEy) { const int f = e - NEx; x = f % 9; y = (f / 9) % 8; z = f / 72; ax = 1; }
+    else { const int f = e - NEx - NEy; x = f % 9; y = (f / 9) % 9; z = f / 81; ax = 2; }
+    et[e] = (x + 9 * (y + 9 * z)) | (ax << 24);
+  }
+  return cudaMemcpyToSymbol(g_tpl8_sn, sn, sizeof(sn)) == cudaSuccess &&
+         cudaMemcpyToSymbol(g_tpl8_et, et, sizeof(et)) == cudaSuccess;
+}
+
+namespace {
+__device__ __forceinline__ unsigned g_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+}
+
+// Closure staging from the template: thread 0 bulk-copies the hats (into Sn)
+// and, when Et != nullptr, the edge table; every thread loads its interior
+// values into registers meanwhile, waits on the copy, then overwrites the
+// interior nodes.  Requires blockDim.x * 2 >= 343.
+__device__ __forceinline__ void stage_closure_tpl8(int jb, const double* __restrict__ Sint, double* Sn, int* Et,
+                                                   unsigned long long* bar) {
+  constexpr int nI = 343;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g_smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned bsn = TPL_NN * 8 * sizeof(double), bet = Et ? TPL_NEP * sizeof(int) : 0;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(g_smem_u32(bar)), "r"(bsn + bet)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     g_smem_u32(Sn)), "l"(g_tpl8_sn), "r"(bsn), "r"(g_smem_u32(bar))
+                 : "memory");
+    if (Et)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       g_smem_u32(Et)), "l"(g_tpl8_et), "r"(bet), "r"(g_smem_u32(bar))
+                   : "memory");
+  }
+  const double* Sb = Sint + (size_t)jb * 8 * nI;
+  double v[2][8];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int a = tid + it * blockDim.x;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) v[it][cc] = a < nI ? __ldg(Sb + (size_t)cc * nI + a) : 0.0;
+  }
+  {
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(g_smem_u32(bar)), "r"(0u)
+          : "memory");
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int a = tid + it * blockDim.x;
+    if (a < nI) {
+      const int x = a % 7, r = a / 7, y = r % 7, z = r / 7;
+      double* d = Sn + ((x + 1) + 9 * ((y + 1) + 9 * (z + 1))) * 8;
+#pragma unroll
+      for (int cc = 0; cc < 8; cc += 2) *reinterpret_cast<double2*>(d + cc) = make_double2(v[it][cc], v[it][cc + 1]);
+    }
+  }
+  if (jb == 0 && tid < 8) Sn[tid] = 0.0;     // pinned node: no row of S
 }
 
 size_t grad_smem_doubles(const Geo& g, int nrhs) {
   const size_t B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1;
   const size_t ne = (size_t)g.b1 * B2 * B3 + B1 * g.b2 * B3 + B1 * B2 * g.b3;
-  return B1 * B2 * B3 * 8 + ne + 16 * (size_t)nrhs + 64 + (ne + 1) / 2;   // + packed edge table (ints)
+  return B1 * B2 * B3 * 8 + ne + 16 * (size_t)nrhs + 64 + (ne + 1) / 2 + 64;   // + packed edge table (ints, padded)
 }
 
-__global__ void __launch_bounds__(GRAD_THREADS)
+// 8^3 blocks run 16 warps per CTA (two CTAs per SM, 64 registers): twice the
+// warps of the 256-thread form at the same shared-memory occupancy.
+constexpr int GRAD_T8 = 512;
+
+template <int BB>
+__global__ void __launch_bounds__(BB == 8 ? GRAD_T8 : GRAD_THREADS, BB == 8 ? 2 : 3)
 k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ T, const double* __restrict__ Y,
              int nrhs, const double* __restrict__ sigma, const int* __restrict__ zslot, const double* __restrict__ Zc,
              const int* __restrict__ rslot, const double* __restrict__ Rc, double* __restrict__ gout, int jb0) {
   extern __shared__ __align__(16) double gsm[];
+  const int b1 = BB ? BB : g.b1, b2 = BB ? BB : g.b2, b3 = BB ? BB : g.b3;
   const int jb = jb0 + blockIdx.x, tid = threadIdx.x;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
-  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
-  const int NEx = g.b1 * B2 * B3, NEy = B1 * g.b2 * B3, NEz = B1 * B2 * g.b3;
+  const int X0 = bi * b1, Y0 = bj * b2, Z0 = bk * b3;
+  const int B1 = b1 + 1, B2 = b2 + 1, B3 = b3 + 1, NN = B1 * B2 * B3;
+  const int NEx = b1 * B2 * B3, NEy = B1 * b2 * B3, NEz = B1 * B2 * b3;
   double* Sn = gsm;                       // [NN][8] basis values on the block closure
   double* xi = Sn + (size_t)NN * 8;       // [NEx | NEy | NEz]
   double* Tj = xi + NEx + NEy + NEz;      // [8][nrhs]
@@ -75,18 +185,29 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   int* Et = reinterpret_cast<int*>(M + 64);  // [NE] lower closure node | axis << 24
 
   for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
-    const int cc = i / nrhs, s = i - cc * nrhs;
+    const int cc = i & 7, s = i >> 3;
     const size_t col = (size_t)corner_col(g, bi, bj, bk, cc);
-    Tj[i] = T[col * nrhs + s];
-    Yj[i] = Y[col * nrhs + s];
+    Tj[cc * nrhs + s] = T[col * nrhs + s];
+    Yj[cc * nrhs + s] = Y[col * nrhs + s];
   }
-  stage_closure(g, jb, Sint, Sn);
+  if (BB == 8) {
+    __shared__ unsigned long long tbar;
+    stage_closure_tpl8(jb, Sint, Sn, Et, &tbar);
+  } else {
+    stage_closure<BB>(g, jb, Sint, Sn);
+  }
   __syncthreads();
-  if (tid < 64) {
-    const int c = tid >> 3, c2 = tid & 7;
-    double v = 0.0;
-    for (int s = 0; s < nrhs; ++s) v += Tj[c * nrhs + s] * Yj[c2 * nrhs + s];
-    M[tid] = v;
+  if (tid < 32) {   // M = Tj Yj^T on the DMMA, 4 sources per step (one warp)
+    const int m = tid >> 2, k = tid & 3;
+    double c0 = 0.0, c1 = 0.0;
+    for (int s0 = 0; s0 < nrhs; s0 += 4) {
+      const bool ok = s0 + k < nrhs;
+      const double a = ok ? Tj[m * nrhs + s0 + k] : 0.0, b = ok ? Yj[m * nrhs + s0 + k] : 0.0;
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+    }
+    M[m * 8 + 2 * k] = c0;
+    M[m * 8 + 2 * k + 1] = c1;
   }
   __syncthreads();
   const int zs = zslot ? zslot[jb] : -1, rs = rslot ? rslot[jb] : -1;
@@ -95,10 +216,10 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   auto edge = [&](int e, int& na, int& step, double& ihs) {
     int x, y, z;
     if (e < NEx) {
-      x = e % g.b1; const int r = e / g.b1; y = r % B2; z = r / B2; step = 1; ihs = g.ih1 * g.ih1;
+      x = e % b1; const int r = e / b1; y = r % B2; z = r / B2; step = 1; ihs = g.ih1 * g.ih1;
     } else if (e < NEx + NEy) {
       const int f = e - NEx;
-      x = f % B1; const int r = f / B1; y = r % g.b2; z = r / g.b2; step = B1; ihs = g.ih2 * g.ih2;
+      x = f % B1; const int r = f / B1; y = r % b2; z = r / b2; step = B1; ihs = g.ih2 * g.ih2;
     } else {
       const int f = e - NEx - NEy;
       x = f % B1; const int r = f / B1; y = r % B2; z = r / B2; step = B1 * B2; ihs = g.ih3 * g.ih3;
@@ -106,19 +227,44 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
     na = x + B1 * (y + B2 * z);
   };
   if (zs < 0 && rs < 0) {
-    for (int e = tid; e < NE; e += blockDim.x) {
-      int na, step;
-      double ihs;
-      edge(e, na, step, ihs);
-      Et[e] = na | ((e < NEx ? 0 : (e < NEx + NEy ? 1 : 2)) << 24);
+    if (BB != 8) {   // no template: decode each edge once into a table
+      for (int e = tid; e < NE; e += blockDim.x) {
+        int na, step;
+        double ihs;
+        edge(e, na, step, ihs);
+        Et[e] = na | ((e < NEx ? 0 : (e < NEx + NEy ? 1 : 2)) << 24);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     const double ihx[3] = {g.ih1 * g.ih1, g.ih2 * g.ih2, g.ih3 * g.ih3};
     // xi_e = dS_e^T M dS_e for 8 edges per warp step: D (8 edges x 8 corners,
     // accumulator layout) times M on the DMMA (D += X Y^T with Y = M^T), then
     // the row-wise product with D and a 4-lane reduction.
     const int lane = tid & 31, wv = tid >> 5, m = lane >> 2, q = lane & 3;
     const double mt0 = M[(2 * q) * 8 + m], mt1 = M[(2 * q + 1) * 8 + m];   // C layout of M^T
+    if (BB == 8) {
+      // padded template table: fixed trip count, no bounds test but on the store
+#pragma unroll 4
+      for (int it = 0; it < TPL_NEP / (8 * (GRAD_T8 / 32)); ++it) {
+        const int e = (it * (GRAD_T8 / 32) + wv) * 8 + m;
+        const int pk = Et[e], ax = pk >> 24, na = pk & 0xFFFFFF;
+        const int nb = na + (ax == 0 ? 1 : (ax == 1 ? 9 : 81));
+        const double ihs = ax == 0 ? ihx[0] : (ax == 1 ? ihx[1] : ihx[2]);
+        const double2 sb = *reinterpret_cast<const double2*>(Sn + nb * 8 + 2 * q);
+        const double2 sa = *reinterpret_cast<const double2*>(Sn + na * 8 + 2 * q);
+        const double d0 = sb.x - sa.x, d1 = sb.y - sa.y;
+        double c0 = 0.0, c1 = 0.0;
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c0), "+d"(c1) : "d"(d0), "d"(mt0));
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c0), "+d"(c1) : "d"(d1), "d"(mt1));
+        double v = c0 * d0 + c1 * d1;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (q == 0 && e < NE) xi[e] = v * ihs;
+      }
+    } else
+#pragma unroll 2
     for (int e0 = 8 * wv; e0 < NE; e0 += 8 * (blockDim.x >> 5)) {
       const int e = e0 + m;
       double d0 = 0.0, d1 = 0.0, ihs = 0.0;
@@ -187,16 +333,16 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   const double* xx = xi;
   const double* xy = xi + NEx;
   const double* xz = xi + NEx + NEy;
-  const int ncell = g.b1 * g.b2 * g.b3;
+  const int ncell = b1 * b2 * b3;
   for (int c = tid; c < ncell; c += blockDim.x) {
-    const int x = c % g.b1, r = c / g.b1, y = r % g.b2, z = r / g.b2;
-    auto ex = [&](int i, int j, int k) { return xx[i + g.b1 * (j + B2 * k)]; };
-    auto ey = [&](int i, int j, int k) { return xy[i + B1 * (j + g.b2 * k)]; };
+    const int x = c % b1, r = c / b1, y = r % b2, z = r / b2;
+    auto ex = [&](int i, int j, int k) { return xx[i + b1 * (j + B2 * k)]; };
+    auto ey = [&](int i, int j, int k) { return xy[i + B1 * (j + b2 * k)]; };
     auto ez = [&](int i, int j, int k) { return xz[i + B1 * (j + B2 * k)]; };
-    double tot = 0.0;
-    tot += ex(x, y, z) + ex(x, y + 1, z) + ex(x, y, z + 1) + ex(x, y + 1, z + 1);
-    tot += ey(x, y, z) + ey(x + 1, y, z) + ey(x, y, z + 1) + ey(x + 1, y, z + 1);
-    tot += ez(x, y, z) + ez(x + 1, y, z) + ez(x, y + 1, z) + ez(x + 1, y + 1, z);
+    const double tx = (ex(x, y, z) + ex(x, y + 1, z)) + (ex(x, y, z + 1) + ex(x, y + 1, z + 1));
+    const double ty = (ey(x, y, z) + ey(x + 1, y, z)) + (ey(x, y, z + 1) + ey(x + 1, y, z + 1));
+    const double tz = (ez(x, y, z) + ez(x + 1, y, z)) + (ez(x, y + 1, z) + ez(x + 1, y + 1, z));
+    const double tot = (tx + ty) + tz;
     const long long cid = cell_id(g, X0 + x, Y0 + y, Z0 + z);
     gout[cid] = -sigma[cid] * (g.qv * tot);
   }
@@ -210,34 +356,41 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
 // j's share (gathered to coarse nodes by k_gather_corners with scale -1).
 // Edge ownership: the edge's lower node is owned by j (node ownership of
 // k_restrict_op).  K_c is a DMMA reduction (lane = corner cc, edge slot).
+template <int BB>
 __global__ void __launch_bounds__(GRAD_THREADS)
 k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cvec, const double* __restrict__ T,
            int nrhs, const int* __restrict__ rslot, const double* __restrict__ Rc, double* __restrict__ part) {
   extern __shared__ __align__(16) double gsm[];
+  const int b1 = BB ? BB : g.b1, b2 = BB ? BB : g.b2, b3 = BB ? BB : g.b3;
   const int jb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
-  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int B1 = g.b1 + 1, B2 = g.b2 + 1, B3 = g.b3 + 1, NN = B1 * B2 * B3;
-  const int ox = g.b1 + (bi == g.nb1 - 1), oy = g.b2 + (bj == g.nb2 - 1), oz = g.b3 + (bk == g.nb3 - 1);
-  const int NOx = g.b1 * oy * oz, NOy = ox * g.b2 * oz, NOz = ox * oy * g.b3, NO = NOx + NOy + NOz;
+  const int X0 = bi * b1, Y0 = bj * b2, Z0 = bk * b3;
+  const int B1 = b1 + 1, B2 = b2 + 1, B3 = b3 + 1, NN = B1 * B2 * B3;
+  const int ox = b1 + (bi == g.nb1 - 1), oy = b2 + (bj == g.nb2 - 1), oz = b3 + (bk == g.nb3 - 1);
+  const int NOx = b1 * oy * oz, NOy = ox * b2 * oz, NOz = ox * oy * b3, NO = NOx + NOy + NOz;
   double* Sn = gsm;                       // [NN][8]
   double* Kw = Sn + (size_t)NN * 8;       // [8 warps][64]
   double* Tj = Kw + 8 * 64;               // [8][nrhs]
-  stage_closure(g, jb, Sint, Sn);
+  if (BB == 8) {
+    __shared__ unsigned long long tbar;
+    stage_closure_tpl8(jb, Sint, Sn, nullptr, &tbar);
+  } else {
+    stage_closure<BB>(g, jb, Sint, Sn);
+  }
   for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
-    const int cc = i / nrhs, s = i - cc * nrhs;
-    Tj[i] = T[(size_t)corner_col(g, bi, bj, bk, cc) * nrhs + s];
+    const int cc = i & 7, s = i >> 3;
+    Tj[cc * nrhs + s] = T[(size_t)corner_col(g, bi, bj, bk, cc) * nrhs + s];
   }
   __syncthreads();
   // owned edge f -> (local lower node, step, global edge id, 1/h^2)
   auto edge = [&](int f, int& na, int& step, long long& eid, double& ihs) {
     int x, y, z;
     if (f < NOx) {
-      x = f % g.b1; const int r = f / g.b1; y = r % oy; z = r / oy;
+      x = f % b1; const int r = f / b1; y = r % oy; z = r / oy;
       step = 1; ihs = g.ih1 * g.ih1; eid = ex_id(g, X0 + x, Y0 + y, Z0 + z);
     } else if (f < NOx + NOy) {
       const int h = f - NOx;
-      x = h % ox; const int r = h / ox; y = r % g.b2; z = r / g.b2;
+      x = h % ox; const int r = h / ox; y = r % b2; z = r / b2;
       step = B1; ihs = g.ih2 * g.ih2; eid = ey_id(g, X0 + x, Y0 + y, Z0 + z);
     } else {
       const int h = f - NOx - NOy;
@@ -319,9 +472,10 @@ size_t jv_smem_doubles(const Geo& g, int nrhs) {
 cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec, const double* T, int nrhs,
                             const int* rslot, const double* Rc, double* part, cudaStream_t st) {
   const size_t smem = jv_smem_doubles(g, nrhs) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_jv_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = g.gtab8 ? k_jv_block<8> : k_jv_block<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_jv_block<<<g.nbl, GRAD_THREADS, smem, st>>>(g, Sint, cvec, T, nrhs, rslot, Rc, part);
+  kern<<<g.nbl, GRAD_THREADS, smem, st>>>(g, Sint, cvec, T, nrhs, rslot, Rc, part);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -332,11 +486,12 @@ cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T,
                               const double* sigma, const int* zslot, const double* Zc, const int* rslot,
                               const double* Rc, double* gout, cudaStream_t st, int jb0, int nb) {
   const size_t smem = grad_smem_doubles(g, nrhs) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_grad_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = g.gtab8 ? k_grad_block<8> : k_grad_block<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (nb < 0) nb = g.nbl - jb0;
   if (nb <= 0) return cudaSuccess;
-  k_grad_block<<<nb, GRAD_THREADS, smem, st>>>(g, Sint, T, Y, nrhs, sigma, zslot, Zc, rslot, Rc, gout, jb0);
+  kern<<<nb, g.gtab8 ? GRAD_T8 : GRAD_THREADS, smem, st>>>(g, Sint, T, Y, nrhs, sigma, zslot, Zc, rslot, Rc, gout, jb0);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -108,6 +108,7 @@ cudaError_t launch_points_scatter_interior(const Geo& g, const PointsDev& P, con
 constexpr int GRAD_THREADS = 256;
 size_t grad_smem_doubles(const Geo& g, int nrhs);
 bool grad_supported(const Geo& g, int nrhs);
+bool grad_template_init(const Geo& g);   // 8^3 blocks: upload the closure template to the current device
 cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T, const double* Y, int nrhs,
                               const double* sigma, const int* zslot, const double* Zc, const int* rslot,
                               const double* Rc, double* gout, cudaStream_t st, int jb0 = 0, int nb = -1);
