@@ -102,7 +102,8 @@ __device__ __forceinline__ unsigned g_smem_u32(const void* p) { return (unsigned
 // Closure staging from the template: thread 0 bulk-copies the hats (into Sn)
 // and, when Et != nullptr, the edge table; every thread loads its interior
 // values into registers meanwhile, waits on the copy, then overwrites the
-// interior nodes.  Requires blockDim.x * 2 >= 343.
+// interior nodes.  NT = blockDim.x.
+template <int NT>
 __device__ __forceinline__ void stage_closure_tpl8(int jb, const double* __restrict__ Sint, double* Sn, int* Et,
                                                    unsigned long long* bar) {
   constexpr int nI = 343;
@@ -125,10 +126,11 @@ __device__ __forceinline__ void stage_closure_tpl8(int jb, const double* __restr
                    : "memory");
   }
   const double* Sb = Sint + (size_t)jb * 8 * nI;
-  double v[2][8];
+  constexpr int NIT = (nI + NT - 1) / NT;
+  double v[NIT][8];
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int a = tid + it * blockDim.x;
+  for (int it = 0; it < NIT; ++it) {
+    const int a = tid + it * NT;
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) v[it][cc] = a < nI ? __ldg(Sb + (size_t)cc * nI + a) : 0.0;
   }
@@ -143,8 +145,8 @@ __device__ __forceinline__ void stage_closure_tpl8(int jb, const double* __restr
     }
   }
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int a = tid + it * blockDim.x;
+  for (int it = 0; it < NIT; ++it) {
+    const int a = tid + it * NT;
     if (a < nI) {
       const int x = a % 7, r = a / 7, y = r % 7, z = r / 7;
       double* d = Sn + ((x + 1) + 9 * ((y + 1) + 9 * (z + 1))) * 8;
@@ -173,7 +175,8 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   extern __shared__ __align__(16) double gsm[];
   const int b1 = BB ? BB : g.b1, b2 = BB ? BB : g.b2, b3 = BB ? BB : g.b3;
   const int jb = jb0 + blockIdx.x, tid = threadIdx.x;
-  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  int bi, bj, bk;
+  decode3f(jb, g.nb1, g.r_nb1, g.nb2, g.r_nb2, bi, bj, bk);
   const int X0 = bi * b1, Y0 = bj * b2, Z0 = bk * b3;
   const int B1 = b1 + 1, B2 = b2 + 1, B3 = b3 + 1, NN = B1 * B2 * B3;
   const int NEx = b1 * B2 * B3, NEy = B1 * b2 * B3, NEz = B1 * B2 * b3;
@@ -192,7 +195,7 @@ k_grad_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ 
   }
   if (BB == 8) {
     __shared__ unsigned long long tbar;
-    stage_closure_tpl8(jb, Sint, Sn, Et, &tbar);
+    stage_closure_tpl8<GRAD_T8>(jb, Sint, Sn, Et, &tbar);
   } else {
     stage_closure<BB>(g, jb, Sint, Sn);
   }
@@ -363,7 +366,8 @@ k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cv
   extern __shared__ __align__(16) double gsm[];
   const int b1 = BB ? BB : g.b1, b2 = BB ? BB : g.b2, b3 = BB ? BB : g.b3;
   const int jb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  int bi, bj, bk;
+  decode3f(jb, g.nb1, g.r_nb1, g.nb2, g.r_nb2, bi, bj, bk);
   const int X0 = bi * b1, Y0 = bj * b2, Z0 = bk * b3;
   const int B1 = b1 + 1, B2 = b2 + 1, B3 = b3 + 1, NN = B1 * B2 * B3;
   const int ox = b1 + (bi == g.nb1 - 1), oy = b2 + (bj == g.nb2 - 1), oz = b3 + (bk == g.nb3 - 1);
@@ -373,7 +377,7 @@ k_jv_block(Geo g, const double* __restrict__ Sint, const double* __restrict__ cv
   double* Tj = Kw + 8 * 64;               // [8][nrhs]
   if (BB == 8) {
     __shared__ unsigned long long tbar;
-    stage_closure_tpl8(jb, Sint, Sn, nullptr, &tbar);
+    stage_closure_tpl8<GRAD_THREADS>(jb, Sint, Sn, nullptr, &tbar);
   } else {
     stage_closure<BB>(g, jb, Sint, Sn);
   }
