@@ -11,7 +11,7 @@ from .errors import (FactorizationError, InvalidModelError, ReducedSingularError
                      StaleBasisError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmsfv.so")
+LIB_PATH = os.environ.get("MSFV_LIB_PATH") or os.path.join(HERE, "libmsfv.so")   # override: A/B runs only
 
 MSFV_OK = 0
 MSFV_INVALID_MODEL = 1
