@@ -1770,6 +1770,8 @@ struct MfPlan {
   int* d_gid = nullptr;
   int* d_maps = nullptr;
   int* d_lvloff = nullptr;
+  int* d_pre = nullptr;   // per-level prefix sums (solve): rows | forward items | backward items, npre each
+  int npre = 0;
   bool use_g = true;      // explicit inverse blocks fit the kernels' shared memory (else staged sweeps)
 };
 
@@ -1976,6 +1978,23 @@ static cudaError_t mf_upload(const Geo& g) {
   if (e == cudaSuccess) e = cudaMalloc(&P->d_lvloff, P->lvl_off.size() * sizeof(int));
   if (e == cudaSuccess)
     e = cudaMemcpy(P->d_lvloff, P->lvl_off.data(), P->lvl_off.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    // level l's prefixes start at lvl_off[l] + l (nf + 1 entries each)
+    const int nl = (int)P->lvl_off.size() - 1;
+    P->npre = P->lvl_off[nl] + nl;
+    std::vector<int> pre(3 * (size_t)P->npre, 0);
+    for (int l = 0; l < nl; ++l) {
+      const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, pb = l0 + l;
+      for (int i = 0; i < nf; ++i) {
+        const MfFront& F = P->fr[P->lvl[l0 + i]];
+        pre[pb + i + 1] = pre[pb + i] + F.NT * TB;
+        pre[P->npre + pb + i + 1] = pre[P->npre + pb + i] + (F.NT * TB + MF_GR - 1) / MF_GR;
+        pre[2 * P->npre + pb + i + 1] = pre[2 * P->npre + pb + i] + (F.nE + MF_GR - 1) / MF_GR;
+      }
+    }
+    e = cudaMalloc(&P->d_pre, pre.size() * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
   return e;
 }
 
@@ -1987,6 +2006,7 @@ void mf_release(Geo& g) {
   if (P->d_gid) cudaFree(P->d_gid);
   if (P->d_maps) cudaFree(P->d_maps);
   if (P->d_lvloff) cudaFree(P->d_lvloff);
+  if (P->d_pre) cudaFree(P->d_pre);
   delete P;
   g.mf = nullptr;
 }
@@ -2963,17 +2983,29 @@ struct MfSolveJob {
   double* Vout;         // per-front outputs (y_E | c_B), Σ rows x nrhs
   double* Vin;          // per-front gathered inputs, Σ rows x nrhs
   int nrhs;
+  unsigned long long* tstamp;   // debug (MSFV_MF_TIMING): globaltimer after every grid barrier
+  const int* pre;       // MfPlan::d_pre
+  int npre;
 };
+__device__ __forceinline__ void mf_stamp(unsigned long long* ts, int i) {
+  if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ts[i] = t;
+  }
+}
 constexpr int MF_FCACHE = 128;   // front descriptors cached per level in the coop solve
 __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) unsigned long long bar;
-  __shared__ int pre[MF_MAXF + 1];
+  __shared__ int pre[MF_MAXF + 1], preB[MF_MAXF + 1];
   __shared__ MfFront fc[MF_FCACHE];
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
   unsigned ph = 0;
+  int nst = 0;
+  mf_stamp(job.tstamp, nst++);
   const MfDev& d = job.d;
   const int nrhs = job.nrhs;
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
@@ -2984,15 +3016,11 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       // ---- (A) gather: flat index over the level's fronts (rows x nrhs
       // each); the level's front descriptors are cached in shared memory and
       // each thread keeps four elements' loads in flight
+      // (descriptors and both phases' prefix sums in one round of loads)
       for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc[i] = d.fr[d.lvl[l0 + i]];
-      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const MfFront F = i < MF_FCACHE ? fc[i] : d.fr[d.lvl[l0 + i]];
-        pre[i + 1] = F.NT * TB * nrhs;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        pre[0] = 0;
-        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+      for (int i = threadIdx.x; i <= nf; i += blockDim.x) {
+        pre[i] = job.pre[l0 + l + i] * nrhs;
+        preB[i] = job.pre[(pass == 0 ? 1 : 2) * job.npre + l0 + l + i];
       }
       __syncthreads();
       {
@@ -3038,25 +3066,16 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
         }
       }
       grid.sync();
+      mf_stamp(job.tstamp, nst++);
       // ---- (B) products
-      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const MfFront F = i < MF_FCACHE ? fc[i] : d.fr[d.lvl[l0 + i]];
-        pre[i + 1] = pass == 0 ? (F.NT * TB + MF_GR - 1) / MF_GR : (F.nE + MF_GR - 1) / MF_GR;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        pre[0] = 0;
-        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
-      }
-      __syncthreads();
       int fi = 0;
-      for (int gi = blockIdx.x; gi < pre[nf]; gi += gridDim.x) {
-        while (pre[fi + 1] <= gi) ++fi;
+      for (int gi = blockIdx.x; gi < preB[nf]; gi += gridDim.x) {
+        while (preB[fi + 1] <= gi) ++fi;
         const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
         const int rows = F.NT * TB, ncol = F.NE * TB;
         const double* vin = job.Vin + (size_t)F.voff * nrhs;
         if (pass == 0) {
-          const int r0c = (gi - pre[fi]) * MF_GR, nr = min(MF_GR, rows - r0c);
+          const int r0c = (gi - preB[fi]) * MF_GR, nr = min(MF_GR, rows - r0c);
           const int kmax = r0c < ncol ? min(ncol, ((r0c + nr - 1) / TB + 1) * TB) : ncol;
           double* Gs = sh;
           double* vs = Gs + (size_t)MF_GR * ncol;
@@ -3099,7 +3118,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
             job.Vout[((size_t)F.voff + r) * nrhs + s] = a;
           }
         } else {
-          const int j0 = (gi - pre[fi]) * MF_GR, nj = min(MF_GR, F.nE - j0);
+          const int j0 = (gi - preB[fi]) * MF_GR, nj = min(MF_GR, F.nE - j0);
           const int rz0 = (j0 / TB) * TB;
           double* Gs = sh;                                 // nj x rows
           double* zs = Gs + (size_t)MF_GR * rows;          // rows x nrhs (from rz0)
@@ -3138,6 +3157,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
         __syncthreads();
       }
       grid.sync();
+      mf_stamp(job.tstamp, nst++);
     }
   }
 }
@@ -3727,11 +3747,11 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 16384);
+      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 24576);
       if (e != cudaSuccess) return e;
       coop_grid = coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     }
-    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 16384 && !getenv("MSFV_MF_NOCOOP")) {
+    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 24576 && !getenv("MSFV_MF_NOCOOP")) {
       if (getenv("MSFV_MF_SCATTER") && smc2 <= (size_t)MF_SMEM_MAX - 8192) {   // scatter variant: fewer barriers, slower at config 4
         static bool a2 = false;
         if (!a2) {
@@ -3746,11 +3766,24 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
       }
-      MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs};
+      static unsigned long long* tst = nullptr;
+      const bool timing = getenv("MSFV_MF_TIMING") != nullptr;
+      if (timing && !tst) cudaMalloc(&tst, 256 * sizeof(unsigned long long));
+      MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
+                     P->npre};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
       count_launches(1);
       if (e != cudaSuccess) return e;
+      if (timing) {   // debug: per-phase durations (us) of this solve, stderr
+        unsigned long long h[256];
+        const int n = 1 + 4 * nl;
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, tst, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[mf solve nrhs=%d] total %.1f us:", nrhs, (h[n - 1] - h[0]) * 1e-3);
+        for (int i = 1; i < n; ++i) fprintf(stderr, " %s%.1f", (i % 2) ? "A" : "B", (h[i] - h[i - 1]) * 1e-3);
+        fprintf(stderr, "\n");
+      }
       return cudaGetLastError();
     }
   }
