@@ -201,15 +201,14 @@ class Engine:
         b3 = self.blocks[2]
         nb3 = n3 // b3
         plane = n1 * n2
-        m_dev, sigma, w, fl = self.empty(self.Nm), self.empty(self.Nm), self.empty(self.E), self.flags()
-        factor = self.empty(max(self.factor_doubles, 1))
-        Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
-        Kloc = self.empty(self.nbl * 64)
+        # the copies go out first: everything else below is host work that
+        # overlaps them
+        m_dev = self.empty(self.Nm)
         cur, cp = torch.cuda.current_stream(), self.copy_stream
         chunks = max(1, min(chunks, nb3))
         bounds = [round(i * nb3 / chunks) for i in range(chunks + 1)]
         ready = torch.cuda.Event()
-        ready.record(cur)                       # m_dev / flags allocated and zeroed on the current stream
+        ready.record(cur)                       # m_dev allocated on the current stream
         cp.wait_event(ready)
         evs = []
         with torch.cuda.stream(cp):
@@ -220,6 +219,10 @@ class Engine:
                 ev.record(cp)
                 evs.append(ev)
         m_dev.record_stream(cp)
+        sigma, w, fl = self.empty(self.Nm), self.empty(self.E), self.flags()
+        factor = self.empty(max(self.factor_doubles, 1))
+        Sint = self.empty(max(self.nbl * 8 * self.nI, 1))
+        Kloc = self.empty(self.nbl * 64)
         with phase("operator+basis (pipelined)"):
             for c in range(chunks):
                 bk0, bk1 = bounds[c], bounds[c + 1]

@@ -120,13 +120,14 @@ class ReducedState:
             self._A_k = _host(eng.coarse_dense(self.basis.Kloc, self.shift))
         return self._A_k
 
-    def check(self):
-        """Resolve the status of the forward chain (one device sync)."""
+    def check(self, host_flags=None):
+        """Resolve the status of the forward chain (one device sync, or none
+        when the caller already read the status word: ``host_flags``)."""
         if not getattr(self, "pending", False):
             return
         self.pending = False
         from .basis import raise_status
-        f = int(self.flags.item())
+        f = int(self.flags.item()) if host_flags is None else int(host_flags)
         raise_status(f & 7)
         if f & 8:
             # diagonal shift fallback (forward.py:122-129)
@@ -189,9 +190,23 @@ def forward_reduced_dev(op, survey, basis, defer_check=False):
 
 
 def forward_reduced(op, survey, basis):
-    """Predicted data through the projected problem (forward.py:105-144)."""
-    D, state = forward_reduced_dev(op, survey, basis)
-    return _host(D), state
+    """Predicted data through the projected problem (forward.py:105-144).
+
+    The status word and D come back in one synchronisation (both copies are
+    queued before the wait); the shift fallback, when the status asks for it,
+    recomputes D and copies it again."""
+    import torch
+    D, state = forward_reduced_dev(op, survey, basis, defer_check=True)
+    Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
+    fh = torch.empty(1, dtype=state.flags.dtype, pin_memory=True)
+    Dh.copy_(D, non_blocking=True)
+    fh.copy_(state.flags, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    f = int(fh[0])
+    state.check(host_flags=f)
+    if f & 8:
+        return _host(state.D_dev), state
+    return Dh.numpy(), state
 
 
 class AdaptiveSensitivity:
