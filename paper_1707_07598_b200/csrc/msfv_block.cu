@@ -96,6 +96,73 @@ __global__ void __launch_bounds__(EW_THREADS * EW_LINES) k_edge_weights_lines(Ge
   }
 }
 
+// Plane-tile form: CTA (tile of EWT_TY edge lines, node plane k) stages the
+// premultiplied cell values (V/4) cv of cell planes k-1 and k, rows
+// j0-1 .. j0+EWT_TY-1, columns -1 .. n1 (zero outside the mesh) in shared
+// memory once, then forms the x- and y-edges of node plane k and the z-edges
+// of cell plane k from it.  Same products and the same ascending-cell
+// summation order as k_edge_weights (a skipped cell adds +0.0, which leaves
+// the sum bit-identical).
+constexpr int EWT_TY = 8, EWT_THREADS = 256, EWT_MAXW = 1024;
+__global__ void __launch_bounds__(EWT_THREADS) k_edge_weights_tile(Geo g, const double* __restrict__ cv,
+                                                                   double* __restrict__ w, int k0, int k1) {
+  extern __shared__ double q[];                 // [2][EWT_TY + 1][W]
+  const int W = g.n1 + 2, RW = (EWT_TY + 1) * W;
+  const int j0 = blockIdx.x * EWT_TY, k = k0 + blockIdx.y;
+  for (int t = threadIdx.x; t < 2 * RW; t += blockDim.x) {
+    const int dz = t / RW, r = (t - dz * RW) / W, c = t - dz * RW - r * W;
+    const int ci = c - 1, cj = j0 - 1 + r, ck = k - 1 + dz;
+    q[t] = (ci >= 0 && ci < g.n1 && cj >= 0 && cj < g.n2 && ck >= 0 && ck < g.n3)
+               ? __dmul_rn(g.qv, __ldg(cv + cell_id(g, ci, cj, ck)))
+               : 0.0;
+  }
+  __syncthreads();
+  auto Q = [&](int dz, int cj, int ci) { return q[dz * RW + (cj - j0 + 1) * W + ci + 1]; };
+  const int n1 = g.n1;
+  // x-edges of node plane k: lines j in [j0, j0 + TY) ∩ [0, n2]
+  {
+    const int nl = min(EWT_TY, g.n2 + 1 - j0);
+    const long long base = (long long)n1 * (j0 + (long long)(g.n2 + 1) * k);
+    for (int t = threadIdx.x; t < nl * n1; t += blockDim.x) {
+      const int jj = t / n1, i = t - jj * n1, j = j0 + jj;
+      double sum = 0.0;
+      sum = __dadd_rn(sum, Q(0, j - 1, i));
+      sum = __dadd_rn(sum, Q(0, j, i));
+      sum = __dadd_rn(sum, Q(1, j - 1, i));
+      sum = __dadd_rn(sum, Q(1, j, i));
+      w[base + t] = sum;
+    }
+  }
+  // y-edges of node plane k: lines j in [j0, j0 + TY) ∩ [0, n2)
+  {
+    const int nl = min(EWT_TY, g.n2 - j0);
+    const long long base = g.Ex + (long long)(n1 + 1) * (j0 + (long long)g.n2 * k);
+    for (int t = threadIdx.x; t < nl * (n1 + 1); t += blockDim.x) {
+      const int jj = t / (n1 + 1), i = t - jj * (n1 + 1), j = j0 + jj;
+      double sum = 0.0;
+      sum = __dadd_rn(sum, Q(0, j, i - 1));
+      sum = __dadd_rn(sum, Q(0, j, i));
+      sum = __dadd_rn(sum, Q(1, j, i - 1));
+      sum = __dadd_rn(sum, Q(1, j, i));
+      w[base + t] = sum;
+    }
+  }
+  // z-edges of cell plane k (k < k1, k < n3): lines j in [j0, j0 + TY) ∩ [0, n2]
+  if (k < k1 && k < g.n3) {
+    const int nl = min(EWT_TY, g.n2 + 1 - j0);
+    const long long base = g.Ex + g.Ey + (long long)(n1 + 1) * (j0 + (long long)(g.n2 + 1) * k);
+    for (int t = threadIdx.x; t < nl * (n1 + 1); t += blockDim.x) {
+      const int jj = t / (n1 + 1), i = t - jj * (n1 + 1), j = j0 + jj;
+      double sum = 0.0;
+      sum = __dadd_rn(sum, Q(1, j - 1, i - 1));
+      sum = __dadd_rn(sum, Q(1, j - 1, i));
+      sum = __dadd_rn(sum, Q(1, j, i - 1));
+      sum = __dadd_rn(sum, Q(1, j, i));
+      w[base + t] = sum;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ basis
 
 // Closed-box edge weights of a block, staged in shared memory.
@@ -720,7 +787,25 @@ cudaError_t launch_mul(long long n, const double* a, const double* b, double* ou
   count_launches(1);
   return cudaGetLastError();
 }
+static bool edge_tile_ok(const Geo& g) {
+  return g.n1 + 2 <= EWT_MAXW && (g.n2 + 1 + EWT_TY - 1) / EWT_TY < 65535 && g.n3 + 1 < 65535 && !getenv("MSFV_EW_LINES");
+}
+static cudaError_t launch_edge_tile(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st) {
+  const size_t smem = (size_t)2 * (EWT_TY + 1) * (g.n1 + 2) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_edge_weights_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)((size_t)2 * (EWT_TY + 1) * EWT_MAXW * sizeof(double)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((g.n2 + 1 + EWT_TY - 1) / EWT_TY, k1 - k0 + 1);
+  k_edge_weights_tile<<<grid, EWT_THREADS, smem, st>>>(g, cv, w, k0, k1);
+  count_launches(1);
+  return cudaGetLastError();
+}
 cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st) {
+  if (edge_tile_ok(g)) return launch_edge_tile(g, cv, w, 0, g.n3, st);
   const unsigned lines = (unsigned)(((long long)(g.n2 + 1) * (g.n3 + 1) + EW_LINES - 1) / EW_LINES);
   if (lines < 65535u) {
     const dim3 grid(1, lines, 3);
@@ -734,6 +819,7 @@ cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaS
 cudaError_t launch_edge_weights_planes(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st) {
   const unsigned lines = (unsigned)(((long long)(g.n2 + 1) * (k1 - k0 + 1) + EW_LINES - 1) / EW_LINES);
   if (k1 < k0 || lines >= 65535u) return cudaErrorInvalidValue;
+  if (edge_tile_ok(g)) return launch_edge_tile(g, cv, w, k0, k1, st);
   const dim3 grid(1, lines, 3);
   k_edge_weights_lines<<<grid, dim3(EW_THREADS, EW_LINES), 0, st>>>(g, cv, w, k0, k1);
   count_launches(1);
