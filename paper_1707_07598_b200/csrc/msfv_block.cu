@@ -103,62 +103,74 @@ __global__ void __launch_bounds__(EW_THREADS * EW_LINES) k_edge_weights_lines(Ge
 // of cell plane k from it.  Same products and the same ascending-cell
 // summation order as k_edge_weights (a skipped cell adds +0.0, which leaves
 // the sum bit-identical).
-constexpr int EWT_TY = 8, EWT_THREADS = 256, EWT_MAXW = 1024;
+constexpr int EWT_TY = 8, EWT_THREADS = 128, EWT_MAXW = 1024;
 __global__ void __launch_bounds__(EWT_THREADS) k_edge_weights_tile(Geo g, const double* __restrict__ cv,
                                                                    double* __restrict__ w, int k0, int k1) {
-  extern __shared__ double q[];                 // [2][EWT_TY + 1][W]
-  const int W = g.n1 + 2, RW = (EWT_TY + 1) * W;
+  constexpr int NR = 2 * (EWT_TY + 1);         // staged rows: (cell plane k-1 | k) x (rows j0-1 .. j0+TY-1)
+  extern __shared__ double q[];                 // [NR][W]
+  const int n1 = g.n1, W = n1 + 2, RW = (EWT_TY + 1) * W;
   const int j0 = blockIdx.x * EWT_TY, k = k0 + blockIdx.y;
-  for (int t = threadIdx.x; t < 2 * RW; t += blockDim.x) {
-    const int dz = t / RW, r = (t - dz * RW) / W, c = t - dz * RW - r * W;
-    const int ci = c - 1, cj = j0 - 1 + r, ck = k - 1 + dz;
-    q[t] = (ci >= 0 && ci < g.n1 && cj >= 0 && cj < g.n2 && ck >= 0 && ck < g.n3)
-               ? __dmul_rn(g.qv, __ldg(cv + cell_id(g, ci, cj, ck)))
-               : 0.0;
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    // all NR loads of a column in flight before the stores
+    const int ci = c - 1;
+    double v[NR];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+      const int dz = rr / (EWT_TY + 1), cj = j0 - 1 + rr - dz * (EWT_TY + 1), ck = k - 1 + dz;
+      v[rr] = (ci >= 0 && ci < n1 && cj >= 0 && cj < g.n2 && ck >= 0 && ck < g.n3)
+                  ? __ldg(cv + cell_id(g, ci, cj, ck)) : 0.0;
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) q[rr * W + c] = __dmul_rn(g.qv, v[rr]);   // (V/4) * 0 = +0 outside
   }
   __syncthreads();
   auto Q = [&](int dz, int cj, int ci) { return q[dz * RW + (cj - j0 + 1) * W + ci + 1]; };
-  const int n1 = g.n1;
   // x-edges of node plane k: lines j in [j0, j0 + TY) ∩ [0, n2]
   {
     const int nl = min(EWT_TY, g.n2 + 1 - j0);
-    const long long base = (long long)n1 * (j0 + (long long)(g.n2 + 1) * k);
-    for (int t = threadIdx.x; t < nl * n1; t += blockDim.x) {
-      const int jj = t / n1, i = t - jj * n1, j = j0 + jj;
-      double sum = 0.0;
-      sum = __dadd_rn(sum, Q(0, j - 1, i));
-      sum = __dadd_rn(sum, Q(0, j, i));
-      sum = __dadd_rn(sum, Q(1, j - 1, i));
-      sum = __dadd_rn(sum, Q(1, j, i));
-      w[base + t] = sum;
+    double* out = w + (long long)n1 * (j0 + (long long)(g.n2 + 1) * k);
+    for (int jj = 0; jj < nl; ++jj) {
+      const int j = j0 + jj;
+      for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+        double sum = 0.0;
+        sum = __dadd_rn(sum, Q(0, j - 1, i));
+        sum = __dadd_rn(sum, Q(0, j, i));
+        sum = __dadd_rn(sum, Q(1, j - 1, i));
+        sum = __dadd_rn(sum, Q(1, j, i));
+        out[jj * n1 + i] = sum;
+      }
     }
   }
   // y-edges of node plane k: lines j in [j0, j0 + TY) ∩ [0, n2)
   {
     const int nl = min(EWT_TY, g.n2 - j0);
-    const long long base = g.Ex + (long long)(n1 + 1) * (j0 + (long long)g.n2 * k);
-    for (int t = threadIdx.x; t < nl * (n1 + 1); t += blockDim.x) {
-      const int jj = t / (n1 + 1), i = t - jj * (n1 + 1), j = j0 + jj;
-      double sum = 0.0;
-      sum = __dadd_rn(sum, Q(0, j, i - 1));
-      sum = __dadd_rn(sum, Q(0, j, i));
-      sum = __dadd_rn(sum, Q(1, j, i - 1));
-      sum = __dadd_rn(sum, Q(1, j, i));
-      w[base + t] = sum;
+    double* out = w + g.Ex + (long long)(n1 + 1) * (j0 + (long long)g.n2 * k);
+    for (int jj = 0; jj < nl; ++jj) {
+      const int j = j0 + jj;
+      for (int i = threadIdx.x; i <= n1; i += blockDim.x) {
+        double sum = 0.0;
+        sum = __dadd_rn(sum, Q(0, j, i - 1));
+        sum = __dadd_rn(sum, Q(0, j, i));
+        sum = __dadd_rn(sum, Q(1, j, i - 1));
+        sum = __dadd_rn(sum, Q(1, j, i));
+        out[jj * (n1 + 1) + i] = sum;
+      }
     }
   }
   // z-edges of cell plane k (k < k1, k < n3): lines j in [j0, j0 + TY) ∩ [0, n2]
   if (k < k1 && k < g.n3) {
     const int nl = min(EWT_TY, g.n2 + 1 - j0);
-    const long long base = g.Ex + g.Ey + (long long)(n1 + 1) * (j0 + (long long)(g.n2 + 1) * k);
-    for (int t = threadIdx.x; t < nl * (n1 + 1); t += blockDim.x) {
-      const int jj = t / (n1 + 1), i = t - jj * (n1 + 1), j = j0 + jj;
-      double sum = 0.0;
-      sum = __dadd_rn(sum, Q(1, j - 1, i - 1));
-      sum = __dadd_rn(sum, Q(1, j - 1, i));
-      sum = __dadd_rn(sum, Q(1, j, i - 1));
-      sum = __dadd_rn(sum, Q(1, j, i));
-      w[base + t] = sum;
+    double* out = w + g.Ex + g.Ey + (long long)(n1 + 1) * (j0 + (long long)(g.n2 + 1) * k);
+    for (int jj = 0; jj < nl; ++jj) {
+      const int j = j0 + jj;
+      for (int i = threadIdx.x; i <= n1; i += blockDim.x) {
+        double sum = 0.0;
+        sum = __dadd_rn(sum, Q(1, j - 1, i - 1));
+        sum = __dadd_rn(sum, Q(1, j - 1, i));
+        sum = __dadd_rn(sum, Q(1, j, i - 1));
+        sum = __dadd_rn(sum, Q(1, j, i));
+        out[jj * (n1 + 1) + i] = sum;
+      }
     }
   }
 }
