@@ -69,6 +69,53 @@ __global__ void k_points_restrict(Geo g, PointsDev P, const double* __restrict__
   out[i] = v;
 }
 
+// Warp per coarse node: the lanes evaluate 32 entries' point factors
+// val_t S(node_t, cc) and columns at once (the dependent index loads of
+// different entries overlap), then each lane sums its right-hand sides over
+// the staged entries in entry order: the same products and summation order as
+// k_points_restrict.
+constexpr int PR_WARPS = 4;
+__global__ void __launch_bounds__(32 * PR_WARPS) k_points_restrict_w(Geo g, PointsDev P, const double* __restrict__ Sint,
+                                                                  const double* __restrict__ Z, int nrhs,
+                                                                  double* __restrict__ out) {
+  __shared__ double pe[PR_WARPS][32];
+  __shared__ int ce[PR_WARPS][32];
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  const int c = blockIdx.x * PR_WARPS + wv;
+  if (c >= g.kc) return;
+  const long long e0 = P.cptr[c], e1 = P.cptr[c + 1];
+  double acc[2] = {0.0, 0.0};                   // s = lane, lane + 32 (nrhs <= 64)
+  for (long long eb = e0; eb < e1; eb += 32) {
+    const int cnt = (int)min((long long)32, e1 - eb);
+    if (lane < cnt) {
+      const long long packed = P.cent[eb + lane];
+      const long long t = packed >> 3;
+      int corner;
+      const double sv = point_s(g, P, Sint, t, (int)(packed & 7), corner);
+      pe[wv][lane] = P.val[t] * sv;
+      ce[wv][lane] = P.col[t];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int sidx = lane + 32 * h;
+      if (sidx >= nrhs) continue;
+      double v = acc[h];
+      for (int j = 0; j < cnt; ++j) {
+        const int col = ce[wv][j];
+        const double z = Z ? Z[(size_t)col * nrhs + sidx] : (col == sidx ? 1.0 : 0.0);
+        if (z != 0.0) v += pe[wv][j] * z;
+      }
+      acc[h] = v;
+    }
+    __syncwarp();
+  }
+  for (int h = 0; h < 2; ++h) {
+    const int sidx = lane + 32 * h;
+    if (sidx < nrhs) out[(size_t)c * nrhs + sidx] = acc[h];
+  }
+}
+
 __global__ void k_points_scatter(Geo g, PointsDev P, const double* __restrict__ Z, int nrhs, double* __restrict__ field) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= P.nu * nrhs) return;
@@ -117,7 +164,10 @@ cudaError_t launch_points_restrict(const Geo& g, const PointsDev& P, const doubl
                                    int nrhs, double* out, cudaStream_t st) {
   long long tot = (long long)g.kc * nrhs;
   if (tot == 0) return cudaSuccess;
-  k_points_restrict<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Z, nrhs, out);
+  if (nrhs <= 64)
+    k_points_restrict_w<<<nblk(g.kc, PR_WARPS), 32 * PR_WARPS, 0, st>>>(g, P, Sint, Z, nrhs, out);
+  else
+    k_points_restrict<<<nblk(tot, 128), 128, 0, st>>>(g, P, Sint, Z, nrhs, out);
   count_launches(1);
   return cudaGetLastError();
 }
