@@ -914,7 +914,7 @@ __host__ __device__ inline int skel_lines_axis(int bp, int bq, int lp, int lq) {
 }
 __global__ void __launch_bounds__(SKL_WARPS * 32) k_skel_lines(Geo g, const double* __restrict__ w,
                                                               double* __restrict__ Kloc, int rec_max, int jb0,
-                                                              int jb1) {
+                                                              int jb1, int overwrite) {
   extern __shared__ __align__(16) double skl[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int jb = jb0 + blockIdx.x * SKL_WARPS + wid;
@@ -996,8 +996,31 @@ __global__ void __launch_bounds__(SKL_WARPS * 32) k_skel_lines(Geo g, const doub
     mma884(K.x, K.y, a, b);
   }
   double* kl = Kloc + (size_t)jb * 64 + lane * 2;
-  kl[0] += K.x;
-  kl[1] += K.y;
+  if (overwrite) {
+    kl[0] = K.x;
+    kl[1] = K.y;
+  } else {
+    kl[0] += K.x;
+    kl[1] += K.y;
+  }
+}
+
+__global__ void k_kloc_add(double* __restrict__ Kloc, const double* __restrict__ Ks, long long i0, long long i1) {
+  const long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < i1) Kloc[i] += Ks[i];
+}
+
+// The skeleton line sums depend only on the edge weights: they run on a side
+// stream beside the basis kernel (into a scratch copy, added to Kloc once
+// both are done).  Per device: stream, two events, scratch.
+namespace {
+struct SkelSide {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ew = nullptr, ed = nullptr;
+  double* buf = nullptr;
+  size_t cap = 0;
+};
+SkelSide g_skel_side[64];
 }
 
 // ------------------------------------------------------------ block solve
@@ -1189,6 +1212,50 @@ template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
                                      double* Kloc, int* flags, bool bwd, cudaStream_t st, int jb0, int jb1) {
   cudaError_t e;
+  const bool lines = g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2 && !getenv("MSFV_SKEL_GENERIC");
+  const int rec_max = skel_lines_axis(g.b2, g.b3, 1, 1) + skel_lines_axis(g.b1, g.b3, 1, 1) +
+                      skel_lines_axis(g.b1, g.b2, 1, 1) + 3;
+  const size_t skl_sm = (size_t)SKL_WARPS * rec_max * 16 * sizeof(double);
+  if (lines && skl_sm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_skel_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)skl_sm);
+    if (e != cudaSuccess) return e;
+  }
+  SkelSide* side = nullptr;
+  if (lines && !getenv("MSFV_SKEL_SERIAL")) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+      side = &g_skel_side[dev];
+      if (!side->st) {
+        e = cudaStreamCreateWithFlags(&side->st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->ew, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->ed, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+      }
+      const size_t need = (size_t)g.nbl * 64;
+      if (side->cap < need) {
+        if (side->buf) {
+          cudaDeviceSynchronize();
+          cudaFree(side->buf);
+        }
+        side->buf = nullptr;
+        side->cap = 0;
+        e = cudaMalloc(&side->buf, need * sizeof(double));
+        if (e != cudaSuccess) return e;
+        side->cap = need;
+      }
+      // skeleton sums first (their CTAs take SMs before the long basis kernel fills them)
+      e = cudaEventRecord(side->ew, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side->st, side->ew, 0);
+      if (e != cudaSuccess) return e;
+      k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, skl_sm, side->st>>>(
+          g, w, side->buf, rec_max, jb0, jb1, 1);
+      count_launches(1);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaEventRecord(side->ed, side->st);
+      if (e != cudaSuccess) return e;
+    }
+  }
   if constexpr (PT == 7) {
     const int v = basis_variant(g);
     if (v == 1)
@@ -1206,16 +1273,14 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
   count_launches(1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2 && !getenv("MSFV_SKEL_GENERIC")) {
-    const int rec_max = skel_lines_axis(g.b2, g.b3, 1, 1) + skel_lines_axis(g.b1, g.b3, 1, 1) +
-                        skel_lines_axis(g.b1, g.b2, 1, 1) + 3;
-    const size_t sm = (size_t)SKL_WARPS * rec_max * 16 * sizeof(double);
-    if (sm > 48 * 1024) {
-      cudaError_t e2 = cudaFuncSetAttribute(k_skel_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e2 != cudaSuccess) return e2;
-    }
-    k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, sm, st>>>(g, w, Kloc, rec_max,
-                                                                                              jb0, jb1);
+  if (side) {
+    e = cudaStreamWaitEvent(st, side->ed, 0);
+    if (e != cudaSuccess) return e;
+    const long long i0 = (long long)jb0 * 64, i1 = (long long)jb1 * 64;
+    k_kloc_add<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, st>>>(Kloc, side->buf, i0, i1);
+  } else if (lines) {
+    k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, skl_sm, st>>>(
+        g, w, Kloc, rec_max, jb0, jb1, 0);
   } else
     k_skel_galerkin<<<(unsigned)((jb1 - jb0 + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc,
                                                                                                      jb0, jb1);
@@ -1239,6 +1304,7 @@ static cudaError_t launch_solve_tc_t(const Geo& g, const double* LT, const doubl
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st, bool bwd, int jb0, int jb1) {
   if (jb1 < 0) jb1 = g.nbl;
+  if (jb1 <= jb0) return cudaSuccess;
   switch (tc_band(g)) {
     case 0: return launch_basis_tc_t<0>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     case 1: return launch_basis_tc_t<1>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
