@@ -524,7 +524,8 @@ def run_gpu(args, rank, world, log):
     except Exception:  # noqa: BLE001
         pass
     roof = {"kernel": "k_basis_tc<PT,false> + k_skel_lines (per-block A_II band Cholesky, 8-RHS forward sweep, "
-                      "local Galerkin; the backward sweeps run concurrently in k_basis_bwd)",
+                      "local Galerkin; skeleton line sums on a side stream beside it; the backward sweeps run "
+                      "concurrently in k_basis_bwd)",
             "bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes", "traffic_source": traffic_src,
             "algorithmic_bytes": int(eng.nbl * (eng.factor_doubles / eng.nbl * 8 + 8 * eng.nI * 8 + 64 * 8)),
