@@ -19,6 +19,7 @@
 // slot t = L_{J+t,J}.   Fragment layouts (m8n8k4 f64):
 //   A[m][k] at lane 4m+k ; B[k][n] at lane 4n+k ; C[m][n] at lane 4m+n/2, slot n%2
 // An 8x8 tile in "A-frag" form is two A fragments (k = 0..3 and 4..7).
+#include <mutex>
 #include <cstdlib>
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
@@ -1016,9 +1017,11 @@ __global__ void k_kloc_add(double* __restrict__ Kloc, const double* __restrict__
 namespace {
 struct SkelSide {
   cudaStream_t st = nullptr;
-  cudaEvent_t ew = nullptr, ed = nullptr;
+  cudaEvent_t ew = nullptr, ed = nullptr, ek = nullptr;   // w ready | sums done | scratch consumed
+  bool ek_live = false;
   double* buf = nullptr;
   size_t cap = 0;
+  std::mutex mu;                                           // host-side sequence (one build at a time per device)
 };
 SkelSide g_skel_side[64];
 }
@@ -1221,15 +1224,18 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
     if (e != cudaSuccess) return e;
   }
   SkelSide* side = nullptr;
+  std::unique_lock<std::mutex> side_lock;
   if (lines && !getenv("MSFV_SKEL_SERIAL")) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64) {
       side = &g_skel_side[dev];
+      side_lock = std::unique_lock<std::mutex>(side->mu);
       if (!side->st) {
         e = cudaStreamCreateWithFlags(&side->st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->ew, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->ed, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->ek, cudaEventDisableTiming);
         if (e != cudaSuccess) return e;
       }
       const size_t need = (size_t)g.nbl * 64;
@@ -1247,6 +1253,8 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
       // skeleton sums first (their CTAs take SMs before the long basis kernel fills them)
       e = cudaEventRecord(side->ew, st);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(side->st, side->ew, 0);
+      // the scratch is reused: the previous build's add (possibly on another stream) must have read it
+      if (e == cudaSuccess && side->ek_live) e = cudaStreamWaitEvent(side->st, side->ek, 0);
       if (e != cudaSuccess) return e;
       k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, skl_sm, side->st>>>(
           g, w, side->buf, rec_max, jb0, jb1, 1);
@@ -1278,6 +1286,9 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
     if (e != cudaSuccess) return e;
     const long long i0 = (long long)jb0 * 64, i1 = (long long)jb1 * 64;
     k_kloc_add<<<(unsigned)((i1 - i0 + 255) / 256), 256, 0, st>>>(Kloc, side->buf, i0, i1);
+    e = cudaEventRecord(side->ek, st);
+    if (e != cudaSuccess) return e;
+    side->ek_live = true;
   } else if (lines) {
     k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, skl_sm, st>>>(
         g, w, Kloc, rec_max, jb0, jb1, 0);
