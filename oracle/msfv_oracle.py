@@ -356,12 +356,34 @@ class Basis:
 
         def task(j):
             I = self.I[j]
-            return sla.cho_solve(self.factors[j], w[I], check_finite=False) if I.size else None
+            return self.factors[j].solve(w[I]) if I.size else None
 
         for I, sol in zip(self.I, run_indexed(task, len(self.I))):
             if sol is not None:
                 out[I] = sol
         return out
+
+
+DENSE_BLOCK_LIMIT = 2000        # basis.py (DENSE_BLOCK_LIMIT)
+
+
+class BlockFactor:
+    """One block's A_II factor (_BlockFactor, basis.py:258-298): dense lower
+    Cholesky up to DENSE_BLOCK_LIMIT unknowns, SuperLU beyond (the explicit
+    inverse the reference switches to for wide solves only changes rounding)."""
+
+    def __init__(self, A_II_sparse):
+        self.n = A_II_sparse.shape[0]
+        self.chol = self.lu = None
+        if self.n <= DENSE_BLOCK_LIMIT:
+            self.chol = sla.cho_factor(A_II_sparse.toarray(), lower=True, check_finite=False)   # basis.py:271-275
+        else:
+            self.lu = spla.splu(sp.csc_matrix(A_II_sparse))                                    # basis.py:276-278
+
+    def solve(self, B):
+        if self.chol is not None:
+            return sla.cho_solve(self.chol, B, check_finite=False)
+        return self.lu.solve(np.asarray(B, dtype=float))
 
 
 def build_basis(op, part, cache=None):
@@ -379,10 +401,9 @@ def build_basis(op, part, cache=None):
         if I.size == 0:
             return None, np.zeros((0, cols.size))
         AI = A[I]
-        A_II = AI[:, I].toarray()
         rhs = -(AI[:, B] @ cache.xb[j])                           # basis.py:548 (rhs0 = 0)
-        f = sla.cho_factor(A_II, lower=True, check_finite=False)    # basis.py:275
-        return f, (sla.cho_solve(f, rhs, check_finite=False) if cols.size else np.zeros((I.size, 0)))
+        f = BlockFactor(AI[:, I])                                   # basis.py:553-563
+        return f, (f.solve(np.asarray(rhs)) if cols.size else np.zeros((I.size, 0)))
 
     res = run_indexed(task, part.n_blocks)
     factors = [r[0] for r in res]
@@ -524,7 +545,7 @@ def apply_Yk(basis, v, m):
         nz = np.flatnonzero(Wd.any(axis=0))
         if nz.size == 0:
             continue
-        sol = -sla.cho_solve(basis.factors[j], Wd[:, nz], check_finite=False)
+        sol = -basis.factors[j].solve(Wd[:, nz])
         rows.append(np.repeat(I, nz.size))
         cols.append(np.tile(cells[nz], I.size))
         vals.append(sol.ravel())

@@ -18,7 +18,9 @@ def pytest_configure(config):
 
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GOLDEN_CASES = ["c444_b222", "c664_b332", "c888_b444_h", "c16_b844", "c16_b8", "c32_b8"]
+GOLDEN_CASES = ["c444_b222", "c664_b332", "c888_b444_h", "c16_b844", "c16_b8", "c32_b8", "c32_b8_int"]
+# 12^3 / 16^3-style blocks beyond the register-tile band (large-block local solver)
+LARGE_CASES = ["c32_b16x4", "c32_b16", "c64_b16_t3"]
 
 
 def load_golden(name):
@@ -55,3 +57,60 @@ def rel(a, b):
     b = np.asarray(b, dtype=float)
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def pattern_digest(M):
+    """sha256 of a sparse matrix's index arrays (tests/golden/make_golden.py)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(M.indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(M.indices, dtype=np.int64).tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8)
+
+
+def basis_errors(g, S, T, w=None):
+    """Pattern checks (bit-exact, asserted) and relative errors of S, S T and w
+    against a golden fixture in either its full or its compact form."""
+    errs = {}
+    if "S_digest" in g:
+        assert S.nnz == int(g["S_nnz"]), "S nnz differs"
+        assert np.array_equal(pattern_digest(S), g["S_digest"]), "S pattern differs"
+        prj = np.random.default_rng(7)
+        rn, rk = prj.standard_normal(S.shape[0]), prj.standard_normal(S.shape[1])
+        errs["S_rn"] = rel(S.T @ rn, g["S_rn"])
+        errs["S_rk"] = rel(S @ rk, g["S_rk"])
+        errs["S_norm"] = abs(np.linalg.norm(S.data) - float(g["S_norm"])) / float(g["S_norm"])
+        errs["US"] = rel((S @ T).T @ rn, g["US_rs"])
+        if w is not None:
+            errs["w"] = abs(np.linalg.norm(w) - float(g["w_norm"])) / float(g["w_norm"])
+    else:
+        assert np.array_equal(S.indptr, g["S_indptr"]), "S indptr differs"
+        assert np.array_equal(S.indices, g["S_indices"]), "S indices differ"
+        errs["S"] = rel(S.data, g["S_data"])
+        errs["US"] = rel(S @ T, g["US"])
+        if w is not None:
+            errs["w"] = rel(w, g["w"])
+    return errs
+
+
+def table3_errors(g, Y=None, X=None):
+    """apply_Yk / apply_Xk against a fixture: patterns bit-exact (asserted),
+    values as relative errors (full arrays or projections)."""
+    errs = {}
+    if X is not None:
+        if "X_digest" in g:
+            assert X.nnz == int(g["X_nnz"]) and np.array_equal(pattern_digest(X), g["X_digest"]), "X_k pattern"
+            errs["X_rm"] = rel(X @ g["rm"], g["X_rm"])
+            errs["X_rt"] = rel(X.T @ g["X_rk"], g["X_rt"])
+        else:
+            assert np.array_equal(X.indptr, g["X_indptr"]) and np.array_equal(X.indices, g["X_indices"]), "X_k pattern"
+            errs["X"] = rel(X.data, g["X_data"])
+    if Y is not None:
+        if "Y_digest" in g:
+            assert Y.nnz == int(g["Y_nnz"]) and np.array_equal(pattern_digest(Y), g["Y_digest"]), "Y_k pattern"
+            errs["Y_rm"] = rel(Y @ g["rm"], g["Y_rm"])
+            errs["Y_rt"] = rel(Y.T @ g["Y_rq"], g["Y_rt"])
+        else:
+            assert np.array_equal(Y.indptr, g["Y_indptr"]) and np.array_equal(Y.indices, g["Y_indices"]), "Y_k pattern"
+            errs["Y"] = rel(Y.data, g["Y_data"])
+    return errs

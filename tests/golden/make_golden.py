@@ -44,6 +44,32 @@ def random_survey(mesh, n_rec, n_src, rng):
     return Survey(P=P, Q=Q)
 
 
+def top_random_survey(mesh, n_rec, n_src, rng):
+    """Random receivers and x-dipoles on the top node plane (models.py:54-83 layout, random positions)."""
+    n = mesh.n_nodes - 1
+    kt = mesh.n3
+    top = mesh.node_index(*np.meshgrid(np.arange(mesh.n1 + 1), np.arange(mesh.n2 + 1), indexing="ij"), kt)
+    top = np.sort(top.ravel()) - 1
+    rec = np.sort(rng.choice(top, size=n_rec, replace=False))
+    P = sp.csc_matrix((np.ones(n_rec), (rec, np.arange(n_rec))), shape=(n, n_rec))
+    i = rng.choice(mesh.n1, size=n_src, replace=False)
+    j = rng.integers(0, mesh.n2 + 1, size=n_src)
+    a = mesh.node_index(i, j, kt) - 1
+    rows = np.concatenate([a, a + 1])
+    cols = np.tile(np.arange(n_src), 2)
+    vals = np.concatenate([np.ones(n_src), -np.ones(n_src)])
+    return Survey(P=P, Q=sp.csc_matrix((vals, (rows, cols)), shape=(n, n_src)))
+
+
+def pattern_digest(M):
+    """sha256 of a CSR/CSC matrix's int32 index arrays (bit-exact pattern check)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(M.indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(M.indices, dtype=np.int64).tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8).copy()
+
+
 def smooth_field(mesh, rng, sigma_cells, std):
     g = rng.standard_normal((mesh.n3, mesh.n2, mesh.n1))
     g = ndi.gaussian_filter(g, sigma_cells, mode="reflect")
@@ -59,7 +85,18 @@ CASES = {
     "c16_b844": ((16, 8, 8), (1.0, 1.0, 1.0), (8, 4, 4), ("smooth", 2.0, 1.0), ("random", 12, 3), True),
     "c16_b8": ((16, 16, 16), (1.0, 1.0, 1.0), (8, 8, 8), ("smooth", 2.0, 1.0), ("top", (2, 2), (4, 4)), False),
     "c32_b8": ((32, 32, 32), (1.0, 1.0, 1.0), (8, 8, 8), ("smooth", 3.0, 1.5), ("top", (2, 2), (8, 8)), False),
+    # round 2: 8^3 blocks with receivers and dipoles inside block interiors
+    "c32_b8_int": ((32, 32, 16), (1.0, 1.0, 1.0), (8, 8, 8), ("smooth", 3.0, 1.5), ("random", 40, 6), False),
+    # blocks beyond the register-tile band: 16x16x4 (n_I 675, half band 225; Y_k as a digest)
+    "c32_b16x4": ((32, 32, 8), (1.0, 1.0, 1.0), (16, 16, 4), ("smooth", 3.0, 1.0), ("random", 24, 4), "digest"),
+    # 16^3 blocks: n_I = 3375 > 2000, the reference factors them with SuperLU (basis.py:276-278)
+    "c32_b16": ((32, 32, 32), (1.0, 1.0, 1.0), (16, 16, 16), ("smooth", 4.0, 1.5), ("random", 30, 5), False),
+    # the paper's Table-3 geometry: 64x64x32 cells, 16^3 blocks, top survey
+    "c64_b16_t3": ((64, 64, 32), (1 / 64, 1 / 64, 1 / 64), (16, 16, 16), ("smooth", 4.0, 1.0), ("toprandom", 64, 6),
+                   "xonly"),
 }
+# fixtures whose large arrays are stored as projections / digests
+COMPACT = {"c32_b16x4", "c32_b16", "c64_b16_t3"}
 
 
 def make_case(name, spec, seed=20240615):
@@ -75,6 +112,8 @@ def make_case(name, spec, seed=20240615):
         m = smooth_field(mesh, rng, mkind[1], mkind[2])
     if skind[0] == "random":
         survey = random_survey(mesh, skind[1], skind[2], rng)
+    elif skind[0] == "toprandom":
+        survey = top_random_survey(mesh, skind[1], skind[2], rng)
     else:
         survey = build_survey(mesh, n_src=skind[1], n_rec=skind[2])
     builder = BasisBuilder(part, BasisSpec(families=("lagrange",)))
@@ -109,7 +148,31 @@ def make_case(name, spec, seed=20240615):
         out.update(A_data=op.A.data, A_indices=op.A.indices, A_indptr=op.A.indptr)
     if basis.k <= 200:
         out["A_k"] = np.asarray(state.A_k)
-    if do_yk:
+    if name in COMPACT:
+        prj = np.random.default_rng(7)
+        rn, rk = prj.standard_normal(basis.n), prj.standard_normal(basis.k)
+        for key in ("S_data", "S_indices", "S_indptr", "US", "w"):
+            out.pop(key)
+        out.update(S_digest=pattern_digest(basis.S), S_nnz=np.array(basis.S.nnz), S_rn=basis.S.T @ rn,
+                   S_rk=basis.S @ rk, S_norm=np.array(np.linalg.norm(basis.S.data)),
+                   US_rs=(basis.S @ state.T).T @ rn, w_norm=np.array(np.linalg.norm(op.edge_weights)),
+                   w_sum=np.array(op.edge_weights.sum()))
+    if do_yk in ("digest", "xonly"):
+        prj = np.random.default_rng(11)
+        v = rng.normal(size=basis.k)
+        wv = rng.normal(size=basis.n)
+        rm = prj.standard_normal(mesh.n_cells)
+        out.update(v=v, wv=wv, rm=rm)
+        X = apply_Xk(basis, wv, m)
+        xk = prj.standard_normal(basis.k)
+        out.update(X_digest=pattern_digest(X), X_nnz=np.array(X.nnz), X_rm=X @ rm, X_rk=xk,
+                   X_rt=X.T @ xk, X_norm=np.array(np.linalg.norm(X.data)))
+        if do_yk == "digest":
+            Y = apply_Yk(basis, v, m)
+            rq = prj.standard_normal(basis.n)
+            out.update(Y_rq=rq, Y_digest=pattern_digest(Y), Y_nnz=np.array(Y.nnz), Y_rm=Y @ rm, Y_rt=Y.T @ rq,
+                       Y_norm=np.array(np.linalg.norm(Y.data)))
+    elif do_yk:
         v = rng.normal(size=basis.k)
         wv = rng.normal(size=basis.n)
         Y = apply_Yk(basis, v, m)

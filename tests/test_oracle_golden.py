@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import GOLDEN_CASES, load_golden, rel
+from conftest import GOLDEN_CASES, LARGE_CASES, basis_errors, load_golden, rel, table3_errors
 from oracle import msfv_oracle as orc
 
 
@@ -17,24 +17,22 @@ def golden_problem(g):
     return mesh, part, orc.Survey(P, Q)
 
 
-@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("name", GOLDEN_CASES + LARGE_CASES)
 def test_oracle_matches_reference(name):
     g = load_golden(name)
     mesh, part, survey = golden_problem(g)
     prob = orc.AdaptiveProblem(part, survey)
     D, st = prob.simulate(g["m"])
     op, basis = st.op, st.basis
-    assert rel(op.w, g["w"]) <= 1e-14
     if "A_data" in g:
         assert np.array_equal(op.A.indptr, g["A_indptr"])
         assert np.array_equal(op.A.indices, g["A_indices"])
         assert rel(op.A.data, g["A_data"]) <= 1e-14
-    # integer pattern of S is bit-exact, values tight
-    assert np.array_equal(basis.S.indptr, g["S_indptr"])
-    assert np.array_equal(basis.S.indices, g["S_indices"])
-    assert rel(basis.S.data, g["S_data"]) <= 1e-13
+    # integer pattern of S is bit-exact (asserted inside), values tight
+    errs = basis_errors(g, basis.S, st.T, op.w)
+    assert errs.pop("w") <= 1e-14
+    assert max(errs.values()) <= 1e-12, errs
     assert rel(st.T, g["T"]) <= 1e-12
-    assert rel(basis.S @ st.T, g["US"]) <= 1e-12
     assert rel(D, g["D"]) <= 1e-12
     phi, resid = orc.misfit(D, g["d_obs"])
     assert abs(phi - float(g["phi"])) <= 1e-11 * abs(float(g["phi"]))
@@ -42,12 +40,8 @@ def test_oracle_matches_reference(name):
     assert rel(J.rapply(resid), g["g"]) <= 1e-11
     assert rel(J.apply(g["dm"]), g["Jv"]) <= 1e-11
     assert rel(J.rapply(g["W"]), g["JtW"]) <= 1e-11
-    if "Y_data" in g:
-        Y = orc.apply_Yk(basis, g["v"], g["m"])
-        assert np.array_equal(Y.indptr, g["Y_indptr"])
-        assert np.array_equal(Y.indices, g["Y_indices"])
-        assert rel(Y.data, g["Y_data"]) <= 1e-12
+    if "v" in g:
+        Y = orc.apply_Yk(basis, g["v"], g["m"]) if ("Y_data" in g or "Y_digest" in g) else None
         X = orc.apply_Xk(basis, g["wv"], g["m"])
-        assert np.array_equal(X.indptr, g["X_indptr"])
-        assert np.array_equal(X.indices, g["X_indices"])
-        assert rel(X.data, g["X_data"]) <= 1e-12
+        errs = table3_errors(g, Y, X)
+        assert max(errs.values()) <= 1e-12, errs
