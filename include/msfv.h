@@ -71,7 +71,8 @@ enum msfv_info {
   MSFV_INFO_PC = 13,
   MSFV_INFO_FACTOR_DOUBLES = 14,  /* size of the per-model local factor buffer  */
   MSFV_INFO_SCRATCH_DOUBLES = 15, /* scratch needed by msfv_basis_build         */
-  MSFV_INFO_TC = 16,              /* 1: FP64 tensor-core (DMMA) tile-band path  */
+  MSFV_INFO_TC = 16,              /* local solver: 1 DMMA register-window band (p <= 56, split build),
+                                     2 DMMA L2-resident band (larger blocks)     */
   MSFV_INFO_COARSE = 17,          /* coarse solver: 0 band, 1 z-plane ND band, 2 multifrontal ND */
   MSFV_INFO_COUNT = 18
 };
@@ -102,7 +103,8 @@ MSFV_API int msfv_edge_average(const msfv_plan* plan, const double* sigma, const
                       void* stream);
 
 /* Lagrange basis at w (assemble_basis, basis.py:511-616 with _BlockFactor
- * basis.py:258-298): per-block banded Cholesky factors (factor buffer of
+ * basis.py:258-298; every block size the reference accepts up to a half
+ * bandwidth ni1*ni2 <= 512, e.g. 16^3-cell blocks): per-block banded Cholesky factors (factor buffer of
  * MSFV_INFO_FACTOR_DOUBLES; opaque layout), interior basis values Sint
  * [nblocks][8][nI] and the per-block 8x8 Galerkin blocks Kloc [nblocks][64].
  * scratch: MSFV_INFO_SCRATCH_DOUBLES doubles.  flags |= LOCAL_NOT_SPD. */

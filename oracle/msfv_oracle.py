@@ -452,8 +452,12 @@ class Reduced:
         return self.lu.solve(np.asarray(B, dtype=float))
 
 
-def forward_reduced(op, survey, basis):
-    """F = S^T Q, A_k = S^T A S, T = A_k^-1 F, D = P^T S T (forward.py:105-144)."""
+def forward_reduced(op, survey, basis, force_shift=False):
+    """F = S^T Q, A_k = S^T A S, T = A_k^-1 F, D = P^T S T (forward.py:105-144).
+
+    ``force_shift`` (test hook) takes the reference's except-branch as if the
+    first factorization had failed: the shifted operator A_k + 1e-12 tr(A_k)/k I
+    (forward.py:122-129, 136-139)."""
     k = basis.k
     S = basis.S
     F = np.asarray((S.T @ survey.Q).todense())
@@ -461,6 +465,8 @@ def forward_reduced(op, survey, basis):
         A_k = (S.T @ (op.A @ S)).toarray()
         shift = 0.0
         try:
+            if force_shift:
+                raise sla.LinAlgError("forced")
             chol = sla.cho_factor(A_k, lower=True)
         except sla.LinAlgError:
             shift = 1e-12 * np.trace(A_k) / k                # forward.py:123
@@ -470,6 +476,8 @@ def forward_reduced(op, survey, basis):
         A_k = (S.T @ (op.A @ S)).tocsc()
         shift = 0.0
         try:
+            if force_shift:
+                raise RuntimeError("forced")
             lu = spla.splu(A_k)
         except RuntimeError:
             shift = 1e-12 * A_k.diagonal().sum() / k

@@ -175,355 +175,6 @@ __global__ void __launch_bounds__(EWT_THREADS) k_edge_weights_tile(Geo g, const 
   }
 }
 
-// ------------------------------------------------------------------ basis
-
-// Closed-box edge weights of a block, staged in shared memory.
-struct BoxW {
-  double* wx; double* wy; double* wz;
-  int b1, b2, b3;
-  __device__ __forceinline__ double x(int i, int j, int k) const { return wx[i + b1 * (j + (b2 + 1) * k)]; }
-  __device__ __forceinline__ double y(int i, int j, int k) const { return wy[i + (b1 + 1) * (j + b2 * k)]; }
-  __device__ __forceinline__ double z(int i, int j, int k) const { return wz[i + (b1 + 1) * (j + (b2 + 1) * k)]; }
-};
-
-__device__ void load_box_weights(const Geo& g, const double* __restrict__ w, int X0, int Y0, int Z0,
-                                 BoxW& bw) {
-  for (int t = threadIdx.x; t < g.nwx; t += blockDim.x) {
-    int i = t % g.b1, r = t / g.b1, j = r % (g.b2 + 1), k = r / (g.b2 + 1);
-    bw.wx[t] = w[ex_id(g, X0 + i, Y0 + j, Z0 + k)];
-  }
-  for (int t = threadIdx.x; t < g.nwy; t += blockDim.x) {
-    int i = t % (g.b1 + 1), r = t / (g.b1 + 1), j = r % g.b2, k = r / g.b2;
-    bw.wy[t] = w[ey_id(g, X0 + i, Y0 + j, Z0 + k)];
-  }
-  for (int t = threadIdx.x; t < g.nwz; t += blockDim.x) {
-    int i = t % (g.b1 + 1), r = t / (g.b1 + 1), j = r % (g.b2 + 1), k = r / (g.b2 + 1);
-    bw.wz[t] = w[ez_id(g, X0 + i, Y0 + j, Z0 + k)];
-  }
-}
-
-// One CTA per block: assemble the band of A_II and the 8 Lagrange right-hand
-// sides (rhs = -A_IB x_B, basis.py:548), factor A_II = L L^T in shared memory
-// (the reference's dense cho_factor, basis.py:275, restricted to the band where
-// all fill lives), solve, write the interior basis values and both band forms
-// of the factor, then accumulate this block's 8x8 Galerkin contribution
-// sum_e w_e/h^2 dS_e dS_e^T over the edges it owns.
-__global__ void __launch_bounds__(BASIS_THREADS)
-k_basis(Geo g, const double* __restrict__ w, double* __restrict__ Lc, double* __restrict__ Lr,
-        double* __restrict__ Sint, double* __restrict__ Kloc, int* __restrict__ flags) {
-  extern __shared__ double sm[];
-  const int jb = blockIdx.x;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
-  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  const int nI = g.nI, p = g.p, P1 = g.P1;
-  const int ntri = p * (p + 1) / 2;
-  const int cbsz = max(nI * P1, BASIS_THREADS * 36);
-
-  double* Cb = sm;                      // column band  Cb[col][r] = A[col+r][col]
-  double* Xs = Cb + cbsz;               // rhs / solution, [a][8]
-  double* invd = Xs + nI * 8;           // 1 / L[a][a]
-  BoxW bw;
-  bw.wx = invd + nI; bw.wy = bw.wx + g.nwx; bw.wz = bw.wy + g.nwy;
-  bw.b1 = g.b1; bw.b2 = g.b2; bw.b3 = g.b3;
-  int* tri = (int*)(bw.wz + g.nwz);     // packed (r << 16 | q) for 1 <= q <= r <= p
-
-  load_box_weights(g, w, X0, Y0, Z0, bw);
-  for (int f = tid; f < ntri; f += nt) {
-    int r = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
-    while (r * (r - 1) / 2 > f) --r;
-    while ((r + 1) * r / 2 <= f) ++r;
-    int q = f - r * (r - 1) / 2 + 1;
-    tri[f] = (r << 16) | q;
-  }
-  __syncthreads();
-
-  const double c1 = g.ih1 * g.ih1, c2 = g.ih2 * g.ih2, c3 = g.ih3 * g.ih3;
-  const bool has0 = (jb == 0);   // block 0 holds the pinned corner node 0
-  // band + rhs
-  for (int a = tid; a < nI; a += nt) {
-    int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
-    double kxm = bw.x(x - 1, y, z) * g.ih1 * g.ih1;
-    double kxp = bw.x(x, y, z) * g.ih1 * g.ih1;
-    double kym = bw.y(x, y - 1, z) * g.ih2 * g.ih2;
-    double kyp = bw.y(x, y, z) * g.ih2 * g.ih2;
-    double kzm = bw.z(x, y, z - 1) * g.ih3 * g.ih3;
-    double kzp = bw.z(x, y, z) * g.ih3 * g.ih3;
-    double* col = Cb + (size_t)a * P1;
-    for (int r = 0; r < P1; ++r) col[r] = 0.0;
-    col[0] = ((((kxm + kxp) + kym) + kyp) + kzm) + kzp;
-    if (x + 1 <= g.ni1) col[1] = -kxp;
-    if (y + 1 <= g.ni2) col[g.ni1] = -kyp;
-    if (z + 1 <= g.ni3) col[p] = -kzp;
-    double rhs[8];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) rhs[cc] = 0.0;
-    // boundary neighbours contribute -A_IB x_B = + k_e * hat(nb)
-    auto add_nb = [&](int xx, int yy, int zz, double kc) {
-      if (interior_index(g, xx, yy, zz) >= 0) return;
-      if (has0 && xx == 0 && yy == 0 && zz == 0) return;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) rhs[cc] += kc * hat_corner(cc, xx, yy, zz, g.b1, g.b2, g.b3);
-    };
-    add_nb(x - 1, y, z, kxm); add_nb(x + 1, y, z, kxp);
-    add_nb(x, y - 1, z, kym); add_nb(x, y + 1, z, kyp);
-    add_nb(x, y, z - 1, kzm); add_nb(x, y, z + 1, kzp);
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) Xs[a * 8 + cc] = rhs[cc];
-  }
-  (void)c1; (void)c2; (void)c3;
-  __syncthreads();
-
-  // right-looking band Cholesky
-  for (int jc = 0; jc < nI; ++jc) {
-    double* col = Cb + (size_t)jc * P1;
-    const int rmax = min(p, nI - 1 - jc);
-    double d = col[0];
-    if (!(d > 0.0)) {
-      if (tid == 0) atomicOr(flags, FLAG_LOCAL_NOT_SPD);
-      d = 1.0;
-    }
-    const double piv = sqrt(d);
-    const double inv = 1.0 / piv;
-    for (int r = 1 + tid; r <= rmax; r += nt) col[r] *= inv;
-    __syncthreads();
-    if (tid == 0) { col[0] = piv; invd[jc] = inv; }
-    const int nup = rmax * (rmax + 1) / 2;
-    for (int f = tid; f < nup; f += nt) {
-      int rq = tri[f];
-      int r = rq >> 16, q = rq & 0xffff;
-      Cb[(size_t)(jc + q) * P1 + (r - q)] -= col[r] * col[q];
-    }
-    __syncthreads();
-  }
-
-  // factor to global, both band forms, slot 0 holds the inverse diagonal
-  {
-    const size_t base = (size_t)jb * nI * g.P1s;
-    for (int t = tid; t < nI * P1; t += nt) {
-      int a = t / P1, r = t - a * P1;
-      double v = (r == 0) ? invd[a] : Cb[(size_t)a * P1 + r];
-      Lc[base + (size_t)a * g.P1s + r] = v;
-      // row form: Lr[i][d] = L[i][i-d]
-      int i = a, dd = r;
-      double u;
-      if (dd == 0) u = invd[i];
-      else u = (i - dd >= 0) ? Cb[(size_t)(i - dd) * P1 + dd] : 0.0;
-      Lr[base + (size_t)i * g.P1s + dd] = u;
-    }
-  }
-
-  // forward substitution L y = rhs (column axpy, deferred row scaling)
-  for (int i = 0; i < nI; ++i) {
-    const int rmax = min(p, nI - 1 - i);
-    const double inv = invd[i];
-    const double* col = Cb + (size_t)i * P1;
-    for (int t = tid; t < (rmax + 1) * 8; t += nt) {
-      int r = t >> 3, s = t & 7;
-      if (r == 0) { if (i > 0) Xs[(i - 1) * 8 + s] *= invd[i - 1]; }
-      else Xs[(i + r) * 8 + s] -= col[r] * (Xs[i * 8 + s] * inv);
-    }
-    __syncthreads();
-  }
-  if (nI > 0) {
-    if (tid < 8) Xs[(nI - 1) * 8 + tid] *= invd[nI - 1];
-    __syncthreads();
-  }
-  // backward substitution L^T x = y (row axpy)
-  for (int i = nI - 1; i >= 0; --i) {
-    const int dmax = min(p, i);
-    const double inv = invd[i];
-    for (int t = tid; t < (dmax + 1) * 8; t += nt) {
-      int d = t >> 3, s = t & 7;
-      if (d == 0) { if (i < nI - 1) Xs[(i + 1) * 8 + s] *= invd[i + 1]; }
-      else Xs[(i - d) * 8 + s] -= Cb[(size_t)(i - d) * P1 + d] * (Xs[i * 8 + s] * inv);
-    }
-    __syncthreads();
-  }
-  if (nI > 0) {
-    if (tid < 8) Xs[tid] *= invd[0];
-    __syncthreads();
-  }
-  for (int t = tid; t < nI * 8; t += nt) {
-    int a = t >> 3, cc = t & 7;
-    Sint[((size_t)jb * 8 + cc) * nI + a] = Xs[t];
-  }
-
-  // local Galerkin block over owned edges
-  const int lx = (bi == g.nb1 - 1), ly = (bj == g.nb2 - 1), lz = (bk == g.nb3 - 1);
-  const int ox = g.b1 * (g.b2 + ly) * (g.b3 + lz);
-  const int oy = (g.b1 + lx) * g.b2 * (g.b3 + lz);
-  const int oz = (g.b1 + lx) * (g.b2 + ly) * g.b3;
-  double acc[36];
-#pragma unroll
-  for (int q = 0; q < 36; ++q) acc[q] = 0.0;
-  for (int f = tid; f < ox + oy + oz; f += nt) {
-    int ax, x, y, z;
-    double kc;
-    if (f < ox) {
-      ax = 0; x = f % g.b1; int r = f / g.b1; y = r % (g.b2 + ly); z = r / (g.b2 + ly);
-      kc = bw.x(x, y, z) * g.ih1 * g.ih1;
-    } else if (f < ox + oy) {
-      ax = 1; int q = f - ox; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % g.b2; z = r / g.b2;
-      kc = bw.y(x, y, z) * g.ih2 * g.ih2;
-    } else {
-      ax = 2; int q = f - ox - oy; x = q % (g.b1 + lx); int r = q / (g.b1 + lx); y = r % (g.b2 + ly); z = r / (g.b2 + ly);
-      kc = bw.z(x, y, z) * g.ih3 * g.ih3;
-    }
-    int x1 = x + (ax == 0), y1 = y + (ax == 1), z1 = z + (ax == 2);
-    bool n0 = has0 && x == 0 && y == 0 && z == 0;
-    int a0 = interior_index(g, x, y, z), a1 = interior_index(g, x1, y1, z1);
-    double ds[8];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) {
-      double s0 = a0 >= 0 ? Xs[a0 * 8 + cc] : (n0 ? 0.0 : hat_corner(cc, x, y, z, g.b1, g.b2, g.b3));
-      double s1 = a1 >= 0 ? Xs[a1 * 8 + cc] : hat_corner(cc, x1, y1, z1, g.b1, g.b2, g.b3);
-      ds[cc] = s1 - s0;
-    }
-#pragma unroll
-    for (int c1i = 0; c1i < 8; ++c1i) {
-      double kd = kc * ds[c1i];
-#pragma unroll
-      for (int c2i = 0; c2i <= c1i; ++c2i) acc[c1i * (c1i + 1) / 2 + c2i] += kd * ds[c2i];
-    }
-  }
-  __syncthreads();           // Cb no longer needed: reuse for the reduction
-  double* red = Cb;
-#pragma unroll
-  for (int q = 0; q < 36; ++q) red[q * nt + tid] = acc[q];
-  __syncthreads();
-  if (tid < 36) {
-    double s = 0.0;
-    for (int t = 0; t < nt; ++t) s += red[tid * nt + t];
-    int c1i = (int)((sqrt(8.0 * tid + 1.0) - 1.0) * 0.5);
-    while (c1i * (c1i + 1) / 2 > tid) --c1i;
-    while ((c1i + 1) * (c1i + 2) / 2 <= tid) ++c1i;
-    int c2i = tid - c1i * (c1i + 1) / 2;
-    Kloc[(size_t)jb * 64 + c1i * 8 + c2i] = s;
-    Kloc[(size_t)jb * 64 + c2i * 8 + c1i] = s;
-  }
-}
-
-size_t basis_smem_bytes(const Geo& g) {
-  size_t cbsz = (size_t)g.nI * g.P1;
-  if (cbsz < (size_t)BASIS_THREADS * 36) cbsz = (size_t)BASIS_THREADS * 36;
-  size_t d = cbsz + (size_t)g.nI * 8 + g.nI + g.nwx + g.nwy + g.nwz;
-  size_t ntri = (size_t)g.p * (g.p + 1) / 2;
-  return d * 8 + ntri * 4 + 16;
-}
-
-// ----------------------------------------------------- block-diagonal solve
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// One CTA per block.  The factor columns (forward) and rows (backward) stream
-// through a RING-deep cp.async pipeline in shared memory; the right-hand sides
-// of NSC sources at a time live in shared memory.  out may alias rhs.
-template <int NSC>
-__global__ void __launch_bounds__(SOLVE_THREADS)
-k_block_solve(Geo g, const double* __restrict__ Lc, const double* __restrict__ Lr,
-              const double* rhs, double* out, int nrhs) {
-  constexpr int RING = SOLVE_RING;
-  extern __shared__ double sm[];
-  const int jb = blockIdx.x;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int nI = g.nI, p = g.p, P1 = g.P1, P1s = g.P1s;
-  if (nI == 0) return;
-  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
-  const int X0 = bi * g.b1, Y0 = bj * g.b2, Z0 = bk * g.b3;
-  double* Xs = sm;                        // [nI][NSC]
-  double* ring = Xs + (size_t)nI * NSC;   // [RING][P1s]
-  double* invd = ring + RING * P1s;       // [nI]
-  const double* Lcb = Lc + (size_t)jb * nI * P1s;
-  const double* Lrb = Lr + (size_t)jb * nI * P1s;
-
-  for (int s0 = 0; s0 < nrhs; s0 += NSC) {
-    const int ns = min(NSC, nrhs - s0);
-    for (int t = tid; t < nI * NSC; t += nt) {
-      int a = t / NSC, s = t - a * NSC;
-      int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
-      long long node = node_id(g, X0 + x, Y0 + y, Z0 + z);
-      Xs[t] = s < ns ? rhs[node * nrhs + s0 + s] : 0.0;
-    }
-    // ---- forward: columns of L
-    for (int q = 0; q < RING - 1; ++q) {
-      if (q < nI)
-        for (int r = tid; r < P1; r += nt) cp_async8(ring + (q % RING) * P1s + r, Lcb + (size_t)q * P1s + r);
-      cp_async_commit();
-    }
-    for (int i = 0; i < nI; ++i) {
-      cp_async_wait<RING - 2>();
-      __syncthreads();
-      {
-        int q = i + RING - 1;
-        if (q < nI)
-          for (int r = tid; r < P1; r += nt) cp_async8(ring + (q % RING) * P1s + r, Lcb + (size_t)q * P1s + r);
-        cp_async_commit();
-      }
-      const double* col = ring + (i % RING) * P1s;
-      const double inv = col[0];
-      if (tid == 0) invd[i] = inv;
-      const int rmax = min(p, nI - 1 - i);
-      for (int t = tid; t < (rmax + 1) * NSC; t += nt) {
-        int r = t / NSC, s = t - r * NSC;
-        if (r == 0) { if (i > 0) Xs[(i - 1) * NSC + s] *= invd[i - 1]; }
-        else Xs[(i + r) * NSC + s] -= col[r] * (Xs[i * NSC + s] * inv);
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int t = tid; t < NSC; t += nt) Xs[(nI - 1) * NSC + t] *= invd[nI - 1];
-    // ---- backward: rows of L, descending
-    for (int q = 0; q < RING - 1; ++q) {
-      int row = nI - 1 - q;
-      if (row >= 0)
-        for (int r = tid; r < P1; r += nt) cp_async8(ring + (q % RING) * P1s + r, Lrb + (size_t)row * P1s + r);
-      cp_async_commit();
-    }
-    for (int it = 0; it < nI; ++it) {
-      const int i = nI - 1 - it;
-      cp_async_wait<RING - 2>();
-      __syncthreads();
-      {
-        int q = it + RING - 1, row = nI - 1 - q;
-        if (row >= 0)
-          for (int r = tid; r < P1; r += nt) cp_async8(ring + (q % RING) * P1s + r, Lrb + (size_t)row * P1s + r);
-        cp_async_commit();
-      }
-      const double* rw = ring + (it % RING) * P1s;
-      const double inv = invd[i];
-      const int dmax = min(p, i);
-      for (int t = tid; t < (dmax + 1) * NSC; t += nt) {
-        int d = t / NSC, s = t - d * NSC;
-        if (d == 0) { if (i < nI - 1) Xs[(i + 1) * NSC + s] *= invd[i + 1]; }
-        else Xs[(i - d) * NSC + s] -= rw[d] * (Xs[i * NSC + s] * inv);
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int t = tid; t < NSC; t += nt) Xs[t] *= invd[0];
-    __syncthreads();
-    for (int t = tid; t < nI * NSC; t += nt) {
-      int a = t / NSC, s = t - a * NSC;
-      if (s >= ns) continue;
-      int x = 1 + a % g.ni1, y = 1 + (a / g.ni1) % g.ni2, z = 1 + a / (g.ni1 * g.ni2);
-      long long node = node_id(g, X0 + x, Y0 + y, Z0 + z);
-      out[node * nrhs + s0 + s] = Xs[t];
-    }
-    __syncthreads();
-  }
-}
-
-size_t solve_smem_bytes(const Geo& g) {
-  return ((size_t)g.nI * SOLVE_NSC + SOLVE_RING * g.P1s + g.nI) * 8 + 16;
-}
-
 // ------------------------------------------------------- fine-grid helpers
 
 // (A_wt X)(node) = sum_e wt_e/h^2 (X(node) - X(nb)) over the node's edges.
@@ -834,25 +485,6 @@ cudaError_t launch_edge_weights_planes(const Geo& g, const double* cv, double* w
   if (edge_tile_ok(g)) return launch_edge_tile(g, cv, w, k0, k1, st);
   const dim3 grid(1, lines, 3);
   k_edge_weights_lines<<<grid, dim3(EW_THREADS, EW_LINES), 0, st>>>(g, cv, w, k0, k1);
-  count_launches(1);
-  return cudaGetLastError();
-}
-cudaError_t launch_basis(const Geo& g, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
-                         int* flags, cudaStream_t st) {
-  size_t smem = basis_smem_bytes(g);
-  cudaError_t e = cudaFuncSetAttribute(k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_basis<<<g.nbl, BASIS_THREADS, smem, st>>>(g, w, Lc, Lr, Sint, Kloc, flags);
-  count_launches(1);
-  return cudaGetLastError();
-}
-cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr, const double* rhs, double* out,
-                               int nrhs, cudaStream_t st) {
-  if (g.nI == 0 || nrhs == 0) return cudaSuccess;
-  size_t smem = solve_smem_bytes(g);
-  cudaError_t e = cudaFuncSetAttribute(k_block_solve<SOLVE_NSC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_block_solve<SOLVE_NSC><<<g.nbl, SOLVE_THREADS, smem, st>>>(g, Lc, Lr, rhs, out, nrhs);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -137,8 +137,8 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
     g.skel = nullptr;
     g.nskel = 0;
   }
-  if (!tc_supported(g) && basis_smem_bytes(g) > 227 * 1024)
-    return fail(MSFV_UNSUPPORTED, "block interior band does not fit in shared memory (nI*(p+1) too large)");
+  if (!tc_supported(g) && !lg_supported(g))
+    return fail(MSFV_UNSUPPORTED, "block interior half bandwidth ni1*ni2 exceeds 512 (largest supported band)");
   if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
   if (g.coarse_nd == 2 && !mf_attach(g)) g.coarse_nd = g.kc >= 1000 ? 1 : 0;
@@ -169,15 +169,15 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_P1S] = g.P1s;
   v[MSFV_INFO_K] = g.kc;
   v[MSFV_INFO_AK_DOUBLES] = (int64_t)coarse_doubles(g);
-  v[MSFV_INFO_BASIS_SMEM] = (int64_t)basis_smem_bytes(g);
+  v[MSFV_INFO_BASIS_SMEM] = 0;
   v[MSFV_INFO_NT] = coarse_tile_rows(g);
   v[MSFV_INFO_PT] = g.PT;
   v[MSFV_INFO_TB] = g.TB;
   v[MSFV_INFO_PC] = g.pc;
   const bool tc = tc_supported(g);
-  v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)2 * g.nbl * g.nI * g.P1s;
+  v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)lg_factor_doubles(g);
   v[MSFV_INFO_SCRATCH_DOUBLES] = tc ? (int64_t)tc_scratch_doubles(g) : 0;
-  v[MSFV_INFO_TC] = tc ? 1 : 0;
+  v[MSFV_INFO_TC] = tc ? 1 : 2;
   v[MSFV_INFO_COARSE] = g.coarse_nd;
   for (int i = 0; i < n && i < MSFV_INFO_COUNT; ++i) info[i] = v[i];
   return MSFV_OK;
@@ -372,8 +372,7 @@ static int basis_build(const msfv_plan* plan, const double* w, double* factor, d
     if (rc) return rc;
     return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, bwd), "basis_build");
   }
-  double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
-  return cuda_check(launch_basis(g, w, factor, Lr, Sint, Kloc, flags, st), "basis_build");
+  return cuda_check(launch_basis_lg(g, w, factor, Sint, Kloc, flags, st), "basis_build");
 }
 
 int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
@@ -478,8 +477,7 @@ int msfv_interior_solve(const msfv_plan* plan, const double* factor, const doubl
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
   if (tc_supported(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
-  const double* Lr = factor + (size_t)g.nbl * g.nI * g.P1s;
-  return cuda_check(launch_block_solve(g, factor, Lr, rhs, out, nrhs, st), "interior_solve");
+  return cuda_check(launch_block_solve_lg(g, factor, rhs, out, nrhs, st), "interior_solve");
 }
 
 int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
@@ -516,7 +514,10 @@ int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, co
   CHECK_PLAN(plan);
   if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
   const Geo& g = plan->g;
-  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "compact interior solve needs the tensor-core band path");
+  if (!tc_supported(g))
+    return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk,
+                                            pts->d.nib, 1),
+                      "points_interior_solve");
   return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk, pts->d.nib, 1),
                     "points_interior_solve");
 }
@@ -580,7 +581,9 @@ int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const 
                              int32_t nrhs, void* stream) {
   CHECK_PLAN(plan);
   const Geo& g = plan->g;
-  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "compact block solve needs the tensor-core band path");
+  if (!tc_supported(g))
+    return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
+                      "block_solve_compact");
   return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
                     "block_solve_compact");
 }
@@ -614,7 +617,6 @@ int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sin
                    const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream) {
   CHECK_PLAN(plan);
   const Geo& g = plan->g;
-  if (xk_smem_bytes(g) > 200 * 1024) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
   return cuda_check(launch_xk_values(g, sigma, Sint, z, present, (const long long*)indptr, indices, vals,
                                      (cudaStream_t)stream), "xk_values");
 }

@@ -6,10 +6,6 @@
 
 namespace msfv {
 
-constexpr int BASIS_THREADS = 256;
-constexpr int SOLVE_THREADS = 128;
-constexpr int SOLVE_NSC = 8;
-constexpr int SOLVE_RING = 8;
 constexpr int RESTRICT_THREADS = 128;
 constexpr int COARSE_TB = 32;
 constexpr int TC_WARPS = 2;      // warps (= coarse blocks) per CTA in the DMMA kernels
@@ -29,16 +25,10 @@ int mf_reserved_sms();   // SMs the multifrontal kernels leave to the backward b
 void mf_release(Geo& g);
 long long launch_count();
 
-size_t basis_smem_bytes(const Geo& g);
-size_t solve_smem_bytes(const Geo& g);
 
 cudaError_t launch_sigma(long long Nm, const double* m, const double* mul, double* out, int* flags, cudaStream_t st);
 cudaError_t launch_mul(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 cudaError_t launch_edge_weights(const Geo& g, const double* cv, double* w, cudaStream_t st);
-cudaError_t launch_basis(const Geo& g, const double* w, double* Lc, double* Lr, double* Sint, double* Kloc,
-                         int* flags, cudaStream_t st);
-cudaError_t launch_block_solve(const Geo& g, const double* Lc, const double* Lr, const double* rhs, double* out,
-                               int nrhs, cudaStream_t st);
 cudaError_t launch_residual(const Geo& g, const double* src, double alpha, const double* wt, const double* X,
                             double beta, int nrhs, double* out, cudaStream_t st);
 cudaError_t launch_prolong(const Geo& g, const double* Sint, const double* Y, int nrhs, double* out, cudaStream_t st);
@@ -61,6 +51,16 @@ cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* S
 cudaError_t launch_edge_weights_planes(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st);
 cudaError_t launch_basis_bwd(const Geo& g, const double* LT, double* Sint, cudaStream_t st);
 cudaError_t launch_block_solve_tc(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
+                                  cudaStream_t st, const int* blist = nullptr, int nlist = 0, int compact = 0);
+
+// L2-resident DMMA band path for larger blocks (msfv_large.cu)
+constexpr int LG_MAX_PT = 64;    // half bandwidth p <= 512
+int lg_band(const Geo& g);
+bool lg_supported(const Geo& g);
+size_t lg_factor_doubles(const Geo& g);
+cudaError_t launch_basis_lg(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc, int* flags,
+                            cudaStream_t st);
+cudaError_t launch_block_solve_lg(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                   cudaStream_t st, const int* blist = nullptr, int nlist = 0, int compact = 0);
 
 // coarse (msfv_coarse.cu)

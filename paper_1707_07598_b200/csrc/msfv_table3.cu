@@ -140,6 +140,9 @@ __global__ void k_xk_rowcount(Geo g, const int* __restrict__ present, long long*
 
 // X_k values: CTA per present block; closure basis values and z staged in
 // shared memory; each thread owns cells, all 8 corner rows.
+// STAGED = false (closures larger than shared memory, e.g. 16^3-cell blocks):
+// the same arithmetic with the basis values and z read from global memory.
+template <bool STAGED>
 __global__ void __launch_bounds__(256) k_xk_values(Geo g, const double* __restrict__ sigma,
                                                    const double* __restrict__ Sint, const double* __restrict__ zf,
                                                    const int* __restrict__ present, const long long* __restrict__ indptr,
@@ -152,7 +155,18 @@ __global__ void __launch_bounds__(256) k_xk_values(Geo g, const double* __restri
   double* Sn = xsm;                 // [NN][8]
   double* Zn = Sn + (size_t)NN * 8;  // [NN]
   const double* Sb = Sint + (size_t)jb * 8 * g.nI;
-  for (int n = threadIdx.x; n < NN; n += blockDim.x) {
+  auto S_at = [&](int n, int cc) -> double {
+    if (STAGED) return Sn[n * 8 + cc];
+    const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
+    return s_value(g, Sb, cc, x, y, z, jb == 0 && n == 0);
+  };
+  auto Z_at = [&](int n) -> double {
+    if (STAGED) return Zn[n];
+    const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
+    const bool in = x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3;
+    return in ? zf[node_id(g, (long long)bi * g.b1 + x, (long long)bj * g.b2 + y, (long long)bk * g.b3 + z)] : 0.0;
+  };
+  if (STAGED) for (int n = threadIdx.x; n < NN; n += blockDim.x) {
     const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
     const bool in = x > 0 && x < g.b1 && y > 0 && y < g.b2 && z > 0 && z < g.b3;
     const bool node0 = jb == 0 && n == 0;
@@ -186,10 +200,10 @@ __global__ void __launch_bounds__(256) k_xk_values(Geo g, const double* __restri
           else if (ax == 1) { ox += u; oz += v; }
           else { ox += u; oy += v; }
           const int na = ox + B1 * (oy + B2 * oz), nb = na + step;
-          const double ae = (Zn[nb] - Zn[na]) * ih;
+          const double ae = (Z_at(nb) - Z_at(na)) * ih;
           if (ae == 0.0) continue;
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) acc[cc] += ((Sn[nb * 8 + cc] - Sn[na * 8 + cc]) * ih * ae) * sc;
+          for (int cc = 0; cc < 8; ++cc) acc[cc] += ((S_at(nb, cc) - S_at(na, cc)) * ih * ae) * sc;
         }
     }
 #pragma unroll
@@ -249,9 +263,13 @@ size_t xk_smem_bytes(const Geo& g) { return (size_t)(g.b1 + 1) * (g.b2 + 1) * (g
 cudaError_t launch_xk_values(const Geo& g, const double* sigma, const double* Sint, const double* zf, const int* present,
                              const long long* indptr, int* indices, double* vals, cudaStream_t st) {
   const size_t smem = xk_smem_bytes(g);
-  cudaError_t e = cudaFuncSetAttribute(k_xk_values, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_xk_values<<<g.nbl, 256, smem, st>>>(g, sigma, Sint, zf, present, indptr, indices, vals);
+  if (smem > 200 * 1024) {
+    k_xk_values<false><<<g.nbl, 256, 0, st>>>(g, sigma, Sint, zf, present, indptr, indices, vals);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(k_xk_values<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_xk_values<true><<<g.nbl, 256, smem, st>>>(g, sigma, Sint, zf, present, indptr, indices, vals);
+  }
   count_launches(1);
   return cudaGetLastError();
 }

@@ -23,35 +23,14 @@
 #include <cstdlib>
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
+#include "msfv_dmma.cuh"
 
 namespace msfv {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-struct F2 {
-  double x, y;
-};
-
-__device__ __forceinline__ void mma884(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-// D += X Y^T for C-layout tiles X, Y (k = 8, see ld_t)
-__device__ __forceinline__ void mma(F2& c, const F2& a, const F2& b) {
-  mma884(c.x, c.y, a.x, b.x);
-  mma884(c.x, c.y, a.y, b.y);
-}
-__device__ __forceinline__ F2 neg(const F2& f) { return {-f.x, -f.y}; }
-
-__device__ __forceinline__ F2 ld2(const double* p) {
-  double2 v = *reinterpret_cast<const double2*>(p);
-  return {v.x, v.y};
-}
-__device__ __forceinline__ void st2(double* p, const F2& f) {
-  *reinterpret_cast<double2*>(p) = make_double2(f.x, f.y);
-}
+using namespace dmma;
 
 // Interior coordinates, packed x | y << 10 | z << 20 (one table per CTA).
 __device__ __forceinline__ void fill_coords(const Geo& g, int* crd) {
@@ -69,10 +48,6 @@ __device__ __forceinline__ void fill_coords(const Geo& g, int* crd) {
 // right-hand sides are carried transposed, so no register shuffles are needed.
 // Tiles are stored row-major (the C layout at lane*2); ld_t loads the C layout
 // of a stored tile's transpose.
-__device__ __forceinline__ F2 ld_t(const double* p, int lane) {
-  const int m = lane >> 2, q = lane & 3;
-  return {__ldcg(p + 16 * q + m), __ldcg(p + 16 * q + 8 + m)};
-}
 
 // Per-block stencil table in shared memory: one row of AROW doubles per
 // interior node, padding rows (up to 8*NTI) are identity:

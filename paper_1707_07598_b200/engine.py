@@ -121,7 +121,9 @@ class Engine:
         self.NT, self.PT, self.TB = info[_lib.INFO_NT], info[_lib.INFO_PT], info[_lib.INFO_TB]
         self.factor_doubles = info[_lib.INFO_FACTOR_DOUBLES]
         self.scratch_doubles = info[_lib.INFO_SCRATCH_DOUBLES]
-        self.tensor_core = bool(info[_lib.INFO_TC])
+        # 1: register-window DMMA band (split build); 2: L2-resident DMMA band (larger blocks)
+        self.local_solver = int(info[_lib.INFO_TC])
+        self.tensor_core = self.local_solver == 1
         self.coarse_multifrontal = info[_lib.INFO_COARSE] == 2
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._csc = None

@@ -114,10 +114,12 @@ class ReducedState:
 
     @property
     def A_k(self):
-        """Dense projected operator (forward.py:102), re-assembled on demand."""
+        """Dense projected operator (forward.py:102), re-assembled on demand.
+        Like the reference it is the unshifted S^T A S: the diagonal shift of
+        the fallback (forward.py:122-129) lives only in the factor."""
         if self._A_k is None:
             eng = self.basis.engine
-            self._A_k = _host(eng.coarse_dense(self.basis.Kloc, self.shift))
+            self._A_k = _host(eng.coarse_dense(self.basis.Kloc, 0.0))
         return self._A_k
 
     def check(self, host_flags=None):

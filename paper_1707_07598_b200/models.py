@@ -83,3 +83,32 @@ def config_problem(cfg_id, seed=0):
     part = create_partition(mesh, cfg["b"], cfg["b"], cfg["b"])
     survey = build_survey(mesh, cfg["n_src"], cfg["n_rec"])
     return mesh, part, survey, config_model(mesh, cfg, seed)
+
+
+def top_random_survey(mesh, n_rec, n_src, seed):
+    """Seeded receivers and x-dipoles at random top-plane nodes (the layout of
+    models.py:54-83 with random positions instead of a regular grid)."""
+    rng = np.random.default_rng(seed)
+    n = mesh.n_nodes - 1
+    I, J = np.meshgrid(np.arange(mesh.n1 + 1), np.arange(mesh.n2 + 1), indexing="ij")
+    top = np.sort(mesh.node_index(I.ravel(), J.ravel(), mesh.n3)) - 1
+    rec = np.sort(rng.choice(top, size=n_rec, replace=False))
+    P = sp.csc_matrix((np.ones(n_rec), (rec, np.arange(n_rec))), shape=(n, n_rec))
+    i = rng.choice(mesh.n1, size=n_src, replace=n_src > mesh.n1)
+    j = rng.integers(0, mesh.n2 + 1, size=n_src)
+    a = mesh.node_index(i, j, mesh.n3) - 1
+    Q = sp.csc_matrix((np.tile([1.0, -1.0], n_src), np.column_stack([a, a + 1]).ravel(),
+                       np.arange(0, 2 * n_src + 1, 2)), shape=(n, n_src))
+    return Survey(P=P, Q=Q)
+
+
+def table3_problem(seed=0):
+    """The paper's Table-3 geometry: 64 x 64 x 32 cells,
+    16^3-cell coarse blocks, 72 sources and 3698 receivers (here on the top
+    plane), m a smoothed Gaussian field (sigma 4 cells, std 1) from the seed.
+    Returns (mesh, partition, survey, m)."""
+    from .mesh import create_mesh, create_partition
+    mesh = create_mesh(64, 64, 32, 1 / 64, 1 / 64, 1 / 64)
+    part = create_partition(mesh, 16, 16, 16)
+    survey = top_random_survey(mesh, 3698, 72, seed + 1)
+    return mesh, part, survey, gaussian_field(mesh, 4.0, 1.0, seed)

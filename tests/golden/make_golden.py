@@ -95,6 +95,7 @@ CASES = {
     "c64_b16_t3": ((64, 64, 32), (1 / 64, 1 / 64, 1 / 64), (16, 16, 16), ("smooth", 4.0, 1.0), ("toprandom", 64, 6),
                    "xonly"),
 }
+PERTURB = {"c64_b16_t3": 1.0}
 # fixtures whose large arrays are stored as projections / digests
 COMPACT = {"c32_b16x4", "c32_b16", "c64_b16_t3"}
 
@@ -117,8 +118,12 @@ def make_case(name, spec, seed=20240615):
     else:
         survey = build_survey(mesh, n_src=skind[1], n_rec=skind[2])
     builder = BasisBuilder(part, BasisSpec(families=("lagrange",)))
-    # observed data: reduced forward at a perturbed model
-    m_true = m + 0.2 * rng.normal(size=mesh.n_cells)
+    # observed data: reduced forward at a perturbed model.  The Table-3 case
+    # uses a larger perturbation: with 0.2 its residual is 1.6% of D, which
+    # amplifies the forward rounding into the gradient 64x (two valid
+    # reference evaluation orders, dense vs SuperLU block factors, then differ
+    # by 8e-11 on g)
+    m_true = m + PERTURB.get(name, 0.2) * rng.normal(size=mesh.n_cells)
     op_t = assemble_operator(mesh, m_true)
     d_obs, _ = forward_reduced(op_t, survey, builder.assemble(op_t))
 

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import GOLDEN_CASES, load_golden, rel
+from conftest import GOLDEN_CASES, LARGE_CASES, basis_errors, load_golden, rel, table3_errors
 
 pytestmark = pytest.mark.gpu
 
@@ -30,21 +30,18 @@ def build_gpu(g):
     return gp, mesh, part, survey, builder
 
 
-@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("name", GOLDEN_CASES + LARGE_CASES)
 def test_forward_gradient_matches_reference(name):
+    """Every golden case, including blocks beyond the register-tile band
+    (16x16x4, 16^3 with n_I = 3375 > 2000 where the reference uses SuperLU,
+    and the paper's Table-3 geometry 64x64x32 / 16^3)."""
     g = load_golden(name)
     gp, mesh, part, survey, builder = build_gpu(g)
     op = gp.assemble_operator(mesh, g["m"])
     basis = builder.assemble(op)
     D, state = gp.forward_reduced(op, survey, basis)
-    errs = {}
-    errs["w"] = rel(op.edge_weights, g["w"])
-    S = basis.S
-    assert np.array_equal(S.indptr, g["S_indptr"]), "S indptr differs"
-    assert np.array_equal(S.indices, g["S_indices"]), "S indices differ"
-    errs["S"] = rel(S.data, g["S_data"])
+    errs = basis_errors(g, basis.S, state.T, op.edge_weights)
     errs["T"] = rel(state.T, g["T"])
-    errs["US"] = rel(S @ state.T, g["US"])
     errs["D"] = rel(D, g["D"])
     phi, resid = gp.misfit_ssd(D, g["d_obs"])
     errs["phi"] = abs(phi - float(g["phi"])) / abs(float(g["phi"]))
@@ -78,23 +75,20 @@ def test_edge_weights_last_ulp():
     assert np.max(np.abs(w - g["w"]) / np.abs(g["w"])) <= 1e-15
 
 
-@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("name", [n for n in GOLDEN_CASES + LARGE_CASES
+                                  if n not in ("c16_b8", "c32_b8", "c32_b8_int", "c32_b16")])
 def test_table3_operators_match_reference(name):
-    """apply_Yk / apply_Xk (basis.py:684-800): CSR pattern bit-exact, values <= 1e-10."""
+    """apply_Yk / apply_Xk (basis.py:684-800): CSR pattern bit-exact, values <= 1e-10
+    (full arrays, or digests + projections for the large fixtures)."""
     g = load_golden(name)
-    if "v" not in g:
-        pytest.skip("fixture without Table-3 vectors (see test_table3_operators_match_oracle)")
     gp, mesh, part, survey, builder = build_gpu(g)
     op = gp.assemble_operator(mesh, g["m"])
     basis = builder.assemble(op)
-    Y = gp.apply_Yk(basis, g["v"], g["m"])
-    assert np.array_equal(Y.indptr, g["Y_indptr"]), "Y_k indptr differs"
-    assert np.array_equal(Y.indices, g["Y_indices"]), "Y_k indices differ"
-    assert rel(Y.data, g["Y_data"]) <= TOL
+    has_y = "Y_data" in g or "Y_digest" in g
+    Y = gp.apply_Yk(basis, g["v"], g["m"]) if has_y else None
     X = gp.apply_Xk(basis, g["wv"], g["m"])
-    assert np.array_equal(X.indptr, g["X_indptr"]), "X_k indptr differs"
-    assert np.array_equal(X.indices, g["X_indices"]), "X_k indices differ"
-    assert rel(X.data, g["X_data"]) <= TOL
+    errs = table3_errors(g, Y, X)
+    assert max(errs.values()) <= TOL, errs
     # stale-model contract (basis.py:333-337)
     with pytest.raises(gp.StaleBasisError):
         gp.apply_Yk(basis, g["v"], g["m"] + 1.0)
