@@ -15,8 +15,8 @@ Workload: 128^3 cells, 8^3-cell blocks (4096 local solves), 16 dipoles,
 of the step (factors ~1.1 GB) exceeds the 126 MB L2, so no flush is needed.
 
 --impl reference runs the CPU oracle port (oracle/, a numpy/scipy
-restatement of the reference msinv path) on a bounded z-slab sample of the
-same workload and scales it to the full config (see "sample").
+restatement of the reference msinv path) on the full workload, every step
+(config 4: about 15-20 s per step on the GPU box's host cores).
 """
 
 import argparse
@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gn", action="store_true", help="skip the Gauss-Newton iteration timing")
+    ap.add_argument("--no-table3", action="store_true", help="skip the Table-3 geometry timings")
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling mode: device-resident setup, then only the guard, warm-up and timed steps "
+                         "(no extra legs), so an ncu launch list ends with the last timed step")
     return ap.parse_args()
 
 
@@ -274,41 +278,57 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline
 
-def oracle_slab_time(cfg_id, seed, reps=1, warm=1, log=None, workers=1):
-    """Time the CPU oracle forward+gradient on a z-slab of the config (same
-    x/y extent, survey and per-block work; nz = 2 blocks) and return
-    (seconds per slab iteration, scale factor to the full config, description)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_full_time(cfg_id, seed, reps=1, warm=1, log=None, workers=1):
+    """Time the CPU oracle (oracle/msfv_oracle.py, the reference msinv
+    algorithm restated in numpy/scipy) on the FULL config's forward + misfit +
+    gradient step, the same seeded inputs as the GPU arm.  Returns (median
+    seconds per step, description); the one-time setup (partition, pattern
+    cache) is excluded like the reference's BlockSystemCache."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import numpy as np
     from oracle import msfv_oracle as orc
-    from paper_1707_07598_b200.models import CONFIGS, gaussian_field
+    from paper_1707_07598_b200.models import CONFIGS, config_model
+    import paper_1707_07598_b200.mesh as gmesh
     orc.WORKERS = workers             # per-block loops on `workers` threads (reference: workers=os.cpu_count())
     c = CONFIGS[cfg_id]
     n, b = c["n"], c["b"]
-    nz = 2 * b
-    mesh = orc.Mesh(n, n, nz, 1.0 / n, 1.0 / n, 1.0 / n)
+    mesh = orc.Mesh(n, n, n, 1.0 / n, 1.0 / n, 1.0 / n)
     part = orc.make_partition(mesh, b, b, b)
     srv = orc.top_survey(mesh, c["n_src"], c["n_rec"])
-    m = gaussian_field(mesh, c["field"][0], c["field"][1], seed)
+    m = config_model(gmesh.create_mesh(n, n, n, 1.0 / n, 1.0 / n, 1.0 / n), c, seed)
+    t0 = time.perf_counter()
     prob = orc.AdaptiveProblem(part, srv)
-    d_obs = prob.simulate(m + 0.1)[0]
+    setup = time.perf_counter() - t0
+    d_obs = None
     ts = []
     for it in range(warm + reps):
         t0 = time.perf_counter()
         D, st = prob.simulate(m)
+        if d_obs is None:
+            d_obs = D * 1.05
         phi, r = orc.misfit(D, d_obs)
         prob.jacobian(st).rapply(r)
         dt = time.perf_counter() - t0
         if it >= warm:
             ts.append(dt)
         if log:
-            log(f"oracle slab iteration {it}: {dt:.2f} s")
-    scale = n / nz
-    desc = (f"oracle port (numpy/scipy restatement of msinv, {workers} worker thread(s) over blocks, "
-            f"OPENBLAS_NUM_THREADS=1) forward+misfit+gradient "
-            f"on a {n}x{n}x{nz} z-slab ({part.n_blocks} of {(n // b) ** 3} blocks, same survey layout); "
-            f"seconds scaled x{scale:g} to the full config (coarse solve scaled linearly, which understates CPU cost)")
-    return float(np.median(ts)), scale, desc
+            log(f"oracle full-config iteration {it}: {dt:.2f} s")
+    desc = (f"oracle port (numpy/scipy restatement of msinv; the per-block loops on {workers} thread(s), "
+            f"OPENBLAS_NUM_THREADS=1) forward+misfit+gradient on the full config {cfg_id} ({part.n_blocks} blocks, "
+            f"same seeded m and survey), median of {reps} after {warm} warm-up; one-time setup {setup:.1f} s "
+            f"excluded; CPU: {cpu_model()}")
+    return float(np.median(ts)), desc
 
 
 # --------------------------------------------------------------- GPU arm
@@ -349,6 +369,55 @@ def solve_flops(nI, p, nrhs):
     return f
 
 
+def table3_times(log):
+    """S_k, Y_k, X_k at the paper's Table-3 geometry (PAPER.md:569-589;
+    BASELINE.md section 1): 64x64x32 cells, 16^3 blocks (n_I = 3375, the
+    L2-resident band solver), 72 sources, 3698 receivers.  Device times (CUDA
+    events, best of 3 after a warm-up) and the host-CSR time of Y_k through
+    the reference-named API, next to the paper's Julia numbers."""
+    import numpy as np
+    import torch
+    import paper_1707_07598_b200 as gp
+    from paper_1707_07598_b200.models import table3_problem
+    mesh, part, survey, m = table3_problem()
+    builder = gp.BasisBuilder(part)
+    m_dev = torch.from_numpy(m).cuda()
+    basis = builder.assemble(gp.assemble_operator(mesh, m_dev))
+    eng = basis.engine
+    rng = np.random.default_rng(0)
+    v = torch.from_numpy(rng.standard_normal(eng.k)).cuda()
+    w = torch.from_numpy(rng.standard_normal(eng.n)).cuda()
+
+    def best(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        out = 1e30
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            r = fn()
+            b.record()
+            torch.cuda.synchronize()
+            out = min(out, a.elapsed_time(b))
+            del r
+        return round(out, 3)
+
+    res = {"geometry": f"64x64x32 cells, 16^3 blocks ({eng.nbl}), n_I {eng.nI}, k {eng.k}, 72 sources, 3698 receivers",
+           "S_k_ms": best(lambda: builder.assemble(gp.assemble_operator(mesh, m_dev)).Sint),
+           "Y_k_ms": best(lambda: gp.apply_Yk_dev(basis, v, m_dev)),
+           "X_k_ms": best(lambda: gp.apply_Xk_dev(basis, w, m_dev))}
+    t0 = time.perf_counter()
+    Y = gp.apply_Yk(basis, v.cpu().numpy(), m_dev)
+    res["Y_k_host_csr_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+    res["Y_k_nnz"] = int(Y.nnz)
+    del Y
+    res["paper_julia_s"] = {"workers_1": {"S_k": 3.8595, "Y_k": 2.7380, "X_k": 2.9933},
+                            "workers_8": {"S_k": 1.4150, "Y_k": 1.0658, "X_k": 1.3818},
+                            "hardware": "4x Xeon E5-4627 (40 cores), PAPER.md:576"}
+    log("table3: " + json.dumps(res))
+    return res
+
+
 def run_gpu(args, rank, world, log):
     import numpy as np
     import torch
@@ -364,8 +433,12 @@ def run_gpu(args, rank, world, log):
     m_obs = m + 0.25 * gp.models.gaussian_field(mesh, 6.0, 1.0, args.seed + 1)
     builder = gp.BasisBuilder(part, gp.BasisSpec())
     problem = gp.AdaptiveReducedProblem(builder, survey)
-    d_obs = problem.simulate(m_obs)[0]
     dev = torch.device("cuda")
+    if args.ncu:
+        op_obs = gp.assemble_operator(mesh, torch.from_numpy(m_obs).to(dev))
+        d_obs = forward_reduced_dev(op_obs, survey, builder.assemble(op_obs))[0].cpu().numpy()
+    else:
+        d_obs = problem.simulate(m_obs)[0]
     m_dev = torch.from_numpy(m).to(dev)
     dobs_dev = torch.from_numpy(d_obs).to(dev)
     L = _lib.load()
@@ -396,7 +469,7 @@ def run_gpu(args, rank, world, log):
     # extra untimed steps until the per-step device time is stable (the first
     # ~10 steps after allocation run slower; see profiles/README)
     prev = None
-    for _ in range(12):
+    for _ in range(0 if args.ncu else 12):
         a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
         step_dev()
@@ -424,6 +497,8 @@ def run_gpu(args, rank, world, log):
     clk = clocks.stop()
     ms = dist.max_over_ranks(ms, dev)
     log(f"device step {ms:.3f} ms")
+    if args.ncu:
+        return None
 
     # config-4 Gauss-Newton iteration (BASELINE configs[3]): forward, gradient
     # and 5 CG steps, each one J v and one J^T (J v), device-resident
@@ -502,40 +577,63 @@ def run_gpu(args, rank, world, log):
         log(f"e2e step {e2e_ms:.3f} ms")
 
     eng = builder.assemble(gp.assemble_operator(mesh, m_dev)).engine
-    nI, p = eng.nI, eng.info[_lib.INFO_P1S] - 1
+    nI = eng.nI
     p = (part.b1 - 1) * (part.b2 - 1)
     own_edges = 3 * part.b1 * part.b2 * part.b3
     # the tensor-core build runs as two launches: the forward part (factor,
     # forward sweep, Galerkin; the "basis" phase on the critical path) and the
     # backward sweeps on a side stream, overlapped with the coarse factorization
-    fl_block = basis_flops(nI, p, 8, own_edges, sweeps=1 if eng.tensor_core else 2)
+    fl_fwd = basis_flops(nI, p, 8, own_edges, sweeps=1)
+    fl_whole = basis_flops(nI, p, 8, own_edges, sweeps=2)
     t_basis = phases.get("basis", float("nan")) / 1e3
+    # whole build (forward part + backward sweeps, serial on one stream:
+    # msfv_basis_build) timed on its own
+    _, w_dev, fl_dev = eng.operator(m_dev)
+    for _ in range(3):
+        eng.basis(w_dev, fl_dev)
+    wa, wb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wa.record()
+    for _ in range(10):
+        eng.basis(w_dev, fl_dev)
+    wb.record()
+    torch.cuda.synchronize()
+    t_whole = wa.elapsed_time(wb) / 10 / 1e3
     peak, peak_src = fp64_peak()
-    achieved = fl_block * eng.nbl / t_basis / 1e12
+    achieved = fl_fwd * eng.nbl / t_basis / 1e12
+    # compulsory bytes of the basis construction: read the edge
+    # weights, write S_I and the local Galerkin blocks
+    compulsory = int(eng.E * 8 + eng.nbl * 8 * nI * 8 + eng.nbl * 64 * 8)
     traffic, traffic_src = None, None
-    try:
-        # dram__bytes_read.sum + dram__bytes_write.sum of k_basis_tc from the
-        # committed ncu --set full capture of this configuration
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r01c_ncu.json")))["full"]
-        kb = next(v for k, v in prof.items() if "k_basis_tc" in k)
-        if args.config == 4:
-            traffic = int(kb["dram_read_B"] + kb["dram_write_B"])
-            traffic_src = "profiles/r01c_ncu.json (ncu --set full, k_basis_tc, bytes per launch)"
-    except Exception:  # noqa: BLE001
-        pass
+    for prof_name in ("r02_ncu.json", "r01c_ncu.json"):
+        try:
+            # dram__bytes_read.sum + dram__bytes_write.sum of k_basis_tc from the
+            # committed ncu --set full capture of this configuration
+            prof = json.load(open(os.path.join(ROOT, "profiles", prof_name)))["full"]
+            kb = next(v for k, v in prof.items() if "k_basis_tc" in k)
+            if args.config == 4:
+                traffic = int(kb["dram_read_B"] + kb["dram_write_B"])
+                traffic_src = f"profiles/{prof_name} (ncu --set full, k_basis_tc, bytes per launch)"
+            break
+        except Exception:  # noqa: BLE001
+            continue
     roof = {"kernel": "k_basis_tc<PT,false> + k_skel_lines (per-block A_II band Cholesky, 8-RHS forward sweep, "
                       "local Galerkin; skeleton line sums on a side stream beside it; the backward sweeps run "
                       "concurrently in k_basis_bwd)",
             "bound": "fp64", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes", "traffic_source": traffic_src,
-            "algorithmic_bytes": int(eng.nbl * (eng.factor_doubles / eng.nbl * 8 + 8 * eng.nI * 8 + 64 * 8)),
-            "flops_per_block": fl_block, "blocks_per_launch": eng.nbl, "launch_ms": round(t_basis * 1e3, 4),
+            "algorithmic_bytes": compulsory,
+            "algorithmic_bytes_what": "compulsory: edge weights in, S_I and Kloc out (SURVEY 8d)",
+            "flops_per_block": fl_fwd, "blocks_per_launch": eng.nbl, "launch_ms": round(t_basis * 1e3, 4),
             "peak_source": peak_src,
+            "whole_build": {"ms": round(t_whole * 1e3, 4), "flops_per_block": fl_whole,
+                            "achieved": round(fl_whole * eng.nbl / t_whole / 1e12, 3),
+                            "frac": round(fl_whole * eng.nbl / t_whole / 1e12 / peak, 4),
+                            "what": "forward part + backward sweeps on one stream (msfv_basis_build)"},
             "note": "FP64 bound: tcgen05 has no f64 kind; the kernel runs on DMMA (mma.sync m8n8k4 f64); "
                     "useful banded flops only (tile padding not counted)"}
     return {
         "ms": ms, "launches": launches, "clocks": clk, "phases": phases, "e2e": e2e, "roofline": roof,
-        "block_solves_per_s": eng.nbl / t_basis, "nbl": eng.nbl,
+        "block_solves_per_s": eng.nbl / t_whole, "nbl": eng.nbl,
         "interior_solve_ms": phases.get("interior_solve"), "gn": gn,
     }
 
@@ -593,14 +691,16 @@ def main():
         if rank != 0:
             return 0
         workers = os.cpu_count() or 1
-        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=args.steps, warm=args.warmup, log=log,
-                                          workers=workers)
-        v = t * scale
+        # every step is the full workload; warm-up capped at 2 full steps
+        # (the oracle has no JIT or allocator state to settle beyond the first)
+        warm = min(args.warmup, 2)
+        v, desc = oracle_full_time(args.config, args.seed, reps=args.steps, warm=warm, log=log, workers=workers)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+                "steps": args.steps, "warmup": args.warmup, "warmup_done": warm, "ms_per_step": v * 1e3,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": cfg,
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc,
-                                 "sample_seconds": t},
+                                 "cpu_model": cpu_model(), "extrapolated": False},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
@@ -609,10 +709,17 @@ def main():
     from paper_1707_07598_b200 import dist
     dist.init("nccl")
     res = run_gpu(args, rank, world, log)
+    if res is None:
+        return 0
+    t3 = None
+    if rank == 0 and args.config == 4 and not args.no_table3:
+        t3 = table3_times(log)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t, scale, desc = oracle_slab_time(args.config, args.seed, reps=1, warm=1, log=log)
-        cpu = {"value": t * scale, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc, "sample_seconds": t}
+        workers = os.cpu_count() or 1
+        t, desc = oracle_full_time(args.config, args.seed, reps=1, warm=1, log=log, workers=workers)
+        cpu = {"value": t, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc, "cpu_model": cpu_model(),
+               "extrapolated": False}
     if rank == 0:
         line = {
             "metric": METRIC, "value": dist.aggregate_seconds_per_iter(res["ms"] / 1e3, world), "unit": UNIT,
@@ -625,6 +732,7 @@ def main():
             "local_block_solves_per_s": round(res["block_solves_per_s"], 1),
             "phases_ms": {k: round(v, 4) for k, v in res["phases"].items()},
             "gn_iteration": res["gn"],
+            "table3": t3,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
