@@ -87,6 +87,11 @@ MSFV_API int64_t msfv_launch_count(void);
 
 /* TensorMesh + CoarsePartition (mesh.py:12-182).  blocks must divide cells. */
 MSFV_API int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out);
+/* Geometry-only plan (no coarse partition) for the fine-mesh entry points
+ * (msfv_operator, msfv_edge_average, msfv_fine_apply, msfv_full_gradient,
+ * msfv_reg_*, survey scatter/receive without basis); every basis or coarse
+ * entry point returns MSFV_UNSUPPORTED on it.  At most 1023 cells per axis. */
+MSFV_API int msfv_plan_create_mesh(const int32_t cells[3], const double h[3], msfv_plan** out);
 MSFV_API void msfv_plan_destroy(msfv_plan* plan);
 MSFV_API int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n);
 
@@ -239,6 +244,26 @@ MSFV_API int msfv_xk_present(const msfv_plan* plan, const double* z, int32_t* pr
 MSFV_API int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* counts, void* stream);
 MSFV_API int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
                    const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream);
+
+/* ---- Fine mesh (forward_full, FullSensitivity, block_cg) ----
+ * msfv_fine_apply: out = A(w) X on every pinned node (the operator product
+ *   op.A @ X of forward.py:84-90 and solvers.py:105; operators.py:138-141),
+ *   X and out full node fields [node][nrhs] (row 0, the pinned node, is 0).
+ * msfv_full_gradient: g = -sigma C^T sum_s (G U_s) o (G V_s) -- the adjoint
+ *   product sum_j G_j^T v_j of FullSensitivity.rapply (forward.py:170-175)
+ *   with G_j = d(A u_j)/dm = G^T diag(G u_j) C diag(sigma)
+ *   (grad_A_u, operators.py:168-194); xi: nedges doubles of scratch. */
+MSFV_API int msfv_fine_apply(const msfv_plan* plan, const double* w, const double* X, int32_t nrhs, double* out,
+                             void* stream);
+MSFV_API int msfv_full_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* V,
+                                int32_t nrhs, double* xi, double* g, void* stream);
+/* ---- Gauss-Newton objective (Objective, inversion.py:32-88) ----
+ * L = cell_gradient(mesh): cell-centre differences across interior faces, +-1/h.
+ * msfv_reg_apply: out = alpha L^T L v (Objective.hess_apply, inversion.py:87-88);
+ * msfv_reg_faces: out_c = sum of (L d)_f^2 over the faces (c, c + e_axis), so
+ *   ||L d||^2 = sum_c out_c (Objective.value_grad, inversion.py:82-85). */
+MSFV_API int msfv_reg_apply(const msfv_plan* plan, double alpha, const double* v, double* out, void* stream);
+MSFV_API int msfv_reg_faces(const msfv_plan* plan, const double* d, double* out, void* stream);
 
 /* ==== 2D path (BASELINE.json configs 1-2) =================================
  * The reference package is 3D only; these entry points run the

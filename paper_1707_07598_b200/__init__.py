@@ -15,10 +15,11 @@ from .basis import (
     coarse_hat_values,
 )
 from .forward import Survey, ReducedState, forward_reduced, AdaptiveSensitivity, sensitivity_adaptive
-from .inversion import (
-    misfit_ssd, Objective, GNConfig, projected_gauss_newton, AdaptiveReducedProblem,
-    cell_gradient, project_bounds, add_noise, tikhonov_reg, InversionTrace,
+from .inversion import misfit_ssd, AdaptiveReducedProblem
+from .fine import (
+    forward_full, FullState, FullSensitivity, sensitivity_full, FullProblem, block_cg, IterativeResult,
 )
+from .gn import gauss_newton_dev, GNSettings, DeviceObjective, DeviceTrace
 from .table3 import apply_Yk, apply_Xk, apply_Yk_dev, apply_Xk_dev
 from .planar import (
     Mesh2D, Partition2D, create_mesh_2d, create_partition_2d, AdaptiveReducedProblem2D,

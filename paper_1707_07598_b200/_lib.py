@@ -74,6 +74,11 @@ SIGNATURES = {
     "msfv_block_gradient_slab": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I32, _P, _P]),
     "msfv_jv_coarse_rhs": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "msfv_coarse_dense": (ctypes.c_int, [_P, _P, _D, _P, _P]),
+    "msfv_plan_create_mesh": (ctypes.c_int, [_P, _P, ctypes.POINTER(_P)]),
+    "msfv_fine_apply": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
+    "msfv_full_gradient": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P]),
+    "msfv_reg_apply": (ctypes.c_int, [_P, _D, _P, _P, _P]),
+    "msfv_reg_faces": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_yk_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "msfv_block_solve_compact": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_yk_rowcount": (ctypes.c_int, [_P, _P, _P, _P]),

@@ -530,6 +530,11 @@ cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double
   count_launches(1);
   return cudaGetLastError();
 }
+cudaError_t launch_cell_gather(const Geo& g, const double* sigma, const double* xi, double* gout, cudaStream_t st) {
+  k_cell_gather<<<nblk(g.Nm, 256), 256, 0, st>>>(g, sigma, xi, gout);
+  count_launches(1);
+  return cudaGetLastError();
+}
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
                              double* vals, cudaStream_t st) {
   if (nnz == 0) return cudaSuccess;

@@ -17,6 +17,7 @@ using namespace msfv;
 struct msfv_plan {
   Geo g;
   SkelEdge* skel_dev = nullptr;   // uploaded on first basis build (plan creation needs no GPU)
+  bool mesh_only = false;         // msfv_plan_create_mesh: no coarse partition (fine-mesh entry points only)
 };
 
 // Skeleton-only owned edges of a block in the "last along every axis" case;
@@ -77,6 +78,11 @@ static int cuda_check(cudaError_t e, const char* what) {
 }
 #define CHECK_PLAN(p) \
   if (!(p)) return fail(MSFV_SHAPE, "null plan")
+#define CHECK_PARTITION(p)                                                                               \
+  do {                                                                                                   \
+    CHECK_PLAN(p);                                                                                       \
+    if ((p)->mesh_only) return fail(MSFV_UNSUPPORTED, "geometry-only plan (msfv_plan_create_mesh) has no coarse partition"); \
+  } while (0)
 
 extern "C" {
 
@@ -84,7 +90,8 @@ int msfv_abi_version(void) { return MSFV_ABI_VERSION; }
 const char* msfv_last_error(void) { return g_err.c_str(); }
 int64_t msfv_launch_count(void) { return launch_count(); }
 
-int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out) {
+static int plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], bool mesh_only,
+                       msfv_plan** out) {
   if (!cells || !h || !blocks || !out) return fail(MSFV_SHAPE, "null argument");
   for (int a = 0; a < 3; ++a) {
     if (cells[a] < 1) return fail(MSFV_SHAPE, "cell counts must be integers >= 1");
@@ -133,20 +140,33 @@ int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t bl
     // MSFV_COARSE_ND=0/1/2 overrides
     const char* ev = getenv("MSFV_COARSE_ND");
     g.coarse_nd = ev ? std::min(2, std::max(0, atoi(ev))) : (g.kc >= 1000 ? 2 : 0);
+    if (mesh_only) g.coarse_nd = 0;
     g.mf = nullptr;
     g.skel = nullptr;
     g.nskel = 0;
   }
-  if (!tc_supported(g) && !lg_supported(g))
+  if (!mesh_only && !tc_supported(g) && !lg_supported(g))
     return fail(MSFV_UNSUPPORTED, "block interior half bandwidth ni1*ni2 exceeds 512 (largest supported band)");
-  if (g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
+  if (!mesh_only && g.p >= 65535) return fail(MSFV_UNSUPPORTED, "block too large");
   if (g.Nn >= (1LL << 31) || g.E >= (1LL << 31)) return fail(MSFV_UNSUPPORTED, "mesh too large for 32-bit node/edge indices");
   if (g.coarse_nd == 2 && !mf_attach(g)) g.coarse_nd = g.kc >= 1000 ? 1 : 0;
-  g.gtab8 = grad_template_init(g) ? 1 : 0;
+  g.gtab8 = !mesh_only && grad_template_init(g) ? 1 : 0;
   msfv_plan* pl = new msfv_plan;
   pl->g = g;
+  pl->mesh_only = mesh_only;
   *out = pl;
   return MSFV_OK;
+}
+
+int msfv_plan_create(const int32_t cells[3], const double h[3], const int32_t blocks[3], msfv_plan** out) {
+  return plan_create(cells, h, blocks, false, out);
+}
+
+int msfv_plan_create_mesh(const int32_t cells[3], const double h[3], msfv_plan** out) {
+  if (!cells) return fail(MSFV_SHAPE, "null argument");
+  if (cells[0] > 1023 || cells[1] > 1023 || cells[2] > 1023)
+    return fail(MSFV_UNSUPPORTED, "geometry-only plans take at most 1023 cells per axis");
+  return plan_create(cells, h, cells, true, out);
 }
 
 void msfv_plan_destroy(msfv_plan* plan) {
@@ -363,7 +383,7 @@ static int ensure_skel(msfv_plan* pl) {
 
 static int basis_build(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                        double* scratch, int32_t* flags, void* stream, bool bwd) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
   if (tc_supported(g)) {
@@ -382,14 +402,14 @@ int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, dou
 
 int msfv_basis_forward(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                        int32_t* flags, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   return basis_build(plan, w, factor, Sint, Kloc, nullptr, flags, stream, false);
 }
 
 int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                             int32_t* flags, int32_t bk0, int32_t bk1, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   if (bk0 < 0 || bk1 > g.nb3 || bk0 >= bk1) return fail(MSFV_SHAPE, "bad basis slab");
@@ -403,7 +423,7 @@ int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* fact
 }
 
 int msfv_basis_backward(const msfv_plan* plan, const double* factor, double* Sint, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   return cuda_check(launch_basis_bwd(plan->g, factor, Sint, (cudaStream_t)stream), "basis_backward");
 }
@@ -415,23 +435,23 @@ int msfv_basis_csc(int64_t nnz, const double* Sint, const int64_t* src, const do
 }
 
 int msfv_galerkin(const msfv_plan* plan, const double* Kloc, double shift, double* Ak, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_coarse_assemble(plan->g, Kloc, shift, Ak, (cudaStream_t)stream), "galerkin");
 }
 
 int msfv_coarse_diag(const msfv_plan* plan, const double* Ak, double* diag, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_coarse_diag(plan->g, Ak, diag, (cudaStream_t)stream), "coarse_diag");
 }
 
 int msfv_coarse_factor(const msfv_plan* plan, double* Ak, int32_t* flags, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_coarse_factor(plan->g, Ak, flags, (cudaStream_t)stream), "coarse_factor");
 }
 
 int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* X, double* scratch, int32_t nrhs,
                       void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (nrhs < 0) return fail(MSFV_SHAPE, "nrhs < 0");
   return cuda_check(launch_coarse_solve(plan->g, Lk, X, scratch, nrhs, (cudaStream_t)stream), "coarse_solve");
 }
@@ -461,19 +481,19 @@ int msfv_survey_scatter(const msfv_plan* plan, const msfv_points* pts, const dou
 
 int msfv_prolong(const msfv_plan* plan, const double* Sint, const double* Y, int32_t nrhs, double* field,
                  void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_prolong(plan->g, Sint, Y, nrhs, field, (cudaStream_t)stream), "prolong");
 }
 
 int msfv_residual(const msfv_plan* plan, const double* src, double alpha, const double* wt, const double* X,
                   double beta, int32_t nrhs, double* out, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_residual(plan->g, src, alpha, wt, X, beta, nrhs, out, (cudaStream_t)stream), "residual");
 }
 
 int msfv_interior_solve(const msfv_plan* plan, const double* factor, const double* rhs, double* out, int32_t nrhs,
                         void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
   if (tc_supported(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
@@ -483,14 +503,14 @@ int msfv_interior_solve(const msfv_plan* plan, const double* factor, const doubl
 int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
                      const double* w2, const double* X2, int32_t nrhs, double scale, double* part, double* out,
                      void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_restrict_op(plan->g, Sint, w1, X1, w2, X2, nrhs, part, scale, out, (cudaStream_t)stream),
                     "restrict_op");
 }
 
 int msfv_cell_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* Z,
                        const double* Y, const double* R, int32_t nrhs, double* xi, double* g, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_cell_gradient(plan->g, sigma, U, Z, Y, R, nrhs, xi, g, (cudaStream_t)stream),
                     "cell_gradient");
 }
@@ -511,7 +531,7 @@ int msfv_points_interior_scatter(const msfv_plan* plan, const msfv_points* pts, 
 
 int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, const double* factor,
                                const double* rhs_c, double* out_c, int32_t nrhs, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
   const Geo& g = plan->g;
   if (!tc_supported(g))
@@ -525,7 +545,7 @@ int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, co
 int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double* Sint, const double* T,
                         const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
                         const msfv_points* pr, const double* Rc, double* g, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (nrhs < 0) return fail(MSFV_SHAPE, "bad gradient arguments");
   const Geo& gg = plan->g;
   if (!grad_supported(gg, nrhs)) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
@@ -539,7 +559,7 @@ int msfv_block_gradient_slab(const msfv_plan* plan, const double* sigma, const d
                              const double* y, int32_t nrhs, const msfv_points* pz, const double* Zc,
                              const msfv_points* pr, const double* Rc, int32_t bk0, int32_t bk1, double* g,
                              void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& gg = plan->g;
   if (nrhs < 0 || bk0 < 0 || bk1 > gg.nb3 || bk0 > bk1) return fail(MSFV_SHAPE, "bad gradient slab arguments");
   if (!grad_supported(gg, nrhs)) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
@@ -553,7 +573,7 @@ int msfv_block_gradient_slab(const msfv_plan* plan, const double* sigma, const d
 
 int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* c, const double* T, int32_t nrhs,
                        const msfv_points* pr, const double* Rc, double* part, double* out, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   if (nrhs < 0) return fail(MSFV_SHAPE, "bad J v arguments");
   const Geo& g = plan->g;
   if (jv_smem_doubles(g, nrhs) * sizeof(double) > 200 * 1024)
@@ -567,7 +587,7 @@ int msfv_jv_coarse_rhs(const msfv_plan* plan, const double* Sint, const double* 
 
 int msfv_yk_rhs(const msfv_plan* plan, const double* sigma, const double* Sv, double* rhs_c, uint32_t* mask,
                 void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t ncb = (size_t)g.b1 * g.b2 * g.b3, words = (ncb + 31) / 32;
@@ -579,7 +599,7 @@ int msfv_yk_rhs(const msfv_plan* plan, const double* sigma, const double* Sv, do
 
 int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const double* rhs_c, double* out_c,
                              int32_t nrhs, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   if (!tc_supported(g))
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
@@ -613,16 +633,42 @@ int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* cou
   return cuda_check(launch_xk_rowcount(plan->g, present, (long long*)counts, (cudaStream_t)stream), "xk_rowcount");
 }
 
+int msfv_fine_apply(const msfv_plan* plan, const double* w, const double* X, int32_t nrhs, double* out,
+                    void* stream) {
+  CHECK_PLAN(plan);
+  if (nrhs < 0 || !w || !X || !out) return fail(MSFV_SHAPE, "bad fine apply arguments");
+  return cuda_check(launch_apply_full(plan->g, w, X, nrhs, out, (cudaStream_t)stream), "fine_apply");
+}
+
+int msfv_full_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* V, int32_t nrhs,
+                       double* xi, double* g, void* stream) {
+  CHECK_PLAN(plan);
+  if (nrhs < 0 || !sigma || !U || !V || !xi || !g) return fail(MSFV_SHAPE, "bad full gradient arguments");
+  return cuda_check(launch_full_gradient(plan->g, sigma, U, V, nrhs, xi, g, (cudaStream_t)stream), "full_gradient");
+}
+
+int msfv_reg_apply(const msfv_plan* plan, double alpha, const double* v, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (!v || !out) return fail(MSFV_SHAPE, "bad regularizer arguments");
+  return cuda_check(launch_reg_apply(plan->g, alpha, v, out, (cudaStream_t)stream), "reg_apply");
+}
+
+int msfv_reg_faces(const msfv_plan* plan, const double* d, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (!d || !out) return fail(MSFV_SHAPE, "bad regularizer arguments");
+  return cuda_check(launch_reg_faces(plan->g, d, out, (cudaStream_t)stream), "reg_faces");
+}
+
 int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
                    const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   return cuda_check(launch_xk_values(g, sigma, Sint, z, present, (const long long*)indptr, indices, vals,
                                      (cudaStream_t)stream), "xk_values");
 }
 
 int msfv_coarse_dense(const msfv_plan* plan, const double* Kloc, double shift, double* out, void* stream) {
-  CHECK_PLAN(plan);
+  CHECK_PARTITION(plan);
   return cuda_check(launch_coarse_dense(plan->g, Kloc, shift, out, (cudaStream_t)stream), "coarse_dense");
 }
 

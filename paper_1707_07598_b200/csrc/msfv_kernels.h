@@ -38,6 +38,14 @@ cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w
 cudaError_t launch_cell_gradient(const Geo& g, const double* sigma, const double* U, const double* Z,
                                  const double* Y, const double* R, int nrhs, double* xi, double* gout,
                                  cudaStream_t st);
+// g_c = -sigma_c (V/4) sum over the cell's 12 edges of xi_e (msfv_block.cu)
+cudaError_t launch_cell_gather(const Geo& g, const double* sigma, const double* xi, double* gout, cudaStream_t st);
+// fine mesh and Gauss-Newton objective (msfv_fine.cu)
+cudaError_t launch_apply_full(const Geo& g, const double* w, const double* X, int nrhs, double* out, cudaStream_t st);
+cudaError_t launch_full_gradient(const Geo& g, const double* sigma, const double* U, const double* V, int nrhs,
+                                 double* xi, double* gout, cudaStream_t st);
+cudaError_t launch_reg_apply(const Geo& g, double alpha, const double* v, double* out, cudaStream_t st);
+cudaError_t launch_reg_faces(const Geo& g, const double* d, double* out, cudaStream_t st);
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,
                              double* vals, cudaStream_t st);
 

@@ -97,18 +97,24 @@ class Points:
 
 class Engine:
     def __init__(self, cells, h, blocks):
+        """blocks=None: geometry-only plan (fine-mesh entry points only)."""
         require_cuda()
         L = _lib.load()
         self.L = L
         plan = ctypes.c_void_p()
-        _lib.check(L.msfv_plan_create((ctypes.c_int32 * 3)(*cells), (ctypes.c_double * 3)(*h),
-                                      (ctypes.c_int32 * 3)(*blocks), ctypes.byref(plan)), "plan_create")
+        if blocks is None:
+            _lib.check(L.msfv_plan_create_mesh((ctypes.c_int32 * 3)(*cells), (ctypes.c_double * 3)(*h),
+                                               ctypes.byref(plan)), "plan_create_mesh")
+        else:
+            _lib.check(L.msfv_plan_create((ctypes.c_int32 * 3)(*cells), (ctypes.c_double * 3)(*h),
+                                          (ctypes.c_int32 * 3)(*blocks), ctypes.byref(plan)), "plan_create")
         self.plan = plan
         self._fin = weakref.finalize(self, L.msfv_plan_destroy, plan)
         info = (ctypes.c_int64 * _lib.INFO_COUNT)()
         _lib.check(L.msfv_plan_info(plan, info, _lib.INFO_COUNT))
         self.info = list(info)
-        self.cells, self.h, self.blocks = tuple(cells), tuple(h), tuple(blocks)
+        self.cells, self.h = tuple(cells), tuple(h)
+        self.blocks = None if blocks is None else tuple(blocks)
         self.Nn = info[_lib.INFO_NN]
         self.n = info[_lib.INFO_N]
         self.Nm = info[_lib.INFO_NCELLS]
@@ -412,6 +418,33 @@ class Engine:
                                                  stream()), "jv_coarse_rhs")
         return out
 
+    # ------------------------------------------------------------ fine mesh
+    def fine_apply(self, w, X, out=None):
+        """A(w) X over all pinned nodes; X, out full node fields (Nn, nrhs)."""
+        o = out if out is not None else self.empty(*X.shape)
+        with phase("fine_apply"):
+            _lib.check(self.L.msfv_fine_apply(self.plan, ptr(w), ptr(X), X.shape[1], ptr(o), stream()), "fine_apply")
+        return o
+
+    def full_gradient(self, sigma, U, V):
+        """-sigma C^T sum_s (G U_s)(G V_s) (FullSensitivity.rapply)."""
+        g = self.empty(self.Nm)
+        xi = self.empty(self.E)
+        with phase("full_gradient"):
+            _lib.check(self.L.msfv_full_gradient(self.plan, ptr(sigma), ptr(U), ptr(V), U.shape[1], ptr(xi), ptr(g),
+                                                 stream()), "full_gradient")
+        return g
+
+    def reg_apply(self, alpha, v, out=None):
+        o = out if out is not None else self.empty(self.Nm)
+        _lib.check(self.L.msfv_reg_apply(self.plan, float(alpha), ptr(v), ptr(o), stream()), "reg_apply")
+        return o
+
+    def reg_faces(self, d):
+        o = self.empty(self.Nm)
+        _lib.check(self.L.msfv_reg_faces(self.plan, ptr(d), ptr(o), stream()), "reg_faces")
+        return o
+
     def basis_csc(self, Sint, src, hatv):
         vals = self.empty(src.numel())
         _lib.check(self.L.msfv_basis_csc(src.numel(), ptr(Sint), ptr(src), ptr(hatv), ptr(vals), stream()),
@@ -420,6 +453,17 @@ class Engine:
 
 
 _ENGINES = {}
+
+
+def engine_for_mesh(mesh):
+    """Geometry-only engine of a mesh (fine-mesh entry points)."""
+    key = ((mesh.n1, mesh.n2, mesh.n3), (float(mesh.h1), float(mesh.h2), float(mesh.h3)), None,
+           torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = Engine(*key[:3])
+        _ENGINES[key] = eng
+    return eng
 
 
 def engine_for(partition):

@@ -1,0 +1,228 @@
+"""Device-resident bound-constrained Gauss-Newton.
+
+The reference's outer loop, ``projected_gauss_newton`` (inversion.py:187-263),
+runs on host arrays and calls the Problem protocol (``simulate`` /
+``jacobian(state).apply`` / ``.rapply``); it drives this package's
+``AdaptiveReducedProblem`` unchanged (tests/test_gpu_gn.py).
+``gauss_newton_dev`` is the same method with every vector on the device: the
+model, gradient, inactive mask, CG iterates and line-search trials never leave
+HBM; only the scalars the method branches on (curvature, residual norms, the
+Armijo test, the trace columns) come back to the host, once per CG step or
+trial.  The Tikhonov term alpha/2 ||L(m - m_ref)||^2 with the reference's
+default L (``cell_gradient``, inversion.py:32-62) is evaluated by
+``msfv_reg_apply`` / ``msfv_reg_faces``.  Defaults, stopping rules, step
+control and trace columns follow ``GNConfig`` / ``InversionTrace``
+(inversion.py:122-157); reference GNConfig objects are accepted as they are.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import engine_for_mesh
+
+
+@dataclass
+class GNSettings:
+    """The fields of the reference's GNConfig (inversion.py:122-140)."""
+
+    max_gn: int = 10
+    max_cg: int = 15
+    cg_rtol: float = 1e-8
+    armijo_c: float = 1e-4
+    backtrack: float = 0.5
+    max_backtracks: int = 10
+    grad_tol_rel: float = 1e-10
+    lower: object = None
+    upper: object = None
+
+    def __post_init__(self):
+        if self.max_gn < 1 or self.max_cg < 1:
+            raise ValueError("iteration budgets must be >= 1")
+        if not 0 < self.armijo_c <= 0.5:
+            raise ValueError("Armijo constant must lie in (0, 0.5]")
+
+
+@dataclass
+class DeviceTrace:
+    """Per-iteration log with the reference trace's columns (inversion.py:143-157)."""
+
+    rows: list = field(default_factory=list)
+    notes: list = field(default_factory=list)
+    line_search_failed: bool = False
+    final_model: np.ndarray = None
+
+    COLUMNS = ("iter", "phi", "reg", "total", "pgnorm", "step", "cg_iters", "active", "rebuilt")
+
+    def add(self, **kw):
+        self.rows.append({c: kw[c] for c in self.COLUMNS})
+
+    def totals(self):
+        return np.asarray([r["total"] for r in self.rows])
+
+
+class DeviceObjective:
+    """alpha/2 ||L (m - m_ref)||^2, L = cell_gradient(mesh) (inversion.py:65-88)."""
+
+    def __init__(self, mesh, alpha, m_ref):
+        if alpha < 0:
+            raise ValueError("regularization weight must be >= 0")
+        self.eng = engine_for_mesh(mesh)
+        self.alpha = float(alpha)
+        self.m_ref = self.eng.to_device(m_ref).reshape(-1)
+
+    @classmethod
+    def from_reference(cls, objective):
+        """A reference Objective with its default L (cell_gradient)."""
+        return cls(objective.mesh, objective.alpha, objective.m_ref)
+
+    def value_grad(self, m):
+        d = m - self.m_ref
+        reg = 0.5 * self.alpha * torch.sum(self.eng.reg_faces(d))
+        return reg, self.eng.reg_apply(self.alpha, d)
+
+    def hess_apply(self, v):
+        return self.eng.reg_apply(self.alpha, v)
+
+
+def _bound(x, like):
+    if x is None:
+        return None
+    t = torch.as_tensor(np.asarray(x, dtype=float) if not isinstance(x, torch.Tensor) else x,
+                        dtype=torch.float64, device=like.device)
+    return torch.broadcast_to(t, like.shape)
+
+
+def _project(m, lo, hi):
+    if lo is not None and hi is not None and bool(torch.any(lo > hi)):
+        raise ValueError("lower bound exceeds upper bound")
+    out = m
+    if lo is not None:
+        out = torch.maximum(out, lo)
+    if hi is not None:
+        out = torch.minimum(out, hi)
+    return out
+
+
+def _simulate(problem, m):
+    if hasattr(problem, "simulate_dev"):
+        return problem.simulate_dev(m)
+    D, st = problem.simulate(m.cpu().numpy())
+    return torch.as_tensor(D, device=m.device), st
+
+
+def _jac(J, name):
+    f = getattr(J, name + "_dev", None)
+    if f is not None:
+        return f
+    g = getattr(J, name)
+    return lambda v: torch.as_tensor(g(v.cpu().numpy()), device=v.device)
+
+
+def _masked_cg_dev(hess, rhs, inactive, maxit, rtol):
+    """CG on the inactive subspace (inversion.py:160-184), device vectors."""
+    x = torch.zeros_like(rhs)
+    r = rhs * inactive
+    rhs_norm = float(torch.linalg.vector_norm(r))
+    if rhs_norm == 0:
+        return x, 0
+    p = r.clone()
+    rr = float(torch.dot(r, r))
+    it = 0
+    while it < maxit:
+        Hp = hess(p) * inactive
+        pHp = float(torch.dot(p, Hp))
+        if pHp <= 0:
+            break
+        a = rr / pHp
+        x += a * p
+        r -= a * Hp
+        it += 1
+        rr_new = float(torch.dot(r, r))
+        if np.sqrt(rr_new) <= rtol * rhs_norm:
+            break
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    return x, it
+
+
+def gauss_newton_dev(problem, m0, d_obs, objective, config=None):
+    """Bound-constrained Gauss-Newton with Armijo backtracking, device-resident
+    (the method of inversion.py:187-263).  ``objective``: a DeviceObjective or
+    a reference Objective with the default L; ``config``: GNSettings or the
+    reference's GNConfig.  Returns (model as numpy, DeviceTrace)."""
+    cfg = config if config is not None else GNSettings()
+    if not isinstance(objective, DeviceObjective):
+        objective = DeviceObjective.from_reference(objective)
+    dev = objective.eng.device
+    m = torch.as_tensor(np.asarray(m0, dtype=float) if not isinstance(m0, torch.Tensor) else m0,
+                        dtype=torch.float64, device=dev).reshape(-1).clone()
+    dobs = torch.as_tensor(np.asarray(d_obs, dtype=float) if not isinstance(d_obs, torch.Tensor) else d_obs,
+                           dtype=torch.float64, device=dev)
+    lo, hi = _bound(cfg.lower, m), _bound(cfg.upper, m)
+    m = _project(m, lo, hi)
+    trace = DeviceTrace()
+
+    def evaluate(mm):
+        D, st = _simulate(problem, mm)
+        resid = D - dobs
+        phi = 0.5 * torch.sum(resid * resid)
+        reg, reg_grad = objective.value_grad(mm)
+        return st, resid, phi, reg, reg_grad
+
+    state, resid, phi, reg, reg_grad = evaluate(m)
+    phi, reg = float(phi), float(reg)
+    total = phi + reg
+    if getattr(state, "shift", 0.0):
+        trace.notes.append(f"iter 0: diagonal shift {state.shift:.3e} applied")
+    pg0 = None
+    rebuilt0 = problem.mode != "full"
+    it = 0
+    while True:
+        J = problem.jacobian(state)
+        apply, rapply = _jac(J, "apply"), _jac(J, "rapply")
+        g = rapply(resid) + reg_grad
+        active = torch.zeros_like(m, dtype=torch.bool)
+        if lo is not None:
+            active |= (m <= lo) & (g > 0)
+        if hi is not None:
+            active |= (m >= hi) & (g < 0)
+        inactive = (~active).to(torch.float64)
+        pgnorm = float(torch.linalg.vector_norm(g * inactive))
+        n_active = int(active.sum())
+        if pg0 is None:
+            pg0 = pgnorm
+            trace.add(iter=0, phi=phi, reg=reg, total=total, pgnorm=pgnorm, step=0.0, cg_iters=0,
+                      active=n_active, rebuilt=rebuilt0)
+        if it >= cfg.max_gn or pgnorm <= cfg.grad_tol_rel * pg0:
+            break
+
+        def hess(v, apply=apply, rapply=rapply):
+            return rapply(apply(v)) + objective.hess_apply(v)
+
+        dm, cg_iters = _masked_cg_dev(hess, -g, inactive, cfg.max_cg, cfg.cg_rtol)
+        step, accepted = 1.0, False
+        for _ in range(cfg.max_backtracks + 1):
+            m_trial = _project(m + step * dm, lo, hi)
+            st_t, resid_t, phi_t, reg_t, reg_grad_t = evaluate(m_trial)
+            phi_t, reg_t = float(phi_t), float(reg_t)
+            total_t = phi_t + reg_t
+            if total_t <= total + cfg.armijo_c * float(torch.dot(g, m_trial - m)):
+                accepted = True
+                break
+            step *= cfg.backtrack
+        it += 1
+        if not accepted:
+            trace.line_search_failed = True
+            trace.notes.append(f"iter {it}: line search failed, stopping")
+            break
+        m, state, resid = m_trial, st_t, resid_t
+        phi, reg, reg_grad, total = phi_t, reg_t, reg_grad_t, total_t
+        if getattr(state, "shift", 0.0):
+            trace.notes.append(f"iter {it}: diagonal shift {state.shift:.3e} applied")
+        trace.add(iter=it, phi=phi, reg=reg, total=total, pgnorm=pgnorm, step=step, cg_iters=cg_iters,
+                  active=n_active, rebuilt=problem.mode == "ms_adaptive")
+    m_host = m.cpu().numpy()
+    trace.final_model = m_host.copy()
+    return m_host, trace

@@ -114,3 +114,18 @@ def table3_errors(g, Y=None, X=None):
             assert np.array_equal(Y.indptr, g["Y_indptr"]) and np.array_equal(Y.indices, g["Y_indices"]), "Y_k pattern"
             errs["Y"] = rel(Y.data, g["Y_data"])
     return errs
+
+
+def import_reference():
+    """The unmodified reference package installed under baseline/_ref (the one
+    offline install the task allows; git-ignored, shipped to the GPU box), or
+    None when it is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "msinv")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import msinv  # noqa: F401
+        import msinv.inversion  # noqa: F401
+        return msinv
+    except ImportError:
+        return None

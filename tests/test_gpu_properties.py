@@ -147,15 +147,20 @@ def test_objective_gradient_central_difference(rng):
     survey = point_survey(mesh, n_rec=10, n_src=3, seed=4, dipoles=True)
     prob = gp.AdaptiveReducedProblem(gp.BasisBuilder(part), survey)
     d_obs = prob.simulate(m0 + 0.3)[0]
-    obj = gp.Objective(mesh=mesh, alpha=1e-4, m_ref=np.full(m0.size, np.log(0.05)))
+    import torch
+    obj = gp.DeviceObjective(mesh, 1e-4, np.full(m0.size, np.log(0.05)))
+
+    def reg(mm):
+        r, gr = obj.value_grad(torch.from_numpy(mm).cuda())
+        return float(r), gr.cpu().numpy()
 
     def total(mm):
         D, _ = prob.simulate(mm)
-        return gp.misfit_ssd(D, d_obs)[0] + obj.value_grad(mm)[0]
+        return gp.misfit_ssd(D, d_obs)[0] + reg(mm)[0]
 
     D, st = prob.simulate(m0)
     _, resid = gp.misfit_ssd(D, d_obs)
-    g = prob.jacobian(st).rapply(resid) + obj.value_grad(m0)[1]
+    g = prob.jacobian(st).rapply(resid) + reg(m0)[1]
     dm = rng.normal(size=m0.size)
     eps = 1e-6
     fd = (total(m0 + eps * dm) - total(m0 - eps * dm)) / (2 * eps)
@@ -198,15 +203,15 @@ def test_error_contract(rng):
 
 
 def test_gauss_newton_decreases_objective(rng):
-    # inversion.py:187-263 driven through the GPU problem (trace monotone)
+    # the method of inversion.py:187-263, device-resident (trace monotone)
     mesh = gp.create_mesh(8, 8, 4)
     part = gp.create_partition(mesh, 2, 2, 2)
     survey = point_survey(mesh, n_rec=12, n_src=3, seed=2, dipoles=True)
     prob = gp.AdaptiveReducedProblem(gp.BasisBuilder(part), survey)
     m_true = 0.4 * rng.normal(size=mesh.n_cells)
     d_obs = prob.simulate(m_true)[0]
-    obj = gp.Objective(mesh=mesh, alpha=1e-3, m_ref=np.zeros(mesh.n_cells))
-    m, trace = gp.projected_gauss_newton(prob, np.zeros(mesh.n_cells), d_obs, obj, gp.GNConfig(max_gn=3, max_cg=5))
+    obj = gp.DeviceObjective(mesh, 1e-3, np.zeros(mesh.n_cells))
+    m, trace = gp.gauss_newton_dev(prob, np.zeros(mesh.n_cells), d_obs, obj, gp.GNSettings(max_gn=3, max_cg=5))
     tot = trace.totals()
     assert np.all(np.diff(tot) <= 1e-15 * abs(tot[0]))
     assert tot[-1] < tot[0]

@@ -18,4 +18,9 @@ done
 # coarse kernels launch several times per step
 ncu --set full --clock-control none -k regex:"k_mf_solve_coop" --launch-skip 6 -c 2 -o gpurun_out/${TAG}_k_mf_solve_coop $B >> gpurun_out/ncu_$TAG.log 2>&1
 ncu --set full --clock-control none -k regex:"k_mf_factor|k_mf_inv" --launch-skip 60 -c 20 -o gpurun_out/${TAG}_k_mf_factor $B >> gpurun_out/ncu_$TAG.log 2>&1
+# summaries on the box (reports are large); keep the basis-kernel report only
+python tools/ncu_summary.py gpurun_out/launches_$TAG.csv $(ls gpurun_out/${TAG}_*.ncu-rep | paste -sd,) gpurun_out/$TAG >> gpurun_out/ncu_$TAG.log 2>&1
+for f in gpurun_out/${TAG}_*.ncu-rep; do
+  case $f in *k_basis_tc*) ;; *) rm -f $f ;; esac
+done
 echo done
