@@ -28,7 +28,6 @@ __global__ void k_apply_full(Geo g, const double* __restrict__ w, const double* 
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= g.Nn * nrhs) return;
   const long long nd = t / nrhs;
-  const int s = (int)(t - nd * nrhs);
   if (nd == 0) {
     out[t] = 0.0;
     return;

@@ -313,7 +313,9 @@ __device__ __forceinline__ F2 potrf_inv8_pipe(const F2& t, double* Ds, double* I
 //   x_J^T = (y_J^T - sum_t x_{J+t}^T X_t) L_JJ^{-1};
 // the window keeps -x^T of the last PT tiles; the next steps' transposed
 // factor tiles and y are prefetched into registers.
-template <int PT>
+// SPX (p = 8 PT - 7): the transposed offset-PT tile has its one entry in
+// column 0, so its product needs only the chunk-0 DMMA.
+template <int PT, bool SPX = false>
 __device__ __forceinline__ void backward_sweep(const Geo& g, const double* __restrict__ LT, double* Sb, int jb,
                                                int lane) {
   const int NTI = (g.nI + 7) >> 3;
@@ -342,7 +344,12 @@ __device__ __forceinline__ void backward_sweep(const Geo& g, const double* __res
       if (J > 1) load_bwd(J - 2, nLt[1], nY[1]);
 #pragma unroll
       for (int t = 1; t <= PT; ++t)
-        if (J + t < NTI) mma(acc, Xw[t - 1], cLt[t]);
+        if (J + t < NTI) {
+          if (SPX && t == PT)
+            mma884(acc.x, acc.y, Xw[t - 1].x, cLt[t].x);
+          else
+            mma(acc, Xw[t - 1], cLt[t]);
+        }
       F2 xj = {0.0, 0.0};
       mma(xj, acc, cLt[0]);
       st_rt(g, Sb, J, lane, xj);
@@ -371,6 +378,13 @@ __device__ __forceinline__ void mma_to(F2& d, const F2& c, const F2& a, const F2
       : "d"(a.x), "d"(b.x), "d"(c.x), "d"(c.y));
   mma884(d.x, d.y, a.y, b.y);
 }
+// d = c + X Y^T when one operand's even columns (chunk 0) are exactly zero:
+// one DMMA instead of two
+__device__ __forceinline__ void mma_to_h1(F2& d, const F2& c, const F2& a, const F2& b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+      : "=d"(d.x), "=d"(d.y)
+      : "d"(a.y), "d"(b.y), "d"(c.x), "d"(c.y));
+}
 // 1/sqrt(d) for a positive normal d: MUFU seed (>= 2^-22) and one cubic
 // Newton-type step y (1 + e/2 + 3e^2/8), e = 1 - d y^2 (relative error ~2^-60
 // before rounding).
@@ -381,7 +395,10 @@ __device__ __forceinline__ double rsq(double d) {
   const double t = fma(0.375, e, 0.5);
   return fma(y * e, t, y);
 }
-template <int PT>
+// SPX: the band is p = 8 PT - 7 (7x7x7 interiors: p = 49, PT = 7), so the
+// offset-PT factor tile L_{J+PT,J} holds one entry, (0, 7): its chunk 0 (even
+// columns) is exactly zero and every product with it needs one DMMA.
+template <int PT, bool SPX = false>
 struct TrailPipe2 {
   F2 (&Wn)[PT + 1][PT + 1];
   const F2 (&W)[PT + 1][PT + 1];
@@ -395,7 +412,10 @@ struct TrailPipe2 {
   __device__ __forceinline__ void run() {
     if constexpr (LO < HI) {
       constexpr int a = tr_a(PT, LO), b = tr_b(PT, LO);
-      mma_to(Wn[a - 1][b - 1], W[a][b], neg(X[a]), X[b]);
+      if constexpr (SPX && a == PT)
+        mma_to_h1(Wn[a - 1][b - 1], W[a][b], neg(X[a]), X[b]);
+      else
+        mma_to(Wn[a - 1][b - 1], W[a][b], neg(X[a]), X[b]);
       run<LO + 1, HI>();
     }
   }
@@ -552,6 +572,8 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
                                                     F2& G) {
   const int NTI = (g.nI + 7) >> 3;
   const int m = lane >> 2, q = lane & 3;
+  // 7x7x7 interiors (OM = {0,1,6,7}): p = 49 = 8 PT - 7, see TrailPipe2
+  constexpr bool SPX = PT == 7 && OM == 0xC3u;
   // per-lane stencil slots (3 bits each) of element (b, s) of W[PT][b]:
   // A(i, i - d), d = 8 (PT - b) + m - 2q - s
   unsigned long long sel = 0;
@@ -591,7 +613,10 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
 #pragma unroll
     for (int t = 1; t <= PT; ++t) {
       X[t] = {0.0, 0.0};
-      mma(X[t], W[t][0], Li);        // X_t = A_t L^{-T}
+      if (SPX && t == PT)
+        mma884(X[t].x, X[t].y, W[t][0].y, Li.y);   // A_{J+PT,J} = its (0, 7) entry (never updated)
+      else
+        mma(X[t], W[t][0], Li);      // X_t = A_t L^{-T}
       st2(Ls + t * 64 + lane * 2, X[t]);
     }
     fence_async_smem();
@@ -606,13 +631,18 @@ __device__ __forceinline__ void factor_forward_lean(const Geo& g, const double* 
     {
       const F2 nY = neg(Yt);
 #pragma unroll
-      for (int t = 1; t <= PT; ++t) mma_to(Rn[t - 1], Rt[t], nY, X[t]);
+      for (int t = 1; t <= PT; ++t) {
+        if (SPX && t == PT)
+          mma_to_h1(Rn[t - 1], Rt[t], nY, X[t]);
+        else
+          mma_to(Rn[t - 1], Rt[t], nY, X[t]);
+      }
     }
     st_rt(g, Sb, J, lane, Yt);       // y parks in the consumed rhs rows
     Rn[PT] = nR;
     if constexpr (PT >= 1) {
       mma_to(Wn[0][0], W[1][1], neg(X[1]), X[1]);
-      TrailPipe2<PT> pipe{Wn, W, X};
+      TrailPipe2<PT, SPX> pipe{Wn, W, X};
       if (J + 1 < NTI) {
         Li = potrf_inv8_lean(Wn[0][0], Ds, Is, lane, flags, pipe);
       } else {
@@ -686,7 +716,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
       double* Lst = As + AFE;                    // 2 x (PT + 1) tiles, 16-byte aligned
       factor_forward_lean<PT, OM, RF>(g, As, Fk, Sb, LT, jb, lane, Ds, Is, Lst, flags, G);
       __syncwarp();
-      if constexpr (BWD) backward_sweep<PT>(g, LT, Sb, jb, lane);
+      if constexpr (BWD) backward_sweep<PT, PT == 7 && OM == 0xC3u>(g, LT, Sb, jb, lane);
       __syncwarp();
     }
   } else if (NTI > 0) {
@@ -801,12 +831,12 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
 // 2-warp CTA per two SMs) so it can run beside the cooperative coarse
 // factorization, which needs a CTA slot on every SM.
 constexpr int BWD_WARPS = 8;   // one 256-thread CTA per SM (register-limited)
-template <int PT>
+template <int PT, bool SPX>
 __global__ void __launch_bounds__(BWD_WARPS * 32) k_basis_bwd(Geo g, const double* __restrict__ LT,
                                                               double* __restrict__ Sint) {
   const int lane = threadIdx.x & 31;
   for (int jb = blockIdx.x * BWD_WARPS + (threadIdx.x >> 5); jb < g.nbl; jb += gridDim.x * BWD_WARPS)
-    backward_sweep<PT>(g, LT, Sint + (size_t)jb * 8 * g.nI, jb, lane);
+    backward_sweep<PT, SPX>(g, LT, Sint + (size_t)jb * 8 * g.nI, jb, lane);
 }
 
 // ------------------------------------------------------- skeleton Galerkin
@@ -1321,7 +1351,10 @@ static cudaError_t launch_basis_bwd_t(const Geo& g, const double* LT, double* Si
   // and run on the SMs the coarse kernels leave free (mf_reserved_sms)
   const int want = g.coarse_nd == 2 ? std::max(1, mf_reserved_sms()) : sms - free_sms;
   const int grid = std::max(1, std::min((g.nbl + BWD_WARPS - 1) / BWD_WARPS, want));
-  k_basis_bwd<PT><<<grid, BWD_WARPS * 32, 0, st>>>(g, LT, Sint);
+  if (PT == 7 && g.p == 8 * PT - 7 && g.ni1 == 7 && g.ni2 == 7)
+    k_basis_bwd<PT, true><<<grid, BWD_WARPS * 32, 0, st>>>(g, LT, Sint);
+  else
+    k_basis_bwd<PT, false><<<grid, BWD_WARPS * 32, 0, st>>>(g, LT, Sint);
   count_launches(1);
   return cudaGetLastError();
 }
