@@ -74,7 +74,9 @@ enum msfv_info {
   MSFV_INFO_TC = 16,              /* local solver: 1 DMMA register-window band (p <= 56, split build),
                                      2 DMMA L2-resident band (larger blocks)     */
   MSFV_INFO_COARSE = 17,          /* coarse solver: 0 band, 1 z-plane ND band, 2 multifrontal ND */
-  MSFV_INFO_COUNT = 18
+  MSFV_INFO_RED_FACE_DOUBLES = 18, /* msfv_boundary_reduced face scratch (reduced plans)        */
+  MSFV_INFO_RED_BOX_DOUBLES = 19,  /* msfv_boundary_reduced box table [nblocks][8][(b+1)^3]      */
+  MSFV_INFO_COUNT = 20
 };
 
 typedef struct msfv_plan msfv_plan;      /* geometry; model-independent        */
@@ -244,6 +246,28 @@ MSFV_API int msfv_xk_present(const msfv_plan* plan, const double* z, int32_t* pr
 MSFV_API int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* counts, void* stream);
 MSFV_API int msfv_xk_values(const msfv_plan* plan, const double* sigma, const double* Sint, const double* z,
                    const int32_t* present, const int64_t* indptr, int32_t* indices, double* vals, void* stream);
+
+/* ---- Reduced-dimension boundary conditions (an extension:
+ * the reference uses the trilinear hats, basis.py:84-116) ----
+ * msfv_plan_set_reduced(plan, 1): the plan's basis entry points use skeleton
+ *   values from 1D line problems (normalized cumulative resistance along each
+ *   skeleton segment) and 2D face-patch problems (5-point, in-plane edge
+ *   weights w_e/h_e^2) instead of the hats; local solves take the L2 band path.
+ * msfv_boundary_reduced: computes them from the edge weights w into the box
+ *   table bx [nblocks][8][(b1+1)(b2+1)(b3+1)] (faces: scratch of
+ *   MSFV_INFO_RED_FACE_DOUBLES); flags |= LOCAL_NOT_SPD on a failed face solve.
+ * msfv_plan_bind_boundary: the table the following launches read (one model
+ *   at a time, like the basis it belongs to).
+ * msfv_basis_csc_box: S values in the reference CSC pattern, skeleton entries
+ *   from the table (bsrc: flat index into bx).
+ * Derivatives (gradient, J v, Y_k / X_k) are not built for reduced plans
+ * (MSFV_UNSUPPORTED). */
+MSFV_API int msfv_plan_set_reduced(msfv_plan* plan, int32_t on);
+MSFV_API int msfv_boundary_reduced(const msfv_plan* plan, const double* w, double* faces, double* bx, int32_t* flags,
+                                   void* stream);
+MSFV_API int msfv_plan_bind_boundary(msfv_plan* plan, const double* bx);
+MSFV_API int msfv_basis_csc_box(int64_t nnz, const double* Sint, const int64_t* src, const int64_t* bsrc,
+                                const double* bx, double* vals, void* stream);
 
 /* ---- Fine mesh (forward_full, FullSensitivity, block_cg) ----
  * msfv_fine_apply: out = A(w) X on every pinned node (the operator product

@@ -29,8 +29,8 @@ FLAG_COARSE_NOT_SPD = 8
 
 INFO_NN, INFO_N, INFO_NCELLS, INFO_NEDGES, INFO_NBLOCKS, INFO_NI, INFO_P1S, INFO_K, \
     INFO_AK_DOUBLES, INFO_BASIS_SMEM, INFO_NT, INFO_PT, INFO_TB, INFO_PC, \
-    INFO_FACTOR_DOUBLES, INFO_SCRATCH_DOUBLES, INFO_TC, INFO_COARSE = range(18)
-INFO_COUNT = 18
+    INFO_FACTOR_DOUBLES, INFO_SCRATCH_DOUBLES, INFO_TC, INFO_COARSE, INFO_RED_FACE, INFO_RED_BOX = range(20)
+INFO_COUNT = 20
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
@@ -74,6 +74,10 @@ SIGNATURES = {
     "msfv_block_gradient_slab": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I32, _P, _P]),
     "msfv_jv_coarse_rhs": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "msfv_coarse_dense": (ctypes.c_int, [_P, _P, _D, _P, _P]),
+    "msfv_plan_set_reduced": (ctypes.c_int, [_P, _I32]),
+    "msfv_boundary_reduced": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "msfv_plan_bind_boundary": (ctypes.c_int, [_P, _P]),
+    "msfv_basis_csc_box": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P]),
     "msfv_plan_create_mesh": (ctypes.c_int, [_P, _P, ctypes.POINTER(_P)]),
     "msfv_fine_apply": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_full_gradient": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P]),

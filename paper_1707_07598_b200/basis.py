@@ -39,6 +39,10 @@ class BasisSpec:
     pca_rank: int = 0
     pca_total: int = 0
     pca_drop_tol: float = 1e-10
+    # extension: "hats" = the reference's trilinear skeleton
+    # data (basis.py:84-116); "reduced" = 1D line / 2D face problems with the
+    # model's edge weights (msfv_reduced.cu; forward path only)
+    boundary: str = "hats"
 
     def __post_init__(self):
         unknown = set(self.families) - set(FAMILIES)
@@ -48,6 +52,8 @@ class BasisSpec:
             raise ValueError("at least one basis family must be enabled")
         if "local_pca" in self.families and self.pca_rank < 1:
             raise ValueError("local_pca requires pca_rank >= 1")
+        if self.boundary not in ("hats", "reduced"):
+            raise ValueError(f"unknown boundary condition kind {self.boundary!r}")
 
 
 def coarse_hat_values(partition, coarse_node, node_ids):
@@ -142,6 +148,34 @@ def csc_pattern(partition):
     return indices, indptr, src[order], hv[order]
 
 
+def box_sources(partition, indices, indptr, src):
+    """For the skeleton entries (src < 0) of the CSC pattern: flat index into
+    the reduced-boundary box table bx[block][corner][(b1+1)(b2+1)(b3+1)] of a
+    block having the entry's coarse node as a corner (msfv_reduced.cu)."""
+    mesh = partition.mesh
+    b = (partition.b1, partition.b2, partition.b3)
+    nb = partition.nb
+    k = partition.n_coarse_nodes
+    cols = np.repeat(np.arange(k), np.diff(indptr))
+    node = indices.astype(np.int64) + 1
+    ijk = mesh.node_triple(node)
+    nbp = (nb[0] + 1, nb[1] + 1)
+    cijk = (cols % nbp[0], (cols // nbp[0]) % nbp[1], cols // (nbp[0] * nbp[1]))
+    blk, loc, bit = [], [], []
+    for ax in range(3):
+        x, c = ijk[ax], cijk[ax]
+        lower = (x < c * b[ax]) | ((x == c * b[ax]) & (c == nb[ax]))
+        bi = np.where(lower, c - 1, c)
+        blk.append(bi)
+        loc.append(x - bi * b[ax])
+        bit.append(lower.astype(np.int64))
+    jb = blk[0] + nb[0] * (blk[1] + nb[1] * blk[2])
+    cc = bit[0] + 2 * bit[1] + 4 * bit[2]
+    nbox = (b[0] + 1) * (b[1] + 1) * (b[2] + 1)
+    flat = (jb * 8 + cc) * nbox + loc[0] + (b[0] + 1) * (loc[1] + (b[1] + 1) * loc[2])
+    return np.where(src < 0, flat, -1).astype(np.int64)
+
+
 class _CscTemplate:
     """csc_pattern uploaded for one engine."""
 
@@ -151,6 +185,9 @@ class _CscTemplate:
         self.shape = (partition.mesh.n_nodes - 1, partition.n_coarse_nodes)
         self.src = torch.from_numpy(src).to(engine.device)
         self.hatv = torch.from_numpy(hv).to(engine.device)
+        self.bsrc = None
+        if engine.reduced:
+            self.bsrc = torch.from_numpy(box_sources(partition, self.indices, self.indptr, src)).to(engine.device)
 
 
 class MultiscaleBasis:
@@ -171,6 +208,7 @@ class MultiscaleBasis:
         self._S = None
         self._EP = None
         self._checked = False
+        self.bx = None                   # reduced-boundary box table (spec.boundary == "reduced")
 
     def start_backward(self):
         """Launch the deferred backward sweeps (split build) on the side stream,
@@ -255,7 +293,11 @@ class MultiscaleBasis:
     def S(self):
         if self._S is None:
             tpl = _template(self.partition, self.engine)
-            vals = self.engine.basis_csc(self.Sint, tpl.src, tpl.hatv).cpu().numpy()
+            if self.bx is not None:
+                self.engine.bind_boundary(self.bx)
+                vals = self.engine.basis_csc_box(self.Sint, tpl.src, tpl.bsrc, self.bx).cpu().numpy()
+            else:
+                vals = self.engine.basis_csc(self.Sint, tpl.src, tpl.hatv).cpu().numpy()
             self._S = sp.csc_matrix((vals, tpl.indices, tpl.indptr), shape=tpl.shape)
         return self._S
 
@@ -305,12 +347,23 @@ def _check_families(spec):
             f"families {tuple(spec.families)} are outside this tier's scope")
 
 
-def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None):
-    """Build the Lagrange basis at the operator's model (basis.py:511-616)."""
+def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None, spec=None):
+    """Build the Lagrange basis at the operator's model (basis.py:511-616).
+    ``spec.boundary == "reduced"``: skeleton data from the reduced 1D/2D
+    problems at this model instead of the hats (extension, forward only)."""
     if bc_sets is not None:
         fams = [getattr(s, "family", "lagrange") for s in bc_sets]
         if fams != ["lagrange"]:
             raise NotImplementedError("the GPU path builds the Lagrange family only")
+    if spec is not None and spec.boundary == "reduced":
+        eng = engine_for(partition, reduced=True)
+        _, m_dev, sigma, w = op.device_state(eng)
+        bx = eng.boundary_reduced(w, op.flags)
+        eng.bind_boundary(bx)
+        factor, Sint, Kloc, fl = eng.basis(w, op.flags)
+        basis = MultiscaleBasis(partition, eng, op, factor, Sint, Kloc, fl)
+        basis.bx = bx
+        return basis
     eng = engine_for(partition)
     _, m_dev, sigma, w = op.device_state(eng)
     if eng.tensor_core:
@@ -351,4 +404,4 @@ class BasisBuilder:
         return self._bc_sets
 
     def assemble(self, op, workers=None):
-        return assemble_basis(op, self.partition, workers=workers)
+        return assemble_basis(op, self.partition, workers=workers, spec=self.spec)

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmsfv.so")
-SOURCES = ["msfv_block.cu", "msfv_tc.cu", "msfv_large.cu", "msfv_fine.cu", "msfv_coarse.cu", "msfv_points.cu", "msfv_grad.cu", "msfv_table3.cu", "msfv_2d.cu", "msfv_capi.cu"]
+SOURCES = ["msfv_block.cu", "msfv_tc.cu", "msfv_large.cu", "msfv_fine.cu", "msfv_reduced.cu", "msfv_coarse.cu", "msfv_points.cu", "msfv_grad.cu", "msfv_table3.cu", "msfv_2d.cu", "msfv_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

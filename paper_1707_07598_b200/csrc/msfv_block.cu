@@ -261,12 +261,13 @@ __global__ void k_prolong(Geo g, const double* __restrict__ Sint, const double* 
     bk = min(fdiv(K, g.b3, g.r_b3), g.nb3 - 1);
     x = I - bi * g.b1; y = J - bj * g.b2; z = K - bk * g.b3;
   }
-  const double* Sb = Sint + (size_t)block_of(g, bi, bj, bk) * 8 * g.nI;
+  const int jbk = block_of(g, bi, bj, bk);
+  const double* Sb = Sint + (size_t)jbk * 8 * g.nI;
   double sv[8];
   int col[8];
   if (G >= 8) {
     const int my = j & 7;
-    const double s1 = valid ? s_value(g, Sb, my, x, y, z, false) : 0.0;
+    const double s1 = valid ? s_value(g, Sb, jbk, my, x, y, z, false) : 0.0;
     const int c1 = corner_col(g, bi, bj, bk, my);
     const int base = (threadIdx.x & 31) & ~(G - 1);
 #pragma unroll
@@ -277,7 +278,7 @@ __global__ void k_prolong(Geo g, const double* __restrict__ Sint, const double* 
   } else {
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) {
-      sv[cc] = valid ? s_value(g, Sb, cc, x, y, z, false) : 0.0;
+      sv[cc] = valid ? s_value(g, Sb, jbk, cc, x, y, z, false) : 0.0;
       col[cc] = corner_col(g, bi, bj, bk, cc);
     }
   }
@@ -317,7 +318,7 @@ k_restrict_op(Geo g, const double* __restrict__ Sint, const double* __restrict__
       if (X1) h += apply_A_row(g, w1, X1, nrhs, s, I, J, K);
       if (X2) h += apply_A_row(g, w2, X2, nrhs, s, I, J, K);
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) acc[cc] += s_value(g, Sb, cc, x, y, z, false) * h;
+      for (int cc = 0; cc < 8; ++cc) acc[cc] += s_value(g, Sb, jb, cc, x, y, z, false) * h;
     }
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) red[cc * nt + tid] = acc[cc];

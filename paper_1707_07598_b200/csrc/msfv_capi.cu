@@ -63,6 +63,11 @@ struct msfv_points {
   void* mem = nullptr;
 };
 
+// the register-window DMMA band path (msfv_tc.cu); plans with reduced
+// boundary conditions always take the L2-resident band path (msfv_large.cu),
+// whose kernels read the bound skeleton-value table
+static inline bool use_tc(const Geo& g) { return tc_supported(g) && !g.reduced; }
+
 static thread_local std::string g_err;
 
 static int fail(int code, const std::string& msg) {
@@ -119,6 +124,7 @@ static int plan_create(const int32_t cells[3], const double h[3], const int32_t 
   g.nwy = (g.b1 + 1) * g.b2 * (g.b3 + 1);
   g.nwz = (g.b1 + 1) * (g.b2 + 1) * g.b3;
   g.Nn = (long long)(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
+  g.nbox = (g.b1 + 1) * (g.b2 + 1) * (g.b3 + 1);
   g.Nm = (long long)g.n1 * g.n2 * g.n3;
   g.Ex = (long long)g.n1 * (g.n2 + 1) * (g.n3 + 1);
   g.Ey = (long long)(g.n1 + 1) * g.n2 * (g.n3 + 1);
@@ -194,11 +200,13 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_PT] = g.PT;
   v[MSFV_INFO_TB] = g.TB;
   v[MSFV_INFO_PC] = g.pc;
-  const bool tc = tc_supported(g);
+  const bool tc = use_tc(g);
   v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)lg_factor_doubles(g);
   v[MSFV_INFO_SCRATCH_DOUBLES] = tc ? (int64_t)tc_scratch_doubles(g) : 0;
   v[MSFV_INFO_TC] = tc ? 1 : 2;
   v[MSFV_INFO_COARSE] = g.coarse_nd;
+  v[MSFV_INFO_RED_FACE_DOUBLES] = g.reduced ? (int64_t)red_face_doubles(g) : 0;
+  v[MSFV_INFO_RED_BOX_DOUBLES] = g.reduced ? (int64_t)red_box_doubles(g) : 0;
   for (int i = 0; i < n && i < MSFV_INFO_COUNT; ++i) info[i] = v[i];
   return MSFV_OK;
 }
@@ -386,7 +394,7 @@ static int basis_build(const msfv_plan* plan, const double* w, double* factor, d
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g)) {
+  if (use_tc(g)) {
     msfv_plan* pl = const_cast<msfv_plan*>(plan);
     int rc = ensure_skel(pl);
     if (rc) return rc;
@@ -403,7 +411,7 @@ int msfv_basis_build(const msfv_plan* plan, const double* w, double* factor, dou
 int msfv_basis_forward(const msfv_plan* plan, const double* w, double* factor, double* Sint, double* Kloc,
                        int32_t* flags, void* stream) {
   CHECK_PARTITION(plan);
-  if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  if (!use_tc(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   return basis_build(plan, w, factor, Sint, Kloc, nullptr, flags, stream, false);
 }
 
@@ -411,7 +419,7 @@ int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* fact
                             int32_t* flags, int32_t bk0, int32_t bk1, void* stream) {
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
-  if (!tc_supported(g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  if (!use_tc(g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   if (bk0 < 0 || bk1 > g.nb3 || bk0 >= bk1) return fail(MSFV_SHAPE, "bad basis slab");
   msfv_plan* pl = const_cast<msfv_plan*>(plan);
   int rc = ensure_skel(pl);
@@ -424,7 +432,7 @@ int msfv_basis_forward_slab(const msfv_plan* plan, const double* w, double* fact
 
 int msfv_basis_backward(const msfv_plan* plan, const double* factor, double* Sint, void* stream) {
   CHECK_PARTITION(plan);
-  if (!tc_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
+  if (!use_tc(plan->g)) return fail(MSFV_UNSUPPORTED, "split basis build needs the tensor-core band path");
   return cuda_check(launch_basis_bwd(plan->g, factor, Sint, (cudaStream_t)stream), "basis_backward");
 }
 
@@ -496,7 +504,7 @@ int msfv_interior_solve(const msfv_plan* plan, const double* factor, const doubl
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
+  if (use_tc(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
   return cuda_check(launch_block_solve_lg(g, factor, rhs, out, nrhs, st), "interior_solve");
 }
 
@@ -534,7 +542,7 @@ int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, co
   CHECK_PARTITION(plan);
   if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
   const Geo& g = plan->g;
-  if (!tc_supported(g))
+  if (!use_tc(g))
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk,
                                             pts->d.nib, 1),
                       "points_interior_solve");
@@ -548,6 +556,7 @@ int msfv_block_gradient(const msfv_plan* plan, const double* sigma, const double
   CHECK_PARTITION(plan);
   if (nrhs < 0) return fail(MSFV_SHAPE, "bad gradient arguments");
   const Geo& gg = plan->g;
+  if (gg.reduced) return fail(MSFV_UNSUPPORTED, "derivatives of reduced boundary conditions are not built");
   if (!grad_supported(gg, nrhs)) return fail(MSFV_UNSUPPORTED, "block closure exceeds shared memory");
   const bool hz = pz && pz->d.nib > 0 && Zc, hr = pr && pr->d.nib > 0 && Rc;
   return cuda_check(launch_grad_block(gg, Sint, T, y, nrhs, sigma, hz ? pz->d.islot : nullptr, Zc,
@@ -601,7 +610,7 @@ int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const 
                              int32_t nrhs, void* stream) {
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
-  if (!tc_supported(g))
+  if (!use_tc(g))
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
                       "block_solve_compact");
   return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
@@ -631,6 +640,36 @@ int msfv_xk_present(const msfv_plan* plan, const double* z, int32_t* present, vo
 int msfv_xk_rowcount(const msfv_plan* plan, const int32_t* present, int64_t* counts, void* stream) {
   CHECK_PLAN(plan);
   return cuda_check(launch_xk_rowcount(plan->g, present, (long long*)counts, (cudaStream_t)stream), "xk_rowcount");
+}
+
+int msfv_plan_set_reduced(msfv_plan* plan, int32_t on) {
+  CHECK_PARTITION(plan);
+  if (on && !lg_supported(plan->g)) return fail(MSFV_UNSUPPORTED, "reduced boundary conditions need the L2 band solver");
+  plan->g.reduced = on ? 1 : 0;
+  plan->g.bx = nullptr;
+  return MSFV_OK;
+}
+
+int msfv_boundary_reduced(const msfv_plan* plan, const double* w, double* faces, double* bx, int32_t* flags,
+                          void* stream) {
+  CHECK_PARTITION(plan);
+  if (!plan->g.reduced) return fail(MSFV_SHAPE, "plan is not set up for reduced boundary conditions");
+  if (!w || !faces || !bx || !flags) return fail(MSFV_SHAPE, "bad reduced boundary arguments");
+  return cuda_check(launch_reduced_boundary(plan->g, w, faces, bx, flags, (cudaStream_t)stream), "boundary_reduced");
+}
+
+int msfv_plan_bind_boundary(msfv_plan* plan, const double* bx) {
+  CHECK_PARTITION(plan);
+  if (!plan->g.reduced) return fail(MSFV_SHAPE, "plan is not set up for reduced boundary conditions");
+  plan->g.bx = bx;
+  return MSFV_OK;
+}
+
+int msfv_basis_csc_box(int64_t nnz, const double* Sint, const int64_t* src, const int64_t* bsrc, const double* bx,
+                       double* vals, void* stream) {
+  return cuda_check(launch_basis_csc_box(nnz, Sint, (const long long*)src, (const long long*)bsrc, bx, vals,
+                                         (cudaStream_t)stream),
+                    "basis_csc_box");
 }
 
 int msfv_fine_apply(const msfv_plan* plan, const double* w, const double* X, int32_t nrhs, double* out,

@@ -53,6 +53,12 @@ struct Geo {
   const SkelEdge* skel;    // device table of the skeleton-only owned edges (msfv_basis_build)
   int nskel;
   int gtab8;               // 1: the 8^3 closure template (hats + edge table) is on the device (grad_template_init)
+  // reduced-dimension boundary conditions (msfv_reduced.cu): per-block closed-box
+  // skeleton values bx[block][corner][nbox] bound by msfv_plan_bind_boundary;
+  // nullptr: the trilinear hats (basis.py:84-116)
+  const double* bx;
+  int nbox;                // (b1+1)(b2+1)(b3+1)
+  int reduced;             // plan built for reduced boundary conditions
   // float reciprocals for division-free index decoding (see fdiv)
   float r_n1, r_n2, r_n1p, r_n2p, r_b1, r_b2, r_b3, r_ni1, r_ni2, r_nI, r_nb1, r_nb2;
 };
@@ -161,15 +167,22 @@ __host__ __device__ __forceinline__ int interior_index(const Geo& g, int x, int 
   return (x - 1) + g.ni1 * ((y - 1) + g.ni2 * (z - 1));
 }
 
+// Skeleton value of corner cc at local node (x, y, z) of block jb: the bound
+// reduced-boundary table, or the model-independent hat.
+__device__ __forceinline__ double skel_value(const Geo& g, int jb, int cc, int x, int y, int z) {
+  if (g.bx) return g.bx[((size_t)jb * 8 + cc) * g.nbox + x + (g.b1 + 1) * (y + (g.b2 + 1) * z)];
+  return hatf(g, cc, x, y, z);
+}
 // Basis value S(node, corner cc) of a node given in local coordinates of block
 // jb.  Interior values come from the per-block solve, skeleton values are the
-// model-independent hats, and the pinned global node 0 has no row (value 0).
-__device__ __forceinline__ double s_value(const Geo& g, const double* __restrict__ Sint_b,
+// hats (or the bound reduced-boundary values), and the pinned global node 0
+// has no row (value 0).
+__device__ __forceinline__ double s_value(const Geo& g, const double* __restrict__ Sint_b, int jb,
                                           int cc, int x, int y, int z, bool is_node0) {
   int a = interior_index(g, x, y, z);
   if (a >= 0) return Sint_b[(size_t)cc * g.nI + a];
   if (is_node0) return 0.0;
-  return hatf(g, cc, x, y, z);
+  return skel_value(g, jb, cc, x, y, z);
 }
 
 }  // namespace msfv

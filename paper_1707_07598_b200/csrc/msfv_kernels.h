@@ -71,6 +71,14 @@ cudaError_t launch_basis_lg(const Geo& g, const double* w, double* LT, double* S
 cudaError_t launch_block_solve_lg(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                   cudaStream_t st, const int* blist = nullptr, int nlist = 0, int compact = 0);
 
+// reduced-dimension boundary conditions (msfv_reduced.cu)
+size_t red_face_doubles(const Geo& g);
+size_t red_box_doubles(const Geo& g);
+cudaError_t launch_reduced_boundary(const Geo& g, const double* w, double* fv, double* bx, int* flags,
+                                    cudaStream_t st);
+cudaError_t launch_basis_csc_box(long long nnz, const double* Sint, const long long* src, const long long* bsrc,
+                                 const double* bx, double* vals, cudaStream_t st);
+
 // coarse (msfv_coarse.cu)
 cudaError_t launch_coarse_assemble(const Geo& g, const double* Kloc, double shift, double* Ak, cudaStream_t st);
 cudaError_t launch_coarse_factor(const Geo& g, double* Ak, int* flags, cudaStream_t st);

@@ -114,7 +114,8 @@ k_lg_factor(Geo g, const double* __restrict__ w, double* __restrict__ LT, double
         if (interior_index(g, xx, yy, zz) >= 0) return;
         if (has0 && xx == 0 && yy == 0 && zz == 0) return;
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) rhs[cc] += kc * hat_corner(cc, xx, yy, zz, g.b1, g.b2, g.b3);
+        for (int cc = 0; cc < 8; ++cc)
+          rhs[cc] += kc * (g.bx ? skel_value(g, jb, cc, xx, yy, zz) : hat_corner(cc, xx, yy, zz, g.b1, g.b2, g.b3));
       };
       add_nb(x - 1, y, z, kxm); add_nb(x + 1, y, z, kxp);
       add_nb(x, y - 1, z, kym); add_nb(x, y + 1, z, kyp);
@@ -386,7 +387,8 @@ k_lg_galerkin(Geo g, const double* __restrict__ w, const double* __restrict__ Si
     const bool n0 = has0 && x == 0 && y == 0 && z == 0;
     double ds[8];
 #pragma unroll
-    for (int cc = 0; cc < 8; ++cc) ds[cc] = s_value(g, Sb, cc, x1, y1, z1, false) - s_value(g, Sb, cc, x, y, z, n0);
+    for (int cc = 0; cc < 8; ++cc)
+      ds[cc] = s_value(g, Sb, jb, cc, x1, y1, z1, false) - s_value(g, Sb, jb, cc, x, y, z, n0);
 #pragma unroll
     for (int c1 = 0; c1 < 8; ++c1) {
       const double kd = kc * ds[c1];

@@ -24,7 +24,7 @@ __device__ __forceinline__ double point_s(const Geo& g, const PointsDev& P, cons
   decode_loc(P.loc[t], x, y, z);
   int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
   corner = corner_col(g, bi, bj, bk, cc);
-  return s_value(g, Sint + (size_t)jb * 8 * g.nI, cc, x, y, z, false);
+  return s_value(g, Sint + (size_t)jb * 8 * g.nI, jb, cc, x, y, z, false);
 }
 
 __global__ void k_points_receive(Geo g, PointsDev P, const double* __restrict__ Sint, const double* __restrict__ Y,

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_xk_values(Geo g, const double* __restri
   auto S_at = [&](int n, int cc) -> double {
     if (STAGED) return Sn[n * 8 + cc];
     const int x = n % B1, r = n / B1, y = r % B2, z = r / B2;
-    return s_value(g, Sb, cc, x, y, z, jb == 0 && n == 0);
+    return s_value(g, Sb, jb, cc, x, y, z, jb == 0 && n == 0);
   };
   auto Z_at = [&](int n) -> double {
     if (STAGED) return Zn[n];

@@ -96,8 +96,9 @@ class Points:
 
 
 class Engine:
-    def __init__(self, cells, h, blocks):
-        """blocks=None: geometry-only plan (fine-mesh entry points only)."""
+    def __init__(self, cells, h, blocks, reduced=False):
+        """blocks=None: geometry-only plan (fine-mesh entry points only);
+        reduced: reduced-dimension boundary conditions for the basis."""
         require_cuda()
         L = _lib.load()
         self.L = L
@@ -110,6 +111,10 @@ class Engine:
                                           (ctypes.c_int32 * 3)(*blocks), ctypes.byref(plan)), "plan_create")
         self.plan = plan
         self._fin = weakref.finalize(self, L.msfv_plan_destroy, plan)
+        self.reduced = bool(reduced)
+        if reduced:
+            _lib.check(L.msfv_plan_set_reduced(plan, 1), "plan_set_reduced")
+        self._bound = None
         info = (ctypes.c_int64 * _lib.INFO_COUNT)()
         _lib.check(L.msfv_plan_info(plan, info, _lib.INFO_COUNT))
         self.info = list(info)
@@ -418,6 +423,22 @@ class Engine:
                                                  stream()), "jv_coarse_rhs")
         return out
 
+    # ------------------------------------------------ reduced boundary values
+    def boundary_reduced(self, w, fl):
+        """Skeleton values of the reduced boundary problems (box table)."""
+        faces = self.empty(max(self.info[_lib.INFO_RED_FACE], 1))
+        bx = self.empty(max(self.info[_lib.INFO_RED_BOX], 1))
+        with phase("boundary_reduced"):
+            _lib.check(self.L.msfv_boundary_reduced(self.plan, ptr(w), ptr(faces), ptr(bx), ptr(fl), stream()),
+                       "boundary_reduced")
+        return bx
+
+    def bind_boundary(self, bx):
+        """Bind the box table the following launches read (reduced plans)."""
+        if self._bound is not bx:
+            _lib.check(self.L.msfv_plan_bind_boundary(self.plan, ptr(bx)), "plan_bind_boundary")
+            self._bound = bx
+
     # ------------------------------------------------------------ fine mesh
     def fine_apply(self, w, X, out=None):
         """A(w) X over all pinned nodes; X, out full node fields (Nn, nrhs)."""
@@ -445,6 +466,12 @@ class Engine:
         _lib.check(self.L.msfv_reg_faces(self.plan, ptr(d), ptr(o), stream()), "reg_faces")
         return o
 
+    def basis_csc_box(self, Sint, src, bsrc, bx):
+        vals = self.empty(src.numel())
+        _lib.check(self.L.msfv_basis_csc_box(src.numel(), ptr(Sint), ptr(src), ptr(bsrc), ptr(bx), ptr(vals),
+                                             stream()), "basis_csc_box")
+        return vals
+
     def basis_csc(self, Sint, src, hatv):
         vals = self.empty(src.numel())
         _lib.check(self.L.msfv_basis_csc(src.numel(), ptr(Sint), ptr(src), ptr(hatv), ptr(vals), stream()),
@@ -466,12 +493,16 @@ def engine_for_mesh(mesh):
     return eng
 
 
-def engine_for(partition):
+def engine_for(partition, reduced=False):
+    """The engine (plan) of a partition; ``reduced``: a separate plan whose
+    basis uses the reduced-dimension boundary conditions (msfv_reduced.cu)."""
     m = partition.mesh
     key = ((m.n1, m.n2, m.n3), (float(m.h1), float(m.h2), float(m.h3)),
            (partition.b1, partition.b2, partition.b3), torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    if reduced:
+        key = key + ("reduced",)
     eng = _ENGINES.get(key)
     if eng is None:
-        eng = Engine(*key[:3])
+        eng = Engine(*key[:3], reduced=reduced)
         _ENGINES[key] = eng
     return eng

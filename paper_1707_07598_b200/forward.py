@@ -175,6 +175,8 @@ def forward_reduced_dev(op, survey, basis, defer_check=False):
     local or coarse factorization failure) are resolved by ``state.check()``,
     which also takes the reference's diagonal-shift fallback (forward.py:122-129)."""
     eng = basis.engine
+    if basis.bx is not None:
+        eng.bind_boundary(basis.bx)          # reduced boundary values of this basis
     if op._dev is None or op._dev[0] is not eng:
         op.device_state(eng)
     if op._dev[1] is not basis._m_dev and not torch.equal(op._dev[1], basis._m_dev):
@@ -219,6 +221,9 @@ class AdaptiveSensitivity:
     def __init__(self, state, survey, workers=1):
         op, basis = state.op, state.basis
         eng = basis.engine
+        if basis.bx is not None:
+            raise NotImplementedError("derivatives through the reduced boundary problems are not built "
+                                      "(BasisSpec(boundary='reduced') serves the forward map only)")
         if not getattr(state, "deferred", False):
             state.check()
         if op._dev is None or op._dev[1] is not basis._m_dev:
