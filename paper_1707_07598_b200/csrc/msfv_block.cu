@@ -456,13 +456,12 @@ static bool edge_tile_ok(const Geo& g) {
 }
 static cudaError_t launch_edge_tile(const Geo& g, const double* cv, double* w, int k0, int k1, cudaStream_t st) {
   const size_t smem = (size_t)2 * (EWT_TY + 1) * (g.n1 + 2) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_edge_weights_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((size_t)2 * (EWT_TY + 1) * EWT_MAXW * sizeof(double)));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static PerDevice<cudaError_t> attr;
+  const cudaError_t ea = attr.get([] {
+    return cudaFuncSetAttribute(k_edge_weights_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)((size_t)2 * (EWT_TY + 1) * EWT_MAXW * sizeof(double)));
+  });
+  if (ea != cudaSuccess) return ea;
   const dim3 grid((g.n2 + 1 + EWT_TY - 1) / EWT_TY, k1 - k0 + 1);
   k_edge_weights_tile<<<grid, EWT_THREADS, smem, st>>>(g, cv, w, k0, k1);
   count_launches(1);

@@ -1550,15 +1550,15 @@ cudaError_t launch_coarse_dense(const Geo& g, const double* Kloc, double shift, 
 }
 
 static cudaError_t launch_factor_job(const FactorJob& job, int* flags, cudaStream_t st) {
-  static int coop_grid = -1;
-  if (coop_grid < 0) {
+  static PerDevice<int> grid_cache;
+  const int coop_grid = grid_cache.get([] {
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_factor, 256, 0);
-    coop_grid = (coop && per_sm > 0) ? sms : 0;
-  }
+    return (coop && per_sm > 0) ? sms : 0;
+  });
   if (coop_grid <= 0) return cudaErrorNotSupported;
   FactorJob j = job;
   void* args[] = {(void*)&j, (void*)&flags};
@@ -1718,7 +1718,8 @@ constexpr int MF_LEAF = 128;   // leaf boxes of <= 128 coarse nodes (tuned on co
 constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative kernels
 constexpr int MF_GR = 16;       // rows per item of the G products
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
-// explicit front inverse blocks (G) for one-product-per-front solves; MSFV_MF_G=0 keeps the staged sweeps
+// explicit front inverse blocks (G) give one-product-per-front solves where
+// the fronts fit the inverse-block budget (MfPlan::use_g); else staged sweeps
 // SMs left to the backward basis sweeps (k_basis_bwd, side stream) while the
 // multifrontal kernels run: the latency-bound coarse work keeps the rest
 int mf_reserved_sms() {
@@ -1728,22 +1729,6 @@ int mf_reserved_sms() {
     v = e ? std::max(0, atoi(e)) : 32;
   }
   return v;
-}
-static bool mf_two_phase() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MSFV_MF_2P");
-    v = e ? (atoi(e) != 0) : 0;
-  }
-  return v == 1;
-}
-static bool mf_use_g() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MSFV_MF_G");
-    v = e ? (atoi(e) != 0) : 1;
-  }
-  return v == 1;
 }
 
 struct MfFront {
@@ -2070,35 +2055,6 @@ __device__ __forceinline__ double mf_u(const Band& C, int r, int c) {
   const int a = max(r, c), b = min(r, c);
   return btile(C.A, C, b / TB, a / TB - b / TB)[(a % TB) * TB + (b % TB)];
 }
-// Front assembly of the fronts lvl[l0 .. l0 + gridDim.y): original entries with
-// a row or column in E, plus the children's update matrices (gathers).
-__device__ __forceinline__ void mf_assemble_elem(const Geo& g, const MfDev& d, const MfFront& F, long long t,
-                                                 const double* __restrict__ A27) {
-  const Band B = mf_band(d.base, F);
-  const int* gid = d.gid + F.goff;
-  const int lt = (int)(t / TT), e = (int)(t % TT);
-  int J = 0, rem = lt;
-  while (rem >= F.NT - J) {
-    rem -= F.NT - J;
-    ++J;
-  }
-  const int tt = rem;
-  const int r = (J + tt) * TB + e / TB, c = J * TB + e % TB;
-  const int gr = gid[r], gc = gid[c];
-  double v = 0.0;
-  if (gr < 0 || gc < 0) {
-    v = (r == c && r < F.NE * TB) ? 1.0 : 0.0;
-  } else {
-    if (r < F.nE || c < F.nE) v = mf_a(g, A27, gr, gc);
-    for (int k = 0; k < 2; ++k) {
-      if (F.c[k] < 0) continue;
-      const int* mk = d.maps + F.moff[k];
-      const int a = mk[r], b = mk[c];
-      if (a >= 0 && b >= 0) v += mf_u(mf_band(d.base, d.fr[F.c[k]]), a, b);
-    }
-  }
-  btile(B.A, B, J, tt)[e] = v;
-}
 // Tile-staged assembly: CTA (lower tile, front); the tile's 32 row and 32
 // column node ids, their coarse coordinates and child-map entries are staged
 // in shared memory once, each thread then assembles 4 elements.
@@ -2157,48 +2113,6 @@ __global__ void __launch_bounds__(256) k_mf_assemble_t(Geo g, MfDev d, int l0, c
     T[e] = v;
   }
 }
-__global__ void k_mf_assemble(Geo g, MfDev d, int l0, const double* __restrict__ A27) {
-  const MfFront F = d.fr[d.lvl[l0 + blockIdx.y]];
-  const Band B = mf_band(d.base, F);
-  const long long ntile = (long long)F.NT * F.NT;
-  const int* gid = d.gid + F.goff;
-  Band C0{}, C1{};
-  if (F.c[0] >= 0) C0 = mf_band(d.base, d.fr[F.c[0]]);
-  if (F.c[1] >= 0) C1 = mf_band(d.base, d.fr[F.c[1]]);
-  const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
-  const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
-  const long long nlow = (long long)F.NT * (F.NT + 1) / 2;   // lower tiles (J, tt), J + tt < NT
-  (void)ntile;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nlow * TT;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int lt = (int)(t / TT), e = (int)(t % TT);
-    // lt -> (J, tt): column J holds NT - J tiles
-    int J = 0, rem = lt;
-    while (rem >= F.NT - J) {
-      rem -= F.NT - J;
-      ++J;
-    }
-    const int tt = rem;
-    const int r = (J + tt) * TB + e / TB, c = J * TB + e % TB;
-    const int gr = gid[r], gc = gid[c];
-    double v = 0.0;
-    if (gr < 0 || gc < 0) {
-      v = (r == c && r < F.NE * TB) ? 1.0 : 0.0;
-    } else {
-      if (r < F.nE || c < F.nE) v = mf_a(g, A27, gr, gc);
-      if (m0) {
-        const int a = m0[r], b = m0[c];
-        if (a >= 0 && b >= 0) v += mf_u(C0, a, b);
-      }
-      if (m1) {
-        const int a = m1[r], b = m1[c];
-        if (a >= 0 && b >= 0) v += mf_u(C1, a, b);
-      }
-    }
-    btile(B.A, B, J, tt)[e] = v;
-  }
-}
-
 // Partial Cholesky (first NE tile columns) of all fronts of one level, one
 // grid barrier per tile column: CTA f (< nf) factors front f's diagonal tiles
 // (one-column lookahead), the other CTAs take the trailing tile tasks of all
@@ -2207,118 +2121,7 @@ struct MfJob {
   MfDev d;
   int l0, nf, jmax;
   Geo g;
-  const double* A27;    // non-null: assemble the level's fronts first (one grid barrier)
 };
-// Panel / update split for the fronts: per tile column, phase P stores the
-// panel tiles L_{J+t,J} = A_{J+t,J} Dinv_J^T once (Lo), grid barrier, phase U
-// applies A_{J+t1,J+t2} -= L_{J+t1,J} L_{J+t2,J}^T with one tile product per
-// task (the banded path's pair tasks recompute both panel tiles: 3 products).
-__device__ void mf_panel_task(const Band& B, int J, int t, FactorSmem& sm) {
-  const int lane = threadIdx.x & 31;
-  load_tile(sm.T, btile(B.A, B, J, t));
-  __syncthreads();
-  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X1, LDT, bi, bj, lane, c); });
-  __syncthreads();
-  store_tile(btile(B.Lo, B, J, t), sm.X1);
-  __syncthreads();
-}
-__device__ void mf_update_task(const Band& B, int J, int f, FactorSmem& sm) {
-  const int lane = threadIdx.x & 31;
-  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
-  while (t1 * (t1 - 1) / 2 > f) --t1;
-  while ((t1 + 1) * t1 / 2 <= f) ++t1;
-  const int t2 = f - t1 * (t1 - 1) / 2 + 1;
-  load_tile(sm.X1, btile(B.Lo, B, J, t1));
-  if (t2 != t1) load_tile(sm.X2, btile(B.Lo, B, J, t2));
-  __syncthreads();
-  const double* Y = (t2 != t1) ? sm.X2 : sm.X1;
-  double* G = btile(B.A, B, J + t2, t1 - t2);
-  const int wv = threadIdx.x >> 5;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
-    F2c c = frag(G, TB, bi, bj, lane), e = {0.0, 0.0};
-#pragma unroll
-    for (int kb = 0; kb < 4; kb += 2) {
-      const F2c a = frag(sm.X1, LDT, bi, kb, lane), a2 = frag(sm.X1, LDT, bi, kb + 1, lane);
-      mxyt(c, {-a.x, -a.y}, frag(Y, LDT, bj, kb, lane));
-      mxyt(e, {-a2.x, -a2.y}, frag(Y, LDT, bj, kb + 1, lane));
-    }
-    c.x += e.x;
-    c.y += e.y;
-    put(G, TB, bi, bj, lane, c);
-  }
-  __syncthreads();
-}
-__global__ void __launch_bounds__(256, 1) k_mf_factor2(MfJob job, int* __restrict__ flags) {
-  __shared__ __align__(16) FactorSmem sm;
-  __shared__ int pre[MF_MAXF + 1];
-  cg::grid_group grid = cg::this_grid();
-  const int nf = job.nf, G = (int)gridDim.x;
-  const bool split = nf < G;
-  auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
-  for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
-  grid.sync();
-  const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
-  for (int J = 0; J < job.jmax; ++J) {
-    // lookahead: pair (1,1) and the POTRF of column J+1 (dedicated CTAs)
-    for (int i = blockIdx.x; i < nf && (split ? blockIdx.x < nf : true); i += G) {
-      const MfFront F = front(i);
-      if (J + 1 < F.NE) {
-        const Band B = mf_band(job.d.base, F);
-        load_tile(sm.D, B.Dinv + (size_t)J * TT);
-        __syncthreads();
-        coarse_task(B, J, 0, sm, true);
-        coarse_potrf(B, J + 1, flags, sm, true);
-      }
-    }
-    for (int phase = 0; phase < 2; ++phase) {
-      if (me >= 0) {
-        for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-          const MfFront F = front(i);
-          int n = 0;
-          if (J < F.NE) {
-            const int pt = F.NT - 1 - J;
-            if (phase == 0) {
-              n = pt >= 1 ? pt : 0;
-            } else {
-              const int first = (pt >= 1 && J + 1 < F.NE) ? 1 : 0;
-              n = pt >= 1 ? pt * (pt + 1) / 2 - first : 0;
-            }
-          }
-          pre[i + 1] = n;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          pre[0] = 0;
-          for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
-        }
-        __syncthreads();
-        const int total = pre[nf];
-        int loaded = -1, fi = 0;
-        for (int gi = me; gi < total; gi += nw) {
-          while (pre[fi + 1] <= gi) ++fi;
-          const MfFront F = front(fi);
-          const Band B = mf_band(job.d.base, F);
-          if (phase == 0) {
-            if (loaded != fi) {
-              load_tile(sm.D, B.Dinv + (size_t)J * TT);
-              __syncthreads();
-              loaded = fi;
-            }
-            // the lookahead CTA computes panel tile 1 itself; storing it again is harmless
-            mf_panel_task(B, J, 1 + (gi - pre[fi]), sm);
-          } else {
-            const int first = (J + 1 < F.NE) ? 1 : 0;
-            mf_update_task(B, J, first + (gi - pre[fi]), sm);
-          }
-        }
-      }
-      grid.sync();
-    }
-  }
-}
-
 __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict__ flags) {
   __shared__ __align__(16) FactorSmem sm;
   __shared__ int pre[MF_MAXF + 1];
@@ -2326,32 +2129,6 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
   const int nf = job.nf, G = (int)gridDim.x;
   const bool split = nf < G;
   auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
-  if (job.A27) {
-    // level assembly (A_k entries + the children's update matrices), all CTAs
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-      const MfFront F = front(i);
-      pre[i + 1] = F.NT * (F.NT + 1) / 2 * TT;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      pre[0] = 0;
-      for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
-    }
-    __syncthreads();
-    const long long total = pre[nf];
-    int fi = 0;
-    MfFront F = front(0);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)G * blockDim.x) {
-      bool moved = false;
-      while (pre[fi + 1] <= t) {
-        ++fi;
-        moved = true;
-      }
-      if (moved) F = front(fi);
-      mf_assemble_elem(job.g, job.d, F, t - pre[fi], job.A27);
-    }
-    grid.sync();
-  }
   for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
   grid.sync();
   const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
@@ -3169,205 +2946,6 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
 // S_{pslot} at fixed rows (no atomics: each slot row has one writer); a
 // backward item reads [y_E; x_B] (x_B in Zb, written by the parent), writes
 // x_E to X and to its children's Zb rows.  Zb reuses the XE workspace.
-struct MfSolveJob2 {
-  MfDev d;
-  const int* lvl_off;
-  int nl, nfront;
-  long long vrows;
-  double* X;
-  double* W;            // 4 x vrows x nrhs: Vout | XE (Zb) | S0 | S1
-  int nrhs;
-};
-__global__ void __launch_bounds__(256, 1) k_mf_solve_coop2(MfSolveJob2 job) {
-  extern __shared__ __align__(16) double sh[];
-  __shared__ __align__(8) unsigned long long bar;
-  __shared__ int pre[MF_MAXF + 1];
-  cg::grid_group grid = cg::this_grid();
-  if (threadIdx.x == 0) mbar_init(&bar);
-  __syncthreads();
-  unsigned ph = 0;
-  const MfDev& d = job.d;
-  const int nrhs = job.nrhs;
-  const size_t ws = (size_t)job.vrows * nrhs;
-  double* Vout = job.W;
-  double* XE = Vout + ws;
-  double* S0 = XE + ws;
-  double* S1 = S0 + ws;
-  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
-  // ---- phase 0: XE = X on E rows, slots zero
-  (void)gtid;
-  (void)gstride;
-  for (int f = blockIdx.x; f < job.nfront; f += gridDim.x) {
-    const MfFront F = d.fr[f];
-    const size_t vo = (size_t)F.voff * nrhs;
-    const int* gid = d.gid + F.goff;
-#pragma unroll 4
-    for (int t = threadIdx.x; t < F.NT * TB * nrhs; t += blockDim.x) {
-      const int r = t / nrhs, s2 = t % nrhs;
-      XE[vo + t] = r < F.nE ? __ldcg(job.X + (size_t)gid[r] * nrhs + s2) : 0.0;
-      S0[vo + t] = 0.0;
-      S1[vo + t] = 0.0;
-    }
-  }
-  grid.sync();
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int li = 0; li < job.nl; ++li) {
-      const int l = pass == 0 ? li : job.nl - 1 - li;
-      const int l0 = job.lvl_off[l], nf = job.lvl_off[l + 1] - l0;
-      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const MfFront F = d.fr[d.lvl[l0 + i]];
-        pre[i + 1] = pass == 0 ? (F.NT * TB + MF_GR - 1) / MF_GR : (F.nE + MF_GR - 1) / MF_GR;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        pre[0] = 0;
-        for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
-      }
-      __syncthreads();
-      int fi = 0;
-      for (int gi = blockIdx.x; gi < pre[nf]; gi += gridDim.x) {
-        while (pre[fi + 1] <= gi) ++fi;
-        const MfFront F = d.fr[d.lvl[l0 + fi]];
-        const int rows = F.NT * TB, ncol = F.NE * TB;
-        const size_t vo = (size_t)F.voff * nrhs;
-        if (pass == 0) {
-          const int r0c = (gi - pre[fi]) * MF_GR, nr = min(MF_GR, rows - r0c);
-          const int kmax = r0c < ncol ? min(ncol, ((r0c + nr - 1) / TB + 1) * TB) : ncol;
-          double* Gs = sh;
-          double* vs = Gs + (size_t)MF_GR * ncol;          // XE rows [0, kmax)
-          double* v0s = vs + (size_t)ncol * nrhs;           // S0 rows [0, kmax)
-          double* v1s = v0s + (size_t)ncol * nrhs;          // S1 rows [0, kmax)
-          double* a0s = v1s + (size_t)ncol * nrhs;          // S0 rows of the chunk (B rows)
-          double* a1s = a0s + (size_t)MF_GR * nrhs;         // S1 rows of the chunk
-          const bool brow = r0c >= ncol;
-          if (threadIdx.x == 0) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            const unsigned bg = (unsigned)(nr * ncol * sizeof(double)), bv = (unsigned)(kmax * nrhs * sizeof(double));
-            const unsigned ba = brow ? (unsigned)(nr * nrhs * sizeof(double)) : 0u;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)),
-                         "r"(bg + 3 * bv + 2 * ba)
-                         : "memory");
-            auto cp = [&](void* dst, const void* src, unsigned bytes) {
-              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                               smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(&bar))
-                           : "memory");
-            };
-            cp(Gs, d.base + F.goff2 + (size_t)r0c * ncol, bg);
-            cp(vs, XE + vo, bv);
-            cp(v0s, S0 + vo, bv);
-            cp(v1s, S1 + vo, bv);
-            if (ba) {
-              cp(a0s, S0 + vo + (size_t)r0c * nrhs, ba);
-              cp(a1s, S1 + vo + (size_t)r0c * nrhs, ba);
-            }
-          }
-          mbar_wait(&bar, ph);
-          ph ^= 1;
-          // input = XE + S0 + S1 (fixed order); B rows add S0 + S1
-          for (int t = threadIdx.x; t < kmax * nrhs; t += blockDim.x) vs[t] = (vs[t] + v0s[t]) + v1s[t];
-          double* addv = a0s;
-          if (brow)
-            for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) a0s[t] = a0s[t] + a1s[t];
-          __syncthreads();
-          const int* up = d.maps + F.upoff;
-          double* pslot = nullptr;
-          size_t pvo = 0;
-          if (F.parent >= 0) {
-            pslot = F.pslot ? S1 : S0;
-            pvo = (size_t)d.fr[F.parent].voff * nrhs;
-          }
-          for (int t = threadIdx.x; t < nr * nrhs; t += blockDim.x) {
-            const int ii = t / nrhs, s2 = t % nrhs, r = r0c + ii;
-            const double* Gr = Gs + (size_t)ii * ncol;
-            const int kend = r < ncol ? min(ncol, (r / TB + 1) * TB) : ncol;
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            int k = 0;
-            for (; k + 3 < kend; k += 4) {
-              a0 = fma(Gr[k], vs[(size_t)k * nrhs + s2], a0);
-              a1 = fma(Gr[k + 1], vs[(size_t)(k + 1) * nrhs + s2], a1);
-              a2 = fma(Gr[k + 2], vs[(size_t)(k + 2) * nrhs + s2], a2);
-              a3 = fma(Gr[k + 3], vs[(size_t)(k + 3) * nrhs + s2], a3);
-            }
-            for (; k < kend; ++k) a0 = fma(Gr[k], vs[(size_t)k * nrhs + s2], a0);
-            double a = (a0 + a1) + (a2 + a3);
-            if (r < ncol) {
-              Vout[vo + (size_t)r * nrhs + s2] = a;
-            } else {
-              a += addv[(size_t)ii * nrhs + s2];
-              const int q = up[r];
-              if (pslot && q >= 0) pslot[pvo + (size_t)q * nrhs + s2] = a;
-            }
-          }
-        } else {
-          double* Zb = XE;
-          const int j0 = (gi - pre[fi]) * MF_GR, nj = min(MF_GR, F.nE - j0);
-          const int rz0 = (j0 / TB) * TB;
-          double* Gs = sh;
-          double* zs = Gs + (size_t)MF_GR * rows;
-          if (threadIdx.x == 0) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            const unsigned bg = (unsigned)(nj * rows * sizeof(double));
-            const unsigned be = (unsigned)((ncol - rz0) * nrhs * sizeof(double));
-            const unsigned bb = (unsigned)((rows - ncol) * nrhs * sizeof(double));
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(bg + be + bb)
-                         : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                             smem_u32(Gs)),
-                         "l"(d.base + F.goff2 + (size_t)F.NT * F.NE * TT + (size_t)j0 * rows), "r"(bg), "r"(smem_u32(&bar))
-                         : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                             smem_u32(zs + (size_t)rz0 * nrhs)), "l"(Vout + vo + (size_t)rz0 * nrhs), "r"(be),
-                         "r"(smem_u32(&bar))
-                         : "memory");
-            if (bb)
-              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                               smem_u32(zs + (size_t)ncol * nrhs)), "l"(Zb + vo + (size_t)ncol * nrhs), "r"(bb),
-                           "r"(smem_u32(&bar))
-                           : "memory");
-          }
-          mbar_wait(&bar, ph);
-          ph ^= 1;
-          const int* m0 = F.c[0] >= 0 ? d.maps + F.moff[0] : nullptr;
-          const int* m1 = F.c[1] >= 0 ? d.maps + F.moff[1] : nullptr;
-          const size_t c0o = m0 ? (size_t)d.fr[F.c[0]].voff * nrhs : 0, c1o = m1 ? (size_t)d.fr[F.c[1]].voff * nrhs : 0;
-          for (int t = threadIdx.x; t < nj * nrhs; t += blockDim.x) {
-            const int ii = t / nrhs, s2 = t % nrhs, j = j0 + ii;
-            const double* Gr = Gs + (size_t)ii * rows;
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            int r = rz0;
-            for (; r + 3 < rows; r += 4) {
-              a0 = fma(Gr[r], zs[(size_t)r * nrhs + s2], a0);
-              a1 = fma(Gr[r + 1], zs[(size_t)(r + 1) * nrhs + s2], a1);
-              a2 = fma(Gr[r + 2], zs[(size_t)(r + 2) * nrhs + s2], a2);
-              a3 = fma(Gr[r + 3], zs[(size_t)(r + 3) * nrhs + s2], a3);
-            }
-            for (; r < rows; ++r) a0 = fma(Gr[r], zs[(size_t)r * nrhs + s2], a0);
-            const double x = (a0 + a1) + (a2 + a3);
-            job.X[(size_t)d.gid[F.goff + j] * nrhs + s2] = x;
-            if (m0) { const int q = m0[j]; if (q >= 0) Zb[c0o + (size_t)q * nrhs + s2] = x; }
-            if (m1) { const int q = m1[j]; if (q >= 0) Zb[c1o + (size_t)q * nrhs + s2] = x; }
-          }
-          // this front's x_B rows travel on to its children (first chunk's CTA)
-          if (j0 == 0 && (m0 || m1)) {
-            for (int t = threadIdx.x; t < (rows - ncol) * nrhs; t += blockDim.x) {
-              const int p = ncol + t / nrhs, s2 = t % nrhs;
-              const double x = zs[(size_t)p * nrhs + s2];
-              if (m0) { const int q = m0[p]; if (q >= 0) Zb[c0o + (size_t)q * nrhs + s2] = x; }
-              if (m1) { const int q = m1[p]; if (q >= 0) Zb[c1o + (size_t)q * nrhs + s2] = x; }
-            }
-          }
-        }
-        __syncthreads();
-      }
-      grid.sync();
-    }
-  }
-}
-
-// Blocked sweeps for fronts too large for the explicit inverse (config 5):
-// CTA (front, group of <= MF_CC right-hand sides); the front vector of the
-// group lives in shared memory, L's tile column J streams through a buffer of
-// MF_LCH tiles (bulk copies), 2x2-blocked FMA products.
 constexpr int MF_CC = 8;
 constexpr int MF_LCH = 4;
 __device__ __forceinline__ void mf_tma_tiles(double* dst, const double* src, int ntile, unsigned long long* bar) {
@@ -3607,35 +3185,17 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
   cudaError_t e = mf_upload(g);
   if (e != cudaSuccess) return e;
   const MfPlan* P = mf_plan(g);
-  static int coop_grid = -1;
-  if (coop_grid < 0) {
+  static PerDevice<int> grid_cache;
+  const int coop_grid = grid_cache.get([] {
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (mf_two_phase())
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor2, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
-    coop_grid = (coop && per_sm > 0) ? std::max(1, sms - mf_reserved_sms()) * std::min(per_sm, 2) : 0;
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
+    return (coop && per_sm > 0) ? std::max(1, sms - mf_reserved_sms()) * std::min(per_sm, 2) : 0;
+  });
   if (coop_grid <= 0) return cudaErrorNotSupported;
   const MfDev d = mf_dev(g, Ak);
-  // helper stream + events for the inverse blocks (created once per process)
-  static cudaStream_t inv_stream = nullptr;
-  static cudaEvent_t mf_events[64], mf_done;
-  static int inv_mode = -1;
-  if (inv_mode < 0) {
-    const char* ev = getenv("MSFV_MF_INV_SIDE");
-    inv_mode = ev ? (atoi(ev) != 0) : 0;   // opt-in: no gain at config 4, occasional placement stalls
-    if (inv_mode) {
-      cudaError_t e2 = cudaStreamCreateWithFlags(&inv_stream, cudaStreamNonBlocking);
-      for (int i = 0; i < 64 && e2 == cudaSuccess; ++i) e2 = cudaEventCreateWithFlags(&mf_events[i], cudaEventDisableTiming);
-      if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&mf_done, cudaEventDisableTiming);
-      if (e2 != cudaSuccess) inv_mode = 0;
-    }
-  }
-  const bool inv_side = inv_mode == 1 && P->lvl_off.size() <= 65;
   for (size_t l = 0; l + 1 < P->lvl_off.size(); ++l) {
     const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0;
     if (nf <= 0) continue;
@@ -3645,55 +3205,31 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
       jmax = std::max(jmax, P->fr[P->lvl[l0 + i]].NE);
       ntmax = std::max(ntmax, P->fr[P->lvl[l0 + i]].NT);
     }
-    // assembly inside the cooperative launch (one fewer launch per level) is
-    // slower at config 4/5 (fewer threads on the gathers): opt-in only
-    const bool fold = !mf_two_phase() && getenv("MSFV_MF_FOLD_ASSEMBLY");
-    if (!fold) {
-      k_mf_assemble_t<<<dim3(ntmax * (ntmax + 1) / 2, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
-      count_launches(1);
-    }
-    MfJob job{d, l0, nf, jmax, g, fold ? Ak + P->a27 : nullptr};
+    k_mf_assemble_t<<<dim3(ntmax * (ntmax + 1) / 2, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
+    count_launches(1);
+    MfJob job{d, l0, nf, jmax, g};
     void* args[] = {(void*)&job, (void*)&flags};
-    e = cudaLaunchCooperativeKernel(mf_two_phase() ? (void*)k_mf_factor2 : (void*)k_mf_factor, dim3(coop_grid),
-                                    dim3(256), args, 0, st);
+    e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
     count_launches(1);
     if (e != cudaSuccess) return e;
-    if (mf_use_g() && P->use_g) {
+    if (P->use_g) {
       int nemax = 1, nbmax = 0;
       for (int i = 0; i < nf; ++i) {
         nemax = std::max(nemax, P->fr[P->lvl[l0 + i]].NE);
         nbmax = std::max(nbmax, P->fr[P->lvl[l0 + i]].NT - P->fr[P->lvl[l0 + i]].NE);
       }
       const size_t smi = ((size_t)nemax * TB * TB + 3 * TT) * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        e = cudaFuncSetAttribute(k_mf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
+      static PerDevice<cudaError_t> attr;
+      e = attr.get([] { return cudaFuncSetAttribute(k_mf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX); });
+      if (e != cudaSuccess) return e;
       if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
-      // the inverse blocks of level l run on a helper stream beside the
-      // factorization of level l + 1 (they are needed only by the solves;
-      // their small grids land on the SMs the coarse kernels leave free)
-      cudaStream_t si = st;
-      if (inv_side) {
-        e = cudaEventRecord(mf_events[l], st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(inv_stream, mf_events[l], 0);
-        if (e != cudaSuccess) return e;
-        si = inv_stream;
-      }
-      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, si>>>(d, l0);
+      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, st>>>(d, l0);
       count_launches(1);
       if (nbmax > 0) {
-        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, si>>>(d, l0, nbmax);
+        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, st>>>(d, l0, nbmax);
         count_launches(1);
       }
     }
-  }
-  if (inv_side && mf_use_g() && P->use_g) {
-    e = cudaEventRecord(mf_done, inv_stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, mf_done, 0);
-    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -3723,52 +3259,41 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
   auto smem_c = [&](int nt) {
     return ((size_t)nt * TB * MF_CC + (size_t)2 * MF_LCH * TT + TT + (size_t)TB * MF_CC) * sizeof(double);
   };
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_mf_fwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_fwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  if (mf_use_g() && P->use_g && nrhs <= 64 && !force_c) {
+  static PerDevice<cudaError_t> attr;
+  e = attr.get([] {
+    cudaError_t r = cudaFuncSetAttribute(k_mf_fwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_mf_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_mf_fwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(k_mf_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
+    return r;
+  });
+  if (e != cudaSuccess) return e;
+  if (P->use_g && nrhs <= 64 && !force_c) {
     // one cooperative launch for both sweeps
-    size_t smc = 0, smc2 = 0;
+    size_t smc = 0;
     for (int l = 0; l < nl; ++l) {
       const int nt = level_nt(l);
       smc = std::max(smc, ((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs + (size_t)MF_GR * nrhs) * sizeof(double));
-      smc2 = std::max(smc2, ((size_t)MF_GR * nt * TB + (size_t)3 * nt * TB * nrhs + (size_t)2 * MF_GR * nrhs) *
-                                sizeof(double));
     }
-    static int coop_grid = -1;
-    if (coop_grid < 0) {
+    static PerDevice<int> grid_cache;
+    const int coop_grid = grid_cache.get([] {
       int dev = 0, sms = 0, coop = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-      e = cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 24576);
-      if (e != cudaSuccess) return e;
-      coop_grid = coop ? std::max(1, sms - mf_reserved_sms()) : 0;
-    }
+      if (cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 24576) !=
+          cudaSuccess)
+        return 0;
+      return coop ? std::max(1, sms - mf_reserved_sms()) : 0;
+    });
     if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 24576 && !getenv("MSFV_MF_NOCOOP")) {
-      if (getenv("MSFV_MF_SCATTER") && smc2 <= (size_t)MF_SMEM_MAX - 8192) {   // scatter variant: fewer barriers, slower at config 4
-        static bool a2 = false;
-        if (!a2) {
-          e = cudaFuncSetAttribute(k_mf_solve_coop2, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 8192);
-          if (e != cudaSuccess) return e;
-          a2 = true;
-        }
-        MfSolveJob2 job2{d, P->d_lvloff, nl, (int)P->fr.size(), (long long)P->vrows, X, scratch, nrhs};
-        void* args2[] = {(void*)&job2};
-        e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop2, dim3(coop_grid), dim3(256), args2, smc2, st);
-        count_launches(1);
-        if (e != cudaSuccess) return e;
-        return cudaGetLastError();
-      }
-      static unsigned long long* tst = nullptr;
       const bool timing = getenv("MSFV_MF_TIMING") != nullptr;
-      if (timing && !tst) cudaMalloc(&tst, 256 * sizeof(unsigned long long));
+      static PerDevice<unsigned long long*> tst_cache;
+      unsigned long long* tst = timing ? tst_cache.get([] {
+        unsigned long long* p = nullptr;
+        cudaMalloc(&p, 256 * sizeof(unsigned long long));
+        return p;
+      }) : nullptr;
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
                      P->npre};
       void* args[] = {(void*)&job};
@@ -3792,14 +3317,14 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
     const int nt = level_nt(l);
     if (((size_t)MF_GR * nt * TB + (size_t)nt * TB * nrhs) * sizeof(double) > (size_t)MF_SMEM_MAX) g_fits = false;
   }
-  if (mf_use_g() && P->use_g && g_fits) {
-    static bool gattr = false;
-    if (!gattr) {
-      e = cudaFuncSetAttribute(k_mf_gfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_mf_gbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
-      if (e != cudaSuccess) return e;
-      gattr = true;
-    }
+  if (P->use_g && g_fits) {
+    static PerDevice<cudaError_t> gattr;
+    e = gattr.get([] {
+      cudaError_t r = cudaFuncSetAttribute(k_mf_gfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k_mf_gbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX);
+      return r;
+    });
+    if (e != cudaSuccess) return e;
     for (int l = 0; l < nl; ++l) {
       const int l0 = P->lvl_off[l], nf = P->lvl_off[l + 1] - l0, nt = level_nt(l);
       int ne = 1;

@@ -1,10 +1,33 @@
 // Internal launcher declarations (not part of the public C-ABI).
 #pragma once
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include "msfv_common.cuh"
 
 namespace msfv {
+
+// A lazily initialised per-device value (function attributes, occupancy-
+// derived grid sizes, helper allocations): keyed by the current device and
+// initialised once under a mutex, so several devices or host threads in one
+// process each get their own, race-free.
+template <class T>
+struct PerDevice {
+  std::mutex mu;
+  std::unordered_map<int, T> vals;
+  template <class F>
+  T get(F&& init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = vals.find(dev);
+    if (it != vals.end()) return it->second;
+    T v = init();
+    vals.emplace(dev, v);
+    return v;
+  }
+};
 
 constexpr int RESTRICT_THREADS = 128;
 constexpr int COARSE_TB = 32;

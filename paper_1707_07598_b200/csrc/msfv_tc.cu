@@ -1220,7 +1220,7 @@ template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
                                      double* Kloc, int* flags, bool bwd, cudaStream_t st, int jb0, int jb1) {
   cudaError_t e;
-  const bool lines = g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2 && !getenv("MSFV_SKEL_GENERIC");
+  const bool lines = g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2;   // k_skel_galerkin: blocks one cell thick
   const int rec_max = skel_lines_axis(g.b2, g.b3, 1, 1) + skel_lines_axis(g.b1, g.b3, 1, 1) +
                       skel_lines_axis(g.b1, g.b2, 1, 1) + 3;
   const size_t skl_sm = (size_t)SKL_WARPS * rec_max * 16 * sizeof(double);
