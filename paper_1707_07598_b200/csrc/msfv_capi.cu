@@ -610,7 +610,10 @@ int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const 
                              int32_t nrhs, void* stream) {
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
-  if (!use_tc(g))
+  // wide solves (apply_Yk: one right-hand side per block cell) take the
+  // CTA-per-block kernel that stages each factor tile column once for up to
+  // 128 right-hand sides (the register-window kernel re-reads the factor per 16)
+  if (!use_tc(g) || nrhs >= 64)
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
                       "block_solve_compact");
   return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),

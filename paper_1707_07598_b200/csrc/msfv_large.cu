@@ -35,7 +35,7 @@ using namespace dmma;
 
 constexpr int LGF_WARPS = 16;
 constexpr int LGF_BATCH = 8;
-constexpr int LGS_MAX_WARPS = 8;
+constexpr int LGS_MAX_WARPS = 16;
 constexpr int LGG_THREADS = 128;
 
 __device__ __forceinline__ F2 lds2(const double* p) { return {p[0], p[1]}; }
@@ -254,7 +254,7 @@ size_t lg_factor_smem(int PT) {
 // rows [corner][a] (8 right-hand sides).  fwd = 0: the input already holds
 // y = L^{-1} r (backward sweep only).  out may alias rhs.
 template <int MODE>
-__global__ void k_lg_solve(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs,
+__global__ void __launch_bounds__(LGS_MAX_WARPS * 32) k_lg_solve(Geo g, const double* __restrict__ LT, const double* rhs, double* out, int nrhs,
                            const int* __restrict__ blist, int PT, int fwd) {
   extern __shared__ __align__(16) double ssm[];
   const int slot = blockIdx.x;
@@ -433,7 +433,13 @@ cudaError_t launch_solve_mode(const Geo& g, const double* LT, const double* rhs,
 
 }  // namespace
 
-int lg_band(const Geo& g) { return (g.p + 7) / 8; }
+// same as tc_band: the two paths share the factor layout, so either solve
+// kernel can consume either factor
+int lg_band(const Geo& g) {
+  const int nti = (g.nI + 7) / 8;
+  if (nti == 0) return 0;
+  return std::min((g.p + 7) / 8, nti - 1);
+}
 
 bool lg_supported(const Geo& g) {
   const int PT = lg_band(g);

@@ -157,7 +157,9 @@ class Engine:
                 t = t.to(F64)
             t = t.to(self.device, non_blocking=True)
         else:
-            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.device, non_blocking=True)
+            h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            # a page-locked source (e.g. misfit_ssd's residual) copies asynchronously
+            t = h.to(self.device, non_blocking=True)
         return t.contiguous()
 
     # ------------------------------------------------------------- kernels
