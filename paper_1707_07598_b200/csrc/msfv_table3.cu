@@ -71,10 +71,16 @@ __global__ void k_yk_rowcount(Geo g, const unsigned* __restrict__ mask, long lon
   counts[r] = c;
 }
 
-// CSR scatter of -sol (one thread per (block, interior node); columns ascending)
-__global__ void k_yk_scatter(Geo g, const unsigned* __restrict__ mask, const double* __restrict__ sol,
-                             const long long* __restrict__ indptr, int* __restrict__ indices, double* __restrict__ vals) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+// CSR scatter of -sol: one warp per (block, interior node) row; the lanes take
+// 32 consecutive cells at a time and place the masked ones with a ballot
+// prefix count, so the row's entries (ascending columns) are written by
+// consecutive lanes to consecutive addresses.
+constexpr int YKS_WARPS = 4;
+__global__ void __launch_bounds__(YKS_WARPS * 32)
+k_yk_scatter(Geo g, const unsigned* __restrict__ mask, const double* __restrict__ sol,
+             const long long* __restrict__ indptr, int* __restrict__ indices, double* __restrict__ vals) {
+  const long long t = (long long)blockIdx.x * YKS_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (t >= (long long)g.nbl * g.nI) return;
   const int jb = (int)(t / g.nI), a = (int)(t - (long long)jb * g.nI);
   const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
@@ -85,12 +91,19 @@ __global__ void k_yk_scatter(Geo g, const unsigned* __restrict__ mask, const dou
   long long p = indptr[r];
   const unsigned* mk = mask + (size_t)jb * mask_words(g);
   const double* srow = sol + ((size_t)jb * g.nI + a) * ncell_b(g);
-  for (int lc = 0; lc < ncell_b(g); ++lc) {
-    if (!((mk[lc >> 5] >> (lc & 31)) & 1u)) continue;
-    const int cx = lc % g.b1, q = lc / g.b1, cy = q % g.b2, cz = q / g.b2;
-    indices[p] = (int)cell_id(g, (long long)bi * g.b1 + cx, (long long)bj * g.b2 + cy, (long long)bk * g.b3 + cz);
-    vals[p] = -srow[lc];
-    ++p;
+  const int ncb = ncell_b(g);
+  const unsigned below = (1u << lane) - 1u;
+  for (int base = 0; base < ncb; base += 32) {
+    const int lc = base + lane;
+    const bool on = lc < ncb && ((mk[lc >> 5] >> (lc & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (on) {
+      const long long q = p + __popc(bal & below);
+      const int cx = lc % g.b1, qq = lc / g.b1, cy = qq % g.b2, cz = qq / g.b2;
+      indices[q] = (int)cell_id(g, (long long)bi * g.b1 + cx, (long long)bj * g.b2 + cy, (long long)bk * g.b3 + cz);
+      vals[q] = -srow[lc];
+    }
+    p += __popc(bal);
   }
 }
 
@@ -243,7 +256,7 @@ cudaError_t launch_yk_scatter(const Geo& g, const unsigned* mask, const double* 
                               int* indices, double* vals, cudaStream_t st) {
   const long long tot = (long long)g.nbl * g.nI;
   if (tot == 0) return cudaSuccess;
-  k_yk_scatter<<<nblk(tot, 128), 128, 0, st>>>(g, mask, sol, indptr, indices, vals);
+  k_yk_scatter<<<nblk(tot, YKS_WARPS), YKS_WARPS * 32, 0, st>>>(g, mask, sol, indptr, indices, vals);
   count_launches(1);
   return cudaGetLastError();
 }
