@@ -617,7 +617,7 @@ def run_gpu(args, rank, world, log):
     # compulsory bytes of the basis construction: read the edge
     # weights, write S_I and the local Galerkin blocks
     compulsory = int(eng.E * 8 + eng.nbl * 8 * nI * 8 + eng.nbl * 64 * 8)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, dmma_pct = None, None, None
     for prof_name in ("r02_ncu.json", "r01c_ncu.json"):
         try:
             # dram__bytes_read.sum + dram__bytes_write.sum of k_basis_tc from the
@@ -627,6 +627,8 @@ def run_gpu(args, rank, world, log):
             if args.config == 4:
                 traffic = int(kb["dram_read_B"] + kb["dram_write_B"])
                 traffic_src = f"profiles/{prof_name} (ncu --set full, k_basis_tc, bytes per launch)"
+                if "dmma_pipe_pct" in kb:
+                    dmma_pct = round(kb["dmma_pipe_pct"], 1)
             break
         except Exception:  # noqa: BLE001
             continue
@@ -639,6 +641,10 @@ def run_gpu(args, rank, world, log):
             "algorithmic_bytes_what": "compulsory: edge weights in, S_I and Kloc out (SURVEY 8d)",
             "flops_per_block": fl_fwd, "blocks_per_launch": eng.nbl, "launch_ms": round(t_basis * 1e3, 4),
             "peak_source": peak_src,
+            "dmma_pipe_active_pct": dmma_pct,
+            "dmma_pipe_note": "ncu sm__pipe_tensor_subpipe_dmma_cycles_active / cycles of the same capture: the FP64 "
+                              "tensor pipe's occupancy including the tile padding of the band (useful flops are "
+                              "the frac above)",
             "whole_build": {"ms": round(t_whole * 1e3, 4), "flops_per_block": fl_whole,
                             "achieved": round(fl_whole * eng.nbl / t_whole / 1e12, 3),
                             "frac": round(fl_whole * eng.nbl / t_whole / 1e12 / peak, 4),

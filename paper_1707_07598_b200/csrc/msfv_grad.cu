@@ -15,6 +15,8 @@
 // memory (interior from Sint, skeleton from the hats), xi is formed for the
 // closure edges and the block's own cells gather their 12 edges, so the
 // gradient is one pass over Sint with no node-field traffic.
+#include <algorithm>
+#include <cstdlib>
 #include "msfv_common.cuh"
 #include "msfv_kernels.h"
 
@@ -486,15 +488,202 @@ cudaError_t launch_jv_block(const Geo& g, const double* Sint, const double* cvec
 
 bool grad_supported(const Geo& g, int nrhs) { return grad_smem_doubles(g, nrhs) * sizeof(double) <= 200 * 1024; }
 
+// ---------------------------------------------------------------------------
+// 8^3 blocks without interior survey nodes (every BASELINE 3D config): a
+// persistent form.  Each CTA (16 warps, two per SM) keeps the closure hats and
+// the edge table in shared memory for all its blocks (one template copy per
+// CTA instead of per block) and streams the blocks: the next block's interior
+// basis values (8 x 343 doubles, one contiguous 21 952-byte run of Sint) and
+// its 512 cell conductivities arrive by bulk / cp.async copies while the
+// current block's xi and cell gather run, so the HBM reads overlap compute.
+namespace {
+constexpr int GP_NI = 343, GP_SINT = 8 * GP_NI;
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(g_smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   g_smem_u32(dst)), "l"(src), "r"(bytes), "r"(g_smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(g_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(g_smem_u32(smem)), "l"(gmem));
+}
+}  // namespace
+
+size_t grad8p_smem_bytes(int nrhs) {
+  return ((size_t)TPL_NN * 8 + TPL_NE + GP_SINT + 512 + 16 * (size_t)nrhs + 64) * sizeof(double) +
+         TPL_NEP * sizeof(int) + 64;
+}
+
+__global__ void __launch_bounds__(GRAD_T8, 2)
+k_grad_block8p(Geo g, const double* __restrict__ Sint, const double* __restrict__ T, const double* __restrict__ Y,
+               int nrhs, const double* __restrict__ sigma, double* __restrict__ gout, int jb0, int nb) {
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ __align__(8) unsigned long long bars[2];   // 0: template, 1: next block's Sint
+  constexpr int B1 = 9, B2 = 9, NEx = 8 * 81, NEy = 8 * 81, NE = TPL_NE;
+  double* Sn = gsm;                               // [729][8] closure basis values (hats + interior)
+  double* xi = Sn + TPL_NN * 8;                   // [1944]
+  double* St = xi + NE;                           // [8][343] staged Sint of the next block
+  double* Sg = St + GP_SINT;                      // [512] staged sigma of the next block (x fastest)
+  double* Tj = Sg + 512;                          // [8][nrhs]
+  double* Yj = Tj + 8 * nrhs;                     // [8][nrhs]
+  double* M = Yj + 8 * nrhs;                      // [64]
+  int* Et = reinterpret_cast<int*>(M + 64);       // [TPL_NEP]
+  const int tid = threadIdx.x, lane = tid & 31, wv = tid >> 5, m = lane >> 2, q = lane & 3;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g_smem_u32(&bars[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(g_smem_u32(&bars[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  int k = blockIdx.x;                             // local block index: jb = jb0 + k
+  if (k >= nb) return;
+  auto stage_next = [&](int kk) {                 // thread 0: Sint run; all threads: sigma rows (cp.async)
+    const int jb = jb0 + kk;
+    if (tid == 0) {
+      expect_tx(&bars[1], GP_SINT * sizeof(double));
+      bulk_g2s(St, Sint + (size_t)jb * GP_SINT, GP_SINT * sizeof(double), &bars[1]);
+    }
+    int bi, bj, bk;
+    decode3f(jb, g.nb1, g.r_nb1, g.nb2, g.r_nb2, bi, bj, bk);
+    if (tid < 256) {                              // 64 rows of 8 cells, 4 x 16 bytes each
+      const int row = tid >> 2, part = tid & 3, y = row & 7, z = row >> 3;
+      const long long cid = cell_id(g, bi * 8, bj * 8 + y, bk * 8 + z);
+      cp_async16(Sg + row * 8 + part * 2, sigma + cid + part * 2);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (tid == 0) {
+    expect_tx(&bars[0], TPL_NN * 8 * sizeof(double) + TPL_NEP * sizeof(int));
+    bulk_g2s(Sn, g_tpl8_sn, TPL_NN * 8 * sizeof(double), &bars[0]);
+    bulk_g2s(Et, g_tpl8_et, TPL_NEP * sizeof(int), &bars[0]);
+  }
+  stage_next(k);
+  mbar_wait(&bars[0], 0);
+  const double ihx[3] = {g.ih1 * g.ih1, g.ih2 * g.ih2, g.ih3 * g.ih3};
+  unsigned par = 0;
+  for (; k < nb; k += gridDim.x) {
+    const int jb = jb0 + k;
+    int bi, bj, bk;
+    decode3f(jb, g.nb1, g.r_nb1, g.nb2, g.r_nb2, bi, bj, bk);
+    for (int i = tid; i < 8 * nrhs; i += blockDim.x) {
+      const int cc = i & 7, s = i >> 3;
+      const size_t col = (size_t)corner_col(g, bi, bj, bk, cc);
+      Tj[cc * nrhs + s] = T[col * nrhs + s];
+      Yj[cc * nrhs + s] = Y[col * nrhs + s];
+    }
+    mbar_wait(&bars[1], par);
+    par ^= 1u;
+    // interior basis values into the closure (the hats stay from the template)
+    for (int a = tid; a < GP_NI; a += blockDim.x) {
+      const int x = a % 7, r = a / 7, y = r % 7, z = r / 7;
+      double* d = Sn + ((x + 1) + 9 * ((y + 1) + 9 * (z + 1))) * 8;
+#pragma unroll
+      for (int cc = 0; cc < 8; cc += 2) *reinterpret_cast<double2*>(d + cc) = make_double2(St[cc * GP_NI + a], St[(cc + 1) * GP_NI + a]);
+    }
+    if (jb == 0 && tid < 8) Sn[tid] = 0.0;        // pinned node: no row of S
+    __syncthreads();                              // St consumed; Tj/Yj/Sn ready
+    const int knext = k + gridDim.x;
+    // M = Tj Yj^T (warp 0) while the next block's copies start
+    if (tid < 32) {
+      double c0 = 0.0, c1 = 0.0;
+      for (int s0 = 0; s0 < nrhs; s0 += 4) {
+        const bool ok = s0 + q < nrhs;
+        const double a = ok ? Tj[m * nrhs + s0 + q] : 0.0, b = ok ? Yj[m * nrhs + s0 + q] : 0.0;
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+      }
+      M[m * 8 + 2 * q] = c0;
+      M[m * 8 + 2 * q + 1] = c1;
+    }
+    __syncthreads();
+    // sigma of this block (cp.async group of the previous stage) is needed by the
+    // gather below; the next block's Sint bulk copy goes out now
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    double sg = 0.0;
+    {
+      const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
+      sg = Sg[(y + 8 * z) * 8 + x];
+    }
+    __syncthreads();                              // everyone has its sigma: Sg may be refilled
+    if (knext < nb) stage_next(knext);
+    const double mt0 = M[(2 * q) * 8 + m], mt1 = M[(2 * q + 1) * 8 + m];
+#pragma unroll 4
+    for (int it = 0; it < TPL_NEP / (8 * (GRAD_T8 / 32)); ++it) {
+      const int e = (it * (GRAD_T8 / 32) + wv) * 8 + m;
+      const int pk = Et[e], ax = pk >> 24, na = pk & 0xFFFFFF;
+      const int nbn = na + (ax == 0 ? 1 : (ax == 1 ? 9 : 81));
+      const double ihs = ax == 0 ? ihx[0] : (ax == 1 ? ihx[1] : ihx[2]);
+      const double2 sb = *reinterpret_cast<const double2*>(Sn + nbn * 8 + 2 * q);
+      const double2 sa = *reinterpret_cast<const double2*>(Sn + na * 8 + 2 * q);
+      const double d0 = sb.x - sa.x, d1 = sb.y - sa.y;
+      double c0 = 0.0, c1 = 0.0;
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c0), "+d"(c1) : "d"(d0), "d"(mt0));
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c0), "+d"(c1) : "d"(d1), "d"(mt1));
+      double v = c0 * d0 + c1 * d1;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (q == 0 && e < NE) xi[e] = v * ihs;
+    }
+    __syncthreads();
+    if (jb == 0 && tid < 8) Sn[tid] = g_tpl8_sn[tid];   // restore the template's node-0 hats
+    {
+      const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
+      const double* xx = xi;
+      const double* xy = xi + NEx;
+      const double* xz = xi + NEx + NEy;
+      auto ex = [&](int i, int j, int kk) { return xx[i + 8 * (j + B2 * kk)]; };
+      auto ey = [&](int i, int j, int kk) { return xy[i + B1 * (j + 8 * kk)]; };
+      auto ez = [&](int i, int j, int kk) { return xz[i + B1 * (j + B2 * kk)]; };
+      const double tx = (ex(x, y, z) + ex(x, y + 1, z)) + (ex(x, y, z + 1) + ex(x, y + 1, z + 1));
+      const double ty = (ey(x, y, z) + ey(x + 1, y, z)) + (ey(x, y, z + 1) + ey(x + 1, y, z + 1));
+      const double tz = (ez(x, y, z) + ez(x + 1, y, z)) + (ez(x, y + 1, z) + ez(x + 1, y + 1, z));
+      const double tot = (tx + ty) + tz;
+      const long long cid = cell_id(g, bi * 8 + x, bj * 8 + y, bk * 8 + z);
+      gout[cid] = -sg * (g.qv * tot);
+    }
+    __syncthreads();                              // xi / Tj / Yj reused by the next block
+  }
+}
+
 cudaError_t launch_grad_block(const Geo& g, const double* Sint, const double* T, const double* Y, int nrhs,
                               const double* sigma, const int* zslot, const double* Zc, const int* rslot,
                               const double* Rc, double* gout, cudaStream_t st, int jb0, int nb) {
+  if (nb < 0) nb = g.nbl - jb0;
+  if (nb <= 0) return cudaSuccess;
+  if (g.gtab8 && !zslot && !rslot && !getenv("MSFV_GRAD_NONPERSISTENT")) {
+    const size_t sm8 = grad8p_smem_bytes(nrhs);
+    static PerDevice<int> sms_cache;
+    const int sms = sms_cache.get([] {
+      int dev = 0, n = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n;
+    });
+    cudaError_t e8 = cudaFuncSetAttribute(k_grad_block8p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8);
+    if (e8 != cudaSuccess) return e8;
+    const int grid = std::min(nb, 2 * sms);
+    k_grad_block8p<<<grid, GRAD_T8, sm8, st>>>(g, Sint, T, Y, nrhs, sigma, gout, jb0, nb);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   const size_t smem = grad_smem_doubles(g, nrhs) * sizeof(double);
   auto kern = g.gtab8 ? k_grad_block<8> : k_grad_block<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (nb < 0) nb = g.nbl - jb0;
-  if (nb <= 0) return cudaSuccess;
   kern<<<nb, g.gtab8 ? GRAD_T8 : GRAD_THREADS, smem, st>>>(g, Sint, T, Y, nrhs, sigma, zslot, Zc, rslot, Rc, gout, jb0);
   count_launches(1);
   return cudaGetLastError();

@@ -796,7 +796,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   F2 K = {0.0, 0.0};
   if constexpr (OM != 0) {
     galerkin_faces7(g, Fk, lane, K);
-  } else {
+  } else if (NTI > 0) {   // blocks one cell thick along an axis have no interior: no boundary-interior edges
 #pragma unroll 1
   for (int face = 0; face < 6; ++face) {
     const int ax = face >> 1, hi = face & 1;

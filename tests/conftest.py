@@ -18,7 +18,8 @@ def pytest_configure(config):
 
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GOLDEN_CASES = ["c444_b222", "c664_b332", "c888_b444_h", "c16_b844", "c16_b8", "c32_b8", "c32_b8_int"]
+GOLDEN_CASES = ["c444_b222", "c664_b332", "c888_b444_h", "c16_b844", "c16_b8", "c32_b8", "c32_b8_int", "c884_b441",
+                "c1688_b1644"]
 # 12^3 / 16^3-style blocks beyond the register-tile band (large-block local solver)
 LARGE_CASES = ["c32_b16x4", "c32_b16", "c64_b16_t3"]
 

@@ -95,6 +95,10 @@ CASES = {
     "c64_b16_t3": ((64, 64, 32), (1 / 64, 1 / 64, 1 / 64), (16, 16, 16), ("smooth", 4.0, 1.0), ("toprandom", 64, 6),
                    "xonly"),
 }
+# edge cases: blocks one cell thick along z (empty interiors, S = hats only)
+# and a single block along x (nb1 = 1)
+CASES["c884_b441"] = ((8, 8, 4), (1.0, 1.0, 1.0), (4, 4, 1), ("normal", 0.5), ("random", 8, 3), True)
+CASES["c1688_b1644"] = ((16, 8, 8), (1.0, 1.0, 1.0), (16, 4, 4), ("smooth", 2.0, 1.0), ("random", 10, 3), True)
 PERTURB = {"c64_b16_t3": 1.0}
 # fixtures whose large arrays are stored as projections / digests
 COMPACT = {"c32_b16x4", "c32_b16", "c64_b16_t3"}
