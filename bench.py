@@ -542,7 +542,7 @@ def run_gpu(args, rank, world, log):
         Dfull, fst = fprob.simulate(m_obs)
         fine = {"seconds": round(time.perf_counter() - t0, 4), "iterations": int(fst.factor.last.iterations),
                 "relres": fst.factor.last.relres,
-                "what": "forward_full(direct) at 128^3 with 16 sources: Jacobi-PCG per column to relres 1e-13",
+                "what": "forward_full(direct) at 128^3 with 16 sources: PCG per column to relres 1e-13, preconditioned by the two-level MSFV method (adaptive basis + Galerkin coarse solve + block interior solves + skeleton Jacobi)",
                 "n_sources": int(Dfull.shape[1])}
         log("fine forward: " + json.dumps(fine))
         del fprob, fst

@@ -161,7 +161,8 @@ MSFV_API int msfv_residual(const msfv_plan* plan, const double* src, double alph
 /* out = blockdiag(A_II^{-1}) rhs on interiors (MultiscaleBasis.interior_solve, basis.py:339-353). */
 MSFV_API int msfv_interior_solve(const msfv_plan* plan, const double* factor, const double* rhs, double* out,
                         int32_t nrhs, void* stream);
-/* out[k][nrhs] = scale * S^T (A_w1 X1 + A_w2 X2); part: nblocks*8*nrhs scratch (forward.py:266). */
+/* out[k][nrhs] = scale * S^T (A_w1 X1 + A_w2 X2); part: nblocks*8*nrhs scratch (forward.py:266).
+ * A null w_i takes the field X_i itself (S^T X: restriction of a node field). */
 MSFV_API int msfv_restrict_op(const msfv_plan* plan, const double* Sint, const double* w1, const double* X1,
                      const double* w2, const double* X2, int32_t nrhs, double scale, double* part, double* out,
                      void* stream);

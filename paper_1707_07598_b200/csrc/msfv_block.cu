@@ -315,8 +315,9 @@ k_restrict_op(Geo g, const double* __restrict__ Sint, const double* __restrict__
       long long I = (long long)bi * g.b1 + x, J = (long long)bj * g.b2 + y, K = (long long)bk * g.b3 + z;
       if (I == 0 && J == 0 && K == 0) continue;   // pinned node has no row
       double h = 0.0;
-      if (X1) h += apply_A_row(g, w1, X1, nrhs, s, I, J, K);
-      if (X2) h += apply_A_row(g, w2, X2, nrhs, s, I, J, K);
+      // w == nullptr: the field itself (S^T X, the coarse restriction of a node field)
+      if (X1) h += w1 ? apply_A_row(g, w1, X1, nrhs, s, I, J, K) : X1[node_id(g, I, J, K) * nrhs + s];
+      if (X2) h += w2 ? apply_A_row(g, w2, X2, nrhs, s, I, J, K) : X2[node_id(g, I, J, K) * nrhs + s];
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) acc[cc] += s_value(g, Sb, jb, cc, x, y, z, false) * h;
     }
@@ -330,6 +331,50 @@ k_restrict_op(Geo g, const double* __restrict__ Sint, const double* __restrict__
       __syncthreads();
     }
     if (tid < 8) part[((size_t)jb * 8 + tid) * nrhs + s] = red[tid * nt];
+    __syncthreads();
+  }
+}
+
+// part[jb][cc][s] = sum over the nodes owned by jb of S(node, cc) X(node, s):
+// the plain restriction S^T X of a node field (no operator), all right-hand
+// sides at once.  Thread (group, s): s = tid % nrhs, the node groups stride
+// the block's owned nodes; the groups' partial sums are reduced in a fixed
+// order in shared memory.
+__global__ void __launch_bounds__(RESTRICT_THREADS)
+k_restrict_field(Geo g, const double* __restrict__ Sint, const double* __restrict__ X, int nrhs,
+                 double* __restrict__ part) {
+  __shared__ double red[RESTRICT_THREADS * 8];
+  const int jb = blockIdx.x, tid = threadIdx.x;
+  const int bi = jb % g.nb1, bj = (jb / g.nb1) % g.nb2, bk = jb / (g.nb1 * g.nb2);
+  const int ox = g.b1 + (bi == g.nb1 - 1), oy = g.b2 + (bj == g.nb2 - 1), oz = g.b3 + (bk == g.nb3 - 1);
+  const int nown = ox * oy * oz;
+  const double* Sb = Sint + (size_t)jb * 8 * g.nI;
+  const int ns_t = nrhs < RESTRICT_THREADS ? nrhs : RESTRICT_THREADS;
+  const int ngroups = RESTRICT_THREADS / ns_t;
+  for (int s0 = 0; s0 < nrhs; s0 += ns_t) {
+    const int s = s0 + tid % ns_t, grp = tid / ns_t;
+    double acc[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
+    if (grp < ngroups && s < nrhs) {
+      for (int f = grp; f < nown; f += ngroups) {
+        const int x = f % ox, r = f / ox, y = r % oy, z = r / oy;
+        const long long I = (long long)bi * g.b1 + x, J = (long long)bj * g.b2 + y, K = (long long)bk * g.b3 + z;
+        if (I == 0 && J == 0 && K == 0) continue;     // pinned node has no row
+        const double h = X[node_id(g, I, J, K) * nrhs + s];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) acc[cc] += s_value(g, Sb, jb, cc, x, y, z, false) * h;
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) red[cc * RESTRICT_THREADS + tid] = acc[cc];
+    __syncthreads();
+    for (int t = tid; t < 8 * ns_t; t += blockDim.x) {
+      const int cc = t / ns_t, sl = t % ns_t;
+      double v = 0.0;
+      for (int q = 0; q < ngroups; ++q) v += red[cc * RESTRICT_THREADS + q * ns_t + sl];
+      if (s0 + sl < nrhs) part[((size_t)jb * 8 + cc) * nrhs + s0 + sl] = v;
+    }
     __syncthreads();
   }
 }
@@ -506,7 +551,10 @@ cudaError_t launch_prolong(const Geo& g, const double* Sint, const double* Y, in
 cudaError_t launch_restrict_op(const Geo& g, const double* Sint, const double* w1, const double* X1,
                                const double* w2, const double* X2, int nrhs, double* part, double scale,
                                double* out, cudaStream_t st) {
-  k_restrict_op<<<g.nbl, RESTRICT_THREADS, 0, st>>>(g, Sint, w1, X1, w2, X2, nrhs, part);
+  if (!w1 && X1 && !X2)
+    k_restrict_field<<<g.nbl, RESTRICT_THREADS, 0, st>>>(g, Sint, X1, nrhs, part);
+  else
+    k_restrict_op<<<g.nbl, RESTRICT_THREADS, 0, st>>>(g, Sint, w1, X1, w2, X2, nrhs, part);
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
