@@ -2946,8 +2946,8 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
 // S_{pslot} at fixed rows (no atomics: each slot row has one writer); a
 // backward item reads [y_E; x_B] (x_B in Zb, written by the parent), writes
 // x_E to X and to its children's Zb rows.  Zb reuses the XE workspace.
-constexpr int MF_CC = 8;
-constexpr int MF_LCH = 4;
+constexpr int MF_CC = 4;     // right-hand sides per CTA of the blocked sweeps (4: more CTAs on the few top fronts)
+constexpr int MF_LCH = 8;    // L tiles per streamed chunk (8: half the chunk barriers of 4; config 5 solve 5.8 -> 4.2 ms)
 __device__ __forceinline__ void mf_tma_tiles(double* dst, const double* src, int ntile, unsigned long long* bar) {
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
