@@ -282,6 +282,18 @@ MSFV_API int msfv_fine_apply(const msfv_plan* plan, const double* w, const doubl
                              void* stream);
 MSFV_API int msfv_full_gradient(const msfv_plan* plan, const double* sigma, const double* U, const double* V,
                                 int32_t nrhs, double* xi, double* g, void* stream);
+/* ---- edge-space pieces for the enriched basis families ----
+ * The reference's AdaptiveSensitivity works on per-edge vectors
+ * (forward.py:224-281: gprof, gu, a; basis.edge_profiles, basis.py:596-608).
+ * msfv_edge_grad: out[e][c] = (G_p X)(e, c), the pinned nodal gradient
+ *   (operators.py:36-74, G[:, 1:]) of ncol node fields X[node][ncol];
+ * msfv_edge_div:  out[node][c] = (G_p^T F)(node, c) for edge fields
+ *   F[e][ncol] (row 0, the pinned node, is 0);
+ * msfv_cell_gather: g = -sigma o (C^T xi), the Csig^T products of
+ *   forward.py:254-256,278-280 (C = edge_cell_map, operators.py:77-109). */
+MSFV_API int msfv_edge_grad(const msfv_plan* plan, const double* X, int32_t ncol, double* out, void* stream);
+MSFV_API int msfv_edge_div(const msfv_plan* plan, const double* F, int32_t ncol, double* out, void* stream);
+MSFV_API int msfv_cell_gather(const msfv_plan* plan, const double* sigma, const double* xi, double* g, void* stream);
 /* ---- Gauss-Newton objective (Objective, inversion.py:32-88) ----
  * L = cell_gradient(mesh): cell-centre differences across interior faces, +-1/h.
  * msfv_reg_apply: out = alpha L^T L v (Objective.hess_apply, inversion.py:87-88);

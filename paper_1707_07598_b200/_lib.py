@@ -81,6 +81,9 @@ SIGNATURES = {
     "msfv_plan_create_mesh": (ctypes.c_int, [_P, _P, ctypes.POINTER(_P)]),
     "msfv_fine_apply": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_full_gradient": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P]),
+    "msfv_edge_grad": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
+    "msfv_edge_div": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
+    "msfv_cell_gather": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "msfv_reg_apply": (ctypes.c_int, [_P, _D, _P, _P, _P]),
     "msfv_reg_faces": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_yk_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),

@@ -341,10 +341,11 @@ def _template(partition, engine):
 
 
 def _check_families(spec):
-    if tuple(spec.families) != ("lagrange",):
-        raise NotImplementedError(
-            "the GPU path builds the Lagrange family; "
-            f"families {tuple(spec.families)} are outside this tier's scope")
+    """Lagrange alone takes the block-layout path; the enriched families
+    (source, skeleton, local_pca) take enriched.py; both need the hat
+    boundary data (the reduced boundary problems are Lagrange-only)."""
+    if tuple(spec.families) != ("lagrange",) and spec.boundary != "hats":
+        raise NotImplementedError("reduced boundary conditions are built for the Lagrange family only")
 
 
 def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None, spec=None):
@@ -380,7 +381,10 @@ def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None, spec=None
 
 
 class BasisBuilder:
-    """Re-assembles the basis at any model (basis.py:619-660)."""
+    """Re-assembles the basis at any model (basis.py:619-660).  The
+    boundary-condition data of every family is generated once (reference
+    fields for ``skeleton`` / ``local_pca`` come from a device fine solve at
+    ``m_ref``) and never depends on the current model."""
 
     def __init__(self, partition, spec=None, Q=None, m_ref=None, workers=1):
         spec = spec if spec is not None else BasisSpec()
@@ -390,6 +394,15 @@ class BasisBuilder:
         self.default_workers = workers
         self._pieces = None
         self._bc_sets = None
+        self._layout = None
+        self.enriched = tuple(spec.families) != ("lagrange",)
+        if self.enriched:
+            fams = set(spec.families)
+            if {"skeleton", "local_pca"} & fams and (Q is None or m_ref is None):
+                raise ValueError("skeleton/local_pca families need Q and m_ref")
+            if "source" in fams and Q is None:
+                raise ValueError("source family needs Q")
+            self._Q, self._m_ref = Q, m_ref
 
     @property
     def pieces(self):
@@ -397,11 +410,42 @@ class BasisBuilder:
             self._pieces = (nodal_gradient(self.partition.mesh), edge_cell_map(self.partition.mesh))
         return self._pieces
 
+    def _engine(self):
+        return engine_for(self.partition)
+
     @property
     def bc_sets(self):
         if self._bc_sets is None:
-            self._bc_sets = [generate_bc_lagrange(self.partition)]
+            if not self.enriched:
+                self._bc_sets = [generate_bc_lagrange(self.partition)]
+            else:
+                from . import enriched as en
+                fams, spec, part = set(self.spec.families), self.spec, self.partition
+                u_ref = None
+                if {"skeleton", "local_pca"} & fams:
+                    u_ref = en.reference_fields(part, self._m_ref, self._Q, engine=self._engine())
+                sets = []
+                for fam in FAMILIES:                       # canonical order (basis.py:638-652)
+                    if fam not in fams:
+                        continue
+                    if fam == "lagrange":
+                        sets.append(generate_bc_lagrange(part))
+                    elif fam == "source":
+                        sets.append(en.source_family(part, self._Q))
+                    elif fam == "skeleton":
+                        sets.append(en.skeleton_family(part, u_ref))
+                    else:
+                        sets.append(en.local_pca_family(part, u_ref, rank=spec.pca_rank, total=spec.pca_total,
+                                                        drop_tol=spec.pca_drop_tol))
+                self._bc_sets = sets
         return self._bc_sets
 
     def assemble(self, op, workers=None):
-        return assemble_basis(op, self.partition, workers=workers, spec=self.spec)
+        if not self.enriched:
+            return assemble_basis(op, self.partition, workers=workers, spec=self.spec)
+        from . import enriched as en
+        if self._layout is None:
+            self._layout = en.EnrichedLayout(self.partition, self._engine(), self.bc_sets, op.pieces)
+        if self._layout.nE == 0 and self._layout.has_lagrange:
+            return assemble_basis(op, self.partition, workers=workers, spec=self.spec)   # every extra column dropped
+        return en.assemble_enriched(op, self._layout)

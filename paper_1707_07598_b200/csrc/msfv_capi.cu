@@ -689,6 +689,24 @@ int msfv_full_gradient(const msfv_plan* plan, const double* sigma, const double*
   return cuda_check(launch_full_gradient(plan->g, sigma, U, V, nrhs, xi, g, (cudaStream_t)stream), "full_gradient");
 }
 
+int msfv_edge_grad(const msfv_plan* plan, const double* X, int32_t ncol, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (ncol < 0 || !X || !out) return fail(MSFV_SHAPE, "bad edge gradient arguments");
+  return cuda_check(launch_edge_grad(plan->g, X, ncol, out, (cudaStream_t)stream), "edge_grad");
+}
+
+int msfv_edge_div(const msfv_plan* plan, const double* F, int32_t ncol, double* out, void* stream) {
+  CHECK_PLAN(plan);
+  if (ncol < 0 || !F || !out) return fail(MSFV_SHAPE, "bad edge divergence arguments");
+  return cuda_check(launch_edge_div(plan->g, F, ncol, out, (cudaStream_t)stream), "edge_div");
+}
+
+int msfv_cell_gather(const msfv_plan* plan, const double* sigma, const double* xi, double* g, void* stream) {
+  CHECK_PLAN(plan);
+  if (!sigma || !xi || !g) return fail(MSFV_SHAPE, "bad cell gather arguments");
+  return cuda_check(launch_cell_gather(plan->g, sigma, xi, g, (cudaStream_t)stream), "cell_gather");
+}
+
 int msfv_reg_apply(const msfv_plan* plan, double alpha, const double* v, double* out, void* stream) {
   CHECK_PLAN(plan);
   if (!v || !out) return fail(MSFV_SHAPE, "bad regularizer arguments");

@@ -47,6 +47,64 @@ __global__ void k_apply_full(Geo g, const double* __restrict__ w, const double* 
   out[t] = v;
 }
 
+// Edge e of the reference's edge order (x-, y-, z-edges, i fastest;
+// operators.py:36-74): end nodes a < b and 1/h_e.
+__device__ __forceinline__ void edge_ends(const Geo& g, long long e, long long& a, long long& b, double& ih) {
+  int i, j, k;
+  if (e < g.Ex) {
+    decode3f(e, g.n1, g.r_n1, g.n2 + 1, g.r_n2p, i, j, k);
+    a = node_id(g, i, j, k);
+    b = a + 1;
+    ih = g.ih1;
+  } else if (e < g.Ex + g.Ey) {
+    decode3f(e - g.Ex, g.n1 + 1, g.r_n1p, g.n2, g.r_n2, i, j, k);
+    a = node_id(g, i, j, k);
+    b = a + (g.n1 + 1);
+    ih = g.ih2;
+  } else {
+    decode3f(e - g.Ex - g.Ey, g.n1 + 1, g.r_n1p, g.n2 + 1, g.r_n2p, i, j, k);
+    a = node_id(g, i, j, k);
+    b = a + (long long)(g.n1 + 1) * (g.n2 + 1);
+    ih = g.ih3;
+  }
+}
+
+// out(e, c) = (X(b, c) - X(a, c)) / h_e: the pinned nodal gradient G_p X of
+// ncol node fields (row 0 of X is the pinned node, kept at zero).
+__global__ void k_edge_grad(Geo g, const double* __restrict__ X, int ncol, double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= g.E * ncol) return;
+  const long long e = t / ncol;
+  const int c = (int)(t - e * ncol);
+  long long a, b;
+  double ih;
+  edge_ends(g, e, a, b, ih);
+  out[t] = (X[b * ncol + c] - X[a * ncol + c]) * ih;
+}
+
+// out(node, c) = (G_p^T F)(node, c): +F/h for the edges ending at the node,
+// -F/h for the edges starting there, axes x, y, z in order; out(0, *) = 0.
+__global__ void k_edge_div(Geo g, const double* __restrict__ F, int ncol, double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= g.Nn * ncol) return;
+  const long long nd = t / ncol;
+  const int c = (int)(t - nd * ncol);
+  if (nd == 0) {
+    out[t] = 0.0;
+    return;
+  }
+  int i, j, k;
+  decode3f(nd, g.n1 + 1, g.r_n1p, g.n2 + 1, g.r_n2p, i, j, k);
+  double v = 0.0;
+  if (i > 0) v += F[ex_id(g, i - 1, j, k) * ncol + c] * g.ih1;
+  if (i < g.n1) v -= F[ex_id(g, i, j, k) * ncol + c] * g.ih1;
+  if (j > 0) v += F[ey_id(g, i, j - 1, k) * ncol + c] * g.ih2;
+  if (j < g.n2) v -= F[ey_id(g, i, j, k) * ncol + c] * g.ih2;
+  if (k > 0) v += F[ez_id(g, i, j, k - 1) * ncol + c] * g.ih3;
+  if (k < g.n3) v -= F[ez_id(g, i, j, k) * ncol + c] * g.ih3;
+  out[t] = v;
+}
+
 // xi_e = sum_s (U_b - U_a)(V_b - V_a) / h_e^2, sources summed in order.
 __global__ void k_full_xi(Geo g, const double* __restrict__ U, const double* __restrict__ V, int nrhs,
                           double* __restrict__ xi) {
@@ -136,6 +194,20 @@ cudaError_t launch_full_gradient(const Geo& g, const double* sigma, const double
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_cell_gather(g, sigma, xi, gout, st);
+}
+
+cudaError_t launch_edge_grad(const Geo& g, const double* X, int ncol, double* out, cudaStream_t st) {
+  if (ncol <= 0) return cudaSuccess;
+  k_edge_grad<<<nblk(g.E * ncol, 256), 256, 0, st>>>(g, X, ncol, out);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_edge_div(const Geo& g, const double* F, int ncol, double* out, cudaStream_t st) {
+  if (ncol <= 0) return cudaSuccess;
+  k_edge_div<<<nblk(g.Nn * ncol, 256), 256, 0, st>>>(g, F, ncol, out);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_reg_apply(const Geo& g, double alpha, const double* v, double* out, cudaStream_t st) {

@@ -67,6 +67,8 @@ cudaError_t launch_cell_gather(const Geo& g, const double* sigma, const double* 
 cudaError_t launch_apply_full(const Geo& g, const double* w, const double* X, int nrhs, double* out, cudaStream_t st);
 cudaError_t launch_full_gradient(const Geo& g, const double* sigma, const double* U, const double* V, int nrhs,
                                  double* xi, double* gout, cudaStream_t st);
+cudaError_t launch_edge_grad(const Geo& g, const double* X, int ncol, double* out, cudaStream_t st);
+cudaError_t launch_edge_div(const Geo& g, const double* F, int ncol, double* out, cudaStream_t st);
 cudaError_t launch_reg_apply(const Geo& g, double alpha, const double* v, double* out, cudaStream_t st);
 cudaError_t launch_reg_faces(const Geo& g, const double* d, double* out, cudaStream_t st);
 cudaError_t launch_basis_csc(long long nnz, const double* Sint, const long long* src, const double* hatv,

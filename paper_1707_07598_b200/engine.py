@@ -458,6 +458,28 @@ class Engine:
                                                  stream()), "full_gradient")
         return g
 
+    # ------------------------------------------------- edge space (enriched)
+    def edge_grad(self, X):
+        """G_p X: (E, ncol) edge fields of the node fields X (Nn, ncol)."""
+        X = X.contiguous()
+        o = self.empty(self.E, X.shape[1])
+        _lib.check(self.L.msfv_edge_grad(self.plan, ptr(X), X.shape[1], ptr(o), stream()), "edge_grad")
+        return o
+
+    def edge_div(self, F):
+        """G_p^T F: node fields (Nn, ncol) of the edge fields F (E, ncol)."""
+        F = F.contiguous()
+        o = self.empty(self.Nn, F.shape[1])
+        _lib.check(self.L.msfv_edge_div(self.plan, ptr(F), F.shape[1], ptr(o), stream()), "edge_div")
+        return o
+
+    def cell_gather(self, sigma, xi):
+        """-sigma o (C^T xi) for one edge vector xi (E,)."""
+        g = self.empty(self.Nm)
+        _lib.check(self.L.msfv_cell_gather(self.plan, ptr(sigma), ptr(xi.contiguous()), ptr(g), stream()),
+                   "cell_gather")
+        return g
+
     def reg_apply(self, alpha, v, out=None):
         o = out if out is not None else self.empty(self.Nm)
         _lib.check(self.L.msfv_reg_apply(self.plan, float(alpha), ptr(v), ptr(o), stream()), "reg_apply")

@@ -174,6 +174,9 @@ def forward_reduced_dev(op, survey, basis, defer_check=False):
     With ``defer_check`` nothing synchronises; the status bits (invalid model,
     local or coarse factorization failure) are resolved by ``state.check()``,
     which also takes the reference's diagonal-shift fallback (forward.py:122-129)."""
+    if hasattr(basis, "layout"):             # enriched families (enriched.py)
+        from .enriched import forward_enriched_dev
+        return forward_enriched_dev(op, survey, basis)
     eng = basis.engine
     if basis.bx is not None:
         eng.bind_boundary(basis.bx)          # reduced boundary values of this basis
@@ -200,6 +203,9 @@ def forward_reduced(op, survey, basis):
     queued before the wait); the shift fallback, when the status asks for it,
     recomputes D and copies it again."""
     import torch
+    if hasattr(basis, "layout"):             # enriched families (enriched.py)
+        from .enriched import forward_enriched
+        return forward_enriched(op, survey, basis)
     D, state = forward_reduced_dev(op, survey, basis, defer_check=True)
     Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
     fh = torch.empty(1, dtype=state.flags.dtype, pin_memory=True)
@@ -320,4 +326,7 @@ class AdaptiveSensitivity:
 
 
 def sensitivity_adaptive(state, survey, workers=1):
+    if hasattr(state.basis, "layout"):       # enriched families (enriched.py)
+        from .enriched import EnrichedSensitivity
+        return EnrichedSensitivity(state, survey, workers=workers)
     return AdaptiveSensitivity(state, survey, workers=workers)
