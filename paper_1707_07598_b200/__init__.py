@@ -16,6 +16,8 @@ from .basis import (
 )
 from .forward import Survey, ReducedState, forward_reduced, AdaptiveSensitivity, sensitivity_adaptive
 from .inversion import misfit_ssd, AdaptiveReducedProblem
+from .models import build_survey
+from .enriched import source_family, skeleton_family, local_pca_family, reference_fields
 from .fine import (
     forward_full, FullState, FullSensitivity, sensitivity_full, FullProblem, block_cg, IterativeResult,
 )
