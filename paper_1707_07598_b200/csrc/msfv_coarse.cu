@@ -320,6 +320,16 @@ __device__ __forceinline__ void tile_xyt(const double* X, const double* Y, F&& o
 // lane factors the block redundantly from shared memory (no shuffles on the
 // pivot chain: ~2x shorter than a row-per-lane factorization); lanes 0..7
 // then form the columns of L^{-1}.
+// 1/sqrt(d) for a positive normal d: MUFU seed and one cubic Newton-type
+// step (relative error ~2^-60 before rounding), no special-case branches --
+// the pivot chain of the 32x32 POTRF is the critical path of every tile column
+__device__ __forceinline__ double rsq_seeded(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double e = fma(-d * y, y, 1.0);
+  const double t = fma(0.375, e, 0.5);
+  return fma(y * e, t, y);
+}
 template <int R>
 __device__ __forceinline__ void c8_inv(double (&d)[8], int c, const double (&a)[8][8], const double (&inv)[8]) {
   if constexpr (R < 8) {
@@ -342,7 +352,7 @@ __device__ __forceinline__ void potrf_inv8w(const double* S, int ld, double* Is,
   for (int c = 0; c < 8; ++c) {
     double d = a[c][c];
     if (!(d > 0.0)) { bad = true; d = 1.0; }
-    inv[c] = rsqrt(d);
+    inv[c] = rsq_seeded(d);
 #pragma unroll
     for (int i = c + 1; i < 8; ++i) a[i][c] *= inv[c];
 #pragma unroll
@@ -1757,6 +1767,9 @@ struct MfPlan {
   int* d_lvloff = nullptr;
   int* d_pre = nullptr;   // per-level prefix sums (solve): rows | forward items | backward items, npre each
   int npre = 0;
+  int4* d_items = nullptr;   // k_mf_inv_all items (front, tile column, slice), longest chain first
+  int nitems = 0;
+  int inv_nemax = 0;
   bool use_g = true;      // explicit inverse blocks fit the kernels' shared memory (else staged sweeps)
 };
 
@@ -1980,6 +1993,21 @@ static cudaError_t mf_upload(const Geo& g) {
     e = cudaMalloc(&P->d_pre, pre.size() * sizeof(int));
     if (e == cudaSuccess) e = cudaMemcpy(P->d_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess && P->use_g) {
+    std::vector<int4> items;
+    for (int f = 0; f < (int)P->fr.size(); ++f) {
+      const MfFront& F = P->fr[f];
+      P->inv_nemax = std::max(P->inv_nemax, F.NE);
+      for (int c = 0; c < F.NE; ++c) {
+        const int cost = (F.NE - c) * (F.NE - c + 1) / 2 + (F.NT - F.NE) * (F.NE - c);
+        for (int sl = 0; sl < TB / 8; ++sl) items.push_back(make_int4(f, c, sl, cost));
+      }
+    }
+    std::stable_sort(items.begin(), items.end(), [](const int4& a, const int4& b) { return a.w > b.w; });
+    P->nitems = (int)items.size();
+    e = cudaMalloc(&P->d_items, items.size() * sizeof(int4));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  }
   return e;
 }
 
@@ -1992,6 +2020,7 @@ void mf_release(Geo& g) {
   if (P->d_maps) cudaFree(P->d_maps);
   if (P->d_lvloff) cudaFree(P->d_lvloff);
   if (P->d_pre) cudaFree(P->d_pre);
+  if (P->d_items) cudaFree(P->d_items);
   delete P;
   g.mf = nullptr;
 }
@@ -2514,14 +2543,11 @@ __global__ void __launch_bounds__(256) k_mf_bwd_s(MfDev d, int l0, double* __res
   }
 }
 
-// Explicit front inverse blocks, after the level's factorization: CTA
-// (front, c) solves L [G_E; G_B](:, block c) = [I; 0](:, block c) by the
-// blocked forward substitution (steps J = c .. NE-1) with the 32 columns in
-// shared memory, then stores G and G^T.  With them a front's forward solve is
+// Explicit front inverse blocks G = [L_EE^-1; -L_BE L_EE^-1] and G^T
+// (k_mf_inv_all below).  With them a front's forward solve is
 // [y_E; c_B] = G v_E + [0; v_B] and its backward solve x_E = G^T [y_E; x_B]:
 // one matrix product per front, so a coarse solve has the depth of the tree
 // (7 levels at config 4) instead of 23 tile steps.
-constexpr int MF_INV_THREADS = 256;
 // one bulk copy global -> shared on an mbarrier (thread 0 issues; all wait)
 __device__ __forceinline__ void mf_tma1(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
   if (threadIdx.x == 0) {
@@ -2534,130 +2560,128 @@ __device__ __forceinline__ void mf_tma1(double* dst, const double* src, unsigned
                  : "memory");
   }
 }
-// 2x2-blocked 32x32 by 32x32 product O = Lt Y, Lt row-major (stride 32),
-// Y / O row-major with stride ld; op(o, value) stores.  256 threads.
-template <class Op>
-__device__ __forceinline__ void mf_tile_mm(const double* Lt, const double* Y, int ld, Op op) {
-  const int cp = threadIdx.x % 16, rp = threadIdx.x / 16, r0 = 2 * rp;
-  double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
-#pragma unroll 8
-  for (int k = 0; k < TB; k += 2) {
-    const double2 l0 = *reinterpret_cast<const double2*>(Lt + r0 * TB + k);
-    const double2 l1 = *reinterpret_cast<const double2*>(Lt + (r0 + 1) * TB + k);
-    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * ld + 2 * cp);
-    const double2 y1 = *reinterpret_cast<const double2*>(Y + (k + 1) * ld + 2 * cp);
-    a00 = fma(l0.x, y0.x, fma(l0.y, y1.x, a00));
-    a01 = fma(l0.x, y0.y, fma(l0.y, y1.y, a01));
-    a10 = fma(l1.x, y0.x, fma(l1.y, y1.x, a10));
-    a11 = fma(l1.x, y0.y, fma(l1.y, y1.y, a11));
-  }
-  op(r0, 2 * cp, a00, a01);
-  op(r0 + 1, 2 * cp, a10, a11);
+// All explicit inverse blocks of the factorization in ONE launch (replaces the
+// per-level k_mf_inv / k_mf_invB pairs, which ran between the levels'
+// factor launches although only the solves read G): item = (front, tile
+// column c, 8-column slice s).  The CTA (4 warps) runs the forward
+// substitution L_EE Y = I(:, 8 columns) with Y (rows x 8) in shared memory,
+// then G_B = -L_BE Y.  The tile sequence (Dinv_J, L_{J+1,J} .. L_{NE-1,J} per
+// step J, then the B rows) is known in advance, so the 32x32 tiles stream
+// through a ring of MF_INV_NS padded shared-memory stages filled by cp.async
+// (MF_INV_NS - 1 tiles in flight: the chain is not bound by L2 latency);
+// each tile product (32x32 by 32x8) is 8 DMMAs per warp.  Items are sorted by
+// chain length (host, mf_upload), longest first.
+constexpr int MF_INV_W = 8;          // identity columns per item
+constexpr int MF_INV_NS = 6;         // ring stages
+constexpr int MF_INV_LD = TB + 4;    // padded tile row stride (288 B: conflict-free fragment loads)
+constexpr int MF_INV2_THREADS = 128;
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__global__ void __launch_bounds__(MF_INV_THREADS) k_mf_inv(MfDev d, int l0) {
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+struct MfInvCur {
+  int ph, J, I;
+};
+__global__ void __launch_bounds__(MF_INV2_THREADS) k_mf_inv_all(MfDev d, const int4* __restrict__ items) {
   extern __shared__ __align__(16) double sh[];
-  __shared__ __align__(8) unsigned long long bar[2];
-  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
-  const int c = blockIdx.y;
-  if (c >= F.NE) return;
+  const int4 it = items[blockIdx.x];
+  const MfFront F = d.fr[it.x];
+  const int c = it.y, s = it.z;
   const Band B = mf_band(d.base, F);
-  const int rows = F.NE * TB;           // the chain runs on the E rows; G_B = -L_BE G_E follows (k_mf_invB)
-  double* V = sh;                       // rows x 32
-  double* ys = V + (size_t)rows * TB;   // 32 x 32
-  double* Tb = ys + TT;                 // 2 tiles: Dinv_J / L tiles, double-buffered
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
+  const int NE = F.NE, NT = F.NT;
+  double* V = sh;                                   // NE*TB x 8
+  double* ring = V + (size_t)NE * TB * MF_INV_W;    // MF_INV_NS x TB x MF_INV_LD
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, m = lane >> 2, q = lane & 3;
+  const int col0 = c * TB + s * MF_INV_W;
+  for (int t = tid; t < NE * TB * MF_INV_W; t += MF_INV2_THREADS)
+    V[t] = (t / MF_INV_W == col0 + t % MF_INV_W) ? 1.0 : 0.0;
+  const int n1 = (NE - c) * (NE - c + 1) / 2, ntot = n1 + (NT - NE) * (NE - c);
+  auto next = [&](MfInvCur& u) {
+    if (u.ph == 1) {
+      if (++u.I >= NE) {
+        ++u.J;
+        u.I = u.J;
+        if (u.J >= NE) u = {2, c, NE};
+      }
+    } else if (++u.J >= NE) {
+      u.J = c;
+      ++u.I;
+    }
+  };
+  auto issue = [&](int n, const MfInvCur& u) {
+    if (n < ntot) {
+      const double* src = u.I == u.J ? B.Dinv + (size_t)u.J * TT : btile(B.Lo, B, u.J, u.I - u.J);
+      double* dst = ring + (size_t)(n % MF_INV_NS) * TB * MF_INV_LD;
+#pragma unroll
+      for (int k = 0; k < TT / 2 / MF_INV2_THREADS; ++k) {
+        const int ch = tid + MF_INV2_THREADS * k, r = ch / (TB / 2), c2 = ch % (TB / 2);
+        cp_async16(dst + r * MF_INV_LD + 2 * c2, src + r * TB + 2 * c2);
+      }
+    }
+    cp_async_commit();
+  };
+  MfInvCur ui{1, c, c}, uc{1, c, c};
+  for (int n = 0; n < MF_INV_NS - 1; ++n) {
+    issue(n, ui);
+    next(ui);
   }
-  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
-    const int r = t / TB, q = t % TB;
-    V[t] = (r == c * TB + q) ? 1.0 : 0.0;
+  // O (8 rows 8w.., 8 columns) = tile rows 8w.. times Y (32 x 8, stride 8)
+  auto prod = [&](const double* T, const double* Y) -> F2c {
+    F2c a = {0.0, 0.0}, b = {0.0, 0.0};
+    const double* Tr = T + (8 * w + m) * MF_INV_LD + q;
+    const double* Yr = Y + q * MF_INV_W + m;
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 2) {
+      dmma(a.x, a.y, Tr[4 * kk], Yr[4 * kk * MF_INV_W]);
+      dmma(b.x, b.y, Tr[4 * kk + 4], Yr[(4 * kk + 4) * MF_INV_W]);
+    }
+    return {a.x + b.x, a.y + b.y};
+  };
+  double* G = d.base + F.goff2;
+  const int frows = NT * TB, ncol = NE * TB;
+  double* GT = G + (size_t)NT * NE * TT;
+  F2c acc = {0.0, 0.0};
+  for (int n = 0; n < ntot; ++n) {
+    cp_async_wait<MF_INV_NS - 2>();
+    __syncthreads();                       // tile n landed for every thread; stage (n-1) % NS is free
+    issue(n + MF_INV_NS - 1, ui);
+    next(ui);
+    const double* T = ring + (size_t)(n % MF_INV_NS) * TB * MF_INV_LD;
+    double* VJ = V + (size_t)uc.J * TB * MF_INV_W;
+    const F2c o = prod(T, VJ);
+    if (uc.ph == 1) {
+      if (uc.I == uc.J) {                  // Y_J = Dinv_J v_J (every warp has read v_J before any row changes)
+        __syncthreads();
+        *reinterpret_cast<double2*>(VJ + (8 * w + m) * MF_INV_W + 2 * q) = make_double2(o.x, o.y);
+      } else {                             // v_I -= L_{I,J} Y_J (own rows)
+        double2* p = reinterpret_cast<double2*>(V + ((size_t)uc.I * TB + 8 * w + m) * MF_INV_W + 2 * q);
+        const double2 v = *p;
+        *p = make_double2(v.x - o.x, v.y - o.y);
+      }
+    } else {                               // G_B[I] = -sum_J L_{I,J} Y_J
+      acc.x += o.x;
+      acc.y += o.y;
+      if (uc.J == NE - 1) {
+        const int r = uc.I * TB + 8 * w + m, cq = col0 + 2 * q;
+        *reinterpret_cast<double2*>(G + (size_t)r * ncol + cq) = make_double2(-acc.x, -acc.y);
+        GT[(size_t)cq * frows + r] = -acc.x;
+        GT[(size_t)(cq + 1) * frows + r] = -acc.y;
+        acc = {0.0, 0.0};
+      }
+    }
+    next(uc);
   }
   __syncthreads();
-  unsigned ph[2] = {0, 0};
-  int buf = 0;
-  // sequence of tiles: per step J, Dinv_J then L_{I,J} for I = J+1 .. NT-1
-  auto src_of = [&](int J, int I) -> const double* {
-    return I == J ? B.Dinv + (size_t)J * TT : btile(B.Lo, B, J, I - J);
-  };
-  mf_tma1(Tb, src_of(c, c), TT * sizeof(double), &bar[0]);
-  for (int J = c; J < F.NE; ++J) {
-    for (int I = J; I < F.NE; ++I) {
-      // prefetch the next tile of the sequence into the other buffer
-      int nJ = J, nI = I + 1;
-      if (nI >= F.NE) { nJ = J + 1; nI = nJ; }
-      if (nJ < F.NE) mf_tma1(Tb + (buf ^ 1) * TT, src_of(nJ, nI), TT * sizeof(double), &bar[buf ^ 1]);
-      mbar_wait(&bar[buf], ph[buf]);
-      ph[buf] ^= 1;
-      const double* T = Tb + buf * TT;
-      if (I == J) {
-        mf_tile_mm(T, V + (size_t)J * TT, TB, [&](int r, int q, double x, double y) {
-          *reinterpret_cast<double2*>(ys + r * TB + q) = make_double2(x, y);
-        });
-        __syncthreads();
-        for (int t = threadIdx.x; t < TT; t += blockDim.x) V[(size_t)J * TT + t] = ys[t];
-      } else {
-        double* VI = V + (size_t)I * TT;
-        mf_tile_mm(T, ys, TB, [&](int r, int q, double x, double y) {
-          double2* o = reinterpret_cast<double2*>(VI + r * TB + q);
-          const double2 p = *o;
-          *o = make_double2(p.x - x, p.y - y);
-        });
-      }
-      __syncthreads();
-      buf ^= 1;
-    }
+  const int rows = NE * TB;
+  for (int t = tid; t < rows * MF_INV_W; t += MF_INV2_THREADS) {
+    const int r = t / MF_INV_W, qq = t % MF_INV_W;
+    G[(size_t)r * ncol + col0 + qq] = V[t];
   }
-  double* G = d.base + F.goff2;
-  const int frows = F.NT * TB;
-  double* GT = G + (size_t)F.NT * F.NE * TT;
-  const int ncol = F.NE * TB;
-  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
-    const int r = t / TB, q = t % TB;
-    G[(size_t)r * ncol + c * TB + q] = V[t];
-  }
-  for (int t = threadIdx.x; t < rows * TB; t += blockDim.x) {
-    const int q = t / rows, r = t % rows;
-    GT[(size_t)(c * TB + q) * frows + r] = V[(size_t)r * TB + q];
-  }
-}
-// G_B = -L_BE G_E: item (front, B tile row I, column block c) sums
-// L_{I,J} G_E[J][c] over J = c .. NE-1 (32x32 tiles through shared memory).
-__global__ void __launch_bounds__(MF_INV_THREADS) k_mf_invB(MfDev d, int l0, int nbmax) {
-  __shared__ __align__(16) double Lt[TT];
-  __shared__ __align__(16) double Gt[TT];
-  const MfFront F = d.fr[d.lvl[l0 + blockIdx.x]];
-  const int NB = F.NT - F.NE;
-  const int I = F.NE + blockIdx.y % nbmax, c = blockIdx.y / nbmax;
-  if (I >= F.NT || c >= F.NE || NB <= 0) return;
-  const Band B = mf_band(d.base, F);
-  const int ncol = F.NE * TB, frows = F.NT * TB;
-  double* G = d.base + F.goff2;
-  double* GT = G + (size_t)F.NT * F.NE * TT;
-  double acc[4] = {0, 0, 0, 0};
-  const int cp = threadIdx.x % 16, r0 = 2 * (threadIdx.x / 16);
-  for (int J = c; J < F.NE; ++J) {
-    const double* Ls = btile(B.Lo, B, J, I - J);
-    for (int t = threadIdx.x; t < TT / 2; t += blockDim.x) {
-      reinterpret_cast<double2*>(Lt)[t] = __ldg(reinterpret_cast<const double2*>(Ls) + t);
-      const int r = (2 * t) / TB, q = (2 * t) % TB;
-      reinterpret_cast<double2*>(Gt)[t] =
-          __ldcg(reinterpret_cast<const double2*>(G + (size_t)(J * TB + r) * ncol + c * TB + q));
-    }
-    __syncthreads();
-    mf_tile_mm(Lt, Gt, TB, [&](int r, int q, double x, double y) {
-      const int h = (r - r0) * 2;
-      acc[h] += x;
-      acc[h + 1] += y;
-    });
-    __syncthreads();
-  }
-  for (int h = 0; h < 2; ++h) {
-    const int r = I * TB + r0 + h, q = c * TB + 2 * cp;
-    G[(size_t)r * ncol + q] = -acc[2 * h];
-    G[(size_t)r * ncol + q + 1] = -acc[2 * h + 1];
-    GT[(size_t)q * frows + r] = -acc[2 * h];
-    GT[(size_t)(q + 1) * frows + r] = -acc[2 * h + 1];
+  for (int t = tid; t < rows * MF_INV_W; t += MF_INV2_THREADS) {
+    const int qq = t / rows, r = t % rows;
+    GT[(size_t)(col0 + qq) * frows + r] = V[(size_t)r * MF_INV_W + qq];
   }
 }
 
@@ -3212,24 +3236,16 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
     count_launches(1);
     if (e != cudaSuccess) return e;
-    if (P->use_g) {
-      int nemax = 1, nbmax = 0;
-      for (int i = 0; i < nf; ++i) {
-        nemax = std::max(nemax, P->fr[P->lvl[l0 + i]].NE);
-        nbmax = std::max(nbmax, P->fr[P->lvl[l0 + i]].NT - P->fr[P->lvl[l0 + i]].NE);
-      }
-      const size_t smi = ((size_t)nemax * TB * TB + 3 * TT) * sizeof(double);
-      static PerDevice<cudaError_t> attr;
-      e = attr.get([] { return cudaFuncSetAttribute(k_mf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX); });
-      if (e != cudaSuccess) return e;
-      if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
-      k_mf_inv<<<dim3(nf, jmax), MF_INV_THREADS, smi, st>>>(d, l0);
-      count_launches(1);
-      if (nbmax > 0) {
-        k_mf_invB<<<dim3(nf, nbmax * jmax), MF_INV_THREADS, 0, st>>>(d, l0, nbmax);
-        count_launches(1);
-      }
-    }
+  }
+  if (P->use_g && P->nitems > 0) {
+    // every explicit inverse block in one launch, after the last level (only the solves read G)
+    const size_t smi = ((size_t)P->inv_nemax * TB * MF_INV_W + (size_t)MF_INV_NS * TB * MF_INV_LD) * sizeof(double);
+    if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
+    static PerDevice<cudaError_t> attr;
+    e = attr.get([] { return cudaFuncSetAttribute(k_mf_inv_all, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX); });
+    if (e != cudaSuccess) return e;
+    k_mf_inv_all<<<P->nitems, MF_INV2_THREADS, smi, st>>>(d, P->d_items);
+    count_launches(1);
   }
   return cudaGetLastError();
 }

@@ -196,8 +196,12 @@ def test_error_contract(rng):
     with pytest.raises(gp.StaleBasisError):
         basis.check_model(m + 1e-3)
     basis.check_model(m.copy())
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(ValueError):                                   # basis.py:631 (needs Q and m_ref)
         gp.BasisBuilder(part, gp.BasisSpec(families=("lagrange", "skeleton")))
+    with pytest.raises(ValueError):                                   # basis.py:47-49
+        gp.BasisSpec(families=("lagrange", "wavelet"))
+    with pytest.raises(NotImplementedError):                          # reduced BCs are Lagrange-only
+        gp.BasisBuilder(part, gp.BasisSpec(families=("lagrange", "source"), boundary="reduced"))
     with pytest.raises(ValueError):
         gp.misfit_ssd(np.zeros((2, 2)), np.zeros((2, 3)))
 
