@@ -330,42 +330,39 @@ __device__ __forceinline__ double rsq_seeded(double d) {
   const double t = fma(0.375, e, 0.5);
   return fma(y * e, t, y);
 }
-template <int R>
-__device__ __forceinline__ void c8_inv(double (&d)[8], int c, const double (&a)[8][8], const double (&inv)[8]) {
-  if constexpr (R < 8) {
-    double acc = (R == c) ? 1.0 : 0.0;
-#pragma unroll
-    for (int m = 0; m < R; ++m) acc -= a[R][m] * d[m];
-    d[R] = (R < c) ? 0.0 : acc * inv[R];
-    c8_inv<R + 1>(d, c, a, inv);
-  }
-}
 __device__ __forceinline__ void potrf_inv8w(const double* S, int ld, double* Is, int lane, int* flags) {
   double a[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j <= i; ++j) a[i][j] = S[i * ld + j];
-  double inv[8];
+  // column ci of L^{-1} rides along the pivots (right-looking forward
+  // substitution of e_ci: independent of the trailing update, so it adds no
+  // latency to the pivot chain)
+  const int ci = lane & 7;
+  double acc[8], dc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = i == ci ? 1.0 : 0.0;
   bool bad = false;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     double d = a[c][c];
     if (!(d > 0.0)) { bad = true; d = 1.0; }
-    inv[c] = rsq_seeded(d);
+    const double inv = rsq_seeded(d);
 #pragma unroll
-    for (int i = c + 1; i < 8; ++i) a[i][c] *= inv[c];
+    for (int i = c + 1; i < 8; ++i) a[i][c] *= inv;
 #pragma unroll
     for (int j = c + 1; j < 8; ++j)
 #pragma unroll
       for (int i = j; i < 8; ++i) a[i][j] -= a[i][c] * a[j][c];
+    dc[c] = acc[c] * inv;
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) acc[i] = fma(-a[i][c], dc[c], acc[i]);
   }
   if (bad && lane == 0) atomicOr(flags, FLAG_COARSE_NOT_SPD);
   if (lane < 8) {
-    double d[8];
-    c8_inv<0>(d, lane, a, inv);
 #pragma unroll
-    for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = d[rr];
+    for (int rr = 0; rr < 8; ++rr) Is[rr * 8 + lane] = dc[rr];
   }
   __syncwarp();
 }
@@ -483,10 +480,8 @@ __device__ void coarse_potrf(const Band& B, int J, int* flags, FactorSmem& sm,
 // Pair task f of tile column J: trailing tile (t1, t2), t2 <= t1, recomputing
 // the panel tiles it needs, L_{J+t,J} = A_{J+t,J} Dinv_J^T (so the panel TRSM
 // costs no grid barrier).  sm.D holds Dinv_J.
-// diag_to_smem (lookahead pair (1,1)): the updated diagonal tile goes to
-// sm.T for the POTRF that follows instead of back to global memory.
-__device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm,
-                            bool diag_to_smem = false) {
+// (The lookahead pair (1,1) is coarse_chain_task.)
+__device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm) {
   const int lane = threadIdx.x & 31;
   int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
   while (t1 * (t1 - 1) / 2 > f) --t1;
@@ -520,10 +515,43 @@ __device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm,
     }
     c.x += e.x;
     c.y += e.y;
-    if (diag_to_smem)
-      put(sm.T, LDT, bi, bj, lane, c);
-    else
-      put(G, TB, bi, bj, lane, c);
+    put(G, TB, bi, bj, lane, c);
+  }
+  __syncthreads();
+}
+
+// Lookahead pair (1,1) of tile column J on the chain CTA (sm.D holds Dinv_J):
+// L_{J+1,J} = A_{J+1,J} Dinv_J^T goes to Lo, the updated next diagonal tile to
+// sm.T for the POTRF that follows.  Both global reads (the panel tile and the
+// diagonal tile's fragments) are in flight together: one L2 round trip on
+// the critical path of the tile column instead of two.
+__device__ void coarse_chain_task(const Band& B, int J, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  const double* G = btile(B.A, B, J + 1, 0);
+  F2c c[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h;
+    c[h] = frag(G, TB, o >> 2, o & 3, lane);
+  }
+  load_tile(sm.T, btile(B.A, B, J, 1));
+  __syncthreads();
+  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& v) { put(sm.X1, LDT, bi, bj, lane, v); });
+  __syncthreads();
+  store_tile(btile(B.Lo, B, J, 1), sm.X1);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
+    F2c e = {0.0, 0.0};
+#pragma unroll
+    for (int kb = 0; kb < 4; kb += 2) {
+      const F2c a = frag(sm.X1, LDT, bi, kb, lane), a2 = frag(sm.X1, LDT, bi, kb + 1, lane);
+      mxyt(c[h], {-a.x, -a.y}, frag(sm.X1, LDT, bj, kb, lane));
+      mxyt(e, {-a2.x, -a2.y}, frag(sm.X1, LDT, bj, kb + 1, lane));
+    }
+    c[h].x += e.x;
+    c[h].y += e.y;
+    put(sm.T, LDT, bi, bj, lane, c[h]);
   }
   __syncthreads();
 }
@@ -550,7 +578,7 @@ __global__ void __launch_bounds__(256, 1) k_coarse_factor(FactorJob job, int* __
     if (mine >= 0) {
       const Band B = mine ? job.b[1] : job.b[0];
       if (J < B.NT - 1) {
-        coarse_task(B, J, 0, sm, true);           // pair (1,1): next diagonal tile, into sm.T
+        coarse_chain_task(B, J, sm);              // pair (1,1): next diagonal tile, into sm.T
         coarse_potrf(B, J + 1, flags, sm, true);  // lookahead factor of column J+1 (keeps Dinv in sm.D)
       }
     }
@@ -2166,9 +2194,11 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
       const MfFront F = front(i);
       if (J + 1 < F.NE) {
         const Band B = mf_band(job.d.base, F);
-        load_tile(sm.D, B.Dinv + (size_t)J * TT);
-        __syncthreads();
-        coarse_task(B, J, 0, sm, true);
+        if (!split) {                              // a chain CTA with one front still holds Dinv_J from its POTRF
+          load_tile(sm.D, B.Dinv + (size_t)J * TT);
+          __syncthreads();
+        }
+        coarse_chain_task(B, J, sm);
         coarse_potrf(B, J + 1, flags, sm, true);
       }
     }
