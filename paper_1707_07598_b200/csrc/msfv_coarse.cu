@@ -1755,6 +1755,11 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 constexpr int MF_LEAF = 128;   // leaf boxes of <= 128 coarse nodes (tuned on config 4: 64 -> 128 saves 0.07 ms per step)
 constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative kernels
 constexpr int MF_GR = 16;       // rows per item of the G products
+constexpr int MF_KC = 256;      // input rows per chunk of the K-chunked G products (fronts beyond one shared-memory load)
+constexpr int MF_INV_W = 8;     // identity columns per item of k_mf_inv_all
+constexpr int MF_INV_NS = 6;    // its tile ring stages
+constexpr int MF_INV_LD = COARSE_TB + 4;   // padded tile row stride (288 B: conflict-free fragment loads)
+constexpr int MF_INV_SMALL = 12;   // fronts of <= 12 E tile columns share the small-footprint launch
 constexpr int MF_SMEM_MAX = 226 * 1024;   // dynamic shared memory of the staged solve kernels
 // explicit front inverse blocks (G) give one-product-per-front solves where
 // the fronts fit the inverse-block budget (MfPlan::use_g); else staged sweeps
@@ -1795,9 +1800,9 @@ struct MfPlan {
   int* d_lvloff = nullptr;
   int* d_pre = nullptr;   // per-level prefix sums (solve): rows | forward items | backward items, npre each
   int npre = 0;
-  int4* d_items = nullptr;   // k_mf_inv_all items (front, tile column, slice), longest chain first
-  int nitems = 0;
-  int inv_nemax = 0;
+  int4* d_items = nullptr;   // k_mf_inv_all items (front, tile column, slice), longest chain first;
+  int nitems[2] = {0, 0};    // group 0: fronts with NE > MF_INV_SMALL, group 1: the rest (own launch, own footprint)
+  int inv_nemax[2] = {0, 0};
   bool use_g = true;      // explicit inverse blocks fit the kernels' shared memory (else staged sweeps)
 };
 
@@ -2022,19 +2027,23 @@ static cudaError_t mf_upload(const Geo& g) {
     if (e == cudaSuccess) e = cudaMemcpy(P->d_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && P->use_g) {
-    std::vector<int4> items;
+    std::vector<int4> items[2];
     for (int f = 0; f < (int)P->fr.size(); ++f) {
       const MfFront& F = P->fr[f];
-      P->inv_nemax = std::max(P->inv_nemax, F.NE);
+      const int grp = F.NE > MF_INV_SMALL ? 0 : 1;
+      P->inv_nemax[grp] = std::max(P->inv_nemax[grp], F.NE);
       for (int c = 0; c < F.NE; ++c) {
         const int cost = (F.NE - c) * (F.NE - c + 1) / 2 + (F.NT - F.NE) * (F.NE - c);
-        for (int sl = 0; sl < TB / 8; ++sl) items.push_back(make_int4(f, c, sl, cost));
+        for (int sl = 0; sl < TB / MF_INV_W; ++sl) items[grp].push_back(make_int4(f, c, sl, cost));
       }
     }
-    std::stable_sort(items.begin(), items.end(), [](const int4& a, const int4& b) { return a.w > b.w; });
-    P->nitems = (int)items.size();
-    e = cudaMalloc(&P->d_items, items.size() * sizeof(int4));
-    if (e == cudaSuccess) e = cudaMemcpy(P->d_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    for (auto& v : items) std::stable_sort(v.begin(), v.end(), [](const int4& a, const int4& b) { return a.w > b.w; });
+    P->nitems[0] = (int)items[0].size();
+    P->nitems[1] = (int)items[1].size();
+    items[0].insert(items[0].end(), items[1].begin(), items[1].end());
+    e = cudaMalloc(&P->d_items, std::max<size_t>(items[0].size(), 1) * sizeof(int4));
+    if (e == cudaSuccess && !items[0].empty())
+      e = cudaMemcpy(P->d_items, items[0].data(), items[0].size() * sizeof(int4), cudaMemcpyHostToDevice);
   }
   return e;
 }
@@ -2062,8 +2071,7 @@ bool mf_attach(Geo& g) {
     nemax = std::max(nemax, F.NE);
     ntmax = std::max(ntmax, F.NT);
   }
-  const size_t inv_b = ((size_t)nemax * TT + 3 * TT) * sizeof(double);
-  const size_t sol_b = ((size_t)MF_GR * ntmax * TB + (size_t)ntmax * TB * 32 + (size_t)MF_GR * 32) * sizeof(double) + 8192;
+  const size_t inv_b = ((size_t)nemax * TB * MF_INV_W + (size_t)MF_INV_NS * TB * MF_INV_LD) * sizeof(double);
   const int nl = (int)P->lvl_off.size() - 1;
   int maxf = 0;
   for (int l = 0; l < nl; ++l) maxf = std::max(maxf, P->lvl_off[l + 1] - P->lvl_off[l]);
@@ -2072,9 +2080,12 @@ bool mf_attach(Geo& g) {
     g.mf = nullptr;
     return false;
   }
-  // fronts too large for the explicit-inverse kernels (config 5's top levels):
-  // keep the multifrontal factorization, solve with the blocked sweeps
-  P->use_g = inv_b <= (size_t)MF_SMEM_MAX && sol_b <= (size_t)MF_SMEM_MAX - 8192;
+  // explicit inverse blocks whenever a front's 8 inverse columns fit shared
+  // memory (k_mf_inv_all); fronts whose G chunk and input vector exceed one
+  // shared-memory load take the K-chunked products of the one-launch solve
+  // (config 5's top levels).  Otherwise the blocked sweeps.
+  (void)ntmax;
+  P->use_g = inv_b <= (size_t)MF_SMEM_MAX;
   g.mf = P;
   return true;
 }
@@ -2601,9 +2612,6 @@ __device__ __forceinline__ void mf_tma1(double* dst, const double* src, unsigned
 // (MF_INV_NS - 1 tiles in flight: the chain is not bound by L2 latency);
 // each tile product (32x32 by 32x8) is 8 DMMAs per warp.  Items are sorted by
 // chain length (host, mf_upload), longest first.
-constexpr int MF_INV_W = 8;          // identity columns per item
-constexpr int MF_INV_NS = 6;         // ring stages
-constexpr int MF_INV_LD = TB + 4;    // padded tile row stride (288 B: conflict-free fragment loads)
 constexpr int MF_INV2_THREADS = 128;
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -2817,6 +2825,24 @@ struct MfSolveJob {
   unsigned long long* tstamp;   // debug (MSFV_MF_TIMING): globaltimer after every grid barrier
   const int* pre;       // MfPlan::d_pre
   int npre;
+  int kchunk;           // > 0: pipelined K-chunked products with this many input rows per chunk
+};
+__device__ __forceinline__ void mf_bulk_raw(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Work unit of the pipelined products: one (front, MF_GR-row chunk) item of a
+// level's phase (B).  Rows of G (forward) or G^T (backward) start at G0 with
+// stride gstride; the product runs over input rows [kbeg, kmax) of vin.
+struct MfItem {
+  const double* G0;
+  const double* vin;
+  size_t gstride;
+  int nr, kbeg, kmax;
+  int r0;        // first output row (forward: front row r0c, backward: E row j0)
+  int fi;        // front (level-local)
 };
 __device__ __forceinline__ void mf_stamp(unsigned long long* ts, int i) {
   if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -2829,12 +2855,17 @@ constexpr int MF_FCACHE = 128;   // front descriptors cached per level in the co
 __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bars2[2];   // the two buffers of the pipelined products
   __shared__ int pre[MF_MAXF + 1], preB[MF_MAXF + 1];
   __shared__ MfFront fc[MF_FCACHE];
   cg::grid_group grid = cg::this_grid();
-  if (threadIdx.x == 0) mbar_init(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_init(&bars2[0]);
+    mbar_init(&bars2[1]);
+  }
   __syncthreads();
-  unsigned ph = 0;
+  unsigned ph = 0, phs2 = 0u;   // phs2: parity bits of bars2
   int nst = 0;
   mf_stamp(job.tstamp, nst++);
   const MfDev& d = job.d;
@@ -2899,8 +2930,156 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       grid.sync();
       mf_stamp(job.tstamp, nst++);
       // ---- (B) products
+      if (job.kchunk) {
+        // Pipelined K-chunked products: the CTA's units (item, chunk of KC
+        // input rows) stream through two shared-memory buffers; the copies of
+        // the unit after next are issued as soon as a buffer is consumed, so
+        // a CTA with many items (config 5: 124 leaf items per CTA) is bound by
+        // the copy / FMA time, not by one L2 round trip per item.
+        const int KC = job.kchunk, GLD = KC + 4;   // padded G row stride: conflict-free fragment loads
+        const size_t bufd = (size_t)MF_GR * GLD + (size_t)KC * nrhs + 8;
+        double* red = sh + 2 * bufd;                // k-part partial sums of an item
+        // warp (tj, part): 8 right-hand sides tj, k-part `part` of every chunk, both 8-row halves
+        const int ntj = (nrhs + 7) >> 3, nparts = max(1, 8 / ntj), RLD = 8 * ntj + 2;
+        const int wv = threadIdx.x >> 5, lane = threadIdx.x & 31, mm = lane >> 2, qq = lane & 3;
+        const bool wact = wv < ntj * nparts;
+        const int tj = wv % ntj, part = wv / ntj;
+        const int total = preB[nf];
+        auto front = [&](int fi2) { return fi2 < MF_FCACHE ? fc[fi2] : d.fr[d.lvl[l0 + fi2]]; };
+        auto item_of = [&](int gi, int& fi2) {
+          while (preB[fi2 + 1] <= gi) ++fi2;
+          const MfFront F = front(fi2);
+          const int rows = F.NT * TB, ncol = F.NE * TB;
+          MfItem it;
+          it.vin = job.Vin + (size_t)F.voff * nrhs;
+          it.fi = fi2;
+          if (pass == 0) {                 // [y_E; c_B] rows r0c.. = G v_E (+ the children's c_B on B rows)
+            const int r0c = (gi - preB[fi2]) * MF_GR;
+            it.nr = min(MF_GR, rows - r0c);
+            it.r0 = r0c;
+            it.kbeg = 0;
+            it.kmax = r0c < ncol ? min(ncol, ((r0c + it.nr - 1) / TB + 1) * TB) : ncol;
+            it.G0 = d.base + F.goff2 + (size_t)r0c * ncol;
+            it.gstride = (size_t)ncol;
+          } else {                         // x_E rows j0.. = G^T [y_E; x_B]
+            const int j0 = (gi - preB[fi2]) * MF_GR;
+            it.nr = min(MF_GR, F.nE - j0);
+            it.r0 = j0;
+            it.kbeg = (j0 / TB) * TB;
+            it.kmax = rows;
+            it.G0 = d.base + F.goff2 + (size_t)F.NT * F.NE * TT + (size_t)j0 * rows;
+            it.gstride = (size_t)rows;
+          }
+          return it;
+        };
+        // issue cursor (thread 0 copies; every thread tracks it: cheap and branch-uniform)
+        int gi_i = blockIdx.x, fi_i = 0, k_i = 0;
+        bool have_i = gi_i < total;
+        MfItem it_i{};
+        if (have_i) {
+          it_i = item_of(gi_i, fi_i);
+          k_i = it_i.kbeg;
+        }
+        auto issue_next = [&](int b) {
+          if (!have_i) return;
+          const int kc = min(KC, it_i.kmax - k_i);
+          if (threadIdx.x < 32) {                  // warp 0: lane 0 arms the barrier, lanes 0..nr-1 copy a row of G each, lane 31 the input rows
+            double* Gs = sh + (size_t)b * bufd;
+            double* vs = Gs + (size_t)MF_GR * GLD;
+            const unsigned bg = (unsigned)(kc * sizeof(double)), bv = (unsigned)(kc * nrhs * sizeof(double));
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            if (threadIdx.x == 0) {
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bars2[b])),
+                           "r"(it_i.nr * bg + bv)
+                           : "memory");
+            }
+            __syncwarp();
+            const int ii = threadIdx.x;
+            if (ii < it_i.nr)
+              mf_bulk_raw(Gs + (size_t)ii * GLD, it_i.G0 + (size_t)ii * it_i.gstride + k_i, bg, &bars2[b]);
+            if (ii == 31) mf_bulk_raw(vs, it_i.vin + (size_t)k_i * nrhs, bv, &bars2[b]);
+          }
+          k_i += KC;
+          if (k_i >= it_i.kmax) {
+            gi_i += gridDim.x;
+            have_i = gi_i < total;
+            if (have_i) {
+              it_i = item_of(gi_i, fi_i);
+              k_i = it_i.kbeg;
+            }
+          }
+        };
+        issue_next(0);
+        issue_next(1);
+        int b = 0, fi_c = 0;
+        for (int gi = blockIdx.x; gi < total; gi += gridDim.x) {
+          const MfItem it = item_of(gi, fi_c);
+          const MfFront F = front(it.fi);
+          const int ncol = F.NE * TB;
+          double addv[4] = {0.0, 0.0, 0.0, 0.0};
+          if (pass == 0 && it.r0 >= ncol) {       // B rows: the children's c_B, fetched while the chunks arrive
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int t = threadIdx.x + 256 * u;
+              if (t < it.nr * nrhs) addv[u] = __ldcg(it.vin + (size_t)it.r0 * nrhs + t);
+            }
+          }
+          // (every row of an item has the same k range: an item's 16 rows lie in one 32-row tile)
+          F2c c0 = {0.0, 0.0}, c1 = {0.0, 0.0};
+          for (int k0 = it.kbeg; k0 < it.kmax; k0 += KC) {
+            const int kc = min(KC, it.kmax - k0);
+            const double* Gs = sh + (size_t)b * bufd;
+            const double* vs = Gs + (size_t)MF_GR * GLD;
+            mbar_wait(&bars2[b], (phs2 >> b) & 1u);
+            phs2 ^= 1u << b;
+            if (wact) {
+              const int kp = kc / nparts, kb = part * kp;             // kc is a multiple of 32, nparts of 8
+              const double* Ga = Gs + (size_t)mm * GLD + kb + qq;
+              const double* Gb = Ga + (size_t)8 * GLD;
+              const double* Vb = vs + (size_t)(kb + qq) * nrhs + 8 * tj + mm;
+              F2c e0 = {0.0, 0.0}, e1 = {0.0, 0.0};
+#pragma unroll 4
+              for (int k = 0; k < kp; k += 8) {
+                const double b0 = Vb[(size_t)k * nrhs], b1 = Vb[(size_t)(k + 4) * nrhs];
+                dmma(c0.x, c0.y, Ga[k], b0);
+                dmma(c1.x, c1.y, Gb[k], b0);
+                if (k + 4 < kp) {
+                  dmma(e0.x, e0.y, Ga[k + 4], b1);
+                  dmma(e1.x, e1.y, Gb[k + 4], b1);
+                }
+              }
+              c0.x += e0.x; c0.y += e0.y;
+              c1.x += e1.x; c1.y += e1.y;
+            }
+            __syncthreads();                     // buffer b consumed by every thread
+            issue_next(b);
+            b ^= 1;
+          }
+          if (wact) {
+            double* rp = red + (size_t)part * 16 * RLD + 8 * tj + 2 * qq;
+            rp[(size_t)mm * RLD] = c0.x;
+            rp[(size_t)mm * RLD + 1] = c0.y;
+            rp[(size_t)(mm + 8) * RLD] = c1.x;
+            rp[(size_t)(mm + 8) * RLD + 1] = c1.y;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = threadIdx.x + 256 * u;
+            if (t < it.nr * nrhs) {
+              const int ii = t / nrhs, s2 = t % nrhs;
+              double a = 0.0;
+              for (int pp = 0; pp < nparts; ++pp) a += red[((size_t)pp * 16 + ii) * RLD + s2];
+              if (pass == 0)
+                job.Vout[((size_t)F.voff + it.r0 + ii) * nrhs + s2] = a + addv[u];
+              else
+                job.X[(size_t)d.gid[F.goff + it.r0 + ii] * nrhs + s2] = a;
+            }
+          }
+        }
+      }
       int fi = 0;
-      for (int gi = blockIdx.x; gi < preB[nf]; gi += gridDim.x) {
+      for (int gi = blockIdx.x; gi < preB[nf] && !job.kchunk; gi += gridDim.x) {
         while (preB[fi + 1] <= gi) ++fi;
         const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
         const int rows = F.NT * TB, ncol = F.NE * TB;
@@ -3267,15 +3446,23 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     count_launches(1);
     if (e != cudaSuccess) return e;
   }
-  if (P->use_g && P->nitems > 0) {
-    // every explicit inverse block in one launch, after the last level (only the solves read G)
-    const size_t smi = ((size_t)P->inv_nemax * TB * MF_INV_W + (size_t)MF_INV_NS * TB * MF_INV_LD) * sizeof(double);
-    if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
+  if (P->use_g) {
+    // every explicit inverse block after the last level (only the solves read G):
+    // one launch per footprint group
     static PerDevice<cudaError_t> attr;
     e = attr.get([] { return cudaFuncSetAttribute(k_mf_inv_all, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX); });
     if (e != cudaSuccess) return e;
-    k_mf_inv_all<<<P->nitems, MF_INV2_THREADS, smi, st>>>(d, P->d_items);
-    count_launches(1);
+    int off = 0;
+    for (int grp = 0; grp < 2; ++grp) {
+      if (P->nitems[grp] > 0) {
+        const size_t smi =
+            ((size_t)P->inv_nemax[grp] * TB * MF_INV_W + (size_t)MF_INV_NS * TB * MF_INV_LD) * sizeof(double);
+        if (smi > (size_t)MF_SMEM_MAX) return cudaErrorInvalidValue;
+        k_mf_inv_all<<<P->nitems[grp], MF_INV2_THREADS, smi, st>>>(d, P->d_items + off);
+        count_launches(1);
+      }
+      off += P->nitems[grp];
+    }
   }
   return cudaGetLastError();
 }
@@ -3332,6 +3519,11 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         return 0;
       return coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     });
+    // fronts whose G chunk + input vector exceed one shared-memory load: K-chunked products
+    // (MSFV_MF_FORCE_KCHUNK: test hook, the chunked products at any size)
+    const bool kchunk = smc > (size_t)MF_SMEM_MAX - 24576 || getenv("MSFV_MF_FORCE_KCHUNK") != nullptr;
+    const int KC = nrhs <= 32 ? MF_KC : MF_KC / 2;
+    if (kchunk) smc = (2 * ((size_t)MF_GR * (KC + 4) + (size_t)KC * nrhs + 8) + 1280) * sizeof(double);
     if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 24576 && !getenv("MSFV_MF_NOCOOP")) {
       const bool timing = getenv("MSFV_MF_TIMING") != nullptr;
       static PerDevice<unsigned long long*> tst_cache;
@@ -3341,7 +3533,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         return p;
       }) : nullptr;
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
-                     P->npre};
+                     P->npre, kchunk ? KC : 0};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
       count_launches(1);

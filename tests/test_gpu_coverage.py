@@ -47,11 +47,16 @@ class _fresh_engines:
         self.E._ENGINES.update(self.saved)
 
 
+@pytest.mark.parametrize("kchunk", [False, True])
 @pytest.mark.parametrize("name", ["c16_b8", "c32_b8", "c32_b8_int", "c16_b844"])
-def test_forced_multifrontal_matches_reference(name, monkeypatch):
+def test_forced_multifrontal_matches_reference(name, kchunk, monkeypatch):
     """MSFV_COARSE_ND=2 (multifrontal nested dissection, the k >= 1000 default)
-    on golden cases with k = 27 .. 125."""
+    on golden cases with k = 27 .. 125; with MSFV_MF_FORCE_KCHUNK the
+    K-chunked products that config 5's large fronts take in the one-launch
+    solve."""
     monkeypatch.setenv("MSFV_COARSE_ND", "2")
+    if kchunk:
+        monkeypatch.setenv("MSFV_MF_FORCE_KCHUNK", "1")
     g = load_golden(name)
     with _fresh_engines():
         gp, mesh, part, survey = _golden_problem(g)
@@ -124,7 +129,9 @@ def _config_vs_oracle(mesh_cells, cfg_id, force_chunked=False, monkeypatch=None)
     part = gp.create_partition(mesh, b, b, b)
     survey = build_survey(mesh, c["n_src"], c["n_rec"])
     m = config_model(mesh, c, 0)
-    if force_chunked:
+    if force_chunked == "kchunk":
+        monkeypatch.setenv("MSFV_MF_FORCE_KCHUNK", "1")
+    elif force_chunked:
         monkeypatch.setenv("MSFV_MF_FORCE_CHUNKED", "1")
     prob = gp.AdaptiveReducedProblem(gp.BasisBuilder(part), survey)
     d_obs = prob.simulate(m + 0.05)[0]
@@ -151,7 +158,7 @@ def _config_vs_oracle(mesh_cells, cfg_id, force_chunked=False, monkeypatch=None)
     return errs
 
 
-@pytest.mark.parametrize("chunked", [False, True])
+@pytest.mark.parametrize("chunked", [False, True, "kchunk"])
 def test_k_above_5000_matches_oracle(chunked, monkeypatch):
     """256 x 256 x 32 cells, 8^3 blocks: k = 33*33*5 = 5445 > 5000, so the
     reference (and the oracle) use the sparse A_k with SuperLU; the GPU uses
