@@ -477,45 +477,103 @@ __device__ void coarse_potrf(const Band& B, int J, int* flags, FactorSmem& sm,
   stamp(14);
 }
 
-// Pair task f of tile column J: trailing tile (t1, t2), t2 <= t1, recomputing
+// Pair task of tile column J: trailing tile (t1, t2), t2 <= t1, recomputing
 // the panel tiles it needs, L_{J+t,J} = A_{J+t,J} Dinv_J^T (so the panel TRSM
-// costs no grid barrier).  sm.D holds Dinv_J.
+// costs no grid barrier).  sm.D holds Dinv_J.  The two panel tiles and the
+// target tile's fragments are read together (one L2 round trip per task).
 // (The lookahead pair (1,1) is coarse_chain_task.)
-__device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm) {
-  const int lane = threadIdx.x & 31;
-  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
-  while (t1 * (t1 - 1) / 2 > f) --t1;
-  while ((t1 + 1) * t1 / 2 <= f) ++t1;
-  const int t2 = f - t1 * (t1 - 1) / 2 + 1;
+__device__ void coarse_pair(const Band& B, int J, int t1, int t2, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  double* G = btile(B.A, B, J + t2, t1 - t2);
+  F2c c[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h;
+    c[h] = frag(G, TB, o >> 2, o & 3, lane);
+  }
   load_tile(sm.T, btile(B.A, B, J, t1));
+  if (t2 != t1) load_tile(sm.X2, btile(B.A, B, J, t2));
   __syncthreads();
-  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X1, LDT, bi, bj, lane, c); });
+  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& v) { put(sm.X1, LDT, bi, bj, lane, v); });
   __syncthreads();
   if (t2 != t1) {
-    load_tile(sm.T, btile(B.A, B, J, t2));
-    __syncthreads();
-    tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& c) { put(sm.X2, LDT, bi, bj, lane, c); });
+    tile_xyt(sm.X2, sm.D, [&](int bi, int bj, const F2c& v) { put(sm.T, LDT, bi, bj, lane, v); });
     __syncthreads();
   } else {
     store_tile(btile(B.Lo, B, J, t1), sm.X1);
   }
-  const double* Y = (t2 != t1) ? sm.X2 : sm.X1;
-  double* G = btile(B.A, B, J + t2, t1 - t2);
-  // G -= X1 Y^T, block by block straight from / to global
-  const int wv = threadIdx.x >> 5;
+  const double* Y = (t2 != t1) ? sm.T : sm.X1;
+  // G -= X1 Y^T, block by block
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
-    F2c c = frag(G, TB, bi, bj, lane), e = {0.0, 0.0};
+    F2c e = {0.0, 0.0};
 #pragma unroll
     for (int kb = 0; kb < 4; kb += 2) {
       const F2c a = frag(sm.X1, LDT, bi, kb, lane), a2 = frag(sm.X1, LDT, bi, kb + 1, lane);
-      mxyt(c, {-a.x, -a.y}, frag(Y, LDT, bj, kb, lane));
+      mxyt(c[h], {-a.x, -a.y}, frag(Y, LDT, bj, kb, lane));
       mxyt(e, {-a2.x, -a2.y}, frag(Y, LDT, bj, kb + 1, lane));
     }
-    c.x += e.x;
-    c.y += e.y;
-    put(G, TB, bi, bj, lane, c);
+    c[h].x += e.x;
+    c[h].y += e.y;
+    put(G, TB, bi, bj, lane, c[h]);
+  }
+  __syncthreads();
+}
+// pair f of the band enumeration: f = t1 (t1 - 1) / 2 + t2 - 1
+__device__ void coarse_task(const Band& B, int J, int f, FactorSmem& sm) {
+  int t1 = (int)((1.0 + sqrt(1.0 + 8.0 * f)) * 0.5);
+  while (t1 * (t1 - 1) / 2 > f) --t1;
+  while ((t1 + 1) * t1 / 2 <= f) ++t1;
+  coarse_pair(B, J, t1, f - t1 * (t1 - 1) / 2 + 1, sm);
+}
+// Panel tile only: L_{J+t1,J} = A_{J+t1,J} Dinv_J^T to Lo (rows whose trailing
+// updates are deferred, see k_mf_factor).
+__device__ void coarse_panel_only(const Band& B, int J, int t1, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  load_tile(sm.T, btile(B.A, B, J, t1));
+  __syncthreads();
+  tile_xyt(sm.T, sm.D, [&](int bi, int bj, const F2c& v) { put(sm.X1, LDT, bi, bj, lane, v); });
+  __syncthreads();
+  store_tile(btile(B.Lo, B, J, t1), sm.X1);
+  __syncthreads();
+}
+// Deferred update of tile (R, C), both beyond the NE eliminated tile columns:
+// A_{R,C} -= sum_{J < NE} L_{R,J} L_{C,J}^T from the stored factor tiles.
+__device__ void coarse_deferred(const Band& B, int NE, int R, int C, FactorSmem& sm) {
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  double* G = btile(B.A, B, C, R - C);
+  F2c c[2], e[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h;
+    c[h] = frag(G, TB, o >> 2, o & 3, lane);
+    e[h] = {0.0, 0.0};
+  }
+  for (int J = 0; J < NE; ++J) {
+    double* X = (J & 1) ? sm.T : sm.X1;       // two (X, Y) buffer pairs: the next loads overlap this product
+    double* Y = (J & 1) ? sm.D : sm.X2;
+    load_tile(X, btile(B.Lo, B, J, R - J));
+    if (R != C) load_tile(Y, btile(B.Lo, B, J, C - J));
+    __syncthreads();
+    const double* Yr = R != C ? Y : X;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = wv + 8 * h, bi = o >> 2, bj = o & 3;
+#pragma unroll
+      for (int kb = 0; kb < 4; kb += 2) {
+        const F2c a = frag(X, LDT, bi, kb, lane), a2 = frag(X, LDT, bi, kb + 1, lane);
+        mxyt(c[h], {-a.x, -a.y}, frag(Yr, LDT, bj, kb, lane));
+        mxyt(e[h], {-a2.x, -a2.y}, frag(Yr, LDT, bj, kb + 1, lane));
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = wv + 8 * h;
+    c[h].x += e[h].x;
+    c[h].y += e[h].y;
+    put(G, TB, o >> 2, o & 3, lane, c[h]);
   }
   __syncthreads();
 }
@@ -2214,14 +2272,16 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
       }
     }
     if (me >= 0) {
-      // prefix of the task counts (each CTA builds the same table)
+      // prefix of the task counts (each CTA builds the same table).  Per
+      // front: the pairs (t1, t2) whose column J + t2 is still an E column
+      // (those tiles feed the next panels), then one panel-only task per B
+      // row; the B x B tiles wait for the deferred phase below.
       for (int i = threadIdx.x; i < nf; i += blockDim.x) {
         const MfFront F = front(i);
         int n = 0;
         if (J < F.NE) {
-          const int pt = F.NT - 1 - J;
-          const int first = (pt >= 1 && J + 1 < F.NE) ? 1 : 0;
-          n = pt >= 1 ? pt * (pt + 1) / 2 - first : 0;
+          const int pt = F.NT - 1 - J, ne = F.NE - 1 - J;
+          n = ne * pt - ne * (ne - 1) / 2 - (ne >= 1 ? 1 : 0) + (pt - ne);
         }
         pre[i + 1] = n;
       }
@@ -2237,16 +2297,51 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
         while (pre[fi + 1] <= gi) ++fi;
         const MfFront F = front(fi);
         const Band B = mf_band(job.d.base, F);
-        const int first = (J + 1 < F.NE) ? 1 : 0;
+        const int pt = F.NT - 1 - J, ne = F.NE - 1 - J;
+        const int npair = ne * pt - ne * (ne - 1) / 2;
         if (loaded != fi) {
           load_tile(sm.D, B.Dinv + (size_t)J * TT);
           __syncthreads();
           loaded = fi;
         }
-        coarse_task(B, J, first + (gi - pre[fi]), sm);
+        int p = (gi - pre[fi]) + (ne >= 1 ? 1 : 0);    // pair (1,1) belongs to the chain CTA
+        if (p < npair) {
+          int t2 = 1;
+          while (p >= pt - t2 + 1) {
+            p -= pt - t2 + 1;
+            ++t2;
+          }
+          coarse_pair(B, J, t2 + p, t2, sm);
+        } else {
+          coarse_panel_only(B, J, ne + 1 + (p - npair), sm);
+        }
       }
     }
     grid.sync();
+  }
+  // ---- deferred phase: the update matrices U = F_BB - L_BE L_BE^T, one task per lower B x B tile
+  {
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+      const MfFront F = front(i);
+      const int nb = F.NT - F.NE;
+      pre[i + 1] = nb * (nb + 1) / 2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pre[0] = 0;
+      for (int i = 0; i < nf; ++i) pre[i + 1] += pre[i];
+    }
+    __syncthreads();
+    const int total = pre[nf];
+    int fi = 0;
+    for (int gi = blockIdx.x; gi < total; gi += G) {
+      while (pre[fi + 1] <= gi) ++fi;
+      const MfFront F = front(fi);
+      const Band B = mf_band(job.d.base, F);
+      int p = gi - pre[fi], r = 0;                     // p = r (r + 1) / 2 + c, c <= r
+      while ((r + 1) * (r + 2) / 2 <= p) ++r;
+      coarse_deferred(B, F.NE, F.NE + r, F.NE + p - r * (r + 1) / 2, sm);
+    }
   }
 }
 
