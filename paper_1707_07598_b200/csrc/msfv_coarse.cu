@@ -3617,8 +3617,10 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
     // fronts whose G chunk + input vector exceed one shared-memory load: K-chunked products
     // (MSFV_MF_FORCE_KCHUNK: test hook, the chunked products at any size)
     const bool kchunk = smc > (size_t)MF_SMEM_MAX - 24576 || getenv("MSFV_MF_FORCE_KCHUNK") != nullptr;
-    const int KC = nrhs <= 32 ? MF_KC : MF_KC / 2;
-    if (kchunk) smc = (2 * ((size_t)MF_GR * (KC + 4) + (size_t)KC * nrhs + 8) + 1280) * sizeof(double);
+    int KC = MF_KC;                                   // largest chunk whose two buffers fit
+    auto smem_k = [&](int kc) { return (2 * ((size_t)MF_GR * (kc + 4) + (size_t)kc * nrhs + 8) + 1280) * sizeof(double); };
+    while (KC > 32 && smem_k(KC) > (size_t)MF_SMEM_MAX - 24576) KC /= 2;
+    if (kchunk) smc = smem_k(KC);
     if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 24576 && !getenv("MSFV_MF_NOCOOP")) {
       const bool timing = getenv("MSFV_MF_TIMING") != nullptr;
       static PerDevice<unsigned long long*> tst_cache;
