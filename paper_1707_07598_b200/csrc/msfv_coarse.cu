@@ -2246,6 +2246,7 @@ __global__ void __launch_bounds__(256) k_mf_assemble_t(Geo g, MfDev d, int l0, c
 struct MfJob {
   MfDev d;
   int l0, nf, jmax;
+  int defer;   // 1: B x B trailing updates deferred to one K-loop task per tile (levels with more B x B tiles than CTAs)
   Geo g;
 };
 __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict__ flags) {
@@ -2280,8 +2281,8 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
         const MfFront F = front(i);
         int n = 0;
         if (J < F.NE) {
-          const int pt = F.NT - 1 - J, ne = F.NE - 1 - J;
-          n = ne * pt - ne * (ne - 1) / 2 - (ne >= 1 ? 1 : 0) + (pt - ne);
+          const int pt = F.NT - 1 - J, ne = F.NE - 1 - J, nep = job.defer ? ne : pt;
+          n = nep * pt - nep * (nep - 1) / 2 - (ne >= 1 ? 1 : 0) + (pt - nep);
         }
         pre[i + 1] = n;
       }
@@ -2297,8 +2298,8 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
         while (pre[fi + 1] <= gi) ++fi;
         const MfFront F = front(fi);
         const Band B = mf_band(job.d.base, F);
-        const int pt = F.NT - 1 - J, ne = F.NE - 1 - J;
-        const int npair = ne * pt - ne * (ne - 1) / 2;
+        const int pt = F.NT - 1 - J, ne = F.NE - 1 - J, nep = job.defer ? ne : pt;
+        const int npair = nep * pt - nep * (nep - 1) / 2;
         if (loaded != fi) {
           load_tile(sm.D, B.Dinv + (size_t)J * TT);
           __syncthreads();
@@ -2313,14 +2314,14 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
           }
           coarse_pair(B, J, t2 + p, t2, sm);
         } else {
-          coarse_panel_only(B, J, ne + 1 + (p - npair), sm);
+          coarse_panel_only(B, J, nep + 1 + (p - npair), sm);
         }
       }
     }
     grid.sync();
   }
   // ---- deferred phase: the update matrices U = F_BB - L_BE L_BE^T, one task per lower B x B tile
-  {
+  if (job.defer) {
     for (int i = threadIdx.x; i < nf; i += blockDim.x) {
       const MfFront F = front(i);
       const int nb = F.NT - F.NE;
@@ -3535,7 +3536,14 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     }
     k_mf_assemble_t<<<dim3(ntmax * (ntmax + 1) / 2, nf), 256, 0, st>>>(g, d, l0, Ak + P->a27);
     count_launches(1);
-    MfJob job{d, l0, nf, jmax, g};
+    // defer the B x B updates where a tile column has more of them than CTAs (throughput-bound levels:
+    // fewer, cheaper tasks); latency-bound levels keep the per-column updates (no extra phase at the end)
+    long long nbb = 0;
+    for (int i = 0; i < nf; ++i) {
+      const long long nb = P->fr[P->lvl[l0 + i]].NT - P->fr[P->lvl[l0 + i]].NE;
+      nbb += nb * (nb + 1) / 2;
+    }
+    MfJob job{d, l0, nf, jmax, nbb > coop_grid ? 1 : 0, g};
     void* args[] = {(void*)&job, (void*)&flags};
     e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
     count_launches(1);
