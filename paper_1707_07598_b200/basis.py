@@ -32,8 +32,9 @@ def raise_status(f):
 
 @dataclass(frozen=True)
 class BasisSpec:
-    """Boundary-condition families (basis.py:37-53).  The GPU path builds the
-    Lagrange family; other families are rejected by BasisBuilder."""
+    """Boundary-condition families (basis.py:37-53): ``lagrange`` takes the
+    block-layout path (basis.py / forward.py here), the enriched families
+    (``source``, ``skeleton``, ``local_pca``) take enriched.py."""
 
     families: tuple = ("lagrange",)
     pca_rank: int = 0
