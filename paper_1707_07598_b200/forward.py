@@ -228,8 +228,8 @@ class AdaptiveSensitivity:
         op, basis = state.op, state.basis
         eng = basis.engine
         if basis.bx is not None:
-            raise NotImplementedError("derivatives through the reduced boundary problems are not built "
-                                      "(BasisSpec(boundary='reduced') serves the forward map only)")
+            raise NotImplementedError("a basis with reduced boundary conditions takes ReducedSensitivity "
+                                      "(sensitivity_adaptive dispatches to it)")
         if not getattr(state, "deferred", False):
             state.check()
         if op._dev is None or op._dev[1] is not basis._m_dev:
@@ -329,4 +329,7 @@ def sensitivity_adaptive(state, survey, workers=1):
     if hasattr(state.basis, "layout"):       # enriched families (enriched.py)
         from .enriched import EnrichedSensitivity
         return EnrichedSensitivity(state, survey, workers=workers)
+    if getattr(state.basis, "bx", None) is not None:   # reduced boundary conditions (reduced_sens.py)
+        from .reduced_sens import ReducedSensitivity
+        return ReducedSensitivity(state, survey, workers=workers)
     return AdaptiveSensitivity(state, survey, workers=workers)
