@@ -42,7 +42,7 @@ class BasisSpec:
     pca_drop_tol: float = 1e-10
     # extension: "hats" = the reference's trilinear skeleton
     # data (basis.py:84-116); "reduced" = 1D line / 2D face problems with the
-    # model's edge weights (msfv_reduced.cu; forward path only)
+    # model's edge weights (msfv_reduced.cu; sensitivities: reduced_sens.py)
     boundary: str = "hats"
 
     def __post_init__(self):
@@ -352,7 +352,7 @@ def _check_families(spec):
 def assemble_basis(op, partition, bc_sets=None, workers=1, cache=None, spec=None):
     """Build the Lagrange basis at the operator's model (basis.py:511-616).
     ``spec.boundary == "reduced"``: skeleton data from the reduced 1D/2D
-    problems at this model instead of the hats (extension, forward only)."""
+    problems at this model instead of the hats (extension)."""
     if bc_sets is not None:
         fams = [getattr(s, "family", "lagrange") for s in bc_sets]
         if fams != ["lagrange"]:
