@@ -261,8 +261,11 @@ MSFV_API int msfv_xk_values(const msfv_plan* plan, const double* sigma, const do
  *   at a time, like the basis it belongs to).
  * msfv_basis_csc_box: S values in the reference CSC pattern, skeleton entries
  *   from the table (bsrc: flat index into bx).
- * Derivatives (gradient, J v, Y_k / X_k) are not built for reduced plans
- * (MSFV_UNSUPPORTED). */
+ * The fused block gradient and the Y_k / X_k operators refuse reduced plans
+ * (MSFV_UNSUPPORTED): the sensitivities through the boundary problems run on
+ * node and edge fields (msfv_prolong, msfv_restrict_op, msfv_fine_apply,
+ * msfv_interior_solve, msfv_edge_grad / msfv_edge_div, msfv_cell_gather read
+ * the bound table), composed by the host (reduced_sens.py). */
 MSFV_API int msfv_plan_set_reduced(msfv_plan* plan, int32_t on);
 MSFV_API int msfv_boundary_reduced(const msfv_plan* plan, const double* w, double* faces, double* bx, int32_t* flags,
                                    void* stream);
