@@ -369,6 +369,55 @@ def solve_flops(nI, p, nrhs):
     return f
 
 
+def reduced_bc_times(args, log):
+    """Extension N4 at the bench config: forward map and the two sensitivity
+    products with BasisSpec(boundary="reduced") (node-field kernel chains +
+    the tensor-level skeleton map), device-timed; the adjoint identity of the
+    two products as a self-check."""
+    import numpy as np
+    import torch
+    import paper_1707_07598_b200 as gp
+    from paper_1707_07598_b200.forward import forward_reduced_dev
+    from paper_1707_07598_b200.models import config_problem
+    try:
+        mesh, part, survey, m = config_problem(args.config, seed=args.seed)
+        builder = gp.BasisBuilder(part, gp.BasisSpec(boundary="reduced"))
+        m_dev = torch.from_numpy(m).cuda()
+        v = torch.from_numpy(np.random.default_rng(args.seed + 3).normal(size=m.size)).cuda()
+
+        def timed(fn, reps=3):
+            fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                out = fn()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            return sorted(ts)[len(ts) // 2], out
+
+        def fwd():
+            op = gp.assemble_operator(mesh, m_dev)
+            return forward_reduced_dev(op, survey, builder.assemble(op))
+
+        t_f, (D, st) = timed(fwd)
+        t_s, J = timed(lambda: gp.sensitivity_adaptive(st, survey))
+        W = torch.randn_like(D)
+        t_r, g = timed(lambda: J.rapply_dev(W))
+        t_a, jv = timed(lambda: J.apply_dev(v))
+        lhs, rhs = float((jv * W).sum()), float(torch.dot(v, g))
+        res = {"forward_ms": round(t_f, 3), "sensitivity_setup_ms": round(t_s, 3), "JTw_ms": round(t_r, 3),
+               "Jv_ms": round(t_a, 3), "adjoint_identity_rel": abs(lhs - rhs) / abs(lhs),
+               "what": "BasisSpec(boundary='reduced') at the bench config: reduced 1D line / 2D face-patch boundary "
+                       "problems, forward map and sensitivities through them (extension N4, no reference)"}
+    except Exception as e:                                   # the headline numbers do not depend on the extension
+        res = {"error": f"{type(e).__name__}: {e}"}
+    log("reduced_bc: " + json.dumps(res))
+    return res
+
+
 def table3_times(log):
     """S_k, Y_k, X_k at the paper's Table-3 geometry (PAPER.md:569-589;
     BASELINE.md section 1): 64x64x32 cells, 16^3 blocks (n_I = 3375, the
@@ -500,6 +549,45 @@ def run_gpu(args, rank, world, log):
     if args.ncu:
         return None
 
+    # end to end through the public API: pinned host m in, D and g out
+    e2e = None
+    if not args.no_e2e:
+        m_pin = torch.from_numpy(m).pin_memory()
+        # measured right after the device-timed steps (before the Gauss-Newton,
+        # fine-mesh and Table-3 legs, whose large allocations leave the caching
+        # allocators in a state the e2e warm-up takes tens of steps to leave);
+        # release the device-resident leg's blocks so the warm-up settles its own
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        for _ in range(max(5, args.warmup)):
+            D, st = problem.simulate(m_pin)
+            phi, resid = gp.misfit_ssd(D, d_obs)
+            problem.jacobian(st).rapply(resid)
+        torch.cuda.synchronize()
+        dist.barrier()
+        # five back-to-back repetitions of the K-step loop, median reported
+        # (the first repetition after the device-resident legs is ~25% slower:
+        # host allocator / page-locked buffer warm-up)
+        reps = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(args.steps):
+                D, st = problem.simulate(m_pin)
+                phi, resid = gp.misfit_ssd(D, d_obs)
+                g_host = problem.jacobian(st).rapply(resid)
+            b.record()
+            torch.cuda.synchronize()
+            reps.append(a.elapsed_time(b) / args.steps)
+        log("e2e repetitions (ms/step): " + ", ".join(f"{x:.3f}" for x in reps))
+        e2e_ms = dist.max_over_ranks(sorted(reps)[2], dev)
+        h2d = m.nbytes + resid.nbytes
+        d2h = D.nbytes + g_host.nbytes
+        e2e = {"value": dist.aggregate_seconds_per_iter(e2e_ms / 1e3, world), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 4),
+               "path": "AdaptiveReducedProblem.simulate -> misfit_ssd -> jacobian(state).rapply (numpy out)"}
+        log(f"e2e step {e2e_ms:.3f} ms")
+
     # config-4 Gauss-Newton iteration (BASELINE configs[3]): one iteration of
     # the device-resident projected Gauss-Newton method (inversion.py:187-263;
     # GNConfig(max_gn=1, max_cg=5), Objective(alpha=1e-3, m_ref=0)): forward,
@@ -552,43 +640,6 @@ def run_gpu(args, rank, world, log):
     step_dev()
     phases = PhaseTimer.stop()
     log("phases (ms): " + json.dumps({k: round(v, 4) for k, v in phases.items()}))
-
-    # end to end through the public API: pinned host m in, D and g out
-    e2e = None
-    if not args.no_e2e:
-        m_pin = torch.from_numpy(m).pin_memory()
-        # the device-resident legs above leave the caching allocator with their
-        # block layout; release it so the e2e leg's warm-up settles its own
-        torch.cuda.synchronize()
-        torch.cuda.empty_cache()
-        for _ in range(max(5, args.warmup)):
-            D, st = problem.simulate(m_pin)
-            phi, resid = gp.misfit_ssd(D, d_obs)
-            problem.jacobian(st).rapply(resid)
-        torch.cuda.synchronize()
-        dist.barrier()
-        # five back-to-back repetitions of the K-step loop, median reported
-        # (the first repetition after the device-resident legs is ~25% slower:
-        # host allocator / page-locked buffer warm-up)
-        reps = []
-        for _ in range(5):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for _ in range(args.steps):
-                D, st = problem.simulate(m_pin)
-                phi, resid = gp.misfit_ssd(D, d_obs)
-                g_host = problem.jacobian(st).rapply(resid)
-            b.record()
-            torch.cuda.synchronize()
-            reps.append(a.elapsed_time(b) / args.steps)
-        log("e2e repetitions (ms/step): " + ", ".join(f"{x:.3f}" for x in reps))
-        e2e_ms = dist.max_over_ranks(sorted(reps)[2], dev)
-        h2d = m.nbytes + resid.nbytes
-        d2h = D.nbytes + g_host.nbytes
-        e2e = {"value": dist.aggregate_seconds_per_iter(e2e_ms / 1e3, world), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 4),
-               "path": "AdaptiveReducedProblem.simulate -> misfit_ssd -> jacobian(state).rapply (numpy out)"}
-        log(f"e2e step {e2e_ms:.3f} ms")
 
     eng = builder.assemble(gp.assemble_operator(mesh, m_dev)).engine
     nI = eng.nI
@@ -734,6 +785,9 @@ def main():
     t3 = None
     if rank == 0 and args.config == 4 and not args.no_table3:
         t3 = table3_times(log)
+    red = None
+    if rank == 0 and args.config == 4 and not args.no_table3:
+        red = reduced_bc_times(args, log)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
@@ -754,6 +808,7 @@ def main():
             "gn_iteration": res["gn"],
             "fine_forward": res.get("fine"),
             "table3": t3,
+            "reduced_bc": red,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
