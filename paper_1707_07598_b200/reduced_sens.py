@@ -108,11 +108,9 @@ class ReducedSensitivity:
         rhs = xdm - self._restrict(gdm + eng.fine_apply(self.w, ydm))
         # boundary term
         dB = self.skel.jvp(self.w, dw)
-        f = eng.zeros(eng.Nn, ns)
-        f.index_add_(0, self.nodes, dB[:, None] * self.T[self.cols])                     # dB T on the skeleton
+        f = self.skel.sum_by_node(dB[:, None] * self.T[self.cols], eng.Nn, eng.k)        # dB T on the skeleton
         delta = f - self._interior(eng.fine_apply(self.w, f))
-        extra = eng.zeros(eng.k, ns)
-        extra.index_add_(0, self.cols, dB[:, None] * self.Rt[self.nodes])                # dB^T (R - A z_R)_B
+        extra = self.skel.sum_by_column(dB[:, None] * self.Rt[self.nodes], eng.k)        # dB^T (R - A z_R)_B
         rhs = rhs + extra - self._restrict(eng.fine_apply(self.w, delta))
         dt = self._solve(rhs)
         field = (ydm + delta).contiguous()
