@@ -67,6 +67,11 @@ struct msfv_points {
 // boundary conditions always take the L2-resident band path (msfv_large.cu),
 // whose kernels read the bound skeleton-value table
 static inline bool use_tc(const Geo& g) { return tc_supported(g) && !g.reduced; }
+// Local factor layout and interior solves: the register-window path whenever
+// the band fits, reduced boundary conditions included (their right-hand sides
+// come from the bound box table, msfv_tc.cu stencil_table; their Galerkin
+// blocks from launch_lg_galerkin).
+static inline bool tc_solver(const Geo& g) { return tc_supported(g); }
 
 static thread_local std::string g_err;
 
@@ -200,9 +205,9 @@ int msfv_plan_info(const msfv_plan* plan, int64_t* info, int32_t n) {
   v[MSFV_INFO_PT] = g.PT;
   v[MSFV_INFO_TB] = g.TB;
   v[MSFV_INFO_PC] = g.pc;
-  const bool tc = use_tc(g);
-  v[MSFV_INFO_FACTOR_DOUBLES] = tc ? (int64_t)tc_factor_doubles(g) : (int64_t)lg_factor_doubles(g);
-  v[MSFV_INFO_SCRATCH_DOUBLES] = tc ? (int64_t)tc_scratch_doubles(g) : 0;
+  const bool tc = use_tc(g), tcs = tc_solver(g);
+  v[MSFV_INFO_FACTOR_DOUBLES] = tcs ? (int64_t)tc_factor_doubles(g) : (int64_t)lg_factor_doubles(g);
+  v[MSFV_INFO_SCRATCH_DOUBLES] = tcs ? (int64_t)tc_scratch_doubles(g) : 0;
   v[MSFV_INFO_TC] = tc ? 1 : 2;
   v[MSFV_INFO_COARSE] = g.coarse_nd;
   v[MSFV_INFO_RED_FACE_DOUBLES] = g.reduced ? (int64_t)red_face_doubles(g) : 0;
@@ -394,11 +399,17 @@ static int basis_build(const msfv_plan* plan, const double* w, double* factor, d
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (use_tc(g)) {
+  if (tc_solver(g)) {
     msfv_plan* pl = const_cast<msfv_plan*>(plan);
     int rc = ensure_skel(pl);
     if (rc) return rc;
-    return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, bwd), "basis_build");
+    if (!g.reduced) return cuda_check(launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, bwd), "basis_build");
+    // reduced boundary conditions: factor + both sweeps on the register-window kernel (right-hand sides
+    // from the bound box table), then the Galerkin blocks from the actual skeleton values
+    if (!g.bx) return fail(MSFV_SHAPE, "reduced plan without a bound boundary table");
+    cudaError_t e = launch_basis_tc(pl->g, w, factor, Sint, Kloc, flags, st, true);
+    if (e == cudaSuccess) e = launch_lg_galerkin(g, w, Sint, Kloc, st);
+    return cuda_check(e, "basis_build");
   }
   return cuda_check(launch_basis_lg(g, w, factor, Sint, Kloc, flags, st), "basis_build");
 }
@@ -504,7 +515,7 @@ int msfv_interior_solve(const msfv_plan* plan, const double* factor, const doubl
   CHECK_PARTITION(plan);
   const Geo& g = plan->g;
   cudaStream_t st = (cudaStream_t)stream;
-  if (use_tc(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
+  if (tc_solver(g)) return cuda_check(launch_block_solve_tc(g, factor, rhs, out, nrhs, st), "interior_solve");
   return cuda_check(launch_block_solve_lg(g, factor, rhs, out, nrhs, st), "interior_solve");
 }
 
@@ -542,7 +553,7 @@ int msfv_points_interior_solve(const msfv_plan* plan, const msfv_points* pts, co
   CHECK_PARTITION(plan);
   if (!pts || nrhs < 0) return fail(MSFV_SHAPE, "bad interior solve arguments");
   const Geo& g = plan->g;
-  if (!use_tc(g))
+  if (!tc_solver(g))
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, pts->d.iblk,
                                             pts->d.nib, 1),
                       "points_interior_solve");
@@ -613,7 +624,7 @@ int msfv_block_solve_compact(const msfv_plan* plan, const double* factor, const 
   // wide solves (apply_Yk: one right-hand side per block cell) take the
   // CTA-per-block kernel that stages each factor tile column once for up to
   // 128 right-hand sides (the register-window kernel re-reads the factor per 16)
-  if (!use_tc(g) || nrhs >= 64)
+  if (!tc_solver(g) || nrhs >= 64)
     return cuda_check(launch_block_solve_lg(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),
                       "block_solve_compact");
   return cuda_check(launch_block_solve_tc(g, factor, rhs_c, out_c, nrhs, (cudaStream_t)stream, nullptr, g.nbl, 1),

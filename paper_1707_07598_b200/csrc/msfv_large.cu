@@ -469,6 +469,15 @@ cudaError_t launch_basis_lg(const Geo& g, const double* w, double* LT, double* S
   return cudaGetLastError();
 }
 
+// Local Galerkin blocks from the edge weights and the basis values (hats or
+// the bound reduced-boundary table on the skeleton), any local solver.
+cudaError_t launch_lg_galerkin(const Geo& g, const double* w, const double* Sint, double* Kloc, cudaStream_t st) {
+  if (g.nbl == 0) return cudaSuccess;
+  k_lg_galerkin<<<g.nbl, LGG_THREADS, 0, st>>>(g, w, Sint, Kloc);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_block_solve_lg(const Geo& g, const double* LT, const double* rhs, double* out, int nrhs,
                                   cudaStream_t st, const int* blist, int nlist, int compact) {
   if (g.nI == 0 || nrhs == 0 || (compact && nlist == 0)) return cudaSuccess;

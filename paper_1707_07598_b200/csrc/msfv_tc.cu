@@ -68,7 +68,7 @@ __device__ __forceinline__ int face_off(const Geo& g, int face) {
 }
 
 __device__ __forceinline__ void stencil_table(const Geo& g, const double* __restrict__ w, int X0, int Y0, int Z0,
-                                              int NR, double* As, double* Fk, double* Sb, int lane) {
+                                              int NR, double* As, double* Fk, double* Sb, int lane, int jb) {
   const double s1 = g.ih1 * g.ih1, s2 = g.ih2 * g.ih2, s3 = g.ih3 * g.ih3;
   for (int i = lane; i < NR; i += 32) {
     double* row = As + i * AROW;
@@ -106,6 +106,21 @@ __device__ __forceinline__ void stencil_table(const Geo& g, const double* __rest
     const double fx0 = x == 1 ? kxm : 0.0, fx1 = x == g.ni1 ? kxp : 0.0;
     const double fy0 = y == 1 ? kym : 0.0, fy1 = y == g.ni2 ? kyp : 0.0;
     const double fz0 = z == 1 ? kzm : 0.0, fz1 = z == g.ni3 ? kzp : 0.0;
+    if (g.bx) {
+      // reduced boundary conditions: the skeleton values of the bound box table
+      // instead of the hats (same sum over the boundary faces)
+      for (int cc = 0; cc < 8; ++cc) {
+        double v = 0.0;
+        if (x == 1) v += fx0 * skel_value(g, jb, cc, 0, y, z);
+        if (x == g.ni1) v += fx1 * skel_value(g, jb, cc, g.b1, y, z);
+        if (y == 1) v += fy0 * skel_value(g, jb, cc, x, 0, z);
+        if (y == g.ni2) v += fy1 * skel_value(g, jb, cc, x, g.b2, z);
+        if (z == 1) v += fz0 * skel_value(g, jb, cc, x, y, 0);
+        if (z == g.ni3) v += fz1 * skel_value(g, jb, cc, x, y, g.b3);
+        Sb[(size_t)cc * g.nI + i] = v;
+      }
+      continue;
+    }
     const double hx0 = hatf1(x, g.ib1), hx1 = hatf1(x - g.b1, g.ib1);
     const double hy0 = hatf1(y, g.ib2), hy1 = hatf1(y - g.b2, g.ib2);
     const double hz0 = hatf1(z, g.ib3), hz1 = hatf1(z - g.b3, g.ib3);
@@ -684,7 +699,7 @@ k_basis_tc(Geo g, const double* __restrict__ w, double* __restrict__ LT, double*
   const int m = lane >> 2, q = lane & 3;
   double* Ds = Dsh[wid];
   double* Is = Ish[wid];
-  stencil_table(g, w, X0, Y0, Z0, NR, As, Fk, Sb, lane);
+  stencil_table(g, w, X0, Y0, Z0, NR, As, Fk, Sb, lane, jb);
   __syncwarp();
   // tile offsets (I - K) that can hold stencil entries: d in {0, 1, ni1, p}
   unsigned omask = 1u;
@@ -1220,7 +1235,10 @@ template <int PT>
 static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, double* Sint,
                                      double* Kloc, int* flags, bool bwd, cudaStream_t st, int jb0, int jb1) {
   cudaError_t e;
-  const bool lines = g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2;   // k_skel_galerkin: blocks one cell thick
+  // reduced boundary conditions (g.bx): the kernel factors, solves and parks its (hat-based) Galerkin block;
+  // the caller recomputes Kloc from the actual skeleton values (launch_lg_galerkin) -- no hat skeleton sums here
+  const bool reduced = g.bx != nullptr;
+  const bool lines = !reduced && g.b1 >= 2 && g.b2 >= 2 && g.b3 >= 2;   // k_skel_galerkin: blocks one cell thick
   const int rec_max = skel_lines_axis(g.b2, g.b3, 1, 1) + skel_lines_axis(g.b1, g.b3, 1, 1) +
                       skel_lines_axis(g.b1, g.b2, 1, 1) + 3;
   const size_t skl_sm = (size_t)SKL_WARPS * rec_max * 16 * sizeof(double);
@@ -1270,7 +1288,7 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
     }
   }
   if constexpr (PT == 7) {
-    const int v = basis_variant(g);
+    const int v = reduced ? (basis_variant(g) ? 1 : 0) : basis_variant(g);   // reduced: right-hand sides from Sint only
     if (v == 1)
       e = launch_basis_tc_k<7, 0xC3u, 0>(g, w, LT, Sint, Kloc, flags, bwd, st, jb0, jb1);
     else if (v == 2)
@@ -1297,6 +1315,8 @@ static cudaError_t launch_basis_tc_t(const Geo& g, const double* w, double* LT, 
   } else if (lines) {
     k_skel_lines<<<(unsigned)((jb1 - jb0 + SKL_WARPS - 1) / SKL_WARPS), SKL_WARPS * 32, skl_sm, st>>>(
         g, w, Kloc, rec_max, jb0, jb1, 0);
+  } else if (reduced) {
+    return cudaSuccess;
   } else
     k_skel_galerkin<<<(unsigned)((jb1 - jb0 + SKEL_WARPS - 1) / SKEL_WARPS), SKEL_WARPS * 32, 0, st>>>(g, w, Kloc,
                                                                                                      jb0, jb1);
