@@ -90,7 +90,7 @@ class ReducedSensitivity:
         xi = (self.gu * eng.edge_grad(z) + self.a * gsy + self.gu * gsy).sum(dim=1)     # forward.py:278-280
         # boundary term: Lam = (R - A z_R)_B y^T + (Rw - A z)_B T^T on the entries of B
         rwt = rw - eng.fine_apply(self.w, z)
-        lam = (self.Rt[self.nodes] * y[self.cols]).sum(dim=1) + (rwt[self.nodes] * self.T[self.cols]).sum(dim=1)
+        lam = self.skel.contract(self.Rt, y) + self.skel.contract(rwt, self.T)
         xi = xi - self.skel.vjp(self.w, lam)
         return eng.cell_gather(self.sigma, xi)
 
@@ -108,9 +108,9 @@ class ReducedSensitivity:
         rhs = xdm - self._restrict(gdm + eng.fine_apply(self.w, ydm))
         # boundary term
         dB = self.skel.jvp(self.w, dw)
-        f = self.skel.sum_by_node(dB[:, None] * self.T[self.cols], eng.Nn, eng.k)        # dB T on the skeleton
+        f = self.skel.spread_nodes(dB, self.T, eng.Nn)                                   # dB T on the skeleton
         delta = f - self._interior(eng.fine_apply(self.w, f))
-        extra = self.skel.sum_by_column(dB[:, None] * self.Rt[self.nodes], eng.k)        # dB^T (R - A z_R)_B
+        extra = self.skel.spread_cols(dB, self.Rt, eng.k)                                # dB^T (R - A z_R)_B
         rhs = rhs + extra - self._restrict(eng.fine_apply(self.w, delta))
         dt = self._solve(rhs)
         field = (ydm + delta).contiguous()

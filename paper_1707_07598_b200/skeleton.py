@@ -262,6 +262,55 @@ class SkeletonMap:
             self._entries = (torch.cat(nodes) if nodes else z, torch.cat(cols) if cols else z)
         return self._entries
 
+    # ------------------------------------------- structured entry contractions
+    # The entries come in groups (a line segment: b-1 nodes x 2 columns; a face
+    # patch: (bu-1)(bv-1) nodes x 4 columns), so products with node fields and
+    # coefficient rows are small batched matrix products instead of per-entry
+    # gathers of ns-wide rows.
+    def _group_tables(self):
+        if getattr(self, "_gt", None) is None:
+            gt = []
+            for L in self.lines:
+                if L["b"] > 1:
+                    gt.append((L["nodes"], L["cols"]))
+            for F in self.faces:
+                if F is not None:
+                    gt.append((F["nodes"], F["cols"]))
+            self._gt = gt
+        return self._gt
+
+    def contract(self, Fn, Fc):
+        """e[g, i, c] = sum_s Fn[nodes[g, i], s] Fc[cols[g, c], s], flat in the order of ``values``."""
+        return torch.cat([torch.bmm(Fn[n], Fc[c].transpose(1, 2)).reshape(-1) for n, c in self._group_tables()])
+
+    def _split(self, v):
+        out, o = [], 0
+        for n, c in self._group_tables():
+            m = n.numel() * c.shape[1]
+            out.append(v[o:o + m].reshape(n.shape[0], n.shape[1], c.shape[1]))
+            o += m
+        return out
+
+    def spread_nodes(self, v, Fc, n_nodes):
+        """f[nodes[g, i], :] = sum_c v[g, i, c] Fc[cols[g, c], :]  (every node belongs to one group)."""
+        f = torch.zeros(n_nodes, Fc.shape[1], dtype=Fc.dtype, device=Fc.device)
+        for (n, c), vg in zip(self._group_tables(), self._split(v)):
+            f[n.reshape(-1)] = torch.bmm(vg, Fc[c]).reshape(-1, Fc.shape[1])
+        return f
+
+    def spread_cols(self, v, Fn, n_cols):
+        """out[col, :] = sum over groups and nodes of v[g, i, c] Fn[nodes[g, i], :] for cols[g, c] == col
+        (fixed-order segment sums over the (group, column) products)."""
+        parts, cols = [], []
+        for (n, c), vg in zip(self._group_tables(), self._split(v)):
+            parts.append(torch.bmm(vg.transpose(1, 2), Fn[n]).reshape(-1, Fn.shape[1]))
+            cols.append(c.reshape(-1))
+        data, cols = torch.cat(parts), torch.cat(cols)
+        if getattr(self, "_cperm", None) is None or self._cperm[0] != n_cols:
+            self._cperm = (n_cols, torch.argsort(cols, stable=True), torch.bincount(cols, minlength=n_cols))
+        _, perm, cnt = self._cperm
+        return torch.segment_reduce(data[perm].contiguous(), "sum", lengths=cnt, axis=0, initial=0.0)
+
     # ------------------------------------------------- fixed-order reductions
     def _groups(self, n_cols):
         """Permutations that sort the entries by coarse column and by node, with
