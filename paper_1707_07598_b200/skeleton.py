@@ -311,32 +311,6 @@ class SkeletonMap:
         _, perm, cnt = self._cperm
         return torch.segment_reduce(data[perm].contiguous(), "sum", lengths=cnt, axis=0, initial=0.0)
 
-    # ------------------------------------------------- fixed-order reductions
-    def _groups(self, n_cols):
-        """Permutations that sort the entries by coarse column and by node, with
-        the group lengths: sums over an entry set run as segment reductions in
-        a fixed order (no floating-point atomics, bitwise-reproducible)."""
-        if getattr(self, "_grp", None) is None or self._grp[0] != n_cols:
-            nodes, cols = self.entries()
-            pc = torch.argsort(cols, stable=True)
-            cc = torch.bincount(cols, minlength=n_cols)
-            pn = torch.argsort(nodes, stable=True)
-            un, cn = torch.unique_consecutive(nodes[pn], return_counts=True)
-            self._grp = (n_cols, pc, cc, pn, un, cn)
-        return self._grp[1:]
-
-    def sum_by_column(self, data, n_cols):
-        """out[c] = sum of data over the entries of coarse column c: (n_cols, m)."""
-        pc, cc, _, _, _ = self._groups(n_cols)
-        return torch.segment_reduce(data[pc].contiguous(), "sum", lengths=cc, axis=0, initial=0.0)
-
-    def sum_by_node(self, data, n_nodes, n_cols):
-        """out[node] = sum of data over the entries of that node: (n_nodes, m)."""
-        _, _, pn, un, cn = self._groups(n_cols)
-        out = torch.zeros(n_nodes, data.shape[1], dtype=data.dtype, device=data.device)
-        out[un] = torch.segment_reduce(data[pn].contiguous(), "sum", lengths=cn, axis=0, initial=0.0)
-        return out
-
     # ------------------------------------------------------------ derivatives
     def vjp(self, w, lam):
         """d<B(w), lam>/dw for entry weights ``lam`` (the gradient path)."""
