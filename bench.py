@@ -783,10 +783,12 @@ def main():
     if res is None:
         return 0
     t3 = None
-    if rank == 0 and args.config == 4 and not args.no_table3:
+    # side legs (Table-3 geometry, reduced boundary conditions): single-GPU runs only, so the ranks of a
+    # scaling run leave the process group together
+    if rank == 0 and world == 1 and args.config == 4 and not args.no_table3:
         t3 = table3_times(log)
     red = None
-    if rank == 0 and args.config == 4 and not args.no_table3:
+    if rank == 0 and world == 1 and args.config == 4 and not args.no_table3:
         red = reduced_bc_times(args, log)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
