@@ -498,8 +498,7 @@ def run_gpu(args, rank, world, log):
         basis = builder.assemble(op)
         D, st = forward_reduced_dev(op, survey, basis, defer_check=True)
         st.deferred = True
-        resid = D - dobs_dev
-        phi = 0.5 * torch.sum(resid * resid)
+        phi, resid = gp.misfit_ssd_dev(D, dobs_dev)
         g = sensitivity_adaptive(st, survey).rapply_dev(resid)
         st.check()
         return phi, g

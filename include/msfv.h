@@ -145,6 +145,10 @@ MSFV_API int msfv_coarse_solve(const msfv_plan* plan, const double* Lk, double* 
  * (P^T S T forward.py:143; P^T (ydm + S dt) forward.py:268) */
 MSFV_API int msfv_survey_receive(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Y,
                         const double* Xfield, int32_t nrhs, double* out, void* stream);
+
+/* misfit_ssd on the device (inversion.py:22-29): resid[i] = D[i] - D_obs[i] (n = receivers x sources
+ * entries) and phi[0] = 0.5 sum resid^2, one launch, fixed summation order. */
+MSFV_API int msfv_misfit(const double* D, const double* D_obs, int64_t n, double* resid, double* phi, void* stream);
 /* out[c][s] = (S^T M Z)[c][s]; Z [ncol][nrhs] or NULL for the identity (S^T Q, forward.py:115). */
 MSFV_API int msfv_survey_restrict(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Z,
                          int32_t nrhs, double* out, void* stream);

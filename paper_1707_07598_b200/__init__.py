@@ -15,7 +15,7 @@ from .basis import (
     coarse_hat_values,
 )
 from .forward import Survey, ReducedState, forward_reduced, AdaptiveSensitivity, sensitivity_adaptive
-from .inversion import misfit_ssd, AdaptiveReducedProblem
+from .inversion import misfit_ssd, misfit_ssd_dev, AdaptiveReducedProblem
 from .models import build_survey
 from .enriched import source_family, skeleton_family, local_pca_family, reference_fields
 from .fine import (

@@ -58,6 +58,7 @@ SIGNATURES = {
     "msfv_coarse_factor": (ctypes.c_int, [_P, _P, _P, _P]),
     "msfv_coarse_solve": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P]),
     "msfv_survey_receive": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _P, _P]),
+    "msfv_misfit": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P, _P]),
     "msfv_survey_restrict": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P]),
     "msfv_survey_scatter": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
     "msfv_prolong": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),

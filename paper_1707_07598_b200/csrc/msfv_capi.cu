@@ -483,6 +483,11 @@ int msfv_survey_receive(const msfv_plan* plan, const msfv_points* pts, const dou
                     "survey_receive");
 }
 
+int msfv_misfit(const double* D, const double* Dobs, int64_t n, double* resid, double* phi, void* stream) {
+  if (n < 0 || !D || !Dobs || !resid || !phi) return fail(MSFV_SHAPE, "bad misfit arguments");
+  return cuda_check(launch_misfit(D, Dobs, (long long)n, resid, phi, (cudaStream_t)stream), "misfit");
+}
+
 int msfv_survey_restrict(const msfv_plan* plan, const msfv_points* pts, const double* Sint, const double* Z,
                          int32_t nrhs, double* out, void* stream) {
   CHECK_PLAN(plan);

@@ -79,6 +79,8 @@ int tc_band(const Geo& g);
 bool tc_supported(const Geo& g);
 size_t tc_factor_doubles(const Geo& g);
 size_t tc_scratch_doubles(const Geo& g);
+cudaError_t launch_misfit(const double* D, const double* Dobs, long long n, double* resid, double* phi,
+                          cudaStream_t st);
 cudaError_t launch_lg_galerkin(const Geo& g, const double* w, const double* Sint, double* Kloc, cudaStream_t st);
 cudaError_t launch_basis_tc(const Geo& g, const double* w, double* LT, double* Sint, double* Kloc,
                             int* flags, cudaStream_t st, bool bwd = true, int jb0 = 0, int jb1 = -1);

@@ -190,4 +190,33 @@ cudaError_t launch_points_scatter_interior(const Geo& g, const PointsDev& P, con
   return cudaGetLastError();
 }
 
+// misfit_ssd on the device (inversion.py:22-29): resid = D - D_obs and phi = 0.5 sum resid^2 in one
+// launch.  One CTA; every thread sums its strided elements in index order, the 512 partial sums are
+// combined by a fixed tree: the value is reproducible bit for bit.
+constexpr int MISFIT_THREADS = 512;
+__global__ void __launch_bounds__(MISFIT_THREADS) k_misfit(const double* __restrict__ D, const double* __restrict__ Dobs,
+                                                           long long n, double* __restrict__ resid,
+                                                           double* __restrict__ phi) {
+  __shared__ double part[MISFIT_THREADS];
+  double a = 0.0;
+  for (long long i = threadIdx.x; i < n; i += MISFIT_THREADS) {
+    const double r = D[i] - Dobs[i];
+    resid[i] = r;
+    a = fma(r, r, a);
+  }
+  part[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = MISFIT_THREADS / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) phi[0] = 0.5 * part[0];
+}
+cudaError_t launch_misfit(const double* D, const double* Dobs, long long n, double* resid, double* phi,
+                          cudaStream_t st) {
+  k_misfit<<<1, MISFIT_THREADS, 0, st>>>(D, Dobs, n, resid, phi);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 }  // namespace msfv

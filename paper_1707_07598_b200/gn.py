@@ -166,8 +166,13 @@ def gauss_newton_dev(problem, m0, d_obs, objective, config=None):
 
     def evaluate(mm):
         D, st = _simulate(problem, mm)
-        resid = D - dobs
-        phi = 0.5 * torch.sum(resid * resid)
+        if D.is_cuda:
+            from .inversion import misfit_ssd_dev
+            phi, resid = misfit_ssd_dev(D, dobs)
+            phi = phi[0]
+        else:
+            resid = D - dobs
+            phi = 0.5 * torch.sum(resid * resid)
         reg, reg_grad = objective.value_grad(mm)
         return st, resid, phi, reg, reg_grad
 

@@ -219,3 +219,18 @@ def test_gauss_newton_decreases_objective(rng):
     tot = trace.totals()
     assert np.all(np.diff(tot) <= 1e-15 * abs(tot[0]))
     assert tot[-1] < tot[0]
+
+
+def test_device_misfit_matches_host(rng):
+    """msfv_misfit (misfit_ssd on the device, inversion.py:22-29): residual bitwise, phi to rounding,
+    reruns bitwise."""
+    import torch
+    D, Dobs = rng.normal(size=(1024, 16)), rng.normal(size=(1024, 16))
+    phi0, r0 = gp.misfit_ssd(D, Dobs)
+    Dd, Do = torch.from_numpy(D).cuda(), torch.from_numpy(Dobs).cuda()
+    phi, r = gp.misfit_ssd_dev(Dd, Do)
+    phi2, _ = gp.misfit_ssd_dev(Dd, Do)
+    assert np.array_equal(r.cpu().numpy(), r0)
+    assert abs(float(phi) - phi0) <= 1e-13 * phi0 and float(phi) == float(phi2)
+    with pytest.raises(ValueError):
+        gp.misfit_ssd_dev(Dd, Do[:, :3])
