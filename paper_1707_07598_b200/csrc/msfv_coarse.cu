@@ -1804,7 +1804,9 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 // U = F_BB - L_BE L_BE^T, which the parent extend-adds.  All fronts of one
 // tree level are factored in one cooperative launch (grid barrier per tile
 // column), the sequential depth is the sum over levels of NE instead of the
-// band's NT (config 4: 23 tile columns instead of 73 + 10).  Solves walk the
+// band's NT (config 4: 26 tile columns instead of 73 + 10).  On levels with
+// more B x B tiles than CTAs the B x B updates are deferred to one K-loop
+// task per tile after the last column (coarse_deferred).  Solves walk the
 // levels up (y_E = L_EE^-1 v_E, v_B -= L_BE y_E) and down
 // (x_E = L_EE^-T (y_E - L_BE^T x_B)); contributions move between fronts by
 // gathers through host-built index maps, so every sum has a fixed order.
@@ -2684,7 +2686,7 @@ __global__ void __launch_bounds__(256) k_mf_bwd_s(MfDev d, int l0, double* __res
 // (k_mf_inv_all below).  With them a front's forward solve is
 // [y_E; c_B] = G v_E + [0; v_B] and its backward solve x_E = G^T [y_E; x_B]:
 // one matrix product per front, so a coarse solve has the depth of the tree
-// (7 levels at config 4) instead of 23 tile steps.
+// (6 levels at config 4) instead of 26 tile steps.
 // one bulk copy global -> shared on an mbarrier (thread 0 issues; all wait)
 __device__ __forceinline__ void mf_tma1(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
   if (threadIdx.x == 0) {
