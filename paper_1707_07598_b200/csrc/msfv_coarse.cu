@@ -1860,6 +1860,8 @@ struct MfPlan {
   int* d_lvloff = nullptr;
   int* d_pre = nullptr;   // per-level prefix sums (solve): rows | forward items | backward items, npre each
   int npre = 0;
+  int4* d_gtab = nullptr;    // gather tables of the one-launch solve: forward rows then backward rows, level order
+  int* d_rowbase = nullptr;  // first table row of every level (nl + 1 entries)
   int4* d_items = nullptr;   // k_mf_inv_all items (front, tile column, slice), longest chain first;
   int nitems[2] = {0, 0};    // group 0: fronts with NE > MF_INV_SMALL, group 1: the rest (own launch, own footprint)
   int inv_nemax[2] = {0, 0};
@@ -2086,6 +2088,40 @@ static cudaError_t mf_upload(const Geo& g) {
     e = cudaMalloc(&P->d_pre, pre.size() * sizeof(int));
     if (e == cudaSuccess) e = cudaMemcpy(P->d_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess) {
+    // Gather tables of the solve's phase (A), one int4 per front row in level order: forward
+    // (V row, X row of an E node or -1, child 0 V row or -1, child 1 V row or -1), backward
+    // (V row, own V row for the E tile rows or -1, X row of a B node or -1, 0): a thread needs one table
+    // load and then its value loads, instead of descriptor, node id, map and child offset loads in turn.
+    const int nl = (int)P->lvl_off.size() - 1;
+    std::vector<int> rowbase(nl + 1, 0);
+    std::vector<int4> tab(2 * P->vrows);
+    int pos = 0;
+    for (int l = 0; l < nl; ++l) {
+      rowbase[l] = pos;
+      for (int i = P->lvl_off[l]; i < P->lvl_off[l + 1]; ++i) {
+        const MfFront& F = P->fr[P->lvl[i]];
+        for (int r = 0; r < F.NT * TB; ++r, ++pos) {
+          const int gidr = P->gid[F.goff + r];
+          int4 f = make_int4((int)F.voff + r, (r < F.nE) ? gidr : -1, -1, -1);
+          for (int c = 0; c < 2; ++c) {
+            if (F.c[c] < 0) continue;
+            const int q = P->maps[F.moff[c] + r];
+            if (q >= 0) (c == 0 ? f.z : f.w) = (int)P->fr[F.c[c]].voff + q;
+          }
+          tab[pos] = f;
+          tab[P->vrows + pos] = make_int4((int)F.voff + r, r < F.NE * TB ? (int)F.voff + r : -1,
+                                          (r >= F.NE * TB && gidr >= 0) ? gidr : -1, 0);
+        }
+      }
+    }
+    rowbase[nl] = pos;
+    e = cudaMalloc(&P->d_gtab, tab.size() * sizeof(int4));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_gtab, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_rowbase, rowbase.size() * sizeof(int));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_rowbase, rowbase.data(), rowbase.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && P->use_g) {
     std::vector<int4> items[2];
     for (int f = 0; f < (int)P->fr.size(); ++f) {
@@ -2118,6 +2154,8 @@ void mf_release(Geo& g) {
   if (P->d_lvloff) cudaFree(P->d_lvloff);
   if (P->d_pre) cudaFree(P->d_pre);
   if (P->d_items) cudaFree(P->d_items);
+  if (P->d_gtab) cudaFree(P->d_gtab);
+  if (P->d_rowbase) cudaFree(P->d_rowbase);
   delete P;
   g.mf = nullptr;
 }
@@ -2924,6 +2962,9 @@ struct MfSolveJob {
   const int* pre;       // MfPlan::d_pre
   int npre;
   int kchunk;           // > 0: pipelined K-chunked products with this many input rows per chunk
+  const int4* gtab;     // MfPlan::d_gtab
+  const int* rowbase;   // MfPlan::d_rowbase
+  int vrows;
 };
 __device__ __forceinline__ void mf_bulk_raw(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -2984,41 +3025,37 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       }
       __syncthreads();
       {
+        // flat index over (front row of the level, right-hand side); four elements' loads in flight per thread
         const long long total = pre[nf];
-        auto front_of = [&](long long gi) {
-          int lo = 0, hi = nf - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pre[mid] <= gi) lo = mid; else hi = mid - 1;
-          }
-          return lo;
-        };
+        const int4* tab = job.gtab + (pass ? job.vrows : 0) + job.rowbase[l];
         for (long long base = gtid; base < total; base += 4 * gstride) {
           double a[4];
           long long dst[4];
+          int4 t4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const long long gi = base + u * gstride;
+            t4[u] = gi < total ? __ldg(tab + gi / nrhs) : make_int4(-1, -1, -1, -1);
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const long long gi = base + u * gstride;
             a[u] = 0.0;
             dst[u] = -1;
             if (gi >= total) continue;
-            const int fi = front_of(gi);
-            const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
-            const int e = (int)(gi - pre[fi]), r = e / nrhs, s2 = e % nrhs;
-            const int g = d.gid[F.goff + r];
+            const int s2 = (int)(gi % nrhs);
+            const int4 t = t4[u];
+            double v = 0.0;
             if (pass == 0) {
-              double v = (r < F.nE) ? __ldcg(job.X + (size_t)g * nrhs + s2) : 0.0;
-              for (int c = 0; c < 2; ++c) {
-                if (F.c[c] < 0) continue;
-                const int q = d.maps[F.moff[c] + r];
-                if (q >= 0) v += __ldcg(job.Vout + ((size_t)d.fr[F.c[c]].voff + q) * nrhs + s2);
-              }
-              a[u] = v;
+              if (t.y >= 0) v = __ldcg(job.X + (size_t)t.y * nrhs + s2);
+              if (t.z >= 0) v += __ldcg(job.Vout + (size_t)t.z * nrhs + s2);
+              if (t.w >= 0) v += __ldcg(job.Vout + (size_t)t.w * nrhs + s2);
             } else {
-              a[u] = r < F.NE * TB ? __ldcg(job.Vout + ((size_t)F.voff + r) * nrhs + s2)
-                                   : (g >= 0 ? __ldcg(job.X + (size_t)g * nrhs + s2) : 0.0);
+              if (t.y >= 0) v = __ldcg(job.Vout + (size_t)t.y * nrhs + s2);
+              else if (t.z >= 0) v = __ldcg(job.X + (size_t)t.z * nrhs + s2);
             }
-            dst[u] = ((long long)F.voff + r) * nrhs + s2;
+            a[u] = v;
+            dst[u] = (long long)t.x * nrhs + s2;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -3640,7 +3677,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         return p;
       }) : nullptr;
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
-                     P->npre, kchunk ? KC : 0};
+                     P->npre, kchunk ? KC : 0, P->d_gtab, P->d_rowbase, (int)P->vrows};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
       count_launches(1);
