@@ -1815,6 +1815,7 @@ cudaError_t launch_coarse_solve(const Geo& g, const double* Ak, double* X, doubl
 constexpr int MF_LEAF = 128;   // leaf boxes of <= 128 coarse nodes (tuned on config 4: 64 -> 128 saves 0.07 ms per step)
 constexpr int MF_MAXF = 1024;   // fronts per level handled by the cooperative kernels
 constexpr int MF_GR = 16;       // rows per item of the G products
+constexpr int MF_FACTOR_FCACHE = 256;  // front descriptors of a level cached by the factor kernel (dynamic shared memory)
 constexpr int MF_KC = 256;      // input rows per chunk of the K-chunked G products (fronts beyond one shared-memory load)
 constexpr int MF_INV_W = 8;     // identity columns per item of k_mf_inv_all
 constexpr int MF_INV_NS = 6;    // its tile ring stages
@@ -1860,6 +1861,7 @@ struct MfPlan {
   int* d_lvloff = nullptr;
   int* d_pre = nullptr;   // per-level prefix sums (solve): rows | forward items | backward items, npre each
   int npre = 0;
+  MfFront* d_frl = nullptr;  // front descriptors in level order (one load instead of d_fr[d_lvl[.]])
   int4* d_gtab = nullptr;    // gather tables of the one-launch solve: forward rows then backward rows, level order
   int* d_rowbase = nullptr;  // first table row of every level (nl + 1 entries)
   int4* d_items = nullptr;   // k_mf_inv_all items (front, tile column, slice), longest chain first;
@@ -2116,7 +2118,11 @@ static cudaError_t mf_upload(const Geo& g) {
       }
     }
     rowbase[nl] = pos;
-    e = cudaMalloc(&P->d_gtab, tab.size() * sizeof(int4));
+    std::vector<MfFront> frl(P->lvl.size());
+    for (size_t i = 0; i < P->lvl.size(); ++i) frl[i] = P->fr[P->lvl[i]];
+    e = cudaMalloc(&P->d_frl, frl.size() * sizeof(MfFront));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_frl, frl.data(), frl.size() * sizeof(MfFront), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_gtab, tab.size() * sizeof(int4));
     if (e == cudaSuccess) e = cudaMemcpy(P->d_gtab, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_rowbase, rowbase.size() * sizeof(int));
     if (e == cudaSuccess)
@@ -2155,6 +2161,7 @@ void mf_release(Geo& g) {
   if (P->d_pre) cudaFree(P->d_pre);
   if (P->d_items) cudaFree(P->d_items);
   if (P->d_gtab) cudaFree(P->d_gtab);
+  if (P->d_frl) cudaFree(P->d_frl);
   if (P->d_rowbase) cudaFree(P->d_rowbase);
   delete P;
   g.mf = nullptr;
@@ -2295,13 +2302,23 @@ __global__ void __launch_bounds__(256, 2) k_mf_factor(MfJob job, int* __restrict
   cg::grid_group grid = cg::this_grid();
   const int nf = job.nf, G = (int)gridDim.x;
   const bool split = nf < G;
-  auto front = [&](int i) { return job.d.fr[job.d.lvl[job.l0 + i]]; };
-  for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, front(i)), 0, flags, sm);
+  // the level's front descriptors are fetched once (dynamic shared memory, the first MF_FACTOR_FCACHE
+  // fronts): d.fr[d.lvl[.]] is two dependent global loads, asked for by every task and every tile column
+  extern __shared__ __align__(16) unsigned char fcache_raw[];
+  MfFront* fcache = reinterpret_cast<MfFront*>(fcache_raw);
+  const int ncache = min(nf, MF_FACTOR_FCACHE);
+  for (int i = threadIdx.x; i < ncache; i += blockDim.x) fcache[i] = job.d.fr[job.d.lvl[job.l0 + i]];
+  __syncthreads();
+  auto front = [&](int i) { return i < ncache ? fcache[i] : job.d.fr[job.d.lvl[job.l0 + i]]; };
+  // a chain CTA with one front keeps its descriptor in registers (critical path of every tile column)
+  MfFront myF{};
+  if (split && (int)blockIdx.x < nf) myF = front(blockIdx.x);
+  for (int i = blockIdx.x; i < nf; i += G) coarse_potrf(mf_band(job.d.base, split ? myF : front(i)), 0, flags, sm);
   grid.sync();
   const int nw = split ? G - nf : G, me = split ? (int)blockIdx.x - nf : (int)blockIdx.x;
   for (int J = 0; J < job.jmax; ++J) {
     for (int i = blockIdx.x; i < nf && (split ? blockIdx.x < nf : true); i += G) {
-      const MfFront F = front(i);
+      const MfFront F = split ? myF : front(i);
       if (J + 1 < F.NE) {
         const Band B = mf_band(job.d.base, F);
         if (!split) {                              // a chain CTA with one front still holds Dinv_J from its POTRF
@@ -2962,6 +2979,7 @@ struct MfSolveJob {
   const int* pre;       // MfPlan::d_pre
   int npre;
   int kchunk;           // > 0: pipelined K-chunked products with this many input rows per chunk
+  const MfFront* frl;   // MfPlan::d_frl
   const int4* gtab;     // MfPlan::d_gtab
   const int* rowbase;   // MfPlan::d_rowbase
   int vrows;
@@ -3018,7 +3036,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       // each); the level's front descriptors are cached in shared memory and
       // each thread keeps four elements' loads in flight
       // (descriptors and both phases' prefix sums in one round of loads)
-      for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc[i] = d.fr[d.lvl[l0 + i]];
+      for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc[i] = job.frl[l0 + i];
       for (int i = threadIdx.x; i <= nf; i += blockDim.x) {
         pre[i] = job.pre[l0 + l + i] * nrhs;
         preB[i] = job.pre[(pass == 0 ? 1 : 2) * job.npre + l0 + l + i];
@@ -3559,7 +3577,10 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, 0);
+    if (cudaFuncSetAttribute(k_mf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(MF_FACTOR_FCACHE * sizeof(MfFront))) != cudaSuccess)
+      return 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_factor, 256, MF_FACTOR_FCACHE * sizeof(MfFront));
     return (coop && per_sm > 0) ? std::max(1, sms - mf_reserved_sms()) * std::min(per_sm, 2) : 0;
   });
   if (coop_grid <= 0) return cudaErrorNotSupported;
@@ -3584,7 +3605,8 @@ cudaError_t launch_mf_factor(const Geo& g, double* Ak, int* flags, cudaStream_t 
     }
     MfJob job{d, l0, nf, jmax, nbb > coop_grid ? 1 : 0, g};
     void* args[] = {(void*)&job, (void*)&flags};
-    e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args, 0, st);
+    e = cudaLaunchCooperativeKernel((void*)k_mf_factor, dim3(coop_grid), dim3(256), args,
+                                    (size_t)std::min(nf, MF_FACTOR_FCACHE) * sizeof(MfFront), st);
     count_launches(1);
     if (e != cudaSuccess) return e;
   }
@@ -3677,7 +3699,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         return p;
       }) : nullptr;
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
-                     P->npre, kchunk ? KC : 0, P->d_gtab, P->d_rowbase, (int)P->vrows};
+                     P->npre, kchunk ? KC : 0, P->d_frl, P->d_gtab, P->d_rowbase, (int)P->vrows};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
       count_launches(1);
