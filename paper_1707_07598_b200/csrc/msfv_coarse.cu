@@ -2980,6 +2980,7 @@ struct MfSolveJob {
   int npre;
   int kchunk;           // > 0: pipelined K-chunked products with this many input rows per chunk
   const MfFront* frl;   // MfPlan::d_frl
+  int lvl_off_total;    // number of fronts
   const int4* gtab;     // MfPlan::d_gtab
   const int* rowbase;   // MfPlan::d_rowbase
   int vrows;
@@ -3009,12 +3010,27 @@ __device__ __forceinline__ void mf_stamp(unsigned long long* ts, int i) {
   }
 }
 constexpr int MF_FCACHE = 128;   // front descriptors cached per level in the coop solve
+constexpr int MF_PRE_CAP = 640;  // prefix entries (fronts + levels) of a tree cached whole by the coop solve
+constexpr int MF_COOP_STATIC = 36864;   // static shared memory of k_mf_solve_coop, rounded up
 __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ __align__(8) unsigned long long bars2[2];   // the two buffers of the pipelined products
-  __shared__ int pre[MF_MAXF + 1], preB[MF_MAXF + 1];
-  __shared__ MfFront fc[MF_FCACHE];
+  __shared__ int pre_s[MF_MAXF + 1], preB_s[MF_MAXF + 1];
+  __shared__ MfFront fc_s[MF_FCACHE];
+  // Small trees (config 4: 63 fronts): the prefix sums of every (pass, level) and all front descriptors
+  // are fetched once at kernel start, so a level phase starts without a global round trip and a barrier.
+  __shared__ int preAll[3 * MF_PRE_CAP];
+  const bool all_cached = job.npre <= MF_PRE_CAP && job.lvl_off_total <= MF_FCACHE;
+  if (all_cached) {
+    for (int i = threadIdx.x; i < 3 * job.npre; i += blockDim.x)
+      preAll[(i / job.npre) * MF_PRE_CAP + i % job.npre] = job.pre[i] * (i < job.npre ? job.nrhs : 1);
+    for (int i = threadIdx.x; i < job.lvl_off_total; i += blockDim.x) fc_s[i] = job.frl[i];
+  }
+  const int* pre = pre_s;
+  const int* preB = preB_s;
+  const MfFront* fc = fc_s;
+  int fcn = 0;                       // descriptors available through fc[]
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) {
     mbar_init(&bar);
@@ -3036,12 +3052,20 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       // each); the level's front descriptors are cached in shared memory and
       // each thread keeps four elements' loads in flight
       // (descriptors and both phases' prefix sums in one round of loads)
-      for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc[i] = job.frl[l0 + i];
-      for (int i = threadIdx.x; i <= nf; i += blockDim.x) {
-        pre[i] = job.pre[l0 + l + i] * nrhs;
-        preB[i] = job.pre[(pass == 0 ? 1 : 2) * job.npre + l0 + l + i];
+      if (all_cached) {
+        pre = preAll + l0 + l;
+        preB = preAll + (pass == 0 ? 1 : 2) * MF_PRE_CAP + l0 + l;
+        fc = fc_s + l0;
+        fcn = nf;
+      } else {
+        for (int i = threadIdx.x; i < nf && i < MF_FCACHE; i += blockDim.x) fc_s[i] = job.frl[l0 + i];
+        for (int i = threadIdx.x; i <= nf; i += blockDim.x) {
+          pre_s[i] = job.pre[l0 + l + i] * nrhs;
+          preB_s[i] = job.pre[(pass == 0 ? 1 : 2) * job.npre + l0 + l + i];
+        }
+        fcn = min(nf, MF_FCACHE);
+        __syncthreads();
       }
-      __syncthreads();
       {
         // flat index over (front row of the level, right-hand side); four elements' loads in flight per thread
         const long long total = pre[nf];
@@ -3098,7 +3122,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
         const bool wact = wv < ntj * nparts;
         const int tj = wv % ntj, part = wv / ntj;
         const int total = preB[nf];
-        auto front = [&](int fi2) { return fi2 < MF_FCACHE ? fc[fi2] : d.fr[d.lvl[l0 + fi2]]; };
+        auto front = [&](int fi2) { return fi2 < fcn ? fc[fi2] : d.fr[d.lvl[l0 + fi2]]; };
         auto item_of = [&](int gi, int& fi2) {
           while (preB[fi2 + 1] <= gi) ++fi2;
           const MfFront F = front(fi2);
@@ -3234,7 +3258,7 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
       int fi = 0;
       for (int gi = blockIdx.x; gi < preB[nf] && !job.kchunk; gi += gridDim.x) {
         while (preB[fi + 1] <= gi) ++fi;
-        const MfFront F = fi < MF_FCACHE ? fc[fi] : d.fr[d.lvl[l0 + fi]];
+        const MfFront F = fi < fcn ? fc[fi] : d.fr[d.lvl[l0 + fi]];
         const int rows = F.NT * TB, ncol = F.NE * TB;
         const double* vin = job.Vin + (size_t)F.voff * nrhs;
         if (pass == 0) {
@@ -3678,19 +3702,19 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-      if (cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - 24576) !=
+      if (cudaFuncSetAttribute(k_mf_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MF_SMEM_MAX - MF_COOP_STATIC) !=
           cudaSuccess)
         return 0;
       return coop ? std::max(1, sms - mf_reserved_sms()) : 0;
     });
     // fronts whose G chunk + input vector exceed one shared-memory load: K-chunked products
     // (MSFV_MF_FORCE_KCHUNK: test hook, the chunked products at any size)
-    const bool kchunk = smc > (size_t)MF_SMEM_MAX - 24576 || getenv("MSFV_MF_FORCE_KCHUNK") != nullptr;
+    const bool kchunk = smc > (size_t)MF_SMEM_MAX - MF_COOP_STATIC || getenv("MSFV_MF_FORCE_KCHUNK") != nullptr;
     int KC = MF_KC;                                   // largest chunk whose two buffers fit
     auto smem_k = [&](int kc) { return (2 * ((size_t)MF_GR * (kc + 4) + (size_t)kc * nrhs + 8) + 1280) * sizeof(double); };
-    while (KC > 32 && smem_k(KC) > (size_t)MF_SMEM_MAX - 24576) KC /= 2;
+    while (KC > 32 && smem_k(KC) > (size_t)MF_SMEM_MAX - MF_COOP_STATIC) KC /= 2;
     if (kchunk) smc = smem_k(KC);
-    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - 24576 && !getenv("MSFV_MF_NOCOOP")) {
+    if (coop_grid > 0 && smc <= (size_t)MF_SMEM_MAX - MF_COOP_STATIC && !getenv("MSFV_MF_NOCOOP")) {
       const bool timing = getenv("MSFV_MF_TIMING") != nullptr;
       static PerDevice<unsigned long long*> tst_cache;
       unsigned long long* tst = timing ? tst_cache.get([] {
@@ -3699,7 +3723,7 @@ cudaError_t launch_mf_solve(const Geo& g, const double* Ak, double* X, double* s
         return p;
       }) : nullptr;
       MfSolveJob job{d, P->d_lvloff, nl, X, scratch, scratch + P->vrows * nrhs, nrhs, timing ? tst : nullptr, P->d_pre,
-                     P->npre, kchunk ? KC : 0, P->d_frl, P->d_gtab, P->d_rowbase, (int)P->vrows};
+                     P->npre, kchunk ? KC : 0, P->d_frl, (int)P->lvl.size(), P->d_gtab, P->d_rowbase, (int)P->vrows};
       void* args[] = {(void*)&job};
       e = cudaLaunchCooperativeKernel((void*)k_mf_solve_coop, dim3(coop_grid), dim3(256), args, smc, st);
       count_launches(1);
