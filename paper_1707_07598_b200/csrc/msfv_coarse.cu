@@ -3031,6 +3031,8 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
   const int* preB = preB_s;
   const MfFront* fc = fc_s;
   int fcn = 0;                       // descriptors available through fc[]
+  int4 t4n[4];                       // prefetched gather-table entries of the next level phase
+  bool have_next = false;
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) {
     mbar_init(&bar);
@@ -3077,7 +3079,8 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const long long gi = base + u * gstride;
-            t4[u] = gi < total ? __ldg(tab + gi / nrhs) : make_int4(-1, -1, -1, -1);
+            if (have_next && base == gtid) t4[u] = t4n[u];     // fetched during the previous level's products
+            else t4[u] = gi < total ? __ldg(tab + gi / nrhs) : make_int4(-1, -1, -1, -1);
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -3102,6 +3105,23 @@ __global__ void __launch_bounds__(256, 1) k_mf_solve_coop(MfSolveJob job) {
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (dst[u] >= 0) job.Vin[dst[u]] = a[u];
+        }
+      }
+      // the next level phase's table entries (static data) travel while this level's products run
+      have_next = false;
+      if (all_cached) {
+        const int li2 = li + 1 < job.nl ? li + 1 : 0, pass2 = li + 1 < job.nl ? pass : pass + 1;
+        if (pass2 < 2) {
+          const int l2 = pass2 == 0 ? li2 : job.nl - 1 - li2;
+          const int l02 = job.lvl_off[l2], nf2 = job.lvl_off[l2 + 1] - l02;
+          const long long total2 = preAll[l02 + l2 + nf2];
+          const int4* tab2 = job.gtab + (pass2 ? job.vrows : 0) + job.rowbase[l2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const long long gi = gtid + u * gstride;
+            t4n[u] = gi < total2 ? __ldg(tab2 + gi / nrhs) : make_int4(-1, -1, -1, -1);
+          }
+          have_next = true;
         }
       }
       grid.sync();
