@@ -333,7 +333,10 @@ _TEMPLATES = {}
 
 
 def _template(partition, engine):
-    key = id(engine)
+    # keyed by what the template depends on (geometry, boundary kind, device), not by id(engine):
+    # ids are reused after garbage collection
+    m = partition.mesh
+    key = (m.n1, m.n2, m.n3, partition.b1, partition.b2, partition.b3, bool(engine.reduced), str(engine.device))
     t = _TEMPLATES.get(key)
     if t is None:
         t = _CscTemplate(partition, engine)

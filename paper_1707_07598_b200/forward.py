@@ -69,9 +69,10 @@ class Survey:
             Pp = Points(engine, self.P)
             Qp = Points(engine, self.Q)
             Qf = engine.scatter_points(Qp, None, self.n_sources)
-            d = (Pp, Qp, Qf)
+            # the entry keeps the engine alive: id(engine) cannot be reused by another engine while it is cached
+            d = (Pp, Qp, Qf, engine)
             self._pts[key] = d
-        return d
+        return d[:3]
 
 
 def _host(t):

@@ -48,7 +48,10 @@ class SkeletonMap:
 
     @classmethod
     def get(cls, partition, device):
-        key = (id(partition), str(device))
+        mesh = partition.mesh
+        # keyed by the geometry, not by id(partition): ids are reused after garbage collection
+        key = (mesh.n1, mesh.n2, mesh.n3, float(mesh.h1), float(mesh.h2), float(mesh.h3), partition.b1, partition.b2,
+               partition.b3, str(device))
         m = cls._cache.get(key)
         if m is None:
             m = cls._cache[key] = SkeletonMap(partition, device)
